@@ -1,0 +1,169 @@
+"""Layer math of the paper's workloads in fp64, NCHW layout (oracle, C1).
+
+The paper trains CNNs made of "convolutional layer, pooling layer,
+Batch-Normalization (BN) layer, fully-connected layer" (Sec. 2.1) with
+back-propagation: forward, backward, update. Each function below is
+the textbook definition of one of those layers; backward functions are the
+adjoints, written out directly (no autograd). Pinned by finite differences and
+closed forms in tests/test_oracle_layers.py.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+BN_EPS = 1e-5          # Reading 23 (paper silent)
+SGD_MOMENTUM = 0.9     # Reading 23
+
+
+# --------------------------------------------------------------------------- conv
+def conv_out_hw(h: int, w: int, r: int, s: int, stride: int, pad: int):
+    return (h + 2 * pad - r) // stride + 1, (w + 2 * pad - s) // stride + 1
+
+
+def conv2d_fwd(x, w, stride=1, pad=0):
+    """y[n,o,i,j] = sum_{c,u,v} x[n,c,s*i+u-p, s*j+v-p] * w[o,c,u,v] (zero padded)."""
+    n, c, h, wd = x.shape
+    o, c2, r, s = w.shape
+    assert c == c2
+    ho, wo = conv_out_hw(h, wd, r, s, stride, pad)
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    y = np.zeros((n, ho, wo, o), dtype=np.float64)
+    for u in range(r):
+        for v in range(s):
+            patch = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
+            y += np.tensordot(patch, w[:, :, u, v], axes=([1], [1]))  # [n,ho,wo,o]
+    return y.transpose(0, 3, 1, 2).copy()
+
+
+def conv2d_dgrad(dy, w, x_shape, stride=1, pad=0):
+    """dx = adjoint of conv2d_fwd w.r.t. x."""
+    n, c, h, wd = x_shape
+    o, _, r, s = w.shape
+    _, _, ho, wo = dy.shape
+    dxp = np.zeros((n, c, h + 2 * pad, wd + 2 * pad), dtype=np.float64)
+    for u in range(r):
+        for v in range(s):
+            contrib = np.tensordot(dy, w[:, :, u, v], axes=([1], [0]))  # [n,ho,wo,c]
+            dxp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride] += \
+                contrib.transpose(0, 3, 1, 2)
+    return dxp[:, :, pad:pad + h, pad:pad + wd].copy()
+
+
+def conv2d_wgrad(x, dy, w_shape, stride=1, pad=0):
+    """dw = adjoint of conv2d_fwd w.r.t. w."""
+    o, c, r, s = w_shape
+    _, _, ho, wo = dy.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    dw = np.zeros(w_shape, dtype=np.float64)
+    for u in range(r):
+        for v in range(s):
+            patch = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
+            dw[:, :, u, v] = np.tensordot(dy, patch, axes=([0, 2, 3], [0, 2, 3]))  # [o,c]
+    return dw
+
+
+# ----------------------------------------------------------------------------- BN
+def bn_fwd(x, gamma, beta, eps=BN_EPS):
+    """Training-mode BN over (n,h,w) per channel; biased variance."""
+    mu = x.mean(axis=(0, 2, 3))
+    var = ((x - mu[None, :, None, None]) ** 2).mean(axis=(0, 2, 3))
+    invstd = 1.0 / np.sqrt(var + eps)
+    xhat = (x - mu[None, :, None, None]) * invstd[None, :, None, None]
+    y = gamma[None, :, None, None] * xhat + beta[None, :, None, None]
+    return y, (xhat, invstd)
+
+
+def bn_bwd(dy, cache, gamma):
+    """Closed form: dbeta = sum dy; dgamma = sum dy*xhat;
+    dx = gamma*invstd*(dy - dbeta/N - xhat*dgamma/N)."""
+    xhat, invstd = cache
+    m = dy.shape[0] * dy.shape[2] * dy.shape[3]
+    dbeta = dy.sum(axis=(0, 2, 3))
+    dgamma = (dy * xhat).sum(axis=(0, 2, 3))
+    dx = (gamma * invstd)[None, :, None, None] * (
+        dy - dbeta[None, :, None, None] / m - xhat * dgamma[None, :, None, None] / m)
+    return dx, dgamma, dbeta
+
+
+# --------------------------------------------------------------------------- ReLU
+def relu_fwd(x):
+    return np.maximum(x, 0.0)
+
+
+def relu_bwd(dy, y):
+    """dx = dy * [y > 0]  (ReLU'(0) = 0, Reading 26)."""
+    return dy * (y > 0)
+
+
+# ------------------------------------------------------------------------ pooling
+def maxpool_fwd(x, k, stride, pad):
+    """Max over k x k windows, -inf padding."""
+    n, c, h, w = x.shape
+    ho, wo = conv_out_hw(h, w, k, k, stride, pad)
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)), constant_values=-np.inf)
+    y = np.full((n, c, ho, wo), -np.inf)
+    for u in range(k):
+        for v in range(k):
+            y = np.maximum(y, xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride])
+    return y
+
+
+def maxpool_bwd(dy, x, k, stride, pad):
+    """Gradient to the FIRST maximum in row-major window order (Reading 25)."""
+    n, c, h, w = x.shape
+    _, _, ho, wo = dy.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)), constant_values=-np.inf)
+    dxp = np.zeros_like(xp)
+    best = np.full((n, c, ho, wo), -np.inf)
+    arg = np.full((n, c, ho, wo), -1, dtype=np.int64)
+    for u in range(k):
+        for v in range(k):
+            win = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
+            better = win > best          # strict: first maximum wins
+            best = np.where(better, win, best)
+            arg = np.where(better, u * k + v, arg)
+    for u in range(k):
+        for v in range(k):
+            sel = (arg == u * k + v)
+            dxp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride] += dy * sel
+    return dxp[:, :, pad:pad + h, pad:pad + w].copy()
+
+
+def avgpool_fwd(x):
+    """Global average pool: [n,c,h,w] -> [n,c]."""
+    return x.mean(axis=(2, 3))
+
+
+def avgpool_bwd(dy, x_shape):
+    n, c, h, w = x_shape
+    return np.broadcast_to(dy[:, :, None, None] / (h * w), x_shape).copy()
+
+
+# ----------------------------------------------------------------------------- FC
+def fc_fwd(x, w, b):
+    """y = x W^T + b."""
+    return x @ w.T + b[None, :]
+
+
+def fc_bwd(dy, x, w):
+    return dy @ w, dy.T @ x, dy.sum(axis=0)
+
+
+# --------------------------------------------------------------------- softmax-CE
+def softmax_ce(z, t):
+    """loss = -mean_n log softmax(z_n)[t_n];  dz = (softmax(z) - onehot(t)) / B."""
+    zmax = z.max(axis=1, keepdims=True)
+    e = np.exp(z - zmax)
+    p = e / e.sum(axis=1, keepdims=True)
+    b = z.shape[0]
+    loss = -np.mean(np.log(p[np.arange(b), t]))
+    dz = p.copy()
+    dz[np.arange(b), t] -= 1.0
+    return loss, dz / b
+
+
+# ---------------------------------------------------------------------------- SGD
+def sgd_momentum(w, v, g, lr, mu=SGD_MOMENTUM, grad_scale=1.0):
+    """v <- mu v + s g ; w <- w - lr v  (update step; s = 1/W under DP)."""
+    v_new = mu * v + grad_scale * g
+    return w - lr * v_new, v_new

@@ -1,0 +1,292 @@
+"""The two CNN workloads as fused task lists, their fp64 training step, and the
+saved-feature-map census (oracle, C1 + C2).
+
+A *task* is one executor kernel group; a *feature map* is a task's output that
+backward needs (Sec. 2.1: "Computation of backward-propagation of layer
+i requires the feature maps, which has been computed in forward propagation of
+layer i"). PoocH classifies feature maps only (Sec. 4.1.1). Reading 1:
+maps = conv outputs, BN(+add)+ReLU outputs, pool outputs and the FC output;
+for ResNet-50 this census gives 105, the row total of every Table 3 line
+(P:L443-446).
+
+Task kinds (inputs are map ids, -1 = the network input, which is not a map
+and is always resident, Reading 2):
+
+* ``conv``      y = conv(x, W)                 bwd needs {x}
+* ``bnrelu``    y = relu(bn(c))                bwd needs {c} (mask from bn(c))
+* ``tail_proj`` y = relu(bn3(c3) + bnp(p))     bwd needs {c3, p}
+* ``tail_id``   y = relu(bn3(c3) + x)          bwd needs {c3, x}
+* ``maxpool``   y = maxpool(x)                 bwd needs {x} (argmax from x)
+* ``avgpool``   y = mean_hw(x)                 bwd needs {}
+* ``fc_ce``     z = flat(x) W^T + b; CE loss   bwd needs {x, z} (sink task)
+
+Flatten order before the FC is (h, w, c) (the GPU's NHWC order); both sides
+use it, so FC weights are shared verbatim.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import layers as L
+
+import synthdata
+
+
+@dataclass
+class Task:
+    name: str
+    kind: str
+    inputs: list            # map ids (task ids), -1 = network input
+    out_chw: tuple          # per-image output shape (C, H, W); FC/avgpool: (C, 1, 1)
+    stride: int = 1
+    pad: int = 0
+    k: int = 0              # conv/pool kernel size
+    cin: int = 0            # conv input channels (true, unpadded)
+
+    @property
+    def needs(self):
+        """Maps bwd(task) reads (see module docstring)."""
+        if self.kind in ("conv", "maxpool"):
+            return [i for i in self.inputs if i >= 0]
+        if self.kind in ("bnrelu", "tail_proj", "tail_id"):
+            return [i for i in self.inputs if i >= 0]
+        if self.kind == "avgpool":
+            return []
+        if self.kind == "fc_ce":
+            return None     # filled by Net (self id needed)
+        raise ValueError(self.kind)
+
+
+@dataclass
+class Net:
+    name: str
+    in_chw: tuple           # (C, H, W) of the network input, unpadded
+    classes: int
+    tasks: list = field(default_factory=list)
+
+    def add(self, t: Task) -> int:
+        self.tasks.append(t)
+        return len(self.tasks) - 1
+
+    def needs(self, i):
+        t = self.tasks[i]
+        if t.kind == "fc_ce":
+            return sorted([j for j in t.inputs if j >= 0] + [i])
+        return sorted(t.needs)
+
+    def map_bytes_per_image(self, i):
+        c, h, w = self.tasks[i].out_chw
+        return 4 * c * h * w
+
+
+# ------------------------------------------------------------------ builders
+def tiny_cnn(width: int = 32, in_hw: int = 32, classes: int = 10) -> Net:
+    """BASELINE.json config 1: 4 x [conv3x3-BN-ReLU] (uniform width 32, SURVEY
+    8(d)), maxpool 2x2, FC-10."""
+    net = Net("tiny", (3, in_hw, in_hw), classes)
+    src, cin, hw = -1, 3, in_hw
+    for l in range(4):
+        c = net.add(Task(f"conv{l}", "conv", [src], (width, hw, hw), 1, 1, 3, cin))
+        src = net.add(Task(f"bn{l}", "bnrelu", [c], (width, hw, hw)))
+        cin = width
+    hw2 = hw // 2
+    p = net.add(Task("maxpool", "maxpool", [src], (width, hw2, hw2), 2, 0, 2))
+    net.add(Task("fc", "fc_ce", [p], (classes, 1, 1), cin=width * hw2 * hw2))
+    return net
+
+
+def resnet50(in_hw: int = 224, classes: int = 1000, v15: bool = True) -> Net:
+    """ResNet-50 [resnet]; v1.5 (stride on the 3x3) by default
+    (Reading 24)."""
+    net = Net("resnet50" if v15 else "resnet50v1", (3, in_hw, in_hw), classes)
+    hw = L.conv_out_hw(in_hw, in_hw, 7, 7, 2, 3)[0]
+    c = net.add(Task("conv1", "conv", [-1], (64, hw, hw), 2, 3, 7, 3))
+    x = net.add(Task("bn1", "bnrelu", [c], (64, hw, hw)))
+    hw = L.conv_out_hw(hw, hw, 3, 3, 2, 1)[0]
+    x = net.add(Task("maxpool", "maxpool", [x], (64, hw, hw), 2, 1, 3))
+    cin = 64
+    for si, (nblocks, mid) in enumerate(zip([3, 4, 6, 3], [64, 128, 256, 512])):
+        out = 4 * mid
+        for b in range(nblocks):
+            s = 2 if (b == 0 and si > 0) else 1
+            pre = f"layer{si + 1}.{b}"
+            s1, s2 = (1, s) if v15 else (s, 1)
+            hw1 = L.conv_out_hw(hw, hw, 1, 1, s1, 0)[0]
+            c1 = net.add(Task(pre + ".conv1", "conv", [x], (mid, hw1, hw1), s1, 0, 1, cin))
+            y1 = net.add(Task(pre + ".bn1", "bnrelu", [c1], (mid, hw1, hw1)))
+            hw2 = L.conv_out_hw(hw1, hw1, 3, 3, s2, 1)[0]
+            c2 = net.add(Task(pre + ".conv2", "conv", [y1], (mid, hw2, hw2), s2, 1, 3, mid))
+            y2 = net.add(Task(pre + ".bn2", "bnrelu", [c2], (mid, hw2, hw2)))
+            c3 = net.add(Task(pre + ".conv3", "conv", [y2], (out, hw2, hw2), 1, 0, 1, mid))
+            if b == 0:
+                p = net.add(Task(pre + ".downsample", "conv", [x], (out, hw2, hw2), s, 0, 1, cin))
+                x = net.add(Task(pre + ".tail", "tail_proj", [c3, p], (out, hw2, hw2)))
+            else:
+                x = net.add(Task(pre + ".tail", "tail_id", [c3, x], (out, hw2, hw2)))
+            hw, cin = hw2, out
+    a = net.add(Task("avgpool", "avgpool", [x], (cin, 1, 1)))
+    net.add(Task("fc", "fc_ce", [a], (classes, 1, 1), cin=cin))
+    return net
+
+
+# -------------------------------------------------------------------- census
+def census(net: Net, batch: int):
+    """[(name, bytes)] of every saved feature map (C2)."""
+    return [(t.name, batch * net.map_bytes_per_image(i)) for i, t in enumerate(net.tasks)]
+
+
+def param_shapes(net: Net):
+    """Ordered {param name: shape}; conv weights OIHW, FC [O, I]."""
+    shapes = {}
+    for t in net.tasks:
+        if t.kind == "conv":
+            shapes[t.name + ".w"] = (t.out_chw[0], t.cin, t.k, t.k)
+        elif t.kind == "bnrelu":
+            shapes[t.name + ".gamma"] = (t.out_chw[0],)
+            shapes[t.name + ".beta"] = (t.out_chw[0],)
+        elif t.kind in ("tail_proj", "tail_id"):
+            shapes[t.name + ".gamma3"] = (t.out_chw[0],)
+            shapes[t.name + ".beta3"] = (t.out_chw[0],)
+            if t.kind == "tail_proj":
+                shapes[t.name + ".gammap"] = (t.out_chw[0],)
+                shapes[t.name + ".betap"] = (t.out_chw[0],)
+        elif t.kind == "fc_ce":
+            shapes[t.name + ".w"] = (t.out_chw[0], t.cin)
+            shapes[t.name + ".b"] = (t.out_chw[0],)
+    return shapes
+
+
+# ------------------------------------------------------------ training step
+def _flat_hwc(x):
+    return x.transpose(0, 2, 3, 1).reshape(x.shape[0], -1)
+
+
+def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndarray):
+    """One fp64 fwd + bwd of ``net``. ``x_nhwc`` is the (unpadded)
+    input batch in NHWC; params are promoted to fp64. Returns (loss, grads,
+    outputs) with grads keyed like ``params`` and outputs the fp64 task
+    outputs (NCHW) for map-level checks."""
+    P = {k: np.asarray(v, dtype=np.float64) for k, v in params.items()}
+    x_in = np.asarray(x_nhwc, dtype=np.float64).transpose(0, 3, 1, 2)
+    outs, caches = [], []
+
+    def get(i):
+        return x_in if i < 0 else outs[i]
+
+    loss = None
+    for t in net.tasks:
+        if t.kind == "conv":
+            y = L.conv2d_fwd(get(t.inputs[0]), P[t.name + ".w"], t.stride, t.pad)
+            cache = None
+        elif t.kind == "bnrelu":
+            z, bc = L.bn_fwd(get(t.inputs[0]), P[t.name + ".gamma"], P[t.name + ".beta"])
+            y = L.relu_fwd(z)
+            cache = (bc,)
+        elif t.kind in ("tail_proj", "tail_id"):
+            z3, bc3 = L.bn_fwd(get(t.inputs[0]), P[t.name + ".gamma3"], P[t.name + ".beta3"])
+            if t.kind == "tail_proj":
+                zp, bcp = L.bn_fwd(get(t.inputs[1]), P[t.name + ".gammap"], P[t.name + ".betap"])
+            else:
+                zp, bcp = get(t.inputs[1]), None
+            y = L.relu_fwd(z3 + zp)
+            cache = (bc3, bcp)
+        elif t.kind == "maxpool":
+            y = L.maxpool_fwd(get(t.inputs[0]), t.k, t.stride, t.pad)
+            cache = None
+        elif t.kind == "avgpool":
+            y = L.avgpool_fwd(get(t.inputs[0]))[:, :, None, None]
+            cache = None
+        elif t.kind == "fc_ce":
+            xf = _flat_hwc(get(t.inputs[0]))
+            z = L.fc_fwd(xf, P[t.name + ".w"], P[t.name + ".b"])
+            loss, dz = L.softmax_ce(z, np.asarray(labels))
+            y = z[:, :, None, None]
+            cache = (xf, dz)
+        else:
+            raise ValueError(t.kind)
+        outs.append(y)
+        caches.append(cache)
+
+    grads = {k: np.zeros_like(v) for k, v in P.items()}
+    gmap = [None] * len(net.tasks)
+
+    def acc(i, g):
+        if i < 0:
+            return
+        gmap[i] = g if gmap[i] is None else gmap[i] + g
+
+    for i in reversed(range(len(net.tasks))):
+        t = net.tasks[i]
+        cache = caches[i]
+        if t.kind == "fc_ce":
+            xf, dz = cache
+            dxf, dw, db = L.fc_bwd(dz, xf, P[t.name + ".w"])
+            grads[t.name + ".w"] += dw
+            grads[t.name + ".b"] += db
+            src = get(t.inputs[0])
+            n, c, h, w = src.shape
+            acc(t.inputs[0], dxf.reshape(n, h, w, c).transpose(0, 3, 1, 2))
+            continue
+        dy = gmap[i]
+        if t.kind == "conv":
+            xin = get(t.inputs[0])
+            w = P[t.name + ".w"]
+            grads[t.name + ".w"] += L.conv2d_wgrad(xin, dy, w.shape, t.stride, t.pad)
+            if t.inputs[0] >= 0:
+                acc(t.inputs[0], L.conv2d_dgrad(dy, w, xin.shape, t.stride, t.pad))
+        elif t.kind == "bnrelu":
+            dz = L.relu_bwd(dy, outs[i])
+            dx, dg, db = L.bn_bwd(dz, cache[0], P[t.name + ".gamma"])
+            grads[t.name + ".gamma"] += dg
+            grads[t.name + ".beta"] += db
+            acc(t.inputs[0], dx)
+        elif t.kind in ("tail_proj", "tail_id"):
+            dz = L.relu_bwd(dy, outs[i])
+            dx3, dg3, db3 = L.bn_bwd(dz, cache[0], P[t.name + ".gamma3"])
+            grads[t.name + ".gamma3"] += dg3
+            grads[t.name + ".beta3"] += db3
+            acc(t.inputs[0], dx3)
+            if t.kind == "tail_proj":
+                dxp, dgp, dbp = L.bn_bwd(dz, cache[1], P[t.name + ".gammap"])
+                grads[t.name + ".gammap"] += dgp
+                grads[t.name + ".betap"] += dbp
+                acc(t.inputs[1], dxp)
+            else:
+                acc(t.inputs[1], dz)
+        elif t.kind == "maxpool":
+            acc(t.inputs[0], L.maxpool_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad))
+        elif t.kind == "avgpool":
+            acc(t.inputs[0], L.avgpool_bwd(dy[:, :, 0, 0], get(t.inputs[0]).shape))
+    return loss, grads, outs
+
+
+def init_params(net: Net, seed: int = 2, bn_random: bool = False) -> dict:
+    """Seeded fp32 parameters (synthdata recipe). With ``bn_random`` gamma ~
+    U(0.5,1.5), beta ~ U(-0.2,0.2) (parity tests, so gamma/beta mix-ups show)."""
+    g = synthdata.rng(seed)
+    params = {}
+    for name, shape in param_shapes(net).items():
+        if name.endswith(".w"):
+            fan_in = int(np.prod(shape[1:]))
+            params[name] = synthdata.he_normal(shape, fan_in, g)
+        elif name.endswith(".b"):
+            params[name] = np.zeros(shape, np.float32)
+        elif ".gamma" in name:
+            params[name] = (g.uniform(0.5, 1.5, shape).astype(np.float32) if bn_random
+                            else np.ones(shape, np.float32))
+        else:
+            params[name] = (g.uniform(-0.2, 0.2, shape).astype(np.float32) if bn_random
+                            else np.zeros(shape, np.float32))
+    return params
+
+
+def sgd_step(params, moms, grads, lr, grad_scale=1.0):
+    """Momentum SGD over every parameter."""
+    newp, newm = {}, {}
+    for k in params:
+        newp[k], newm[k] = L.sgd_momentum(np.asarray(params[k], np.float64),
+                                          np.asarray(moms[k], np.float64),
+                                          grads[k], lr, grad_scale=grad_scale)
+    return newp, newm
