@@ -1,0 +1,292 @@
+/* pooch.h -- C ABI of the B200-native PoocH out-of-core training-step executor.
+ *
+ * PoocH (arXiv 1907.05013, "Profiling-based out-of-core Hybrid method") trains a CNN whose
+ * feature maps exceed device memory by classifying every feature map as keep / swap /
+ * recompute (Sec. 4.1.1) from a plan built by simulating a profiled iteration
+ * (Sec. 4.1.2). The flow is "1. Profiling  2. Classification  3. Execution"
+ * (P:L169-173); the calls below follow it:
+ *
+ *   pooch_create -> pooch_set_budget -> pooch_set_streams -> [pooch_set_comm]
+ *     -> pooch_profile (Sec. 4.2) -> pooch_plan (Sec. 4.4) -> pooch_train_step* (execution)
+ *
+ * Citations: P:Lnnn = PAPER.md line (section / equation named alongside).
+ *
+ * Conventions for every function:
+ *  - Returns pooch_status; nothing throws or aborts across the ABI. On failure the
+ *    per-context message is available from pooch_last_error (ctx-less calls: pass NULL).
+ *  - Pointers are plain host or device pointers as stated per argument; sizes are bytes
+ *    unless stated otherwise. Activations are NHWC fp32, conv weights KRSC fp32
+ *    ([Cout][R][S][Cin], Cin padded to a multiple of 4), FC weight [Cout][Cin].
+ *  - Ownership: the caller owns the device arena, the pinned host arena and the CUDA
+ *    streams and keeps them alive until pooch_destroy; the library never calls
+ *    cudaMalloc / cudaHostAlloc. The library owns the context, profile, plan, schedule,
+ *    CUDA events and the NCCL communicator.
+ *  - A context is single-threaded: one context per device / rank.
+ *  - Asynchronous CUDA faults surface as POOCH_ECUDA at the next call that synchronises.
+ */
+#ifndef POOCH_H
+#define POOCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pooch_ctx pooch_ctx;
+
+typedef enum {
+  POOCH_OK = 0,
+  POOCH_EUSAGE = 1,      /* bad argument / call order */
+  POOCH_EINFEASIBLE = 2, /* no plan fits the budget (memory must never exceed capacity) */
+  POOCH_ENOPLAN = 3,     /* train_step without a current plan (budget / comm changed since) */
+  POOCH_ECUDA = 4,       /* CUDA runtime error; message has the runtime's string */
+  POOCH_ENCCL = 5        /* NCCL error */
+} pooch_status;
+
+/* The three classes of a feature map (Sec. 4.1.1). */
+typedef enum { POOCH_KEEP = 0, POOCH_SWAP = 1, POOCH_RECOMPUTE = 2 } pooch_class;
+
+/* Planning strategies: PoocH itself (Sec. 4.4) and the comparison points of Sec. 5.1-5.2
+ * (P:L352-356). EXHAUSTIVE enumerates all 2*3^(n-1) classifications (n <= 12). */
+typedef enum {
+  POOCH_STRAT_POOCH = 0,
+  POOCH_STRAT_INCORE = 1,
+  POOCH_STRAT_SWAP_ALL_NAIVE = 2,
+  POOCH_STRAT_SWAP_ALL = 3,
+  POOCH_STRAT_SWAP_OPT = 4,
+  POOCH_STRAT_SUPERNEURONS = 5, /* reserved (NEXT f1): returns POOCH_EUSAGE in this build */
+  POOCH_STRAT_EXHAUSTIVE = 6,
+  POOCH_STRAT_FIXED = 7
+} pooch_strategy;
+
+/* Swap-in scheduling (Sec. 4.3): EAGER = "when there is room in the GPU memory";
+ * NAIVE = starts with the computation just before its first user. */
+typedef enum { POOCH_SCHED_EAGER = 0, POOCH_SCHED_NAIVE = 1 } pooch_sched;
+
+/* ------------------------------------------------------------------ network description */
+/* One fused executor task. A task's output is one feature map. */
+typedef enum {
+  POOCH_L_CONV = 0,      /* y = conv(x, W), no bias                     bwd reads {x}      */
+  POOCH_L_BNRELU = 1,    /* y = relu(BN(c)), training-mode BN           bwd reads {c}      */
+  POOCH_L_TAIL_PROJ = 2, /* y = relu(BN3(c3) + BNp(p))  (bottleneck end) bwd reads {c3, p}  */
+  POOCH_L_TAIL_ID = 3,   /* y = relu(BN3(c3) + x)                        bwd reads {c3, x}  */
+  POOCH_L_MAXPOOL = 4,   /* y = maxpool(x)                               bwd reads {x}      */
+  POOCH_L_AVGPOOL = 5,   /* y = mean_hw(x)                               bwd reads {}       */
+  POOCH_L_FC_CE = 6      /* z = flat_hwc(x) W^T + b, softmax-CE loss     bwd reads {x, z}   */
+} pooch_layer_kind;
+
+typedef struct {
+  int32_t kind;          /* pooch_layer_kind */
+  int32_t in0, in1;      /* producer task ids (< this id); -1 = network input / unused */
+  int32_t cin;           /* input channels as stored (padded to a multiple of 4) */
+  int32_t cout, hout, wout; /* output map shape per image (C, H, W) */
+  int32_t k, stride, pad;   /* conv / pool geometry */
+  char name[48];
+} pooch_layer_desc;
+
+typedef struct {
+  int32_t batch;         /* per-rank batch */
+  int32_t in_c, in_h, in_w; /* network input, in_c padded to a multiple of 4 */
+  int32_t classes;
+} pooch_io_desc;
+
+/* Built-in workloads of BASELINE.json: 0 = tiny CNN (config 1), 1 = ResNet-50 v1.5
+ * (configs 2, 3, 5), 2 = ResNet-50 v1. Fills up to *n_layers entries of `out` (host) and
+ * sets *n_layers to the task count (call with out=NULL to query). */
+pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t classes, int32_t width,
+                             pooch_layer_desc* out, int32_t* n_layers);
+
+/* ---------------------------------------------------------------------------- context */
+/* Creates a context for `device`. Parameters are initialised to zero; set them with
+ * pooch_set_param. Returns POOCH_EUSAGE on an invalid graph (non-topological inputs,
+ * unsupported shapes). */
+pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_layers, const pooch_io_desc* io,
+                          int32_t device, pooch_ctx** out);
+void pooch_destroy(pooch_ctx* ctx);
+const char* pooch_last_error(const pooch_ctx* ctx);
+
+/* Device arena (dev_base, dev_bytes: device memory) holds EVERYTHING the library places on
+ * the GPU: parameters, gradients, momentum, BN statistics, the input slot, feature maps,
+ * gradient maps and workspace -- the device-memory budget of the problem statement
+ * (P:L165). Host arena (host_base, host_bytes: page-locked host memory) receives swapped
+ * maps. Marks any plan stale. No device work. */
+pooch_status pooch_set_budget(pooch_ctx* ctx, void* dev_base, size_t dev_bytes, void* host_base,
+                              size_t host_bytes);
+/* Bytes of the resident part of the device arena (params, grads, momentum, stats, input
+ * slot, workspace) -- the minimum budget before any feature map is placed. */
+pooch_status pooch_resident_bytes(const pooch_ctx* ctx, uint64_t* out);
+
+/* cudaStream_t handles (passed as void*): compute, swap-out (D2H), swap-in (H2D), and the
+ * allreduce stream (may be NULL when world == 1). */
+pooch_status pooch_set_streams(pooch_ctx* ctx, void* compute, void* d2h, void* h2d, void* comm);
+
+/* Data parallelism: `nccl_unique_id` points at the 128-byte ncclUniqueId broadcast by the
+ * caller (rank 0 creates it). The library creates its own communicator. Gradients are
+ * summed across ranks and scaled by 1/world in the update. Marks the plan stale. */
+pooch_status pooch_set_comm(pooch_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t world);
+
+/* Input slot inside the device arena: x_dev [batch, in_h, in_w, in_c] fp32, labels_dev
+ * [batch] int32. Valid after pooch_set_budget. */
+pooch_status pooch_input_slot(pooch_ctx* ctx, float** x_dev, int32_t** labels_dev);
+
+/* ------------------------------------------------------------------------- parameters */
+pooch_status pooch_num_params(const pooch_ctx* ctx, int32_t* n);
+/* name (up to 63 chars + NUL) and element count of parameter i; layout as in the header. */
+pooch_status pooch_param_info(const pooch_ctx* ctx, int32_t i, char* name64, int64_t* numel);
+/* which: 0 = value, 1 = gradient of the last step, 2 = momentum. Host buffers, `count`
+ * floats. Synchronises the compute stream. set_param(which=0) also zeroes momentum. */
+pooch_status pooch_get_param(pooch_ctx* ctx, int32_t i, int32_t which, float* host, int64_t count);
+pooch_status pooch_set_param(pooch_ctx* ctx, int32_t i, int32_t which, const float* host, int64_t count);
+
+/* ---------------------------------------------------------------------------- profile */
+/* Per-task measurements of Sec. 4.2: forward / backward / recompute time,
+ * swap-out / swap-in time and feature-map bytes; plus the host-link probe. Arrays are
+ * context-owned and valid until the next pooch_profile / pooch_set_profile / destroy. */
+typedef struct {
+  int32_t n;                 /* tasks == feature maps */
+  const int64_t* fwd_ns;
+  const int64_t* bwd_ns;
+  const int64_t* rec_ns;     /* time of the replay kernels used when the map is recomputed */
+  const int64_t* d2h_ns;
+  const int64_t* h2d_ns;
+  const uint64_t* bytes;     /* feature-map bytes */
+  int64_t tail_ns;           /* update (+ allreduce) after the last backward task */
+  uint64_t resident_bytes;
+  double d2h_gbs, h2d_gbs, duplex_gbs; /* probed host-link bandwidth (GB/s) */
+} pooch_profile_t;
+
+/* Runs `iters` (>= 1) measured iterations under the all-swap classification ("all
+ * feature maps are classified into swap as the default classification") after one warm-up,
+ * keeping the per-task median; if the host arena or budget cannot hold all-swap, tasks are
+ * timed in isolation instead (DESIGN.md Reading 22). Parameters are NOT updated. */
+pooch_status pooch_profile(pooch_ctx* ctx, int32_t iters, pooch_profile_t* out);
+/* Replace the measured times (e.g. the element-wise max over DP ranks). Arrays of n. */
+pooch_status pooch_set_profile(pooch_ctx* ctx, const int64_t* fwd_ns, const int64_t* bwd_ns,
+                               const int64_t* rec_ns, const int64_t* d2h_ns, const int64_t* h2d_ns,
+                               int64_t tail_ns);
+
+/* ----------------------------------------------------------------- host-only planning */
+/* A planning problem in plain arrays (host memory): the simulator's input (Sec. 4.1.2).
+ * inputs / needs are CSR lists: task i consumes maps in_idx[in_ptr[i] .. in_ptr[i+1]) in
+ * forward and its backward reads maps need_idx[need_ptr[i] .. need_ptr[i+1]). */
+typedef struct {
+  int32_t n;
+  const int64_t* fwd_ns;
+  const int64_t* bwd_ns;
+  const int64_t* rec_ns;     /* nullable: = fwd_ns */
+  const int64_t* d2h_ns;
+  const int64_t* h2d_ns;
+  const uint64_t* bytes;
+  const int32_t* in_ptr;
+  const int32_t* in_idx;
+  const int32_t* need_ptr;
+  const int32_t* need_idx;
+  uint64_t resident_bytes;
+  uint64_t budget_bytes;
+  int64_t tail_ns;
+} pooch_problem;
+
+typedef struct {
+  int32_t oom;
+  int64_t makespan_ns;       /* last task end, excluding tail_ns */
+  uint64_t peak_bytes;
+  int32_t n_events;
+  /* optional outputs (nullable), arrays of n: */
+  uint8_t* in_lo;            /* 1 if map in L_O */
+  uint8_t* in_li;            /* 1 if map in L_I */
+  int64_t* stall_ns;         /* swap-in stall charged to the map */
+  /* optional event list (nullable): lane (0 COMPUTE, 1 D2H, 2 H2D), kind ('F','B','R','O','I'),
+   * task id, start, end; up to events_cap entries are written. */
+  int32_t events_cap;
+  int32_t* ev_lane;
+  int32_t* ev_kind;
+  int32_t* ev_id;
+  int64_t* ev_start;
+  int64_t* ev_end;
+} pooch_sim_result;
+
+/* Timeline + memory simulation of one iteration under `classes` (n bytes, pooch_class;
+ * 3 = zero-cost keep used for the Eq. (1) baseline). Host only, deterministic. */
+pooch_status pooch_simulate(const pooch_problem* prob, const uint8_t* classes, int32_t sched,
+                            pooch_sim_result* out);
+
+typedef struct {
+  int32_t li_cap;            /* max |tree| of step 1 (default 16; Reading 16) */
+  int32_t threads;           /* planner threads (0 = hardware concurrency) */
+  int32_t sched;             /* pooch_sched used inside the search (default EAGER) */
+} pooch_search_cfg;
+
+typedef struct {
+  int64_t makespan_ns;       /* simulated iteration time incl. tail */
+  uint64_t peak_bytes;       /* simulated peak device bytes (<= budget) */
+  uint64_t arena_bytes;      /* packed high-water mark of the static offsets (ctx plans only) */
+  int32_t n_keep, n_swap, n_recompute;  /* Table 3 counts */
+  uint64_t host_bytes;       /* pinned bytes needed for the swap class */
+  int64_t n_sims;
+  double wall_ms;
+  int32_t lo_size, li_size;  /* |L_O|, |L_I| of the all-swap timeline */
+  int32_t feasible;
+} pooch_plan_report;
+
+/* Classify with `strategy` (classes_out: n bytes, host). fixed_classes only for
+ * STRAT_FIXED. Returns POOCH_EINFEASIBLE when nothing fits, POOCH_EUSAGE for EXHAUSTIVE
+ * with n > 12. */
+pooch_status pooch_plan_problem(const pooch_problem* prob, int32_t strategy, const pooch_search_cfg* cfg,
+                                const uint8_t* fixed_classes, uint8_t* classes_out,
+                                pooch_plan_report* report);
+
+/* ------------------------------------------------------------------------- execution */
+/* Plans the context's network with its profile and budget, packs static arena offsets and
+ * compiles the three-stream schedule. classes_out (nullable, n bytes) receives the plan. */
+pooch_status pooch_plan(pooch_ctx* ctx, int32_t strategy, const pooch_search_cfg* cfg,
+                        const uint8_t* fixed_classes, uint8_t* classes_out, pooch_plan_report* report);
+
+/* One training iteration: forward, backward with swap / recompute per the plan,
+ * [allreduce], momentum-SGD update with learning rate lr. The batch must already be in the
+ * input slot. loss_host (nullable): if non-NULL the call synchronises and writes the mean
+ * cross-entropy loss; if NULL the call only enqueues work on the caller's streams. */
+pooch_status pooch_train_step(pooch_ctx* ctx, float lr, float* loss_host);
+
+/* Instrumentation: when enabled, train_step records CUDA events around every task and copy.
+ * pooch_last_timing fills per-task durations (ns, arrays of n, nullable) of the last step:
+ * forward, backward, recompute (0 if none), swap-out, swap-in; and the step's total. */
+pooch_status pooch_set_timing(pooch_ctx* ctx, int32_t enable);
+pooch_status pooch_last_timing(pooch_ctx* ctx, int64_t* fwd_ns, int64_t* bwd_ns, int64_t* rec_ns,
+                               int64_t* d2h_ns, int64_t* h2d_ns, int64_t* step_ns);
+
+/* Kernel-family accounting of the last instrumented step: for family f (0 conv-fwd,
+ * 1 conv-dgrad, 2 conv-wgrad, 3 bn-fwd, 4 bn-bwd, 5 pool, 6 fc/ce, 7 sgd, 8 swap-out,
+ * 9 swap-in, 10 allreduce) the summed event time, launch count, algorithmic flops and
+ * algorithmic DRAM bytes. */
+pooch_status pooch_family_stats(pooch_ctx* ctx, int32_t family, double* time_ms, int64_t* launches,
+                                double* flops, double* bytes);
+
+/* ---------------------------------------------------------------- kernel entry points */
+/* Single convolution passes on caller device buffers, launched on `stream` (cudaStream_t).
+ * Used by the parity tests; the executor calls the same launchers.
+ *   fwd  : y[N,Ho,Wo,K] = conv(x[N,H,W,C], w[K,R,S,C]); stat_sum/stat_sq (nullable) receive
+ *          per-128-row-tile column sums [ceil(N*Ho*Wo/128)][K].
+ *   dgrad: dx[N,H,W,C] (=|+=) conv^T(dy[N,Ho,Wo,K], wt[C,R,S,K]).
+ *   wgrad: dw[K,R,S,C] = sum_pixels dy x im2col(x); `ws` device workspace of ws_bytes. */
+typedef struct {
+  int32_t N, H, W, C, K, R, S, stride, pad;
+} pooch_conv_desc;
+
+pooch_status pooch_op_conv_fwd(const pooch_conv_desc* d, const float* x, const float* w, float* y,
+                               float* stat_sum, float* stat_sq, void* stream);
+pooch_status pooch_op_conv_dgrad(const pooch_conv_desc* d, const float* dy, const float* wt, float* dx,
+                                 int32_t accumulate, void* stream);
+pooch_status pooch_op_conv_wgrad(const pooch_conv_desc* d, const float* x, const float* dy, float* dw,
+                                 float* ws, size_t ws_bytes, void* stream);
+size_t pooch_op_conv_wgrad_ws_bytes(const pooch_conv_desc* d);
+/* D[split][M][N] = A * B^T on the tensor-core core; a_mn/b_mn select MN-major operands
+ * (A stored [K][M], B stored [K][N]); bn in {64,128,256}; splits >= 1. Unit test only. */
+pooch_status pooch_op_gemm_test(const float* A, const float* B, float* D, int32_t M, int32_t N, int32_t K,
+                                int32_t a_mn, int32_t b_mn, int32_t bn, int32_t splits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POOCH_H */

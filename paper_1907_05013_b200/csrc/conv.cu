@@ -1,0 +1,212 @@
+// conv.cu -- launchers for the tcgen05 implicit-GEMM convolution passes (fwd, dgrad, wgrad)
+// and the FC layer (a 1x1 "conv" on a 1x1 image), plus the split-K reduction of wgrad.
+#include <algorithm>
+
+#include "common.h"
+#include "conv.h"
+#include "igemm.cuh"
+
+namespace pooch {
+
+ConvGeom conv_geom(const pooch_conv_desc& d) {
+  ConvGeom g{d.N, d.H, d.W, d.C, d.K, d.R, d.S, d.stride, d.pad, 0, 0};
+  g.Ho = (d.H + 2 * d.pad - d.R) / d.stride + 1;
+  g.Wo = (d.W + 2 * d.pad - d.S) / d.stride + 1;
+  return g;
+}
+
+bool conv_shape_ok(const ConvGeom& g) {
+  return g.N > 0 && g.H > 0 && g.W > 0 && g.C > 0 && g.K > 0 && g.R > 0 && g.S > 0 && g.stride > 0 &&
+         g.pad >= 0 && g.C % 4 == 0 && g.K % 4 == 0 && g.Ho > 0 && g.Wo > 0;
+}
+
+template <int MODE, int BN, bool AMN, bool BMN>
+static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st) {
+  constexpr int STAGES = 4;
+  constexpr int SMEM = GemmSmem<BN, STAGES>::TOTAL;
+  auto kern = igemm_kernel<MODE, BN, STAGES, AMN, BMN>;
+  static bool configured = false;
+  if (!configured) {
+    POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    configured = true;
+  }
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return POOCH_OK;
+  kern<<<grid, NUM_THREADS, SMEM, st>>>(p);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+template <int MODE, bool AMN, bool BMN>
+static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st) {
+  switch (bn) {
+    case 64: return launch_igemm<MODE, 64, AMN, BMN>(p, grid, st);
+    case 128: return launch_igemm<MODE, 128, AMN, BMN>(p, grid, st);
+    case 256: return launch_igemm<MODE, 256, AMN, BMN>(p, grid, st);
+  }
+  return fail(POOCH_EUSAGE, "bad tile width %d", bn);
+}
+
+static int pick_bn(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
+
+static GemmParams base_params(const ConvGeom& g) {
+  GemmParams p{};
+  p.N = g.N; p.H = g.H; p.W = g.W; p.C = g.C;
+  p.K = g.K; p.R = g.R; p.S = g.S;
+  p.Ho = g.Ho; p.Wo = g.Wo; p.stride = g.stride; p.pad = g.pad;
+  return p;
+}
+
+pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
+                             float* stat_sq, const float* bias, cudaStream_t st) {
+  GemmParams p = base_params(g);
+  p.M = g.N * g.Ho * g.Wo;
+  p.Ng = g.K;
+  p.Kg = g.R * g.S * g.C;
+  p.a = x; p.b = w; p.d = y;
+  p.stat_sum = stat_sum; p.stat_sq = stat_sq; p.bias = bias;
+  int bn = pick_bn(g.K);
+  dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
+  return launch_bn<CONV_FWD, false, false>(bn, p, grid, st);
+}
+
+pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
+                               cudaStream_t st) {
+  GemmParams p = base_params(g);
+  p.M = g.N * g.H * g.W;
+  p.Ng = g.C;
+  p.Kg = g.R * g.S * g.K;
+  p.a = dy; p.b = wt; p.d = dx;
+  p.accumulate = accumulate ? 1 : 0;
+  int bn = pick_bn(g.C);
+  dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
+  return launch_bn<CONV_DGRAD, false, false>(bn, p, grid, st);
+}
+
+// ---- wgrad: split-K over pixels into a workspace, then a fixed-order reduction.
+struct WgradPlan {
+  int bn, mt, nt, kb, splits, kb_per_split;
+};
+
+static WgradPlan wgrad_plan(const ConvGeom& g) {
+  WgradPlan w{};
+  int rsc = g.R * g.S * g.C;
+  w.bn = pick_bn(rsc);
+  w.mt = (g.K + BM - 1) / BM;
+  w.nt = (rsc + w.bn - 1) / w.bn;
+  w.kb = (g.N * g.Ho * g.Wo + BK - 1) / BK;
+  int tiles = w.mt * w.nt;
+  int want = std::max(1, (2 * 148 + tiles - 1) / tiles);
+  int max_by_k = std::max(1, w.kb / 8);  // at least 8 k-blocks (256 pixels) per split
+  w.splits = std::min(want, max_by_k);
+  w.kb_per_split = (w.kb + w.splits - 1) / w.splits;
+  w.splits = (w.kb + w.kb_per_split - 1) / w.kb_per_split;
+  return w;
+}
+
+size_t conv_wgrad_ws_bytes(const ConvGeom& g) {
+  WgradPlan w = wgrad_plan(g);
+  return w.splits > 1 ? (size_t)w.splits * g.K * g.R * g.S * g.C * sizeof(float) : 0;
+}
+
+__global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out, int64_t n4,
+                                     int splits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = ws[i];
+    for (int s = 1; s < splits; ++s) {
+      float4 b = ws[(int64_t)s * n4 + i];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+
+pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
+                               size_t ws_bytes, cudaStream_t st) {
+  WgradPlan w = wgrad_plan(g);
+  GemmParams p = base_params(g);
+  p.M = g.K;
+  p.Ng = g.R * g.S * g.C;
+  p.Kg = g.N * g.Ho * g.Wo;
+  p.a = dy; p.b = x;
+  p.kb_per_split = w.kb_per_split;
+  bool split = w.splits > 1;
+  if (split && ws_bytes < conv_wgrad_ws_bytes(g))
+    return fail(POOCH_EUSAGE, "wgrad workspace too small: %zu < %zu", ws_bytes, conv_wgrad_ws_bytes(g));
+  p.d = split ? ws : dw;
+  dim3 grid(w.mt, w.nt, w.splits);
+  POOCH_CHECK((launch_bn<CONV_WGRAD, true, true>(w.bn, p, grid, st)));
+  if (split) {
+    int64_t n4 = (int64_t)g.K * p.Ng / 4;
+    int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(ws), reinterpret_cast<float4*>(dw),
+                                                  n4, w.splits);
+    POOCH_CUDA(cudaGetLastError());
+  }
+  return POOCH_OK;
+}
+
+}  // namespace pooch
+
+using namespace pooch;
+
+extern "C" pooch_status pooch_op_conv_fwd(const pooch_conv_desc* d, const float* x, const float* w, float* y,
+                                          float* stat_sum, float* stat_sq, void* stream) {
+  if (!d || !x || !w || !y) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  if ((stat_sum == nullptr) != (stat_sq == nullptr)) return fail(POOCH_EUSAGE, "stat_sum/stat_sq must pair");
+  return launch_conv_fwd(g, x, w, y, stat_sum, stat_sq, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_conv_dgrad(const pooch_conv_desc* d, const float* dy, const float* wt, float* dx,
+                                            int32_t accumulate, void* stream) {
+  if (!d || !dy || !wt || !dx) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  return launch_conv_dgrad(g, dy, wt, dx, accumulate != 0, (cudaStream_t)stream);
+}
+
+extern "C" size_t pooch_op_conv_wgrad_ws_bytes(const pooch_conv_desc* d) {
+  if (!d) return 0;
+  return conv_wgrad_ws_bytes(conv_geom(*d));
+}
+
+extern "C" pooch_status pooch_op_conv_wgrad(const pooch_conv_desc* d, const float* x, const float* dy, float* dw,
+                                            float* ws, size_t ws_bytes, void* stream) {
+  if (!d || !x || !dy || !dw) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  return launch_conv_wgrad(g, x, dy, dw, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+static int g_dbg[5] = {0, 0, 0, 0, 0};
+extern "C" void pooch_dbg_set(int a_lbo, int a_sbo, int a_layout, int a_step, int idesc_xor) {
+  g_dbg[0] = a_lbo; g_dbg[1] = a_sbo; g_dbg[2] = a_layout; g_dbg[3] = a_step; g_dbg[4] = idesc_xor;
+}
+extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float* D, int32_t M, int32_t N,
+                                           int32_t K, int32_t a_mn, int32_t b_mn, int32_t bn, int32_t splits,
+                                           void* stream) {
+  if (!A || !B || !D || M <= 0 || N <= 0 || K <= 0 || splits < 1) return fail(POOCH_EUSAGE, "bad gemm args");
+  int dbg = 0;
+  if (a_mn >= 2) { dbg |= 1; a_mn = 1; }
+  if (b_mn >= 2) { dbg |= 2; b_mn = 1; }
+  if (splits >= 100) { dbg |= 4; splits -= 100; }
+  if (M % 4 || N % 4 || K % 4) return fail(POOCH_EUSAGE, "M, N, K must be multiples of 4");
+  GemmParams p{};
+  p.M = M; p.Ng = N; p.Kg = K;
+  p.a = A; p.b = B; p.d = D;
+  p.lda = a_mn ? M : K;
+  p.ldb = b_mn ? N : K;
+  p.ldd = N;
+  int kb = (K + BK - 1) / BK;
+  p.kb_per_split = (kb + splits - 1) / splits;
+  p.dbg_swap_mn = dbg;
+  p.dbg_a_lbo = g_dbg[0]; p.dbg_a_sbo = g_dbg[1]; p.dbg_a_layout = g_dbg[2]; p.dbg_a_step = g_dbg[3];
+  p.dbg_idesc_xor = (uint32_t)g_dbg[4];
+  dim3 grid((M + BM - 1) / BM, (N + bn - 1) / bn, splits);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a_mn && b_mn) return launch_bn<GEMM_TEST, true, true>(bn, p, grid, st);
+  if (a_mn) return launch_bn<GEMM_TEST, true, false>(bn, p, grid, st);
+  if (b_mn) return launch_bn<GEMM_TEST, false, true>(bn, p, grid, st);
+  return launch_bn<GEMM_TEST, false, false>(bn, p, grid, st);
+}

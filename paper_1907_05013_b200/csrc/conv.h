@@ -1,0 +1,25 @@
+// conv.h -- host launchers of the tensor-core implicit-GEMM kernels (igemm.cuh).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/pooch.h"
+
+namespace pooch {
+
+struct ConvGeom {
+  int N, H, W, C, K, R, S, stride, pad, Ho, Wo;
+};
+ConvGeom conv_geom(const pooch_conv_desc& d);
+bool conv_shape_ok(const ConvGeom& g);
+
+// y = conv(x, w); bias (nullable) per output channel; stat_sum/sq nullable.
+pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
+                             float* stat_sq, const float* bias, cudaStream_t st);
+pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
+                               cudaStream_t st);
+size_t conv_wgrad_ws_bytes(const ConvGeom& g);
+pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
+                               size_t ws_bytes, cudaStream_t st);
+inline int conv_mtiles(const ConvGeom& g) { return (g.N * g.Ho * g.Wo + 127) / 128; }
+
+}  // namespace pooch

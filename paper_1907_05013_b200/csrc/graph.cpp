@@ -1,0 +1,242 @@
+// graph.cpp -- network builders (tiny CNN, ResNet-50) and task-graph derivation.
+//
+// Feature maps are the task outputs retained for backward (Sec. 2.1; P:L160,
+// Sec. 4.1.1). For ResNet-50 the census is 53 conv + 49 BN(+add)+ReLU + maxpool + avgpool
+// + FC = 105 maps, the row total of Table 3.
+#include <algorithm>
+#include <cstring>
+
+#include "common.h"
+#include "graph.h"
+
+namespace pooch {
+
+namespace {
+
+struct Builder {
+  std::vector<pooch_layer_desc> out;
+  int add(int kind, int in0, int in1, int cin, int cout, int h, int w, int k, int s, int p, const std::string& nm) {
+    pooch_layer_desc d{};
+    d.kind = kind; d.in0 = in0; d.in1 = in1; d.cin = cin; d.cout = cout; d.hout = h; d.wout = w;
+    d.k = k; d.stride = s; d.pad = p;
+    std::snprintf(d.name, sizeof(d.name), "%s", nm.c_str());
+    out.push_back(d);
+    return (int)out.size() - 1;
+  }
+};
+
+int co(int h, int k, int s, int p) { return (h + 2 * p - k) / s + 1; }
+
+void tiny(Builder& b, int hw, int classes, int width) {
+  int src = -1, cin = 4;  // input channels padded 3 -> 4
+  for (int l = 0; l < 4; ++l) {
+    int c = b.add(POOCH_L_CONV, src, -1, cin, width, hw, hw, 3, 1, 1, "conv" + std::to_string(l));
+    src = b.add(POOCH_L_BNRELU, c, -1, width, width, hw, hw, 0, 1, 0, "bn" + std::to_string(l));
+    cin = width;
+  }
+  int h2 = hw / 2;
+  int p = b.add(POOCH_L_MAXPOOL, src, -1, width, width, h2, h2, 2, 2, 0, "maxpool");
+  b.add(POOCH_L_FC_CE, p, -1, width * h2 * h2, classes, 1, 1, 0, 1, 0, "fc");
+}
+
+void resnet50(Builder& b, int in_hw, int classes, bool v15) {
+  int hw = co(in_hw, 7, 2, 3);
+  int c = b.add(POOCH_L_CONV, -1, -1, 4, 64, hw, hw, 7, 2, 3, "conv1");
+  int x = b.add(POOCH_L_BNRELU, c, -1, 64, 64, hw, hw, 0, 1, 0, "bn1");
+  hw = co(hw, 3, 2, 1);
+  x = b.add(POOCH_L_MAXPOOL, x, -1, 64, 64, hw, hw, 3, 2, 1, "maxpool");
+  int cin = 64;
+  const int nblocks[4] = {3, 4, 6, 3}, mids[4] = {64, 128, 256, 512};
+  for (int si = 0; si < 4; ++si) {
+    int mid = mids[si], out = 4 * mid;
+    for (int bi = 0; bi < nblocks[si]; ++bi) {
+      int s = (bi == 0 && si > 0) ? 2 : 1;
+      std::string pre = "layer" + std::to_string(si + 1) + "." + std::to_string(bi);
+      int s1 = v15 ? 1 : s, s2 = v15 ? s : 1;
+      int hw1 = co(hw, 1, s1, 0);
+      int c1 = b.add(POOCH_L_CONV, x, -1, cin, mid, hw1, hw1, 1, s1, 0, pre + ".conv1");
+      int y1 = b.add(POOCH_L_BNRELU, c1, -1, mid, mid, hw1, hw1, 0, 1, 0, pre + ".bn1");
+      int hw2 = co(hw1, 3, s2, 1);
+      int c2 = b.add(POOCH_L_CONV, y1, -1, mid, mid, hw2, hw2, 3, s2, 1, pre + ".conv2");
+      int y2 = b.add(POOCH_L_BNRELU, c2, -1, mid, mid, hw2, hw2, 0, 1, 0, pre + ".bn2");
+      int c3 = b.add(POOCH_L_CONV, y2, -1, mid, out, hw2, hw2, 1, 1, 0, pre + ".conv3");
+      if (bi == 0) {
+        int p = b.add(POOCH_L_CONV, x, -1, cin, out, hw2, hw2, 1, s, 0, pre + ".downsample");
+        x = b.add(POOCH_L_TAIL_PROJ, c3, p, out, out, hw2, hw2, 0, 1, 0, pre + ".tail");
+      } else {
+        x = b.add(POOCH_L_TAIL_ID, c3, x, out, out, hw2, hw2, 0, 1, 0, pre + ".tail");
+      }
+      hw = hw2;
+      cin = out;
+    }
+  }
+  int a = b.add(POOCH_L_AVGPOOL, x, -1, cin, cin, 1, 1, 0, 1, 0, "avgpool");
+  b.add(POOCH_L_FC_CE, a, -1, cin, classes, 1, 1, 0, 1, 0, "fc");
+}
+
+}  // namespace
+
+bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io, Graph& g, std::string& err) {
+  g.t.clear();
+  g.io = io;
+  if (n <= 0 || io.batch <= 0 || io.in_c % 4 != 0) {
+    err = "empty graph, bad batch or input channels not a multiple of 4";
+    return false;
+  }
+  for (int i = 0; i < n; ++i) {
+    const pooch_layer_desc& d = layers[i];
+    Task t{};
+    t.kind = d.kind; t.in0 = d.in0; t.in1 = d.in1; t.cin = d.cin; t.cout = d.cout; t.hout = d.hout;
+    t.wout = d.wout; t.k = d.k; t.stride = d.stride; t.pad = d.pad;
+    t.name = std::string(d.name, strnlen(d.name, sizeof(d.name)));
+    if (d.in0 >= i || d.in1 >= i || d.in0 < -1 || d.in1 < -1) {
+      err = "task " + std::to_string(i) + ": inputs must be topological";
+      return false;
+    }
+    if (d.kind < POOCH_L_CONV || d.kind > POOCH_L_FC_CE) {
+      err = "task " + std::to_string(i) + ": bad kind";
+      return false;
+    }
+    if (d.in0 >= 0) t.inputs.push_back(d.in0);
+    if (d.in1 >= 0) t.inputs.push_back(d.in1);
+    bool two = d.kind == POOCH_L_TAIL_PROJ || d.kind == POOCH_L_TAIL_ID;
+    if (two != (d.in1 >= 0) || (d.kind != POOCH_L_CONV && d.in0 < 0)) {
+      err = "task " + std::to_string(i) + ": wrong number of inputs";
+      return false;
+    }
+    // input spatial dims
+    if (d.in0 >= 0) {
+      t.hin = g.t[d.in0].hout;
+      t.win = g.t[d.in0].wout;
+      int cprev = g.t[d.in0].cout;
+      if (d.kind == POOCH_L_FC_CE) cprev *= t.hin * t.win;
+      if (cprev != d.cin) {
+        err = "task " + std::to_string(i) + ": cin does not match producer";
+        return false;
+      }
+    } else {
+      t.hin = io.in_h;
+      t.win = io.in_w;
+      if (d.cin != io.in_c) {
+        err = "task " + std::to_string(i) + ": cin does not match network input";
+        return false;
+      }
+    }
+    if (d.cout % 4 != 0 || d.cin % 4 != 0 || d.cout <= 0 || d.hout <= 0 || d.wout <= 0) {
+      if (!(d.kind == POOCH_L_FC_CE && d.cin % 4 == 0 && d.cout > 0)) {
+        err = "task " + std::to_string(i) + ": channels must be positive multiples of 4";
+        return false;
+      }
+    }
+    if (d.kind == POOCH_L_CONV || d.kind == POOCH_L_MAXPOOL) {
+      if (co(t.hin, d.k, d.stride, d.pad) != d.hout || co(t.win, d.k, d.stride, d.pad) != d.wout) {
+        err = "task " + std::to_string(i) + ": output shape does not match geometry";
+        return false;
+      }
+    }
+    if (d.kind == POOCH_L_FC_CE && i != n - 1) {
+      err = "the FC + cross-entropy task must be the sink";
+      return false;
+    }
+    // bwd reads (see pooch_layer_kind)
+    switch (d.kind) {
+      case POOCH_L_CONV:
+      case POOCH_L_BNRELU:
+      case POOCH_L_TAIL_PROJ:
+      case POOCH_L_TAIL_ID:
+      case POOCH_L_MAXPOOL: t.needs = t.inputs; break;
+      case POOCH_L_AVGPOOL: break;
+      case POOCH_L_FC_CE:
+        t.needs = t.inputs;
+        t.needs.push_back(i);
+        break;
+    }
+    std::sort(t.needs.begin(), t.needs.end());
+    t.map_bytes = (uint64_t)io.batch * d.cout * d.hout * d.wout * 4ull;
+    g.t.push_back(t);
+  }
+  if (g.t.back().kind != POOCH_L_FC_CE) {
+    err = "the last task must be FC + cross-entropy";
+    return false;
+  }
+  for (int i = 0; i < n; ++i)
+    for (int m : g.t[i].inputs) g.t[m].consumers.push_back(i);
+  for (int i = 0; i + 1 < n; ++i)
+    if (g.t[i].consumers.empty()) {
+      err = "task " + std::to_string(i) + " has no consumer (single-sink DAG required)";
+      return false;
+    }
+  return true;
+}
+
+bool problem_from_c(const pooch_problem& p, Problem& o, std::string& err) {
+  if (p.n <= 0 || !p.fwd_ns || !p.bwd_ns || !p.d2h_ns || !p.h2d_ns || !p.bytes || !p.in_ptr || !p.in_idx ||
+      !p.need_ptr || !p.need_idx) {
+    err = "incomplete problem";
+    return false;
+  }
+  o.n = p.n;
+  o.fwd.assign(p.fwd_ns, p.fwd_ns + p.n);
+  o.bwd.assign(p.bwd_ns, p.bwd_ns + p.n);
+  o.rec.assign(p.rec_ns ? p.rec_ns : p.fwd_ns, (p.rec_ns ? p.rec_ns : p.fwd_ns) + p.n);
+  o.d2h.assign(p.d2h_ns, p.d2h_ns + p.n);
+  o.h2d.assign(p.h2d_ns, p.h2d_ns + p.n);
+  o.bytes.assign(p.bytes, p.bytes + p.n);
+  o.inputs.assign(p.n, {});
+  o.needs.assign(p.n, {});
+  for (int i = 0; i < p.n; ++i) {
+    if (o.fwd[i] <= 0 || o.bwd[i] <= 0 || o.rec[i] <= 0 || o.d2h[i] <= 0 || o.h2d[i] <= 0) {
+      err = "durations must be positive (task " + std::to_string(i) + ")";
+      return false;
+    }
+    for (int k = p.in_ptr[i]; k < p.in_ptr[i + 1]; ++k) {
+      int m = p.in_idx[k];
+      if (m < 0) continue;
+      if (m >= i) {
+        err = "task " + std::to_string(i) + ": inputs must be topological";
+        return false;
+      }
+      o.inputs[i].push_back(m);
+    }
+    for (int k = p.need_ptr[i]; k < p.need_ptr[i + 1]; ++k) {
+      int m = p.need_idx[k];
+      if (m < 0 || m > i) {
+        err = "task " + std::to_string(i) + ": needs out of range";
+        return false;
+      }
+      o.needs[i].push_back(m);
+    }
+    std::sort(o.needs[i].begin(), o.needs[i].end());
+    o.needs[i].erase(std::unique(o.needs[i].begin(), o.needs[i].end()), o.needs[i].end());
+  }
+  o.resident = p.resident_bytes;
+  o.budget = p.budget_bytes;
+  o.tail = p.tail_ns;
+  return true;
+}
+
+}  // namespace pooch
+
+using namespace pooch;
+
+extern "C" pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t classes, int32_t width,
+                                        pooch_layer_desc* out, int32_t* n_layers) {
+  if (!n_layers) return fail(POOCH_EUSAGE, "n_layers is null");
+  Builder b;
+  if (which == 0) {
+    if (in_hw <= 0 || in_hw % 2 || width <= 0 || width % 4) return fail(POOCH_EUSAGE, "bad tiny CNN size");
+    tiny(b, in_hw, classes, width);
+  } else if (which == 1 || which == 2) {
+    if (in_hw < 32) return fail(POOCH_EUSAGE, "ResNet-50 input too small");
+    resnet50(b, in_hw, classes, which == 1);
+  } else {
+    return fail(POOCH_EUSAGE, "unknown network %d", which);
+  }
+  int n = (int)b.out.size();
+  if (out) {
+    if (*n_layers < n) return fail(POOCH_EUSAGE, "output array too small (%d < %d)", *n_layers, n);
+    std::copy(b.out.begin(), b.out.end(), out);
+  }
+  *n_layers = n;
+  return POOCH_OK;
+}

@@ -1,0 +1,473 @@
+// igemm.cuh -- implicit-GEMM convolution / FC core on 5th-gen tensor cores (sm_100a).
+//
+// One CTA computes a 128 x BN fp32 tile D = A * B^T with tcgen05.mma kind::tf32
+// (TF32 in, FP32 accumulate in TMEM), K consumed in blocks of 32 elements.
+//
+//   warps 0-3 : producers -- gather A/B chunks (16 B = 4 fp32) straight from the NHWC
+//               tensors with cp.async (zero-fill for padding / tails) into the canonical
+//               SWIZZLE_NONE core-matrix layout, then become the epilogue warps
+//               (tcgen05.ld TMEM -> registers -> fused epilogue -> global).
+//   warp 4    : TMEM allocator + single-thread MMA issuer (tcgen05.mma, tcgen05.commit).
+//
+// Pipeline: STAGES smem slots, mbarrier full/empty ring. A producer thread commits its
+// cp.async group per k-block and, LAG = STAGES-1 blocks later, waits for it, issues
+// fence.proxy.async and arrives on full[]; the MMA thread's tcgen05.commit arrives on
+// empty[] when the tensor core is done reading the slot.
+//
+// Modes (which tensors A and B are, and what the epilogue does):
+//   CONV_FWD  : A = im2col(x) [M=N*Ho*Wo, K=R*S*C] (K-major gather), B = W [Cout, R*S*C];
+//               epilogue stores y (NHWC) + deterministic per-tile BN partial sums.
+//   CONV_DGRAD: A = dy gathered by the transposed-conv rule [M=N*H*W, K=R*S*Cout],
+//               B = Wt [C, R*S*Cout]; epilogue stores (or accumulates into) dx.
+//   CONV_WGRAD: A = dy^T [Cout, K=N*Ho*Wo] (MN-major), B = im2col(x)^T [R*S*C, K] (MN-major);
+//               split-K over pixels, epilogue stores the split's partial dW (KRSC).
+//   GEMM_TEST : plain A/B with either major-ness, for unit tests of the core.
+#pragma once
+#include <cstdint>
+#include <type_traits>
+
+#include "ptx.cuh"
+
+namespace pooch {
+
+enum GemmMode { CONV_FWD = 0, CONV_DGRAD = 1, CONV_WGRAD = 2, GEMM_TEST = 3 };
+
+struct GemmParams {
+  // conv geometry (NHWC activations, KRSC weights)
+  int N, H, W, C;        // input
+  int K, R, S;           // output channels, filter
+  int Ho, Wo, stride, pad;
+  // GEMM view
+  int M, Ng, Kg;
+  // operands
+  const float* a;        // FWD: x, DGRAD: dy, WGRAD: dy, TEST: A
+  const float* b;        // FWD: W, DGRAD: Wt, WGRAD: x, TEST: B
+  float* d;              // FWD: y, DGRAD: dx, WGRAD: partial ws [split][Cout][RSC], TEST: D
+  int lda, ldb, ldd;     // TEST only
+  // epilogue extras
+  float* stat_sum;       // FWD: [Mtiles][K] per-tile column sums (nullptr: skip stats)
+  float* stat_sq;        // FWD: [Mtiles][K] per-tile column sums of squares
+  const float* bias;     // FWD (FC): per-column bias, nullable
+  int accumulate;        // DGRAD: dx += result
+  int kb_per_split;      // WGRAD / TEST: k-blocks handled by one blockIdx.z
+  int dbg_swap_mn;       // TEST only: bit0 swap LBO/SBO of MN-major A, bit1 of MN-major B
+  int dbg_a_lbo, dbg_a_sbo, dbg_a_layout, dbg_a_step;  // TEST only: override A descriptor (lbo>0)
+  uint32_t dbg_idesc_xor;  // TEST only
+};
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per k-block (128 B per row)
+constexpr int NUM_THREADS = 160;
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 4 * BN * 4 * 2 + 1024;
+};
+
+// ---------------------------------------------------------------------------------------
+// K-major operand tile of ROWS rows x 32 k: chunk (row, j) -> ((j*(ROWS/8) + row/8)*128 + (row%8)*16)
+template <int ROWS>
+__device__ __forceinline__ uint32_t kmaj_off(int row, int j) {
+  return (uint32_t)((j * (ROWS / 8) + (row >> 3)) * 128 + (row & 7) * 16);
+}
+// MN-major operand tile of ROWS mn x 32 k, SWIZZLE_128B canonical layout: 1024-B atoms of
+// 8 k-rows x 128 B (32 mn); atom (mn/32, k/8) at ((k/8)*(ROWS/32) + mn/32)*1024; inside an
+// atom the 16-B chunk c = (mn%32)/4 of row r = k%8 sits at r*128 + ((c ^ r)*16).
+template <int ROWS>
+__device__ __forceinline__ uint32_t mnmaj_off(int g, int k) {
+  int r = k & 7, c = g & 7;
+  return (uint32_t)((((k >> 3) * (ROWS / 32) + (g >> 3)) * 1024) + r * 128 + ((c ^ r) << 4));
+}
+
+// ------------------------------------------------------------------------------ loaders
+// Each producer thread (tid 0..127; warp w = tid/32, lane l) owns a fixed set of tile rows
+// (K-major: ROWS/32 rows, 2 chunk columns) or MN groups (MN-major) for the whole k loop.
+
+template <int MODE, int ROWS, bool IS_A>
+struct Loader;
+
+// ---- K-major row gathers (FWD A/B, DGRAD A/B, TEST K-major)
+template <int MODE, int ROWS, bool IS_A>
+struct KLoader {
+  static constexpr int RPT = ROWS / 32;
+  const float* rowp[RPT];   // FWD-A: image base of row's sample; B: row pointer
+  int hi0[RPT], wi0[RPT];   // FWD-A: top-left input coords; DGRAD-A: h+pad, w+pad
+  int nimg[RPT];
+  bool valid[RPT];
+  int lane, warp;
+
+  __device__ void init(const GemmParams& p, int row0, int tid) {
+    warp = tid >> 5;
+    lane = tid & 31;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      int r = warp * (ROWS / 4) + i * 8 + (lane & 7);
+      int gr = row0 + r;
+      if constexpr (IS_A && MODE == CONV_FWD) {
+        valid[i] = gr < p.M;
+        int g = valid[i] ? gr : 0;
+        int wo = g % p.Wo;
+        int t = g / p.Wo;
+        int ho = t % p.Ho;
+        int n = t / p.Ho;
+        rowp[i] = p.a + (size_t)n * p.H * p.W * p.C;
+        hi0[i] = ho * p.stride - p.pad;
+        wi0[i] = wo * p.stride - p.pad;
+      } else if constexpr (IS_A && MODE == CONV_DGRAD) {
+        valid[i] = gr < p.M;
+        int g = valid[i] ? gr : 0;
+        int w = g % p.W;
+        int t = g / p.W;
+        int h = t % p.H;
+        int n = t / p.H;
+        rowp[i] = p.a + (size_t)n * p.Ho * p.Wo * p.K;
+        hi0[i] = h + p.pad;
+        wi0[i] = w + p.pad;
+      } else if constexpr (MODE == GEMM_TEST) {
+        int lim = IS_A ? p.M : p.Ng;
+        int ld = IS_A ? p.lda : p.ldb;
+        valid[i] = gr < lim;
+        rowp[i] = (IS_A ? p.a : p.b) + (size_t)(valid[i] ? gr : 0) * ld;
+      } else {  // B operand of FWD / DGRAD: plain rows of the (transposed) weight
+        valid[i] = gr < p.Ng;
+        rowp[i] = p.b + (size_t)(valid[i] ? gr : 0) * p.Kg;
+      }
+    }
+  }
+
+  __device__ void load(const GemmParams& p, uint32_t sbase, int kb) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int j = (lane >> 3) + 4 * h;
+      int kk = kb * BK + j * 4;
+      bool kok = kk < p.Kg;
+      if constexpr (IS_A && MODE == CONV_FWD) {
+        int rs = kok ? kk / p.C : 0;
+        int c = kk - rs * p.C;
+        int r = rs / p.S;
+        int s = rs - r * p.S;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          int hi = hi0[i] + r, wi = wi0[i] + s;
+          bool ok = kok && valid[i] && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
+          const float* src = ok ? rowp[i] + ((size_t)hi * p.W + wi) * p.C + c : p.a;
+          int row = warp * (ROWS / 4) + i * 8 + (lane & 7);
+          ptx::cp_async16(sbase + kmaj_off<ROWS>(row, j), src, ok ? 16 : 0);
+        }
+      } else if constexpr (IS_A && MODE == CONV_DGRAD) {
+        // k = (r, s, cout): dx[n,h,w,:] += dy[n,(h+pad-r)/st,(w+pad-s)/st,cout] * W[cout,r,s,:]
+        int rs = kok ? kk / p.K : 0;
+        int co = kk - rs * p.K;
+        int r = rs / p.S;
+        int s = rs - r * p.S;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          int th = hi0[i] - r, tw = wi0[i] - s;
+          int ho = th / p.stride, wo = tw / p.stride;
+          bool ok = kok && valid[i] && th >= 0 && tw >= 0 && ho * p.stride == th && wo * p.stride == tw &&
+                    ho < p.Ho && wo < p.Wo;
+          const float* src = ok ? rowp[i] + ((size_t)ho * p.Wo + wo) * p.K + co : p.a;
+          int row = warp * (ROWS / 4) + i * 8 + (lane & 7);
+          ptx::cp_async16(sbase + kmaj_off<ROWS>(row, j), src, ok ? 16 : 0);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          bool ok = kok && valid[i];
+          const float* src = ok ? rowp[i] + kk : p.b;
+          int row = warp * (ROWS / 4) + i * 8 + (lane & 7);
+          ptx::cp_async16(sbase + kmaj_off<ROWS>(row, j), src, ok ? 16 : 0);
+        }
+      }
+    }
+  }
+};
+
+// ---- MN-major gathers (WGRAD A = dy^T, WGRAD B = im2col(x)^T, TEST MN-major)
+template <int MODE, int ROWS, bool IS_A>
+struct MNLoader {
+  static constexpr int GPW = ROWS / 16;   // 4-element MN groups per warp
+  static constexpr int GQ = GPW / 4;      // group sub-blocks per thread
+  int lane, warp;
+  int mn[GQ];                              // first MN element of each owned group
+  bool mnok[GQ];
+  // WGRAD-B: (r, s, c) of the owned groups
+  int gr_[GQ], gs_[GQ], gc_[GQ];
+
+  __device__ void init(const GemmParams& p, int mn0, int tid) {
+    warp = tid >> 5;
+    lane = tid & 31;
+#pragma unroll
+    for (int q = 0; q < GQ; ++q) {
+      int g = warp * GPW + (lane >> 3) + 4 * q;
+      mn[q] = mn0 + 4 * g;
+      int lim = IS_A ? p.M : p.Ng;
+      mnok[q] = mn[q] < lim;
+      if constexpr (MODE == CONV_WGRAD && !IS_A) {
+        int v = mnok[q] ? mn[q] : 0;     // v = (r*S + s)*C + c
+        int rs = v / p.C;
+        gc_[q] = v - rs * p.C;
+        gr_[q] = rs / p.S;
+        gs_[q] = rs - gr_[q] * p.S;
+      }
+    }
+  }
+
+  __device__ void load(const GemmParams& p, uint32_t sbase, int kb) {
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      int k = (lane & 7) + 8 * kq;
+      int kg = kb * BK + k;
+      bool kok = kg < p.Kg;
+      if constexpr (MODE == CONV_WGRAD && IS_A) {
+        const float* rowk = p.a + (size_t)(kok ? kg : 0) * p.K;   // dy[pixel][:]
+#pragma unroll
+        for (int q = 0; q < GQ; ++q) {
+          bool ok = kok && mnok[q];
+          int g = warp * GPW + (lane >> 3) + 4 * q;
+          ptx::cp_async16(sbase + mnmaj_off<ROWS>(g, k), ok ? rowk + mn[q] : p.a, ok ? 16 : 0);
+        }
+      } else if constexpr (MODE == CONV_WGRAD && !IS_A) {
+        int v = kok ? kg : 0;
+        int wo = v % p.Wo;
+        int t = v / p.Wo;
+        int ho = t % p.Ho;
+        int n = t / p.Ho;
+        const float* img = p.b + (size_t)n * p.H * p.W * p.C;
+        int hb = ho * p.stride - p.pad, wb = wo * p.stride - p.pad;
+#pragma unroll
+        for (int q = 0; q < GQ; ++q) {
+          int hi = hb + gr_[q], wi = wb + gs_[q];
+          bool ok = kok && mnok[q] && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
+          int g = warp * GPW + (lane >> 3) + 4 * q;
+          const float* src = ok ? img + ((size_t)hi * p.W + wi) * p.C + gc_[q] : p.b;
+          ptx::cp_async16(sbase + mnmaj_off<ROWS>(g, k), src, ok ? 16 : 0);
+        }
+      } else {  // TEST: [K][MN] row-major
+        const float* base = IS_A ? p.a : p.b;
+        int ld = IS_A ? p.lda : p.ldb;
+#pragma unroll
+        for (int q = 0; q < GQ; ++q) {
+          bool ok = kok && mnok[q];
+          int g = warp * GPW + (lane >> 3) + 4 * q;
+          const float* src = ok ? base + (size_t)kg * ld + mn[q] : base;
+          ptx::cp_async16(sbase + mnmaj_off<ROWS>(g, k), src, ok ? 16 : 0);
+        }
+      }
+    }
+  }
+};
+
+// ------------------------------------------------------------------------------- kernel
+// Butterfly transpose-reduce: on return lane l holds sum over the 32 lanes of v[l].
+__device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      float send = upper ? v[i] : v[i + off];
+      float keep = upper ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams p) {
+  using SM = GemmSmem<BN, STAGES>;
+  constexpr int LAG = STAGES - 1;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float* red = reinterpret_cast<float*>(smem + SM::BAR_OFF + (2 * STAGES + 1) * 8 + 16);  // [4][BN] x2
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  int kb_begin = 0, kb_end = (p.Kg + BK - 1) / BK;
+  if (p.kb_per_split > 0) {
+    kb_begin = blockIdx.z * p.kb_per_split;
+    kb_end = min(kb_end, kb_begin + p.kb_per_split);
+  }
+  const int nkb = max(kb_end - kb_begin, 0);
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 128);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(done, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, BN);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = ptx::smem_u32(smem);
+
+  if (warp < 4) {
+    // ------------------------------------------------------------------ producers
+    using LA = typename std::conditional<A_MN, MNLoader<MODE, BM, true>, KLoader<MODE, BM, true>>::type;
+    using LB = typename std::conditional<B_MN, MNLoader<MODE, BN, false>, KLoader<MODE, BN, false>>::type;
+    LA la;
+    LB lb;
+    la.init(p, m0, tid);
+    lb.init(p, n0, tid);
+    for (int it = 0; it < nkb + LAG; ++it) {
+      if (it < nkb) {
+        int s = it % STAGES;
+        if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        uint32_t st = sbase + s * SM::STAGE_BYTES;
+        la.load(p, st, kb_begin + it);
+        lb.load(p, st + SM::A_BYTES, kb_begin + it);
+      }
+      ptx::cp_async_commit();
+      if (it >= LAG) {
+        ptx::cp_async_wait<LAG>();
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&full[(it - LAG) % STAGES]);
+      }
+    }
+    // ------------------------------------------------------------------ epilogue
+    ptx::mbar_wait(done, 0);
+    ptx::tc_fence_after();
+    if constexpr (MODE == GEMM_TEST) {
+      if (p.dbg_swap_mn & 4) {   // debug: dump smem stage 0 (A then B) after D
+        const float* sm = reinterpret_cast<const float*>(smem);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+          for (int i = tid; i < SM::STAGE_BYTES / 4; i += 128) p.d[(size_t)p.M * p.ldd + i] = sm[i];
+      }
+    }
+    const int lane = tid & 31;
+    const int row = warp * 32 + lane;
+    const int gm = m0 + row;
+    const bool rok = gm < p.M;
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      if (nkb > 0) {
+        ptx::tmem_ld32(taddr + c * 32, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      const int nb = n0 + c * 32;
+      if constexpr (MODE == CONV_FWD) {
+        if (p.bias != nullptr) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Ng) ? __ldg(p.bias + nb + i) : 0.f;
+        }
+      }
+      if (rok) {
+        float* dst;
+        if constexpr (MODE == GEMM_TEST) {
+          dst = p.d + (size_t)blockIdx.z * p.M * p.ldd + (size_t)gm * p.ldd + nb;
+        } else if constexpr (MODE == CONV_WGRAD) {
+          dst = p.d + ((size_t)blockIdx.z * p.M + gm) * p.Ng + nb;
+        } else {
+          dst = p.d + (size_t)gm * p.Ng + nb;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          if (nb + i < p.Ng) {
+            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            if constexpr (MODE == CONV_DGRAD) {
+              if (p.accumulate) {
+                float4 q = *reinterpret_cast<const float4*>(dst + i);
+                o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+              }
+            }
+            *reinterpret_cast<float4*>(dst + i) = o;
+          }
+        }
+      }
+      if constexpr (MODE == CONV_FWD) {
+        if (p.stat_sum != nullptr) {
+          float sq[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v[i] = rok ? v[i] : 0.f;
+            sq[i] = v[i] * v[i];
+          }
+          float s1 = warp_transpose_sum32(v, lane);
+          float s2 = warp_transpose_sum32(sq, lane);
+          red[warp * BN + c * 32 + lane] = s1;
+          red[4 * BN + warp * BN + c * 32 + lane] = s2;
+        }
+      }
+    }
+    if constexpr (MODE == CONV_FWD) {
+      if (p.stat_sum != nullptr) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int j = tid; j < BN; j += 128) {
+          int n = n0 + j;
+          if (n < p.Ng) {
+            float a = ((red[j] + red[BN + j]) + red[2 * BN + j]) + red[3 * BN + j];
+            float b = ((red[4 * BN + j] + red[5 * BN + j]) + red[6 * BN + j]) + red[7 * BN + j];
+            p.stat_sum[(size_t)blockIdx.x * p.Ng + n] = a;
+            p.stat_sq[(size_t)blockIdx.x * p.Ng + n] = b;
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ MMA issuer
+    constexpr uint32_t IDESC = ptx::idesc_tf32(BM, BN, A_MN, B_MN);
+    // K-major (SWIZZLE_NONE): LBO = K-adjacent core-matrix distance, SBO = 128.
+    // MN-major (SWIZZLE_128B): LBO = MN-adjacent atom distance (1024), SBO = 8-k-row group distance.
+    constexpr uint32_t A_LBO = A_MN ? 1024 : BM * 16;
+    constexpr uint32_t B_LBO = B_MN ? 1024 : BN * 16;
+    constexpr uint32_t A_SBO = A_MN ? (BM / 32) * 1024 : 128;
+    constexpr uint32_t B_SBO = B_MN ? (BN / 32) * 1024 : 128;
+    constexpr uint32_t A_STEP = A_MN ? A_SBO : 2 * A_LBO;   // bytes per 8-element MMA k-step
+    constexpr uint32_t B_STEP = B_MN ? B_SBO : 2 * B_LBO;
+    const int lane = tid & 31;
+    for (int it = 0; it < nkb; ++it) {
+      int s = it % STAGES;
+      ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+      ptx::tc_fence_after();
+      if (lane == 0) {
+        uint32_t sa = sbase + s * SM::STAGE_BYTES;
+        uint32_t sb = sa + SM::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          uint64_t ad, bd;
+          if (MODE == GEMM_TEST && p.dbg_a_lbo > 0)
+            ad = ptx::smem_desc(sa + kk * p.dbg_a_step, p.dbg_a_lbo, p.dbg_a_sbo, p.dbg_a_layout);
+          else if (A_MN && (p.dbg_swap_mn & 1)) ad = ptx::smem_desc(sa + kk * A_STEP, A_SBO, A_LBO, 2);
+          else ad = ptx::smem_desc(sa + kk * A_STEP, A_LBO, A_SBO, A_MN ? 2 : 0);
+          if (B_MN && (p.dbg_swap_mn & 2)) bd = ptx::smem_desc(sb + kk * B_STEP, B_SBO, B_LBO, 2);
+          else bd = ptx::smem_desc(sb + kk * B_STEP, B_LBO, B_SBO, B_MN ? 2 : 0);
+          ptx::mma_tf32(tmem, ad, bd, IDESC ^ (MODE == GEMM_TEST ? p.dbg_idesc_xor : 0u), (it | kk) != 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      if (nkb > 0) ptx::mma_commit(done);
+      else ptx::mbar_arrive(done);
+    }
+    __syncwarp();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, BN);
+  }
+}
+
+}  // namespace pooch

@@ -1,0 +1,155 @@
+"""GPU parity of the tensor-core implicit-GEMM passes against the fp64 oracle.
+
+Each case runs one kernel through the C ABI (pooch_op_*) on cuda:0 and
+compares every output element with oracle/layers.py (relative L2 error; TF32
+inputs with fp32 accumulation, tolerance derived in DESIGN.md "Tolerances")."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import synthdata  # noqa: E402
+from oracle import layers as L  # noqa: E402
+
+TOL_OP = 3e-3
+
+
+def _lib():
+    from paper_1907_05013_b200 import _lib
+    return _lib
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+@pytest.mark.parametrize("M,N,K,amn,bmn,bn,splits", [
+    (128, 64, 32, 0, 0, 64, 1), (256, 128, 96, 0, 0, 128, 1), (300, 200, 100, 0, 0, 256, 1),
+    (128, 64, 32, 1, 0, 64, 1), (128, 64, 32, 0, 1, 64, 1), (260, 136, 72, 1, 1, 128, 1),
+    (384, 256, 520, 1, 1, 256, 3), (132, 1000, 2048, 0, 0, 256, 1), (256, 64, 64, 1, 1, 64, 2)])
+def test_gemm_core(M, N, K, amn, bmn, bn, splits):
+    lib = _lib()
+    g = synthdata.rng(M * 7 + N + K)
+    A = g.standard_normal((M, K)).astype(np.float32)
+    B = g.standard_normal((N, K)).astype(np.float32)
+    dA = torch.from_numpy(np.ascontiguousarray(A.T if amn else A)).cuda()
+    dB = torch.from_numpy(np.ascontiguousarray(B.T if bmn else B)).cuda()
+    dD = torch.zeros((splits, M, N), dtype=torch.float32, device="cuda")
+    lib.check(lib.lib.pooch_op_gemm_test(ptr(dA), ptr(dB), ptr(dD), M, N, K, amn, bmn, bn, splits, None))
+    torch.cuda.synchronize()
+    D = dD.cpu().numpy().astype(np.float64).sum(0)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    assert rel(D, ref) < TOL_OP
+
+
+CONV_CASES = [
+    # N, H, W, C, K, R, stride, pad   (ResNet-50 / tiny-CNN shapes, shrunk spatially)
+    (2, 16, 16, 4, 64, 7, 2, 3),      # stem (Cin padded 3->4)
+    (2, 8, 8, 64, 64, 1, 1, 0),       # 1x1
+    (2, 8, 8, 64, 64, 3, 1, 1),       # 3x3
+    (2, 9, 9, 128, 128, 3, 2, 1),     # strided 3x3, ragged
+    (3, 7, 7, 256, 512, 1, 2, 0),     # projection 1x1 stride 2
+    (8, 32, 32, 4, 32, 3, 1, 1),      # tiny CNN first conv
+    (8, 32, 32, 32, 32, 3, 1, 1),     # tiny CNN conv
+    (1, 5, 5, 512, 2048, 1, 1, 0),    # wide 1x1, M < 128
+]
+
+
+def _conv_inputs(N, H, W, Cin, K, R, seed):
+    g = synthdata.rng(seed)
+    x = g.standard_normal((N, H, W, Cin)).astype(np.float32)
+    w = (g.standard_normal((K, R, R, Cin)) / np.sqrt(R * R * Cin)).astype(np.float32)
+    return x, w
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fwd_and_stats(case):
+    lib = _lib()
+    N, H, W, Cin, K, R, s, p = case
+    x, w = _conv_inputs(N, H, W, Cin, K, R, sum(case))
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p)
+    ho, wo = L.conv_out_hw(H, W, R, R, s, p)
+    M = N * ho * wo
+    mt = (M + 127) // 128
+    dx, dw = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    dy = torch.full((N, ho, wo, K), float("nan"), device="cuda")
+    s1 = torch.zeros((mt, K), device="cuda")
+    s2 = torch.zeros((mt, K), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_fwd(C.byref(d), ptr(dx), ptr(dw), ptr(dy), ptr(s1), ptr(s2), None))
+    torch.cuda.synchronize()
+    ref = L.conv2d_fwd(x.transpose(0, 3, 1, 2).astype(np.float64), w.transpose(0, 3, 1, 2).astype(np.float64), s, p)
+    ref = ref.transpose(0, 2, 3, 1)
+    y = dy.cpu().numpy()
+    assert rel(y, ref) < TOL_OP
+    # per-tile partial sums add up to the column sums of y (checked against the oracle output)
+    flat = ref.reshape(-1, K)
+    assert rel(s1.cpu().numpy().astype(np.float64).sum(0), flat.sum(0)) < TOL_OP
+    assert rel(s2.cpu().numpy().astype(np.float64).sum(0), (flat ** 2).sum(0)) < TOL_OP
+
+
+@pytest.mark.parametrize("case", CONV_CASES[1:])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_conv_dgrad(case, accumulate):
+    lib = _lib()
+    N, H, W, Cin, K, R, s, p = case
+    x, w = _conv_inputs(N, H, W, Cin, K, R, sum(case) + 1)
+    ho, wo = L.conv_out_hw(H, W, R, R, s, p)
+    gy = synthdata.rng(5).standard_normal((N, ho, wo, K)).astype(np.float32)
+    prev = synthdata.rng(6).standard_normal((N, H, W, Cin)).astype(np.float32)
+    wt = np.ascontiguousarray(w.transpose(3, 1, 2, 0))   # [C][R][S][K]
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p)
+    dgy, dwt = torch.from_numpy(gy).cuda(), torch.from_numpy(wt).cuda()
+    ddx = torch.from_numpy(prev.copy()).cuda() if accumulate else torch.full((N, H, W, Cin), float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_dgrad(C.byref(d), ptr(dgy), ptr(dwt), ptr(ddx), accumulate, None))
+    torch.cuda.synchronize()
+    ref = L.conv2d_dgrad(gy.transpose(0, 3, 1, 2).astype(np.float64), w.transpose(0, 3, 1, 2).astype(np.float64),
+                         (N, Cin, H, W), s, p).transpose(0, 2, 3, 1)
+    if accumulate:
+        ref = ref + prev
+    assert rel(ddx.cpu().numpy(), ref) < TOL_OP
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_wgrad(case):
+    lib = _lib()
+    N, H, W, Cin, K, R, s, p = case
+    x, w = _conv_inputs(N, H, W, Cin, K, R, sum(case) + 2)
+    ho, wo = L.conv_out_hw(H, W, R, R, s, p)
+    gy = synthdata.rng(7).standard_normal((N, ho, wo, K)).astype(np.float32)
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p)
+    wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(wsb // 4, 1), device="cuda")
+    dx, dgy = torch.from_numpy(x).cuda(), torch.from_numpy(gy).cuda()
+    ddw = torch.full((K, R, R, Cin), float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(dx), ptr(dgy), ptr(ddw), ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    ref = L.conv2d_wgrad(x.transpose(0, 3, 1, 2).astype(np.float64), gy.transpose(0, 3, 1, 2).astype(np.float64),
+                         (K, Cin, R, R), s, p).transpose(0, 2, 3, 1)
+    assert rel(ddw.cpu().numpy(), ref) < TOL_OP
+
+
+def test_conv_large_wgrad_splitk():
+    """A ResNet-50 stage-1 3x3 at batch 16 (M*K large enough to split K many ways)."""
+    lib = _lib()
+    N, H, W, Cin, K, R, s, p = 16, 56, 56, 64, 64, 3, 1, 1
+    x, w = _conv_inputs(N, H, W, Cin, K, R, 11)
+    gy = synthdata.rng(8).standard_normal((N, H, W, K)).astype(np.float32)
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p)
+    wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
+    assert wsb > 0
+    ws = torch.empty(wsb // 4, device="cuda")
+    ddw = torch.empty((K, R, R, Cin), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(torch.from_numpy(x).cuda()), ptr(torch.from_numpy(gy).cuda()),
+                                          ptr(ddw), ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    ref = L.conv2d_wgrad(x.transpose(0, 3, 1, 2).astype(np.float64), gy.transpose(0, 3, 1, 2).astype(np.float64),
+                         (K, Cin, R, R), s, p).transpose(0, 2, 3, 1)
+    assert rel(ddw.cpu().numpy(), ref) < TOL_OP

@@ -1,0 +1,138 @@
+"""The C++ simulator and planner (libpooch.so, host-only calls) against the
+oracle: identical timelines (tolerance 0) and identical class vectors."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synthdata
+from oracle import nets, planner as OP, sim as OS
+
+pp = pytest.importorskip("paper_1907_05013_b200.planning")
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def both(d, **kw):
+    return OS.Profile.from_dict(d, **kw), pp.PlanProblem.from_dict(d, **kw)
+
+
+def _cmp_sim(po, pc, cls, sched):
+    ro = OS.simulate(po, cls, sched)
+    rc = pc.simulate(cls, sched, events=True)
+    assert rc["oom"] == ro.oom
+    assert rc["peak"] == ro.peak or ro.oom
+    if ro.oom:
+        return ro
+    assert rc["makespan"] == ro.makespan
+    assert rc["events"] == [tuple(e) for e in ro.events]
+    assert rc["L_O"] == ro.L_O and rc["L_I"] == ro.L_I
+    assert rc["stall"] == ro.stall
+    return ro
+
+
+def test_spec_and_fig11_through_cabi():
+    d = json.load(open(os.path.join(G, "spec_traces.json")))
+    _, pc = both(d["profile"])
+    assert pc.simulate([OS.KEEP])["makespan"] == d["keep_makespan"]
+    assert pc.simulate([OS.SWAP])["makespan"] == d["swap_makespan"]
+    f = json.load(open(os.path.join(G, "fig11_chain.json")))
+    _, pc = both(f)
+    r = pc.simulate([OS.SWAP] * 8)
+    assert sorted(r["L_O"]) == f["L_O"] and sorted(r["L_I"]) == f["L_I"]
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_sim_differential(seed):
+    g = synthdata.rng(500 + seed)
+    n = int(g.integers(1, 9))
+    d = synthdata.random_profile(n, seed, dag=seed % 2 == 0)
+    budget = int(10 + sum(d["bytes"]) * g.uniform(0.3, 1.6))
+    po, pc = both(d, resident=10, budget=budget)
+    for _ in range(8):
+        cls = [int(c) for c in g.integers(0, 4, n)]
+        if cls[-1] == OS.RECOMPUTE:
+            cls[-1] = OS.SWAP
+        for sched in (OS.EAGER, OS.NAIVE):
+            _cmp_sim(po, pc, cls, sched)
+
+
+def _tight(seed, n):
+    d = synthdata.random_profile(n, seed, dag=seed % 3 == 0)
+    g = synthdata.rng(91 + seed)
+    budget = 10 + max(3 * max(d["bytes"]), int(sum(d["bytes"]) * g.uniform(0.45, 0.95)))
+    return d, budget
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_pooch_identical_to_oracle(seed):
+    d, budget = _tight(seed, 6 + seed % 7)
+    po, pc = both(d, resident=10, budget=budget)
+    ref = OP.pooch(po, li_cap=16)
+    cls, rep = pc.plan("pooch", threads=4)
+    if not ref["feasible"]:
+        assert cls is None
+        return
+    assert cls == ref["cls"]
+    assert rep.makespan_ns == ref["makespan"]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_exhaustive_equals_brute_force(seed):
+    d, budget = _tight(seed, 5 + seed % 3)
+    po, pc = both(d, resident=10, budget=budget)
+    bf = OP.brute_force(po)
+    cls, rep = pc.plan("exhaustive", threads=4)
+    assert cls == bf["cls"]
+    if cls is not None:
+        assert rep.makespan_ns == bf["makespan"]
+
+
+def _net_profile(net, batch, link_gbs, budget, scale_ns=1.0):
+    """Synthetic per-task times for a real graph: compute ~ flops, copies ~ bytes / link."""
+    n = len(net.tasks)
+    fwd, nbytes = [], []
+    for i, t in enumerate(net.tasks):
+        b = batch * net.map_bytes_per_image(i)
+        nbytes.append(b)
+        if t.kind == "conv":
+            c, h, w = t.out_chw
+            fl = 2 * batch * c * h * w * t.cin * t.k * t.k
+            fwd.append(max(1, int(fl / 300e3 * scale_ns)))      # ~300 TFLOP/s
+        else:
+            fwd.append(max(1, int(3 * b / 6e3 * scale_ns)))     # ~6 TB/s, 3 passes
+    bwd = [2 * f for f in fwd]
+    x = [max(1, int(b / link_gbs)) for b in nbytes]
+    inputs = [[j for j in t.inputs if j >= 0] for t in net.tasks]
+    needs = [net.needs(i) for i in range(n)]
+    d = dict(fwd=fwd, bwd=bwd, bytes=nbytes, d2h=x, h2d=x, inputs=inputs, needs=needs)
+    return d
+
+
+@pytest.mark.parametrize("link", [16.0, 75.0])
+def test_tiny_cnn_profile_parity(link):
+    net = nets.tiny_cnn()
+    d = _net_profile(net, 8, link, 0)
+    total = sum(d["bytes"])
+    po, pc = both(d, resident=1_500_000, budget=1_500_000 + total // 2)
+    ref = OP.pooch(po, li_cap=16)
+    cls, _ = pc.plan("pooch")
+    assert cls == (ref["cls"] if ref["feasible"] else None)
+    bf = OP.brute_force(po)
+    if bf["cls"] is not None and ref["feasible"]:
+        assert ref["makespan"] >= bf["makespan"]
+
+
+@pytest.mark.parametrize("link", [16.0, 75.0])
+def test_resnet50_profile_parity_small_cap(link):
+    """Full 105-task ResNet-50 graph at batch 64; li_cap 3 keeps the oracle fast."""
+    net = nets.resnet50()
+    d = _net_profile(net, 64, link, 0)
+    total = sum(d["bytes"])
+    po, pc = both(d, resident=200_000_000, budget=200_000_000 + int(total * 0.35))
+    for cls in ([OS.SWAP] * 105, [OS.KEEP] * 105):
+        _cmp_sim(po, pc, cls, OS.EAGER)
+    ref = OP.pooch(po, li_cap=3)
+    cls, rep = pc.plan("pooch", li_cap=3)
+    assert cls == (ref["cls"] if ref["feasible"] else None)
