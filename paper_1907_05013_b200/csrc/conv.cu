@@ -1,6 +1,7 @@
 // conv.cu -- launchers for the tcgen05 implicit-GEMM convolution passes (fwd, dgrad, wgrad)
 // and the FC layer (a 1x1 "conv" on a 1x1 image), plus the split-K reduction of wgrad.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.h"
 #include "conv.h"
@@ -20,11 +21,11 @@ bool conv_shape_ok(const ConvGeom& g) {
          g.pad >= 0 && g.C % 4 == 0 && g.K % 4 == 0 && g.Ho > 0 && g.Wo > 0;
 }
 
-template <int MODE, int BN, bool AMN, bool BMN>
+template <int MODE, int BN>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st) {
   constexpr int STAGES = 4;
   constexpr int SMEM = GemmSmem<BN, STAGES>::TOTAL;
-  auto kern = igemm_kernel<MODE, BN, STAGES, AMN, BMN>;
+  auto kern = igemm_kernel<MODE, BN, STAGES>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -36,12 +37,12 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   return POOCH_OK;
 }
 
-template <int MODE, bool AMN, bool BMN>
+template <int MODE>
 static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st) {
   switch (bn) {
-    case 64: return launch_igemm<MODE, 64, AMN, BMN>(p, grid, st);
-    case 128: return launch_igemm<MODE, 128, AMN, BMN>(p, grid, st);
-    case 256: return launch_igemm<MODE, 256, AMN, BMN>(p, grid, st);
+    case 64: return launch_igemm<MODE, 64>(p, grid, st);
+    case 128: return launch_igemm<MODE, 128>(p, grid, st);
+    case 256: return launch_igemm<MODE, 256>(p, grid, st);
   }
   return fail(POOCH_EUSAGE, "bad tile width %d", bn);
 }
@@ -66,7 +67,7 @@ pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, 
   p.stat_sum = stat_sum; p.stat_sq = stat_sq; p.bias = bias;
   int bn = pick_bn(g.K);
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
-  return launch_bn<CONV_FWD, false, false>(bn, p, grid, st);
+  return launch_bn<CONV_FWD>(bn, p, grid, st);
 }
 
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
@@ -79,7 +80,7 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
   p.accumulate = accumulate ? 1 : 0;
   int bn = pick_bn(g.C);
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
-  return launch_bn<CONV_DGRAD, false, false>(bn, p, grid, st);
+  return launch_bn<CONV_DGRAD>(bn, p, grid, st);
 }
 
 // ---- wgrad: split-K over pixels into a workspace, then a fixed-order reduction.
@@ -90,7 +91,7 @@ struct WgradPlan {
 static WgradPlan wgrad_plan(const ConvGeom& g) {
   WgradPlan w{};
   int rsc = g.R * g.S * g.C;
-  w.bn = pick_bn(rsc);
+  w.bn = 128;
   w.mt = (g.K + BM - 1) / BM;
   w.nt = (rsc + w.bn - 1) / w.bn;
   w.kb = (g.N * g.Ho * g.Wo + BK - 1) / BK;
@@ -98,6 +99,7 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
   int want = std::max(1, (2 * 148 + tiles - 1) / tiles);
   int max_by_k = std::max(1, w.kb / 8);  // at least 8 k-blocks (256 pixels) per split
   w.splits = std::min(want, max_by_k);
+  if (const char* e = getenv("POOCH_WGRAD_SPLITS")) w.splits = std::max(1, std::min(atoi(e), w.kb));
   w.kb_per_split = (w.kb + w.splits - 1) / w.splits;
   w.splits = (w.kb + w.kb_per_split - 1) / w.kb_per_split;
   return w;
@@ -134,7 +136,7 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
     return fail(POOCH_EUSAGE, "wgrad workspace too small: %zu < %zu", ws_bytes, conv_wgrad_ws_bytes(g));
   p.d = split ? ws : dw;
   dim3 grid(w.mt, w.nt, w.splits);
-  POOCH_CHECK((launch_bn<CONV_WGRAD, true, true>(w.bn, p, grid, st)));
+  POOCH_CHECK((launch_igemm<CONV_WGRAD, 128>(p, grid, st)));
   if (split) {
     int64_t n4 = (int64_t)g.K * p.Ng / 4;
     int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
@@ -179,34 +181,20 @@ extern "C" pooch_status pooch_op_conv_wgrad(const pooch_conv_desc* d, const floa
   return launch_conv_wgrad(g, x, dy, dw, ws, ws_bytes, (cudaStream_t)stream);
 }
 
-static int g_dbg[5] = {0, 0, 0, 0, 0};
-extern "C" void pooch_dbg_set(int a_lbo, int a_sbo, int a_layout, int a_step, int idesc_xor) {
-  g_dbg[0] = a_lbo; g_dbg[1] = a_sbo; g_dbg[2] = a_layout; g_dbg[3] = a_step; g_dbg[4] = idesc_xor;
-}
 extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float* D, int32_t M, int32_t N,
                                            int32_t K, int32_t a_mn, int32_t b_mn, int32_t bn, int32_t splits,
                                            void* stream) {
   if (!A || !B || !D || M <= 0 || N <= 0 || K <= 0 || splits < 1) return fail(POOCH_EUSAGE, "bad gemm args");
-  int dbg = 0;
-  if (a_mn >= 2) { dbg |= 1; a_mn = 1; }
-  if (b_mn >= 2) { dbg |= 2; b_mn = 1; }
-  if (splits >= 100) { dbg |= 4; splits -= 100; }
   if (M % 4 || N % 4 || K % 4) return fail(POOCH_EUSAGE, "M, N, K must be multiples of 4");
+  if (a_mn || b_mn) return fail(POOCH_EUSAGE, "MN-major operands are not supported (K-major only)");
   GemmParams p{};
   p.M = M; p.Ng = N; p.Kg = K;
   p.a = A; p.b = B; p.d = D;
-  p.lda = a_mn ? M : K;
-  p.ldb = b_mn ? N : K;
+  p.lda = K;
+  p.ldb = K;
   p.ldd = N;
   int kb = (K + BK - 1) / BK;
   p.kb_per_split = (kb + splits - 1) / splits;
-  p.dbg_swap_mn = dbg;
-  p.dbg_a_lbo = g_dbg[0]; p.dbg_a_sbo = g_dbg[1]; p.dbg_a_layout = g_dbg[2]; p.dbg_a_step = g_dbg[3];
-  p.dbg_idesc_xor = (uint32_t)g_dbg[4];
   dim3 grid((M + BM - 1) / BM, (N + bn - 1) / bn, splits);
-  cudaStream_t st = (cudaStream_t)stream;
-  if (a_mn && b_mn) return launch_bn<GEMM_TEST, true, true>(bn, p, grid, st);
-  if (a_mn) return launch_bn<GEMM_TEST, true, false>(bn, p, grid, st);
-  if (b_mn) return launch_bn<GEMM_TEST, false, true>(bn, p, grid, st);
-  return launch_bn<GEMM_TEST, false, false>(bn, p, grid, st);
+  return launch_bn<GEMM_TEST>(bn, p, grid, (cudaStream_t)stream);
 }

@@ -1,0 +1,113 @@
+// ctx.h -- the pooch_ctx: resident layout, plan, packed offsets and compiled three-stream
+// schedule of the out-of-core executor.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/pooch.h"
+#include "conv.h"
+#include "graph.h"
+#include "sim.h"
+
+namespace pooch {
+
+enum Family {
+  FAM_CONV_FWD = 0, FAM_CONV_DGRAD, FAM_CONV_WGRAD, FAM_BN_FWD, FAM_BN_BWD, FAM_POOL, FAM_FC_CE, FAM_SGD,
+  FAM_SWAP_OUT, FAM_SWAP_IN, FAM_ALLREDUCE, FAM_OTHER, FAM_COUNT
+};
+
+struct ParamT {
+  std::string name;
+  int task;
+  int64_t numel;
+  size_t off;  // float offset inside the param region
+};
+
+// Per task resident pointers / derived geometry
+struct TaskRt {
+  ConvGeom geom{};      // conv / fc
+  bool is_conv = false; // conv or fc (uses the igemm)
+  int w = -1, b = -1;   // param indices (conv/fc weight, fc bias)
+  int g1 = -1, b1 = -1, g2 = -1, b2 = -1;  // BN params: (gamma, beta) of BN(in0) [and BN(in1)]
+  size_t wt_off = 0;    // float offset of the transposed weight in the wt region
+  // BN statistics of this task's output (conv outputs feeding a BN): floats offset, 4*C
+  size_t stat_off = 0;
+  bool has_stats = false;
+  int bn_gamma = -1, bn_beta = -1;  // params of the BN consuming this conv output
+  int64_t rows = 0;     // N*H*W of the output
+  int cpad = 0;         // FC: padded classes
+  double flops = 0;     // per pass (fwd == dgrad == wgrad for convs)
+};
+
+// One host-enqueued operation of the compiled schedule.
+struct Op {
+  int lane;   // 0 compute, 1 d2h, 2 h2d
+  char kind;  // 'F','R','B','O','I'
+  int id;
+  std::vector<int> waits;  // op indices on other lanes whose completion event must be waited
+  bool record = false;     // another lane waits on this op
+};
+
+struct pooch_ctx_impl;
+
+}  // namespace pooch
+
+struct pooch_ctx {
+  pooch::Graph g;
+  int device = 0;
+  std::string err;
+  // arenas
+  char* dev = nullptr;
+  size_t dev_bytes = 0;
+  char* host = nullptr;
+  size_t host_bytes = 0;
+  // streams
+  cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};  // compute, d2h, h2d, comm
+  bool own_streams = false;
+  // resident layout
+  std::vector<pooch::ParamT> params;
+  int64_t param_floats = 0;
+  std::vector<pooch::TaskRt> rt;
+  size_t off_w = 0, off_g = 0, off_v = 0, off_wt = 0, off_stats = 0, off_tile = 0, off_fin = 0, off_bnws = 0,
+         off_wgws = 0, off_mparg = 0, off_x = 0, off_lab = 0, off_lossrows = 0, off_loss = 0, off_dz = 0;
+  size_t wt_floats = 0, stats_floats = 0, tile_bytes = 0, fin_bytes = 0, bnws_bytes = 0, wgws_bytes = 0,
+         mparg_bytes = 0;
+  size_t resident_end = 0;
+  bool budget_set = false;
+  // profile
+  std::vector<int64_t> fwd_ns, bwd_ns, rec_ns, d2h_ns, h2d_ns;
+  std::vector<uint64_t> map_bytes;
+  int64_t tail_ns = 0;
+  double d2h_gbs = 0, h2d_gbs = 0, duplex_gbs = 0;
+  bool have_profile = false;
+  // plan
+  std::vector<uint8_t> cls;
+  bool have_plan = false;
+  std::vector<size_t> buf_off;   // 3n buffer instances: fwd, bwd, grad (byte offset in dev)
+  std::vector<size_t> host_off;  // per map, swap class only
+  uint64_t arena_high = 0;
+  std::vector<pooch::Op> ops;
+  std::vector<pooch::ProgTask> program;
+  std::vector<int> first_writer;  // per map: task whose bwd writes (not accumulates) its gradient
+  // events
+  std::vector<cudaEvent_t> ev;    // one per op (sync events)
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;   // timing events
+  std::vector<std::pair<int, int>> tseg;  // (event index start, family), per segment
+  std::vector<double> seg_flops, seg_bytes;
+  std::vector<int> seg_task, seg_kind;  // task id and 'F','R','B','O','I','U'
+  int t_used = 0;
+  double fam_ms[pooch::FAM_COUNT] = {0};
+  int64_t fam_launch[pooch::FAM_COUNT] = {0};
+  double fam_flops[pooch::FAM_COUNT] = {0}, fam_bytes[pooch::FAM_COUNT] = {0};
+  std::vector<int64_t> last_fwd, last_bwd, last_rec, last_d2h, last_h2d;
+  int64_t last_step_ns = 0;
+  // dp
+  void* nccl = nullptr;
+  int rank = 0, world = 1;
+  int64_t step_count = 0;
+};

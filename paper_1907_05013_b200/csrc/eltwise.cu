@@ -1,0 +1,569 @@
+// eltwise.cu -- memory-bound kernels (see eltwise.h). HBM-bound: 128-bit loads/stores,
+// grid-stride loops sized to the 148 SMs, fixed-order (deterministic) reductions so that any
+// keep / swap / recompute plan reproduces the in-core run bit for bit.
+#include <algorithm>
+#include <cmath>
+
+#include "common.h"
+#include "eltwise.h"
+
+namespace pooch {
+
+namespace {
+
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float f4get(const float4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+int grid_for(int64_t n, int per_block, int max_blocks = kSMs * 8) {
+  int64_t b = (n + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, max_blocks));
+}
+
+// ------------------------------------------------------------------ BN finalize
+constexpr int kFinRows = 256;  // row-chunks of the tile partials
+
+__global__ void bn_fin_partial_kernel(const float* __restrict__ ts, const float* __restrict__ tq, int tiles, int C,
+                                      double* __restrict__ part) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  int chunk = blockIdx.y;
+  if (c >= C) return;
+  int per = (tiles + kFinRows - 1) / kFinRows;
+  int t0 = chunk * per, t1 = min(tiles, t0 + per);
+  double s = 0, q = 0;
+  for (int t = t0; t < t1; ++t) {
+    s += (double)ts[(size_t)t * C + c];
+    q += (double)tq[(size_t)t * C + c];
+  }
+  part[(size_t)chunk * C + c] = s;
+  part[(size_t)(kFinRows + chunk) * C + c] = q;
+}
+
+__global__ void bn_fin_final_kernel(const double* __restrict__ part, int C, double count, const float* gamma,
+                                    const float* beta, float* mean, float* invstd, float* scale, float* shift) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0, q = 0;
+  for (int r = 0; r < kFinRows; ++r) {
+    s += part[(size_t)r * C + c];
+    q += part[(size_t)(kFinRows + r) * C + c];
+  }
+  double mu = s / count;
+  double var = q / count - mu * mu;
+  if (var < 0) var = 0;
+  float is = (float)(1.0 / sqrt(var + 1e-5));
+  float m = (float)mu;
+  mean[c] = m;
+  invstd[c] = is;
+  float sc = gamma[c] * is;
+  scale[c] = sc;
+  shift[c] = __fsub_rn(beta[c], __fmul_rn(m, sc));
+}
+
+// ------------------------------------------------------------------ BN apply (+add) + ReLU
+template <int MODE>
+__device__ __forceinline__ float pre_act(float a, float sa, float ta, float b, float sb, float tb) {
+  float v = __fmaf_rn(a, sa, ta);
+  if (MODE == 1) v = __fadd_rn(v, __fmaf_rn(b, sb, tb));
+  if (MODE == 2) v = __fadd_rn(v, b);
+  return v;
+}
+
+template <int MODE>
+__global__ void bn_apply_kernel(const float* __restrict__ a, const float* __restrict__ sa, const float* __restrict__ ta,
+                                const float* __restrict__ b, const float* __restrict__ sb,
+                                const float* __restrict__ tb, float* __restrict__ y, int64_t n4, int C4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C4) * 4;
+    float4 av = ld4(a + 4 * i), s1 = ld4(sa + c), t1 = ld4(ta + c);
+    float4 bv = make_float4(0, 0, 0, 0), s2 = bv, t2 = bv;
+    if (MODE != 0) bv = ld4(b + 4 * i);
+    if (MODE == 1) {
+      s2 = ld4(sb + c);
+      t2 = ld4(tb + c);
+    }
+    float4 o;
+    o.x = fmaxf(pre_act<MODE>(av.x, s1.x, t1.x, bv.x, s2.x, t2.x), 0.f);
+    o.y = fmaxf(pre_act<MODE>(av.y, s1.y, t1.y, bv.y, s2.y, t2.y), 0.f);
+    o.z = fmaxf(pre_act<MODE>(av.z, s1.z, t1.z, bv.z, s2.z, t2.z), 0.f);
+    o.w = fmaxf(pre_act<MODE>(av.w, s1.w, t1.w, bv.w, s2.w, t2.w), 0.f);
+    st4(y + 4 * i, o);
+  }
+}
+
+// ------------------------------------------------------------------ BN backward
+constexpr int kBwdThreads = 256;
+constexpr int kBwdMaxBlocks = 592;
+
+int bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, kBwdMaxBlocks)); }
+
+// partial layout in ws: [q][block][C] for q in {sum dz, sum dz*xa, sum dz*xb}
+template <int MODE, int CGPT>
+__global__ void __launch_bounds__(kBwdThreads) bn_bwd_reduce_kernel(BnBwdArgs p, float* __restrict__ part) {
+  extern __shared__ float red[];  // [nq][rpi][C]
+  const int C = p.C, C4 = C / 4;
+  const int tpr = C4 / CGPT;  // threads per row
+  const int rpi = kBwdThreads / tpr;
+  const int tid = threadIdx.x;
+  const int roff = tid / tpr, cg0 = tid % tpr;
+  const int64_t per = (p.rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(p.rows, r0 + per);
+  constexpr int NQ = MODE == 1 ? 3 : 2;
+  float acc[NQ][CGPT][4];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int j = 0; j < CGPT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[q][j][e] = 0.f;
+  if (roff < rpi) {
+    for (int64_t r = r0 + roff; r < r1; r += rpi) {
+#pragma unroll
+      for (int j = 0; j < CGPT; ++j) {
+        int c = 4 * (cg0 + j * tpr);
+        size_t off = (size_t)r * C + c;
+        float4 av = ld4(p.a + off), g = ld4(p.gy + off);
+        float4 s1 = ld4(p.sa + c), t1 = ld4(p.ta + c), m1 = ld4(p.mean_a + c), i1 = ld4(p.invstd_a + c);
+        float4 bv = make_float4(0, 0, 0, 0), s2 = bv, t2 = bv, m2 = bv, i2 = bv;
+        if (MODE != 0) bv = ld4(p.b + off);
+        if (MODE == 1) {
+          s2 = ld4(p.sb + c); t2 = ld4(p.tb + c); m2 = ld4(p.mean_b + c); i2 = ld4(p.invstd_b + c);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float v = pre_act<MODE>(f4get(av, e), f4get(s1, e), f4get(t1, e), f4get(bv, e), f4get(s2, e), f4get(t2, e));
+          float dz = v > 0.f ? f4get(g, e) : 0.f;
+          acc[0][j][e] += dz;
+          acc[1][j][e] += dz * ((f4get(av, e) - f4get(m1, e)) * f4get(i1, e));
+          if (MODE == 1) acc[2 % NQ][j][e] += dz * ((f4get(bv, e) - f4get(m2, e)) * f4get(i2, e));
+        }
+      }
+    }
+  }
+  if (roff < rpi) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int j = 0; j < CGPT; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) red[((size_t)q * rpi + roff) * C + 4 * (cg0 + j * tpr) + e] = acc[q][j][e];
+  }
+  __syncthreads();
+  for (int c = tid; c < C; c += kBwdThreads) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float s = 0.f;
+      for (int r = 0; r < rpi; ++r) s += red[((size_t)q * rpi + r) * C + c];
+      part[((size_t)q * gridDim.x + blockIdx.x) * C + c] = s;
+    }
+  }
+}
+
+// coef layout after the partials: [ka, kb, kc] for BN(a) then BN(b), each [C]
+template <int MODE>
+__global__ void bn_bwd_finalize_kernel(BnBwdArgs p, const float* __restrict__ part, int blocks, float* coef) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= p.C) return;
+  constexpr int NQ = MODE == 1 ? 3 : 2;
+  double s[NQ];
+  for (int q = 0; q < NQ; ++q) {
+    double t = 0;
+    for (int b = 0; b < blocks; ++b) t += (double)part[((size_t)q * blocks + b) * p.C + c];
+    s[q] = t;
+  }
+  double M = (double)p.rows;
+  p.dbeta_a[c] = (float)s[0];
+  p.dgamma_a[c] = (float)s[1];
+  coef[c] = p.gamma_a[c] * p.invstd_a[c];
+  coef[p.C + c] = (float)(s[0] / M);
+  coef[2 * p.C + c] = (float)(s[1] / M);
+  if (MODE == 1) {
+    p.dbeta_b[c] = (float)s[0];
+    p.dgamma_b[c] = (float)s[2 % NQ];
+    coef[3 * p.C + c] = p.gamma_b[c] * p.invstd_b[c];
+    coef[4 * p.C + c] = (float)(s[0] / M);
+    coef[5 * p.C + c] = (float)(s[2 % NQ] / M);
+  }
+}
+
+template <int MODE>
+__global__ void bn_bwd_apply_kernel(BnBwdArgs p, const float* __restrict__ coef, int64_t n4) {
+  const int C = p.C, C4 = C / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C4) * 4;
+    size_t off = 4 * (size_t)i;
+    float4 av = ld4(p.a + off), g = ld4(p.gy + off);
+    float4 s1 = ld4(p.sa + c), t1 = ld4(p.ta + c), m1 = ld4(p.mean_a + c), i1 = ld4(p.invstd_a + c);
+    float4 ka = ld4(coef + c), kb = ld4(coef + C + c), kc = ld4(coef + 2 * C + c);
+    float4 bv = make_float4(0, 0, 0, 0), s2 = bv, t2 = bv, m2 = bv, i2 = bv, la = bv, lb = bv, lc = bv;
+    if (MODE != 0) bv = ld4(p.b + off);
+    if (MODE == 1) {
+      s2 = ld4(p.sb + c); t2 = ld4(p.tb + c); m2 = ld4(p.mean_b + c); i2 = ld4(p.invstd_b + c);
+      la = ld4(coef + 3 * C + c); lb = ld4(coef + 4 * C + c); lc = ld4(coef + 5 * C + c);
+    }
+    float oa[4], ob[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float v = pre_act<MODE>(f4get(av, e), f4get(s1, e), f4get(t1, e), f4get(bv, e), f4get(s2, e), f4get(t2, e));
+      float dz = v > 0.f ? f4get(g, e) : 0.f;
+      float xa = (f4get(av, e) - f4get(m1, e)) * f4get(i1, e);
+      oa[e] = f4get(ka, e) * (dz - f4get(kb, e) - xa * f4get(kc, e));
+      if (MODE == 1) {
+        float xb = (f4get(bv, e) - f4get(m2, e)) * f4get(i2, e);
+        ob[e] = f4get(la, e) * (dz - f4get(lb, e) - xb * f4get(lc, e));
+      } else {
+        ob[e] = dz;
+      }
+    }
+    st4(p.ga + off, make_float4(oa[0], oa[1], oa[2], oa[3]));
+    if (MODE == 1) st4(p.gb + off, make_float4(ob[0], ob[1], ob[2], ob[3]));
+    if (MODE == 2) {
+      float4 o = make_float4(ob[0], ob[1], ob[2], ob[3]);
+      if (p.gb_accumulate) {
+        float4 q = ld4(p.gb + off);
+        o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+      }
+      st4(p.gb + off, o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pooling
+__global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int N, int H, int W, int C4,
+                                   int k, int s, int p, int Ho, int Wo) {
+  int64_t total = (int64_t)N * Ho * Wo * C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int c4 = (int)(i % C4);
+    int64_t t = i / C4;
+    int wo = (int)(t % Wo);
+    t /= Wo;
+    int ho = (int)(t % Ho);
+    int n = (int)(t / Ho);
+    float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    for (int u = 0; u < k; ++u) {
+      int h = ho * s - p + u;
+      if (h < 0 || h >= H) continue;
+      for (int v = 0; v < k; ++v) {
+        int w = wo * s - p + v;
+        if (w < 0 || w >= W) continue;
+        float4 q = ld4(x + (((size_t)n * H + h) * W + w) * C4 * 4 + 4 * c4);
+        m.x = fmaxf(m.x, q.x); m.y = fmaxf(m.y, q.y); m.z = fmaxf(m.z, q.z); m.w = fmaxf(m.w, q.w);
+      }
+    }
+    st4(y + 4 * i, m);
+  }
+}
+
+// window argmax (first maximum in row-major order; -inf padding never wins) -> u*k+v per channel
+__global__ void maxpool_arg_kernel(const float* __restrict__ x, uint8_t* __restrict__ arg, int N, int H, int W,
+                                   int C4, int k, int s, int p, int Ho, int Wo) {
+  int64_t total = (int64_t)N * Ho * Wo * C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int c4 = (int)(i % C4);
+    int64_t t = i / C4;
+    int wo = (int)(t % Wo);
+    t /= Wo;
+    int ho = (int)(t % Ho);
+    int n = (int)(t / Ho);
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    uint8_t a[4] = {255, 255, 255, 255};
+    for (int u = 0; u < k; ++u) {
+      int h = ho * s - p + u;
+      if (h < 0 || h >= H) continue;
+      for (int v = 0; v < k; ++v) {
+        int w = wo * s - p + v;
+        if (w < 0 || w >= W) continue;
+        float4 q = ld4(x + (((size_t)n * H + h) * W + w) * C4 * 4 + 4 * c4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float val = f4get(q, e);
+          if (a[e] == 255 || val > best[e]) {
+            best[e] = val;
+            a[e] = (uint8_t)(u * k + v);
+          }
+        }
+      }
+    }
+    *reinterpret_cast<uchar4*>(arg + 4 * i) = make_uchar4(a[0], a[1], a[2], a[3]);
+  }
+}
+
+__global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ gy,
+                                   float* __restrict__ gx, int N, int H, int W, int C4, int k, int s, int p, int Ho,
+                                   int Wo) {
+  int64_t total = (int64_t)N * H * W * C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int c4 = (int)(i % C4);
+    int64_t t = i / C4;
+    int w = (int)(t % W);
+    t /= W;
+    int h = (int)(t % H);
+    int n = (int)(t / H);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int ho_lo = max(0, (h + p - k + s) / s), ho_hi = min(Ho - 1, (h + p) / s);
+    int wo_lo = max(0, (w + p - k + s) / s), wo_hi = min(Wo - 1, (w + p) / s);
+    for (int ho = ho_lo; ho <= ho_hi; ++ho) {
+      int u = h - (ho * s - p);
+      if (u < 0 || u >= k) continue;
+      for (int wo = wo_lo; wo <= wo_hi; ++wo) {
+        int v = w - (wo * s - p);
+        if (v < 0 || v >= k) continue;
+        size_t o = (((size_t)n * Ho + ho) * Wo + wo) * C4 + c4;
+        uchar4 a = *reinterpret_cast<const uchar4*>(arg + 4 * o);
+        float4 g = ld4(gy + 4 * o);
+        int me = u * k + v;
+        if (a.x == me) acc[0] += g.x;
+        if (a.y == me) acc[1] += g.y;
+        if (a.z == me) acc[2] += g.z;
+        if (a.w == me) acc[3] += g.w;
+      }
+    }
+    st4(gx + 4 * i, make_float4(acc[0], acc[1], acc[2], acc[3]));
+  }
+}
+
+__global__ void avgpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int HW, int C4) {
+  int n = blockIdx.y;
+  int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c4 >= C4) return;
+  float4 s = make_float4(0, 0, 0, 0);
+  for (int i = 0; i < HW; ++i) {
+    float4 q = ld4(x + ((size_t)n * HW + i) * C4 * 4 + 4 * c4);
+    s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+  }
+  float inv = 1.0f / (float)HW;
+  st4(y + ((size_t)n * C4 + c4) * 4, make_float4(s.x * inv, s.y * inv, s.z * inv, s.w * inv));
+}
+
+__global__ void avgpool_bwd_kernel(const float* __restrict__ gy, float* __restrict__ gx, int64_t n4, int HW, int C4) {
+  float inv = 1.0f / (float)HW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    int c4 = (int)(i % C4);
+    int64_t n = i / C4 / HW;
+    float4 g = ld4(gy + (n * C4 + c4) * 4);
+    st4(gx + 4 * i, make_float4(g.x * inv, g.y * inv, g.z * inv, g.w * inv));
+  }
+}
+
+// ------------------------------------------------------------------ softmax cross-entropy
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void ce_rows_kernel(const float* __restrict__ z, const int32_t* __restrict__ lab, int B, int classes,
+                               int ld, float* __restrict__ loss_rows, float* __restrict__ dz, int write_dz) {
+  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (row >= B) return;
+  const float* zr = z + (size_t)row * ld;
+  float m = -INFINITY;
+  for (int c = lane; c < classes; c += 32) m = fmaxf(m, zr[c]);
+  m = warp_max(m);
+  float s = 0.f;
+  for (int c = lane; c < classes; c += 32) s += expf(zr[c] - m);
+  s = warp_sum(s);
+  int t = lab[row];
+  if (!write_dz) {
+    if (lane == 0) loss_rows[row] = logf(s) + m - zr[t];
+    return;
+  }
+  float invB = 1.0f / (float)B;
+  for (int c = lane; c < ld; c += 32) {
+    float v = 0.f;
+    if (c < classes) v = (expf(zr[c] - m) / s - (c == t ? 1.f : 0.f)) * invB;
+    dz[(size_t)row * ld + c] = v;
+  }
+}
+
+__global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+  __shared__ double sh[256];
+  double s = 0;
+  for (int i = threadIdx.x; i < n; i += 256) s += (double)v[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = (float)(sh[0] / n);
+}
+
+__global__ void colsum_kernel(const float* __restrict__ m, int rows, int ld, float* __restrict__ out) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ld) return;
+  float s = 0.f;
+  for (int r = 0; r < rows; ++r) s += m[(size_t)r * ld + c];
+  out[c] = s;
+}
+
+// ------------------------------------------------------------------ SGD, transpose
+__global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g, int64_t n4,
+                           float lr, float mu, float scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 wv = ld4(w + 4 * i), vv = ld4(v + 4 * i), gv = ld4(g + 4 * i);
+    vv.x = mu * vv.x + scale * gv.x; vv.y = mu * vv.y + scale * gv.y;
+    vv.z = mu * vv.z + scale * gv.z; vv.w = mu * vv.w + scale * gv.w;
+    wv.x -= lr * vv.x; wv.y -= lr * vv.y; wv.z -= lr * vv.z; wv.w -= lr * vv.w;
+    st4(v + 4 * i, vv);
+    st4(w + 4 * i, wv);
+  }
+}
+
+__global__ void sgd_tail_kernel(float* w, float* v, const float* g, int64_t start, int64_t n, float lr, float mu,
+                                float scale) {
+  int64_t i = start + threadIdx.x;
+  if (i < n) {
+    v[i] = mu * v[i] + scale * g[i];
+    w[i] -= lr * v[i];
+  }
+}
+
+__global__ void transpose_kernel(const float* __restrict__ w, float* __restrict__ wt, int K, int RS, int C) {
+  __shared__ float tile[32][33];
+  int rs = blockIdx.z;
+  int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int k = k0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && c < C) ? w[((size_t)k * RS + rs) * C + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int c = c0 + i, k = k0 + threadIdx.x;
+    if (c < C && k < K) wt[((size_t)c * RS + rs) * K + k] = tile[threadIdx.x][i];
+  }
+}
+
+}  // namespace
+
+// ======================================================================== launchers
+size_t bn_finalize_ws_bytes(int C) { return (size_t)2 * kFinRows * C * sizeof(double); }
+
+pooch_status bn_finalize(const float* ts, const float* tq, int tiles, int C, int64_t count, const float* gamma,
+                         const float* beta, float* mean, float* invstd, float* scale, float* shift, double* ws,
+                         cudaStream_t st) {
+  dim3 g1((C + 127) / 128, kFinRows);
+  bn_fin_partial_kernel<<<g1, 128, 0, st>>>(ts, tq, tiles, C, ws);
+  bn_fin_final_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, C, (double)count, gamma, beta, mean, invstd, scale, shift);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status bn_apply_relu(const float* a, const float* sa, const float* ta, const float* b, const float* sb,
+                           const float* tb, int mode, float* y, int64_t rows, int C, cudaStream_t st) {
+  int64_t n4 = rows * C / 4;
+  int grid = grid_for(n4, 256);
+  if (mode == 0) bn_apply_kernel<0><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4);
+  else if (mode == 1) bn_apply_kernel<1><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4);
+  else bn_apply_kernel<2><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+size_t bn_bwd_ws_bytes(int C) { return ((size_t)3 * kBwdMaxBlocks * C + 6 * (size_t)C) * sizeof(float); }
+
+template <int MODE>
+static pooch_status bn_bwd_mode(const BnBwdArgs& a, float* ws, cudaStream_t st) {
+  const int C = a.C, C4 = C / 4;
+  int blocks = bwd_blocks(a.rows);
+  int cgpt = C4 > kBwdThreads ? C4 / kBwdThreads : 1;
+  constexpr int NQ = MODE == 1 ? 3 : 2;
+  int tpr = C4 / cgpt;
+  int rpi = kBwdThreads / tpr;
+  size_t smem = (size_t)NQ * rpi * C * sizeof(float);
+  float* coef = ws + (size_t)3 * kBwdMaxBlocks * C;
+  if (cgpt == 1) {
+    if (smem > 48 * 1024) POOCH_CUDA(cudaFuncSetAttribute(bn_bwd_reduce_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bn_bwd_reduce_kernel<MODE, 1><<<blocks, kBwdThreads, smem, st>>>(a, ws);
+  } else if (cgpt == 2) {
+    if (smem > 48 * 1024) POOCH_CUDA(cudaFuncSetAttribute(bn_bwd_reduce_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bn_bwd_reduce_kernel<MODE, 2><<<blocks, kBwdThreads, smem, st>>>(a, ws);
+  } else {
+    return fail(POOCH_EUSAGE, "BN backward supports C <= 2048 (C = %d)", C);
+  }
+  bn_bwd_finalize_kernel<MODE><<<(C + 127) / 128, 128, 0, st>>>(a, ws, blocks, coef);
+  int64_t n4 = a.rows * C / 4;
+  bn_bwd_apply_kernel<MODE><<<grid_for(n4, 256), 256, 0, st>>>(a, coef, n4);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status bn_bwd(const BnBwdArgs& a, float* ws, cudaStream_t st) {
+  if (a.C % 4 != 0 || a.C > 2048 || a.C < 4) return fail(POOCH_EUSAGE, "BN backward: bad C %d", a.C);
+  if (a.mode == 0) return bn_bwd_mode<0>(a, ws, st);
+  if (a.mode == 1) return bn_bwd_mode<1>(a, ws, st);
+  return bn_bwd_mode<2>(a, ws, st);
+}
+
+pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, int k, int s, int p, int Ho, int Wo,
+                         cudaStream_t st) {
+  int64_t total = (int64_t)N * Ho * Wo * C / 4;
+  maxpool_fwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, y, N, H, W, C / 4, k, s, p, Ho, Wo);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* arg_ws, int N, int H, int W, int C,
+                         int k, int s, int p, int Ho, int Wo, cudaStream_t st) {
+  int64_t tot_o = (int64_t)N * Ho * Wo * C / 4, tot_i = (int64_t)N * H * W * C / 4;
+  maxpool_arg_kernel<<<grid_for(tot_o, 256), 256, 0, st>>>(x, arg_ws, N, H, W, C / 4, k, s, p, Ho, Wo);
+  maxpool_bwd_kernel<<<grid_for(tot_i, 256), 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C / 4, k, s, p, Ho, Wo);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status avgpool_fwd(const float* x, float* y, int N, int HW, int C, cudaStream_t st) {
+  dim3 g((C / 4 + 127) / 128, N);
+  avgpool_fwd_kernel<<<g, 128, 0, st>>>(x, y, HW, C / 4);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status avgpool_bwd(const float* gy, float* gx, int N, int HW, int C, cudaStream_t st) {
+  int64_t n4 = (int64_t)N * HW * C / 4;
+  avgpool_bwd_kernel<<<grid_for(n4, 256), 256, 0, st>>>(gy, gx, n4, HW, C / 4);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status ce_fwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* loss_rows, float* loss,
+                    cudaStream_t st) {
+  ce_rows_kernel<<<(B + 7) / 8, 256, 0, st>>>(z, labels, B, classes, ld, loss_rows, nullptr, 0);
+  mean_kernel<<<1, 256, 0, st>>>(loss_rows, B, loss);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status ce_bwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* dz, float* db,
+                    cudaStream_t st) {
+  ce_rows_kernel<<<(B + 7) / 8, 256, 0, st>>>(z, labels, B, classes, ld, nullptr, dz, 1);
+  colsum_kernel<<<(ld + 127) / 128, 128, 0, st>>>(dz, B, ld, db);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status sgd_momentum(float* w, float* v, const float* g, int64_t n, float lr, float mu, float scale,
+                          cudaStream_t st) {
+  int64_t n4 = n / 4;
+  if (n4 > 0) sgd_kernel<<<grid_for(n4, 256), 256, 0, st>>>(w, v, g, n4, lr, mu, scale);
+  if (n % 4) sgd_tail_kernel<<<1, 32, 0, st>>>(w, v, g, n4 * 4, n, lr, mu, scale);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status transpose_krsc(const float* w, float* wt, int K, int RS, int C, cudaStream_t st) {
+  dim3 g((C + 31) / 32, (K + 31) / 32, RS);
+  transpose_kernel<<<g, dim3(32, 8), 0, st>>>(w, wt, K, RS, C);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+}  // namespace pooch

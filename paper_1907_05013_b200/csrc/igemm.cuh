@@ -19,9 +19,13 @@
 //               epilogue stores y (NHWC) + deterministic per-tile BN partial sums.
 //   CONV_DGRAD: A = dy gathered by the transposed-conv rule [M=N*H*W, K=R*S*Cout],
 //               B = Wt [C, R*S*Cout]; epilogue stores (or accumulates into) dx.
-//   CONV_WGRAD: A = dy^T [Cout, K=N*Ho*Wo] (MN-major), B = im2col(x)^T [R*S*C, K] (MN-major);
-//               split-K over pixels, epilogue stores the split's partial dW (KRSC).
-//   GEMM_TEST : plain A/B with either major-ness, for unit tests of the core.
+//   CONV_WGRAD: A = dy^T [Cout, K=N*Ho*Wo], B = im2col(x)^T [R*S*C, K]; both are strided along
+//               K in NHWC, so the producers load 4x4 blocks and transpose them in registers
+//               (TLoader); split-K over pixels, epilogue stores the split's partial dW (KRSC).
+//   GEMM_TEST : plain K-major A [M][K], B [N][K], for unit tests of the core.
+// (All smem operands are K-major SWIZZLE_NONE. MN-major tf32 operands -- transpose bits 15/16
+//  of the instruction descriptor -- produced all-zero results on B200 in our tests, see
+//  DESIGN.md "MN-major tf32".)
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -50,9 +54,6 @@ struct GemmParams {
   const float* bias;     // FWD (FC): per-column bias, nullable
   int accumulate;        // DGRAD: dx += result
   int kb_per_split;      // WGRAD / TEST: k-blocks handled by one blockIdx.z
-  int dbg_swap_mn;       // TEST only: bit0 swap LBO/SBO of MN-major A, bit1 of MN-major B
-  int dbg_a_lbo, dbg_a_sbo, dbg_a_layout, dbg_a_step;  // TEST only: override A descriptor (lbo>0)
-  uint32_t dbg_idesc_xor;  // TEST only
 };
 
 constexpr int BM = 128;
@@ -74,21 +75,9 @@ template <int ROWS>
 __device__ __forceinline__ uint32_t kmaj_off(int row, int j) {
   return (uint32_t)((j * (ROWS / 8) + (row >> 3)) * 128 + (row & 7) * 16);
 }
-// MN-major operand tile of ROWS mn x 32 k, SWIZZLE_128B canonical layout: 1024-B atoms of
-// 8 k-rows x 128 B (32 mn); atom (mn/32, k/8) at ((k/8)*(ROWS/32) + mn/32)*1024; inside an
-// atom the 16-B chunk c = (mn%32)/4 of row r = k%8 sits at r*128 + ((c ^ r)*16).
-template <int ROWS>
-__device__ __forceinline__ uint32_t mnmaj_off(int g, int k) {
-  int r = k & 7, c = g & 7;
-  return (uint32_t)((((k >> 3) * (ROWS / 32) + (g >> 3)) * 1024) + r * 128 + ((c ^ r) << 4));
-}
-
 // ------------------------------------------------------------------------------ loaders
 // Each producer thread (tid 0..127; warp w = tid/32, lane l) owns a fixed set of tile rows
 // (K-major: ROWS/32 rows, 2 chunk columns) or MN groups (MN-major) for the whole k loop.
-
-template <int MODE, int ROWS, bool IS_A>
-struct Loader;
 
 // ---- K-major row gathers (FWD A/B, DGRAD A/B, TEST K-major)
 template <int MODE, int ROWS, bool IS_A>
@@ -187,76 +176,81 @@ struct KLoader {
   }
 };
 
-// ---- MN-major gathers (WGRAD A = dy^T, WGRAD B = im2col(x)^T, TEST MN-major)
-template <int MODE, int ROWS, bool IS_A>
-struct MNLoader {
-  static constexpr int GPW = ROWS / 16;   // 4-element MN groups per warp
-  static constexpr int GQ = GPW / 4;      // group sub-blocks per thread
+// ---- Transposing loaders for wgrad (both operands are contiguous along M/N, strided along
+// K = pixels, in NHWC). Each thread loads 4x4 blocks (4 pixels x 4 channels) with 128-bit
+// global loads into registers, transposes them and stores K-major 16-B chunks with st.shared;
+// the row written at step i is rotated per lane so that every 8-lane phase hits 8 distinct
+// 16-B bank groups. Lane l owns channel group g = l (4 consecutive M/N rows); warp w owns the
+// k chunks h = 2w, 2w+1 of every 32-pixel block. Loads for block kb+1 are issued before the
+// stores of block kb (register double buffering).
+__device__ __forceinline__ float sel4(const float4& v, int i) {
+  float a = (i & 1) ? v.y : v.x;
+  float b = (i & 1) ? v.w : v.z;
+  return (i & 2) ? b : a;
+}
+
+template <bool IS_A>
+struct TLoader {
   int lane, warp;
-  int mn[GQ];                              // first MN element of each owned group
-  bool mnok[GQ];
-  // WGRAD-B: (r, s, c) of the owned groups
-  int gr_[GQ], gs_[GQ], gc_[GQ];
+  bool gok;
+  int mn;                 // first M/N row of this lane's group
+  int gr, gs, gc;         // B: (r, s, c) of the group
+  float4 reg[2][4];
 
   __device__ void init(const GemmParams& p, int mn0, int tid) {
     warp = tid >> 5;
     lane = tid & 31;
+    mn = mn0 + 4 * lane;
+    gok = mn < (IS_A ? p.M : p.Ng);
+    if (!IS_A) {
+      int v = gok ? mn : 0;
+      int rs = v / p.C;
+      gc = v - rs * p.C;
+      gr = rs / p.S;
+      gs = rs - gr * p.S;
+    }
+  }
+
+  __device__ void load(const GemmParams& p, int kb) {
 #pragma unroll
-    for (int q = 0; q < GQ; ++q) {
-      int g = warp * GPW + (lane >> 3) + 4 * q;
-      mn[q] = mn0 + 4 * g;
-      int lim = IS_A ? p.M : p.Ng;
-      mnok[q] = mn[q] < lim;
-      if constexpr (MODE == CONV_WGRAD && !IS_A) {
-        int v = mnok[q] ? mn[q] : 0;     // v = (r*S + s)*C + c
-        int rs = v / p.C;
-        gc_[q] = v - rs * p.C;
-        gr_[q] = rs / p.S;
-        gs_[q] = rs - gr_[q] * p.S;
+    for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        int k = kb * BK + 4 * (2 * warp + hh) + kk;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (IS_A) {
+          if (gok && k < p.Kg) v = __ldg(reinterpret_cast<const float4*>(p.a + (size_t)k * p.K + mn));
+        } else {
+          if (gok && k < p.Kg) {
+            int wo = k % p.Wo;
+            int t = k / p.Wo;
+            int ho = t % p.Ho;
+            int n = t / p.Ho;
+            int hi = ho * p.stride - p.pad + gr, wi = wo * p.stride - p.pad + gs;
+            if ((unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W)
+              v = __ldg(reinterpret_cast<const float4*>(p.b + (((size_t)n * p.H + hi) * p.W + wi) * p.C + gc));
+          }
+        }
+        reg[hh][kk] = v;
       }
     }
   }
 
-  __device__ void load(const GemmParams& p, uint32_t sbase, int kb) {
+  template <int ROWS>
+  __device__ void store(uint32_t sbase) const {
+    const int rot = (lane >> 1) & 3;
 #pragma unroll
-    for (int kq = 0; kq < 4; ++kq) {
-      int k = (lane & 7) + 8 * kq;
-      int kg = kb * BK + k;
-      bool kok = kg < p.Kg;
-      if constexpr (MODE == CONV_WGRAD && IS_A) {
-        const float* rowk = p.a + (size_t)(kok ? kg : 0) * p.K;   // dy[pixel][:]
+    for (int hh = 0; hh < 2; ++hh) {
+      int h = 2 * warp + hh;
 #pragma unroll
-        for (int q = 0; q < GQ; ++q) {
-          bool ok = kok && mnok[q];
-          int g = warp * GPW + (lane >> 3) + 4 * q;
-          ptx::cp_async16(sbase + mnmaj_off<ROWS>(g, k), ok ? rowk + mn[q] : p.a, ok ? 16 : 0);
-        }
-      } else if constexpr (MODE == CONV_WGRAD && !IS_A) {
-        int v = kok ? kg : 0;
-        int wo = v % p.Wo;
-        int t = v / p.Wo;
-        int ho = t % p.Ho;
-        int n = t / p.Ho;
-        const float* img = p.b + (size_t)n * p.H * p.W * p.C;
-        int hb = ho * p.stride - p.pad, wb = wo * p.stride - p.pad;
-#pragma unroll
-        for (int q = 0; q < GQ; ++q) {
-          int hi = hb + gr_[q], wi = wb + gs_[q];
-          bool ok = kok && mnok[q] && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
-          int g = warp * GPW + (lane >> 3) + 4 * q;
-          const float* src = ok ? img + ((size_t)hi * p.W + wi) * p.C + gc_[q] : p.b;
-          ptx::cp_async16(sbase + mnmaj_off<ROWS>(g, k), src, ok ? 16 : 0);
-        }
-      } else {  // TEST: [K][MN] row-major
-        const float* base = IS_A ? p.a : p.b;
-        int ld = IS_A ? p.lda : p.ldb;
-#pragma unroll
-        for (int q = 0; q < GQ; ++q) {
-          bool ok = kok && mnok[q];
-          int g = warp * GPW + (lane >> 3) + 4 * q;
-          const float* src = ok ? base + (size_t)kg * ld + mn[q] : base;
-          ptx::cp_async16(sbase + mnmaj_off<ROWS>(g, k), src, ok ? 16 : 0);
-        }
+      for (int i = 0; i < 4; ++i) {
+        int mi = (i + rot) & 3;
+        int row = 4 * lane + mi;
+        float x0 = sel4(reg[hh][0], mi), x1 = sel4(reg[hh][1], mi), x2 = sel4(reg[hh][2], mi),
+              x3 = sel4(reg[hh][3], mi);
+        uint32_t addr = sbase + kmaj_off<ROWS>(row, h);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x0), "f"(x1), "f"(x2), "f"(x3)
+                     : "memory");
       }
     }
   }
@@ -278,7 +272,7 @@ __device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
   return v[0];
 }
 
-template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN>
+template <int MODE, int BN, int STAGES>
 __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams p) {
   using SM = GemmSmem<BN, STAGES>;
   constexpr int LAG = STAGES - 1;
@@ -318,37 +312,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams 
 
   if (warp < 4) {
     // ------------------------------------------------------------------ producers
-    using LA = typename std::conditional<A_MN, MNLoader<MODE, BM, true>, KLoader<MODE, BM, true>>::type;
-    using LB = typename std::conditional<B_MN, MNLoader<MODE, BN, false>, KLoader<MODE, BN, false>>::type;
-    LA la;
-    LB lb;
-    la.init(p, m0, tid);
-    lb.init(p, n0, tid);
-    for (int it = 0; it < nkb + LAG; ++it) {
-      if (it < nkb) {
+    if constexpr (MODE == CONV_WGRAD) {
+      static_assert(BN == 128, "wgrad uses 128 x 128 tiles");
+      TLoader<true> la;
+      TLoader<false> lb;
+      la.init(p, m0, tid);
+      lb.init(p, n0, tid);
+      TLoader<true> na;
+      TLoader<false> nb;
+      na = la;
+      nb = lb;
+      if (nkb > 0) {
+        la.load(p, kb_begin);
+        lb.load(p, kb_begin);
+      }
+      for (int it = 0; it < nkb; ++it) {
+        if (it + 1 < nkb) {
+          na.load(p, kb_begin + it + 1);
+          nb.load(p, kb_begin + it + 1);
+        }
         int s = it % STAGES;
         if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
-        la.load(p, st, kb_begin + it);
-        lb.load(p, st + SM::A_BYTES, kb_begin + it);
-      }
-      ptx::cp_async_commit();
-      if (it >= LAG) {
-        ptx::cp_async_wait<LAG>();
+        la.template store<BM>(st);
+        lb.template store<BN>(st + SM::A_BYTES);
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&full[(it - LAG) % STAGES]);
+        ptx::mbar_arrive(&full[s]);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            la.reg[hh][kk] = na.reg[hh][kk];
+            lb.reg[hh][kk] = nb.reg[hh][kk];
+          }
+      }
+    } else {
+      KLoader<MODE, BM, true> la;
+      KLoader<MODE, BN, false> lb;
+      la.init(p, m0, tid);
+      lb.init(p, n0, tid);
+      for (int it = 0; it < nkb + LAG; ++it) {
+        if (it < nkb) {
+          int s = it % STAGES;
+          if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          uint32_t st = sbase + s * SM::STAGE_BYTES;
+          la.load(p, st, kb_begin + it);
+          lb.load(p, st + SM::A_BYTES, kb_begin + it);
+        }
+        ptx::cp_async_commit();
+        if (it >= LAG) {
+          ptx::cp_async_wait<LAG>();
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&full[(it - LAG) % STAGES]);
+        }
       }
     }
     // ------------------------------------------------------------------ epilogue
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
-    if constexpr (MODE == GEMM_TEST) {
-      if (p.dbg_swap_mn & 4) {   // debug: dump smem stage 0 (A then B) after D
-        const float* sm = reinterpret_cast<const float*>(smem);
-        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-          for (int i = tid; i < SM::STAGE_BYTES / 4; i += 128) p.d[(size_t)p.M * p.ldd + i] = sm[i];
-      }
-    }
     const int lane = tid & 31;
     const int row = warp * 32 + lane;
     const int gm = m0 + row;
@@ -424,15 +445,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams 
     }
   } else {
     // ------------------------------------------------------------------ MMA issuer
-    constexpr uint32_t IDESC = ptx::idesc_tf32(BM, BN, A_MN, B_MN);
-    // K-major (SWIZZLE_NONE): LBO = K-adjacent core-matrix distance, SBO = 128.
-    // MN-major (SWIZZLE_128B): LBO = MN-adjacent atom distance (1024), SBO = 8-k-row group distance.
-    constexpr uint32_t A_LBO = A_MN ? 1024 : BM * 16;
-    constexpr uint32_t B_LBO = B_MN ? 1024 : BN * 16;
-    constexpr uint32_t A_SBO = A_MN ? (BM / 32) * 1024 : 128;
-    constexpr uint32_t B_SBO = B_MN ? (BN / 32) * 1024 : 128;
-    constexpr uint32_t A_STEP = A_MN ? A_SBO : 2 * A_LBO;   // bytes per 8-element MMA k-step
-    constexpr uint32_t B_STEP = B_MN ? B_SBO : 2 * B_LBO;
+    constexpr uint32_t IDESC = ptx::idesc_tf32(BM, BN, false, false);
+    // K-major SWIZZLE_NONE: LBO = distance of K-adjacent core matrices, SBO = 128 (M/N-adjacent)
+    constexpr uint32_t A_LBO = BM * 16;
+    constexpr uint32_t B_LBO = BN * 16;
     const int lane = tid & 31;
     for (int it = 0; it < nkb; ++it) {
       int s = it % STAGES;
@@ -443,14 +459,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams 
         uint32_t sb = sa + SM::A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          uint64_t ad, bd;
-          if (MODE == GEMM_TEST && p.dbg_a_lbo > 0)
-            ad = ptx::smem_desc(sa + kk * p.dbg_a_step, p.dbg_a_lbo, p.dbg_a_sbo, p.dbg_a_layout);
-          else if (A_MN && (p.dbg_swap_mn & 1)) ad = ptx::smem_desc(sa + kk * A_STEP, A_SBO, A_LBO, 2);
-          else ad = ptx::smem_desc(sa + kk * A_STEP, A_LBO, A_SBO, A_MN ? 2 : 0);
-          if (B_MN && (p.dbg_swap_mn & 2)) bd = ptx::smem_desc(sb + kk * B_STEP, B_SBO, B_LBO, 2);
-          else bd = ptx::smem_desc(sb + kk * B_STEP, B_LBO, B_SBO, B_MN ? 2 : 0);
-          ptx::mma_tf32(tmem, ad, bd, IDESC ^ (MODE == GEMM_TEST ? p.dbg_idesc_xor : 0u), (it | kk) != 0 ? 1u : 0u);
+          uint64_t ad = ptx::smem_desc(sa + kk * 2 * A_LBO, A_LBO, 128);
+          uint64_t bd = ptx::smem_desc(sb + kk * 2 * B_LBO, B_LBO, 128);
+          ptx::mma_tf32(tmem, ad, bd, IDESC, (it | kk) != 0 ? 1u : 0u);
         }
         ptx::mma_commit(&empty[s]);
       }

