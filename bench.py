@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""Benchmark of the out-of-core ResNet-50 training step (BASELINE.json metric).
+
+Default workload (N=1): BASELINE.json config 2 -- ResNet-50 v1.5, batch 640 at
+224x224 (the paper's 50 GB case) under a 16 GiB device-memory budget,
+feature maps swapped over the host link / recomputed per the PoocH plan. The
+timed step is one full training iteration (forward, backward with swap-in /
+recompute, [allreduce], momentum SGD) -- the whole hot path of SURVEY.md 8(a).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--batch B] [--budget-gib G] [--workload cfg2|cfg3]
+
+Under torchrun (N>1) every rank runs its own out-of-core executor on its own
+shard (weak scaling) with an NCCL gradient allreduce; the step time is the max
+over ranks of the CUDA-event time. Rank 0 prints ONE JSON line.
+
+--impl reference times the CPU oracle (oracle/, fp64 NumPy) on the box's host
+cores on a bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "ResNet-50 images/s at >HBM batch, 1/2/4/8 B200; overhead vs in-core; swap GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--budget-gib", type=float, default=None)
+    ap.add_argument("--li-cap", type=int, default=12)
+    ap.add_argument("--no-incore", action="store_true", help="skip the in-core comparison run")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--profile-iters", type=int, default=2)
+    return ap.parse_args()
+
+
+def workload(args):
+    if args.workload == "cfg2":
+        batch = args.batch or 640
+        budget = int((args.budget_gib or 16.0) * (1 << 30))
+        name = "cfg2: ResNet-50 v1.5 batch %d 224^2, device budget %.0f GiB (paper's 50 GB case)" % (
+            batch, budget / (1 << 30))
+    else:
+        batch = args.batch or 2560
+        budget = None  # all free HBM
+        name = "cfg3: ResNet-50 v1.5 batch %d 224^2, all free HBM" % batch
+    return batch, budget, name
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    def __init__(self, idx=0):
+        self.samples = []
+        self.stop = threading.Event()
+        self.idx = idx
+
+    def run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th = threading.Thread(target=self.run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons}
+
+
+def peaks():
+    p = {"hbm_gbs": 6536.0, "bf16_tflops": 1651.0, "bf16_tflops_sustained": 1385.7, "src": "MEASURED_PEAKS.json"}
+    try:
+        p.update(json.load(open(os.path.join(HERE, "MEASURED_PEAKS.json"))))
+    except Exception:
+        p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+             "src": "fallback (B200_PROFILING.md)"}
+    # TF32 = bf16 x the guide's nominal ratio (1.1 / 2.25 PFLOP/s dense)
+    p["tf32_tflops_sustained"] = p["bf16_tflops_sustained"] * (1.1 / 2.25)
+    return p
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def cpu_sample(target_s=15.0, batch=1):
+    """The oracle as it stands: fp64 NumPy ResNet-50 fwd+bwd at 224^2 on host cores."""
+    import numpy as np
+    import synthdata
+    from oracle import nets
+    cores = len(os.sched_getaffinity(0))
+    net = nets.resnet50()
+    params = nets.init_params(net, seed=2)
+    x = synthdata.images(batch, 224, 224, 3, seed=0)
+    t = synthdata.labels(batch, 1000, seed=1)
+    n_img, t0 = 0, time.time()
+    while True:
+        nets.forward_backward(net, params, x, t)
+        n_img += batch
+        if time.time() - t0 > target_s:
+            break
+    dt = time.time() - t0
+    return {"value": n_img / dt, "unit": "images/s", "cores": cores, "kind": "oracle",
+            "sample": "%d fp64 ResNet-50 v1.5 fwd+bwd step(s) at batch %d, 224^2 (NumPy, BLAS threads = cores)" % (
+                n_img // batch, batch)}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    batch, budget, name = workload(args)
+    per = []
+    cs = None
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(target_s=0.0, batch=1)
+        if i >= args.warmup:
+            per.append(s["value"])
+        cs = s
+    v = statistics.median(per)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name + " -- oracle sample: 1 image per step"},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": cs["cores"], "kind": "oracle",
+                             "sample": "1 fp64 ResNet-50 fwd+bwd image per step, 224^2"},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def our_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1907_05013_b200.executor import Context
+    import synthdata
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev_idx = local
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    batch, budget, wname = workload(args)
+    ctx = Context.builtin("resnet50", batch, in_hw=224, classes=1000, device=dev_idx)
+    free, total = torch.cuda.mem_get_info()
+    if budget is None:
+        budget = int(free - (3 << 30))
+    budget = budget // 256 * 256
+    maps_total = sum(ctx_map_bytes(ctx))
+    host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.8 * os.sysconf("SC_PAGE_SIZE") *
+                         os.sysconf("SC_PHYS_PAGES") / max(1, world)))
+    dev = torch.empty(budget, dtype=torch.uint8, device="cuda")
+    host = torch.empty(host_bytes, dtype=torch.uint8, pin_memory=True)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    ctx.set_budget(dev, budget, host, host_bytes)
+    ctx.set_streams(*streams)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            import ctypes
+            nccl = ctypes.CDLL("libnccl.so.2")
+            buf = ctypes.create_string_buffer(128)
+            nccl.ncclGetUniqueId(buf)
+            uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+        uid = uid.cuda()
+        dist.broadcast(uid, 0)
+        ctx.set_comm(bytes(uid.cpu().numpy().tobytes()), rank, world)
+    # parameters and the synthetic batch (seed 0 + rank / 1 + rank; identical weights)
+    g = synthdata.rng(2)
+    for i, (name, numel) in enumerate(ctx.params()):
+        if name.endswith(".w"):
+            fan = numel // int(name_out_channels(ctx, name))
+            ctx.set_param(i, synthdata.he_normal((numel,), fan, g))
+        elif ".gamma" in name:
+            ctx.set_param(i, np.ones(numel, np.float32))
+        else:
+            ctx.set_param(i, np.zeros(numel, np.float32))
+    xp, lp = ctx.input_slot()
+    x_host = torch.from_numpy(np.ascontiguousarray(pad4(synthdata.images(batch, 224, 224, 3, seed=0 + rank))))
+    x_host = x_host.reshape(-1).pin_memory()
+    l_host = torch.from_numpy(synthdata.labels(batch, 1000, seed=1 + rank)).pin_memory()
+    base = dev.data_ptr()
+    x_dev = dev[xp - base: xp - base + x_host.numel() * 4].view(torch.float32)
+    l_dev = dev[lp - base: lp - base + l_host.numel() * 4].view(torch.int32)
+    x_dev.copy_(x_host)
+    l_dev.copy_(l_host)
+    torch.cuda.synchronize()
+
+    # ---- profile (Sec. 4.2) + plan (Sec. 4.4); max over ranks so every rank runs one plan
+    t0 = time.time()
+    prof = ctx.profile(args.profile_iters)
+    prof_s = time.time() - t0
+    if world > 1:
+        arr = torch.tensor([prof[k] for k in ("fwd", "bwd", "rec", "d2h", "h2d")], dtype=torch.int64).cuda()
+        dist.all_reduce(arr, op=dist.ReduceOp.MAX)
+        tail = torch.tensor([prof["tail"]], dtype=torch.int64).cuda()
+        dist.all_reduce(tail, op=dist.ReduceOp.MAX)
+        a = arr.cpu().numpy()
+        ctx.set_profile(a[0], a[1], a[2], a[3], a[4], int(tail.item()))
+    cls, rep = ctx.plan("pooch", li_cap=args.li_cap)
+    counts = {"keep": cls.count(0), "swap": cls.count(1), "recompute": cls.count(2)}
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(n_steps, e2e=False):
+        s = streams[0]
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+        e0.record(s)
+        for _ in range(n_steps):
+            if e2e:
+                with torch.cuda.stream(s):
+                    x_dev.copy_(x_host, non_blocking=True)
+                    l_dev.copy_(l_host, non_blocking=True)
+            ctx.train_step(0.01, sync_loss=False)
+            if e2e:
+                loss_dev = dev[ctx_loss_off(ctx, base):][:4].view(torch.float32)
+                with torch.cuda.stream(s):
+                    loss_h.copy_(loss_dev, non_blocking=True)
+        e1.record(s)
+        barrier()
+        ms = e0.elapsed_time(e1) / n_steps
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64).cuda()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        ctx.train_step(0.01, sync_loss=False)
+    torch.cuda.synchronize()
+    with Clocks(dev_idx) as clk:
+        ms = timed(args.steps)
+    ms_e2e = timed(max(2, args.steps // 2), e2e=True)
+    # instrumented step: per kernel family times (CUDA events on the launching streams)
+    ctx.set_timing(True)
+    ctx.train_step(0.01, sync_loss=True)
+    fam = ctx.family_stats()
+    tim = ctx.last_timing()
+    ctx.set_timing(False)
+    launches = kernel_launches(ctx, args.steps)
+
+    # ---- in-core comparison (the same kernels, every map kept) where it fits
+    incore = None
+    if not args.no_incore and world == 1:
+        incore = incore_run(ctx, dev, host, host_bytes, streams, args, free)
+
+    value = batch * world * 1000.0 / ms
+    pk = peaks()
+    roof = roofline(fam, pk)
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (tf32 tensor-core contractions, fp32 accumulate/storage)",
+        "data": "synthetic (x ~ N(0,1), labels U[0,1000), He-normal weights; seeded)",
+        "config": {"workload": wname, "global_batch": batch * world, "seq_len": None,
+                   "parallelism": "dp%d" % world, "budget_bytes_per_gpu": budget,
+                   "host_arena_bytes": host_bytes, "l2": "inputs > L2 (maps are GBs)",
+                   "plan_counts": counts, "planner_ms": rep["wall_ms"], "planner_sims": rep["n_sims"],
+                   "profile_s": prof_s, "simulated_ms_per_step": rep["makespan_ns"] / 1e6,
+                   "arena_high_water_bytes": rep["arena_bytes"], "L_O": rep["lo_size"], "L_I": rep["li_size"]},
+        "clocks": clk.summary(),
+        "e2e": {"value": batch * world * 1000.0 / ms_e2e, "unit": "images/s",
+                "h2d_bytes_per_step": int(x_host.numel() * 4 + l_host.numel() * 4), "d2h_bytes_per_step": 4},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "swap": swap_stats(fam, prof),
+        "families_ms": {k: round(v["ms"], 3) for k, v in fam.items()},
+    }
+    if incore is not None:
+        line["incore"] = incore
+        if incore.get("images_per_s"):
+            line["overhead_vs_incore"] = 1.0 - value / incore["images_per_s"]
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_sample(15.0, batch=1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def pad4(x):
+    import numpy as np
+    out = np.zeros(x.shape[:3] + (4,), np.float32)
+    out[..., :3] = x
+    return out
+
+
+def ctx_map_bytes(ctx):
+    return [ctx.batch * l.cout * l.hout * l.wout * 4 for l in ctx.layers]
+
+
+def name_out_channels(ctx, pname):
+    task = pname.rsplit(".", 1)[0]
+    for l in ctx.layers:
+        if l.name.decode() == task:
+            return l.cout if l.kind == 0 else ((l.cout + 3) // 4 * 4)
+    raise KeyError(pname)
+
+
+def ctx_loss_off(ctx, base):
+    import ctypes as C
+    from paper_1907_05013_b200._lib import lib
+    x, l = ctx.input_slot()
+    # loss scalar follows the label and loss-row slots (see executor.cpp layout_resident)
+    b = ctx.batch
+    off = l - base
+    off = (off + b * 4 + 255) // 256 * 256          # loss rows
+    off = (off + b * 4 + 255) // 256 * 256          # loss
+    return off
+
+
+def kernel_launches(ctx, steps):
+    import ctypes as C
+    from paper_1907_05013_b200._lib import lib
+    v = C.c_int64()
+    if hasattr(lib, "pooch_kernel_launches"):
+        lib.pooch_kernel_launches(ctx.h, C.byref(v))
+        return int(v.value) * steps
+    return None
+
+
+def roofline(fam, pk):
+    """Dominant kernel family of the instrumented step vs its roof."""
+    cand = {k: v for k, v in fam.items() if k not in ("other", "swap_out", "swap_in") and v["ms"] > 0}
+    if not cand:
+        return None
+    k, v = max(cand.items(), key=lambda kv: kv[1]["ms"])
+    t = v["ms"] / 1e3
+    tf = pk["tf32_tflops_sustained"] * 1e12
+    bw = pk["hbm_gbs"] * 1e9
+    if v["flops"] / tf >= v["bytes"] / bw and v["flops"] > 0:
+        ach = v["flops"] / t / 1e12
+        return {"kernel": k, "bound": "tensor", "achieved": ach, "peak": pk["tf32_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": ach / pk["tf32_tflops_sustained"], "traffic": traffic_for(k),
+                "launches": v["launches"], "peak_src": pk["src"] + " bf16 sustained x (1.1/2.25) nominal tf32 ratio"}
+    ach = v["bytes"] / t / 1e9
+    return {"kernel": k, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": ach / pk["hbm_gbs"], "traffic": traffic_for(k), "launches": v["launches"],
+            "peak_src": pk["src"]}
+
+
+def traffic_for(family):
+    try:
+        d = json.load(open(os.path.join(HERE, "profiles", "ncu_traffic.json")))
+        return d.get(family)
+    except Exception:
+        return None
+
+
+def swap_stats(fam, prof):
+    out = {"probe_d2h_gbs": prof["d2h_gbs"], "probe_h2d_gbs": prof["h2d_gbs"], "probe_duplex_gbs": prof["duplex_gbs"]}
+    for k in ("swap_out", "swap_in"):
+        v = fam[k]
+        out[k + "_gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
+        out[k + "_bytes"] = v["bytes"]
+    return out
+
+
+def incore_run(ctx_ooc, dev, host, host_bytes, streams, args, free):
+    """Same kernels with every map kept: needs the full footprint in HBM."""
+    import torch
+    from paper_1907_05013_b200.executor import Context
+    batch = ctx_ooc.batch
+    try:
+        ctx = Context.builtin("resnet50", batch, in_hw=224, classes=1000)
+        need = int(ctx.resident_bytes() + sum(ctx_map_bytes(ctx)) * 1.4)
+        free_now, _ = torch.cuda.mem_get_info()
+        if need > free_now - (2 << 30):
+            return {"images_per_s": None, "note": "in-core does not fit (%d GB needed)" % (need >> 30)}
+        big = torch.empty(need // 256 * 256, dtype=torch.uint8, device="cuda")
+        ctx.set_budget(big, big.numel(), None, 0)
+        ctx.set_streams(*streams)
+        for i, (name, numel) in enumerate(ctx.params()):
+            ctx.set_param(i, ctx_ooc.get_param(i, 0))
+        ctx.profile(1)
+        ctx.plan("incore")
+        for _ in range(2):
+            ctx.train_step(0.01, sync_loss=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = max(2, args.steps)
+        e0.record(streams[0])
+        for _ in range(n):
+            ctx.train_step(0.01, sync_loss=False)
+        e1.record(streams[0])
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        ctx.close()
+        del big
+        torch.cuda.empty_cache()
+        return {"images_per_s": batch * 1000.0 / ms, "ms_per_step": ms}
+    except Exception as e:  # report, never fake
+        return {"images_per_s": None, "note": "in-core run failed: %s" % e}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -249,12 +249,26 @@ pooch_status pooch_plan(pooch_ctx* ctx, int32_t strategy, const pooch_search_cfg
  * cross-entropy loss; if NULL the call only enqueues work on the caller's streams. */
 pooch_status pooch_train_step(pooch_ctx* ctx, float lr, float* loss_host);
 
+/* Device address of the step's mean loss (fp32 scalar inside the arena), for callers that
+ * read it back asynchronously on their own stream. */
+pooch_status pooch_loss_slot(pooch_ctx* ctx, float** loss_dev);
+
+/* Test / debug access: copies up to `bytes` of buffer instance `which` (0 = forward
+ * instance, 1 = backward-phase instance, 2 = gradient) of feature map `map` as placed by the
+ * current plan into `host`. Synchronises the compute stream. Contents are only meaningful
+ * while the instance is live in the last step (e.g. every map under the in-core plan). */
+pooch_status pooch_read_buffer(pooch_ctx* ctx, int32_t which, int32_t map, void* host, size_t bytes);
+
 /* Instrumentation: when enabled, train_step records CUDA events around every task and copy.
  * pooch_last_timing fills per-task durations (ns, arrays of n, nullable) of the last step:
  * forward, backward, recompute (0 if none), swap-out, swap-in; and the step's total. */
 pooch_status pooch_set_timing(pooch_ctx* ctx, int32_t enable);
 pooch_status pooch_last_timing(pooch_ctx* ctx, int64_t* fwd_ns, int64_t* bwd_ns, int64_t* rec_ns,
                                int64_t* d2h_ns, int64_t* h2d_ns, int64_t* step_ns);
+
+/* Number of CUDA kernels this library launched in the last pooch_train_step (all streams;
+ * copies and NCCL calls not counted). */
+pooch_status pooch_kernel_launches(pooch_ctx* ctx, int64_t* per_step);
 
 /* Kernel-family accounting of the last instrumented step: for family f (0 conv-fwd,
  * 1 conv-dgrad, 2 conv-wgrad, 3 bn-fwd, 4 bn-bwd, 5 pool, 6 fc/ce, 7 sgd, 8 swap-out,

@@ -15,6 +15,18 @@ BN_EPS = 1e-5          # Reading 23 (paper silent)
 SGD_MOMENTUM = 0.9     # Reading 23
 
 
+# ---------------------------------------------------------------- TF32 operands
+def tf32(x):
+    """Operand precision of the kernels' tensor-core contractions (BASELINE.json
+    north_star: "TF32 in, FP32 accumulate"; DESIGN.md Reading 27): the value is
+    rounded to fp32, then the 13 low mantissa bits are dropped (truncation, as
+    measured on B200 -- tools/dbg_tf32.py). Returned as fp64. Used only when the
+    oracle is asked to take decisions (ReLU masks, max-pool argmax) in the
+    kernel's precision; the default oracle is exact fp64."""
+    u = np.asarray(x, dtype=np.float32).view(np.uint32) & np.uint32(0xFFFFE000)
+    return u.view(np.float32).astype(np.float64)
+
+
 # --------------------------------------------------------------------------- conv
 def conv_out_hw(h: int, w: int, r: int, s: int, stride: int, pad: int):
     return (h + 2 * pad - r) // stride + 1, (w + 2 * pad - s) // stride + 1

@@ -163,11 +163,16 @@ def _flat_hwc(x):
     return x.transpose(0, 2, 3, 1).reshape(x.shape[0], -1)
 
 
-def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndarray):
+def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndarray, map_grads=None,
+                     precision: str = "fp64"):
     """One fp64 fwd + bwd of ``net``. ``x_nhwc`` is the (unpadded)
     input batch in NHWC; params are promoted to fp64. Returns (loss, grads,
     outputs) with grads keyed like ``params`` and outputs the fp64 task
-    outputs (NCHW) for map-level checks."""
+    outputs (NCHW) for map-level checks; ``map_grads`` (a list) receives the
+    gradient of every map. ``precision="tf32"`` rounds the operands of every
+    contraction (conv fwd / dgrad / wgrad, FC) with ``layers.tf32`` -- the
+    kernels' operand precision -- and keeps everything else in fp64."""
+    q = L.tf32 if precision == "tf32" else (lambda a: a)
     P = {k: np.asarray(v, dtype=np.float64) for k, v in params.items()}
     x_in = np.asarray(x_nhwc, dtype=np.float64).transpose(0, 3, 1, 2)
     outs, caches = [], []
@@ -178,7 +183,7 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
     loss = None
     for t in net.tasks:
         if t.kind == "conv":
-            y = L.conv2d_fwd(get(t.inputs[0]), P[t.name + ".w"], t.stride, t.pad)
+            y = L.conv2d_fwd(q(get(t.inputs[0])), q(P[t.name + ".w"]), t.stride, t.pad)
             cache = None
         elif t.kind == "bnrelu":
             z, bc = L.bn_fwd(get(t.inputs[0]), P[t.name + ".gamma"], P[t.name + ".beta"])
@@ -200,7 +205,7 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             cache = None
         elif t.kind == "fc_ce":
             xf = _flat_hwc(get(t.inputs[0]))
-            z = L.fc_fwd(xf, P[t.name + ".w"], P[t.name + ".b"])
+            z = L.fc_fwd(q(xf), q(P[t.name + ".w"]), P[t.name + ".b"])
             loss, dz = L.softmax_ce(z, np.asarray(labels))
             y = z[:, :, None, None]
             cache = (xf, dz)
@@ -222,7 +227,8 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
         cache = caches[i]
         if t.kind == "fc_ce":
             xf, dz = cache
-            dxf, dw, db = L.fc_bwd(dz, xf, P[t.name + ".w"])
+            dxf, dw, db = L.fc_bwd(q(dz), q(xf), q(P[t.name + ".w"]))
+            db = dz.sum(axis=0)
             grads[t.name + ".w"] += dw
             grads[t.name + ".b"] += db
             src = get(t.inputs[0])
@@ -233,9 +239,9 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
         if t.kind == "conv":
             xin = get(t.inputs[0])
             w = P[t.name + ".w"]
-            grads[t.name + ".w"] += L.conv2d_wgrad(xin, dy, w.shape, t.stride, t.pad)
+            grads[t.name + ".w"] += L.conv2d_wgrad(q(xin), q(dy), w.shape, t.stride, t.pad)
             if t.inputs[0] >= 0:
-                acc(t.inputs[0], L.conv2d_dgrad(dy, w, xin.shape, t.stride, t.pad))
+                acc(t.inputs[0], L.conv2d_dgrad(q(dy), q(w), xin.shape, t.stride, t.pad))
         elif t.kind == "bnrelu":
             dz = L.relu_bwd(dy, outs[i])
             dx, dg, db = L.bn_bwd(dz, cache[0], P[t.name + ".gamma"])
@@ -259,6 +265,8 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             acc(t.inputs[0], L.maxpool_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad))
         elif t.kind == "avgpool":
             acc(t.inputs[0], L.avgpool_bwd(dy[:, :, 0, 0], get(t.inputs[0]).shape))
+    if map_grads is not None:
+        map_grads.extend(gmap)
     return loss, grads, outs
 
 

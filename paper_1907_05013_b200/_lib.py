@@ -100,6 +100,9 @@ SIGNATURES = {
     "pooch_set_timing": (c_i32, [c_vp, c_i32]),
     "pooch_last_timing": (c_i32, [c_vp, P(c_i64), P(c_i64), P(c_i64), P(c_i64), P(c_i64), P(c_i64)]),
     "pooch_family_stats": (c_i32, [c_vp, c_i32, P(c_f64), P(c_i64), P(c_f64), P(c_f64)]),
+    "pooch_loss_slot": (c_i32, [c_vp, P(c_vp)]),
+    "pooch_read_buffer": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_sz]),
+    "pooch_kernel_launches": (c_i32, [c_vp, P(c_i64)]),
     "pooch_op_conv_fwd": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pooch_op_conv_dgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_i32, c_vp]),
     "pooch_op_conv_wgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),

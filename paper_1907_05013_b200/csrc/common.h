@@ -10,6 +10,10 @@
 
 namespace pooch {
 
+// Kernel launches issued by the library (process-wide; read per step by the executor).
+long long& launch_counter();
+inline void count_launch() { ++launch_counter(); }
+
 // Last error of calls made without a context (and the fallback for context calls).
 std::string& tls_error();
 

@@ -32,6 +32,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
     configured = true;
   }
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return POOCH_OK;
+  count_launch();
   kern<<<grid, NUM_THREADS, SMEM, st>>>(p);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -140,6 +141,7 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
   if (split) {
     int64_t n4 = (int64_t)g.K * p.Ng / 4;
     int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+    count_launch();
     splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(ws), reinterpret_cast<float4*>(dw),
                                                   n4, w.splits);
     POOCH_CUDA(cudaGetLastError());

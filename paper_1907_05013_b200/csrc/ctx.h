@@ -110,4 +110,5 @@ struct pooch_ctx {
   void* nccl = nullptr;
   int rank = 0, world = 1;
   int64_t step_count = 0;
+  int64_t last_launches = 0;
 };

@@ -451,7 +451,9 @@ pooch_status bn_finalize(const float* ts, const float* tq, int tiles, int C, int
                          const float* beta, float* mean, float* invstd, float* scale, float* shift, double* ws,
                          cudaStream_t st) {
   dim3 g1((C + 127) / 128, kFinRows);
+  count_launch();
   bn_fin_partial_kernel<<<g1, 128, 0, st>>>(ts, tq, tiles, C, ws);
+  count_launch();
   bn_fin_final_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, C, (double)count, gamma, beta, mean, invstd, scale, shift);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -461,9 +463,9 @@ pooch_status bn_apply_relu(const float* a, const float* sa, const float* ta, con
                            const float* tb, int mode, float* y, int64_t rows, int C, cudaStream_t st) {
   int64_t n4 = rows * C / 4;
   int grid = grid_for(n4, 256);
-  if (mode == 0) bn_apply_kernel<0><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4);
-  else if (mode == 1) bn_apply_kernel<1><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4);
-  else bn_apply_kernel<2><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4);
+  if (mode == 0) { count_launch(); bn_apply_kernel<0><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4); }
+  else if (mode == 1) { count_launch(); bn_apply_kernel<1><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4); }
+  else { count_launch(); bn_apply_kernel<2><<<grid, 256, 0, st>>>(a, sa, ta, b, sb, tb, y, n4, C / 4); }
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
@@ -482,15 +484,19 @@ static pooch_status bn_bwd_mode(const BnBwdArgs& a, float* ws, cudaStream_t st) 
   float* coef = ws + (size_t)3 * kBwdMaxBlocks * C;
   if (cgpt == 1) {
     if (smem > 48 * 1024) POOCH_CUDA(cudaFuncSetAttribute(bn_bwd_reduce_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    count_launch();
     bn_bwd_reduce_kernel<MODE, 1><<<blocks, kBwdThreads, smem, st>>>(a, ws);
   } else if (cgpt == 2) {
     if (smem > 48 * 1024) POOCH_CUDA(cudaFuncSetAttribute(bn_bwd_reduce_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    count_launch();
     bn_bwd_reduce_kernel<MODE, 2><<<blocks, kBwdThreads, smem, st>>>(a, ws);
   } else {
     return fail(POOCH_EUSAGE, "BN backward supports C <= 2048 (C = %d)", C);
   }
+  count_launch();
   bn_bwd_finalize_kernel<MODE><<<(C + 127) / 128, 128, 0, st>>>(a, ws, blocks, coef);
   int64_t n4 = a.rows * C / 4;
+  count_launch();
   bn_bwd_apply_kernel<MODE><<<grid_for(n4, 256), 256, 0, st>>>(a, coef, n4);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -506,6 +512,7 @@ pooch_status bn_bwd(const BnBwdArgs& a, float* ws, cudaStream_t st) {
 pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, int k, int s, int p, int Ho, int Wo,
                          cudaStream_t st) {
   int64_t total = (int64_t)N * Ho * Wo * C / 4;
+  count_launch();
   maxpool_fwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, y, N, H, W, C / 4, k, s, p, Ho, Wo);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -514,7 +521,9 @@ pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, i
 pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* arg_ws, int N, int H, int W, int C,
                          int k, int s, int p, int Ho, int Wo, cudaStream_t st) {
   int64_t tot_o = (int64_t)N * Ho * Wo * C / 4, tot_i = (int64_t)N * H * W * C / 4;
+  count_launch();
   maxpool_arg_kernel<<<grid_for(tot_o, 256), 256, 0, st>>>(x, arg_ws, N, H, W, C / 4, k, s, p, Ho, Wo);
+  count_launch();
   maxpool_bwd_kernel<<<grid_for(tot_i, 256), 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C / 4, k, s, p, Ho, Wo);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -522,6 +531,7 @@ pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* ar
 
 pooch_status avgpool_fwd(const float* x, float* y, int N, int HW, int C, cudaStream_t st) {
   dim3 g((C / 4 + 127) / 128, N);
+  count_launch();
   avgpool_fwd_kernel<<<g, 128, 0, st>>>(x, y, HW, C / 4);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -529,6 +539,7 @@ pooch_status avgpool_fwd(const float* x, float* y, int N, int HW, int C, cudaStr
 
 pooch_status avgpool_bwd(const float* gy, float* gx, int N, int HW, int C, cudaStream_t st) {
   int64_t n4 = (int64_t)N * HW * C / 4;
+  count_launch();
   avgpool_bwd_kernel<<<grid_for(n4, 256), 256, 0, st>>>(gy, gx, n4, HW, C / 4);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -536,7 +547,9 @@ pooch_status avgpool_bwd(const float* gy, float* gx, int N, int HW, int C, cudaS
 
 pooch_status ce_fwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* loss_rows, float* loss,
                     cudaStream_t st) {
+  count_launch();
   ce_rows_kernel<<<(B + 7) / 8, 256, 0, st>>>(z, labels, B, classes, ld, loss_rows, nullptr, 0);
+  count_launch();
   mean_kernel<<<1, 256, 0, st>>>(loss_rows, B, loss);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -544,7 +557,9 @@ pooch_status ce_fwd(const float* z, const int32_t* labels, int B, int classes, i
 
 pooch_status ce_bwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* dz, float* db,
                     cudaStream_t st) {
+  count_launch();
   ce_rows_kernel<<<(B + 7) / 8, 256, 0, st>>>(z, labels, B, classes, ld, nullptr, dz, 1);
+  count_launch();
   colsum_kernel<<<(ld + 127) / 128, 128, 0, st>>>(dz, B, ld, db);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -553,14 +568,15 @@ pooch_status ce_bwd(const float* z, const int32_t* labels, int B, int classes, i
 pooch_status sgd_momentum(float* w, float* v, const float* g, int64_t n, float lr, float mu, float scale,
                           cudaStream_t st) {
   int64_t n4 = n / 4;
-  if (n4 > 0) sgd_kernel<<<grid_for(n4, 256), 256, 0, st>>>(w, v, g, n4, lr, mu, scale);
-  if (n % 4) sgd_tail_kernel<<<1, 32, 0, st>>>(w, v, g, n4 * 4, n, lr, mu, scale);
+  if (n4 > 0) { count_launch(); sgd_kernel<<<grid_for(n4, 256), 256, 0, st>>>(w, v, g, n4, lr, mu, scale); }
+  if (n % 4) { count_launch(); sgd_tail_kernel<<<1, 32, 0, st>>>(w, v, g, n4 * 4, n, lr, mu, scale); }
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
 
 pooch_status transpose_krsc(const float* w, float* wt, int K, int RS, int C, cudaStream_t st) {
   dim3 g((C + 31) / 32, (K + 31) / 32, RS);
+  count_launch();
   transpose_kernel<<<g, dim3(32, 8), 0, st>>>(w, wt, K, RS, C);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;

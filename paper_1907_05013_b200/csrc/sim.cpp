@@ -190,7 +190,7 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
       s.end_of[q] = t;
       live -= s.Fr[q];
       if (L)
-        for (int b : s.free_at[q]) led.push_back({t, b, false, 0});
+        for (int b : s.free_at[q]) led.push_back({t, b, false, 0, 0, s.prog[q].kind, s.prog[q].id});
       c_q = -1;
       if (s.prog[q].kind == 'F') {
         ++fwd_done;
@@ -204,7 +204,7 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
     if (d_m >= 0 && d_end == t) {
       live -= s.size[d_m];
       s.out_end[d_m] = t;
-      if (L) led.push_back({t, d_m, false, 0});
+      if (L) led.push_back({t, d_m, false, 0, 1, 'O', d_m});
       d_m = -1;
     }
     if (h_m >= 0 && h_end == t) {
@@ -228,7 +228,7 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
         c_end = t + dur(tk);
         if (E) ev.push_back({0, tk.kind, tk.id, t, c_end});
         if (L)
-          for (int b : s.alloc_at[pc]) led.push_back({t, b, true, 0});
+          for (int b : s.alloc_at[pc]) led.push_back({t, b, true, 0, 0, tk.kind, tk.id});
         ++pc;
       }
     }
@@ -259,7 +259,7 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
           h_m = m;
           h_end = t + p.h2d[m];
           if (E) ev.push_back({2, 'I', m, t, h_end});
-          if (L) led.push_back({t, n + m, true, 0});
+          if (L) led.push_back({t, n + m, true, 0, 2, 'I', m});
           ++hq;
         }
       }

@@ -26,6 +26,9 @@ struct LedgerEntry {
   int buf;
   bool alloc;
   uint64_t bytes;
+  int lane;   // op performing the alloc / free: lane, kind, id
+  char kind;
+  int id;
 };
 
 struct ProgTask {

@@ -1,0 +1,178 @@
+"""Python binding of the out-of-core training-step executor (pooch_ctx).
+
+Argument marshalling only: profiling (Sec. 4.2), classification (Sec. 4.4) and
+execution (fwd / bwd with swap and recompute, update) all run in libpooch.so.
+PyTorch is used by callers for device memory, pinned host memory, streams and
+process groups; this module only passes their raw pointers through the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import P, IODesc, LayerDesc, PlanReport, ProfileT, SearchCfg, check, lib
+from .planning import STRATEGIES
+
+NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2}
+KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce"]
+FAMILIES = ["conv_fwd", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd", "pool", "fc_ce", "sgd",
+            "swap_out", "swap_in", "allreduce", "other"]
+
+
+def build_net(name: str, in_hw: int, classes: int, width: int = 32):
+    """Layer descriptors of a built-in workload (pooch_build_net)."""
+    n = C.c_int32(0)
+    check(lib.pooch_build_net(NETS[name], in_hw, classes, width, None, C.byref(n)))
+    arr = (LayerDesc * n.value)()
+    check(lib.pooch_build_net(NETS[name], in_hw, classes, width, arr, C.byref(n)))
+    return arr
+
+
+def _ptr(x):
+    """Raw address of a torch tensor / int / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return C.c_void_p(x)
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr())
+    if hasattr(x, "cuda_stream"):
+        return C.c_void_p(x.cuda_stream)
+    raise TypeError(type(x))
+
+
+class Context:
+    def __init__(self, layers, batch: int, in_c: int, in_h: int, in_w: int, classes: int, device: int = 0):
+        self.layers = layers
+        self.n = len(layers)
+        self.batch, self.in_c, self.in_h, self.in_w, self.classes = batch, in_c, in_h, in_w, classes
+        io = IODesc(batch, in_c, in_h, in_w, classes)
+        h = C.c_void_p()
+        check(lib.pooch_create(layers, len(layers), C.byref(io), device, C.byref(h)))
+        self.h = h
+        self._keep = []
+
+    @classmethod
+    def builtin(cls, name, batch, in_hw=None, classes=None, width=32, device=0):
+        in_hw = in_hw or (32 if name == "tiny" else 224)
+        classes = classes or (10 if name == "tiny" else 1000)
+        return cls(build_net(name, in_hw, classes, width), batch, 4, in_hw, in_hw, classes, device)
+
+    def close(self):
+        if self.h:
+            lib.pooch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st):
+        check(st, self.h)
+
+    # ---------------------------------------------------------------- setup
+    def resident_bytes(self) -> int:
+        v = C.c_uint64()
+        self._chk(lib.pooch_resident_bytes(self.h, C.byref(v)))
+        return v.value
+
+    def set_budget(self, dev, dev_bytes, host=None, host_bytes=0):
+        self._keep = [dev, host]
+        self._chk(lib.pooch_set_budget(self.h, _ptr(dev), int(dev_bytes), _ptr(host), int(host_bytes)))
+
+    def set_streams(self, compute, d2h, h2d, comm=None):
+        self._streams = (compute, d2h, h2d, comm)
+        self._chk(lib.pooch_set_streams(self.h, _ptr(compute), _ptr(d2h), _ptr(h2d), _ptr(comm)))
+
+    def set_comm(self, unique_id: bytes, rank: int, world: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._chk(lib.pooch_set_comm(self.h, buf, rank, world))
+
+    def input_slot(self):
+        x, l = C.c_void_p(), C.c_void_p()
+        self._chk(lib.pooch_input_slot(self.h, C.byref(x), C.byref(l)))
+        return x.value, l.value
+
+    # ---------------------------------------------------------------- parameters
+    def params(self):
+        n = C.c_int32()
+        self._chk(lib.pooch_num_params(self.h, C.byref(n)))
+        out = []
+        buf = C.create_string_buffer(64)
+        for i in range(n.value):
+            k = C.c_int64()
+            self._chk(lib.pooch_param_info(self.h, i, buf, C.byref(k)))
+            out.append((buf.value.decode(), k.value))
+        return out
+
+    def set_param(self, i, arr, which=0):
+        a = np.ascontiguousarray(arr, dtype=np.float32).ravel()
+        self._chk(lib.pooch_set_param(self.h, i, which, a.ctypes.data_as(P(C.c_float)), a.size))
+
+    def get_param(self, i, which=0):
+        k = self.params()[i][1]
+        a = np.empty(k, np.float32)
+        self._chk(lib.pooch_get_param(self.h, i, which, a.ctypes.data_as(P(C.c_float)), k))
+        return a
+
+    # ---------------------------------------------------------------- profile / plan / step
+    def profile(self, iters=3):
+        pr = ProfileT()
+        self._chk(lib.pooch_profile(self.h, iters, C.byref(pr)))
+        n = pr.n
+        g = lambda p: [int(p[i]) for i in range(n)]
+        return dict(fwd=g(pr.fwd_ns), bwd=g(pr.bwd_ns), rec=g(pr.rec_ns), d2h=g(pr.d2h_ns), h2d=g(pr.h2d_ns),
+                    bytes=g(pr.bytes), tail=int(pr.tail_ns), resident=int(pr.resident_bytes),
+                    d2h_gbs=pr.d2h_gbs, h2d_gbs=pr.h2d_gbs, duplex_gbs=pr.duplex_gbs)
+
+    def set_profile(self, fwd, bwd, rec, d2h, h2d, tail):
+        arrs = [np.asarray(v, np.int64) for v in (fwd, bwd, rec, d2h, h2d)]
+        self._chk(lib.pooch_set_profile(self.h, *[a.ctypes.data_as(P(C.c_int64)) for a in arrs], int(tail)))
+
+    def plan(self, strategy="pooch", li_cap=16, threads=0, sched=0, fixed=None):
+        out = np.zeros(self.n, np.uint8)
+        rep = PlanReport()
+        fx = None if fixed is None else np.asarray(fixed, np.uint8)
+        self._chk(lib.pooch_plan(self.h, STRATEGIES[strategy], C.byref(SearchCfg(li_cap, threads, sched)),
+                                 None if fx is None else fx.ctypes.data_as(P(C.c_uint8)),
+                                 out.ctypes.data_as(P(C.c_uint8)), C.byref(rep)))
+        rd = {k: getattr(rep, k) for k, _ in PlanReport._fields_}
+        return [int(v) for v in out], rd
+
+    def train_step(self, lr: float, sync_loss: bool = True):
+        if sync_loss:
+            loss = C.c_float()
+            self._chk(lib.pooch_train_step(self.h, lr, C.byref(loss)))
+            return loss.value
+        self._chk(lib.pooch_train_step(self.h, lr, None))
+        return None
+
+    def read_buffer(self, which, m, nbytes):
+        a = np.empty(nbytes // 4, np.float32)
+        self._chk(lib.pooch_read_buffer(self.h, which, m, a.ctypes.data, nbytes))
+        return a
+
+    def loss_slot(self):
+        p = C.c_void_p()
+        self._chk(lib.pooch_loss_slot(self.h, C.byref(p)))
+        return p.value
+
+    def set_timing(self, on: bool):
+        self._chk(lib.pooch_set_timing(self.h, 1 if on else 0))
+
+    def last_timing(self):
+        arrs = [np.zeros(self.n, np.int64) for _ in range(5)]
+        step = C.c_int64()
+        self._chk(lib.pooch_last_timing(self.h, *[a.ctypes.data_as(P(C.c_int64)) for a in arrs], C.byref(step)))
+        return dict(zip(("fwd", "bwd", "rec", "d2h", "h2d"), arrs), step_ns=step.value)
+
+    def family_stats(self):
+        out = {}
+        for f, name in enumerate(FAMILIES):
+            t, l, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+            self._chk(lib.pooch_family_stats(self.h, f, C.byref(t), C.byref(l), C.byref(fl), C.byref(by)))
+            out[name] = dict(ms=t.value, launches=l.value, flops=fl.value, bytes=by.value)
+        return out

@@ -1,0 +1,62 @@
+"""Test-side glue between the oracle's parameter layout (OIHW, unpadded) and the
+C ABI's (KRSC with Cin padded to 4, FC rows padded to a multiple of 4).
+Pure re-layout (transpose / zero-pad / crop): no arithmetic of the method."""
+import numpy as np
+
+
+def to_pooch(name, arr, numel):
+    a = np.asarray(arr, np.float32)
+    if name.endswith(".w") and a.ndim == 4:          # OIHW -> KRSC, pad C
+        o, c, r, s = a.shape
+        cp = numel // (o * r * s)
+        out = np.zeros((o, r, s, cp), np.float32)
+        out[..., :c] = a.transpose(0, 2, 3, 1)
+        return out
+    if name.endswith(".w") and a.ndim == 2:          # FC [classes, cin] -> [cpad, cin]
+        k, cin = a.shape
+        out = np.zeros((numel // cin, cin), np.float32)
+        out[:k] = a
+        return out
+    if a.size != numel:                              # FC bias
+        out = np.zeros(numel, np.float32)
+        out[:a.size] = a.ravel()
+        return out
+    return a
+
+
+def from_pooch(name, flat, ref_shape):
+    """Pooch layout -> oracle layout of shape ref_shape."""
+    ref_shape = tuple(ref_shape)
+    if name.endswith(".w") and len(ref_shape) == 4:
+        o, c, r, s = ref_shape
+        cp = flat.size // (o * r * s)
+        return flat.reshape(o, r, s, cp)[..., :c].transpose(0, 3, 1, 2)
+    if name.endswith(".w") and len(ref_shape) == 2:
+        k, cin = ref_shape
+        return flat.reshape(-1, cin)[:k]
+    return flat[:int(np.prod(ref_shape))].reshape(ref_shape)
+
+
+def pad_input(x_nhwc, c=4):
+    n, h, w, c0 = x_nhwc.shape
+    out = np.zeros((n, h, w, c), np.float32)
+    out[..., :c0] = x_nhwc
+    return out
+
+
+def load_params(ctx, params):
+    for i, (name, numel) in enumerate(ctx.params()):
+        ctx.set_param(i, to_pooch(name, params[name], numel))
+
+
+def read_params(ctx, params_ref, which):
+    out = {}
+    for i, (name, numel) in enumerate(ctx.params()):
+        out[name] = from_pooch(name, ctx.get_param(i, which), np.shape(params_ref[name]))
+    return out
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))

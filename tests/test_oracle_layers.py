@@ -192,3 +192,17 @@ def test_tiny_cnn_fd_spot():
     for name in ["conv0.w", "bn2.gamma", "conv3.w", "fc.w"]:
         f = lambda: nets.forward_backward(net, params, x, t)[0]
         assert rel(grads[name], fd_grad(f, params[name])) < 1e-5, name
+
+
+def test_tf32_operand_rounding_bits():
+    """tf32() keeps sign, exponent and the top 10 mantissa bits of the fp32 value."""
+    x = np.array([1.0, 1.0 + 2.0 ** -10, 1.0 + 2.0 ** -11, -3.0000001, 2.0 ** -126, 65504.123, 0.0])
+    q = L.tf32(x)
+    u = q.astype(np.float32).view(np.uint32)
+    assert np.all(u & 0x1FFF == 0)
+    assert q[0] == 1.0 and q[1] == 1.0 + 2.0 ** -10 and q[2] == 1.0      # truncation, not rounding
+    assert np.all(np.abs(q) <= np.abs(x.astype(np.float32)))              # toward zero
+    assert np.array_equal(L.tf32(q), q)                                   # idempotent
+    r = np.random.default_rng(0).standard_normal(10000)
+    rel = np.abs(L.tf32(r) - r) / np.abs(r)
+    assert rel.max() < 2.0 ** -10 + 1e-7
