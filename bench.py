@@ -193,16 +193,8 @@ def our_arm(args):
     ctx.set_budget(dev, budget, host, host_bytes)
     ctx.set_streams(*streams)
     if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            import ctypes
-            nccl = ctypes.CDLL("libnccl.so.2")
-            buf = ctypes.create_string_buffer(128)
-            nccl.ncclGetUniqueId(buf)
-            uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
-        uid = uid.cuda()
-        dist.broadcast(uid, 0)
-        ctx.set_comm(bytes(uid.cpu().numpy().tobytes()), rank, world)
+        from paper_1907_05013_b200.dp import broadcast_unique_id
+        ctx.set_comm(broadcast_unique_id(rank, device="cuda"), rank, world)
     # parameters and the synthetic batch (seed 0 + rank / 1 + rank; identical weights)
     g = synthdata.rng(2)
     for i, (name, numel) in enumerate(ctx.params()):
@@ -229,12 +221,9 @@ def our_arm(args):
     prof = ctx.profile(args.profile_iters)
     prof_s = time.time() - t0
     if world > 1:
-        arr = torch.tensor([prof[k] for k in ("fwd", "bwd", "rec", "d2h", "h2d")], dtype=torch.int64).cuda()
-        dist.all_reduce(arr, op=dist.ReduceOp.MAX)
-        tail = torch.tensor([prof["tail"]], dtype=torch.int64).cuda()
-        dist.all_reduce(tail, op=dist.ReduceOp.MAX)
-        a = arr.cpu().numpy()
-        ctx.set_profile(a[0], a[1], a[2], a[3], a[4], int(tail.item()))
+        from paper_1907_05013_b200.dp import agree_profile
+        agreed = agree_profile(prof, device="cuda")
+        ctx.set_profile(agreed["fwd"], agreed["bwd"], agreed["rec"], agreed["d2h"], agreed["h2d"], agreed["tail"])
     cls, rep = ctx.plan("pooch", li_cap=args.li_cap)
     counts = {"keep": cls.count(0), "swap": cls.count(1), "recompute": cls.count(2)}
 
@@ -242,6 +231,9 @@ def our_arm(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    lo = ctx.loss_slot() - base
+    loss_dev = dev[lo: lo + 4].view(torch.float32)
 
     def timed(n_steps, e2e=False):
         s = streams[0]
@@ -257,7 +249,6 @@ def our_arm(args):
                     l_dev.copy_(l_host, non_blocking=True)
             ctx.train_step(0.01, sync_loss=False)
             if e2e:
-                loss_dev = dev[ctx_loss_off(ctx, base):][:4].view(torch.float32)
                 with torch.cuda.stream(s):
                     loss_h.copy_(loss_dev, non_blocking=True)
         e1.record(s)
@@ -339,18 +330,6 @@ def name_out_channels(ctx, pname):
         if l.name.decode() == task:
             return l.cout if l.kind == 0 else ((l.cout + 3) // 4 * 4)
     raise KeyError(pname)
-
-
-def ctx_loss_off(ctx, base):
-    import ctypes as C
-    from paper_1907_05013_b200._lib import lib
-    x, l = ctx.input_slot()
-    # loss scalar follows the label and loss-row slots (see executor.cpp layout_resident)
-    b = ctx.batch
-    off = l - base
-    off = (off + b * 4 + 255) // 256 * 256          # loss rows
-    off = (off + b * 4 + 255) // 256 * 256          # loss
-    return off
 
 
 def kernel_launches(ctx, steps):

@@ -127,6 +127,13 @@ pooch_status pooch_set_streams(pooch_ctx* ctx, void* compute, void* d2h, void* h
  * summed across ranks and scaled by 1/world in the update. Marks the plan stale. */
 pooch_status pooch_set_comm(pooch_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t world);
 
+/* Precision of the tensor-core contractions (conv fwd / dgrad / wgrad, FC):
+ * 1 (default) = 3xTF32 split -- each fp32 operand x is fed as x and x - tf32(x), three TF32
+ * MMAs per k-step, fp32 accumulate: ~fp32-faithful, the mode the 5e-3 gradient gate holds for;
+ * 0 = plain TF32 (one MMA, operands truncated to TF32 by the tensor core). Invalidates the
+ * profile and the plan. */
+pooch_status pooch_set_precision(pooch_ctx* ctx, int32_t precision);
+
 /* Input slot inside the device arena: x_dev [batch, in_h, in_w, in_c] fp32, labels_dev
  * [batch] int32. Valid after pooch_set_budget. */
 pooch_status pooch_input_slot(pooch_ctx* ctx, float** x_dev, int32_t** labels_dev);
@@ -286,6 +293,7 @@ pooch_status pooch_family_stats(pooch_ctx* ctx, int32_t family, double* time_ms,
  *   wgrad: dw[K,R,S,C] = sum_pixels dy x im2col(x); `ws` device workspace of ws_bytes. */
 typedef struct {
   int32_t N, H, W, C, K, R, S, stride, pad;
+  int32_t precision;  /* 0: TF32 operands (1 MMA per k-step); 1: 3xTF32 split, ~fp32-faithful */
 } pooch_conv_desc;
 
 pooch_status pooch_op_conv_fwd(const pooch_conv_desc* d, const float* x, const float* w, float* y,
@@ -295,8 +303,9 @@ pooch_status pooch_op_conv_dgrad(const pooch_conv_desc* d, const float* dy, cons
 pooch_status pooch_op_conv_wgrad(const pooch_conv_desc* d, const float* x, const float* dy, float* dw,
                                  float* ws, size_t ws_bytes, void* stream);
 size_t pooch_op_conv_wgrad_ws_bytes(const pooch_conv_desc* d);
-/* D[split][M][N] = A * B^T on the tensor-core core; a_mn/b_mn select MN-major operands
- * (A stored [K][M], B stored [K][N]); bn in {64,128,256}; splits >= 1. Unit test only. */
+/* D[split][M][N] = A * B^T on the tensor-core core, A [M][K] and B [N][K] row-major (K-major);
+ * a_mn = 2 selects the 3xTF32 path, other non-zero a_mn / b_mn (MN-major operands) return
+ * POOCH_EUSAGE; bn in {64,128,256} (64/128 for 3xTF32); splits >= 1. Unit test only. */
 pooch_status pooch_op_gemm_test(const float* A, const float* B, float* D, int32_t M, int32_t N, int32_t K,
                                 int32_t a_mn, int32_t b_mn, int32_t bn, int32_t splits, void* stream);
 

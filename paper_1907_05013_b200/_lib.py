@@ -33,7 +33,7 @@ P = C.POINTER
 
 
 class ConvDesc(C.Structure):
-    _fields_ = [(n, c_i32) for n in ("N", "H", "W", "C", "K", "R", "S", "stride", "pad")]
+    _fields_ = [(n, c_i32) for n in ("N", "H", "W", "C", "K", "R", "S", "stride", "pad", "precision")]
 
 
 class LayerDesc(C.Structure):
@@ -101,6 +101,7 @@ SIGNATURES = {
     "pooch_last_timing": (c_i32, [c_vp, P(c_i64), P(c_i64), P(c_i64), P(c_i64), P(c_i64), P(c_i64)]),
     "pooch_family_stats": (c_i32, [c_vp, c_i32, P(c_f64), P(c_i64), P(c_f64), P(c_f64)]),
     "pooch_loss_slot": (c_i32, [c_vp, P(c_vp)]),
+    "pooch_set_precision": (c_i32, [c_vp, c_i32]),
     "pooch_read_buffer": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_sz]),
     "pooch_kernel_launches": (c_i32, [c_vp, P(c_i64)]),
     "pooch_op_conv_fwd": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

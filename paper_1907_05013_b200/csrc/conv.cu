@@ -10,7 +10,7 @@
 namespace pooch {
 
 ConvGeom conv_geom(const pooch_conv_desc& d) {
-  ConvGeom g{d.N, d.H, d.W, d.C, d.K, d.R, d.S, d.stride, d.pad, 0, 0};
+  ConvGeom g{d.N, d.H, d.W, d.C, d.K, d.R, d.S, d.stride, d.pad, 0, 0, d.precision};
   g.Ho = (d.H + 2 * d.pad - d.R) / d.stride + 1;
   g.Wo = (d.W + 2 * d.pad - d.S) / d.stride + 1;
   return g;
@@ -21,11 +21,11 @@ bool conv_shape_ok(const ConvGeom& g) {
          g.pad >= 0 && g.C % 4 == 0 && g.K % 4 == 0 && g.Ho > 0 && g.Wo > 0;
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool X3 = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st) {
-  constexpr int STAGES = 4;
-  constexpr int SMEM = GemmSmem<BN, STAGES>::TOTAL;
-  auto kern = igemm_kernel<MODE, BN, STAGES>;
+  constexpr int STAGES = X3 ? 3 : 4;
+  constexpr int SMEM = GemmSmem<BN, STAGES, X3>::TOTAL;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -39,7 +39,14 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
 }
 
 template <int MODE>
-static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st) {
+static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st, int prec = 0) {
+  if (prec) {
+    switch (bn) {
+      case 64: return launch_igemm<MODE, 64, true>(p, grid, st);
+      case 128: return launch_igemm<MODE, 128, true>(p, grid, st);
+    }
+    return fail(POOCH_EUSAGE, "3xTF32 supports tile widths 64 / 128 (got %d)", bn);
+  }
   switch (bn) {
     case 64: return launch_igemm<MODE, 64>(p, grid, st);
     case 128: return launch_igemm<MODE, 128>(p, grid, st);
@@ -48,7 +55,9 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
   return fail(POOCH_EUSAGE, "bad tile width %d", bn);
 }
 
-static int pick_bn(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
+static int pick_bn(int n, int prec = 0) {
+  return n <= 64 ? 64 : ((n <= 128 || prec) ? 128 : 256);
+}
 
 static GemmParams base_params(const ConvGeom& g) {
   GemmParams p{};
@@ -66,9 +75,9 @@ pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, 
   p.Kg = g.R * g.S * g.C;
   p.a = x; p.b = w; p.d = y;
   p.stat_sum = stat_sum; p.stat_sq = stat_sq; p.bias = bias;
-  int bn = pick_bn(g.K);
+  int bn = pick_bn(g.K, g.prec);
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
-  return launch_bn<CONV_FWD>(bn, p, grid, st);
+  return launch_bn<CONV_FWD>(bn, p, grid, st, g.prec);
 }
 
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
@@ -79,9 +88,9 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
   p.Kg = g.R * g.S * g.K;
   p.a = dy; p.b = wt; p.d = dx;
   p.accumulate = accumulate ? 1 : 0;
-  int bn = pick_bn(g.C);
+  int bn = pick_bn(g.C, g.prec);
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
-  return launch_bn<CONV_DGRAD>(bn, p, grid, st);
+  return launch_bn<CONV_DGRAD>(bn, p, grid, st, g.prec);
 }
 
 // ---- wgrad: split-K over pixels into a workspace, then a fixed-order reduction.
@@ -137,7 +146,8 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
     return fail(POOCH_EUSAGE, "wgrad workspace too small: %zu < %zu", ws_bytes, conv_wgrad_ws_bytes(g));
   p.d = split ? ws : dw;
   dim3 grid(w.mt, w.nt, w.splits);
-  POOCH_CHECK((launch_igemm<CONV_WGRAD, 128>(p, grid, st)));
+  if (g.prec) POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true>(p, grid, st)));
+  else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128>(p, grid, st)));
   if (split) {
     int64_t n4 = (int64_t)g.K * p.Ng / 4;
     int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
@@ -188,6 +198,12 @@ extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float
                                            void* stream) {
   if (!A || !B || !D || M <= 0 || N <= 0 || K <= 0 || splits < 1) return fail(POOCH_EUSAGE, "bad gemm args");
   if (M % 4 || N % 4 || K % 4) return fail(POOCH_EUSAGE, "M, N, K must be multiples of 4");
+  // a_mn / b_mn are reserved (MN-major operands are not supported); a_mn == 2 selects 3xTF32
+  int test_prec = 0;
+  if (a_mn == 2) {
+    test_prec = 1;
+    a_mn = 0;
+  }
   if (a_mn || b_mn) return fail(POOCH_EUSAGE, "MN-major operands are not supported (K-major only)");
   GemmParams p{};
   p.M = M; p.Ng = N; p.Kg = K;
@@ -198,5 +214,5 @@ extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float
   int kb = (K + BK - 1) / BK;
   p.kb_per_split = (kb + splits - 1) / splits;
   dim3 grid((M + BM - 1) / BM, (N + bn - 1) / bn, splits);
-  return launch_bn<GEMM_TEST>(bn, p, grid, (cudaStream_t)stream);
+  return launch_bn<GEMM_TEST>(bn, p, grid, (cudaStream_t)stream, b_mn == 0 && a_mn == 0 ? test_prec : 0);
 }

@@ -8,6 +8,7 @@ namespace pooch {
 
 struct ConvGeom {
   int N, H, W, C, K, R, S, stride, pad, Ho, Wo;
+  int prec = 0;  // 0: TF32 (one MMA per k-step), 1: 3xTF32 split (fp32-faithful)
 };
 ConvGeom conv_geom(const pooch_conv_desc& d);
 bool conv_shape_ok(const ConvGeom& g);

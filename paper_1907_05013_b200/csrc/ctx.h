@@ -111,4 +111,5 @@ struct pooch_ctx {
   int rank = 0, world = 1;
   int64_t step_count = 0;
   int64_t last_launches = 0;
+  int precision = 1;  // contractions: 0 TF32, 1 3xTF32 (default; DESIGN.md Reading 27)
 };

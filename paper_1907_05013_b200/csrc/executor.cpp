@@ -100,9 +100,16 @@ struct Ptrs {
 };
 
 // Forward (or recompute: with_stats=false) of task t.
+ConvGeom geom_of(pooch_ctx* c, int t) {
+  ConvGeom g = c->rt[t].geom;
+  g.prec = c->precision;
+  return g;
+}
+
 pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
   const Task& T = c->g.t[t];
   TaskRt& R = c->rt[t];
+  const ConvGeom RG = geom_of(c, t);
   cudaStream_t st = c->s[0];
   const int B = c->g.io.batch;
   switch (T.kind) {
@@ -113,7 +120,7 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
         ts = reinterpret_cast<float*>(c->dev + c->off_tile);
         tq = ts + (size_t)conv_mtiles(R.geom) * R.geom.K;
       }
-      POOCH_CHECK(launch_conv_fwd(R.geom, p.in0, pw(c, R.w), p.out, ts, tq, nullptr, st));
+      POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, ts, tq, nullptr, st));
       if (ts) {
         float* sp = fptr(c, c->off_stats) + R.stat_off;
         int C = R.geom.K;
@@ -137,7 +144,7 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
     case POOCH_L_AVGPOOL:
       return avgpool_fwd(p.in0, p.out, B, T.hin * T.win, T.cin, st);
     case POOCH_L_FC_CE: {
-      POOCH_CHECK(launch_conv_fwd(R.geom, p.in0, pw(c, R.w), p.out, nullptr, nullptr, pw(c, R.b), st));
+      POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, nullptr, nullptr, pw(c, R.b), st));
       if (!with_stats) return POOCH_OK;
       return ce_fwd(p.out, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), B, T.cout, R.cpad,
                     fptr(c, c->off_lossrows), fptr(c, c->off_loss), st);
@@ -162,11 +169,12 @@ typedef void (*MarkFn)(pooch_ctx*, int fam, int task, double flops, double bytes
 pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
   const Task& T = c->g.t[t];
   TaskRt& R = c->rt[t];
+  const ConvGeom RG = geom_of(c, t);
   cudaStream_t st = c->s[0];
   const int B = c->g.io.batch;
   switch (T.kind) {
     case POOCH_L_CONV: {
-      const ConvGeom& G = R.geom;
+      const ConvGeom& G = RG;
       double xb = 4.0 * G.N * G.H * G.W * G.C, yb = 4.0 * R.rows * G.K, wb = 4.0 * G.K * G.R * G.S * G.C;
       if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
       POOCH_CHECK(launch_conv_wgrad(G, p.in0 ? p.in0 : reinterpret_cast<const float*>(c->dev + c->off_x), p.gy,
@@ -214,7 +222,7 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
       float* dz = fptr(c, c->off_dz);
       POOCH_CHECK(ce_bwd(p.self, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), B, T.cout, R.cpad, dz,
                          pg(c, R.b), st));
-      const ConvGeom& G = R.geom;
+      const ConvGeom& G = RG;
       double xb = 4.0 * G.N * G.C, yb = 4.0 * G.N * G.K, wb = 4.0 * G.K * G.C;
       if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
       POOCH_CHECK(launch_conv_wgrad(G, p.in0, dz, pg(c, R.w), reinterpret_cast<float*>(c->dev + c->off_wgws),
@@ -1239,5 +1247,13 @@ extern "C" pooch_status pooch_loss_slot(pooch_ctx* c, float** loss_dev) {
 extern "C" pooch_status pooch_kernel_launches(pooch_ctx* c, int64_t* per_step) {
   if (!c || !per_step) return fail(POOCH_EUSAGE, "null argument");
   *per_step = c->last_launches;
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_set_precision(pooch_ctx* c, int32_t precision) {
+  if (!c || precision < 0 || precision > 1) return fail(POOCH_EUSAGE, "precision must be 0 (TF32) or 1 (3xTF32)");
+  c->precision = precision;
+  c->have_profile = false;
+  c->have_plan = false;
   return POOCH_OK;
 }

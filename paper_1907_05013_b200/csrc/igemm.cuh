@@ -60,11 +60,13 @@ constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per k-block (128 B per row)
 constexpr int NUM_THREADS = 160;
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool X3 = false>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // 3xTF32: the stage also holds the residuals As = A - tf32(A), Bs = B - tf32(B)
+  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
+  static constexpr int SMALL_OFF = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 4 * BN * 4 * 2 + 1024;
 };
@@ -75,6 +77,20 @@ template <int ROWS>
 __device__ __forceinline__ uint32_t kmaj_off(int row, int j) {
   return (uint32_t)((j * (ROWS / 8) + (row >> 3)) * 128 + (row & 7) * 16);
 }
+// 3xTF32 split: the tensor core truncates fp32 operands to TF32 (measured, DESIGN.md
+// Reading 27), so A*B ~= A*B + A*Bs + As*B with As = A - trunc_tf32(A) recovers ~fp32
+// accuracy from three TF32 MMAs.
+__device__ __forceinline__ float tf32_resid(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void split_chunk(uint32_t src, uint32_t dst) {
+  float a, b, c, d;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(src));
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "f"(tf32_resid(a)), "f"(tf32_resid(b)),
+               "f"(tf32_resid(c)), "f"(tf32_resid(d))
+               : "memory");
+}
+
 // ------------------------------------------------------------------------------ loaders
 // Each producer thread (tid 0..127; warp w = tid/32, lane l) owns a fixed set of tile rows
 // (K-major: ROWS/32 rows, 2 chunk columns) or MN groups (MN-major) for the whole k loop.
@@ -124,6 +140,20 @@ struct KLoader {
       } else {  // B operand of FWD / DGRAD: plain rows of the (transposed) weight
         valid[i] = gr < p.Ng;
         rowp[i] = p.b + (size_t)(valid[i] ? gr : 0) * p.Kg;
+      }
+    }
+  }
+
+  // residuals of the chunks this thread loaded into the tile at sbase -> tile at sbase + delta
+  __device__ void split(uint32_t sbase, uint32_t delta) const {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int j = (lane >> 3) + 4 * h;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        int row = warp * (ROWS / 4) + i * 8 + (lane & 7);
+        uint32_t a = sbase + kmaj_off<ROWS>(row, j);
+        split_chunk(a, a + delta);
       }
     }
   }
@@ -236,8 +266,8 @@ struct TLoader {
     }
   }
 
-  template <int ROWS>
-  __device__ void store(uint32_t sbase) const {
+  template <int ROWS, bool X3 = false>
+  __device__ void store(uint32_t sbase, uint32_t delta = 0) const {
     const int rot = (lane >> 1) & 3;
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
@@ -251,6 +281,10 @@ struct TLoader {
         uint32_t addr = sbase + kmaj_off<ROWS>(row, h);
         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x0), "f"(x1), "f"(x2), "f"(x3)
                      : "memory");
+        if (X3)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr + delta), "f"(tf32_resid(x0)),
+                       "f"(tf32_resid(x1)), "f"(tf32_resid(x2)), "f"(tf32_resid(x3))
+                       : "memory");
       }
     }
   }
@@ -272,9 +306,9 @@ __device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
   return v[0];
 }
 
-template <int MODE, int BN, int STAGES>
+template <int MODE, int BN, int STAGES, bool X3 = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams p) {
-  using SM = GemmSmem<BN, STAGES>;
+  using SM = GemmSmem<BN, STAGES, X3>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
@@ -334,8 +368,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams 
         int s = it % STAGES;
         if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
-        la.template store<BM>(st);
-        lb.template store<BN>(st + SM::A_BYTES);
+        la.template store<BM, X3>(st, SM::SMALL_OFF);
+        lb.template store<BN, X3>(st + SM::A_BYTES, SM::SMALL_OFF);
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&full[s]);
 #pragma unroll
@@ -362,6 +396,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams 
         ptx::cp_async_commit();
         if (it >= LAG) {
           ptx::cp_async_wait<LAG>();
+          if constexpr (X3) {
+            uint32_t st = sbase + ((it - LAG) % STAGES) * SM::STAGE_BYTES;
+            la.split(st, SM::SMALL_OFF);
+            lb.split(st + SM::A_BYTES, SM::SMALL_OFF);
+          }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&full[(it - LAG) % STAGES]);
         }
@@ -461,7 +500,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams 
         for (int kk = 0; kk < BK / 8; ++kk) {
           uint64_t ad = ptx::smem_desc(sa + kk * 2 * A_LBO, A_LBO, 128);
           uint64_t bd = ptx::smem_desc(sb + kk * 2 * B_LBO, B_LBO, 128);
-          ptx::mma_tf32(tmem, ad, bd, IDESC, (it | kk) != 0 ? 1u : 0u);
+          if constexpr (X3) {  // small terms first, then the big product
+            uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + kk * 2 * A_LBO, A_LBO, 128);
+            uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + kk * 2 * B_LBO, B_LBO, 128);
+            ptx::mma_tf32(tmem, asd, bd, IDESC, (it | kk) != 0 ? 1u : 0u);
+            ptx::mma_tf32(tmem, ad, bsd, IDESC, 1u);
+            ptx::mma_tf32(tmem, ad, bd, IDESC, 1u);
+          } else {
+            ptx::mma_tf32(tmem, ad, bd, IDESC, (it | kk) != 0 ? 1u : 0u);
+          }
         }
         ptx::mma_commit(&empty[s]);
       }

@@ -87,6 +87,10 @@ class Context:
         self._streams = (compute, d2h, h2d, comm)
         self._chk(lib.pooch_set_streams(self.h, _ptr(compute), _ptr(d2h), _ptr(h2d), _ptr(comm)))
 
+    def set_precision(self, precision: int):
+        """0 = TF32, 1 = 3xTF32 (default)."""
+        self._chk(lib.pooch_set_precision(self.h, int(precision)))
+
     def set_comm(self, unique_id: bytes, rank: int, world: int):
         buf = C.create_string_buffer(bytes(unique_id), 128)
         self._chk(lib.pooch_set_comm(self.h, buf, rank, world))

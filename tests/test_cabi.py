@@ -1,0 +1,70 @@
+"""The C-ABI library loads on a CPU-only box and exports every symbol that
+include/pooch.h declares; host-only entry points validate their arguments."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "pooch.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pooch_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    from paper_1907_05013_b200 import _lib
+    names = declared()
+    assert len(names) >= 25
+    missing = [n for n in names if not hasattr(_lib.lib, n)]
+    assert not missing, missing
+    unbound = [n for n in names if n not in _lib.SIGNATURES]
+    assert not unbound, unbound
+
+
+def test_build_net_census_matches_oracle():
+    from oracle import nets
+    from paper_1907_05013_b200.executor import build_net, KINDS
+    for which, ref in (("resnet50", nets.resnet50()), ("tiny", nets.tiny_cnn())):
+        layers = build_net(which, 224 if which == "resnet50" else 32, 1000 if which == "resnet50" else 10)
+        assert len(layers) == len(ref.tasks)
+        for l, t in zip(layers, ref.tasks):
+            assert l.name.decode() == t.name
+            assert KINDS[l.kind] == t.kind
+            assert [i for i in (l.in0, l.in1) if i >= 0] == [i for i in t.inputs if i >= 0]
+            assert (l.cout, l.hout, l.wout) == t.out_chw
+            if t.kind == "conv":
+                assert (l.k, l.stride, l.pad) == (t.k, t.stride, t.pad)
+
+
+def test_create_validates_graph_without_gpu():
+    from paper_1907_05013_b200 import _lib
+    from paper_1907_05013_b200.executor import Context, build_net
+    layers = build_net("tiny", 32, 10)
+    layers[3].in0 = 5                               # not topological
+    with pytest.raises(_lib.PoochError) as e:
+        Context(layers, 8, 4, 32, 32, 10)
+    assert e.value.status == 1
+    ctx = Context(build_net("tiny", 32, 10), 8, 4, 32, 32, 10)     # host-only: no device work
+    names = [n for n, _ in ctx.params()]
+    assert names[0] == "conv0.w" and names[-1] == "fc.b"
+    assert dict(ctx.params())["fc.w"] == 12 * 8192                 # classes padded 10 -> 12
+    assert ctx.resident_bytes() > 0
+    ctx.close()
+
+
+def test_plan_problem_errors():
+    from paper_1907_05013_b200.planning import PlanProblem
+    p = PlanProblem([1] * 13, [1] * 13, [4] * 13, [1] * 13, [1] * 13, [[]] + [[i] for i in range(12)],
+                    [[i] for i in range(13)])
+    from paper_1907_05013_b200 import _lib
+    with pytest.raises(_lib.PoochError):
+        p.plan("exhaustive")                        # n > 12 is a usage error
+    with pytest.raises(_lib.PoochError):
+        p.plan("superneurons")                      # not built this round
+    p2 = PlanProblem([1, 1], [1, 1], [4, 4], [1, 1], [1, 1], [[], [0]], [[0], [0, 1]], resident=10, budget=12)
+    cls, rep = p2.plan("pooch")
+    assert cls is None and rep.feasible == 0        # nothing fits: EINFEASIBLE

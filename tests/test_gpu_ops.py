@@ -16,6 +16,7 @@ import synthdata  # noqa: E402
 from oracle import layers as L  # noqa: E402
 
 TOL_OP = 3e-3
+TOL_X3 = 2e-5     # 3xTF32 split: ~fp32 accumulation error
 
 
 def _lib():
@@ -34,20 +35,21 @@ def ptr(t):
 @pytest.mark.parametrize("M,N,K,amn,bmn,bn,splits", [
     (128, 64, 32, 0, 0, 64, 1), (256, 128, 96, 0, 0, 128, 1), (300, 200, 100, 0, 0, 256, 1),
     (260, 136, 72, 0, 0, 128, 1), (384, 256, 520, 0, 0, 256, 3), (132, 1000, 2048, 0, 0, 256, 1),
-    (256, 64, 64, 0, 0, 64, 2), (4096, 512, 1024, 0, 0, 256, 1)])
+    (256, 64, 64, 0, 0, 64, 2), (4096, 512, 1024, 0, 0, 256, 1),
+    (300, 200, 100, 2, 0, 128, 1), (4096, 512, 1024, 2, 0, 128, 1)])
 def test_gemm_core(M, N, K, amn, bmn, bn, splits):
     lib = _lib()
     g = synthdata.rng(M * 7 + N + K)
     A = g.standard_normal((M, K)).astype(np.float32)
     B = g.standard_normal((N, K)).astype(np.float32)
-    dA = torch.from_numpy(np.ascontiguousarray(A.T if amn else A)).cuda()
-    dB = torch.from_numpy(np.ascontiguousarray(B.T if bmn else B)).cuda()
+    dA = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    dB = torch.from_numpy(np.ascontiguousarray(B)).cuda()
     dD = torch.zeros((splits, M, N), dtype=torch.float32, device="cuda")
     lib.check(lib.lib.pooch_op_gemm_test(ptr(dA), ptr(dB), ptr(dD), M, N, K, amn, bmn, bn, splits, None))
     torch.cuda.synchronize()
     D = dD.cpu().numpy().astype(np.float64).sum(0)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
-    assert rel(D, ref) < TOL_OP
+    assert rel(D, ref) < (TOL_X3 if amn == 2 else TOL_OP)
 
 
 CONV_CASES = [
@@ -70,12 +72,13 @@ def _conv_inputs(N, H, W, Cin, K, R, seed):
     return x, w
 
 
+@pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_fwd_and_stats(case):
+def test_conv_fwd_and_stats(case, prec):
     lib = _lib()
     N, H, W, Cin, K, R, s, p = case
     x, w = _conv_inputs(N, H, W, Cin, K, R, sum(case))
-    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p)
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p, prec)
     ho, wo = L.conv_out_hw(H, W, R, R, s, p)
     M = N * ho * wo
     mt = (M + 127) // 128
@@ -88,16 +91,17 @@ def test_conv_fwd_and_stats(case):
     ref = L.conv2d_fwd(x.transpose(0, 3, 1, 2).astype(np.float64), w.transpose(0, 3, 1, 2).astype(np.float64), s, p)
     ref = ref.transpose(0, 2, 3, 1)
     y = dy.cpu().numpy()
-    assert rel(y, ref) < TOL_OP
+    assert rel(y, ref) < (TOL_X3 if prec else TOL_OP)
     # per-tile partial sums add up to the column sums of y (checked against the oracle output)
     flat = ref.reshape(-1, K)
     assert rel(s1.cpu().numpy().astype(np.float64).sum(0), flat.sum(0)) < TOL_OP
     assert rel(s2.cpu().numpy().astype(np.float64).sum(0), (flat ** 2).sum(0)) < TOL_OP
 
 
+@pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("case", CONV_CASES[1:])
 @pytest.mark.parametrize("accumulate", [0, 1])
-def test_conv_dgrad(case, accumulate):
+def test_conv_dgrad(case, accumulate, prec):
     lib = _lib()
     N, H, W, Cin, K, R, s, p = case
     x, w = _conv_inputs(N, H, W, Cin, K, R, sum(case) + 1)
@@ -105,7 +109,7 @@ def test_conv_dgrad(case, accumulate):
     gy = synthdata.rng(5).standard_normal((N, ho, wo, K)).astype(np.float32)
     prev = synthdata.rng(6).standard_normal((N, H, W, Cin)).astype(np.float32)
     wt = np.ascontiguousarray(w.transpose(3, 1, 2, 0))   # [C][R][S][K]
-    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p)
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p, prec)
     dgy, dwt = torch.from_numpy(gy).cuda(), torch.from_numpy(wt).cuda()
     ddx = torch.from_numpy(prev.copy()).cuda() if accumulate else torch.full((N, H, W, Cin), float("nan"), device="cuda")
     lib.check(lib.lib.pooch_op_conv_dgrad(C.byref(d), ptr(dgy), ptr(dwt), ptr(ddx), accumulate, None))
@@ -114,17 +118,18 @@ def test_conv_dgrad(case, accumulate):
                          (N, Cin, H, W), s, p).transpose(0, 2, 3, 1)
     if accumulate:
         ref = ref + prev
-    assert rel(ddx.cpu().numpy(), ref) < TOL_OP
+    assert rel(ddx.cpu().numpy(), ref) < (TOL_X3 if prec else TOL_OP)
 
 
+@pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_wgrad(case):
+def test_conv_wgrad(case, prec):
     lib = _lib()
     N, H, W, Cin, K, R, s, p = case
     x, w = _conv_inputs(N, H, W, Cin, K, R, sum(case) + 2)
     ho, wo = L.conv_out_hw(H, W, R, R, s, p)
     gy = synthdata.rng(7).standard_normal((N, ho, wo, K)).astype(np.float32)
-    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p)
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p, prec)
     wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
     ws = torch.empty(max(wsb // 4, 1), device="cuda")
     dx, dgy = torch.from_numpy(x).cuda(), torch.from_numpy(gy).cuda()
@@ -133,7 +138,7 @@ def test_conv_wgrad(case):
     torch.cuda.synchronize()
     ref = L.conv2d_wgrad(x.transpose(0, 3, 1, 2).astype(np.float64), gy.transpose(0, 3, 1, 2).astype(np.float64),
                          (K, Cin, R, R), s, p).transpose(0, 2, 3, 1)
-    assert rel(ddw.cpu().numpy(), ref) < TOL_OP
+    assert rel(ddw.cpu().numpy(), ref) < (TOL_X3 if prec else TOL_OP)
 
 
 def test_conv_large_wgrad_splitk():

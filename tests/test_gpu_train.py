@@ -1,12 +1,11 @@
 """End-to-end GPU parity of the out-of-core training step (C ABI, cuda:0).
 
-* gradients and loss of one step match the oracle within rel-L2 5e-3
-  (BASELINE.json north_star) -- tiny CNN (config 1) and ResNet-50 at a small batch.
-  The oracle takes its ReLU-mask and max-pool argmax decisions in the kernels'
-  precision (contraction operands rounded to TF32, everything else fp64;
-  DESIGN.md Reading 27): with exact-fp64 operands, ~0.1% of the max-pool
-  windows pick a different maximum and those gradients move by O(1), which no
-  tolerance on the kernels can absorb;
+* gradients and loss of one step match the fp64 oracle within rel-L2 5e-3
+  (BASELINE.json north_star) -- tiny CNN (config 1) and ResNet-50 at 224^2 --
+  with the default 3xTF32 contractions (DESIGN.md Reading 27: with single
+  TF32 operands the forward drifts ~1e-3 from fp64 and flips enough ReLU /
+  max-pool decisions to move the gradients by O(1%); that mode is covered by
+  the kernel-level tests and the bit-exactness test below);
 * every keep / swap / recompute plan is bit-exact against the in-core run of
   the same kernels (north_star), including PoocH's plan at 50% of the in-core
   peak (config 1's budget) -- which also exercises the arena bound.
@@ -72,7 +71,7 @@ def tiny():
     params = nets.init_params(net, seed=2, bn_random=True)
     x = synthdata.images(8, 32, 32, 3, seed=0)
     t = synthdata.labels(8, 10, seed=1)
-    loss, grads, _ = nets.forward_backward(net, params, x, t, precision="tf32")
+    loss, grads, _ = nets.forward_backward(net, params, x, t)
     ctx = _ctx_for("tiny", 8, 32, 10, 256 << 20, 64 << 20)
     ctx.profile(2)
     return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, ctx=ctx)
@@ -137,12 +136,13 @@ def test_tiny_cnn_pooch_at_half_budget(tiny):
 
 @pytest.fixture(scope="module")
 def r50():
-    net = nets.resnet50(in_hw=64, classes=100)
+    # 224^2 (the paper's input size) at batch 8: every BN sees >= 392 samples per channel
+    net = nets.resnet50(in_hw=224, classes=1000)
     params = nets.init_params(net, seed=2, bn_random=True)
-    x = synthdata.images(4, 64, 64, 3, seed=0)
-    t = synthdata.labels(4, 100, seed=1)
-    loss, grads, _ = nets.forward_backward(net, params, x, t, precision="tf32")
-    ctx = _ctx_for("resnet50", 4, 64, 100, 2 << 30, 1 << 30)
+    x = synthdata.images(8, 224, 224, 3, seed=0)
+    t = synthdata.labels(8, 1000, seed=1)
+    loss, grads, _ = nets.forward_backward(net, params, x, t)
+    ctx = _ctx_for("resnet50", 8, 224, 1000, 4 << 30, 2 << 30)
     ctx.profile(1)
     return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, ctx=ctx)
 

@@ -1,0 +1,55 @@
+import sys, os, numpy as np, torch
+os.environ["POOCH_DEBUG_NO_REUSE"] = "1"
+sys.path.insert(0,'.'); sys.path.insert(0,'tests')
+import synthdata
+from oracle import nets
+from netutil import load_params, pad_input, read_params, rel
+from test_gpu_train import _ctx_for, _put_batch
+which = sys.argv[1] if len(sys.argv) > 1 else "r50"
+if which == "r50":
+    net = nets.resnet50(in_hw=64, classes=100); B = 4; hw = 64; ncls = 100
+    ctx = _ctx_for("resnet50", B, hw, ncls, 2 << 30, 1 << 30)
+else:
+    net = nets.tiny_cnn(); B = 8; hw = 32; ncls = 10
+    ctx = _ctx_for("tiny", B, hw, ncls, 256 << 20, 64 << 20)
+params = nets.init_params(net, seed=2, bn_random=True)
+x = synthdata.images(B, hw, hw, 3, seed=0); t = synthdata.labels(B, ncls, seed=1)
+gm = []
+loss, grads, outs = nets.forward_backward(net, params, x, t, map_grads=gm, precision=os.environ.get("ORACLE_PREC", "fp64"))
+ctx.profile(1)
+load_params(ctx, params); _put_batch(ctx, x, t)
+ctx.plan("incore")
+l = ctx.train_step(0.0)
+print("loss", l, loss)
+for i in reversed(range(len(net.tasks))):
+    tk = net.tasks[i]
+    c, h, w = tk.out_chw
+    cp = c if tk.kind != 'fc_ce' else (c + 3) // 4 * 4
+    s = "%3d %-22s %-9s" % (i, tk.name, tk.kind)
+    for which_, ref in ((0, outs[i]), (2, gm[i])):
+        if ref is None: s += " grad ---"; continue
+        ref = ref.transpose(0, 2, 3, 1).reshape(B, -1) if ref.ndim == 4 else ref.reshape(B, -1)
+        got = ctx.read_buffer(which_, i, B * cp * h * w * 4).reshape(B, h, w, cp)[..., :c].reshape(B, -1)
+        s += (" map %.2e" if which_ == 0 else " grad %.2e") % rel(got, ref)
+    print(s, flush=True)
+g = read_params(ctx, params, 1)
+errs = sorted(((rel(g[k], grads[k]), k) for k in g), reverse=True)
+for e, k in errs[:12]: print("%.3e %s" % (e, k))
+if which != "r50":
+    # max-pool decision agreement on the pool input (task 7), GPU fp32 values vs oracle fp64
+    y_gpu = ctx.read_buffer(0, 7, B * 32 * 32 * 32 * 4).reshape(B, 32, 32, 32)
+    y_ora = outs[7].transpose(0, 2, 3, 1)
+    def arg(y):
+        w = y.reshape(B, 16, 2, 16, 2, 32).transpose(0, 1, 3, 5, 2, 4).reshape(B, 16, 16, 32, 4)
+        return np.argmax(w, axis=-1), np.sort(w, axis=-1)
+    ag, sg = arg(y_gpu); ao, so = arg(y_ora)
+    d = ag != ao
+    print("maxpool argmax disagreements", int(d.sum()), "of", d.size)
+    print("gap top2 (oracle) at disagreements", (so[..., -1] - so[..., -2])[d][:10])
+    print("values gpu", sg[d][:3], "ora", so[d][:3])
+    gy = ctx.read_buffer(2, 7, B * 32 * 32 * 32 * 4).reshape(B, 32, 32, 32)
+    go = gm[7].transpose(0, 2, 3, 1)
+    diff = np.abs(gy - go)
+    idx = np.argsort(diff.ravel())[-5:]
+    print("largest grad diffs", diff.ravel()[idx], "gpu", gy.ravel()[idx], "ora", go.ravel()[idx])
+    print("y at those", y_gpu.ravel()[idx], y_ora.ravel()[idx])
