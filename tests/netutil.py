@@ -60,3 +60,10 @@ def rel(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def global_rel(g, ref):
+    """rel-L2 of the whole gradient (every parameter tensor concatenated)."""
+    num = sum(float(np.sum((np.asarray(g[k], np.float64) - np.asarray(ref[k], np.float64)) ** 2)) for k in ref)
+    den = sum(float(np.sum(np.asarray(ref[k], np.float64) ** 2)) for k in ref)
+    return (num / max(den, 1e-300)) ** 0.5

@@ -7,8 +7,9 @@ from netutil import load_params, pad_input, read_params, rel
 from test_gpu_train import _ctx_for, _put_batch
 which = sys.argv[1] if len(sys.argv) > 1 else "r50"
 if which == "r50":
-    net = nets.resnet50(in_hw=64, classes=100); B = 4; hw = 64; ncls = 100
-    ctx = _ctx_for("resnet50", B, hw, ncls, 2 << 30, 1 << 30)
+    hw = int(os.environ.get("HW", "64")); B = int(os.environ.get("B", "4")); ncls = int(os.environ.get("NCLS", "100"))
+    net = nets.resnet50(in_hw=hw, classes=ncls)
+    ctx = _ctx_for("resnet50", B, hw, ncls, 4 << 30, 2 << 30)
 else:
     net = nets.tiny_cnn(); B = 8; hw = 32; ncls = 10
     ctx = _ctx_for("tiny", B, hw, ncls, 256 << 20, 64 << 20)
