@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-incore", action="store_true", help="skip the in-core comparison run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--profile-iters", type=int, default=2)
+    ap.add_argument("--precision", type=int, default=1, choices=[0, 1],
+                    help="contractions: 1 = 3xTF32 (default, fp32-faithful), 0 = single TF32")
     return ap.parse_args()
 
 
@@ -180,6 +182,7 @@ def our_arm(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     batch, budget, wname = workload(args)
     ctx = Context.builtin("resnet50", batch, in_hw=224, classes=1000, device=dev_idx)
+    ctx.set_precision(args.precision)
     free, total = torch.cuda.mem_get_info()
     if budget is None:
         budget = int(free - (3 << 30))
@@ -285,7 +288,8 @@ def our_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (tf32 tensor-core contractions, fp32 accumulate/storage)",
+        "vs_baseline": None,
+        "dtype": "f32 (%s tensor-core contractions, fp32 accumulate/storage)" % ("3xtf32" if args.precision else "tf32"),
         "data": "synthetic (x ~ N(0,1), labels U[0,1000), He-normal weights; seeded)",
         "config": {"workload": wname, "global_batch": batch * world, "seq_len": None,
                    "parallelism": "dp%d" % world, "budget_bytes_per_gpu": budget,
@@ -386,6 +390,7 @@ def incore_run(ctx_ooc, dev, host, host_bytes, streams, args, free):
     batch = ctx_ooc.batch
     try:
         ctx = Context.builtin("resnet50", batch, in_hw=224, classes=1000)
+        ctx.set_precision(args.precision)
         need = int(ctx.resident_bytes() + sum(ctx_map_bytes(ctx)) * 1.4)
         free_now, _ = torch.cuda.mem_get_info()
         if need > free_now - (2 << 30):

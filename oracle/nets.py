@@ -270,9 +270,12 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
     return loss, grads, outs
 
 
-def init_params(net: Net, seed: int = 2, bn_random: bool = False) -> dict:
+def init_params(net: Net, seed: int = 2, bn_random: bool = False, residual_gamma=None) -> dict:
     """Seeded fp32 parameters (synthdata recipe). With ``bn_random`` gamma ~
-    U(0.5,1.5), beta ~ U(-0.2,0.2) (parity tests, so gamma/beta mix-ups show)."""
+    U(0.5,1.5), beta ~ U(-0.2,0.2) (parity tests, so gamma/beta mix-ups show).
+    ``residual_gamma=(lo, hi)`` draws the last BN gamma of every residual branch
+    (``gamma3``) from U(lo, hi) -- the small-residual initialisation of
+    large-batch ResNet training (DESIGN.md Reading 28)."""
     g = synthdata.rng(seed)
     params = {}
     for name, shape in param_shapes(net).items():
@@ -284,6 +287,8 @@ def init_params(net: Net, seed: int = 2, bn_random: bool = False) -> dict:
         elif ".gamma" in name:
             params[name] = (g.uniform(0.5, 1.5, shape).astype(np.float32) if bn_random
                             else np.ones(shape, np.float32))
+            if residual_gamma is not None and name.endswith(".gamma3"):
+                params[name] = g.uniform(residual_gamma[0], residual_gamma[1], shape).astype(np.float32)
         else:
             params[name] = (g.uniform(-0.2, 0.2, shape).astype(np.float32) if bn_random
                             else np.zeros(shape, np.float32))

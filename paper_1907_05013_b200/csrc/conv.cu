@@ -32,8 +32,11 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
     configured = true;
   }
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return POOCH_OK;
+  // persistent: one CTA per SM (smem-limited), tiles strided over the grid
+  int64_t tiles = (int64_t)grid.x * grid.y * grid.z;
+  int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
-  kern<<<grid, NUM_THREADS, SMEM, st>>>(p);
+  kern<<<ctas, NUM_THREADS_P, SMEM, st>>>(p);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }

@@ -77,8 +77,14 @@ template <int MODE>
 __global__ void bn_apply_kernel(const float* __restrict__ a, const float* __restrict__ sa, const float* __restrict__ ta,
                                 const float* __restrict__ b, const float* __restrict__ sb,
                                 const float* __restrict__ tb, float* __restrict__ y, int64_t n4, int C4) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(i % C4) * 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int cstep = (int)(stride % C4);
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int cg = (int)(i % C4);  // channel group, advanced incrementally (no 64-bit modulo per element)
+  for (; i < n4; i += stride) {
+    int c = cg * 4;
+    cg += cstep;
+    if (cg >= C4) cg -= C4;
     float4 av = ld4(a + 4 * i), s1 = ld4(sa + c), t1 = ld4(ta + c);
     float4 bv = make_float4(0, 0, 0, 0), s2 = bv, t2 = bv;
     if (MODE != 0) bv = ld4(b + 4 * i);
@@ -193,8 +199,14 @@ __global__ void bn_bwd_finalize_kernel(BnBwdArgs p, const float* __restrict__ pa
 template <int MODE>
 __global__ void bn_bwd_apply_kernel(BnBwdArgs p, const float* __restrict__ coef, int64_t n4) {
   const int C = p.C, C4 = C / 4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(i % C4) * 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int cstep = (int)(stride % C4);
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int cg = (int)(i % C4);
+  for (; i < n4; i += stride) {
+    int c = cg * 4;
+    cg += cstep;
+    if (cg >= C4) cg -= C4;
     size_t off = 4 * (size_t)i;
     float4 av = ld4(p.a + off), g = ld4(p.gy + off);
     float4 s1 = ld4(p.sa + c), t1 = ld4(p.ta + c), m1 = ld4(p.mean_a + c), i1 = ld4(p.invstd_a + c);

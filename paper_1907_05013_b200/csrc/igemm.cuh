@@ -68,7 +68,7 @@ struct GemmSmem {
   static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
   static constexpr int SMALL_OFF = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 4 * BN * 4 * 2 + 1024;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 4 * BN * 4 * 2 + 1024;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -306,64 +306,107 @@ __device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
   return v[0];
 }
 
+// Persistent, warp-specialised kernel: each CTA walks tiles t = blockIdx.x + i*gridDim.x
+// (M-tiles fastest, so concurrently running CTAs share the B tile in L2). Two TMEM
+// accumulators let the epilogue of tile i overlap the mainloop of tile i+1.
+//   warps 0-3 : epilogue (TMEM lane quadrant = warp), warps 4-7 : producers,
+//   warp 8    : TMEM allocator + single-thread MMA issuer.
+constexpr int NUM_THREADS_P = 288;
+
+struct TileMap {
+  int mt, nt, zt, kb_total, kbps;
+  __device__ void decode(int t, int& m0, int& n0, int& kb0, int& nkb, int bn) const {
+    int m = t % mt;
+    int r = t / mt;
+    int n = r % nt;
+    int z = r / nt;
+    m0 = m * BM;
+    n0 = n * bn;
+    kb0 = z * kbps;
+    nkb = max(0, min(kb_total, kb0 + kbps) - kb0);
+  }
+};
+
 template <int MODE, int BN, int STAGES, bool X3 = false>
-__global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams p) {
+__global__ void __launch_bounds__(NUM_THREADS_P, 1) igemm_kernel(const GemmParams p) {
   using SM = GemmSmem<BN, STAGES, X3>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  float* red = reinterpret_cast<float*>(smem + SM::BAR_OFF + (2 * STAGES + 1) * 8 + 16);  // [4][BN] x2
+  uint64_t* tfull = empty + STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* red = reinterpret_cast<float*>(smem + SM::BAR_OFF + (2 * STAGES + 4) * 8 + 16);  // [4][BN] x2
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int m0 = blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
-  int kb_begin = 0, kb_end = (p.Kg + BK - 1) / BK;
-  if (p.kb_per_split > 0) {
-    kb_begin = blockIdx.z * p.kb_per_split;
-    kb_end = min(kb_end, kb_begin + p.kb_per_split);
-  }
-  const int nkb = max(kb_end - kb_begin, 0);
+  const int lane = tid & 31;
+  TileMap tm;
+  tm.mt = (p.M + BM - 1) / BM;
+  tm.nt = (p.Ng + BN - 1) / BN;
+  tm.kb_total = (p.Kg + BK - 1) / BK;
+  tm.kbps = p.kb_per_split > 0 ? p.kb_per_split : max(tm.kb_total, 1);
+  tm.zt = p.kb_per_split > 0 ? (tm.kb_total + tm.kbps - 1) / tm.kbps : 1;
+  const int ntiles = tm.mt * tm.nt * tm.zt;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 128);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, BN);
+  if (warp == 8) ptx::tmem_alloc(tmem_slot, 2 * BN);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = ptx::smem_u32(smem);
 
-  if (warp < 4) {
+  if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------------ producers
+    const int ptid = tid - 128;
     if constexpr (MODE == CONV_WGRAD) {
       static_assert(BN == 128, "wgrad uses 128 x 128 tiles");
-      TLoader<true> la;
-      TLoader<false> lb;
-      la.init(p, m0, tid);
-      lb.init(p, n0, tid);
-      TLoader<true> na;
-      TLoader<false> nb;
-      na = la;
-      nb = lb;
-      if (nkb > 0) {
-        la.load(p, kb_begin);
-        lb.load(p, kb_begin);
+      // flattened (tile, k-block) sequence with one block of register prefetch
+      int t = blockIdx.x, m0 = 0, n0 = 0, kb0 = 0, nkb = 0, kb = 0;
+      while (t < ntiles) {
+        tm.decode(t, m0, n0, kb0, nkb, BN);
+        if (nkb > 0) break;
+        t += gridDim.x;
       }
-      for (int it = 0; it < nkb; ++it) {
-        if (it + 1 < nkb) {
-          na.load(p, kb_begin + it + 1);
-          nb.load(p, kb_begin + it + 1);
+      TLoader<true> la, na;
+      TLoader<false> lb, nb;
+      if (t < ntiles) {
+        la.init(p, m0, ptid);
+        lb.init(p, n0, ptid);
+        la.load(p, kb0);
+        lb.load(p, kb0);
+      }
+      int it = 0;
+      while (t < ntiles) {
+        // cursor of the next block
+        int t2 = t, kb2 = kb + 1, m2 = m0, n2 = n0, kb02 = kb0, nkb2 = nkb;
+        if (kb2 >= nkb2) {
+          kb2 = 0;
+          t2 += gridDim.x;
+          while (t2 < ntiles) {
+            tm.decode(t2, m2, n2, kb02, nkb2, BN);
+            if (nkb2 > 0) break;
+            t2 += gridDim.x;
+          }
+        }
+        if (t2 < ntiles) {
+          na.init(p, m2, ptid);
+          nb.init(p, n2, ptid);
+          na.load(p, kb02 + kb2);
+          nb.load(p, kb02 + kb2);
         }
         int s = it % STAGES;
         if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
@@ -372,159 +415,199 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) igemm_kernel(const GemmParams 
         lb.template store<BN, X3>(st + SM::A_BYTES, SM::SMALL_OFF);
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&full[s]);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            la.reg[hh][kk] = na.reg[hh][kk];
-            lb.reg[hh][kk] = nb.reg[hh][kk];
-          }
+        ++it;
+        la = na;
+        lb = nb;
+        t = t2;
+        kb = kb2;
+        m0 = m2;
+        n0 = n2;
+        kb0 = kb02;
+        nkb = nkb2;
       }
     } else {
       KLoader<MODE, BM, true> la;
       KLoader<MODE, BN, false> lb;
-      la.init(p, m0, tid);
-      lb.init(p, n0, tid);
-      for (int it = 0; it < nkb + LAG; ++it) {
-        if (it < nkb) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, n0, kb0, nkb;
+        tm.decode(t, m0, n0, kb0, nkb, BN);
+        la.init(p, m0, ptid);
+        lb.init(p, n0, ptid);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
           int s = it % STAGES;
           if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
           uint32_t st = sbase + s * SM::STAGE_BYTES;
-          la.load(p, st, kb_begin + it);
-          lb.load(p, st + SM::A_BYTES, kb_begin + it);
-        }
-        ptx::cp_async_commit();
-        if (it >= LAG) {
-          ptx::cp_async_wait<LAG>();
-          if constexpr (X3) {
-            uint32_t st = sbase + ((it - LAG) % STAGES) * SM::STAGE_BYTES;
-            la.split(st, SM::SMALL_OFF);
-            lb.split(st + SM::A_BYTES, SM::SMALL_OFF);
-          }
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&full[(it - LAG) % STAGES]);
-        }
-      }
-    }
-    // ------------------------------------------------------------------ epilogue
-    ptx::mbar_wait(done, 0);
-    ptx::tc_fence_after();
-    const int lane = tid & 31;
-    const int row = warp * 32 + lane;
-    const int gm = m0 + row;
-    const bool rok = gm < p.M;
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float v[32];
-      if (nkb > 0) {
-        ptx::tmem_ld32(taddr + c * 32, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
-      const int nb = n0 + c * 32;
-      if constexpr (MODE == CONV_FWD) {
-        if (p.bias != nullptr) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Ng) ? __ldg(p.bias + nb + i) : 0.f;
-        }
-      }
-      if (rok) {
-        float* dst;
-        if constexpr (MODE == GEMM_TEST) {
-          dst = p.d + (size_t)blockIdx.z * p.M * p.ldd + (size_t)gm * p.ldd + nb;
-        } else if constexpr (MODE == CONV_WGRAD) {
-          dst = p.d + ((size_t)blockIdx.z * p.M + gm) * p.Ng + nb;
-        } else {
-          dst = p.d + (size_t)gm * p.Ng + nb;
-        }
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          if (nb + i < p.Ng) {
-            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            if constexpr (MODE == CONV_DGRAD) {
-              if (p.accumulate) {
-                float4 q = *reinterpret_cast<const float4*>(dst + i);
-                o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-              }
+          la.load(p, st, kb0 + kb);
+          lb.load(p, st + SM::A_BYTES, kb0 + kb);
+          ptx::cp_async_commit();
+          if (it >= LAG) {
+            ptx::cp_async_wait<LAG>();
+            int so = (it - LAG) % STAGES;
+            if constexpr (X3) {
+              uint32_t sto = sbase + so * SM::STAGE_BYTES;
+              la.split(sto, SM::SMALL_OFF);
+              lb.split(sto + SM::A_BYTES, SM::SMALL_OFF);
             }
-            *reinterpret_cast<float4*>(dst + i) = o;
+            ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive(&full[so]);
           }
         }
       }
-      if constexpr (MODE == CONV_FWD) {
-        if (p.stat_sum != nullptr) {
-          float sq[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            v[i] = rok ? v[i] : 0.f;
-            sq[i] = v[i] * v[i];
-          }
-          float s1 = warp_transpose_sum32(v, lane);
-          float s2 = warp_transpose_sum32(sq, lane);
-          red[warp * BN + c * 32 + lane] = s1;
-          red[4 * BN + warp * BN + c * 32 + lane] = s2;
+      // drain: the last min(LAG, it) stages
+      ptx::cp_async_wait<0>();
+      for (int q = max(0, it - LAG); q < it; ++q) {
+        int so = q % STAGES;
+        if constexpr (X3) {
+          uint32_t sto = sbase + so * SM::STAGE_BYTES;
+          la.split(sto, SM::SMALL_OFF);
+          lb.split(sto + SM::A_BYTES, SM::SMALL_OFF);
         }
-      }
-    }
-    if constexpr (MODE == CONV_FWD) {
-      if (p.stat_sum != nullptr) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int j = tid; j < BN; j += 128) {
-          int n = n0 + j;
-          if (n < p.Ng) {
-            float a = ((red[j] + red[BN + j]) + red[2 * BN + j]) + red[3 * BN + j];
-            float b = ((red[4 * BN + j] + red[5 * BN + j]) + red[6 * BN + j]) + red[7 * BN + j];
-            p.stat_sum[(size_t)blockIdx.x * p.Ng + n] = a;
-            p.stat_sq[(size_t)blockIdx.x * p.Ng + n] = b;
-          }
-        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&full[so]);
       }
     }
-  } else {
+  } else if (warp == 8) {
     // ------------------------------------------------------------------ MMA issuer
     constexpr uint32_t IDESC = ptx::idesc_tf32(BM, BN, false, false);
     // K-major SWIZZLE_NONE: LBO = distance of K-adjacent core matrices, SBO = 128 (M/N-adjacent)
     constexpr uint32_t A_LBO = BM * 16;
     constexpr uint32_t B_LBO = BN * 16;
-    const int lane = tid & 31;
-    for (int it = 0; it < nkb; ++it) {
-      int s = it % STAGES;
-      ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+    int it = 0, j = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      int m0, n0, kb0, nkb;
+      tm.decode(t, m0, n0, kb0, nkb, BN);
+      const int ab = j & 1;
+      if (j >= 2) ptx::mbar_wait(&tempty[ab], ((j >> 1) - 1) & 1);
       ptx::tc_fence_after();
-      if (lane == 0) {
-        uint32_t sa = sbase + s * SM::STAGE_BYTES;
-        uint32_t sb = sa + SM::A_BYTES;
+      const uint32_t acc = tmem + ab * BN;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        int s = it % STAGES;
+        ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+          uint32_t sa = sbase + s * SM::STAGE_BYTES;
+          uint32_t sb = sa + SM::A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          uint64_t ad = ptx::smem_desc(sa + kk * 2 * A_LBO, A_LBO, 128);
-          uint64_t bd = ptx::smem_desc(sb + kk * 2 * B_LBO, B_LBO, 128);
-          if constexpr (X3) {  // small terms first, then the big product
-            uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + kk * 2 * A_LBO, A_LBO, 128);
-            uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + kk * 2 * B_LBO, B_LBO, 128);
-            ptx::mma_tf32(tmem, asd, bd, IDESC, (it | kk) != 0 ? 1u : 0u);
-            ptx::mma_tf32(tmem, ad, bsd, IDESC, 1u);
-            ptx::mma_tf32(tmem, ad, bd, IDESC, 1u);
-          } else {
-            ptx::mma_tf32(tmem, ad, bd, IDESC, (it | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            uint64_t ad = ptx::smem_desc(sa + kk * 2 * A_LBO, A_LBO, 128);
+            uint64_t bd = ptx::smem_desc(sb + kk * 2 * B_LBO, B_LBO, 128);
+            if constexpr (X3) {  // small terms first, then the big product
+              uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + kk * 2 * A_LBO, A_LBO, 128);
+              uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + kk * 2 * B_LBO, B_LBO, 128);
+              ptx::mma_tf32(acc, asd, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+              ptx::mma_tf32(acc, ad, bsd, IDESC, 1u);
+              ptx::mma_tf32(acc, ad, bd, IDESC, 1u);
+            } else {
+              ptx::mma_tf32(acc, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            }
           }
+          ptx::mma_commit(&empty[s]);
         }
-        ptx::mma_commit(&empty[s]);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (nkb > 0) ptx::mma_commit(&tfull[ab]);
+        else ptx::mbar_arrive(&tfull[ab]);
       }
       __syncwarp();
     }
-    if (lane == 0) {
-      if (nkb > 0) ptx::mma_commit(done);
-      else ptx::mbar_arrive(done);
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    const int row = warp * 32 + lane;
+    int j = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      int m0, n0, kb0, nkb;
+      tm.decode(t, m0, n0, kb0, nkb, BN);
+      const int ab = j & 1;
+      ptx::mbar_wait(&tfull[ab], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      const int gm = m0 + row;
+      const bool rok = gm < p.M;
+      const uint32_t taddr = tmem + ab * BN + ((uint32_t)(warp * 32) << 16);
+      const int z = t / (tm.mt * tm.nt);
+      bool stats = false;
+      if constexpr (MODE == CONV_FWD) stats = p.stat_sum != nullptr;
+      if (stats) asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's reads of red[] done
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        if (nkb > 0) {
+          ptx::tmem_ld32(taddr + c * 32, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        const int nb = n0 + c * 32;
+        if constexpr (MODE == CONV_FWD) {
+          if (p.bias != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Ng) ? __ldg(p.bias + nb + i) : 0.f;
+          }
+        }
+        if (rok) {
+          float* dst;
+          if constexpr (MODE == GEMM_TEST) {
+            dst = p.d + (size_t)z * p.M * p.ldd + (size_t)gm * p.ldd + nb;
+          } else if constexpr (MODE == CONV_WGRAD) {
+            dst = p.d + ((size_t)z * p.M + gm) * p.Ng + nb;
+          } else {
+            dst = p.d + (size_t)gm * p.Ng + nb;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            if (nb + i < p.Ng) {
+              float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+              if constexpr (MODE == CONV_DGRAD) {
+                if (p.accumulate) {
+                  float4 q = *reinterpret_cast<const float4*>(dst + i);
+                  o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+                }
+              }
+              *reinterpret_cast<float4*>(dst + i) = o;
+            }
+          }
+        }
+        if constexpr (MODE == CONV_FWD) {
+          if (stats) {
+            float sq[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              v[i] = rok ? v[i] : 0.f;
+              sq[i] = v[i] * v[i];
+            }
+            float s1 = warp_transpose_sum32(v, lane);
+            float s2 = warp_transpose_sum32(sq, lane);
+            red[warp * BN + c * 32 + lane] = s1;
+            red[4 * BN + warp * BN + c * 32 + lane] = s2;
+          }
+        }
+      }
+      // accumulator drained: hand the TMEM buffer back to the MMA warp
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[ab]);
+      if constexpr (MODE == CONV_FWD) {
+        if (stats) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const int mt_idx = m0 / BM;
+          for (int jj = tid; jj < BN; jj += 128) {
+            int n = n0 + jj;
+            if (n < p.Ng) {
+              float a = ((red[jj] + red[BN + jj]) + red[2 * BN + jj]) + red[3 * BN + jj];
+              float b = ((red[4 * BN + jj] + red[5 * BN + jj]) + red[6 * BN + jj]) + red[7 * BN + jj];
+              p.stat_sum[(size_t)mt_idx * p.Ng + n] = a;
+              p.stat_sq[(size_t)mt_idx * p.Ng + n] = b;
+            }
+          }
+        }
+      }
     }
-    __syncwarp();
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, BN);
+    ptx::tmem_dealloc(tmem, 2 * BN);
   }
 }
 

@@ -138,9 +138,11 @@ def test_tiny_cnn_pooch_at_half_budget(tiny):
 
 @pytest.fixture(scope="module")
 def r50():
-    # 224^2 (the paper's input size) at batch 8: every BN sees >= 392 samples per channel
+    # 224^2 (the paper's input size) at batch 8; small-residual init (gamma3 ~ U(0.1, 0.3),
+    # DESIGN.md Reading 28): with gamma3 ~ 1 the random network is chaotic and fp32 rounding
+    # alone moves its gradients by ~4% against fp64 (measured), whatever the kernels do.
     net = nets.resnet50(in_hw=224, classes=1000)
-    params = nets.init_params(net, seed=2, bn_random=True)
+    params = nets.init_params(net, seed=2, bn_random=True, residual_gamma=(0.1, 0.3))
     x = synthdata.images(8, 224, 224, 3, seed=0)
     t = synthdata.labels(8, 1000, seed=1)
     loss, grads, _ = nets.forward_backward(net, params, x, t)

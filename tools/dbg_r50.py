@@ -13,7 +13,13 @@ if which == "r50":
 else:
     net = nets.tiny_cnn(); B = 8; hw = 32; ncls = 10
     ctx = _ctx_for("tiny", B, hw, ncls, 256 << 20, 64 << 20)
-params = nets.init_params(net, seed=2, bn_random=True)
+init = os.environ.get("INIT", "random")
+params = nets.init_params(net, seed=2, bn_random=(init != "bench"))
+if init == "smallres":
+    g0 = np.random.default_rng(9)
+    for k in params:
+        if k.endswith(".gamma3"):
+            params[k] = g0.uniform(0.1, 0.3, params[k].shape).astype(np.float32)
 x = synthdata.images(B, hw, hw, 3, seed=0); t = synthdata.labels(B, ncls, seed=1)
 gm = []
 loss, grads, outs = nets.forward_backward(net, params, x, t, map_grads=gm, precision=os.environ.get("ORACLE_PREC", "fp64"))
@@ -22,6 +28,11 @@ load_params(ctx, params); _put_batch(ctx, x, t)
 ctx.plan("incore")
 l = ctx.train_step(0.0)
 print("loss", l, loss)
+from netutil import global_rel
+g_all = read_params(ctx, params, 1)
+print("INIT", init, "global rel-L2 %.3e" % global_rel(g_all, grads))
+if os.environ.get("SHORT"):
+    sys.exit(0)
 for i in reversed(range(len(net.tasks))):
     tk = net.tasks[i]
     c, h, w = tk.out_chw
