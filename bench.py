@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-incore", action="store_true", help="skip the in-core comparison run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--profile-iters", type=int, default=2)
+    ap.add_argument("--ncu-step", action="store_true",
+                    help="profile/plan, 1 warm-up step, then exactly one step inside cudaProfilerStart/Stop "
+                         "(for ncu --profile-from-start off); prints nothing")
     ap.add_argument("--precision", type=int, default=1, choices=[0, 1],
                     help="contractions: 1 = 3xTF32 (default, fp32-faithful), 0 = single TF32")
     return ap.parse_args()
@@ -263,6 +266,14 @@ def our_arm(args):
             ms = float(t.item())
         return ms
 
+    if args.ncu_step:
+        ctx.train_step(0.01, sync_loss=False)
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
+        ctx.train_step(0.01, sync_loss=False)
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        return
     for _ in range(args.warmup):
         ctx.train_step(0.01, sync_loss=False)
     torch.cuda.synchronize()

@@ -36,7 +36,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   int64_t tiles = (int64_t)grid.x * grid.y * grid.z;
   int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
-  kern<<<ctas, NUM_THREADS_P, SMEM, st>>>(p);
+  kern<<<ctas, igemm_threads(MODE, X3), SMEM, st>>>(p);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }

@@ -68,7 +68,7 @@ struct GemmSmem {
   static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
   static constexpr int SMALL_OFF = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 4 * BN * 4 * 2 + 1024;
+  static constexpr int TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 4 * BN * 4 * 2 + 1024;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -311,7 +311,12 @@ __device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
 // accumulators let the epilogue of tile i overlap the mainloop of tile i+1.
 //   warps 0-3 : epilogue (TMEM lane quadrant = warp), warps 4-7 : producers,
 //   warp 8    : TMEM allocator + single-thread MMA issuer.
-constexpr int NUM_THREADS_P = 288;
+constexpr int NUM_THREADS_P = 288;      // 4 epilogue + 4 producer + 1 MMA warps
+constexpr int NUM_THREADS_X3 = 416;     // + 4 residual ("split") warps for 3xTF32
+// wgrad's producers write residuals themselves (register transpose), so it needs no split warps
+__host__ __device__ constexpr int igemm_threads(int mode, bool x3) {
+  return (x3 && mode != CONV_WGRAD) ? NUM_THREADS_X3 : NUM_THREADS_P;
+}
 
 struct TileMap {
   int mt, nt, zt, kb_total, kbps;
@@ -328,7 +333,7 @@ struct TileMap {
 };
 
 template <int MODE, int BN, int STAGES, bool X3 = false>
-__global__ void __launch_bounds__(NUM_THREADS_P, 1) igemm_kernel(const GemmParams p) {
+__global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const GemmParams p) {
   using SM = GemmSmem<BN, STAGES, X3>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -337,8 +342,9 @@ __global__ void __launch_bounds__(NUM_THREADS_P, 1) igemm_kernel(const GemmParam
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* red = reinterpret_cast<float*>(smem + SM::BAR_OFF + (2 * STAGES + 4) * 8 + 16);  // [4][BN] x2
+  uint64_t* rawfull = tempty + 2;     // [STAGES] 3xTF32: raw operands landed (cp.async arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rawfull + STAGES);
+  float* red = reinterpret_cast<float*>(smem + SM::BAR_OFF + (3 * STAGES + 4) * 8 + 16);  // [4][BN] x2
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -360,6 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS_P, 1) igemm_kernel(const GemmParam
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&rawfull[s], 128);
     ptx::fence_mbar_init();
   }
   if (warp == 8) ptx::tmem_alloc(tmem_slot, 2 * BN);
@@ -440,31 +447,32 @@ __global__ void __launch_bounds__(NUM_THREADS_P, 1) igemm_kernel(const GemmParam
           uint32_t st = sbase + s * SM::STAGE_BYTES;
           la.load(p, st, kb0 + kb);
           lb.load(p, st + SM::A_BYTES, kb0 + kb);
-          ptx::cp_async_commit();
-          if (it >= LAG) {
-            ptx::cp_async_wait<LAG>();
-            int so = (it - LAG) % STAGES;
-            if constexpr (X3) {
-              uint32_t sto = sbase + so * SM::STAGE_BYTES;
-              la.split(sto, SM::SMALL_OFF);
-              lb.split(sto + SM::A_BYTES, SM::SMALL_OFF);
-            }
-            ptx::fence_proxy_async_smem();
-            ptx::mbar_arrive(&full[so]);
-          }
+          // the barrier completes when this thread's copies land: no wait in the producer
+          ptx::cp_async_arrive_noinc(X3 ? &rawfull[s] : &full[s]);
         }
       }
-      // drain: the last min(LAG, it) stages
       ptx::cp_async_wait<0>();
-      for (int q = max(0, it - LAG); q < it; ++q) {
-        int so = q % STAGES;
-        if constexpr (X3) {
-          uint32_t sto = sbase + so * SM::STAGE_BYTES;
-          la.split(sto, SM::SMALL_OFF);
-          lb.split(sto + SM::A_BYTES, SM::SMALL_OFF);
+    }
+  } else if (X3 && warp >= 9) {
+    // ------------------------------------------------------------------ 3xTF32 residual warps
+    // For every stage: wait for the raw operands, write x - tf32(x) for all chunks of A and B
+    // (an element-wise pass, any partition works), publish to the async proxy, arrive full[].
+    if constexpr (X3 && MODE != CONV_WGRAD) {
+      const int stid = tid - 9 * 32;
+      constexpr int CHUNKS = (BM + BN) * BK / 4;  // 16-B chunks of A and B (contiguous)
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, n0, kb0, nkb;
+        tm.decode(t, m0, n0, kb0, nkb, BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          int s = it % STAGES;
+          ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
+          uint32_t st = sbase + s * SM::STAGE_BYTES;
+#pragma unroll 4
+          for (int c = stid; c < CHUNKS; c += 128) split_chunk(st + c * 16, st + SM::SMALL_OFF + c * 16);
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&full[s]);
         }
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&full[so]);
       }
     }
   } else if (warp == 8) {
@@ -520,7 +528,7 @@ __global__ void __launch_bounds__(NUM_THREADS_P, 1) igemm_kernel(const GemmParam
       int m0, n0, kb0, nkb;
       tm.decode(t, m0, n0, kb0, nkb, BN);
       const int ab = j & 1;
-      ptx::mbar_wait(&tfull[ab], (j >> 1) & 1);
+      ptx::mbar_wait_sleep(&tfull[ab], (j >> 1) & 1);
       ptx::tc_fence_after();
       const int gm = m0 + row;
       const bool rok = gm < p.M;
