@@ -314,7 +314,7 @@ def our_arm(args):
         "gpu_launches": launches,
         "roofline": roof,
         "swap": swap_stats(fam, prof),
-        "families_ms": {k: round(v["ms"], 3) for k, v in fam.items()},
+        "families": families_table(fam, peaks()),
     }
     if incore is not None:
         line["incore"] = incore
@@ -375,6 +375,33 @@ def roofline(fam, pk):
     return {"kernel": k, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": ach / pk["hbm_gbs"], "traffic": traffic_for(k), "launches": v["launches"],
             "peak_src": pk["src"]}
+
+
+def families_table(fam, pk):
+    """Per kernel family of the instrumented step: time, launches, achieved algorithmic
+    GB/s and TFLOP/s, and the fraction of the binding roof (HBM copy peak or TF32 peak)."""
+    out = {}
+    tf = pk["tf32_tflops_sustained"] * 1e12
+    bw = pk["hbm_gbs"] * 1e9
+    for k, v in fam.items():
+        if v["ms"] <= 0:
+            continue
+        t = v["ms"] / 1e3
+        e = {"ms": round(v["ms"], 3), "launches": v["launches"]}
+        if v["bytes"] > 0:
+            e["gbs"] = round(v["bytes"] / t / 1e9, 1)
+        if v["flops"] > 0:
+            e["tflops"] = round(v["flops"] / t / 1e12, 2)
+        if k in ("swap_out", "swap_in"):
+            pass
+        elif v["flops"] / tf >= v["bytes"] / bw and v["flops"] > 0:
+            e["bound"] = "tensor"
+            e["frac"] = round(v["flops"] / t / tf, 4)
+        elif v["bytes"] > 0:
+            e["bound"] = "hbm"
+            e["frac"] = round(v["bytes"] / t / bw, 4)
+        out[k] = e
+    return out
 
 
 def traffic_for(family):

@@ -43,25 +43,41 @@ __global__ void bn_fin_partial_kernel(const float* __restrict__ ts, const float*
   part[(size_t)(kFinRows + chunk) * C + c] = q;
 }
 
+// 32 channels per block, 8 warps stride the rows; fixed-order combine (deterministic)
 __global__ void bn_fin_final_kernel(const double* __restrict__ part, int C, double count, const float* gamma,
                                     const float* beta, float* mean, float* invstd, float* scale, float* shift) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+  __shared__ double sh[2][8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   double s = 0, q = 0;
-  for (int r = 0; r < kFinRows; ++r) {
-    s += part[(size_t)r * C + c];
-    q += part[(size_t)(kFinRows + r) * C + c];
+  if (c < C) {
+#pragma unroll 4
+    for (int r = w; r < kFinRows; r += 8) {
+      s += part[(size_t)r * C + c];
+      q += part[(size_t)(kFinRows + r) * C + c];
+    }
   }
-  double mu = s / count;
-  double var = q / count - mu * mu;
-  if (var < 0) var = 0;
-  float is = (float)(1.0 / sqrt(var + 1e-5));
-  float m = (float)mu;
-  mean[c] = m;
-  invstd[c] = is;
-  float sc = gamma[c] * is;
-  scale[c] = sc;
-  shift[c] = __fsub_rn(beta[c], __fmul_rn(m, sc));
+  sh[0][w][lane] = s;
+  sh[1][w][lane] = q;
+  __syncthreads();
+  if (w == 0 && c < C) {
+    s = 0;
+    q = 0;
+    for (int k = 0; k < 8; ++k) {
+      s += sh[0][k][lane];
+      q += sh[1][k][lane];
+    }
+    double mu = s / count;
+    double var = q / count - mu * mu;
+    if (var < 0) var = 0;
+    float is = (float)(1.0 / sqrt(var + 1e-5));
+    float m = (float)mu;
+    mean[c] = m;
+    invstd[c] = is;
+    float sc = gamma[c] * is;
+    scale[c] = sc;
+    shift[c] = __fsub_rn(beta[c], __fmul_rn(m, sc));
+  }
 }
 
 // ------------------------------------------------------------------ BN apply (+add) + ReLU
@@ -172,13 +188,28 @@ __global__ void __launch_bounds__(kBwdThreads) bn_bwd_reduce_kernel(BnBwdArgs p,
 // coef layout after the partials: [ka, kb, kc] for BN(a) then BN(b), each [C]
 template <int MODE>
 __global__ void bn_bwd_finalize_kernel(BnBwdArgs p, const float* __restrict__ part, int blocks, float* coef) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= p.C) return;
   constexpr int NQ = MODE == 1 ? 3 : 2;
+  __shared__ double sh[NQ][8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0;
+  if (c < p.C) {
+    for (int b = w; b < blocks; b += 8) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) acc[q] += (double)part[((size_t)q * blocks + b) * p.C + c];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) sh[q][w][lane] = acc[q];
+  __syncthreads();
+  if (w != 0 || c >= p.C) return;
   double s[NQ];
+#pragma unroll
   for (int q = 0; q < NQ; ++q) {
     double t = 0;
-    for (int b = 0; b < blocks; ++b) t += (double)part[((size_t)q * blocks + b) * p.C + c];
+    for (int k = 0; k < 8; ++k) t += sh[q][k][lane];
     s[q] = t;
   }
   double M = (double)p.rows;
@@ -466,7 +497,7 @@ pooch_status bn_finalize(const float* ts, const float* tq, int tiles, int C, int
   count_launch();
   bn_fin_partial_kernel<<<g1, 128, 0, st>>>(ts, tq, tiles, C, ws);
   count_launch();
-  bn_fin_final_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, C, (double)count, gamma, beta, mean, invstd, scale, shift);
+  bn_fin_final_kernel<<<(C + 31) / 32, 256, 0, st>>>(ws, C, (double)count, gamma, beta, mean, invstd, scale, shift);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
@@ -506,7 +537,7 @@ static pooch_status bn_bwd_mode(const BnBwdArgs& a, float* ws, cudaStream_t st) 
     return fail(POOCH_EUSAGE, "BN backward supports C <= 2048 (C = %d)", C);
   }
   count_launch();
-  bn_bwd_finalize_kernel<MODE><<<(C + 127) / 128, 128, 0, st>>>(a, ws, blocks, coef);
+  bn_bwd_finalize_kernel<MODE><<<(C + 31) / 32, 256, 0, st>>>(a, ws, blocks, coef);
   int64_t n4 = a.rows * C / 4;
   count_launch();
   bn_bwd_apply_kernel<MODE><<<grid_for(n4, 256), 256, 0, st>>>(a, coef, n4);

@@ -20,8 +20,9 @@
 //   CONV_DGRAD: A = dy gathered by the transposed-conv rule [M=N*H*W, K=R*S*Cout],
 //               B = Wt [C, R*S*Cout]; epilogue stores (or accumulates into) dx.
 //   CONV_WGRAD: A = dy^T [Cout, K=N*Ho*Wo], B = im2col(x)^T [R*S*C, K]; both are strided along
-//               K in NHWC, so the producers load 4x4 blocks and transpose them in registers
-//               (TLoader); split-K over pixels, epilogue stores the split's partial dW (KRSC).
+//               K in NHWC: producers cp.async 16-B (4-channel) chunks into their 4x4 blocks and
+//               the auxiliary warps transpose each block in place (WLoader / transpose_block);
+//               split-K over pixels, the epilogue stores the split's partial dW (KRSC).
 //   GEMM_TEST : plain K-major A [M][K], B [N][K], for unit tests of the core.
 // (All smem operands are K-major SWIZZLE_NONE. MN-major tf32 operands -- transpose bits 15/16
 //  of the instruction descriptor -- produced all-zero results on B200 in our tests, see
@@ -206,89 +207,117 @@ struct KLoader {
   }
 };
 
-// ---- Transposing loaders for wgrad (both operands are contiguous along M/N, strided along
-// K = pixels, in NHWC). Each thread loads 4x4 blocks (4 pixels x 4 channels) with 128-bit
-// global loads into registers, transposes them and stores K-major 16-B chunks with st.shared;
-// the row written at step i is rotated per lane so that every 8-lane phase hits 8 distinct
-// 16-B bank groups. Lane l owns channel group g = l (4 consecutive M/N rows); warp w owns the
-// k chunks h = 2w, 2w+1 of every 32-pixel block. Loads for block kb+1 are issued before the
-// stores of block kb (register double buffering).
-__device__ __forceinline__ float sel4(const float4& v, int i) {
-  float a = (i & 1) ? v.y : v.x;
-  float b = (i & 1) ? v.w : v.z;
-  return (i & 2) ? b : a;
-}
-
+// ---- wgrad operands. Both are contiguous along M/N and strided along K (= pixels) in NHWC:
+// A = dy^T [Cout][pixels], B = im2col(x)^T [R*S*C][pixels]. Producers cp.async each 16-B
+// chunk (4 channels of one pixel) to the K-major position of the 4x4 (channel x pixel) block
+// it belongs to -- the block's 64 B hold its four pixel-chunks untransposed -- and the
+// transform warps transpose every block in place (plus the 3xTF32 residuals) before the
+// MMA reads the stage. Warp pw (0..3) covers chunk blocks b = 8 pw .. 8 pw + 7 per tile:
+// g = 8 (b & 3) + (l & 7) (channel group), k = 4 (b >> 2) + (l >> 3) (pixel) -- each
+// instruction writes 4 whole core matrices (conflict-free) and reads 4 x 128 B of global.
 template <bool IS_A>
-struct TLoader {
-  int lane, warp;
-  bool gok;
-  int mn;                 // first M/N row of this lane's group
-  int gr, gs, gc;         // B: (r, s, c) of the group
-  float4 reg[2][4];
+struct WLoader {
+  int lane, pw;
+  const float* base[4];   // B: image-independent part of the address of the 4 owned groups
+  int gr[4], gs[4], gc[4];
+  bool gok[4];
+  int mn0;
 
-  __device__ void init(const GemmParams& p, int mn0, int tid) {
-    warp = tid >> 5;
-    lane = tid & 31;
-    mn = mn0 + 4 * lane;
-    gok = mn < (IS_A ? p.M : p.Ng);
-    if (!IS_A) {
-      int v = gok ? mn : 0;
-      int rs = v / p.C;
-      gc = v - rs * p.C;
-      gr = rs / p.S;
-      gs = rs - gr * p.S;
-    }
-  }
-
-  __device__ void load(const GemmParams& p, int kb) {
+  __device__ void init(const GemmParams& p, int mn_start, int ptid) {
+    pw = ptid >> 5;
+    lane = ptid & 31;
+    mn0 = mn_start;
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        int k = kb * BK + 4 * (2 * warp + hh) + kk;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (IS_A) {
-          if (gok && k < p.Kg) v = __ldg(reinterpret_cast<const float4*>(p.a + (size_t)k * p.K + mn));
-        } else {
-          if (gok && k < p.Kg) {
-            int wo = k % p.Wo;
-            int t = k / p.Wo;
-            int ho = t % p.Ho;
-            int n = t / p.Ho;
-            int hi = ho * p.stride - p.pad + gr, wi = wo * p.stride - p.pad + gs;
-            if ((unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W)
-              v = __ldg(reinterpret_cast<const float4*>(p.b + (((size_t)n * p.H + hi) * p.W + wi) * p.C + gc));
-          }
-        }
-        reg[hh][kk] = v;
+    for (int q = 0; q < 4; ++q) {
+      int g = 8 * q + (lane & 7);
+      int mn = mn_start + 4 * g;
+      gok[q] = mn < (IS_A ? p.M : p.Ng);
+      if (!IS_A) {
+        int v = gok[q] ? mn : 0;
+        int rs = v / p.C;
+        gc[q] = v - rs * p.C;
+        gr[q] = rs / p.S;
+        gs[q] = rs - gr[q] * p.S;
       }
     }
   }
 
-  template <int ROWS, bool X3 = false>
-  __device__ void store(uint32_t sbase, uint32_t delta = 0) const {
-    const int rot = (lane >> 1) & 3;
+  __device__ void load(const GemmParams& p, uint32_t sbase, int kb) {
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      int h = 2 * warp + hh;
+    for (int h = 0; h < 2; ++h) {                 // the two pixels this thread touches
+      int k = 4 * (2 * pw + h) + (lane >> 3);
+      int pix = kb * BK + k;
+      bool kok = pix < p.Kg;
+      int n = 0, hb = 0, wb = 0;
+      if (!IS_A && kok) {
+        int wo = pix % p.Wo;
+        int t = pix / p.Wo;
+        int ho = t % p.Ho;
+        n = t / p.Ho;
+        hb = ho * p.stride - p.pad;
+        wb = wo * p.stride - p.pad;
+      }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int mi = (i + rot) & 3;
-        int row = 4 * lane + mi;
-        float x0 = sel4(reg[hh][0], mi), x1 = sel4(reg[hh][1], mi), x2 = sel4(reg[hh][2], mi),
-              x3 = sel4(reg[hh][3], mi);
-        uint32_t addr = sbase + kmaj_off<ROWS>(row, h);
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x0), "f"(x1), "f"(x2), "f"(x3)
-                     : "memory");
-        if (X3)
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr + delta), "f"(tf32_resid(x0)),
-                       "f"(tf32_resid(x1)), "f"(tf32_resid(x2)), "f"(tf32_resid(x3))
-                       : "memory");
+      for (int q = 0; q < 4; ++q) {
+        int g = 8 * q + (lane & 7);
+        uint32_t dst = sbase + kmaj_off<128>(4 * g + (k & 3), k >> 2);
+        const float* src;
+        bool ok;
+        if (IS_A) {
+          ok = kok && gok[q];
+          src = ok ? p.a + (size_t)pix * p.K + mn0 + 4 * g : p.a;
+        } else {
+          int hi = hb + gr[q], wi = wb + gs[q];
+          ok = kok && gok[q] && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
+          src = ok ? p.b + (((size_t)n * p.H + hi) * p.W + wi) * p.C + gc[q] : p.b;
+        }
+        ptx::cp_async16(dst, src, ok ? 16 : 0);
       }
     }
   }
 };
+
+__device__ __forceinline__ float4 sel4v(const float4* u, int i) {  // u[i] without local memory
+  float4 a = (i & 1) ? u[1] : u[0];
+  float4 b = (i & 1) ? u[3] : u[2];
+  return (i & 2) ? b : a;
+}
+__device__ __forceinline__ float comp(const float4& v, int c) {
+  float a = (c & 1) ? v.y : v.x;
+  float b = (c & 1) ? v.w : v.z;
+  return (c & 2) ? b : a;
+}
+
+// In-place transpose of one 4x4 block (64 B at blk): chunk e holds pixel e's 4 channels on
+// entry and channel e's 4 pixels on exit. Accesses are rotated by `rot` (bank-conflict free
+// across an 8-lane phase). With X3 the residuals go to blk + delta.
+template <bool X3>
+__device__ __forceinline__ void transpose_block(uint32_t blk, int rot, uint32_t delta) {
+  float4 u[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int ce = (e + rot) & 3;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(u[e].x), "=f"(u[e].y), "=f"(u[e].z), "=f"(u[e].w)
+                 : "r"(blk + ce * 16));
+  }
+  // u[e] = chunk (e + rot) & 3  ->  chunk q = u[(q - rot) & 3]
+  float4 ch[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) ch[q] = sel4v(u, (q - rot) & 3);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int c = (e + rot) & 3;    // output row (channel) c
+    float x0 = comp(ch[0], c), x1 = comp(ch[1], c), x2 = comp(ch[2], c), x3 = comp(ch[3], c);
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(blk + c * 16), "f"(x0), "f"(x1), "f"(x2),
+                 "f"(x3)
+                 : "memory");
+    if (X3)
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(blk + delta + c * 16), "f"(tf32_resid(x0)),
+                   "f"(tf32_resid(x1)), "f"(tf32_resid(x2)), "f"(tf32_resid(x3))
+                   : "memory");
+  }
+}
 
 // ------------------------------------------------------------------------------- kernel
 // Butterfly transpose-reduce: on return lane l holds sum over the 32 lanes of v[l].
@@ -313,9 +342,10 @@ __device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
 //   warp 8    : TMEM allocator + single-thread MMA issuer.
 constexpr int NUM_THREADS_P = 288;      // 4 epilogue + 4 producer + 1 MMA warps
 constexpr int NUM_THREADS_X3 = 416;     // + 4 residual ("split") warps for 3xTF32
-// wgrad's producers write residuals themselves (register transpose), so it needs no split warps
+// the auxiliary warps 9-12 compute 3xTF32 residuals and / or transpose wgrad operands
+__host__ __device__ constexpr bool igemm_aux(int mode, bool x3) { return x3 || mode == CONV_WGRAD; }
 __host__ __device__ constexpr int igemm_threads(int mode, bool x3) {
-  return (x3 && mode != CONV_WGRAD) ? NUM_THREADS_X3 : NUM_THREADS_P;
+  return igemm_aux(mode, x3) ? NUM_THREADS_X3 : NUM_THREADS_P;
 }
 
 struct TileMap {
@@ -381,57 +411,24 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const
     const int ptid = tid - 128;
     if constexpr (MODE == CONV_WGRAD) {
       static_assert(BN == 128, "wgrad uses 128 x 128 tiles");
-      // flattened (tile, k-block) sequence with one block of register prefetch
-      int t = blockIdx.x, m0 = 0, n0 = 0, kb0 = 0, nkb = 0, kb = 0;
-      while (t < ntiles) {
+      WLoader<true> la;
+      WLoader<false> lb;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, n0, kb0, nkb;
         tm.decode(t, m0, n0, kb0, nkb, BN);
-        if (nkb > 0) break;
-        t += gridDim.x;
-      }
-      TLoader<true> la, na;
-      TLoader<false> lb, nb;
-      if (t < ntiles) {
         la.init(p, m0, ptid);
         lb.init(p, n0, ptid);
-        la.load(p, kb0);
-        lb.load(p, kb0);
-      }
-      int it = 0;
-      while (t < ntiles) {
-        // cursor of the next block
-        int t2 = t, kb2 = kb + 1, m2 = m0, n2 = n0, kb02 = kb0, nkb2 = nkb;
-        if (kb2 >= nkb2) {
-          kb2 = 0;
-          t2 += gridDim.x;
-          while (t2 < ntiles) {
-            tm.decode(t2, m2, n2, kb02, nkb2, BN);
-            if (nkb2 > 0) break;
-            t2 += gridDim.x;
-          }
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          int s = it % STAGES;
+          if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          uint32_t st = sbase + s * SM::STAGE_BYTES;
+          la.load(p, st, kb0 + kb);
+          lb.load(p, st + SM::A_BYTES, kb0 + kb);
+          ptx::cp_async_arrive_noinc(&rawfull[s]);
         }
-        if (t2 < ntiles) {
-          na.init(p, m2, ptid);
-          nb.init(p, n2, ptid);
-          na.load(p, kb02 + kb2);
-          nb.load(p, kb02 + kb2);
-        }
-        int s = it % STAGES;
-        if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        uint32_t st = sbase + s * SM::STAGE_BYTES;
-        la.template store<BM, X3>(st, SM::SMALL_OFF);
-        lb.template store<BN, X3>(st + SM::A_BYTES, SM::SMALL_OFF);
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&full[s]);
-        ++it;
-        la = na;
-        lb = nb;
-        t = t2;
-        kb = kb2;
-        m0 = m2;
-        n0 = n2;
-        kb0 = kb02;
-        nkb = nkb2;
       }
+      ptx::cp_async_wait<0>();
     } else {
       KLoader<MODE, BM, true> la;
       KLoader<MODE, BN, false> lb;
@@ -453,26 +450,35 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const
       }
       ptx::cp_async_wait<0>();
     }
-  } else if (X3 && warp >= 9) {
-    // ------------------------------------------------------------------ 3xTF32 residual warps
-    // For every stage: wait for the raw operands, write x - tf32(x) for all chunks of A and B
-    // (an element-wise pass, any partition works), publish to the async proxy, arrive full[].
-    if constexpr (X3 && MODE != CONV_WGRAD) {
-      const int stid = tid - 9 * 32;
-      constexpr int CHUNKS = (BM + BN) * BK / 4;  // 16-B chunks of A and B (contiguous)
-      int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int m0, n0, kb0, nkb;
-        tm.decode(t, m0, n0, kb0, nkb, BN);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          int s = it % STAGES;
-          ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
-          uint32_t st = sbase + s * SM::STAGE_BYTES;
+  } else if (igemm_aux(MODE, X3) && warp >= 9) {
+    // ------------------------------------------------------------------ auxiliary warps
+    // Per stage: wait for the raw operands, (wgrad) transpose every 4x4 block in place,
+    // (3xTF32) write x - tf32(x) of every chunk, publish to the async proxy, arrive full[].
+    const int stid = tid - 9 * 32;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int m0, n0, kb0, nkb;
+      tm.decode(t, m0, n0, kb0, nkb, BN);
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        int s = it % STAGES;
+        ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
+        uint32_t st = sbase + s * SM::STAGE_BYTES;
+        if constexpr (MODE == CONV_WGRAD) {
+          // 256 blocks in A (rows = Cout) and 256 in B (rows = R*S*C); block (g, j) = rows 4g..4g+3, k-chunk j
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            int bi = stid + 128 * (q & 1);
+            int g = bi & 31, j = bi >> 5;
+            uint32_t tile = st + (q < 2 ? 0 : SM::A_BYTES);
+            transpose_block<X3>(tile + kmaj_off<128>(4 * g, j), (stid >> 1) & 3, SM::SMALL_OFF);
+          }
+        } else {
+          constexpr int CHUNKS = (BM + BN) * BK / 4;  // 16-B chunks of A and B (contiguous)
 #pragma unroll 4
           for (int c = stid; c < CHUNKS; c += 128) split_chunk(st + c * 16, st + SM::SMALL_OFF + c * 16);
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&full[s]);
         }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&full[s]);
       }
     }
   } else if (warp == 8) {
