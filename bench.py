@@ -407,7 +407,8 @@ def families_table(fam, pk):
 def traffic_for(family):
     try:
         d = json.load(open(os.path.join(HERE, "profiles", "ncu_traffic.json")))
-        return d.get(family)
+        e = d.get(family)
+        return None if e is None else e["dram_bytes_per_launch"]
     except Exception:
         return None
 
