@@ -56,14 +56,16 @@ typedef enum {
   POOCH_STRAT_SWAP_ALL_NAIVE = 2,
   POOCH_STRAT_SWAP_ALL = 3,
   POOCH_STRAT_SWAP_OPT = 4,
-  POOCH_STRAT_SUPERNEURONS = 5, /* reserved (NEXT f1): returns POOCH_EUSAGE in this build */
+  POOCH_STRAT_SUPERNEURONS = 5, /* static rule of P:L395-400, scheduled with POOCH_SCHED_SN */
   POOCH_STRAT_EXHAUSTIVE = 6,
   POOCH_STRAT_FIXED = 7
 } pooch_strategy;
 
 /* Swap-in scheduling (Sec. 4.3): EAGER = "when there is room in the GPU memory";
  * NAIVE = starts with the computation just before its first user. */
-typedef enum { POOCH_SCHED_EAGER = 0, POOCH_SCHED_NAIVE = 1 } pooch_sched;
+typedef enum { POOCH_SCHED_EAGER = 0, POOCH_SCHED_NAIVE = 1, POOCH_SCHED_SN = 2 } pooch_sched;
+/* POOCH_SCHED_SN: SuperNeurons' rule, "each swap-in starts simultaneously with the computation
+ * of the immediately preceding convolution layer". */
 
 /* ------------------------------------------------------------------ network description */
 /* One fused executor task. A task's output is one feature map. */
@@ -193,6 +195,7 @@ typedef struct {
   uint64_t resident_bytes;
   uint64_t budget_bytes;
   int64_t tail_ns;
+  const uint8_t* is_conv;    /* nullable: 1 for convolution tasks (SuperNeurons rule only) */
 } pooch_problem;
 
 typedef struct {

@@ -33,7 +33,7 @@ from __future__ import annotations
 import itertools
 import math
 
-from .sim import EAGER, FREE, KEEP, NAIVE, RECOMPUTE, SWAP, simulate
+from .sim import EAGER, FREE, KEEP, NAIVE, RECOMPUTE, SN, SWAP, simulate
 
 INF = math.inf
 
@@ -155,6 +155,27 @@ def pooch(p, li_cap=16, sched=EAGER, log=None):
                 swap_opt_makespan=ms1)
 
 
+def superneurons(p):
+    """SuperNeurons' static hybrid rule as the paper describes it (Sec. 5.2):
+    "Feature maps are stored on GPU memory preferentially from output layer" (keep from the
+    sink down while resident + kept bytes fit the budget); "Among the feature maps
+    that do not fit ... the feature maps of convolution layer are targets of swapping. The
+    feature maps of layers with other types are recomputed"; swap-ins use the SN schedule.
+    Returns (cls, makespan or INF)."""
+    n = p.n
+    cls = [None] * n
+    kept = p.resident
+    for m in reversed(range(n)):
+        if kept + p.bytes[m] > p.budget:
+            break
+        cls[m] = KEEP
+        kept += p.bytes[m]
+    for m in range(n):
+        if cls[m] is None:
+            cls[m] = SWAP if (p.is_conv[m] or m == n - 1) else RECOMPUTE
+    return cls, _ms(p, cls, SN)
+
+
 def strategies(p, li_cap=16):
     """Makespans of the paper's comparison strategies (Sec. 5.1)."""
     n = p.n
@@ -166,4 +187,5 @@ def strategies(p, li_cap=16):
     out["swap_opt"] = ms1
     res = pooch(p, li_cap)
     out["pooch"] = res["makespan"]
+    out["superneurons"] = superneurons(p)[1]
     return out

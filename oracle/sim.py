@@ -32,7 +32,10 @@ Memory ledger (Reading 4): resident base R at t=0. Map m is allocated at
   A COMPUTE task whose allocation does not fit waits; if no lane can make
   progress the plan is out of memory (reported, not raised).
 
-Swap-in issue (Sec. 4.3): FIFO in need order, no bypass. Eager
+Swap-in issue (Sec. 4.3): FIFO in need order, no bypass. SuperNeurons
+  ("Each swap-in starts simultaneously with the computation of the
+  immediately preceding convolution layer"): once the last convolution
+  backward task before the map's first user has started. Eager
   ("simply executes swapping-in when there is room"): once every
   forward task has ended. Naive ("each swap-in simply
   starts simultaneously with the previous computation", Reading 8): once the
@@ -54,7 +57,7 @@ Outputs: makespan (last task end), peak bytes, OOM flag, per-map swap-in
 from __future__ import annotations
 
 KEEP, SWAP, RECOMPUTE, FREE = 0, 1, 2, 3   # FREE = zero-byte, zero-transfer keep (Eq. 1 baseline)
-EAGER, NAIVE = 0, 1
+EAGER, NAIVE, SN = 0, 1, 2     # SN: swap-in with the preceding convolution (SuperNeurons)
 
 
 class Profile:
@@ -62,7 +65,7 @@ class Profile:
     swap-out/in ns, graph (inputs, needs), resident base, budget, tail."""
 
     def __init__(self, fwd, bwd, nbytes, d2h, h2d, inputs, needs, resident=0,
-                 budget=1 << 62, rec=None, tail=0):
+                 budget=1 << 62, rec=None, tail=0, is_conv=None):
         self.n = len(fwd)
         self.fwd, self.bwd, self.bytes = list(fwd), list(bwd), list(nbytes)
         self.d2h, self.h2d = list(d2h), list(h2d)
@@ -70,6 +73,7 @@ class Profile:
         self.inputs = [[j for j in ins if j >= 0] for ins in inputs]
         self.needs = [sorted(set(nd)) for nd in needs]
         self.resident, self.budget, self.tail = resident, budget, tail
+        self.is_conv = [False] * self.n if is_conv is None else [bool(v) for v in is_conv]
         for i in range(self.n):
             assert all(j < i for j in self.inputs[i]), "inputs must be topological"
             assert self.fwd[i] > 0 and self.bwd[i] > 0 and self.rec[i] > 0
@@ -77,6 +81,8 @@ class Profile:
 
     @staticmethod
     def from_dict(d, **kw):
+        if "is_conv" in d and "is_conv" not in kw:
+            kw["is_conv"] = d["is_conv"]
         return Profile(d["fwd"], d["bwd"], d["bytes"], d["d2h"], d["h2d"], d["inputs"],
                        d["needs"], **kw)
 
@@ -193,6 +199,12 @@ def simulate(p: Profile, cls, sched=EAGER, budget=None) -> Result:
     fwd_done = 0
     fwd_end = None
 
+    def sn_trig(m):
+        for q in range(need[m] - 1, n - 1, -1):
+            if prog[q][0] == "B" and p.is_conv[prog[q][1]]:
+                return q
+        return n - 1
+
     def headroom(m):
         best, acc = 0, 0
         for q in range(pc, need[m] + 1):
@@ -247,6 +259,8 @@ def simulate(p: Profile, cls, sched=EAGER, budget=None) -> Result:
                 phase_ok = fwd_end is not None and fwd_end <= t
             else:
                 trig = need[m] - 1
+                if sched == SN:     # the backward task of the preceding convolution layer
+                    trig = sn_trig(m)
                 phase_ok = start_of[trig] is not None and start_of[trig] <= t
             if phase_ok and m in out_end and out_end[m] <= t and \
                     live + size[m] + headroom(m) <= budget:

@@ -634,6 +634,8 @@ static Problem make_problem(pooch_ctx* c, uint64_t budget) {
     p.inputs[t] = c->g.t[t].inputs;
     p.needs[t] = c->g.t[t].needs;
   }
+  p.is_conv.assign(n, 0);
+  for (int t = 0; t < n; ++t) p.is_conv[t] = c->g.t[t].kind == POOCH_L_CONV ? 1 : 0;
   p.resident = 0;
   p.budget = budget;
   p.tail = c->tail_ns;

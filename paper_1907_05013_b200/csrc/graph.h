@@ -36,6 +36,7 @@ struct Problem {
   std::vector<int64_t> fwd, bwd, rec, d2h, h2d;
   std::vector<uint64_t> bytes;
   std::vector<std::vector<int>> inputs, needs;
+  std::vector<uint8_t> is_conv;
   uint64_t resident = 0, budget = 0;
   int64_t tail = 0;
 };

@@ -265,8 +265,22 @@ pooch_status Planner::run(int strategy, const uint8_t* fixed, std::vector<uint8_
       }
       break;
     }
-    case POOCH_STRAT_SUPERNEURONS:
-      return fail(POOCH_EUSAGE, "STRAT_SUPERNEURONS is not built in this round (SURVEY 8(f) f1)");
+    case POOCH_STRAT_SUPERNEURONS: {
+      // keep from the output layer while resident + kept bytes fit;
+      // the rest: convolution outputs swap, others recompute; swap-in with the preceding conv.
+      cls.assign(n, 255);
+      uint64_t kept = p_.resident;
+      for (int m = n - 1; m >= 0; --m) {
+        if (kept + p_.bytes[m] > p_.budget) break;
+        cls[m] = C_KEEP;
+        kept += p_.bytes[m];
+      }
+      for (int m = 0; m < n; ++m)
+        if (cls[m] == 255) cls[m] = ((!p_.is_conv.empty() && p_.is_conv[m]) || m == n - 1) ? C_SWAP : C_RECOMPUTE;
+      sched_ = SCHED_SN;
+      makespan = ms(cls);
+      break;
+    }
     default:
       return fail(POOCH_EUSAGE, "unknown strategy %d", strategy);
   }
@@ -314,7 +328,7 @@ extern "C" pooch_status pooch_simulate(const pooch_problem* prob, const uint8_t*
   for (int i = 0; i < p.n; ++i)
     if (classes[i] > C_FREE) return fail(POOCH_EUSAGE, "class value out of range");
   SimOptions o;
-  o.sched = sched == POOCH_SCHED_NAIVE ? SCHED_NAIVE : SCHED_EAGER;
+  o.sched = sched == POOCH_SCHED_NAIVE ? SCHED_NAIVE : (sched == POOCH_SCHED_SN ? SCHED_SN : SCHED_EAGER);
   o.record_events = out->events_cap > 0;
   SimOut s;
   simulate(p, classes, o, s);

@@ -15,7 +15,9 @@ struct Decision {
 class Planner {
  public:
   Planner(const Problem& p, const pooch_search_cfg& cfg)
-      : p_(p), cfg_(cfg), sched_(cfg.sched == POOCH_SCHED_NAIVE ? SCHED_NAIVE : SCHED_EAGER) {}
+      : p_(p),
+        cfg_(cfg),
+        sched_(cfg.sched == POOCH_SCHED_NAIVE ? SCHED_NAIVE : (cfg.sched == POOCH_SCHED_SN ? SCHED_SN : SCHED_EAGER)) {}
   // Fills cls (empty when infeasible) and the simulated makespan (without tail).
   pooch_status run(int strategy, const uint8_t* fixed, std::vector<uint8_t>& cls, int64_t& makespan);
   void report(const std::vector<uint8_t>& cls, int64_t makespan, pooch_plan_report* r) const;

@@ -249,6 +249,14 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
         phase_ok = fwd_end >= 0 && fwd_end <= t;
       } else {
         int trig = s.need[m] - 1;
+        if (opt.sched == SCHED_SN) {  // the preceding convolution's backward task
+          trig = n - 1;
+          for (int q = s.need[m] - 1; q >= n; --q)
+            if (s.prog[q].kind == 'B' && !p.is_conv.empty() && p.is_conv[s.prog[q].id]) {
+              trig = q;
+              break;
+            }
+        }
         phase_ok = s.start_of[trig] >= 0 && s.start_of[trig] <= t;
       }
       if (phase_ok && s.out_end[m] >= 0 && s.out_end[m] <= t) {

@@ -10,7 +10,7 @@
 namespace pooch {
 
 enum : uint8_t { C_KEEP = 0, C_SWAP = 1, C_RECOMPUTE = 2, C_FREE = 3 };
-enum : int { SCHED_EAGER = 0, SCHED_NAIVE = 1 };
+enum : int { SCHED_EAGER = 0, SCHED_NAIVE = 1, SCHED_SN = 2 };
 
 struct SimEvent {
   int lane;   // 0 COMPUTE, 1 D2H, 2 H2D

@@ -12,7 +12,7 @@ import numpy as np
 from ._lib import P, PlanReport, Problem, SearchCfg, SimResult, check, lib
 
 KEEP, SWAP, RECOMPUTE, FREE = 0, 1, 2, 3
-EAGER, NAIVE = 0, 1
+EAGER, NAIVE, SN = 0, 1, 2
 STRATEGIES = {"pooch": 0, "incore": 1, "swap_all_naive": 2, "swap_all": 3, "swap_opt": 4,
               "superneurons": 5, "exhaustive": 6, "fixed": 7}
 
@@ -29,13 +29,14 @@ class PlanProblem:
     """Owns the arrays a pooch_problem points at."""
 
     def __init__(self, fwd, bwd, nbytes, d2h, h2d, inputs, needs, resident=0, budget=(1 << 62),
-                 rec=None, tail=0):
+                 rec=None, tail=0, is_conv=None):
         self.n = len(fwd)
         self._a = {
             "fwd": np.asarray(fwd, np.int64), "bwd": np.asarray(bwd, np.int64),
             "rec": np.asarray(fwd if rec is None else rec, np.int64),
             "d2h": np.asarray(d2h, np.int64), "h2d": np.asarray(h2d, np.int64),
             "bytes": np.asarray(nbytes, np.uint64),
+            "is_conv": np.asarray([0] * len(fwd) if is_conv is None else is_conv, np.uint8),
         }
         self._a["in_ptr"], self._a["in_idx"] = _csr([[j for j in l if j >= 0] for l in inputs])
         self._a["need_ptr"], self._a["need_idx"] = _csr(needs)
@@ -45,10 +46,12 @@ class PlanProblem:
                          a["h2d"].ctypes.data_as(P(C.c_int64)), a["bytes"].ctypes.data_as(P(C.c_uint64)),
                          a["in_ptr"].ctypes.data_as(P(C.c_int32)), a["in_idx"].ctypes.data_as(P(C.c_int32)),
                          a["need_ptr"].ctypes.data_as(P(C.c_int32)), a["need_idx"].ctypes.data_as(P(C.c_int32)),
-                         int(resident), int(budget), int(tail))
+                         int(resident), int(budget), int(tail), a["is_conv"].ctypes.data_as(P(C.c_uint8)))
 
     @staticmethod
     def from_dict(d, **kw):
+        if "is_conv" in d and "is_conv" not in kw:
+            kw["is_conv"] = d["is_conv"]
         return PlanProblem(d["fwd"], d["bwd"], d["bytes"], d["d2h"], d["h2d"], d["inputs"], d["needs"], **kw)
 
     def simulate(self, classes, sched=EAGER, events=False):

@@ -63,8 +63,6 @@ def test_plan_problem_errors():
     from paper_1907_05013_b200 import _lib
     with pytest.raises(_lib.PoochError):
         p.plan("exhaustive")                        # n > 12 is a usage error
-    with pytest.raises(_lib.PoochError):
-        p.plan("superneurons")                      # not built this round
     p2 = PlanProblem([1, 1], [1, 1], [4, 4], [1, 1], [1, 1], [[], [0]], [[0], [0, 1]], resident=10, budget=12)
     cls, rep = p2.plan("pooch")
     assert cls is None and rep.feasible == 0        # nothing fits: EINFEASIBLE

@@ -136,3 +136,38 @@ def test_resnet50_profile_parity_small_cap(link):
     ref = OP.pooch(po, li_cap=3)
     cls, rep = pc.plan("pooch", li_cap=3)
     assert cls == (ref["cls"] if ref["feasible"] else None)
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_superneurons_sched_differential(seed):
+    g = synthdata.rng(900 + seed)
+    n = int(g.integers(2, 9))
+    d = synthdata.random_profile(n, seed, dag=seed % 2 == 0)
+    d["is_conv"] = [int(v) for v in g.integers(0, 2, n)]
+    budget = int(10 + sum(d["bytes"]) * g.uniform(0.3, 1.6))
+    po, pc = both(d, resident=10, budget=budget)
+    for _ in range(6):
+        cls = [int(c) for c in g.integers(0, 3, n)]
+        cls[-1] = min(cls[-1], OS.SWAP)
+        _cmp_sim(po, pc, cls, OS.SN)
+    ref_cls, ref_ms = OP.superneurons(po)
+    cls, rep = pc.plan("superneurons")
+    if ref_ms == OP.INF:
+        assert cls is None
+    else:
+        assert cls == ref_cls and rep.makespan_ns == ref_ms
+
+
+def test_superneurons_rule_on_resnet50_census():
+    """Table 3's SuperNeurons row has the same counts on both machines:
+    the rule depends only on sizes and layer types, never on the link."""
+    net = nets.resnet50()
+    counts = []
+    for link in (16.0, 75.0):
+        d = _net_profile(net, 512, link, 0)
+        d["is_conv"] = [int(t.kind == "conv") for t in net.tasks]
+        po = OS.Profile.from_dict(d, resident=2_000_000_000, budget=16_000_000_000)
+        cls, _ = OP.superneurons(po)
+        counts.append((cls.count(OS.KEEP), cls.count(OS.SWAP), cls.count(OS.RECOMPUTE)))
+    assert counts[0] == counts[1]
+    assert sum(counts[0]) == 105
