@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-incore", action="store_true", help="skip the in-core comparison run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--profile-iters", type=int, default=2)
+    ap.add_argument("--ablation", action="store_true",
+                    help="also run the paper's strategies (Sec. 5.1-5.2) on the same executor and report each")
     ap.add_argument("--ncu-step", action="store_true",
                     help="profile/plan, 1 warm-up step, then exactly one step inside cudaProfilerStart/Stop "
                          "(for ncu --profile-from-start off); prints nothing")
@@ -191,10 +193,12 @@ def our_arm(args):
         budget = int(free - (3 << 30))
     budget = budget // 256 * 256
     maps_total = sum(ctx_map_bytes(ctx))
-    host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.8 * os.sysconf("SC_PAGE_SIZE") *
+    host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.75 * os.sysconf("SC_PAGE_SIZE") *
                          os.sysconf("SC_PHYS_PAGES") / max(1, world)))
+    host_bytes = host_bytes // 4096 * 4096
     dev = torch.empty(budget, dtype=torch.uint8, device="cuda")
-    host = torch.empty(host_bytes, dtype=torch.uint8, pin_memory=True)
+    from paper_1907_05013_b200.executor import PinnedHost
+    host = PinnedHost(host_bytes)
     streams = [torch.cuda.Stream() for _ in range(3)]
     ctx.set_budget(dev, budget, host, host_bytes)
     ctx.set_streams(*streams)
@@ -288,6 +292,22 @@ def our_arm(args):
     ctx.set_timing(False)
     launches = kernel_launches(ctx, args.steps)
 
+    ablation = None
+    if args.ablation:
+        ablation = {}
+        for strat in ("swap_all_naive", "swap_all", "swap_opt", "superneurons", "pooch"):
+            try:
+                c2, r2 = ctx.plan(strat, li_cap=args.li_cap)
+            except Exception as e:  # infeasible plans are a result (superneurons OOM)
+                ablation[strat] = {"feasible": False, "why": str(e)[:160]}
+                continue
+            ctx.train_step(0.01, sync_loss=False)
+            ms_s = timed(2)
+            ablation[strat] = {"feasible": True, "ms_per_step": ms_s, "images_per_s": batch * world * 1000.0 / ms_s,
+                               "simulated_ms": r2["makespan_ns"] / 1e6,
+                               "counts": [c2.count(0), c2.count(1), c2.count(2)]}
+        ctx.plan("pooch", li_cap=args.li_cap)
+
     # ---- in-core comparison (the same kernels, every map kept) where it fits
     incore = None
     if not args.no_incore and world == 1:
@@ -316,6 +336,8 @@ def our_arm(args):
         "swap": swap_stats(fam, prof),
         "families": families_table(fam, peaks()),
     }
+    if ablation is not None:
+        line["ablation"] = ablation
     if incore is not None:
         line["incore"] = incore
         if incore.get("images_per_s"):

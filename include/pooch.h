@@ -247,6 +247,16 @@ pooch_status pooch_plan_problem(const pooch_problem* prob, int32_t strategy, con
                                 const uint8_t* fixed_classes, uint8_t* classes_out,
                                 pooch_plan_report* report);
 
+/* Static arena offsets (replaces the paper's hooked allocator): simulate `classes`,
+ * replay the allocation ledger best-fit over [0, capacity). Buffer instances b in [0, 3n):
+ * b = m forward instance of map m, n + m its backward-phase (swapped-in / recomputed)
+ * instance, 2n + m its gradient. Outputs (host arrays of 3n, nullable except offsets):
+ * byte offsets, ledger positions of allocation / free (-1 = never allocated / never freed),
+ * sizes. POOCH_EINFEASIBLE on OOM or fragmentation. Host only. */
+pooch_status pooch_pack_problem(const pooch_problem* prob, const uint8_t* classes, int32_t sched, uint64_t capacity,
+                                uint64_t* offsets, int32_t* alloc_seq, int32_t* free_seq, uint64_t* sizes,
+                                uint64_t* high_water);
+
 /* ------------------------------------------------------------------------- execution */
 /* Plans the context's network with its profile and budget, packs static arena offsets and
  * compiles the three-stream schedule. classes_out (nullable, n bytes) receives the plan. */

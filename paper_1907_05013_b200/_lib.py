@@ -95,6 +95,8 @@ SIGNATURES = {
     "pooch_set_profile": (c_i32, [c_vp, P(c_i64), P(c_i64), P(c_i64), P(c_i64), P(c_i64), c_i64]),
     "pooch_simulate": (c_i32, [P(Problem), P(C.c_uint8), c_i32, P(SimResult)]),
     "pooch_plan_problem": (c_i32, [P(Problem), c_i32, P(SearchCfg), P(C.c_uint8), P(C.c_uint8), P(PlanReport)]),
+    "pooch_pack_problem": (c_i32, [P(Problem), P(C.c_uint8), c_i32, c_u64, P(c_u64), P(c_i32), P(c_i32), P(c_u64),
+                                   P(c_u64)]),
     "pooch_plan": (c_i32, [c_vp, c_i32, P(SearchCfg), P(C.c_uint8), P(C.c_uint8), P(PlanReport)]),
     "pooch_train_step": (c_i32, [c_vp, c_f32, P(c_f32)]),
     "pooch_set_timing": (c_i32, [c_vp, c_i32]),

@@ -48,7 +48,9 @@ struct Op {
   char kind;  // 'F','R','B','O','I'
   int id;
   std::vector<int> waits;  // op indices on other lanes whose completion event must be waited
-  bool record = false;     // another lane waits on this op
+  bool record = false;     // another lane waits on this op's completion
+  bool record_start = false;  // another lane waits on this op's start (naive / SN swap-in triggers)
+  std::vector<int> start_waits;  // compute ops whose START must precede this op
 };
 
 struct pooch_ctx_impl;
@@ -94,6 +96,8 @@ struct pooch_ctx {
   std::vector<int> first_writer;  // per map: task whose bwd writes (not accumulates) its gradient
   // events
   std::vector<cudaEvent_t> ev;    // one per op (sync events)
+  std::vector<cudaEvent_t> ev_start;  // start events (only for ops with record_start)
+  int sched = 0;                  // swap-in schedule of the current plan
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> tev;   // timing events

@@ -506,6 +506,7 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
 extern "C" void pooch_destroy(pooch_ctx* c) {
   if (!c) return;
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto e : c->ev_start) cudaEventDestroy(e);
   for (auto e : c->tev) cudaEventDestroy(e);
   if (c->nccl && g_nccl.commDestroy) g_nccl.commDestroy(c->nccl);
   if (c->own_streams)
@@ -643,59 +644,68 @@ static Problem make_problem(pooch_ctx* c, uint64_t budget) {
 }
 
 // Best-fit replay of the simulated ledger; fills c->buf_off. false on fragmentation.
-static bool pack(pooch_ctx* c, const SimOut& so, uint64_t cap, std::vector<int>& alloc_op_buf) {
-  const int n = c->g.n();
-  c->buf_off.assign(3 * n, 0);
-  std::map<size_t, size_t> freel;  // offset -> length
+// Best-fit (address-ordered ties) replay of the simulated allocation ledger over [0, cap).
+// off[b] receives the region of every buffer instance b; false on fragmentation.
+bool pack_ledger(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap, bool no_reuse,
+                 std::vector<uint64_t>& off, uint64_t& high) {
+  off.assign(nbuf, 0);
+  std::map<uint64_t, uint64_t> freel;  // offset -> length
   freel[0] = cap;
-  std::vector<size_t> sz(3 * n, 0);
-  uint64_t high = 0;
-  const bool no_reuse = getenv("POOCH_DEBUG_NO_REUSE") != nullptr;  // debug: every buffer its own region
-  size_t bump = 0;
-  for (const LedgerEntry& e : so.ledger) {
-    if (e.alloc && no_reuse) {
-      size_t need = align_up(std::max<uint64_t>(e.bytes, 1));
+  std::vector<uint64_t> sz(nbuf, 0);
+  high = 0;
+  uint64_t bump = 0;
+  for (const LedgerEntry& e : ledger) {
+    if (no_reuse) {  // debug: every buffer its own region
+      if (!e.alloc) continue;
+      uint64_t need = align_up(std::max<uint64_t>(e.bytes, 1));
       if (bump + need > cap) return false;
-      c->buf_off[e.buf] = bump;
+      off[e.buf] = bump;
       sz[e.buf] = need;
       bump += need;
       high = bump;
       continue;
     }
-    if (!e.alloc && no_reuse) continue;
     if (e.alloc) {
-      size_t need = align_up(std::max<uint64_t>(e.bytes, 1));
+      uint64_t need = align_up(std::max<uint64_t>(e.bytes, 1));
       auto best = freel.end();
       for (auto it = freel.begin(); it != freel.end(); ++it)
         if (it->second >= need && (best == freel.end() || it->second < best->second)) best = it;
       if (best == freel.end()) return false;
-      size_t off = best->first, len = best->second;
+      uint64_t o = best->first, len = best->second;
       freel.erase(best);
-      if (len > need) freel[off + need] = len - need;
-      c->buf_off[e.buf] = off;
+      if (len > need) freel[o + need] = len - need;
+      off[e.buf] = o;
       sz[e.buf] = need;
-      high = std::max<uint64_t>(high, off + need);
+      high = std::max<uint64_t>(high, o + need);
     } else {
-      size_t off = c->buf_off[e.buf], len = sz[e.buf];
-      auto nx = freel.lower_bound(off);
-      if (nx != freel.end() && nx->first == off + len) {
+      uint64_t o = off[e.buf], len = sz[e.buf];
+      auto nx = freel.lower_bound(o);
+      if (nx != freel.end() && nx->first == o + len) {
         len += nx->second;
         freel.erase(nx);
       }
-      auto pv = freel.lower_bound(off);
+      auto pv = freel.lower_bound(o);
       if (pv != freel.begin()) {
         --pv;
-        if (pv->first + pv->second == off) {
-          off = pv->first;
+        if (pv->first + pv->second == o) {
+          o = pv->first;
           len += pv->second;
           freel.erase(pv);
         }
       }
-      freel[off] = len;
+      freel[o] = len;
     }
   }
+  return true;
+}
+
+static bool pack(pooch_ctx* c, const SimOut& so, uint64_t cap, std::vector<int>& alloc_op_buf) {
   (void)alloc_op_buf;
-  for (size_t b = 0; b < c->buf_off.size(); ++b) c->buf_off[b] += c->resident_end;  // arena offsets
+  std::vector<uint64_t> off;
+  uint64_t high;
+  if (!pack_ledger(so.ledger, 3 * c->g.n(), cap, getenv("POOCH_DEBUG_NO_REUSE") != nullptr, off, high)) return false;
+  c->buf_off.assign(off.size(), 0);
+  for (size_t b = 0; b < off.size(); ++b) c->buf_off[b] = c->resident_end + off[b];  // arena offsets
   c->arena_high = high;
   return true;
 }
@@ -734,6 +744,39 @@ static void compile(pooch_ctx* c, const SimOut& so) {
       const std::vector<int>& reads = o.kind == 'B' ? c->g.t[o.id].needs : c->g.t[o.id].inputs;
       for (int m : reads)
         if (c->cls[m] == C_SWAP) add_wait(i, opof('I', m));
+    }
+  }
+  // swap-in issue policy (Sec. 4.3): eager = not before the forward pass has ended; naive / SN =
+  // not before the trigger compute task (the one before the first user / the preceding conv)
+  // has started -- the same rule the simulator applied
+  {
+    std::vector<int> need(n, -1);
+    const int P = (int)c->program.size();
+    for (int q = n; q < P; ++q) {
+      const ProgTask& t = c->program[q];
+      const std::vector<int>& reads = t.kind == 'B' ? c->g.t[t.id].needs : c->g.t[t.id].inputs;
+      for (int m : reads)
+        if (need[m] < 0) need[m] = q;
+    }
+    for (int i = 0; i < (int)c->ops.size(); ++i) {
+      Op& o = c->ops[i];
+      if (o.kind != 'I') continue;
+      if (c->sched == SCHED_EAGER) {
+        add_wait(i, opof('F', n - 1));
+        continue;
+      }
+      int trig = need[o.id] - 1;
+      if (c->sched == SCHED_SN) {
+        trig = n - 1;
+        for (int q = need[o.id] - 1; q >= n; --q)
+          if (c->program[q].kind == 'B' && c->g.t[c->program[q].id].kind == POOCH_L_CONV) {
+            trig = q;
+            break;
+          }
+      }
+      int top = opof(c->program[trig].kind, c->program[trig].id);
+      o.start_waits.push_back(top);
+      c->ops[top].record_start = true;
     }
   }
   // region reuse: most recent occupant per byte (painted intervals) -> wait on its freeing op
@@ -817,8 +860,9 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
     std::vector<int> dummy;
     c->cls = cls;
     if (!so.oom && pack(c, so, cap, dummy)) {
-      compile(c, so);
       c->program = so.program;
+      c->sched = pl.sched();
+      compile(c, so);
       c->host_off.assign(n, 0);
       size_t ho = 0;
       for (int m = 0; m < n; ++m)
@@ -826,11 +870,16 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
           c->host_off[m] = ho;
           ho += align_up(c->map_bytes[m]);
         }
-      // events: one sync event per op
+      // events: one sync event per op (+ start events)
       while (c->ev.size() < c->ops.size()) {
         cudaEvent_t e;
         POOCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->ev.push_back(e);
+      }
+      while (c->ev_start.size() < c->ops.size()) {
+        cudaEvent_t e;
+        POOCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_start.push_back(e);
       }
       c->have_plan = true;
       pl.report(cls, mk, report);
@@ -915,6 +964,8 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
     const Op& o = c->ops[i];
     cudaStream_t st = c->s[o.lane];
     for (int w : o.waits) POOCH_CUDA(cudaStreamWaitEvent(st, c->ev[w], 0));
+    for (int w : o.start_waits) POOCH_CUDA(cudaStreamWaitEvent(st, c->ev_start[w], 0));
+    if (o.record_start) POOCH_CUDA(cudaEventRecord(c->ev_start[i], st));
     if (timing && o.lane != 0) {
       copy_ev[i].first = lt.get();
       POOCH_CUDA(cudaEventRecord(copy_ev[i].first, st));
@@ -1257,5 +1308,42 @@ extern "C" pooch_status pooch_set_precision(pooch_ctx* c, int32_t precision) {
   c->precision = precision;
   c->have_profile = false;
   c->have_plan = false;
+  return POOCH_OK;
+}
+
+// host-only: the static offsets the executor would use (a6), for tests
+extern "C" pooch_status pooch_pack_problem(const pooch_problem* prob, const uint8_t* classes, int32_t sched,
+                                           uint64_t capacity, uint64_t* offsets, int32_t* alloc_seq,
+                                           int32_t* free_seq, uint64_t* sizes, uint64_t* high_water) {
+  if (!prob || !classes || !offsets || !high_water) return fail(POOCH_EUSAGE, "null argument");
+  Problem p;
+  std::string err;
+  if (!problem_from_c(*prob, p, err)) return fail(POOCH_EUSAGE, "%s", err.c_str());
+  SimOptions o;
+  o.sched = sched == POOCH_SCHED_NAIVE ? SCHED_NAIVE : (sched == POOCH_SCHED_SN ? SCHED_SN : SCHED_EAGER);
+  o.record_ledger = true;
+  SimOut so;
+  simulate(p, classes, o, so);
+  if (so.oom) return fail(POOCH_EINFEASIBLE, "classification runs out of memory");
+  std::vector<uint64_t> off;
+  uint64_t high;
+  const int nb = 3 * p.n;
+  if (!pack_ledger(so.ledger, nb, capacity, false, off, high)) return fail(POOCH_EINFEASIBLE, "fragmentation");
+  for (int b = 0; b < nb; ++b) {
+    offsets[b] = off[b];
+    if (alloc_seq) alloc_seq[b] = -1;
+    if (free_seq) free_seq[b] = -1;
+    if (sizes) sizes[b] = 0;
+  }
+  for (size_t k = 0; k < so.ledger.size(); ++k) {
+    const LedgerEntry& e = so.ledger[k];
+    if (e.alloc) {
+      if (alloc_seq) alloc_seq[e.buf] = (int32_t)k;
+      if (sizes) sizes[e.buf] = e.bytes;
+    } else if (free_seq) {
+      free_seq[e.buf] = (int32_t)k;
+    }
+  }
+  *high_water = high;
   return POOCH_OK;
 }

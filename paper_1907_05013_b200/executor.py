@@ -29,6 +29,33 @@ def build_net(name: str, in_hw: int, classes: int, width: int = 32):
     return arr
 
 
+class PinnedHost:
+    """Page-locked host arena of exactly `nbytes` (numpy pages registered with
+    cudaHostRegister; torch's pinned allocator rounds up to a power of two, which
+    turns 157 GB into 256 GB). The caller owns it (pooch_set_budget's host arena)."""
+
+    def __init__(self, nbytes: int):
+        import torch
+        self.nbytes = int(nbytes)
+        self.buf = np.empty(self.nbytes, np.uint8)
+        self.cudart = torch.cuda.cudart()
+        err = self.cudart.cudaHostRegister(self.buf.ctypes.data, self.nbytes, 0)
+        if int(err) != 0:
+            raise RuntimeError("cudaHostRegister(%d bytes) failed: %s" % (self.nbytes, err))
+
+    def data_ptr(self):
+        return self.buf.ctypes.data
+
+    def numel(self):
+        return self.nbytes
+
+    def __del__(self):
+        try:
+            self.cudart.cudaHostUnregister(self.buf.ctypes.data)
+        except Exception:
+            pass
+
+
 def _ptr(x):
     """Raw address of a torch tensor / int / None."""
     if x is None:

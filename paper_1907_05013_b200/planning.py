@@ -97,3 +97,20 @@ class PlanProblem:
             return None, rep
         check(st)
         return [int(c) for c in out], rep
+
+    def pack(self, classes, capacity, sched=EAGER):
+        """Static offsets of every buffer instance (pooch_pack_problem); None if infeasible."""
+        nb = 3 * self.n
+        cls = np.asarray(classes, np.uint8)
+        off = np.zeros(nb, np.uint64)
+        a = np.zeros(nb, np.int32)
+        f = np.zeros(nb, np.int32)
+        sz = np.zeros(nb, np.uint64)
+        hw = C.c_uint64()
+        st = lib.pooch_pack_problem(C.byref(self.c), cls.ctypes.data_as(P(C.c_uint8)), sched, int(capacity),
+                                    off.ctypes.data_as(P(C.c_uint64)), a.ctypes.data_as(P(C.c_int32)),
+                                    f.ctypes.data_as(P(C.c_int32)), sz.ctypes.data_as(P(C.c_uint64)), C.byref(hw))
+        if st == 2:
+            return None
+        check(st)
+        return dict(offsets=off, alloc=a, free=f, sizes=sz, high_water=hw.value)
