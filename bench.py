@@ -193,12 +193,19 @@ def our_arm(args):
         budget = int(free - (3 << 30))
     budget = budget // 256 * 256
     maps_total = sum(ctx_map_bytes(ctx))
-    host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.75 * os.sysconf("SC_PAGE_SIZE") *
+    host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.6 * os.sysconf("SC_PAGE_SIZE") *
                          os.sysconf("SC_PHYS_PAGES") / max(1, world)))
     host_bytes = host_bytes // 4096 * 4096
     dev = torch.empty(budget, dtype=torch.uint8, device="cuda")
     from paper_1907_05013_b200.executor import PinnedHost
-    host = PinnedHost(host_bytes)
+    while True:  # the host may cap page-locked memory: halve until registration succeeds
+        try:
+            host = PinnedHost(host_bytes)
+            break
+        except RuntimeError:
+            if host_bytes < (8 << 30):
+                raise
+            host_bytes = host_bytes // 2 // 4096 * 4096
     streams = [torch.cuda.Stream() for _ in range(3)]
     ctx.set_budget(dev, budget, host, host_bytes)
     ctx.set_streams(*streams)

@@ -196,6 +196,7 @@ typedef struct {
   uint64_t budget_bytes;
   int64_t tail_ns;
   const uint8_t* is_conv;    /* nullable: 1 for convolution tasks (SuperNeurons rule only) */
+  uint64_t host_budget_bytes; /* pinned host bytes for the swap class; 0 = unlimited */
 } pooch_problem;
 
 typedef struct {

@@ -70,10 +70,30 @@ def _ms(p, cls, sched=EAGER):
     return INF if r.oom else r.makespan
 
 
+def host_fit_base(p):
+    """Step 1's starting point. The paper starts from all-swap; when the swap class
+    of all-swap exceeds the pinned host arena (Reading 37) the swap maps with the cheapest
+    replay per byte (recompute time / bytes; ties: larger bytes, smaller id; never the sink)
+    move to recompute until the swap class fits."""
+    n = p.n
+    cls = [SWAP] * n
+    if p.host_budget is None:
+        return cls
+    total = sum(p.bytes)
+    order = sorted(range(n - 1), key=lambda m: (p.rec[m] / max(p.bytes[m], 1), -p.bytes[m], m))
+    for m in order:
+        if total <= p.host_budget:
+            break
+        cls[m] = RECOMPUTE
+        total -= p.bytes[m]
+    return cls
+
+
 def step1(p, li_cap=16, sched=EAGER, log=None):
     """Keep/swap search (Sec. 4.4.2). Returns (cls, makespan, n_sims)."""
     n = p.n
-    base = simulate(p, [SWAP] * n, sched)
+    start = host_fit_base(p)
+    base = simulate(p, start, sched)
     if base.oom:
         return None, INF, 1
     sims = 1
@@ -82,9 +102,9 @@ def step1(p, li_cap=16, sched=EAGER, log=None):
     tree = sorted(ranked[:li_cap])
     overflow = ranked[li_cap:]
     scan = sorted((L_O - set(tree)) | set(overflow), reverse=True)
-    best = _key(base.makespan, [SWAP] * n)
+    best = _key(base.makespan, start)
     for leaf in range(1 << len(tree)):
-        cls = [SWAP] * n
+        cls = list(start)
         for b, m in enumerate(tree):
             if leaf >> b & 1:
                 cls[m] = KEEP

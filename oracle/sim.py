@@ -65,7 +65,7 @@ class Profile:
     swap-out/in ns, graph (inputs, needs), resident base, budget, tail."""
 
     def __init__(self, fwd, bwd, nbytes, d2h, h2d, inputs, needs, resident=0,
-                 budget=1 << 62, rec=None, tail=0, is_conv=None):
+                 budget=1 << 62, rec=None, tail=0, is_conv=None, host_budget=None):
         self.n = len(fwd)
         self.fwd, self.bwd, self.bytes = list(fwd), list(bwd), list(nbytes)
         self.d2h, self.h2d = list(d2h), list(h2d)
@@ -74,6 +74,7 @@ class Profile:
         self.needs = [sorted(set(nd)) for nd in needs]
         self.resident, self.budget, self.tail = resident, budget, tail
         self.is_conv = [False] * self.n if is_conv is None else [bool(v) for v in is_conv]
+        self.host_budget = host_budget      # pinned host bytes for the swap class (None: unlimited)
         for i in range(self.n):
             assert all(j < i for j in self.inputs[i]), "inputs must be topological"
             assert self.fwd[i] > 0 and self.bwd[i] > 0 and self.rec[i] > 0
@@ -178,6 +179,10 @@ def simulate(p: Profile, cls, sched=EAGER, budget=None) -> Result:
         return p.fwd[i] if kind == "F" else (p.rec[i] if kind == "R" else p.bwd[i])
 
     fifo = sorted([m for m in range(n) if is_swap[m]], key=lambda m: (need[m], m))
+    if p.host_budget is not None and sum(p.bytes[m] for m in fifo) > p.host_budget:
+        res = Result()                     # the swap class does not fit the host arena (Reading 36)
+        res.oom = True
+        return res
     ready_at = [[] for _ in range(n)]          # swap maps whose swap-out may start after F(q)
     for m in range(n):
         if is_swap[m]:

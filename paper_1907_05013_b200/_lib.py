@@ -56,7 +56,8 @@ class Problem(C.Structure):
     _fields_ = [("n", c_i32), ("fwd_ns", P(c_i64)), ("bwd_ns", P(c_i64)), ("rec_ns", P(c_i64)),
                 ("d2h_ns", P(c_i64)), ("h2d_ns", P(c_i64)), ("bytes", P(c_u64)),
                 ("in_ptr", P(c_i32)), ("in_idx", P(c_i32)), ("need_ptr", P(c_i32)), ("need_idx", P(c_i32)),
-                ("resident_bytes", c_u64), ("budget_bytes", c_u64), ("tail_ns", c_i64), ("is_conv", P(C.c_uint8))]
+                ("resident_bytes", c_u64), ("budget_bytes", c_u64), ("tail_ns", c_i64), ("is_conv", P(C.c_uint8)),
+                ("host_budget_bytes", c_u64)]
 
 
 class SimResult(C.Structure):

@@ -640,6 +640,8 @@ static Problem make_problem(pooch_ctx* c, uint64_t budget) {
   p.resident = 0;
   p.budget = budget;
   p.tail = c->tail_ns;
+  // pinned host arena (each swapped map padded to 256 B); 1 = no host arena at all
+  p.host_budget = c->host_bytes > (uint64_t)n * 256 ? c->host_bytes - (uint64_t)n * 256 : 1;
   return p;
 }
 

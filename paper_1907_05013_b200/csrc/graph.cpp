@@ -212,6 +212,7 @@ bool problem_from_c(const pooch_problem& p, Problem& o, std::string& err) {
   o.resident = p.resident_bytes;
   o.budget = p.budget_bytes;
   o.tail = p.tail_ns;
+  o.host_budget = p.host_budget_bytes;
   o.is_conv.assign(p.n, 0);
   if (p.is_conv)
     for (int i = 0; i < p.n; ++i) o.is_conv[i] = p.is_conv[i] ? 1 : 0;

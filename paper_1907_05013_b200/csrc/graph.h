@@ -38,6 +38,7 @@ struct Problem {
   std::vector<std::vector<int>> inputs, needs;
   std::vector<uint8_t> is_conv;
   uint64_t resident = 0, budget = 0;
+  uint64_t host_budget = 0;  // 0: unlimited
   int64_t tail = 0;
 };
 

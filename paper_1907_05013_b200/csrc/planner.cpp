@@ -64,9 +64,35 @@ int64_t Planner::ms(const std::vector<uint8_t>& cls) {
   return sim_makespan(p_, cls, sched_);
 }
 
+// Step 1's starting point: all-swap, or -- when its swap class exceeds the pinned
+// host arena (Reading 37) -- all-swap with the cheapest-to-replay maps (recompute ns per byte;
+// ties: larger bytes, smaller id; never the sink) moved to recompute until it fits.
+static std::vector<uint8_t> host_fit_base(const Problem& p) {
+  const int n = p.n;
+  std::vector<uint8_t> cls(n, C_SWAP);
+  if (p.host_budget == 0) return cls;
+  uint64_t total = 0;
+  for (int m = 0; m < n; ++m) total += p.bytes[m];
+  std::vector<int> order;
+  for (int m = 0; m + 1 < n; ++m) order.push_back(m);
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    double ra = (double)p.rec[a] / (double)std::max<uint64_t>(p.bytes[a], 1);
+    double rb = (double)p.rec[b] / (double)std::max<uint64_t>(p.bytes[b], 1);
+    if (ra != rb) return ra < rb;
+    if (p.bytes[a] != p.bytes[b]) return p.bytes[a] > p.bytes[b];
+    return a < b;
+  });
+  for (int m : order) {
+    if (total <= p.host_budget) break;
+    cls[m] = C_RECOMPUTE;
+    total -= p.bytes[m];
+  }
+  return cls;
+}
+
 bool Planner::step1(std::vector<uint8_t>& best_cls, int64_t& best_ms) {
   const int n = p_.n;
-  std::vector<uint8_t> all_swap(n, C_SWAP);
+  std::vector<uint8_t> all_swap = host_fit_base(p_);
   SimOptions o;
   o.sched = sched_;
   SimOut base;
@@ -103,7 +129,7 @@ bool Planner::step1(std::vector<uint8_t>& best_cls, int64_t& best_ms) {
   std::vector<Key> leaf_best((size_t)leaves);
   std::vector<int64_t> leaf_sims((size_t)leaves, 0);
   parallel_for((int)leaves, T, [&](int leaf) {
-    std::vector<uint8_t> cls(n, C_SWAP);
+    std::vector<uint8_t> cls = all_swap;
     for (size_t b = 0; b < tree.size(); ++b)
       if ((leaf >> b) & 1) cls[tree[b]] = C_KEEP;
     Key kb{INT64_MAX, INT_MAX, {}};

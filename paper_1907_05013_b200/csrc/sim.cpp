@@ -155,6 +155,14 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
   std::sort(s.fifo.begin(), s.fifo.end(), [&](int a, int b) {
     return s.need[a] != s.need[b] ? s.need[a] < s.need[b] : a < b;
   });
+  if (p.host_budget > 0) {  // the swap class must fit the pinned host arena (Reading 36)
+    uint64_t hb = 0;
+    for (int m : s.fifo) hb += p.bytes[m];
+    if (hb > p.host_budget) {
+      out.oom = true;
+      return;
+    }
+  }
   s.ready_at.assign(n, {});
   for (int m = 0; m < n; ++m)
     if (s.is_swap[m]) s.ready_at[s.last_fwd[m]].push_back(m);

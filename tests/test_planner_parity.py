@@ -171,3 +171,18 @@ def test_superneurons_rule_on_resnet50_census():
         counts.append((cls.count(OS.KEEP), cls.count(OS.SWAP), cls.count(OS.RECOMPUTE)))
     assert counts[0] == counts[1]
     assert sum(counts[0]) == 105
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_host_budget_limits_swap_class(seed):
+    d, budget = _tight(seed, 8)
+    hb = sum(d["bytes"]) // 3
+    po, pc = both(d, resident=10, budget=budget, host_budget=hb)
+    ref = OP.pooch(po, li_cap=16)
+    cls, rep = pc.plan("pooch")
+    if not ref["feasible"]:
+        assert cls is None
+        return
+    assert cls == ref["cls"]
+    assert sum(d["bytes"][m] for m in range(8) if cls[m] == OS.SWAP) <= hb
+    assert pc.simulate([OS.SWAP] * 8)["oom"]          # all-swap needs more host memory than hb
