@@ -302,7 +302,7 @@ pooch_status pooch_family_stats(pooch_ctx* ctx, int32_t family, double* time_ms,
 /* Single convolution passes on caller device buffers, launched on `stream` (cudaStream_t).
  * Used by the parity tests; the executor calls the same launchers.
  *   fwd  : y[N,Ho,Wo,K] = conv(x[N,H,W,C], w[K,R,S,C]); stat_sum/stat_sq (nullable) receive
- *          per-128-row-tile column sums [ceil(N*Ho*Wo/128)][K].
+ *          per-M-tile column sums [pooch_op_conv_stat_tiles(d)][K].
  *   dgrad: dx[N,H,W,C] (=|+=) conv^T(dy[N,Ho,Wo,K], wt[C,R,S,K]).
  *   wgrad: dw[K,R,S,C] = sum_pixels dy x im2col(x); `ws` device workspace of ws_bytes. */
 typedef struct {
@@ -317,6 +317,8 @@ pooch_status pooch_op_conv_dgrad(const pooch_conv_desc* d, const float* dy, cons
 pooch_status pooch_op_conv_wgrad(const pooch_conv_desc* d, const float* x, const float* dy, float* dw,
                                  float* ws, size_t ws_bytes, void* stream);
 size_t pooch_op_conv_wgrad_ws_bytes(const pooch_conv_desc* d);
+/* Number of M-tiles (rows of the partial-sum arrays) of pooch_op_conv_fwd for `d`. */
+int64_t pooch_op_conv_stat_tiles(const pooch_conv_desc* d);
 /* D[split][M][N] = A * B^T on the tensor-core core, A [M][K] and B [N][K] row-major (K-major);
  * a_mn = 2 selects the 3xTF32 path, other non-zero a_mn / b_mn (MN-major operands) return
  * POOCH_EUSAGE; bn in {64,128,256} (64/128 for 3xTF32); splits >= 1. Unit test only. */

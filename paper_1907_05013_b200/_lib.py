@@ -111,6 +111,7 @@ SIGNATURES = {
     "pooch_op_conv_dgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_i32, c_vp]),
     "pooch_op_conv_wgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pooch_op_conv_wgrad_ws_bytes": (c_sz, [P(ConvDesc)]),
+    "pooch_op_conv_stat_tiles": (c_i64, [P(ConvDesc)]),
     "pooch_op_gemm_test": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
 }
 

@@ -1,7 +1,12 @@
 // conv.cu -- launchers for the tcgen05 implicit-GEMM convolution passes (fwd, dgrad, wgrad)
 // and the FC layer (a 1x1 "conv" on a 1x1 image), plus the split-K reduction of wgrad.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.h"
 #include "conv.h"
@@ -21,11 +26,14 @@ bool conv_shape_ok(const ConvGeom& g) {
          g.pad >= 0 && g.C % 4 == 0 && g.K % 4 == 0 && g.Ho > 0 && g.Wo > 0;
 }
 
-template <int MODE, int BN, bool X3 = false>
-static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st) {
+static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
+
+template <int MODE, int BN, bool X3 = false, bool TMA = false>
+static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
+                                 const CUtensorMap* tb = nullptr) {
   constexpr int STAGES = X3 ? 3 : 4;
   constexpr int SMEM = GemmSmem<BN, STAGES, X3>::TOTAL;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3>;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -36,27 +44,105 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   int64_t tiles = (int64_t)grid.x * grid.y * grid.z;
   int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
-  kern<<<ctas, igemm_threads(MODE, X3), SMEM, st>>>(p);
+  kern<<<ctas, igemm_threads(MODE, X3), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
 
-template <int MODE>
-static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st, int prec = 0) {
+template <int MODE, bool TMA = false>
+static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st, int prec = 0,
+                              const CUtensorMap* ta = nullptr, const CUtensorMap* tb = nullptr) {
   if (prec) {
     switch (bn) {
-      case 64: return launch_igemm<MODE, 64, true>(p, grid, st);
-      case 128: return launch_igemm<MODE, 128, true>(p, grid, st);
+      case 64: return launch_igemm<MODE, 64, true, TMA>(p, grid, st, ta, tb);
+      case 128: return launch_igemm<MODE, 128, true, TMA>(p, grid, st, ta, tb);
     }
     return fail(POOCH_EUSAGE, "3xTF32 supports tile widths 64 / 128 (got %d)", bn);
   }
   switch (bn) {
-    case 64: return launch_igemm<MODE, 64>(p, grid, st);
-    case 128: return launch_igemm<MODE, 128>(p, grid, st);
-    case 256: return launch_igemm<MODE, 256>(p, grid, st);
+    case 64: return launch_igemm<MODE, 64, false, TMA>(p, grid, st, ta, tb);
+    case 128: return launch_igemm<MODE, 128, false, TMA>(p, grid, st, ta, tb);
+    case 256: return launch_igemm<MODE, 256, false, TMA>(p, grid, st, ta, tb);
   }
   return fail(POOCH_EUSAGE, "bad tile width %d", bn);
 }
+
+// ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  });
+  return fn;
+}
+
+// 4-D NHWC activation map: dims {C, W, H, N}; box {32, tw*st, th*st, tn}, traversal stride st.
+static bool map_nhwc(CUtensorMap* m, const float* base, int N, int H, int W, int C, int tw, int th, int tn, int st) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
+  cuuint32_t box[4] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)tn};
+  cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// 2-D row-major matrix [rows][cols]: box {32 cols, bn rows}
+static bool map_2d(CUtensorMap* m, const float* base, int rows, int cols, int bn) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)bn};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// Output-pixel box per M-tile: maximise useful rows / (tiles * 128).
+struct PixBox {
+  int tw, th, tn, tiles_w, tiles_h, tiles_n;
+};
+static PixBox choose_box(int N, int Ho, int Wo, int st) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, PixBox> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(N, Ho, Wo, st);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  PixBox best{1, 1, 1, Wo, Ho, N};
+  double best_eff = -1;
+  for (int tw = 1; tw <= std::min(Wo, 128) && tw * st <= 256; ++tw)
+    for (int th = 1; th <= std::min(Ho, 128 / tw) && th * st <= 256; ++th) {
+      int tnmax = th >= Ho ? std::min(std::min(N, 256), 128 / (tw * th)) : 1;
+      for (int tn = 1; tn <= tnmax; ++tn) {
+        int tx = (Wo + tw - 1) / tw, ty = (Ho + th - 1) / th, tz = (N + tn - 1) / tn;
+        double eff = (double)N * Ho * Wo / ((double)tx * ty * tz * 128.0);
+        if (eff > best_eff + 1e-12 || (std::abs(eff - best_eff) <= 1e-12 && tw > best.tw)) {
+          best_eff = eff;
+          best = PixBox{tw, th, tn, tx, ty, tz};
+        }
+      }
+    }
+  cache[key] = best;
+  return best;
+}
+
+static bool tma_enabled() {
+  static int on = getenv("POOCH_NO_TMA") ? 0 : 1;
+  return on != 0 && encode_fn() != nullptr;
+}
+
+static bool fwd_uses_tma(const ConvGeom& g) { return tma_enabled() && g.C % 32 == 0 && g.stride <= 2; }
+static bool dgrad_uses_tma(const ConvGeom& g) { return tma_enabled() && g.K % 32 == 0 && g.stride == 1; }
 
 static int pick_bn(int n, int prec = 0) {
   return n <= 64 ? 64 : ((n <= 128 || prec) ? 128 : 256);
@@ -70,6 +156,14 @@ static GemmParams base_params(const ConvGeom& g) {
   return p;
 }
 
+int conv_stat_tiles(const ConvGeom& g) {
+  if (fwd_uses_tma(g)) {
+    PixBox b = choose_box(g.N, g.Ho, g.Wo, g.stride);
+    return b.tiles_w * b.tiles_h * b.tiles_n;
+  }
+  return (g.N * g.Ho * g.Wo + 127) / 128;
+}
+
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
                              float* stat_sq, const float* bias, cudaStream_t st) {
   GemmParams p = base_params(g);
@@ -79,6 +173,19 @@ pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, 
   p.a = x; p.b = w; p.d = y;
   p.stat_sum = stat_sum; p.stat_sq = stat_sq; p.bias = bias;
   int bn = pick_bn(g.K, g.prec);
+  if (fwd_uses_tma(g)) {
+    PixBox b = choose_box(g.N, g.Ho, g.Wo, g.stride);
+    p.tw = b.tw; p.th = b.th; p.tn = b.tn;
+    p.tiles_w = b.tiles_w; p.tiles_h = b.tiles_h; p.tiles_n = b.tiles_n;
+    p.hout = g.Ho; p.wout = g.Wo;
+    p.cchunks = g.C / 32;
+    CUtensorMap ta, tb;
+    if (!map_nhwc(&ta, x, g.N, g.H, g.W, g.C, b.tw, b.th, b.tn, g.stride) ||
+        !map_2d(&tb, w, g.K, g.R * g.S * g.C, bn))
+      return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv fwd)");
+    dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
+    return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb);
+  }
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
   return launch_bn<CONV_FWD>(bn, p, grid, st, g.prec);
 }
@@ -92,6 +199,19 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
   p.a = dy; p.b = wt; p.d = dx;
   p.accumulate = accumulate ? 1 : 0;
   int bn = pick_bn(g.C, g.prec);
+  if (dgrad_uses_tma(g)) {
+    PixBox b = choose_box(g.N, g.H, g.W, 1);
+    p.tw = b.tw; p.th = b.th; p.tn = b.tn;
+    p.tiles_w = b.tiles_w; p.tiles_h = b.tiles_h; p.tiles_n = b.tiles_n;
+    p.hout = g.H; p.wout = g.W;
+    p.cchunks = g.K / 32;
+    CUtensorMap ta, tb;
+    if (!map_nhwc(&ta, dy, g.N, g.Ho, g.Wo, g.K, b.tw, b.th, b.tn, 1) ||
+        !map_2d(&tb, wt, g.C, g.R * g.S * g.K, bn))
+      return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv dgrad)");
+    dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
+    return launch_bn<CONV_DGRAD, true>(bn, p, grid, st, g.prec, &ta, &tb);
+  }
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
   return launch_bn<CONV_DGRAD>(bn, p, grid, st, g.prec);
 }
@@ -150,7 +270,7 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
   p.d = split ? ws : dw;
   dim3 grid(w.mt, w.nt, w.splits);
   if (g.prec) POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true>(p, grid, st)));
-  else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128>(p, grid, st)));
+  else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, false>(p, grid, st)));
   if (split) {
     int64_t n4 = (int64_t)g.K * p.Ng / 4;
     int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
@@ -218,4 +338,9 @@ extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float
   p.kb_per_split = (kb + splits - 1) / splits;
   dim3 grid((M + BM - 1) / BM, (N + bn - 1) / bn, splits);
   return launch_bn<GEMM_TEST>(bn, p, grid, (cudaStream_t)stream, b_mn == 0 && a_mn == 0 ? test_prec : 0);
+}
+
+extern "C" int64_t pooch_op_conv_stat_tiles(const pooch_conv_desc* d) {
+  if (!d) return 0;
+  return conv_stat_tiles(conv_geom(*d));
 }

@@ -21,6 +21,8 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
 size_t conv_wgrad_ws_bytes(const ConvGeom& g);
 pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
                                size_t ws_bytes, cudaStream_t st);
-inline int conv_mtiles(const ConvGeom& g) { return (g.N * g.Ho * g.Wo + 127) / 128; }
+// number of M-tiles of the forward pass = rows of its BN partial-sum arrays
+int conv_stat_tiles(const ConvGeom& g);
+inline int conv_mtiles(const ConvGeom& g) { return conv_stat_tiles(g); }
 
 }  // namespace pooch

@@ -28,6 +28,8 @@
 //  of the instruction descriptor -- produced all-zero results on B200 in our tests, see
 //  DESIGN.md "MN-major tf32".)
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
 #include <type_traits>
 
@@ -55,6 +57,11 @@ struct GemmParams {
   const float* bias;     // FWD (FC): per-column bias, nullable
   int accumulate;        // DGRAD: dx += result
   int kb_per_split;      // WGRAD / TEST: k-blocks handled by one blockIdx.z
+  // TMA-fed FWD / DGRAD: an M-tile is a TW x TH x TN box of output pixels (rows = TW*TH*TN <= 128)
+  int tw, th, tn;        // box of output pixels per tile
+  int tiles_w, tiles_h, tiles_n;
+  int hout, wout;        // output pixel grid of this GEMM (FWD: Ho x Wo, DGRAD: H x W)
+  int cchunks;           // 32-channel chunks of the reduced channel dim (FWD: C/32, DGRAD: K/32)
 };
 
 constexpr int BM = 128;
@@ -349,7 +356,7 @@ __host__ __device__ constexpr int igemm_threads(int mode, bool x3) {
 }
 
 struct TileMap {
-  int mt, nt, zt, kb_total, kbps;
+  int mt, nt, zt, kb_total, kbps;  // mt = M-tiles (TMA: tiles_n * tiles_h * tiles_w)
   __device__ void decode(int t, int& m0, int& n0, int& kb0, int& nkb, int bn) const {
     int m = t % mt;
     int r = t / mt;
@@ -362,8 +369,10 @@ struct TileMap {
   }
 };
 
-template <int MODE, int BN, int STAGES, bool X3 = false>
-__global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const GemmParams p) {
+template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false>
+__global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
+    igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b) {
+  static_assert(!TMA || MODE == CONV_FWD || MODE == CONV_DGRAD, "TMA path: conv fwd / dgrad");
   using SM = GemmSmem<BN, STAGES, X3>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const
   const int warp = tid >> 5;
   const int lane = tid & 31;
   TileMap tm;
-  tm.mt = (p.M + BM - 1) / BM;
+  tm.mt = TMA ? p.tiles_n * p.tiles_h * p.tiles_w : (p.M + BM - 1) / BM;
   tm.nt = (p.Ng + BN - 1) / BN;
   tm.kb_total = (p.Kg + BK - 1) / BK;
   tm.kbps = p.kb_per_split > 0 ? p.kb_per_split : max(tm.kb_total, 1);
@@ -389,14 +398,15 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], 128);
+      // full: 128 producer (cp.async) or auxiliary-warp arrivals; 1 expect_tx arrival (TMA, no aux)
+      ptx::mbar_init(&full[s], (TMA && !X3) ? 1 : 128);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
-    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&rawfull[s], 128);
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&rawfull[s], TMA ? 1 : 128);
     ptx::fence_mbar_init();
   }
   if (warp == 8) ptx::tmem_alloc(tmem_slot, 2 * BN);
@@ -429,6 +439,46 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const
         }
       }
       ptx::cp_async_wait<0>();
+    } else if constexpr (TMA) {
+      // one elected thread drives the tensor-memory accelerator: per k-block (r, s, 32-channel
+      // chunk) a 4-D box of input (FWD: x, DGRAD: dy) pixels -- out-of-range rows / columns of the
+      // padding are zero-filled by the TMA -- and a 2-D box of the (transposed) weight.
+      if (ptid == 0) {
+        ptx::tma_prefetch_desc(&tma_a);
+        ptx::tma_prefetch_desc(&tma_b);
+        const uint32_t a_bytes = 32u * p.tw * p.th * p.tn * 4u;
+        const uint32_t bytes = a_bytes + (uint32_t)BN * 32u * 4u;
+        const int cred = MODE == CONV_FWD ? p.C : p.K;  // reduced channels
+        int it = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          int m0, n0, kb0, nkb;
+          tm.decode(t, m0, n0, kb0, nkb, BN);
+          const int mt_i = m0 / BM;
+          const int tw_i = mt_i % p.tiles_w;
+          const int th_i = (mt_i / p.tiles_w) % p.tiles_h;
+          const int tn_i = mt_i / (p.tiles_w * p.tiles_h);
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            int s = it % STAGES;
+            if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+            uint32_t st = sbase + s * SM::STAGE_BYTES;
+            uint64_t* bar = X3 ? &rawfull[s] : &full[s];
+            const int k = kb0 + kb;
+            const int rs = k / p.cchunks, cc = k - rs * p.cchunks;
+            const int r = rs / p.S, sx = rs - r * p.S;
+            int cw, chh;
+            if (MODE == CONV_FWD) {
+              cw = tw_i * p.tw * p.stride - p.pad + sx;
+              chh = th_i * p.th * p.stride - p.pad + r;
+            } else {
+              cw = tw_i * p.tw + p.pad - sx;
+              chh = th_i * p.th + p.pad - r;
+            }
+            ptx::mbar_arrive_expect_tx(bar, bytes);
+            ptx::tma_load_4d(st, &tma_a, bar, cc * 32, cw, chh, tn_i * p.tn);
+            ptx::tma_load_2d(st + SM::A_BYTES, &tma_b, bar, rs * cred + cc * 32, n0);
+          }
+        }
+      }
     } else {
       KLoader<MODE, BM, true> la;
       KLoader<MODE, BN, false> lb;
@@ -504,11 +554,15 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const
           uint32_t sb = sa + SM::A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            uint64_t ad = ptx::smem_desc(sa + kk * 2 * A_LBO, A_LBO, 128);
-            uint64_t bd = ptx::smem_desc(sb + kk * 2 * B_LBO, B_LBO, 128);
+            // SWIZZLE_NONE (cp.async tiles): k-step = 2 core matrices; SWIZZLE_128B (TMA tiles):
+            // 128-B rows in 1024-B atoms (SBO), k-step = +32 B inside the row
+            const uint32_t ka = TMA ? kk * 32 : kk * 2 * A_LBO, kbo = TMA ? kk * 32 : kk * 2 * B_LBO;
+            const uint32_t la = TMA ? 16 : A_LBO, lb = TMA ? 16 : B_LBO, sbo = TMA ? 1024 : 128, lay = TMA ? 2 : 0;
+            uint64_t ad = ptx::smem_desc(sa + ka, la, sbo, lay);
+            uint64_t bd = ptx::smem_desc(sb + kbo, lb, sbo, lay);
             if constexpr (X3) {  // small terms first, then the big product
-              uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + kk * 2 * A_LBO, A_LBO, 128);
-              uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + kk * 2 * B_LBO, B_LBO, 128);
+              uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + ka, la, sbo, lay);
+              uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + kbo, lb, sbo, lay);
               ptx::mma_tf32(acc, asd, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
               ptx::mma_tf32(acc, ad, bsd, IDESC, 1u);
               ptx::mma_tf32(acc, ad, bd, IDESC, 1u);
@@ -536,8 +590,18 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1) igemm_kernel(const
       const int ab = j & 1;
       ptx::mbar_wait_sleep(&tfull[ab], (j >> 1) & 1);
       ptx::tc_fence_after();
-      const int gm = m0 + row;
-      const bool rok = gm < p.M;
+      int gm = m0 + row;
+      bool rok = gm < p.M;
+      if constexpr (TMA) {  // row -> (n, h, w) of the tile's pixel box
+        const int mt_i = m0 / BM;
+        const int tw_i = mt_i % p.tiles_w;
+        const int th_i = (mt_i / p.tiles_w) % p.tiles_h;
+        const int tn_i = mt_i / (p.tiles_w * p.tiles_h);
+        const int per = p.tw * p.th;
+        const int nn = tn_i * p.tn + row / per, hh = th_i * p.th + (row / p.tw) % p.th, ww = tw_i * p.tw + row % p.tw;
+        rok = row < per * p.tn && nn < p.N && hh < p.hout && ww < p.wout;
+        gm = (nn * p.hout + hh) * p.wout + ww;
+      }
       const uint32_t taddr = tmem + ab * BN + ((uint32_t)(warp * 32) << 16);
       const int z = t / (tm.mt * tm.nt);
       bool stats = false;

@@ -81,7 +81,7 @@ def test_conv_fwd_and_stats(case, prec):
     d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p, prec)
     ho, wo = L.conv_out_hw(H, W, R, R, s, p)
     M = N * ho * wo
-    mt = (M + 127) // 128
+    mt = lib.lib.pooch_op_conv_stat_tiles(C.byref(d))
     dx, dw = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
     dy = torch.full((N, ho, wo, K), float("nan"), device="cuda")
     s1 = torch.zeros((mt, K), device="cuda")

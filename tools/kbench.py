@@ -19,7 +19,7 @@ for name, H, Cin, K, R, s in shapes:
     y = torch.empty(B, Ho, Ho, K, device="cuda"); gy = torch.randn(B, Ho, Ho, K, device="cuda")
     wt = w.permute(3, 1, 2, 0).contiguous(); dx = torch.empty_like(x); dw = torch.empty_like(w)
     d = _lib.ConvDesc(B, H, H, Cin, K, R, R, s, p, PREC)
-    mt = (B * Ho * Ho + 127) // 128
+    mt = _lib.lib.pooch_op_conv_stat_tiles(C.byref(d))
     s1 = torch.empty(mt, K, device="cuda"); s2 = torch.empty(mt, K, device="cuda")
     wsb = _lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d)); ws = torch.empty(max(wsb // 4, 1), device="cuda")
     P = lambda t: C.c_void_p(t.data_ptr())
