@@ -388,7 +388,7 @@ def kernel_launches(ctx, steps):
 
 def roofline(fam, pk):
     """Dominant kernel family of the instrumented step vs its roof."""
-    cand = {k: v for k, v in fam.items() if k not in ("other", "swap_out", "swap_in") and v["ms"] > 0}
+    cand = {k: v for k, v in fam.items() if k not in ("other", "stall", "swap_out", "swap_in") and v["ms"] > 0}
     if not cand:
         return None
     k, v = max(cand.items(), key=lambda kv: kv[1]["ms"])
@@ -481,10 +481,15 @@ def incore_run(ctx_ooc, dev, host, host_bytes, streams, args, free):
         e1.record(streams[0])
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / n
+        ctx.set_timing(True)
+        ctx.train_step(0.01, sync_loss=False)
+        torch.cuda.synchronize()
+        fam = families_table(ctx.family_stats(), peaks())
+        ctx.set_timing(False)
         ctx.close()
         del big
         torch.cuda.empty_cache()
-        return {"images_per_s": batch * 1000.0 / ms, "ms_per_step": ms}
+        return {"images_per_s": batch * 1000.0 / ms, "ms_per_step": ms, "families": fam}
     except Exception as e:  # report, never fake
         return {"images_per_s": None, "note": "in-core run failed: %s" % e}
 

@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -31,7 +32,10 @@ static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 template <int MODE, int BN, bool X3 = false, bool TMA = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr) {
-  constexpr int STAGES = X3 ? 3 : 4;
+  // deepest ring that fits 227 KB: TMA wgrad has the longest load -> MMA latency (TMA, then an
+  // in-place transpose by the auxiliary warps), so it gets every stage that fits
+  constexpr int STAGE_B = (BM + BN) * BK * 4 * (X3 ? 2 : 1);
+  constexpr int STAGES = (MODE == CONV_WGRAD && TMA) ? std::min(8, (200 * 1024) / STAGE_B) : (X3 ? 3 : 4);
   constexpr int SMEM = GemmSmem<BN, STAGES, X3>::TOTAL;
   auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA>;
   static bool configured = false;
@@ -90,6 +94,21 @@ static bool map_nhwc(CUtensorMap* m, const float* base, int N, int H, int W, int
   cuuint32_t box[4] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)tn};
   cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// 5-D view of an NHWC activation for wgrad: dims {32, W, H, N, C/32} (the 32-channel chunk index
+// outermost, stride 128 B); box {32, tw*st, th*st, tn, cb} lands as cb consecutive [pixel][32] blocks.
+static bool map_nhwc_chunks(CUtensorMap* m, const float* base, int N, int H, int W, int C, int tw, int th, int tn,
+                            int st, int cb) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[5] = {32, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)(C / 32)};
+  cuuint64_t strides[4] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4, 128};
+  cuuint32_t box[5] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)tn, (cuuint32_t)cb};
+  cuuint32_t es[5] = {1, (cuuint32_t)st, (cuuint32_t)st, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
@@ -217,21 +236,77 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
 }
 
 // ---- wgrad: split-K over pixels into a workspace, then a fixed-order reduction.
+// TMA path (C, Cout multiples of 32, stride <= 2): a k-block is a box of exactly 32 output
+// pixels; the operand whose GEMM side is <= 64 rows becomes B with BN = 64, so a 64-channel
+// layer does not pad the 128-row A tile (when that is x, A = im2col(x)^T and the reduction
+// transposes the workspace [split][RSC][Cout] into KRSC).
 struct WgradPlan {
+  bool tma, swap;
   int bn, mt, nt, kb, splits, kb_per_split;
+  PixBox box;
 };
+
+static PixBox choose_kbox(int N, int Ho, int Wo, int st) {
+  PixBox best{};
+  int64_t best_boxes = -1;
+  for (int tw = 1; tw <= 32; tw *= 2)
+    for (int th = 1; tw * th <= 32; th *= 2) {
+      int tn = 32 / (tw * th);
+      if (tw * st > 256 || th * st > 256) continue;
+      int64_t tx = (Wo + tw - 1) / tw, ty = (Ho + th - 1) / th, tz = (N + tn - 1) / tn;
+      int64_t boxes = tx * ty * tz;
+      if (best_boxes < 0 || boxes < best_boxes || (boxes == best_boxes && tw > best.tw)) {
+        best_boxes = boxes;
+        best = PixBox{tw, th, tn, (int)tx, (int)ty, (int)tz};
+      }
+    }
+  return best;
+}
+
+static bool wgrad_uses_tma(const ConvGeom& g) {
+  return tma_enabled() && g.C % 32 == 0 && g.K % 32 == 0 && g.stride <= 2;
+}
 
 static WgradPlan wgrad_plan(const ConvGeom& g) {
   WgradPlan w{};
   int rsc = g.R * g.S * g.C;
+  w.tma = wgrad_uses_tma(g);
+  int M = g.K, Ng = rsc;
   w.bn = 128;
-  w.mt = (g.K + BM - 1) / BM;
-  w.nt = (rsc + w.bn - 1) / w.bn;
-  w.kb = (g.N * g.Ho * g.Wo + BK - 1) / BK;
-  int tiles = w.mt * w.nt;
-  int want = std::max(1, (2 * 148 + tiles - 1) / tiles);
-  int max_by_k = std::max(1, w.kb / 8);  // at least 8 k-blocks (256 pixels) per split
-  w.splits = std::min(want, max_by_k);
+  if (w.tma) {
+    w.box = choose_kbox(g.N, g.Ho, g.Wo, g.stride);
+    if (const char* e = getenv("POOCH_KBOX")) {  // profiling experiments only
+      int a = 0, b = 0, c = 0;
+      if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && a * b * c == 32)
+        w.box = PixBox{a, b, c, (g.Wo + a - 1) / a, (g.Ho + b - 1) / b, (g.N + c - 1) / c};
+    }
+    w.kb = w.box.tiles_w * w.box.tiles_h * w.box.tiles_n;
+    if (g.K <= 64 && rsc > 64) {
+      w.swap = true;
+      M = rsc;
+      Ng = g.K;
+    }
+    if (Ng <= 64) w.bn = 64;
+  } else {
+    w.kb = (g.N * g.Ho * g.Wo + BK - 1) / BK;
+  }
+  w.mt = (M + BM - 1) / BM;
+  w.nt = (Ng + w.bn - 1) / w.bn;
+  const int64_t tiles = (int64_t)w.mt * w.nt;
+  // split-K count from a small cost model in units of one k-block (~0.7 us on a busy SM): waves of
+  // persistent CTAs x (k-blocks per split + ~6 for pipeline fill and epilogue), plus the workspace
+  // write + reduction read (8 B per dW element per split at ~6.5 TB/s ~ 4.5 MB per k-block time)
+  const double ws_per_split = 8.0 * g.K * rsc / 4.5e6;
+  double best = 1e300;
+  w.splits = 1;
+  for (int s = 1; s <= std::max(1, w.kb / 4); ++s) {
+    const int64_t waves = (tiles * s + 147) / 148;
+    const double cost = (double)waves * ((w.kb + s - 1) / s + 6) + (s > 1 ? s * ws_per_split : 0.0);
+    if (cost < best - 1e-9) {
+      best = cost;
+      w.splits = s;
+    }
+  }
   if (const char* e = getenv("POOCH_WGRAD_SPLITS")) w.splits = std::max(1, std::min(atoi(e), w.kb));
   w.kb_per_split = (w.kb + w.splits - 1) / w.splits;
   w.splits = (w.kb + w.kb_per_split - 1) / w.kb_per_split;
@@ -240,7 +315,7 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
 
 size_t conv_wgrad_ws_bytes(const ConvGeom& g) {
   WgradPlan w = wgrad_plan(g);
-  return w.splits > 1 ? (size_t)w.splits * g.K * g.R * g.S * g.C * sizeof(float) : 0;
+  return (w.splits > 1 || w.swap) ? (size_t)w.splits * g.K * g.R * g.S * g.C * sizeof(float) : 0;
 }
 
 __global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out, int64_t n4,
@@ -255,23 +330,78 @@ __global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __re
   }
 }
 
+// ws [split][rows][cols] -> out [cols][rows] = sum over splits (in split order), 32 x 32 tiles
+__global__ void splitk_reduce_t_kernel(const float* __restrict__ ws, float* __restrict__ out, int rows, int cols,
+                                       int splits) {
+  __shared__ float tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const int64_t plane = (int64_t)rows * cols;
+  for (int i = ty; i < 32; i += 8) {
+    int r = r0 + i, c = c0 + tx;
+    float a = 0.f;
+    if (r < rows && c < cols) {
+      const float* q = ws + (int64_t)r * cols + c;
+      a = q[0];
+      for (int s = 1; s < splits; ++s) a += q[s * plane];
+    }
+    tile[i][tx] = a;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    int c = c0 + i, r = r0 + tx;
+    if (c < cols && r < rows) out[(int64_t)c * rows + r] = tile[tx][i];
+  }
+}
+
 pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
                                size_t ws_bytes, cudaStream_t st) {
   WgradPlan w = wgrad_plan(g);
   GemmParams p = base_params(g);
-  p.M = g.K;
-  p.Ng = g.R * g.S * g.C;
+  const int rsc = g.R * g.S * g.C;
+  p.M = w.swap ? rsc : g.K;
+  p.Ng = w.swap ? g.K : rsc;
   p.Kg = g.N * g.Ho * g.Wo;
   p.a = dy; p.b = x;
   p.kb_per_split = w.kb_per_split;
-  bool split = w.splits > 1;
-  if (split && ws_bytes < conv_wgrad_ws_bytes(g))
+  bool use_ws = w.splits > 1 || w.swap;
+  if (use_ws && ws_bytes < conv_wgrad_ws_bytes(g))
     return fail(POOCH_EUSAGE, "wgrad workspace too small: %zu < %zu", ws_bytes, conv_wgrad_ws_bytes(g));
-  p.d = split ? ws : dw;
+  p.d = use_ws ? ws : dw;
   dim3 grid(w.mt, w.nt, w.splits);
-  if (g.prec) POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true>(p, grid, st)));
-  else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, false>(p, grid, st)));
-  if (split) {
+  if (w.tma) {
+    p.tw = w.box.tw; p.th = w.box.th; p.tn = w.box.tn;
+    p.tiles_w = w.box.tiles_w; p.tiles_h = w.box.tiles_h; p.tiles_n = w.box.tiles_n;
+    p.hout = g.Ho; p.wout = g.Wo;
+    p.wg_a_is_x = w.swap ? 1 : 0;
+    // chunks per box: the largest power of two <= 4 dividing the channel count in chunks (so a
+    // box never straddles two taps) and no larger than the tile
+    auto cb_of = [](int ch, int rows) {
+      int cb = 4;
+      while (cb > 1 && ((ch / 32) % cb != 0 || 32 * cb > rows)) cb >>= 1;
+      return cb;
+    };
+    const int cb_dy = cb_of(g.K, w.swap ? w.bn : BM), cb_x = cb_of(g.C, w.swap ? BM : w.bn);
+    p.wg_cba = w.swap ? cb_x : cb_dy;
+    p.wg_cbb = w.swap ? cb_dy : cb_x;
+    CUtensorMap tdy, tx;
+    if (!map_nhwc_chunks(&tdy, dy, g.N, g.Ho, g.Wo, g.K, w.box.tw, w.box.th, w.box.tn, 1, cb_dy) ||
+        !map_nhwc_chunks(&tx, x, g.N, g.H, g.W, g.C, w.box.tw, w.box.th, w.box.tn, g.stride, cb_x))
+      return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv wgrad)");
+    const CUtensorMap* ta = w.swap ? &tx : &tdy;
+    const CUtensorMap* tb = w.swap ? &tdy : &tx;
+    POOCH_CHECK((launch_bn<CONV_WGRAD, true>(w.bn, p, grid, st, g.prec, ta, tb)));
+  } else if (g.prec) {
+    POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true>(p, grid, st)));
+  } else {
+    POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, false>(p, grid, st)));
+  }
+  if (w.swap) {
+    count_launch();
+    dim3 rg((g.K + 31) / 32, (rsc + 31) / 32);
+    splitk_reduce_t_kernel<<<rg, dim3(32, 8), 0, st>>>(ws, dw, rsc, g.K, w.splits);
+    POOCH_CUDA(cudaGetLastError());
+  } else if (use_ws) {
     int64_t n4 = (int64_t)g.K * p.Ng / 4;
     int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
     count_launch();

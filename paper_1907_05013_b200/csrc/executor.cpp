@@ -965,6 +965,8 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
   for (size_t i = 0; i < c->ops.size(); ++i) {
     const Op& o = c->ops[i];
     cudaStream_t st = c->s[o.lane];
+    // compute-stream time spent blocked on another stream is its own family, not the next kernel's
+    if (timing && o.lane == 0 && (!o.waits.empty() || !o.start_waits.empty())) mark_seg(c, FAM_STALL, -1, 0, 0);
     for (int w : o.waits) POOCH_CUDA(cudaStreamWaitEvent(st, c->ev[w], 0));
     for (int w : o.start_waits) POOCH_CUDA(cudaStreamWaitEvent(st, c->ev_start[w], 0));
     if (o.record_start) POOCH_CUDA(cudaEventRecord(c->ev_start[i], st));
@@ -1017,7 +1019,8 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
       size_t k0 = op_seg_begin[comp[j]];
       size_t k1 = j + 1 < comp.size() ? (size_t)op_seg_begin[comp[j + 1]] : (size_t)seg_end_compute;
       double ms = 0;
-      for (size_t k = k0; k < k1 && k < seg_ms.size(); ++k) ms += seg_ms[k];
+      for (size_t k = k0; k < k1 && k < seg_ms.size(); ++k)
+        if (c->tseg[k].second != FAM_STALL) ms += seg_ms[k];
       int64_t ns = (int64_t)(ms * 1e6);
       if (o.kind == 'F') c->last_fwd[o.id] = ns;
       if (o.kind == 'R') c->last_rec[o.id] = ns;

@@ -62,6 +62,10 @@ struct GemmParams {
   int tiles_w, tiles_h, tiles_n;
   int hout, wout;        // output pixel grid of this GEMM (FWD: Ho x Wo, DGRAD: H x W)
   int cchunks;           // 32-channel chunks of the reduced channel dim (FWD: C/32, DGRAD: K/32)
+  // TMA-fed WGRAD: a k-block is a TW x TH x TN box of 32 output pixels (tiles_* count the boxes);
+  // wg_a_is_x = 1: A = im2col(x)^T [R*S*C] and B = dy^T [Cout] (the transposed orientation)
+  int wg_a_is_x;
+  int wg_cba, wg_cbb;    // 32-channel chunks per TMA box of A / B (5-D maps, chunk index outermost)
 };
 
 constexpr int BM = 128;
@@ -326,6 +330,27 @@ __device__ __forceinline__ void transpose_block(uint32_t blk, int rot, uint32_t 
   }
 }
 
+// In-place transpose of one TMA box of 32 pixels x 32 channels (4 KB, SWIZZLE_128B: 16-B chunk j
+// of 128-B row r sits at chunk j ^ (r & 7)) into the K-major SWIZZLE_128B operand layout (row =
+// channel, k = pixel). Lane l holds pixel l's row in registers, then writes column l of every
+// channel row: each store instruction covers one 128-B row, conflict free. X3: residuals -> +delta.
+template <bool X3>
+__device__ __forceinline__ void transpose32(uint32_t blk, int lane, uint32_t delta) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
+                 : "r"(blk + lane * 128 + ((j ^ (lane & 7)) << 4)));
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const uint32_t a = blk + c * 128 + ((((lane >> 2) ^ (c & 7))) << 4) + (lane & 3) * 4;
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[c]) : "memory");
+    if (X3) asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + delta), "f"(tf32_resid(v[c])) : "memory");
+  }
+}
+
 // ------------------------------------------------------------------------------- kernel
 // Butterfly transpose-reduce: on return lane l holds sum over the 32 lanes of v[l].
 __device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
@@ -372,7 +397,10 @@ struct TileMap {
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b) {
-  static_assert(!TMA || MODE == CONV_FWD || MODE == CONV_DGRAD, "TMA path: conv fwd / dgrad");
+  static_assert(!TMA || MODE != GEMM_TEST, "TMA path: conv fwd / dgrad / wgrad");
+  // TMA tiles whose M rows are a box of output pixels (FWD / DGRAD); TMA wgrad boxes pixels along K
+  constexpr bool PIXM = TMA && MODE != CONV_WGRAD;
+  constexpr bool AUX = igemm_aux(MODE, X3);
   using SM = GemmSmem<BN, STAGES, X3>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -389,9 +417,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
   const int warp = tid >> 5;
   const int lane = tid & 31;
   TileMap tm;
-  tm.mt = TMA ? p.tiles_n * p.tiles_h * p.tiles_w : (p.M + BM - 1) / BM;
+  tm.mt = PIXM ? p.tiles_n * p.tiles_h * p.tiles_w : (p.M + BM - 1) / BM;
   tm.nt = (p.Ng + BN - 1) / BN;
-  tm.kb_total = (p.Kg + BK - 1) / BK;
+  tm.kb_total = (TMA && MODE == CONV_WGRAD) ? p.tiles_n * p.tiles_h * p.tiles_w : (p.Kg + BK - 1) / BK;
   tm.kbps = p.kb_per_split > 0 ? p.kb_per_split : max(tm.kb_total, 1);
   tm.zt = p.kb_per_split > 0 ? (tm.kb_total + tm.kbps - 1) / tm.kbps : 1;
   const int ntiles = tm.mt * tm.nt * tm.zt;
@@ -399,7 +427,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // full: 128 producer (cp.async) or auxiliary-warp arrivals; 1 expect_tx arrival (TMA, no aux)
-      ptx::mbar_init(&full[s], (TMA && !X3) ? 1 : 128);
+      ptx::mbar_init(&full[s], (TMA && !AUX) ? 1 : 128);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -419,7 +447,51 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
   if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------------ producers
     const int ptid = tid - 128;
-    if constexpr (MODE == CONV_WGRAD) {
+    if constexpr (MODE == CONV_WGRAD && TMA) {
+      // one elected thread: per k-block (a box of 32 output pixels) one 4-D TMA box per 32 rows
+      // of each operand -- dy: 32 output channels x the pixel box; x: the 32 input channels of
+      // one (r, s) tap over the box's input pixels (traversal stride = conv stride, padding
+      // zero-filled). Rows past M / Ng are skipped: they only feed accumulator rows / columns
+      // the epilogue never stores.
+      if (ptid == 0) {
+        ptx::tma_prefetch_desc(&tma_a);
+        ptx::tma_prefetch_desc(&tma_b);
+        int it = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          int m0, n0, kb0, nkb;
+          tm.decode(t, m0, n0, kb0, nkb, BN);
+          uint32_t bytes = 0;
+          for (int q = 0; q < BM / 32; q += p.wg_cba) bytes += (m0 + 32 * q < p.M) ? 4096u * p.wg_cba : 0u;
+          for (int q = 0; q < BN / 32; q += p.wg_cbb) bytes += (n0 + 32 * q < p.Ng) ? 4096u * p.wg_cbb : 0u;
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            int s = it % STAGES;
+            if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+            uint32_t st = sbase + s * SM::STAGE_BYTES;
+            const int b = kb0 + kb;
+            const int ow = (b % p.tiles_w) * p.tw;
+            const int oh = ((b / p.tiles_w) % p.tiles_h) * p.th;
+            const int on = (b / (p.tiles_w * p.tiles_h)) * p.tn;
+            ptx::mbar_arrive_expect_tx(&rawfull[s], bytes);
+            // one box = cb consecutive 32-channel chunks of the same tap over the pixel box; the
+            // 5-D map puts the chunk index outermost, so the box lands as cb consecutive 4-KB blocks
+            auto box = [&](uint32_t dst, const CUtensorMap* map, bool is_x, int row) {
+              if (is_x) {
+                const int rs = row / p.C, c = row - rs * p.C;
+                const int r = rs / p.S, sx = rs - r * p.S;
+                ptx::tma_load_5d(dst, map, &rawfull[s], 0, ow * p.stride - p.pad + sx, oh * p.stride - p.pad + r, on,
+                                 c >> 5);
+              } else {
+                ptx::tma_load_5d(dst, map, &rawfull[s], 0, ow, oh, on, row >> 5);
+              }
+            };
+            for (int q = 0; q < BM / 32; q += p.wg_cba)
+              if (m0 + 32 * q < p.M) box(st + q * 4096, &tma_a, p.wg_a_is_x != 0, m0 + 32 * q);
+            for (int q = 0; q < BN / 32; q += p.wg_cbb)
+              if (n0 + 32 * q < p.Ng) box(st + SM::A_BYTES + q * 4096, &tma_b, p.wg_a_is_x == 0, n0 + 32 * q);
+          }
+        }
+      }
+    } else if constexpr (MODE == CONV_WGRAD) {
       static_assert(BN == 128, "wgrad uses 128 x 128 tiles");
       WLoader<true> la;
       WLoader<false> lb;
@@ -433,8 +505,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
           int s = it % STAGES;
           if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
           uint32_t st = sbase + s * SM::STAGE_BYTES;
-          la.load(p, st, kb0 + kb);
-          lb.load(p, st + SM::A_BYTES, kb0 + kb);
+          const int k = kb0 + kb;
+          la.load(p, st, k);
+          lb.load(p, st + SM::A_BYTES, k);
           ptx::cp_async_arrive_noinc(&rawfull[s]);
         }
       }
@@ -461,7 +534,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             int s = it % STAGES;
             if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
             uint32_t st = sbase + s * SM::STAGE_BYTES;
-            uint64_t* bar = X3 ? &rawfull[s] : &full[s];
+            uint64_t* bar = AUX ? &rawfull[s] : &full[s];
             const int k = kb0 + kb;
             const int rs = k / p.cchunks, cc = k - rs * p.cchunks;
             const int r = rs / p.S, sx = rs - r * p.S;
@@ -500,7 +573,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
       }
       ptx::cp_async_wait<0>();
     }
-  } else if (igemm_aux(MODE, X3) && warp >= 9) {
+  } else if (AUX && warp >= 9) {
     // ------------------------------------------------------------------ auxiliary warps
     // Per stage: wait for the raw operands, (wgrad) transpose every 4x4 block in place,
     // (3xTF32) write x - tf32(x) of every chunk, publish to the async proxy, arrive full[].
@@ -513,7 +586,10 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
         int s = it % STAGES;
         ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
-        if constexpr (MODE == CONV_WGRAD) {
+        if constexpr (MODE == CONV_WGRAD && TMA) {
+          // (BM + BN) / 32 TMA boxes, A's then B's, 4 KB each; residuals at the same offsets + SMALL_OFF
+          for (int bi = warp - 9; bi < (BM + BN) / 32; bi += 4) transpose32<X3>(st + bi * 4096, lane, SM::SMALL_OFF);
+        } else if constexpr (MODE == CONV_WGRAD) {
           // 256 blocks in A (rows = Cout) and 256 in B (rows = R*S*C); block (g, j) = rows 4g..4g+3, k-chunk j
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -592,7 +668,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
       ptx::tc_fence_after();
       int gm = m0 + row;
       bool rok = gm < p.M;
-      if constexpr (TMA) {  // row -> (n, h, w) of the tile's pixel box
+      if constexpr (PIXM) {  // row -> (n, h, w) of the tile's pixel box
         const int mt_i = m0 / BM;
         const int tw_i = mt_i % p.tiles_w;
         const int th_i = (mt_i / p.tiles_w) % p.tiles_h;

@@ -17,7 +17,7 @@ from .planning import STRATEGIES
 NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2}
 KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce"]
 FAMILIES = ["conv_fwd", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd", "pool", "fc_ce", "sgd",
-            "swap_out", "swap_in", "allreduce", "other"]
+            "swap_out", "swap_in", "allreduce", "other", "stall"]
 
 
 def build_net(name: str, in_hw: int, classes: int, width: int = 32):

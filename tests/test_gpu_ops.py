@@ -62,6 +62,9 @@ CONV_CASES = [
     (8, 32, 32, 4, 32, 3, 1, 1),      # tiny CNN first conv
     (8, 32, 32, 32, 32, 3, 1, 1),     # tiny CNN conv
     (1, 5, 5, 512, 2048, 1, 1, 0),    # wide 1x1, M < 128
+    (3, 6, 6, 256, 64, 1, 1, 0),      # 1x1 reduce to 64 (wgrad: transposed orientation)
+    (2, 6, 6, 64, 256, 1, 1, 0),      # 1x1 expand from 64 (wgrad: 64-wide B tile)
+    (5, 7, 7, 64, 96, 3, 1, 1),       # odd batch, ragged pixel boxes
 ]
 
 

@@ -8,7 +8,9 @@ PREC = int(os.environ.get("PREC", "1"))
 shapes = [  # name, H, C, K, R, stride
     ("stem7x7", 224, 4, 64, 7, 2), ("l1.c1 1x1", 56, 256, 64, 1, 1), ("l1.c2 3x3", 56, 64, 64, 3, 1),
     ("l1.c3 1x1", 56, 64, 256, 1, 1), ("l2.c2 3x3", 28, 128, 128, 3, 1), ("l3.c2 3x3", 14, 256, 256, 3, 1),
-    ("l3.c3 1x1", 14, 256, 1024, 1, 1), ("l4.c2 3x3", 7, 512, 512, 3, 1), ("l4.c1 1x1", 7, 2048, 512, 1, 1)]
+    ("l3.c3 1x1", 14, 256, 1024, 1, 1), ("l4.c2 3x3", 7, 512, 512, 3, 1), ("l4.c1 1x1", 7, 2048, 512, 1, 1),
+    ("l2.c2s2 3x3", 56, 128, 128, 3, 2), ("l2.ds 1x1s2", 56, 256, 512, 1, 2)]
+OPS = os.environ.get("OPS", "fwd,dgrad,wgrad").split(",")
 only = os.environ.get("ONLY")
 res = []
 for name, H, Cin, K, R, s in shapes:
@@ -30,7 +32,7 @@ for name, H, Cin, K, R, s in shapes:
     }
     flops = 2.0 * B * Ho * Ho * K * R * R * Cin
     for op, f in ops.items():
-        if name.startswith("stem") and op == "dgrad": continue
+        if (name.startswith("stem") and op == "dgrad") or op not in OPS: continue
         for _ in range(2): f()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
