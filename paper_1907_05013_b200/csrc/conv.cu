@@ -161,7 +161,7 @@ static bool tma_enabled() {
 }
 
 static bool fwd_uses_tma(const ConvGeom& g) { return tma_enabled() && g.C % 32 == 0 && g.stride <= 2; }
-static bool dgrad_uses_tma(const ConvGeom& g) { return tma_enabled() && g.K % 32 == 0 && g.stride == 1; }
+static bool dgrad_uses_tma(const ConvGeom& g) { return tma_enabled() && g.K % 32 == 0 && g.stride <= 2; }
 
 static int pick_bn(int n, int prec = 0) {
   return n <= 64 ? 64 : ((n <= 128 || prec) ? 128 : 256);
@@ -219,17 +219,37 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
   p.accumulate = accumulate ? 1 : 0;
   int bn = pick_bn(g.C, g.prec);
   if (dgrad_uses_tma(g)) {
-    PixBox b = choose_box(g.N, g.H, g.W, 1);
-    p.tw = b.tw; p.th = b.th; p.tn = b.tn;
-    p.tiles_w = b.tiles_w; p.tiles_h = b.tiles_h; p.tiles_n = b.tiles_n;
-    p.hout = g.H; p.wout = g.W;
-    p.cchunks = g.K / 32;
-    CUtensorMap ta, tb;
-    if (!map_nhwc(&ta, dy, g.N, g.Ho, g.Wo, g.K, b.tw, b.th, b.tn, 1) ||
-        !map_2d(&tb, wt, g.C, g.R * g.S * g.K, bn))
-      return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv dgrad)");
-    dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
-    return launch_bn<CONV_DGRAD, true>(bn, p, grid, st, g.prec, &ta, &tb);
+    // stride st: one launch per output-parity class (a, b); each is a stride-1 correlation of dy
+    // with the taps of that class (sub-pixel decomposition), so every A box is a dense dy box.
+    // A class with no taps (e.g. odd pixels of a 1x1 stride-2 conv) runs with K = 0: its epilogue
+    // stores zeros (or leaves dx unchanged when accumulating).
+    const int s_ = g.stride;
+    CUtensorMap tb;
+    if (!map_2d(&tb, wt, g.C, g.R * g.S * g.K, bn)) return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (dgrad W)");
+    for (int a = 0; a < s_; ++a)
+      for (int bb = 0; bb < s_; ++bb) {
+        const int hc = (g.H - a + s_ - 1) / s_, wc = (g.W - bb + s_ - 1) / s_;
+        if (hc <= 0 || wc <= 0) continue;
+        GemmParams q = p;
+        q.dg_a = a; q.dg_b = bb;
+        q.dg_r0 = ((a + g.pad) % s_ + s_) % s_;
+        q.dg_s0 = ((bb + g.pad) % s_ + s_) % s_;
+        q.dg_nr = q.dg_r0 < g.R ? (g.R - q.dg_r0 + s_ - 1) / s_ : 0;
+        q.dg_ns = q.dg_s0 < g.S ? (g.S - q.dg_s0 + s_ - 1) / s_ : 0;
+        q.Kg = q.dg_nr * q.dg_ns * g.K;
+        if (q.Kg == 0 && accumulate) continue;  // nothing reaches these pixels: dx stays as it is
+        PixBox b = choose_box(g.N, hc, wc, 1);
+        q.tw = b.tw; q.th = b.th; q.tn = b.tn;
+        q.tiles_w = b.tiles_w; q.tiles_h = b.tiles_h; q.tiles_n = b.tiles_n;
+        q.hout = hc; q.wout = wc;
+        q.cchunks = g.K / 32;
+        CUtensorMap ta;
+        if (!map_nhwc(&ta, dy, g.N, g.Ho, g.Wo, g.K, b.tw, b.th, b.tn, 1))
+          return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv dgrad)");
+        dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
+        POOCH_CHECK((launch_bn<CONV_DGRAD, true>(bn, q, grid, st, g.prec, &ta, &tb)));
+      }
+    return POOCH_OK;
   }
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
   return launch_bn<CONV_DGRAD>(bn, p, grid, st, g.prec);

@@ -66,6 +66,10 @@ struct GemmParams {
   // wg_a_is_x = 1: A = im2col(x)^T [R*S*C] and B = dy^T [Cout] (the transposed orientation)
   int wg_a_is_x;
   int wg_cba, wg_cbb;    // 32-channel chunks per TMA box of A / B (5-D maps, chunk index outermost)
+  // TMA-fed DGRAD, one output-parity class (a, b) of a stride-st conv: dx pixels (st*i + a, st*j + b)
+  // receive the taps r = dg_r0 + st*t (t < dg_nr), s = dg_s0 + st*u (u < dg_ns) from dy pixel
+  // (i + (a + pad - r)/st, j + (b + pad - s)/st); stride 1 is the single class a = b = 0
+  int dg_a, dg_b, dg_r0, dg_s0, dg_nr, dg_ns;
 };
 
 constexpr int BM = 128;
@@ -536,15 +540,19 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             uint32_t st = sbase + s * SM::STAGE_BYTES;
             uint64_t* bar = AUX ? &rawfull[s] : &full[s];
             const int k = kb0 + kb;
-            const int rs = k / p.cchunks, cc = k - rs * p.cchunks;
-            const int r = rs / p.S, sx = rs - r * p.S;
-            int cw, chh;
+            const int tap = k / p.cchunks, cc = k - tap * p.cchunks;
+            int cw, chh, rs;
             if (MODE == CONV_FWD) {
+              const int r = tap / p.S, sx = tap - r * p.S;
+              rs = tap;
               cw = tw_i * p.tw * p.stride - p.pad + sx;
               chh = th_i * p.th * p.stride - p.pad + r;
             } else {
-              cw = tw_i * p.tw + p.pad - sx;
-              chh = th_i * p.th + p.pad - r;
+              const int tr = tap / p.dg_ns, ts = tap - tr * p.dg_ns;
+              const int r = p.dg_r0 + p.stride * tr, sx = p.dg_s0 + p.stride * ts;
+              rs = r * p.S + sx;
+              cw = tw_i * p.tw + (p.dg_b + p.pad - sx) / p.stride;   // exact: the class selects the taps
+              chh = th_i * p.th + (p.dg_a + p.pad - r) / p.stride;
             }
             ptx::mbar_arrive_expect_tx(bar, bytes);
             ptx::tma_load_4d(st, &tma_a, bar, cc * 32, cw, chh, tn_i * p.tn);
@@ -676,7 +684,10 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
         const int per = p.tw * p.th;
         const int nn = tn_i * p.tn + row / per, hh = th_i * p.th + (row / p.tw) % p.th, ww = tw_i * p.tw + row % p.tw;
         rok = row < per * p.tn && nn < p.N && hh < p.hout && ww < p.wout;
-        gm = (nn * p.hout + hh) * p.wout + ww;
+        if (MODE == CONV_DGRAD)  // class grid -> dx pixel (st*hh + a, st*ww + b)
+          gm = (nn * p.H + hh * p.stride + p.dg_a) * p.W + ww * p.stride + p.dg_b;
+        else
+          gm = (nn * p.hout + hh) * p.wout + ww;
       }
       const uint32_t taddr = tmem + ab * BN + ((uint32_t)(warp * 32) << 16);
       const int z = t / (tm.mt * tm.nt);

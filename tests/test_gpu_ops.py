@@ -102,7 +102,7 @@ def test_conv_fwd_and_stats(case, prec):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("case", CONV_CASES[1:])
+@pytest.mark.parametrize("case", CONV_CASES)
 @pytest.mark.parametrize("accumulate", [0, 1])
 def test_conv_dgrad(case, accumulate, prec):
     lib = _lib()
