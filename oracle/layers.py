@@ -74,14 +74,138 @@ def conv2d_wgrad(x, dy, w_shape, stride=1, pad=0):
     return dw
 
 
+# ------------------------------------------------------------------------- conv3d
+# 3D workload of BASELINE.json config 4 ("3D U-Net-style, conv3d-BN-ReLU"; the paper's
+# 3D-image motivation). NCDHW layout, cubic kernels.
+def conv3d_out(d: int, k: int, stride: int, pad: int):
+    return (d + 2 * pad - k) // stride + 1
+
+
+def _win3(xp, u, v, t, stride, do, ho, wo):
+    return xp[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
+              t:t + stride * (wo - 1) + 1:stride]
+
+
+def conv3d_fwd(x, w, stride=1, pad=0):
+    """y[n,o,a,i,j] = sum_{c,u,v,t} x[n,c,s*a+u-p, s*i+v-p, s*j+t-p] * w[o,c,u,v,t] (zero padded)."""
+    n, c, d, h, wd = x.shape
+    o, c2, k, _, _ = w.shape
+    assert c == c2
+    do, ho, wo = (conv3d_out(e, k, stride, pad) for e in (d, h, wd))
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad), (pad, pad)))
+    y = np.zeros((n, do, ho, wo, o), dtype=np.float64)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                y += np.tensordot(_win3(xp, u, v, t, stride, do, ho, wo), w[:, :, u, v, t], axes=([1], [1]))
+    return y.transpose(0, 4, 1, 2, 3).copy()
+
+
+def conv3d_dgrad(dy, w, x_shape, stride=1, pad=0):
+    """dx = adjoint of conv3d_fwd w.r.t. x."""
+    n, c, d, h, wd = x_shape
+    o, _, k, _, _ = w.shape
+    _, _, do, ho, wo = dy.shape
+    dxp = np.zeros((n, c, d + 2 * pad, h + 2 * pad, wd + 2 * pad), dtype=np.float64)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                contrib = np.tensordot(dy, w[:, :, u, v, t], axes=([1], [0]))  # [n,do,ho,wo,c]
+                dxp[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
+                    t:t + stride * (wo - 1) + 1:stride] += contrib.transpose(0, 4, 1, 2, 3)
+    return dxp[:, :, pad:pad + d, pad:pad + h, pad:pad + wd].copy()
+
+
+def conv3d_wgrad(x, dy, w_shape, stride=1, pad=0):
+    """dw = adjoint of conv3d_fwd w.r.t. w."""
+    o, c, k, _, _ = w_shape
+    _, _, do, ho, wo = dy.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad), (pad, pad)))
+    dw = np.zeros(w_shape, dtype=np.float64)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                dw[:, :, u, v, t] = np.tensordot(dy, _win3(xp, u, v, t, stride, do, ho, wo),
+                                                 axes=([0, 2, 3, 4], [0, 2, 3, 4]))
+    return dw
+
+
+def upconv3d_fwd(x, w):
+    """Transposed convolution, kernel 2, stride 2 (the U-Net's up-sampling):
+    y[n,o,2a+u,2i+v,2j+t] = sum_c x[n,c,a,i,j] * w[c,o,u,v,t]  -- every output voxel
+    receives exactly one kernel tap. w is [Cin, Cout, 2, 2, 2]."""
+    n, c, d, h, wd = x.shape
+    c2, o = w.shape[:2]
+    assert c == c2
+    y = np.zeros((n, o, 2 * d, 2 * h, 2 * wd), dtype=np.float64)
+    for u in range(2):
+        for v in range(2):
+            for t in range(2):
+                y[:, :, u::2, v::2, t::2] = np.tensordot(x, w[:, :, u, v, t], axes=([1], [0])).transpose(0, 4, 1, 2, 3)
+    return y
+
+
+def upconv3d_bwd(dy, x, w):
+    """Adjoints of upconv3d_fwd: (dx, dw)."""
+    dx = np.zeros_like(x, dtype=np.float64)
+    dw = np.zeros(w.shape, dtype=np.float64)
+    for u in range(2):
+        for v in range(2):
+            for t in range(2):
+                g = dy[:, :, u::2, v::2, t::2]                                   # [n,o,d,h,w]
+                dx += np.tensordot(g, w[:, :, u, v, t], axes=([1], [1])).transpose(0, 4, 1, 2, 3)
+                dw[:, :, u, v, t] = np.tensordot(x, g, axes=([0, 2, 3, 4], [0, 2, 3, 4]))
+    return dx, dw
+
+
+def maxpool3d_fwd(x, k=2, stride=2):
+    """Max over k^3 windows (no padding)."""
+    n, c, d, h, w = x.shape
+    do, ho, wo = ((e - k) // stride + 1 for e in (d, h, w))
+    y = np.full((n, c, do, ho, wo), -np.inf)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                y = np.maximum(y, _win3(x, u, v, t, stride, do, ho, wo))
+    return y
+
+
+def maxpool3d_bwd(dy, x, k=2, stride=2):
+    """Gradient to the FIRST maximum in (u, v, t) row-major window order (Reading 25)."""
+    n, c, d, h, w = x.shape
+    _, _, do, ho, wo = dy.shape
+    best = np.full(dy.shape, -np.inf)
+    arg = np.full(dy.shape, -1, dtype=np.int64)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                win = _win3(x, u, v, t, stride, do, ho, wo)
+                better = win > best
+                best = np.where(better, win, best)
+                arg = np.where(better, (u * k + v) * k + t, arg)
+    dx = np.zeros_like(x, dtype=np.float64)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                dx[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
+                   t:t + stride * (wo - 1) + 1:stride] += dy * (arg == (u * k + v) * k + t)
+    return dx
+
+
 # ----------------------------------------------------------------------------- BN
+def _chan(v, ndim):
+    """Per-channel vector broadcast against an N C spatial... array."""
+    return v.reshape((1, -1) + (1,) * (ndim - 2))
+
+
 def bn_fwd(x, gamma, beta, eps=BN_EPS):
-    """Training-mode BN over (n,h,w) per channel; biased variance."""
-    mu = x.mean(axis=(0, 2, 3))
-    var = ((x - mu[None, :, None, None]) ** 2).mean(axis=(0, 2, 3))
+    """Training-mode BN over (n, spatial...) per channel; biased variance."""
+    ax = (0,) + tuple(range(2, x.ndim))
+    mu = x.mean(axis=ax)
+    var = ((x - _chan(mu, x.ndim)) ** 2).mean(axis=ax)
     invstd = 1.0 / np.sqrt(var + eps)
-    xhat = (x - mu[None, :, None, None]) * invstd[None, :, None, None]
-    y = gamma[None, :, None, None] * xhat + beta[None, :, None, None]
+    xhat = (x - _chan(mu, x.ndim)) * _chan(invstd, x.ndim)
+    y = _chan(gamma, x.ndim) * xhat + _chan(beta, x.ndim)
     return y, (xhat, invstd)
 
 
@@ -89,11 +213,11 @@ def bn_bwd(dy, cache, gamma):
     """Closed form: dbeta = sum dy; dgamma = sum dy*xhat;
     dx = gamma*invstd*(dy - dbeta/N - xhat*dgamma/N)."""
     xhat, invstd = cache
-    m = dy.shape[0] * dy.shape[2] * dy.shape[3]
-    dbeta = dy.sum(axis=(0, 2, 3))
-    dgamma = (dy * xhat).sum(axis=(0, 2, 3))
-    dx = (gamma * invstd)[None, :, None, None] * (
-        dy - dbeta[None, :, None, None] / m - xhat * dgamma[None, :, None, None] / m)
+    ax = (0,) + tuple(range(2, dy.ndim))
+    m = dy.size // dy.shape[1]
+    dbeta = dy.sum(axis=ax)
+    dgamma = (dy * xhat).sum(axis=ax)
+    dx = _chan(gamma * invstd, dy.ndim) * (dy - _chan(dbeta, dy.ndim) / m - xhat * _chan(dgamma, dy.ndim) / m)
     return dx, dgamma, dbeta
 
 

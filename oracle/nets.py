@@ -20,6 +20,13 @@ and is always resident, Reading 2):
 * ``avgpool``   y = mean_hw(x)                 bwd needs {}
 * ``fc_ce``     z = flat(x) W^T + b; CE loss   bwd needs {x, z} (sink task)
 
+3D network (BASELINE.json config 4, "3D U-Net-style, conv3d-BN-ReLU"):
+
+* ``conv`` with two inputs    y = conv3d(concat_c(a, b), W)  bwd needs {a, b}
+* ``upconv``    y = transposed conv3d k2 s2 (up-sampling)     bwd needs {x}
+* ``maxpool``   (3D) k2 s2 over 2x2x2 windows               bwd needs {x}
+* ``head_ce``   z = x W^T + b per voxel; CE averaged over voxels   bwd needs {x, z} (sink)
+
 Flatten order before the FC is (h, w, c) (the GPU's NHWC order); both sides
 use it, so FC weights are shared verbatim.
 """
@@ -39,7 +46,7 @@ class Task:
     name: str
     kind: str
     inputs: list            # map ids (task ids), -1 = network input
-    out_chw: tuple          # per-image output shape (C, H, W); FC/avgpool: (C, 1, 1)
+    out_chw: tuple          # per-image output shape (C, H, W) -- (C, D, H, W) in 3D nets; FC/avgpool: (C, 1, 1)
     stride: int = 1
     pad: int = 0
     k: int = 0              # conv/pool kernel size
@@ -48,13 +55,13 @@ class Task:
     @property
     def needs(self):
         """Maps bwd(task) reads (see module docstring)."""
-        if self.kind in ("conv", "maxpool"):
+        if self.kind in ("conv", "maxpool", "upconv"):
             return [i for i in self.inputs if i >= 0]
         if self.kind in ("bnrelu", "tail_proj", "tail_id"):
             return [i for i in self.inputs if i >= 0]
         if self.kind == "avgpool":
             return []
-        if self.kind == "fc_ce":
+        if self.kind in ("fc_ce", "head_ce"):
             return None     # filled by Net (self id needed)
         raise ValueError(self.kind)
 
@@ -62,9 +69,13 @@ class Task:
 @dataclass
 class Net:
     name: str
-    in_chw: tuple           # (C, H, W) of the network input, unpadded
+    in_chw: tuple           # (C, H, W) of the network input, unpadded; (C, D, H, W) in 3D
     classes: int
     tasks: list = field(default_factory=list)
+
+    @property
+    def dims(self):
+        return len(self.in_chw) - 1
 
     def add(self, t: Task) -> int:
         self.tasks.append(t)
@@ -72,13 +83,12 @@ class Net:
 
     def needs(self, i):
         t = self.tasks[i]
-        if t.kind == "fc_ce":
+        if t.kind in ("fc_ce", "head_ce"):
             return sorted([j for j in t.inputs if j >= 0] + [i])
         return sorted(t.needs)
 
     def map_bytes_per_image(self, i):
-        c, h, w = self.tasks[i].out_chw
-        return 4 * c * h * w
+        return 4 * int(np.prod(self.tasks[i].out_chw))
 
 
 # ------------------------------------------------------------------ builders
@@ -131,6 +141,41 @@ def resnet50(in_hw: int = 224, classes: int = 1000, v15: bool = True) -> Net:
     return net
 
 
+def unet3d(in_d: int = 256, width: int = 256, classes: int = 2, cin: int = 1) -> Net:
+    """BASELINE.json config 4 / SURVEY 8(d): a 3D U-Net -- 4 levels of widths w, 2w, 4w,
+    4w (256/512/1024/1024 at w = 256), each 2 x [conv3d 3^3 -> BN -> ReLU]; 2^3 max-pool
+    between levels; a 4w bottleneck; decoder levels up-sample with a k2 s2 transposed conv
+    to the level's width, concatenate the skip (read as a second input of the first conv)
+    and apply 2 x [conv3d -> BN -> ReLU]; a 1^3 head to ``classes`` with per-voxel softmax
+    cross-entropy. 45 maps; 207.2 GB at 256^3."""
+    net = Net("unet3d", (cin, in_d, in_d, in_d), classes)
+    widths = [width, 2 * width, 4 * width, 4 * width]
+    src, c, e = -1, cin, in_d
+    skips = []
+
+    def block(pre, x, cin_, w, e_):
+        c1 = net.add(Task(pre + ".conv1", "conv", x, (w, e_, e_, e_), 1, 1, 3, cin_))
+        y1 = net.add(Task(pre + ".bn1", "bnrelu", [c1], (w, e_, e_, e_)))
+        c2 = net.add(Task(pre + ".conv2", "conv", [y1], (w, e_, e_, e_), 1, 1, 3, w))
+        return net.add(Task(pre + ".bn2", "bnrelu", [c2], (w, e_, e_, e_)))
+
+    for lv, w in enumerate(widths):
+        y = block(f"enc{lv + 1}", [src], c, w, e)
+        skips.append((y, w, e))
+        e //= 2
+        src = net.add(Task(f"pool{lv + 1}", "maxpool", [y], (w, e, e, e), 2, 0, 2))
+        c = w
+    src = block("mid", [src], c, widths[-1], e)
+    c = widths[-1]
+    for lv in reversed(range(4)):
+        sk, w, e = skips[lv]
+        u = net.add(Task(f"up{lv + 1}", "upconv", [src], (w, e, e, e), 2, 0, 2, c))
+        src = block(f"dec{lv + 1}", [u, sk], 2 * w, w, e)
+        c = w
+    net.add(Task("head", "head_ce", [src], (classes, e, e, e), cin=c))
+    return net
+
+
 # -------------------------------------------------------------------- census
 def census(net: Net, batch: int):
     """[(name, bytes)] of every saved feature map (C2)."""
@@ -142,7 +187,9 @@ def param_shapes(net: Net):
     shapes = {}
     for t in net.tasks:
         if t.kind == "conv":
-            shapes[t.name + ".w"] = (t.out_chw[0], t.cin, t.k, t.k)
+            shapes[t.name + ".w"] = (t.out_chw[0], t.cin) + (t.k,) * (len(t.out_chw) - 1)
+        elif t.kind == "upconv":
+            shapes[t.name + ".w"] = (t.cin, t.out_chw[0], 2, 2, 2)
         elif t.kind == "bnrelu":
             shapes[t.name + ".gamma"] = (t.out_chw[0],)
             shapes[t.name + ".beta"] = (t.out_chw[0],)
@@ -152,7 +199,7 @@ def param_shapes(net: Net):
             if t.kind == "tail_proj":
                 shapes[t.name + ".gammap"] = (t.out_chw[0],)
                 shapes[t.name + ".betap"] = (t.out_chw[0],)
-        elif t.kind == "fc_ce":
+        elif t.kind in ("fc_ce", "head_ce"):
             shapes[t.name + ".w"] = (t.out_chw[0], t.cin)
             shapes[t.name + ".b"] = (t.out_chw[0],)
     return shapes
@@ -174,17 +221,33 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
     kernels' operand precision -- and keeps everything else in fp64."""
     q = L.tf32 if precision == "tf32" else (lambda a: a)
     P = {k: np.asarray(v, dtype=np.float64) for k, v in params.items()}
-    x_in = np.asarray(x_nhwc, dtype=np.float64).transpose(0, 3, 1, 2)
+    x_np = np.asarray(x_nhwc, dtype=np.float64)
+    x_in = np.moveaxis(x_np, -1, 1)          # N(D)HWC -> NC(D)HW
+    three = net.dims == 3
     outs, caches = [], []
 
     def get(i):
         return x_in if i < 0 else outs[i]
 
+    def conv_in(t):   # a conv with two inputs reads their channel concatenation
+        return np.concatenate([get(i) for i in t.inputs], axis=1) if len(t.inputs) > 1 else get(t.inputs[0])
+
     loss = None
     for t in net.tasks:
         if t.kind == "conv":
-            y = L.conv2d_fwd(q(get(t.inputs[0])), q(P[t.name + ".w"]), t.stride, t.pad)
+            f = L.conv3d_fwd if three else L.conv2d_fwd
+            y = f(q(conv_in(t)), q(P[t.name + ".w"]), t.stride, t.pad)
             cache = None
+        elif t.kind == "upconv":
+            y = L.upconv3d_fwd(q(get(t.inputs[0])), q(P[t.name + ".w"]))
+            cache = None
+        elif t.kind == "head_ce":
+            xin = get(t.inputs[0])
+            xf = np.moveaxis(xin, 1, -1).reshape(-1, xin.shape[1])         # [voxels, C]
+            z = L.fc_fwd(q(xf), q(P[t.name + ".w"]), P[t.name + ".b"])
+            loss, dz = L.softmax_ce(z, np.asarray(labels).reshape(-1))
+            y = np.moveaxis(z.reshape(xin.shape[:1] + xin.shape[2:] + (z.shape[1],)), -1, 1)
+            cache = (xf, dz)
         elif t.kind == "bnrelu":
             z, bc = L.bn_fwd(get(t.inputs[0]), P[t.name + ".gamma"], P[t.name + ".beta"])
             y = L.relu_fwd(z)
@@ -198,7 +261,8 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             y = L.relu_fwd(z3 + zp)
             cache = (bc3, bcp)
         elif t.kind == "maxpool":
-            y = L.maxpool_fwd(get(t.inputs[0]), t.k, t.stride, t.pad)
+            y = (L.maxpool3d_fwd(get(t.inputs[0]), t.k, t.stride) if three
+                 else L.maxpool_fwd(get(t.inputs[0]), t.k, t.stride, t.pad))
             cache = None
         elif t.kind == "avgpool":
             y = L.avgpool_fwd(get(t.inputs[0]))[:, :, None, None]
@@ -235,13 +299,31 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             n, c, h, w = src.shape
             acc(t.inputs[0], dxf.reshape(n, h, w, c).transpose(0, 3, 1, 2))
             continue
+        if t.kind == "head_ce":
+            xf, dz = cache
+            dxf, dw, _ = L.fc_bwd(q(dz), q(xf), q(P[t.name + ".w"]))
+            grads[t.name + ".w"] += dw
+            grads[t.name + ".b"] += dz.sum(axis=0)
+            src = get(t.inputs[0])
+            acc(t.inputs[0], np.moveaxis(dxf.reshape(src.shape[:1] + src.shape[2:] + (src.shape[1],)), -1, 1))
+            continue
         dy = gmap[i]
         if t.kind == "conv":
-            xin = get(t.inputs[0])
+            xin = conv_in(t)
             w = P[t.name + ".w"]
-            grads[t.name + ".w"] += L.conv2d_wgrad(q(xin), q(dy), w.shape, t.stride, t.pad)
+            fw, fd = (L.conv3d_wgrad, L.conv3d_dgrad) if three else (L.conv2d_wgrad, L.conv2d_dgrad)
+            grads[t.name + ".w"] += fw(q(xin), q(dy), w.shape, t.stride, t.pad)
             if t.inputs[0] >= 0:
-                acc(t.inputs[0], L.conv2d_dgrad(q(dy), q(w), xin.shape, t.stride, t.pad))
+                dx = fd(q(dy), q(w), xin.shape, t.stride, t.pad)
+                c0 = 0
+                for j in t.inputs:          # split the concatenation's gradient per input
+                    cj = get(j).shape[1]
+                    acc(j, dx[:, c0:c0 + cj])
+                    c0 += cj
+        elif t.kind == "upconv":
+            dx, dw = L.upconv3d_bwd(q(dy), q(get(t.inputs[0])), q(P[t.name + ".w"]))
+            grads[t.name + ".w"] += dw
+            acc(t.inputs[0], dx)
         elif t.kind == "bnrelu":
             dz = L.relu_bwd(dy, outs[i])
             dx, dg, db = L.bn_bwd(dz, cache[0], P[t.name + ".gamma"])
@@ -262,7 +344,8 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             else:
                 acc(t.inputs[1], dz)
         elif t.kind == "maxpool":
-            acc(t.inputs[0], L.maxpool_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad))
+            acc(t.inputs[0], L.maxpool3d_bwd(dy, get(t.inputs[0]), t.k, t.stride) if three
+                else L.maxpool_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad))
         elif t.kind == "avgpool":
             acc(t.inputs[0], L.avgpool_bwd(dy[:, :, 0, 0], get(t.inputs[0]).shape))
     if map_grads is not None:
