@@ -76,8 +76,14 @@ typedef enum {
   POOCH_L_TAIL_ID = 3,   /* y = relu(BN3(c3) + x)                        bwd reads {c3, x}  */
   POOCH_L_MAXPOOL = 4,   /* y = maxpool(x)                               bwd reads {x}      */
   POOCH_L_AVGPOOL = 5,   /* y = mean_hw(x)                               bwd reads {}       */
-  POOCH_L_FC_CE = 6      /* z = flat_hwc(x) W^T + b, softmax-CE loss     bwd reads {x, z}   */
+  POOCH_L_FC_CE = 6,     /* z = flat_hwc(x) W^T + b, softmax-CE loss     bwd reads {x, z}   */
+  POOCH_L_UPCONV = 7,    /* y = transposed conv k2 s2 of x (3D U-Net up-sampling)  bwd reads {x} */
+  POOCH_L_HEAD_CE = 8    /* z = x W^T + b per voxel, softmax-CE averaged over voxels  bwd reads {x, z} */
 } pooch_layer_kind;
+/* A POOCH_L_CONV with in1 >= 0 reads the channel concatenation [in0, in1] in place (the
+ * U-Net's skip connection): cin = cout(in0) + cout(in1), both multiples of 32.
+ * 3D networks (io.in_d > 0, batch 1): every conv is k x k x k; maxpool is k2 s2 p0 over 2^3
+ * windows; UPCONV has k = stride = 2 and doubles each spatial extent. */
 
 typedef struct {
   int32_t kind;          /* pooch_layer_kind */
@@ -86,17 +92,21 @@ typedef struct {
   int32_t cout, hout, wout; /* output map shape per image (C, H, W) */
   int32_t k, stride, pad;   /* conv / pool geometry */
   char name[48];
+  int32_t dout;             /* output depth of a 3D network's map (0 in 2D networks) */
 } pooch_layer_desc;
 
 typedef struct {
   int32_t batch;         /* per-rank batch */
   int32_t in_c, in_h, in_w; /* network input, in_c padded to a multiple of 4 */
   int32_t classes;
+  int32_t in_d;          /* 0: 2D network (NHWC input); > 0: 3D network, input [batch, in_d, in_h, in_w, in_c] */
 } pooch_io_desc;
 
 /* Built-in workloads of BASELINE.json: 0 = tiny CNN (config 1), 1 = ResNet-50 v1.5
- * (configs 2, 3, 5), 2 = ResNet-50 v1. Fills up to *n_layers entries of `out` (host) and
- * sets *n_layers to the task count (call with out=NULL to query). */
+ * (configs 2, 3, 5), 2 = ResNet-50 v1, 3 = 3D U-Net (config 4: in_hw^3 volume, base width
+ * `width` -> level widths w, 2w, 4w, 4w, input channels padded 1 -> 32). Fills up to
+ * *n_layers entries of `out` (host) and sets *n_layers to the task count (call with
+ * out=NULL to query). */
 pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t classes, int32_t width,
                              pooch_layer_desc* out, int32_t* n_layers);
 
@@ -136,8 +146,9 @@ pooch_status pooch_set_comm(pooch_ctx* ctx, const void* nccl_unique_id, int32_t 
  * profile and the plan. */
 pooch_status pooch_set_precision(pooch_ctx* ctx, int32_t precision);
 
-/* Input slot inside the device arena: x_dev [batch, in_h, in_w, in_c] fp32, labels_dev
- * [batch] int32. Valid after pooch_set_budget. */
+/* Input slot inside the device arena: x_dev [batch, in_h, in_w, in_c] fp32 (3D networks:
+ * [batch, in_d, in_h, in_w, in_c]), labels_dev [batch] int32 (POOCH_L_HEAD_CE networks: one
+ * label per output voxel, [batch, d, h, w]). Valid after pooch_set_budget. */
 pooch_status pooch_input_slot(pooch_ctx* ctx, float** x_dev, int32_t** labels_dev);
 
 /* ------------------------------------------------------------------------- parameters */
@@ -308,6 +319,10 @@ pooch_status pooch_family_stats(pooch_ctx* ctx, int32_t family, double* time_ms,
 typedef struct {
   int32_t N, H, W, C, K, R, S, stride, pad;
   int32_t precision;  /* 0: TF32 operands (1 MMA per k-step); 1: 3xTF32 split, ~fp32-faithful */
+  int32_t D;          /* 0: 2D. > 0: 3D conv3d over x[1,D,H,W,C] (N must be 1), kernel R^3,
+                         weights [K,R,R,R,C]; requires C, K multiples of 32 (TMA-fed kernels) */
+  int32_t C1;         /* 0: one input. > 0: the input is the channel concatenation of two
+                         tensors x0 [..,C1] and x1 [..,C-C1] (the *2 entry points); C1 % 32 == 0 */
 } pooch_conv_desc;
 
 pooch_status pooch_op_conv_fwd(const pooch_conv_desc* d, const float* x, const float* w, float* y,
@@ -317,6 +332,14 @@ pooch_status pooch_op_conv_dgrad(const pooch_conv_desc* d, const float* dy, cons
 pooch_status pooch_op_conv_wgrad(const pooch_conv_desc* d, const float* x, const float* dy, float* dw,
                                  float* ws, size_t ws_bytes, void* stream);
 size_t pooch_op_conv_wgrad_ws_bytes(const pooch_conv_desc* d);
+/* Two-source variants (d->C1 > 0): the convolution's input is concat_c(x0, x1), read in place
+ * (never materialised); dgrad writes (or accumulates into, per destination) dx0 and dx1. */
+pooch_status pooch_op_conv_fwd2(const pooch_conv_desc* d, const float* x0, const float* x1, const float* w, float* y,
+                                float* stat_sum, float* stat_sq, void* stream);
+pooch_status pooch_op_conv_dgrad2(const pooch_conv_desc* d, const float* dy, const float* wt, float* dx0, float* dx1,
+                                  int32_t accumulate0, int32_t accumulate1, void* stream);
+pooch_status pooch_op_conv_wgrad2(const pooch_conv_desc* d, const float* x0, const float* x1, const float* dy,
+                                  float* dw, float* ws, size_t ws_bytes, void* stream);
 /* Number of M-tiles (rows of the partial-sum arrays) of pooch_op_conv_fwd for `d`. */
 int64_t pooch_op_conv_stat_tiles(const pooch_conv_desc* d);
 /* D[split][M][N] = A * B^T on the tensor-core core, A [M][K] and B [N][K] row-major (K-major);

@@ -33,17 +33,18 @@ P = C.POINTER
 
 
 class ConvDesc(C.Structure):
-    _fields_ = [(n, c_i32) for n in ("N", "H", "W", "C", "K", "R", "S", "stride", "pad", "precision")]
+    _fields_ = [(n, c_i32) for n in ("N", "H", "W", "C", "K", "R", "S", "stride", "pad", "precision", "D", "C1")]
 
 
 class LayerDesc(C.Structure):
     _fields_ = [("kind", c_i32), ("in0", c_i32), ("in1", c_i32), ("cin", c_i32), ("cout", c_i32),
                 ("hout", c_i32), ("wout", c_i32), ("k", c_i32), ("stride", c_i32), ("pad", c_i32),
-                ("name", C.c_char * 48)]
+                ("name", C.c_char * 48), ("dout", c_i32)]
 
 
 class IODesc(C.Structure):
-    _fields_ = [("batch", c_i32), ("in_c", c_i32), ("in_h", c_i32), ("in_w", c_i32), ("classes", c_i32)]
+    _fields_ = [("batch", c_i32), ("in_c", c_i32), ("in_h", c_i32), ("in_w", c_i32), ("classes", c_i32),
+                ("in_d", c_i32)]
 
 
 class ProfileT(C.Structure):
@@ -112,6 +113,9 @@ SIGNATURES = {
     "pooch_op_conv_wgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pooch_op_conv_wgrad_ws_bytes": (c_sz, [P(ConvDesc)]),
     "pooch_op_conv_stat_tiles": (c_i64, [P(ConvDesc)]),
+    "pooch_op_conv_fwd2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pooch_op_conv_dgrad2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "pooch_op_conv_wgrad2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pooch_op_gemm_test": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
 }
 

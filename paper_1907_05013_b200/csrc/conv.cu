@@ -1,5 +1,10 @@
 // conv.cu -- launchers for the tcgen05 implicit-GEMM convolution passes (fwd, dgrad, wgrad)
 // and the FC layer (a 1x1 "conv" on a 1x1 image), plus the split-K reduction of wgrad.
+//
+// 2D convs use NHWC activations and KRSC weights; 3D convs (BASELINE config 4, batch 1) use
+// DHWC activations and KTRSC weights: the fourth TMA dimension is the image index in 2D and
+// the depth (with its own taps, stride and padding) in 3D. A conv may read the channel
+// concatenation of two tensors in place (the U-Net's skip connections).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -19,19 +24,30 @@ ConvGeom conv_geom(const pooch_conv_desc& d) {
   ConvGeom g{d.N, d.H, d.W, d.C, d.K, d.R, d.S, d.stride, d.pad, 0, 0, d.precision};
   g.Ho = (d.H + 2 * d.pad - d.R) / d.stride + 1;
   g.Wo = (d.W + 2 * d.pad - d.S) / d.stride + 1;
+  g.D = d.D;
+  g.Do = d.D > 0 ? (d.D + 2 * d.pad - d.R) / d.stride + 1 : 0;
+  g.C1 = d.C1;
   return g;
 }
 
 bool conv_shape_ok(const ConvGeom& g) {
-  return g.N > 0 && g.H > 0 && g.W > 0 && g.C > 0 && g.K > 0 && g.R > 0 && g.S > 0 && g.stride > 0 &&
-         g.pad >= 0 && g.C % 4 == 0 && g.K % 4 == 0 && g.Ho > 0 && g.Wo > 0;
+  bool ok = g.N > 0 && g.H > 0 && g.W > 0 && g.C > 0 && g.K > 0 && g.R > 0 && g.S > 0 && g.stride > 0 &&
+            g.pad >= 0 && g.C % 4 == 0 && g.K % 4 == 0 && g.Ho > 0 && g.Wo > 0;
+  if (g.is3d() || g.C1 > 0) {
+    // the 3D / two-source convs run only on the TMA-fed kernels (the launchers fail with
+    // POOCH_EUSAGE if the driver offers no tensor maps); this check is structural
+    ok = ok && g.C % 32 == 0 && g.K % 32 == 0 && g.stride <= 2;
+    if (g.is3d()) ok = ok && g.N == 1 && g.R == g.S && g.Do > 0;
+    if (g.C1 > 0) ok = ok && g.C1 % 32 == 0 && g.C1 < g.C;
+  }
+  return ok;
 }
 
 static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
 template <int MODE, int BN, bool X3 = false, bool TMA = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
-                                 const CUtensorMap* tb = nullptr) {
+                                 const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr) {
   // deepest ring that fits 227 KB: TMA wgrad has the longest load -> MMA latency (TMA, then an
   // in-place transpose by the auxiliary warps), so it gets every stage that fits
   constexpr int STAGE_B = (BM + BN) * BK * 4 * (X3 ? 2 : 1);
@@ -48,30 +64,37 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   int64_t tiles = (int64_t)grid.x * grid.y * grid.z;
   int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
-  kern<<<ctas, igemm_threads(MODE, X3), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map);
+  kern<<<ctas, igemm_threads(MODE, X3), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
+                                                      tc ? *tc : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
 
 template <int MODE, bool TMA = false>
 static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st, int prec = 0,
-                              const CUtensorMap* ta = nullptr, const CUtensorMap* tb = nullptr) {
+                              const CUtensorMap* ta = nullptr, const CUtensorMap* tb = nullptr,
+                              const CUtensorMap* tc = nullptr) {
   if (prec) {
     switch (bn) {
-      case 64: return launch_igemm<MODE, 64, true, TMA>(p, grid, st, ta, tb);
-      case 128: return launch_igemm<MODE, 128, true, TMA>(p, grid, st, ta, tb);
+      case 64: return launch_igemm<MODE, 64, true, TMA>(p, grid, st, ta, tb, tc);
+      case 128: return launch_igemm<MODE, 128, true, TMA>(p, grid, st, ta, tb, tc);
     }
     return fail(POOCH_EUSAGE, "3xTF32 supports tile widths 64 / 128 (got %d)", bn);
   }
   switch (bn) {
-    case 64: return launch_igemm<MODE, 64, false, TMA>(p, grid, st, ta, tb);
-    case 128: return launch_igemm<MODE, 128, false, TMA>(p, grid, st, ta, tb);
-    case 256: return launch_igemm<MODE, 256, false, TMA>(p, grid, st, ta, tb);
+    case 64: return launch_igemm<MODE, 64, false, TMA>(p, grid, st, ta, tb, tc);
+    case 128: return launch_igemm<MODE, 128, false, TMA>(p, grid, st, ta, tb, tc);
+    case 256: return launch_igemm<MODE, 256, false, TMA>(p, grid, st, ta, tb, tc);
   }
   return fail(POOCH_EUSAGE, "bad tile width %d", bn);
 }
 
 // ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
+static bool tma_enabled() {
+  static int on = getenv("POOCH_NO_TMA") ? 0 : 1;
+  return on != 0 && encode_fn() != nullptr;
+}
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -85,29 +108,32 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 4-D NHWC activation map: dims {C, W, H, N}; box {32, tw*st, th*st, tn}, traversal stride st.
-static bool map_nhwc(CUtensorMap* m, const float* base, int N, int H, int W, int C, int tw, int th, int tn, int st) {
+// Activation map: dims {C, W, H, N3} (N3 = images in 2D, depth in 3D); box {32, tw*st, th*st,
+// tn*st3}, traversal strides {1, st, st, st3}.
+static bool map_act(CUtensorMap* m, const float* base, int N3, int H, int W, int C, int tw, int th, int tn, int st,
+                    int st3) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N3};
   cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
-  cuuint32_t box[4] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)tn};
-  cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)(tn * st3)};
+  cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, (cuuint32_t)st3};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
-// 5-D view of an NHWC activation for wgrad: dims {32, W, H, N, C/32} (the 32-channel chunk index
-// outermost, stride 128 B); box {32, tw*st, th*st, tn, cb} lands as cb consecutive [pixel][32] blocks.
-static bool map_nhwc_chunks(CUtensorMap* m, const float* base, int N, int H, int W, int C, int tw, int th, int tn,
-                            int st, int cb) {
+// 5-D view of an activation for wgrad: dims {32, W, H, N3, C/32} (the 32-channel chunk index
+// outermost, stride 128 B); box {32, tw*st, th*st, tn*st3, cb} lands as cb consecutive
+// [pixel][32] blocks.
+static bool map_act_chunks(CUtensorMap* m, const float* base, int N3, int H, int W, int C, int tw, int th, int tn,
+                           int st, int st3, int cb) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[5] = {32, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)(C / 32)};
+  cuuint64_t dims[5] = {32, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N3, (cuuint64_t)(C / 32)};
   cuuint64_t strides[4] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4, 128};
-  cuuint32_t box[5] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)tn, (cuuint32_t)cb};
-  cuuint32_t es[5] = {1, (cuuint32_t)st, (cuuint32_t)st, 1, 1};
+  cuuint32_t box[5] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)(tn * st3), (cuuint32_t)cb};
+  cuuint32_t es[5] = {1, (cuuint32_t)st, (cuuint32_t)st, (cuuint32_t)st3, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
@@ -126,25 +152,26 @@ static bool map_2d(CUtensorMap* m, const float* base, int rows, int cols, int bn
          CUDA_SUCCESS;
 }
 
-// Output-pixel box per M-tile: maximise useful rows / (tiles * 128).
+// Output-pixel box per M-tile: maximise useful rows / (tiles * 128). In 2D the box spans several
+// images only when it covers whole image heights; in 3D it is any w x h x d box.
 struct PixBox {
   int tw, th, tn, tiles_w, tiles_h, tiles_n;
 };
-static PixBox choose_box(int N, int Ho, int Wo, int st) {
+static PixBox choose_box(int N3, int Ho, int Wo, int st, int st3, bool three) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, PixBox> cache;
+  static std::map<std::tuple<int, int, int, int, int, int>, PixBox> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(N, Ho, Wo, st);
+  auto key = std::make_tuple(N3, Ho, Wo, st, st3, (int)three);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  PixBox best{1, 1, 1, Wo, Ho, N};
+  PixBox best{1, 1, 1, Wo, Ho, N3};
   double best_eff = -1;
   for (int tw = 1; tw <= std::min(Wo, 128) && tw * st <= 256; ++tw)
     for (int th = 1; th <= std::min(Ho, 128 / tw) && th * st <= 256; ++th) {
-      int tnmax = th >= Ho ? std::min(std::min(N, 256), 128 / (tw * th)) : 1;
+      int tnmax = (three || th >= Ho) ? std::min(std::min(N3, 256 / st3), 128 / (tw * th)) : 1;
       for (int tn = 1; tn <= tnmax; ++tn) {
-        int tx = (Wo + tw - 1) / tw, ty = (Ho + th - 1) / th, tz = (N + tn - 1) / tn;
-        double eff = (double)N * Ho * Wo / ((double)tx * ty * tz * 128.0);
+        int tx = (Wo + tw - 1) / tw, ty = (Ho + th - 1) / th, tz = (N3 + tn - 1) / tn;
+        double eff = (double)N3 * Ho * Wo / ((double)tx * ty * tz * 128.0);
         if (eff > best_eff + 1e-12 || (std::abs(eff - best_eff) <= 1e-12 && tw > best.tw)) {
           best_eff = eff;
           best = PixBox{tw, th, tn, tx, ty, tz};
@@ -153,11 +180,6 @@ static PixBox choose_box(int N, int Ho, int Wo, int st) {
     }
   cache[key] = best;
   return best;
-}
-
-static bool tma_enabled() {
-  static int on = getenv("POOCH_NO_TMA") ? 0 : 1;
-  return on != 0 && encode_fn() != nullptr;
 }
 
 static bool fwd_uses_tma(const ConvGeom& g) { return tma_enabled() && g.C % 32 == 0 && g.stride <= 2; }
@@ -172,85 +194,115 @@ static GemmParams base_params(const ConvGeom& g) {
   p.N = g.N; p.H = g.H; p.W = g.W; p.C = g.C;
   p.K = g.K; p.R = g.R; p.S = g.S;
   p.Ho = g.Ho; p.Wo = g.Wo; p.stride = g.stride; p.pad = g.pad;
+  p.T = g.T();
+  p.st3 = g.is3d() ? g.stride : 1;
+  p.pad3 = g.is3d() ? g.pad : 0;
+  p.dg_nt = 1;
   return p;
 }
 
+// fourth-dimension extents of the input and output grids
+static int in3(const ConvGeom& g) { return g.is3d() ? g.D : g.N; }
+static int out3(const ConvGeom& g) { return g.is3d() ? g.Do : g.N; }
+static int64_t out_pixels(const ConvGeom& g) { return (int64_t)out3(g) * g.Ho * g.Wo; }
+
 int conv_stat_tiles(const ConvGeom& g) {
   if (fwd_uses_tma(g)) {
-    PixBox b = choose_box(g.N, g.Ho, g.Wo, g.stride);
+    PixBox b = choose_box(out3(g), g.Ho, g.Wo, g.stride, g.is3d() ? g.stride : 1, g.is3d());
     return b.tiles_w * b.tiles_h * b.tiles_n;
   }
-  return (g.N * g.Ho * g.Wo + 127) / 128;
+  return (int)((out_pixels(g) + 127) / 128);
 }
 
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
-                             float* stat_sq, const float* bias, cudaStream_t st) {
+                             float* stat_sq, const float* bias, cudaStream_t st, const float* x1) {
   GemmParams p = base_params(g);
-  p.M = g.N * g.Ho * g.Wo;
+  p.M = (int)out_pixels(g);
   p.Ng = g.K;
-  p.Kg = g.R * g.S * g.C;
+  p.Kg = g.T() * g.R * g.S * g.C;
   p.a = x; p.b = w; p.d = y;
   p.stat_sum = stat_sum; p.stat_sq = stat_sq; p.bias = bias;
   int bn = pick_bn(g.K, g.prec);
   if (fwd_uses_tma(g)) {
-    PixBox b = choose_box(g.N, g.Ho, g.Wo, g.stride);
+    const int st3 = p.st3;
+    PixBox b = choose_box(out3(g), g.Ho, g.Wo, g.stride, st3, g.is3d());
     p.tw = b.tw; p.th = b.th; p.tn = b.tn;
     p.tiles_w = b.tiles_w; p.tiles_h = b.tiles_h; p.tiles_n = b.tiles_n;
-    p.hout = g.Ho; p.wout = g.Wo;
+    p.hout = g.Ho; p.wout = g.Wo; p.n3 = out3(g);
     p.cchunks = g.C / 32;
-    CUtensorMap ta, tb;
-    if (!map_nhwc(&ta, x, g.N, g.H, g.W, g.C, b.tw, b.th, b.tn, g.stride) ||
-        !map_2d(&tb, w, g.K, g.R * g.S * g.C, bn))
+    const int c0 = g.C1 > 0 ? g.C1 : g.C;
+    CUtensorMap ta, tb, tc;
+    if (!map_act(&ta, x, in3(g), g.H, g.W, c0, b.tw, b.th, b.tn, g.stride, st3) ||
+        !map_2d(&tb, w, g.K, g.T() * g.R * g.S * g.C, bn))
       return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv fwd)");
+    if (g.C1 > 0) {
+      p.c_split = g.C1;
+      if (!map_act(&tc, x1, in3(g), g.H, g.W, g.C - g.C1, b.tw, b.th, b.tn, g.stride, st3))
+        return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv fwd, second source)");
+    }
     dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
-    return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb);
+    return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb, g.C1 > 0 ? &tc : nullptr);
   }
+  if (g.is3d() || g.C1 > 0) return fail(POOCH_EUSAGE, "3D / two-source conv needs the TMA path");
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
   return launch_bn<CONV_FWD>(bn, p, grid, st, g.prec);
 }
 
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
-                               cudaStream_t st) {
+                               cudaStream_t st, float* dx1, bool accumulate1) {
   GemmParams p = base_params(g);
-  p.M = g.N * g.H * g.W;
+  p.M = (int)((int64_t)in3(g) * g.H * g.W);
   p.Ng = g.C;
-  p.Kg = g.R * g.S * g.K;
+  p.Kg = g.T() * g.R * g.S * g.K;
   p.a = dy; p.b = wt; p.d = dx;
   p.accumulate = accumulate ? 1 : 0;
+  if (g.C1 > 0) {
+    p.n_split = g.C1;
+    p.d2 = dx1;
+    p.accumulate2 = accumulate1 ? 1 : 0;
+  }
   int bn = pick_bn(g.C, g.prec);
   if (dgrad_uses_tma(g)) {
-    // stride st: one launch per output-parity class (a, b); each is a stride-1 correlation of dy
-    // with the taps of that class (sub-pixel decomposition), so every A box is a dense dy box.
+    // stride st: one launch per output-parity class (a, b[, c]); each is a stride-1 correlation of
+    // dy with the taps of that class (sub-pixel decomposition), so every A box is a dense dy box.
     // A class with no taps (e.g. odd pixels of a 1x1 stride-2 conv) runs with K = 0: its epilogue
     // stores zeros (or leaves dx unchanged when accumulating).
-    const int s_ = g.stride;
+    const int s_ = g.stride, s3 = p.st3;
     CUtensorMap tb;
-    if (!map_2d(&tb, wt, g.C, g.R * g.S * g.K, bn)) return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (dgrad W)");
-    for (int a = 0; a < s_; ++a)
-      for (int bb = 0; bb < s_; ++bb) {
-        const int hc = (g.H - a + s_ - 1) / s_, wc = (g.W - bb + s_ - 1) / s_;
-        if (hc <= 0 || wc <= 0) continue;
-        GemmParams q = p;
-        q.dg_a = a; q.dg_b = bb;
-        q.dg_r0 = ((a + g.pad) % s_ + s_) % s_;
-        q.dg_s0 = ((bb + g.pad) % s_ + s_) % s_;
-        q.dg_nr = q.dg_r0 < g.R ? (g.R - q.dg_r0 + s_ - 1) / s_ : 0;
-        q.dg_ns = q.dg_s0 < g.S ? (g.S - q.dg_s0 + s_ - 1) / s_ : 0;
-        q.Kg = q.dg_nr * q.dg_ns * g.K;
-        if (q.Kg == 0 && accumulate) continue;  // nothing reaches these pixels: dx stays as it is
-        PixBox b = choose_box(g.N, hc, wc, 1);
-        q.tw = b.tw; q.th = b.th; q.tn = b.tn;
-        q.tiles_w = b.tiles_w; q.tiles_h = b.tiles_h; q.tiles_n = b.tiles_n;
-        q.hout = hc; q.wout = wc;
-        q.cchunks = g.K / 32;
-        CUtensorMap ta;
-        if (!map_nhwc(&ta, dy, g.N, g.Ho, g.Wo, g.K, b.tw, b.th, b.tn, 1))
-          return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv dgrad)");
-        dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
-        POOCH_CHECK((launch_bn<CONV_DGRAD, true>(bn, q, grid, st, g.prec, &ta, &tb)));
-      }
+    if (!map_2d(&tb, wt, g.C, g.T() * g.R * g.S * g.K, bn))
+      return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (dgrad W)");
+    auto first_tap = [](int cls, int pad, int st_) { return ((cls + pad) % st_ + st_) % st_; };
+    auto ntaps = [](int t0, int k, int st_) { return t0 < k ? (k - t0 + st_ - 1) / st_ : 0; };
+    for (int cz = 0; cz < s3; ++cz)
+      for (int a = 0; a < s_; ++a)
+        for (int bb = 0; bb < s_; ++bb) {
+          const int dc = g.is3d() ? (g.D - cz + s3 - 1) / s3 : g.N;
+          const int hc = (g.H - a + s_ - 1) / s_, wc = (g.W - bb + s_ - 1) / s_;
+          if (hc <= 0 || wc <= 0 || dc <= 0) continue;
+          GemmParams q = p;
+          q.dg_a = a; q.dg_b = bb; q.dg_c = cz;
+          q.dg_r0 = first_tap(a, g.pad, s_);
+          q.dg_s0 = first_tap(bb, g.pad, s_);
+          q.dg_t0 = g.is3d() ? first_tap(cz, g.pad, s3) : 0;
+          q.dg_nr = ntaps(q.dg_r0, g.R, s_);
+          q.dg_ns = ntaps(q.dg_s0, g.S, s_);
+          q.dg_nt = g.is3d() ? ntaps(q.dg_t0, g.R, s3) : 1;
+          q.Kg = q.dg_nt * q.dg_nr * q.dg_ns * g.K;
+          if (q.Kg == 0 && accumulate && (g.C1 == 0 || accumulate1)) continue;  // nothing reaches these pixels
+          PixBox b = choose_box(dc, hc, wc, 1, 1, g.is3d());
+          q.tw = b.tw; q.th = b.th; q.tn = b.tn;
+          q.tiles_w = b.tiles_w; q.tiles_h = b.tiles_h; q.tiles_n = b.tiles_n;
+          q.hout = hc; q.wout = wc; q.n3 = dc;
+          q.cchunks = g.K / 32;
+          CUtensorMap ta;
+          if (!map_act(&ta, dy, out3(g), g.Ho, g.Wo, g.K, b.tw, b.th, b.tn, 1, 1))
+            return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv dgrad)");
+          dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
+          POOCH_CHECK((launch_bn<CONV_DGRAD, true>(bn, q, grid, st, g.prec, &ta, &tb)));
+        }
     return POOCH_OK;
   }
+  if (g.is3d() || g.C1 > 0) return fail(POOCH_EUSAGE, "3D / two-source conv needs the TMA path");
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
   return launch_bn<CONV_DGRAD>(bn, p, grid, st, g.prec);
 }
@@ -266,14 +318,14 @@ struct WgradPlan {
   PixBox box;
 };
 
-static PixBox choose_kbox(int N, int Ho, int Wo, int st) {
+static PixBox choose_kbox(int N3, int Ho, int Wo, int st, int st3) {
   PixBox best{};
   int64_t best_boxes = -1;
   for (int tw = 1; tw <= 32; tw *= 2)
     for (int th = 1; tw * th <= 32; th *= 2) {
       int tn = 32 / (tw * th);
-      if (tw * st > 256 || th * st > 256) continue;
-      int64_t tx = (Wo + tw - 1) / tw, ty = (Ho + th - 1) / th, tz = (N + tn - 1) / tn;
+      if (tw * st > 256 || th * st > 256 || tn * st3 > 256) continue;
+      int64_t tx = (Wo + tw - 1) / tw, ty = (Ho + th - 1) / th, tz = (N3 + tn - 1) / tn;
       int64_t boxes = tx * ty * tz;
       if (best_boxes < 0 || boxes < best_boxes || (boxes == best_boxes && tw > best.tw)) {
         best_boxes = boxes;
@@ -289,16 +341,16 @@ static bool wgrad_uses_tma(const ConvGeom& g) {
 
 static WgradPlan wgrad_plan(const ConvGeom& g) {
   WgradPlan w{};
-  int rsc = g.R * g.S * g.C;
+  int rsc = g.T() * g.R * g.S * g.C;
   w.tma = wgrad_uses_tma(g);
   int M = g.K, Ng = rsc;
   w.bn = 128;
   if (w.tma) {
-    w.box = choose_kbox(g.N, g.Ho, g.Wo, g.stride);
+    w.box = choose_kbox(out3(g), g.Ho, g.Wo, g.stride, g.is3d() ? g.stride : 1);
     if (const char* e = getenv("POOCH_KBOX")) {  // profiling experiments only
       int a = 0, b = 0, c = 0;
       if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && a * b * c == 32)
-        w.box = PixBox{a, b, c, (g.Wo + a - 1) / a, (g.Ho + b - 1) / b, (g.N + c - 1) / c};
+        w.box = PixBox{a, b, c, (g.Wo + a - 1) / a, (g.Ho + b - 1) / b, (out3(g) + c - 1) / c};
     }
     w.kb = w.box.tiles_w * w.box.tiles_h * w.box.tiles_n;
     if (g.K <= 64 && rsc > 64) {
@@ -308,7 +360,7 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
     }
     if (Ng <= 64) w.bn = 64;
   } else {
-    w.kb = (g.N * g.Ho * g.Wo + BK - 1) / BK;
+    w.kb = (int)((out_pixels(g) + BK - 1) / BK);
   }
   w.mt = (M + BM - 1) / BM;
   w.nt = (Ng + w.bn - 1) / w.bn;
@@ -335,7 +387,7 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
 
 size_t conv_wgrad_ws_bytes(const ConvGeom& g) {
   WgradPlan w = wgrad_plan(g);
-  return (w.splits > 1 || w.swap) ? (size_t)w.splits * g.K * g.R * g.S * g.C * sizeof(float) : 0;
+  return (w.splits > 1 || w.swap) ? (size_t)w.splits * g.K * g.T() * g.R * g.S * g.C * sizeof(float) : 0;
 }
 
 __global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out, int64_t n4,
@@ -375,13 +427,13 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ ws, float* __re
 }
 
 pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
-                               size_t ws_bytes, cudaStream_t st) {
+                               size_t ws_bytes, cudaStream_t st, const float* x1) {
   WgradPlan w = wgrad_plan(g);
   GemmParams p = base_params(g);
-  const int rsc = g.R * g.S * g.C;
+  const int rsc = g.T() * g.R * g.S * g.C;
   p.M = w.swap ? rsc : g.K;
   p.Ng = w.swap ? g.K : rsc;
-  p.Kg = g.N * g.Ho * g.Wo;
+  p.Kg = (int)out_pixels(g);
   p.a = dy; p.b = x;
   p.kb_per_split = w.kb_per_split;
   bool use_ws = w.splits > 1 || w.swap;
@@ -390,27 +442,39 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
   p.d = use_ws ? ws : dw;
   dim3 grid(w.mt, w.nt, w.splits);
   if (w.tma) {
+    const int st3 = p.st3;
     p.tw = w.box.tw; p.th = w.box.th; p.tn = w.box.tn;
     p.tiles_w = w.box.tiles_w; p.tiles_h = w.box.tiles_h; p.tiles_n = w.box.tiles_n;
-    p.hout = g.Ho; p.wout = g.Wo;
+    p.hout = g.Ho; p.wout = g.Wo; p.n3 = out3(g);
     p.wg_a_is_x = w.swap ? 1 : 0;
     // chunks per box: the largest power of two <= 4 dividing the channel count in chunks (so a
-    // box never straddles two taps) and no larger than the tile
+    // box never straddles two taps or the two sources) and no larger than the tile
     auto cb_of = [](int ch, int rows) {
       int cb = 4;
       while (cb > 1 && ((ch / 32) % cb != 0 || 32 * cb > rows)) cb >>= 1;
       return cb;
     };
-    const int cb_dy = cb_of(g.K, w.swap ? w.bn : BM), cb_x = cb_of(g.C, w.swap ? BM : w.bn);
+    const int cb_dy = cb_of(g.K, w.swap ? w.bn : BM);
+    const int cx_rows = w.swap ? BM : w.bn;
+    int cb_x = cb_of(g.C, cx_rows);
+    if (g.C1 > 0) cb_x = std::min(cb_of(g.C1, cx_rows), cb_of(g.C - g.C1, cx_rows));
     p.wg_cba = w.swap ? cb_x : cb_dy;
     p.wg_cbb = w.swap ? cb_dy : cb_x;
-    CUtensorMap tdy, tx;
-    if (!map_nhwc_chunks(&tdy, dy, g.N, g.Ho, g.Wo, g.K, w.box.tw, w.box.th, w.box.tn, 1, cb_dy) ||
-        !map_nhwc_chunks(&tx, x, g.N, g.H, g.W, g.C, w.box.tw, w.box.th, w.box.tn, g.stride, cb_x))
+    const int c0 = g.C1 > 0 ? g.C1 : g.C;
+    CUtensorMap tdy, tx, tx1;
+    if (!map_act_chunks(&tdy, dy, out3(g), g.Ho, g.Wo, g.K, w.box.tw, w.box.th, w.box.tn, 1, 1, cb_dy) ||
+        !map_act_chunks(&tx, x, in3(g), g.H, g.W, c0, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x))
       return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv wgrad)");
+    if (g.C1 > 0) {
+      p.c_split = g.C1;
+      if (!map_act_chunks(&tx1, x1, in3(g), g.H, g.W, g.C - g.C1, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x))
+        return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv wgrad, second source)");
+    }
     const CUtensorMap* ta = w.swap ? &tx : &tdy;
     const CUtensorMap* tb = w.swap ? &tdy : &tx;
-    POOCH_CHECK((launch_bn<CONV_WGRAD, true>(w.bn, p, grid, st, g.prec, ta, tb)));
+    POOCH_CHECK((launch_bn<CONV_WGRAD, true>(w.bn, p, grid, st, g.prec, ta, tb, g.C1 > 0 ? &tx1 : nullptr)));
+  } else if (g.is3d() || g.C1 > 0) {
+    return fail(POOCH_EUSAGE, "3D / two-source conv needs the TMA path");
   } else if (g.prec) {
     POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true>(p, grid, st)));
   } else {
@@ -440,7 +504,7 @@ extern "C" pooch_status pooch_op_conv_fwd(const pooch_conv_desc* d, const float*
                                           float* stat_sum, float* stat_sq, void* stream) {
   if (!d || !x || !w || !y) return fail(POOCH_EUSAGE, "null argument");
   ConvGeom g = conv_geom(*d);
-  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  if (g.C1 != 0 || !conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
   if ((stat_sum == nullptr) != (stat_sq == nullptr)) return fail(POOCH_EUSAGE, "stat_sum/stat_sq must pair");
   return launch_conv_fwd(g, x, w, y, stat_sum, stat_sq, nullptr, (cudaStream_t)stream);
 }
@@ -449,7 +513,7 @@ extern "C" pooch_status pooch_op_conv_dgrad(const pooch_conv_desc* d, const floa
                                             int32_t accumulate, void* stream) {
   if (!d || !dy || !wt || !dx) return fail(POOCH_EUSAGE, "null argument");
   ConvGeom g = conv_geom(*d);
-  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  if (g.C1 != 0 || !conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
   return launch_conv_dgrad(g, dy, wt, dx, accumulate != 0, (cudaStream_t)stream);
 }
 
@@ -462,8 +526,33 @@ extern "C" pooch_status pooch_op_conv_wgrad(const pooch_conv_desc* d, const floa
                                             float* ws, size_t ws_bytes, void* stream) {
   if (!d || !x || !dy || !dw) return fail(POOCH_EUSAGE, "null argument");
   ConvGeom g = conv_geom(*d);
-  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  if (g.C1 != 0 || !conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
   return launch_conv_wgrad(g, x, dy, dw, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_conv_fwd2(const pooch_conv_desc* d, const float* x0, const float* x1, const float* w,
+                                           float* y, float* stat_sum, float* stat_sq, void* stream) {
+  if (!d || !x0 || !x1 || !w || !y) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (g.C1 <= 0 || !conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported two-source conv shape");
+  if ((stat_sum == nullptr) != (stat_sq == nullptr)) return fail(POOCH_EUSAGE, "stat_sum/stat_sq must pair");
+  return launch_conv_fwd(g, x0, w, y, stat_sum, stat_sq, nullptr, (cudaStream_t)stream, x1);
+}
+
+extern "C" pooch_status pooch_op_conv_dgrad2(const pooch_conv_desc* d, const float* dy, const float* wt, float* dx0,
+                                             float* dx1, int32_t accumulate0, int32_t accumulate1, void* stream) {
+  if (!d || !dy || !wt || !dx0 || !dx1) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (g.C1 <= 0 || !conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported two-source conv shape");
+  return launch_conv_dgrad(g, dy, wt, dx0, accumulate0 != 0, (cudaStream_t)stream, dx1, accumulate1 != 0);
+}
+
+extern "C" pooch_status pooch_op_conv_wgrad2(const pooch_conv_desc* d, const float* x0, const float* x1,
+                                             const float* dy, float* dw, float* ws, size_t ws_bytes, void* stream) {
+  if (!d || !x0 || !x1 || !dy || !dw) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (g.C1 <= 0 || !conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported two-source conv shape");
+  return launch_conv_wgrad(g, x0, dy, dw, ws, ws_bytes, (cudaStream_t)stream, x1);
 }
 
 extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float* D, int32_t M, int32_t N,

@@ -9,18 +9,25 @@ namespace pooch {
 struct ConvGeom {
   int N, H, W, C, K, R, S, stride, pad, Ho, Wo;
   int prec = 0;  // 0: TF32 (one MMA per k-step), 1: 3xTF32 split (fp32-faithful)
+  // 3D (D > 0): NDHWC with N = 1, cubic kernel (T = R taps along depth); Do = output depth
+  int D = 0, Do = 0;
+  // two-source input: x = concat_c(x0 [.., C1], x1 [.., C - C1]); 0 = one source
+  int C1 = 0;
+  bool is3d() const { return D > 0; }
+  int T() const { return D > 0 ? R : 1; }
 };
 ConvGeom conv_geom(const pooch_conv_desc& d);
 bool conv_shape_ok(const ConvGeom& g);
 
 // y = conv(x, w); bias (nullable) per output channel; stat_sum/sq nullable.
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
-                             float* stat_sq, const float* bias, cudaStream_t st);
+                             float* stat_sq, const float* bias, cudaStream_t st, const float* x1 = nullptr);
+// dx (and, two-source, dx1 for channels [C1, C)); accumulate / accumulate1 per destination
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
-                               cudaStream_t st);
+                               cudaStream_t st, float* dx1 = nullptr, bool accumulate1 = false);
 size_t conv_wgrad_ws_bytes(const ConvGeom& g);
 pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
-                               size_t ws_bytes, cudaStream_t st);
+                               size_t ws_bytes, cudaStream_t st, const float* x1 = nullptr);
 // number of M-tiles of the forward pass = rows of its BN partial-sum arrays
 int conv_stat_tiles(const ConvGeom& g);
 inline int conv_mtiles(const ConvGeom& g) { return conv_stat_tiles(g); }

@@ -369,6 +369,69 @@ __global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const float*
   }
 }
 
+// 3D max-pool, k2 s2 p0 (the U-Net's down-sampling): the 2x2x2 windows tile the input, so the
+// backward pass is a gather -- each thread owns one output voxel x 4 channels, re-reads its
+// window and routes the gradient to the FIRST maximum in (u, v, t) row-major order.
+__global__ void maxpool3d_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int D, int H, int W, int C4) {
+  const int Do = D / 2, Ho = H / 2, Wo = W / 2;
+  const int64_t total = (int64_t)Do * Ho * Wo * C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = (int)(i % C4);
+    int64_t t = i / C4;
+    const int wo = (int)(t % Wo);
+    t /= Wo;
+    const int ho = (int)(t % Ho);
+    const int dz = (int)(t / Ho);
+    float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    for (int u = 0; u < 2; ++u)
+      for (int v = 0; v < 2; ++v)
+        for (int w = 0; w < 2; ++w) {
+          const float4 q = ld4(x + ((((size_t)(2 * dz + u) * H + 2 * ho + v) * W + 2 * wo + w) * C4 + c4) * 4);
+          m.x = fmaxf(m.x, q.x); m.y = fmaxf(m.y, q.y); m.z = fmaxf(m.z, q.z); m.w = fmaxf(m.w, q.w);
+        }
+    st4(y + 4 * i, m);
+  }
+}
+
+__global__ void maxpool3d_bwd_kernel(const float* __restrict__ x, const float* __restrict__ gy, float* __restrict__ gx,
+                                     int D, int H, int W, int C4, int accumulate) {
+  const int Do = D / 2, Ho = H / 2, Wo = W / 2;
+  const int64_t total = (int64_t)Do * Ho * Wo * C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = (int)(i % C4);
+    int64_t t = i / C4;
+    const int wo = (int)(t % Wo);
+    t /= Wo;
+    const int ho = (int)(t % Ho);
+    const int dz = (int)(t / Ho);
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int arg[4] = {-1, -1, -1, -1};
+    for (int e = 0; e < 8; ++e) {
+      const int u = e >> 2, v = (e >> 1) & 1, w = e & 1;
+      const float4 q = ld4(x + ((((size_t)(2 * dz + u) * H + 2 * ho + v) * W + 2 * wo + w) * C4 + c4) * 4);
+      const float qa[4] = {q.x, q.y, q.z, q.w};
+      for (int j = 0; j < 4; ++j)
+        if (qa[j] > best[j]) {  // strict: the first maximum wins
+          best[j] = qa[j];
+          arg[j] = e;
+        }
+    }
+    const float4 g = ld4(gy + 4 * i);
+    const float ga[4] = {g.x, g.y, g.z, g.w};
+    for (int e = 0; e < 8; ++e) {
+      const int u = e >> 2, v = (e >> 1) & 1, w = e & 1;
+      float o[4];
+      for (int j = 0; j < 4; ++j) o[j] = arg[j] == e ? ga[j] : 0.f;
+      float* dst = gx + ((((size_t)(2 * dz + u) * H + 2 * ho + v) * W + 2 * wo + w) * C4 + c4) * 4;
+      if (accumulate) {  // windows do not overlap: this thread is the only writer of these elements
+        const float4 q = ld4(dst);
+        o[0] += q.x; o[1] += q.y; o[2] += q.z; o[3] += q.w;
+      }
+      st4(dst, make_float4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
 __global__ void avgpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int HW, int C4) {
   int n = blockIdx.y;
   int c4 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -568,6 +631,25 @@ pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* ar
   maxpool_arg_kernel<<<grid_for(tot_o, 256), 256, 0, st>>>(x, arg_ws, N, H, W, C / 4, k, s, p, Ho, Wo);
   count_launch();
   maxpool_bwd_kernel<<<grid_for(tot_i, 256), 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C / 4, k, s, p, Ho, Wo);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status maxpool3d_fwd(const float* x, float* y, int D, int H, int W, int C, cudaStream_t st) {
+  if (D % 2 || H % 2 || W % 2 || C % 4) return fail(POOCH_EUSAGE, "3D max-pool needs even extents, C % 4 == 0");
+  int64_t total = (int64_t)(D / 2) * (H / 2) * (W / 2) * C / 4;
+  count_launch();
+  maxpool3d_fwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, y, D, H, W, C / 4);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status maxpool3d_bwd(const float* x, const float* gy, float* gx, int D, int H, int W, int C, bool accumulate,
+                           cudaStream_t st) {
+  if (D % 2 || H % 2 || W % 2 || C % 4) return fail(POOCH_EUSAGE, "3D max-pool needs even extents, C % 4 == 0");
+  int64_t total = (int64_t)(D / 2) * (H / 2) * (W / 2) * C / 4;
+  count_launch();
+  maxpool3d_bwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, gy, gx, D, H, W, C / 4, accumulate ? 1 : 0);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }

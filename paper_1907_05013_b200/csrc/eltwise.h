@@ -47,6 +47,10 @@ pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, i
                          cudaStream_t st);
 // gx = gradient routed to the first maximum of every window (argmax recomputed from x)
 // arg_ws: N*Ho*Wo*C bytes of scratch for the window argmax indices
+// 3D max-pool k2 s2 p0 over x [D][H][W][C] (batch 1); bwd re-derives the first-max argmax from x
+pooch_status maxpool3d_fwd(const float* x, float* y, int D, int H, int W, int C, cudaStream_t st);
+pooch_status maxpool3d_bwd(const float* x, const float* gy, float* gx, int D, int H, int W, int C, bool accumulate,
+                           cudaStream_t st);
 pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* arg_ws, int N, int H, int W, int C,
                          int k, int s, int p, int Ho, int Wo, cudaStream_t st);
 pooch_status avgpool_fwd(const float* x, float* y, int N, int HW, int C, cudaStream_t st);

@@ -120,7 +120,7 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
         ts = reinterpret_cast<float*>(c->dev + c->off_tile);
         tq = ts + (size_t)conv_mtiles(R.geom) * R.geom.K;
       }
-      POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, ts, tq, nullptr, st));
+      POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, ts, tq, nullptr, st, p.in1));
       if (ts) {
         float* sp = fptr(c, c->off_stats) + R.stat_off;
         int C = R.geom.K;
@@ -140,13 +140,20 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
                            mode, p.out, R.rows, C, st);
     }
     case POOCH_L_MAXPOOL:
+      if (T.dout > 0)
+        return maxpool3d_fwd(p.in0, p.out, T.din, T.hin, T.win, T.cin, st);
       return maxpool_fwd(p.in0, p.out, B, T.hin, T.win, T.cin, T.k, T.stride, T.pad, T.hout, T.wout, st);
     case POOCH_L_AVGPOOL:
       return avgpool_fwd(p.in0, p.out, B, T.hin * T.win, T.cin, st);
-    case POOCH_L_FC_CE: {
+    case POOCH_L_UPCONV:
+      // transposed conv = the input-gradient pass of the equivalent k2 s2 conv (weights KTRSC
+      // [cin][2][2][2][cout]), run through the parity-class dgrad with the transposed weights
+      return launch_conv_dgrad(RG, p.in0, fptr(c, c->off_wt) + R.wt_off, p.out, false, st);
+    case POOCH_L_FC_CE:
+    case POOCH_L_HEAD_CE: {
       POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, nullptr, nullptr, pw(c, R.b), st));
       if (!with_stats) return POOCH_OK;
-      return ce_fwd(p.out, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), B, T.cout, R.cpad,
+      return ce_fwd(p.out, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), (int)R.rows, T.cout, R.cpad,
                     fptr(c, c->off_lossrows), fptr(c, c->off_loss), st);
     }
   }
@@ -175,15 +182,29 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
   switch (T.kind) {
     case POOCH_L_CONV: {
       const ConvGeom& G = RG;
-      double xb = 4.0 * G.N * G.H * G.W * G.C, yb = 4.0 * R.rows * G.K, wb = 4.0 * G.K * G.R * G.S * G.C;
+      const double din = G.is3d() ? G.D : 1.0;
+      double xb = 4.0 * G.N * din * G.H * G.W * G.C, yb = 4.0 * R.rows * G.K,
+             wb = 4.0 * G.K * G.T() * G.R * G.S * G.C;
       if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
       POOCH_CHECK(launch_conv_wgrad(G, p.in0 ? p.in0 : reinterpret_cast<const float*>(c->dev + c->off_x), p.gy,
-                                    pg(c, R.w), reinterpret_cast<float*>(c->dev + c->off_wgws), c->wgws_bytes, st));
+                                    pg(c, R.w), reinterpret_cast<float*>(c->dev + c->off_wgws), c->wgws_bytes, st,
+                                    p.in1));
       if (T.in0 >= 0) {
         if (mark) mark(c, FAM_CONV_DGRAD, t, R.flops, yb + xb * (p.acc0 ? 2 : 1) + wb);
-        POOCH_CHECK(launch_conv_dgrad(G, p.gy, fptr(c, c->off_wt) + R.wt_off, p.g0, p.acc0, st));
+        POOCH_CHECK(launch_conv_dgrad(G, p.gy, fptr(c, c->off_wt) + R.wt_off, p.g0, p.acc0, st, p.g1, p.acc1));
       }
       return POOCH_OK;
+    }
+    case POOCH_L_UPCONV: {
+      // equivalent conv: x = the up-sampled grid (its gradient gy), dy = the upconv input
+      const ConvGeom& G = RG;
+      double xb = 4.0 * R.rows * T.cout, yb = 4.0 * (double)T.din * T.hin * T.win * T.cin, wb = 4.0 * 8 * G.K * G.C;
+      if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
+      POOCH_CHECK(launch_conv_wgrad(G, p.gy, p.in0, pg(c, R.w), reinterpret_cast<float*>(c->dev + c->off_wgws),
+                                    c->wgws_bytes, st));
+      if (p.acc0) return fail(POOCH_EUSAGE, "UPCONV must be the only writer of its input's gradient");
+      if (mark) mark(c, FAM_CONV_DGRAD, t, R.flops, xb + yb + wb);
+      return launch_conv_fwd(G, p.gy, pw(c, R.w), p.g0, nullptr, nullptr, nullptr, st);
     }
     case POOCH_L_BNRELU:
     case POOCH_L_TAIL_PROJ:
@@ -214,14 +235,17 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
       return bn_bwd(a, reinterpret_cast<float*>(c->dev + c->off_bnws), st);
     }
     case POOCH_L_MAXPOOL:
+      if (T.dout > 0)
+        return maxpool3d_bwd(p.in0, p.gy, p.g0, T.din, T.hin, T.win, T.cin, p.acc0, st);
       return maxpool_bwd(p.in0, p.gy, p.g0, reinterpret_cast<uint8_t*>(c->dev + c->off_mparg), B, T.hin, T.win, T.cin,
                          T.k, T.stride, T.pad, T.hout, T.wout, st);
     case POOCH_L_AVGPOOL:
       return avgpool_bwd(p.gy, p.g0, B, T.hin * T.win, T.cin, st);
-    case POOCH_L_FC_CE: {
+    case POOCH_L_FC_CE:
+    case POOCH_L_HEAD_CE: {
       float* dz = fptr(c, c->off_dz);
-      POOCH_CHECK(ce_bwd(p.self, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), B, T.cout, R.cpad, dz,
-                         pg(c, R.b), st));
+      POOCH_CHECK(ce_bwd(p.self, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), (int)R.rows, T.cout, R.cpad,
+                         dz, pg(c, R.b), st));
       const ConvGeom& G = RG;
       double xb = 4.0 * G.N * G.C, yb = 4.0 * G.N * G.K, wb = 4.0 * G.K * G.C;
       if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
@@ -236,7 +260,8 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
 
 int fam_fwd(int kind) {
   switch (kind) {
-    case POOCH_L_CONV: return FAM_CONV_FWD;
+    case POOCH_L_CONV:
+    case POOCH_L_UPCONV: return FAM_CONV_FWD;
     case POOCH_L_BNRELU:
     case POOCH_L_TAIL_PROJ:
     case POOCH_L_TAIL_ID: return FAM_BN_FWD;
@@ -247,7 +272,8 @@ int fam_fwd(int kind) {
 }
 int fam_bwd(int kind) {
   switch (kind) {
-    case POOCH_L_CONV: return FAM_CONV_WGRAD;
+    case POOCH_L_CONV:
+    case POOCH_L_UPCONV: return FAM_CONV_WGRAD;
     case POOCH_L_BNRELU:
     case POOCH_L_TAIL_PROJ:
     case POOCH_L_TAIL_ID: return FAM_BN_BWD;
@@ -262,13 +288,15 @@ double fwd_bytes(pooch_ctx* c, int t) {
   const Task& T = c->g.t[t];
   const TaskRt& R = c->rt[t];
   double e = (double)R.rows * T.cout;
+  const double din = T.dout > 0 ? T.din : 1.0;
   switch (T.kind) {
-    case POOCH_L_CONV: return 4.0 * (R.geom.N * (double)R.geom.H * R.geom.W * R.geom.C + e +
-                                      (double)R.geom.K * R.geom.R * R.geom.S * R.geom.C);
+    case POOCH_L_CONV: return 4.0 * (R.geom.N * din * R.geom.H * R.geom.W * R.geom.C + e +
+                                      (double)R.geom.K * R.geom.T() * R.geom.R * R.geom.S * R.geom.C);
+    case POOCH_L_UPCONV: return 4.0 * (din * T.hin * T.win * T.cin + e + 8.0 * T.cin * T.cout);
     case POOCH_L_BNRELU: return 8.0 * e;
     case POOCH_L_TAIL_PROJ:
     case POOCH_L_TAIL_ID: return 12.0 * e;
-    case POOCH_L_MAXPOOL: return 4.0 * ((double)c->g.io.batch * T.hin * T.win * T.cin + e);
+    case POOCH_L_MAXPOOL: return 4.0 * ((double)c->g.io.batch * din * T.hin * T.win * T.cin + e);
     case POOCH_L_AVGPOOL: return 4.0 * ((double)c->g.io.batch * T.hin * T.win * T.cin + e);
     default: return 4.0 * (R.geom.N * (double)R.geom.C + R.geom.N * (double)R.geom.K + (double)R.geom.K * R.geom.C);
   }
@@ -281,7 +309,8 @@ double bwd_bytes(pooch_ctx* c, int t) {
     case POOCH_L_BNRELU: return 4.0 * 5 * e;     // reduce: a, gy; apply: a, gy, write ga
     case POOCH_L_TAIL_PROJ: return 4.0 * 8 * e;  // + b twice, write gb
     case POOCH_L_TAIL_ID: return 4.0 * 8 * e;
-    case POOCH_L_MAXPOOL: return 4.0 * (2.0 * c->g.io.batch * T.hin * T.win * T.cin + e) + e;
+    case POOCH_L_MAXPOOL:
+      return 4.0 * (2.0 * c->g.io.batch * (T.dout > 0 ? T.din : 1) * T.hin * T.win * T.cin + e) + e;
     case POOCH_L_AVGPOOL: return 4.0 * ((double)c->g.io.batch * T.hin * T.win * T.cin + e);
     default: return 0;
   }
@@ -307,11 +336,13 @@ pooch_status layout_resident(pooch_ctx* c) {
   c->off_bnws = take(c->bnws_bytes);
   c->off_wgws = take(c->wgws_bytes);
   c->off_mparg = take(c->mparg_bytes);
-  c->off_x = take((size_t)B * g.io.in_h * g.io.in_w * g.io.in_c * 4);
-  c->off_lab = take((size_t)B * 4);
-  c->off_lossrows = take((size_t)B * 4);
+  c->off_x = take((size_t)B * std::max(g.io.in_d, 1) * g.io.in_h * g.io.in_w * g.io.in_c * 4);
+  // one label / loss row per CE row: the batch (FC head) or every output voxel (voxel head)
+  const size_t ce_rows = (size_t)c->rt[n - 1].rows;
+  c->off_lab = take(ce_rows * 4);
+  c->off_lossrows = take(ce_rows * 4);
   c->off_loss = take(16);
-  c->off_dz = take((size_t)B * c->rt[n - 1].cpad * 4);
+  c->off_dz = take(ce_rows * c->rt[n - 1].cpad * 4);
   c->resident_end = align_up(o, 1 << 20);
   return POOCH_OK;
 }
@@ -354,7 +385,7 @@ BwdPtrs bwd_ptrs(pooch_ctx* c, int t) {
   BwdPtrs p;
   p.in0 = T.in0 >= 0 ? map_bwd(c, T.in0) : nullptr;
   p.in1 = T.in1 >= 0 ? map_bwd(c, T.in1) : nullptr;
-  if (T.kind == POOCH_L_FC_CE) p.self = map_bwd(c, t);
+  if (T.kind == POOCH_L_FC_CE || T.kind == POOCH_L_HEAD_CE) p.self = map_bwd(c, t);
   if (t != n - 1) p.gy = buf(c, 2 * n + t);
   if (T.in0 >= 0) {
     p.g0 = buf(c, 2 * n + T.in0);
@@ -422,25 +453,53 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
   for (int t = 0; t < n; ++t) {
     const Task& T = g.t[t];
     TaskRt& R = c->rt[t];
-    R.rows = (int64_t)B * T.hout * T.wout;
+    const bool three = T.dout > 0;
+    R.rows = (int64_t)B * T.hout * T.wout * (three ? T.dout : 1);
     if (T.kind == POOCH_L_CONV) {
       R.is_conv = true;
       R.geom = ConvGeom{B, T.hin, T.win, T.cin, T.cout, T.k, T.k, T.stride, T.pad, T.hout, T.wout};
-      R.w = param_add(c, T.name + ".w", t, (int64_t)T.cout * T.k * T.k * T.cin);
+      if (three) {
+        R.geom.D = T.din;
+        R.geom.Do = T.dout;
+      }
+      if (T.in1 >= 0) R.geom.C1 = g.t[T.in0].cout;
+      const int64_t wn = (int64_t)T.cout * R.geom.T() * T.k * T.k * T.cin;
+      if (!conv_shape_ok(R.geom)) {
+        delete c;
+        return fail(POOCH_EUSAGE, "task %d: unsupported conv shape (3D / two-source convs need 32-channel multiples)", t);
+      }
+      R.w = param_add(c, T.name + ".w", t, wn);
       R.wt_off = wt;
-      wt += (size_t)T.cout * T.k * T.k * T.cin;
-      R.flops = 2.0 * R.rows * T.cout * T.k * T.k * T.cin;
+      wt += (size_t)wn;
+      R.flops = 2.0 * R.rows * wn;
       wg = std::max(wg, conv_wgrad_ws_bytes(R.geom));
-    } else if (T.kind == POOCH_L_FC_CE) {
+    } else if (T.kind == POOCH_L_UPCONV) {
+      // the equivalent k2 s2 conv maps the up-sampled grid (cout channels) to the input grid (cin)
+      R.is_conv = true;
+      R.geom = ConvGeom{B, T.hout, T.wout, T.cout, T.cin, 2, 2, 2, 0, T.hin, T.win};
+      R.geom.D = T.dout;
+      R.geom.Do = T.din;
+      if (!conv_shape_ok(R.geom)) {
+        delete c;
+        return fail(POOCH_EUSAGE, "task %d: UPCONV channels must be multiples of 32", t);
+      }
+      const int64_t wn = (int64_t)T.cin * 8 * T.cout;
+      R.w = param_add(c, T.name + ".w", t, wn);
+      R.wt_off = wt;
+      wt += (size_t)wn;
+      R.flops = 2.0 * R.rows * T.cin * T.cout;
+      wg = std::max(wg, conv_wgrad_ws_bytes(R.geom));
+    } else if (T.kind == POOCH_L_FC_CE || T.kind == POOCH_L_HEAD_CE) {
+      // FC: one row per image; voxel head: one row per output voxel (a 1x1x1 conv)
       R.is_conv = true;
       R.cpad = (T.cout + 3) / 4 * 4;
-      R.geom = ConvGeom{B, 1, 1, T.cin, R.cpad, 1, 1, 1, 0, 1, 1};
+      if (T.kind == POOCH_L_FC_CE) R.rows = B;
+      R.geom = ConvGeom{(int)R.rows, 1, 1, T.cin, R.cpad, 1, 1, 1, 0, 1, 1};
       R.w = param_add(c, T.name + ".w", t, (int64_t)R.cpad * T.cin);
       R.b = param_add(c, T.name + ".b", t, R.cpad);
       R.wt_off = wt;
       wt += (size_t)R.cpad * T.cin;
-      R.rows = B;
-      R.flops = 2.0 * B * R.cpad * T.cin;
+      R.flops = 2.0 * R.rows * R.cpad * T.cin;
       wg = std::max(wg, conv_wgrad_ws_bytes(R.geom));
     } else if (T.kind == POOCH_L_BNRELU) {
       R.g1 = param_add(c, T.name + ".gamma", t, T.cout);
@@ -453,7 +512,7 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
         R.b2 = param_add(c, T.name + ".betap", t, T.cout);
       }
     } else if (T.kind == POOCH_L_MAXPOOL) {
-      mparg = std::max(mparg, (size_t)B * T.hout * T.wout * T.cout);
+      mparg = std::max(mparg, (size_t)R.rows * T.cout);
     }
     if (T.kind == POOCH_L_BNRELU || T.kind == POOCH_L_TAIL_PROJ || T.kind == POOCH_L_TAIL_ID) {
       bnws_c = std::max(bnws_c, T.cout);
@@ -481,7 +540,8 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
     const Task& T = g.t[t];
     for (int k = 0; k < (int)T.inputs.size(); ++k) {
       int m = T.inputs[k];
-      bool can_acc = T.kind == POOCH_L_CONV || T.kind == POOCH_L_FC_CE || (T.kind == POOCH_L_TAIL_ID && k == 1);
+      bool can_acc = T.kind == POOCH_L_CONV || T.kind == POOCH_L_FC_CE || T.kind == POOCH_L_HEAD_CE ||
+                     (T.kind == POOCH_L_TAIL_ID && k == 1) || (T.kind == POOCH_L_MAXPOOL && T.dout > 0);
       if (!can_acc && c->first_writer[m] != t) {
         delete c;
         return fail(POOCH_EUSAGE, "task %d cannot accumulate into the gradient of map %d", t, m);
@@ -497,7 +557,8 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
   c->mparg_bytes = std::max<size_t>(mparg, 256);
   c->map_bytes.resize(n);
   for (int t = 0; t < n; ++t)
-    c->map_bytes[t] = (uint64_t)c->rt[t].rows * (g.t[t].kind == POOCH_L_FC_CE ? c->rt[t].cpad : g.t[t].cout) * 4;
+    c->map_bytes[t] = (uint64_t)c->rt[t].rows *
+                      ((g.t[t].kind == POOCH_L_FC_CE || g.t[t].kind == POOCH_L_HEAD_CE) ? c->rt[t].cpad : g.t[t].cout) * 4;
   layout_resident(c);
   *out = c;
   return POOCH_OK;
@@ -636,7 +697,7 @@ static Problem make_problem(pooch_ctx* c, uint64_t budget) {
     p.needs[t] = c->g.t[t].needs;
   }
   p.is_conv.assign(n, 0);
-  for (int t = 0; t < n; ++t) p.is_conv[t] = c->g.t[t].kind == POOCH_L_CONV ? 1 : 0;
+  for (int t = 0; t < n; ++t) p.is_conv[t] = (c->g.t[t].kind == POOCH_L_CONV || c->g.t[t].kind == POOCH_L_UPCONV) ? 1 : 0;
   p.resident = 0;
   p.budget = budget;
   p.tail = c->tail_ns;
@@ -914,7 +975,7 @@ static pooch_status enqueue_transposes(pooch_ctx* c) {
     const TaskRt& R = c->rt[t];
     if (!R.is_conv) continue;
     const ConvGeom& G = R.geom;
-    POOCH_CHECK(transpose_krsc(pw(c, R.w), fptr(c, c->off_wt) + R.wt_off, G.K, G.R * G.S, G.C, c->s[0]));
+    POOCH_CHECK(transpose_krsc(pw(c, R.w), fptr(c, c->off_wt) + R.wt_off, G.K, G.T() * G.R * G.S, G.C, c->s[0]));
   }
   return POOCH_OK;
 }
@@ -931,9 +992,9 @@ static pooch_status run_op(pooch_ctx* c, const Op& o, bool timing) {
                            c->rt[o.id].is_conv ? c->rt[o.id].flops : 0, fwd_bytes(c, o.id));
       return run_fwd(c, o.id, fwd_ptrs(c, o.id, true), false);
     case 'B':
-      if (timing && c->g.t[o.id].kind != POOCH_L_CONV && c->g.t[o.id].kind != POOCH_L_FC_CE)
-        mark_seg(c, fam_bwd(c->g.t[o.id].kind), o.id, 0, bwd_bytes(c, o.id));
-      if (timing && c->g.t[o.id].kind == POOCH_L_FC_CE) mark_seg(c, FAM_FC_CE, o.id, 0, 0);
+      if (timing && !c->rt[o.id].is_conv) mark_seg(c, fam_bwd(c->g.t[o.id].kind), o.id, 0, bwd_bytes(c, o.id));
+      if (timing && (c->g.t[o.id].kind == POOCH_L_FC_CE || c->g.t[o.id].kind == POOCH_L_HEAD_CE))
+        mark_seg(c, FAM_FC_CE, o.id, 0, 0);
       return run_bwd(c, o.id, bwd_ptrs(c, o.id), timing ? mark_seg : nullptr);
     case 'O':
       POOCH_CUDA(cudaMemcpyAsync(c->host + c->host_off[o.id], buf(c, o.id), c->map_bytes[o.id],

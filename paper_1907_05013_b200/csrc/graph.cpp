@@ -15,10 +15,11 @@ namespace {
 
 struct Builder {
   std::vector<pooch_layer_desc> out;
-  int add(int kind, int in0, int in1, int cin, int cout, int h, int w, int k, int s, int p, const std::string& nm) {
+  int add(int kind, int in0, int in1, int cin, int cout, int h, int w, int k, int s, int p, const std::string& nm,
+          int dout = 0) {
     pooch_layer_desc d{};
     d.kind = kind; d.in0 = in0; d.in1 = in1; d.cin = cin; d.cout = cout; d.hout = h; d.wout = w;
-    d.k = k; d.stride = s; d.pad = p;
+    d.k = k; d.stride = s; d.pad = p; d.dout = dout;
     std::snprintf(d.name, sizeof(d.name), "%s", nm.c_str());
     out.push_back(d);
     return (int)out.size() - 1;
@@ -74,13 +75,49 @@ void resnet50(Builder& b, int in_hw, int classes, bool v15) {
   b.add(POOCH_L_FC_CE, a, -1, cin, classes, 1, 1, 0, 1, 0, "fc");
 }
 
+// 3D U-Net of BASELINE config 4: 4 levels of widths w, 2w, 4w, 4w, each
+// 2 x [conv3d 3^3 -> BN -> ReLU]; 2^3 max-pool; 4w bottleneck; decoder: k2 s2 transposed conv
+// to the level width, then the first conv reads [up, skip] as two sources; 1^3 head + voxel CE.
+void unet3d(Builder& b, int e, int classes, int w) {
+  const int widths[4] = {w, 2 * w, 4 * w, 4 * w};
+  int src = -1, c = 32;  // input channels padded 1 -> 32 (every 3D conv is TMA-fed)
+  int skip[4], skw[4], ske[4];
+  auto block = [&](const std::string& pre, int x0, int x1, int cin, int cw, int ee) {
+    int c1 = b.add(POOCH_L_CONV, x0, x1, cin, cw, ee, ee, 3, 1, 1, pre + ".conv1", ee);
+    int y1 = b.add(POOCH_L_BNRELU, c1, -1, cw, cw, ee, ee, 0, 1, 0, pre + ".bn1", ee);
+    int c2 = b.add(POOCH_L_CONV, y1, -1, cw, cw, ee, ee, 3, 1, 1, pre + ".conv2", ee);
+    return b.add(POOCH_L_BNRELU, c2, -1, cw, cw, ee, ee, 0, 1, 0, pre + ".bn2", ee);
+  };
+  for (int lv = 0; lv < 4; ++lv) {
+    int y = block("enc" + std::to_string(lv + 1), src, -1, c, widths[lv], e);
+    skip[lv] = y; skw[lv] = widths[lv]; ske[lv] = e;
+    e /= 2;
+    src = b.add(POOCH_L_MAXPOOL, y, -1, widths[lv], widths[lv], e, e, 2, 2, 0, "pool" + std::to_string(lv + 1), e);
+    c = widths[lv];
+  }
+  src = block("mid", src, -1, c, widths[3], e);
+  c = widths[3];
+  for (int lv = 3; lv >= 0; --lv) {
+    e = ske[lv];
+    int u = b.add(POOCH_L_UPCONV, src, -1, c, skw[lv], e, e, 2, 2, 0, "up" + std::to_string(lv + 1), e);
+    src = block("dec" + std::to_string(lv + 1), u, skip[lv], 2 * skw[lv], skw[lv], e);
+    c = skw[lv];
+  }
+  b.add(POOCH_L_HEAD_CE, src, -1, c, classes, e, e, 1, 1, 0, "head", e);
+}
+
 }  // namespace
 
 bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io, Graph& g, std::string& err) {
   g.t.clear();
   g.io = io;
-  if (n <= 0 || io.batch <= 0 || io.in_c % 4 != 0) {
+  if (n <= 0 || io.batch <= 0 || io.in_c % 4 != 0 || io.in_d < 0) {
     err = "empty graph, bad batch or input channels not a multiple of 4";
+    return false;
+  }
+  const bool three = io.in_d > 0;
+  if (three && io.batch != 1) {
+    err = "3D networks run at batch 1 (BASELINE config 4)";
     return false;
   }
   for (int i = 0; i < n; ++i) {
@@ -88,19 +125,20 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
     Task t{};
     t.kind = d.kind; t.in0 = d.in0; t.in1 = d.in1; t.cin = d.cin; t.cout = d.cout; t.hout = d.hout;
     t.wout = d.wout; t.k = d.k; t.stride = d.stride; t.pad = d.pad;
+    t.dout = three ? d.dout : 0;
     t.name = std::string(d.name, strnlen(d.name, sizeof(d.name)));
     if (d.in0 >= i || d.in1 >= i || d.in0 < -1 || d.in1 < -1) {
       err = "task " + std::to_string(i) + ": inputs must be topological";
       return false;
     }
-    if (d.kind < POOCH_L_CONV || d.kind > POOCH_L_FC_CE) {
+    if (d.kind < POOCH_L_CONV || d.kind > POOCH_L_HEAD_CE) {
       err = "task " + std::to_string(i) + ": bad kind";
       return false;
     }
     if (d.in0 >= 0) t.inputs.push_back(d.in0);
     if (d.in1 >= 0) t.inputs.push_back(d.in1);
-    bool two = d.kind == POOCH_L_TAIL_PROJ || d.kind == POOCH_L_TAIL_ID;
-    if (two != (d.in1 >= 0) || (d.kind != POOCH_L_CONV && d.in0 < 0)) {
+    const bool two = d.kind == POOCH_L_TAIL_PROJ || d.kind == POOCH_L_TAIL_ID || (d.kind == POOCH_L_CONV && d.in1 >= 0);
+    if (two != (d.in1 >= 0) || ((d.kind != POOCH_L_CONV || two) && d.in0 < 0)) {
       err = "task " + std::to_string(i) + ": wrong number of inputs";
       return false;
     }
@@ -108,8 +146,17 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
     if (d.in0 >= 0) {
       t.hin = g.t[d.in0].hout;
       t.win = g.t[d.in0].wout;
+      t.din = g.t[d.in0].dout;
       int cprev = g.t[d.in0].cout;
       if (d.kind == POOCH_L_FC_CE) cprev *= t.hin * t.win;
+      if (d.kind == POOCH_L_CONV && d.in1 >= 0) {  // two-source conv: same grid, channels concatenated
+        const Task& o = g.t[d.in1];
+        if (o.hout != t.hin || o.wout != t.win || o.dout != t.din || cprev % 32 || o.cout % 32) {
+          err = "task " + std::to_string(i) + ": two-source conv needs equal grids and 32-aligned channels";
+          return false;
+        }
+        cprev += o.cout;
+      }
       if (cprev != d.cin) {
         err = "task " + std::to_string(i) + ": cin does not match producer";
         return false;
@@ -117,25 +164,44 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
     } else {
       t.hin = io.in_h;
       t.win = io.in_w;
+      t.din = three ? io.in_d : 0;
       if (d.cin != io.in_c) {
         err = "task " + std::to_string(i) + ": cin does not match network input";
         return false;
       }
     }
     if (d.cout % 4 != 0 || d.cin % 4 != 0 || d.cout <= 0 || d.hout <= 0 || d.wout <= 0) {
-      if (!(d.kind == POOCH_L_FC_CE && d.cin % 4 == 0 && d.cout > 0)) {
+      if (!((d.kind == POOCH_L_FC_CE || d.kind == POOCH_L_HEAD_CE) && d.cin % 4 == 0 && d.cout > 0)) {
         err = "task " + std::to_string(i) + ": channels must be positive multiples of 4";
         return false;
       }
     }
     if (d.kind == POOCH_L_CONV || d.kind == POOCH_L_MAXPOOL) {
-      if (co(t.hin, d.k, d.stride, d.pad) != d.hout || co(t.win, d.k, d.stride, d.pad) != d.wout) {
+      if (co(t.hin, d.k, d.stride, d.pad) != d.hout || co(t.win, d.k, d.stride, d.pad) != d.wout ||
+          (three && co(t.din, d.k, d.stride, d.pad) != t.dout)) {
         err = "task " + std::to_string(i) + ": output shape does not match geometry";
         return false;
       }
     }
-    if (d.kind == POOCH_L_FC_CE && i != n - 1) {
-      err = "the FC + cross-entropy task must be the sink";
+    if (three && d.kind == POOCH_L_MAXPOOL && (d.k != 2 || d.stride != 2 || d.pad != 0)) {
+      err = "task " + std::to_string(i) + ": 3D max-pool is k2 s2 p0";
+      return false;
+    }
+    if (d.kind == POOCH_L_UPCONV && (!three || d.k != 2 || d.stride != 2 || d.hout != 2 * t.hin ||
+                                     d.wout != 2 * t.win || t.dout != 2 * t.din)) {
+      err = "task " + std::to_string(i) + ": UPCONV is a 3D k2 s2 transposed conv doubling each extent";
+      return false;
+    }
+    if (d.kind == POOCH_L_HEAD_CE && (d.hout != t.hin || d.wout != t.win || t.dout != t.din)) {
+      err = "task " + std::to_string(i) + ": the head keeps the grid";
+      return false;
+    }
+    if (d.kind == POOCH_L_AVGPOOL && three) {
+      err = "task " + std::to_string(i) + ": 3D networks have no global average pool";
+      return false;
+    }
+    if ((d.kind == POOCH_L_FC_CE || d.kind == POOCH_L_HEAD_CE) && i != n - 1) {
+      err = "the FC / head + cross-entropy task must be the sink";
       return false;
     }
     // bwd reads (see pooch_layer_kind)
@@ -144,19 +210,21 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
       case POOCH_L_BNRELU:
       case POOCH_L_TAIL_PROJ:
       case POOCH_L_TAIL_ID:
+      case POOCH_L_UPCONV:
       case POOCH_L_MAXPOOL: t.needs = t.inputs; break;
       case POOCH_L_AVGPOOL: break;
       case POOCH_L_FC_CE:
+      case POOCH_L_HEAD_CE:
         t.needs = t.inputs;
         t.needs.push_back(i);
         break;
     }
     std::sort(t.needs.begin(), t.needs.end());
-    t.map_bytes = (uint64_t)io.batch * d.cout * d.hout * d.wout * 4ull;
+    t.map_bytes = (uint64_t)io.batch * d.cout * d.hout * d.wout * (three ? (uint64_t)t.dout : 1ull) * 4ull;
     g.t.push_back(t);
   }
-  if (g.t.back().kind != POOCH_L_FC_CE) {
-    err = "the last task must be FC + cross-entropy";
+  if (g.t.back().kind != POOCH_L_FC_CE && g.t.back().kind != POOCH_L_HEAD_CE) {
+    err = "the last task must be FC / head + cross-entropy";
     return false;
   }
   for (int i = 0; i < n; ++i)
@@ -233,6 +301,9 @@ extern "C" pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t cl
   } else if (which == 1 || which == 2) {
     if (in_hw < 32) return fail(POOCH_EUSAGE, "ResNet-50 input too small");
     resnet50(b, in_hw, classes, which == 1);
+  } else if (which == 3) {
+    if (in_hw < 16 || in_hw % 16 || width <= 0 || width % 32) return fail(POOCH_EUSAGE, "bad 3D U-Net size");
+    unet3d(b, in_hw, classes, width);
   } else {
     return fail(POOCH_EUSAGE, "unknown network %d", which);
   }

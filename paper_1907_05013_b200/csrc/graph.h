@@ -14,6 +14,7 @@ struct Task {
   int in0, in1;        // producer ids, -1 = network input / unused
   int cin, cout, hout, wout, k, stride, pad;
   int hin, win;        // derived: input spatial dims (conv / pool)
+  int din, dout;       // 3D networks: input / output depth (0 in 2D networks)
   std::string name;
   std::vector<int> inputs;  // map inputs (ids >= 0)
   std::vector<int> needs;   // maps bwd(task) reads

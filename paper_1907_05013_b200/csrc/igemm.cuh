@@ -70,6 +70,15 @@ struct GemmParams {
   // receive the taps r = dg_r0 + st*t (t < dg_nr), s = dg_s0 + st*u (u < dg_ns) from dy pixel
   // (i + (a + pad - r)/st, j + (b + pad - s)/st); stride 1 is the single class a = b = 0
   int dg_a, dg_b, dg_r0, dg_s0, dg_nr, dg_ns;
+  // TMA paths, fourth tensor dimension: images (2D: no taps, st3 = 1, pad3 = 0) or depth of a
+  // 3D conv (batch 1): T taps, stride st3, padding pad3; n3 = extent of the output grid's fourth
+  // dimension (PIXM epilogue); DGRAD classes along it: dg_c, dg_t0, dg_nt
+  int T, st3, pad3, n3;
+  int dg_c, dg_t0, dg_nt;
+  // two-source input (a channel concatenation read in place): FWD A / WGRAD x channels
+  // [c_split, C) come from the third tensor map; DGRAD columns [n_split, Ng) go to d2
+  int c_split, n_split, accumulate2;
+  float* d2;
 };
 
 constexpr int BM = 128;
@@ -400,7 +409,8 @@ struct TileMap {
 
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
-    igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b) {
+    igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                 const __grid_constant__ CUtensorMap tma_c) {
   static_assert(!TMA || MODE != GEMM_TEST, "TMA path: conv fwd / dgrad / wgrad");
   // TMA tiles whose M rows are a box of output pixels (FWD / DGRAD); TMA wgrad boxes pixels along K
   constexpr bool PIXM = TMA && MODE != CONV_WGRAD;
@@ -460,6 +470,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
       if (ptid == 0) {
         ptx::tma_prefetch_desc(&tma_a);
         ptx::tma_prefetch_desc(&tma_b);
+        if (p.c_split) ptx::tma_prefetch_desc(&tma_c);
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
           int m0, n0, kb0, nkb;
@@ -480,10 +491,17 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             // 5-D map puts the chunk index outermost, so the box lands as cb consecutive 4-KB blocks
             auto box = [&](uint32_t dst, const CUtensorMap* map, bool is_x, int row) {
               if (is_x) {
-                const int rs = row / p.C, c = row - rs * p.C;
-                const int r = rs / p.S, sx = rs - r * p.S;
-                ptx::tma_load_5d(dst, map, &rawfull[s], 0, ow * p.stride - p.pad + sx, oh * p.stride - p.pad + r, on,
-                                 c >> 5);
+                // row = ((t * R + r) * S + s) * C + c; channels past c_split come from the second source
+                const int rs = row / p.C;
+                int c = row - rs * p.C;
+                const int t3 = rs / (p.R * p.S), r2 = rs - t3 * p.R * p.S;
+                const int r = r2 / p.S, sx = r2 - r * p.S;
+                if (p.c_split && c >= p.c_split) {
+                  map = &tma_c;
+                  c -= p.c_split;
+                }
+                ptx::tma_load_5d(dst, map, &rawfull[s], 0, ow * p.stride - p.pad + sx, oh * p.stride - p.pad + r,
+                                 on * p.st3 - p.pad3 + t3, c >> 5);
               } else {
                 ptx::tma_load_5d(dst, map, &rawfull[s], 0, ow, oh, on, row >> 5);
               }
@@ -523,6 +541,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
       if (ptid == 0) {
         ptx::tma_prefetch_desc(&tma_a);
         ptx::tma_prefetch_desc(&tma_b);
+        if (p.c_split) ptx::tma_prefetch_desc(&tma_c);
         const uint32_t a_bytes = 32u * p.tw * p.th * p.tn * 4u;
         const uint32_t bytes = a_bytes + (uint32_t)BN * 32u * 4u;
         const int cred = MODE == CONV_FWD ? p.C : p.K;  // reduced channels
@@ -541,21 +560,28 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             uint64_t* bar = AUX ? &rawfull[s] : &full[s];
             const int k = kb0 + kb;
             const int tap = k / p.cchunks, cc = k - tap * p.cchunks;
-            int cw, chh, rs;
-            if (MODE == CONV_FWD) {
-              const int r = tap / p.S, sx = tap - r * p.S;
+            int cw, chh, c3, rs;
+            if (MODE == CONV_FWD) {  // tap = (t * R + r) * S + s over the [K][T][R][S][C] weights
+              const int t3 = tap / (p.R * p.S), r2 = tap - t3 * p.R * p.S;
+              const int r = r2 / p.S, sx = r2 - r * p.S;
               rs = tap;
               cw = tw_i * p.tw * p.stride - p.pad + sx;
               chh = th_i * p.th * p.stride - p.pad + r;
+              c3 = tn_i * p.tn * p.st3 - p.pad3 + t3;
             } else {
-              const int tr = tap / p.dg_ns, ts = tap - tr * p.dg_ns;
-              const int r = p.dg_r0 + p.stride * tr, sx = p.dg_s0 + p.stride * ts;
-              rs = r * p.S + sx;
+              const int tt = tap / (p.dg_nr * p.dg_ns), t2 = tap - tt * p.dg_nr * p.dg_ns;
+              const int tr = t2 / p.dg_ns, ts = t2 - tr * p.dg_ns;
+              const int r = p.dg_r0 + p.stride * tr, sx = p.dg_s0 + p.stride * ts, t3 = p.dg_t0 + p.st3 * tt;
+              rs = (t3 * p.R + r) * p.S + sx;
               cw = tw_i * p.tw + (p.dg_b + p.pad - sx) / p.stride;   // exact: the class selects the taps
               chh = th_i * p.th + (p.dg_a + p.pad - r) / p.stride;
+              c3 = tn_i * p.tn + (p.dg_c + p.pad3 - t3) / p.st3;
             }
             ptx::mbar_arrive_expect_tx(bar, bytes);
-            ptx::tma_load_4d(st, &tma_a, bar, cc * 32, cw, chh, tn_i * p.tn);
+            if (MODE == CONV_FWD && p.c_split && cc * 32 >= p.c_split)
+              ptx::tma_load_4d(st, &tma_c, bar, cc * 32 - p.c_split, cw, chh, c3);
+            else
+              ptx::tma_load_4d(st, &tma_a, bar, cc * 32, cw, chh, c3);
             ptx::tma_load_2d(st + SM::A_BYTES, &tma_b, bar, rs * cred + cc * 32, n0);
           }
         }
@@ -683,9 +709,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
         const int tn_i = mt_i / (p.tiles_w * p.tiles_h);
         const int per = p.tw * p.th;
         const int nn = tn_i * p.tn + row / per, hh = th_i * p.th + (row / p.tw) % p.th, ww = tw_i * p.tw + row % p.tw;
-        rok = row < per * p.tn && nn < p.N && hh < p.hout && ww < p.wout;
-        if (MODE == CONV_DGRAD)  // class grid -> dx pixel (st*hh + a, st*ww + b)
-          gm = (nn * p.H + hh * p.stride + p.dg_a) * p.W + ww * p.stride + p.dg_b;
+        rok = row < per * p.tn && nn < p.n3 && hh < p.hout && ww < p.wout;
+        if (MODE == CONV_DGRAD)  // class grid -> dx pixel (st3*nn + c, st*hh + a, st*ww + b)
+          gm = ((nn * p.st3 + p.dg_c) * p.H + hh * p.stride + p.dg_a) * p.W + ww * p.stride + p.dg_b;
         else
           gm = (nn * p.hout + hh) * p.wout + ww;
       }
@@ -716,15 +742,19 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             dst = p.d + (size_t)z * p.M * p.ldd + (size_t)gm * p.ldd + nb;
           } else if constexpr (MODE == CONV_WGRAD) {
             dst = p.d + ((size_t)z * p.M + gm) * p.Ng + nb;
+          } else if (MODE == CONV_DGRAD && p.n_split > 0) {  // two-source input: split dx by channel
+            dst = nb < p.n_split ? p.d + (size_t)gm * p.n_split + nb
+                                 : p.d2 + (size_t)gm * (p.Ng - p.n_split) + (nb - p.n_split);
           } else {
             dst = p.d + (size_t)gm * p.Ng + nb;
           }
+          const int accum = (p.n_split > 0 && nb >= p.n_split) ? p.accumulate2 : p.accumulate;
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             if (nb + i < p.Ng) {
               float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
               if constexpr (MODE == CONV_DGRAD) {
-                if (p.accumulate) {
+                if (accum) {
                   float4 q = *reinterpret_cast<const float4*>(dst + i);
                   o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
                 }

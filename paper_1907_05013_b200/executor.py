@@ -14,8 +14,8 @@ import numpy as np
 from ._lib import P, IODesc, LayerDesc, PlanReport, ProfileT, SearchCfg, check, lib
 from .planning import STRATEGIES
 
-NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2}
-KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce"]
+NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2, "unet3d": 3}
+KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce", "upconv", "head_ce"]
 FAMILIES = ["conv_fwd", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd", "pool", "fc_ce", "sgd",
             "swap_out", "swap_in", "allreduce", "other", "stall"]
 
@@ -70,11 +70,13 @@ def _ptr(x):
 
 
 class Context:
-    def __init__(self, layers, batch: int, in_c: int, in_h: int, in_w: int, classes: int, device: int = 0):
+    def __init__(self, layers, batch: int, in_c: int, in_h: int, in_w: int, classes: int, device: int = 0,
+                 in_d: int = 0):
         self.layers = layers
         self.n = len(layers)
         self.batch, self.in_c, self.in_h, self.in_w, self.classes = batch, in_c, in_h, in_w, classes
-        io = IODesc(batch, in_c, in_h, in_w, classes)
+        self.in_d = in_d
+        io = IODesc(batch, in_c, in_h, in_w, classes, in_d)
         h = C.c_void_p()
         check(lib.pooch_create(layers, len(layers), C.byref(io), device, C.byref(h)))
         self.h = h
@@ -82,6 +84,11 @@ class Context:
 
     @classmethod
     def builtin(cls, name, batch, in_hw=None, classes=None, width=32, device=0):
+        if name == "unet3d":   # config 4: in_hw^3 volume, input channels padded 1 -> 32
+            in_hw = in_hw or 256
+            classes = classes or 2
+            return cls(build_net(name, in_hw, classes, width), batch, 32, in_hw, in_hw, classes, device,
+                       in_d=in_hw)
         in_hw = in_hw or (32 if name == "tiny" else 224)
         classes = classes or (10 if name == "tiny" else 1000)
         return cls(build_net(name, in_hw, classes, width), batch, 4, in_hw, in_hw, classes, device)

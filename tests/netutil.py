@@ -6,11 +6,12 @@ import numpy as np
 
 def to_pooch(name, arr, numel):
     a = np.asarray(arr, np.float32)
-    if name.endswith(".w") and a.ndim == 4:          # OIHW -> KRSC, pad C
-        o, c, r, s = a.shape
-        cp = numel // (o * r * s)
-        out = np.zeros((o, r, s, cp), np.float32)
-        out[..., :c] = a.transpose(0, 2, 3, 1)
+    if name.endswith(".w") and a.ndim in (4, 5):     # OI(D)HW -> K(T)RSC, pad C
+        o, c = a.shape[:2]
+        sp = a.shape[2:]
+        cp = numel // (o * int(np.prod(sp)))
+        out = np.zeros((o,) + sp + (cp,), np.float32)
+        out[..., :c] = np.moveaxis(a, 1, -1)
         return out
     if name.endswith(".w") and a.ndim == 2:          # FC [classes, cin] -> [cpad, cin]
         k, cin = a.shape
@@ -27,10 +28,11 @@ def to_pooch(name, arr, numel):
 def from_pooch(name, flat, ref_shape):
     """Pooch layout -> oracle layout of shape ref_shape."""
     ref_shape = tuple(ref_shape)
-    if name.endswith(".w") and len(ref_shape) == 4:
-        o, c, r, s = ref_shape
-        cp = flat.size // (o * r * s)
-        return flat.reshape(o, r, s, cp)[..., :c].transpose(0, 3, 1, 2)
+    if name.endswith(".w") and len(ref_shape) in (4, 5):
+        o, c = ref_shape[:2]
+        sp = ref_shape[2:]
+        cp = flat.size // (o * int(np.prod(sp)))
+        return np.moveaxis(flat.reshape((o,) + sp + (cp,))[..., :c], -1, 1)
     if name.endswith(".w") and len(ref_shape) == 2:
         k, cin = ref_shape
         return flat.reshape(-1, cin)[:k]
@@ -38,9 +40,9 @@ def from_pooch(name, flat, ref_shape):
 
 
 def pad_input(x_nhwc, c=4):
-    n, h, w, c0 = x_nhwc.shape
-    out = np.zeros((n, h, w, c), np.float32)
-    out[..., :c0] = x_nhwc
+    """Zero-pad the channel (last) axis of an N(D)HWC batch to c channels."""
+    out = np.zeros(x_nhwc.shape[:-1] + (c,), np.float32)
+    out[..., :x_nhwc.shape[-1]] = x_nhwc
     return out
 
 

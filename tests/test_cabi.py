@@ -66,3 +66,27 @@ def test_plan_problem_errors():
     p2 = PlanProblem([1, 1], [1, 1], [4, 4], [1, 1], [1, 1], [[], [0]], [[0], [0, 1]], resident=10, budget=12)
     cls, rep = p2.plan("pooch")
     assert cls is None and rep.feasible == 0        # nothing fits: EINFEASIBLE
+
+
+def test_unet3d_graph_matches_oracle_without_gpu():
+    """Config 4's 3D U-Net: the C builder's tasks equal the oracle's (names, kinds, inputs,
+    shapes), and a context for it is created host-only with every map of the oracle's size."""
+    from oracle import nets
+    from paper_1907_05013_b200.executor import KINDS, Context, build_net
+    ref = nets.unet3d(in_d=32, width=32, classes=2)
+    layers = build_net("unet3d", 32, 2, 32)
+    assert len(layers) == len(ref.tasks) == 45
+    for l, t in zip(layers, ref.tasks):
+        assert l.name.decode() == t.name
+        assert KINDS[l.kind] == t.kind
+        assert [i for i in (l.in0, l.in1) if i >= 0] == [i for i in t.inputs if i >= 0]
+        assert (l.cout, l.dout, l.hout, l.wout) == t.out_chw
+    ctx = Context.builtin("unet3d", 1, in_hw=32, classes=2, width=32)
+    prob = ctx.plan_problem() if hasattr(ctx, "plan_problem") else None
+    names = dict(ctx.params())
+    assert names["up1.w"] == 64 * 8 * 32 and names["enc1.conv1.w"] == 32 * 27 * 32   # Cin padded 1 -> 32
+    assert names["head.w"] == 4 * 32                                                   # classes padded 2 -> 4
+    ctx.close()
+    bad = build_net("unet3d", 32, 2, 32)
+    with pytest.raises(Exception):
+        Context(bad, 2, 32, 32, 32, 2, in_d=32)          # 3D networks run at batch 1

@@ -1,0 +1,224 @@
+"""GPU parity of the 3D U-Net path (BASELINE.json config 4) against the fp64 oracle.
+
+* conv3d forward / dgrad / wgrad through the C ABI (pooch_op_conv_*, desc.D > 0), stride 1
+  and the k2 s2 pair behind the transposed conv, plus the two-source (channel-concatenating)
+  variants (pooch_op_conv_*2) -- element-wise rel-L2 against oracle/layers.py;
+* one full training step of a small 3D U-Net (16^3 volume, widths 32/64/128/128) against
+  oracle/nets.py (loss; whole-gradient rel-L2 5e-3, the north_star gate);
+* PoocH's plan at a budget below the in-core peak is bit-exact against the in-core run.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synthdata  # noqa: E402
+from oracle import layers as L  # noqa: E402
+from oracle import nets  # noqa: E402
+from netutil import global_rel, load_params, pad_input, read_params, rel  # noqa: E402
+
+TOL_X3 = 2e-5
+TOL = 5e-3
+TOL_TENSOR = 5e-2
+
+
+def _lib():
+    from paper_1907_05013_b200 import _lib
+    return _lib
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def ndhwc(a):     # oracle NCDHW -> device NDHWC
+    return np.ascontiguousarray(np.moveaxis(a, 1, -1))
+
+
+def ncdhw(a):
+    return np.moveaxis(a, -1, 1)
+
+
+def wkrsc(w):     # OIDHW -> KTRSC
+    return np.ascontiguousarray(np.moveaxis(w, 1, -1))
+
+
+CASES3 = [
+    # D, H, W, C, K, k, stride, pad
+    (6, 5, 7, 32, 64, 3, 1, 1),       # ragged 3x3x3
+    (4, 4, 4, 64, 32, 3, 1, 1),
+    (4, 6, 4, 32, 96, 2, 2, 0),       # the k2 s2 conv behind the transposed conv
+    (5, 5, 5, 128, 32, 1, 1, 0),      # 1x1x1
+]
+
+
+def _inputs(D, H, W, Cin, K, k, seed):
+    g = synthdata.rng(seed)
+    x = g.standard_normal((1, Cin, D, H, W))
+    w = g.standard_normal((K, Cin, k, k, k)) / np.sqrt(Cin * k ** 3)
+    return x.astype(np.float32).astype(np.float64), w.astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("case", CASES3)
+def test_conv3d_fwd_dgrad_wgrad(case):
+    lib = _lib()
+    D, H, W, Cin, K, k, s, p = case
+    x, w = _inputs(D, H, W, Cin, K, k, sum(case))
+    y_ref = L.conv3d_fwd(x, w, s, p)
+    d = lib.ConvDesc(1, H, W, Cin, K, k, k, s, p, 1, D, 0)
+    dx = torch.from_numpy(ndhwc(x).astype(np.float32)).cuda()
+    dw = torch.from_numpy(wkrsc(w).astype(np.float32)).cuda()
+    dy = torch.full((1,) + y_ref.shape[2:] + (K,), float("nan"), device="cuda")
+    mt = lib.lib.pooch_op_conv_stat_tiles(C.byref(d))
+    s1, s2 = torch.zeros((mt, K), device="cuda"), torch.zeros((mt, K), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_fwd(C.byref(d), ptr(dx), ptr(dw), ptr(dy), ptr(s1), ptr(s2), None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(dy.cpu().numpy()), y_ref) < TOL_X3
+    flat = ndhwc(y_ref).reshape(-1, K)
+    assert rel(s1.cpu().numpy().astype(np.float64).sum(0), flat.sum(0)) < 1e-4
+    # dgrad
+    gy = synthdata.rng(3).standard_normal(y_ref.shape).astype(np.float32).astype(np.float64)
+    dgy = torch.from_numpy(ndhwc(gy).astype(np.float32)).cuda()
+    wt = torch.from_numpy(np.ascontiguousarray(np.transpose(wkrsc(w), (4, 1, 2, 3, 0))).astype(np.float32)).cuda()  # C T R S K
+    gx = torch.full(dx.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_dgrad(C.byref(d), ptr(dgy), ptr(wt), ptr(gx), 0, None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(gx.cpu().numpy()), L.conv3d_dgrad(gy, w, x.shape, s, p)) < TOL_X3
+    # wgrad
+    wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(wsb // 4, 1), device="cuda")
+    gw = torch.full(dw.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(dx), ptr(dgy), ptr(gw), ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    gw_ref = L.conv3d_wgrad(x, gy, w.shape, s, p)
+    assert rel(np.moveaxis(gw.cpu().numpy(), -1, 1), gw_ref) < TOL_X3
+
+
+@pytest.mark.parametrize("c1", [32, 64])
+def test_two_source_conv3d(c1):
+    """conv3d over concat_c(x0, x1) read in place, and its split dgrad (with accumulation
+    into the second destination) and wgrad."""
+    lib = _lib()
+    D, H, W, Cin, K = 4, 5, 4, 96, 64
+    x, w = _inputs(D, H, W, Cin, K, 3, 7 + c1)
+    d = lib.ConvDesc(1, H, W, Cin, K, 3, 3, 1, 1, 1, D, c1)
+    xs = ndhwc(x).astype(np.float32)
+    x0 = torch.from_numpy(np.ascontiguousarray(xs[..., :c1])).cuda()
+    x1 = torch.from_numpy(np.ascontiguousarray(xs[..., c1:])).cuda()
+    dw = torch.from_numpy(wkrsc(w).astype(np.float32)).cuda()
+    y_ref = L.conv3d_fwd(x, w, 1, 1)
+    y = torch.full((1, D, H, W, K), float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_fwd2(C.byref(d), ptr(x0), ptr(x1), ptr(dw), ptr(y), None, None, None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(y.cpu().numpy()), y_ref) < TOL_X3
+    gy = synthdata.rng(4).standard_normal(y_ref.shape).astype(np.float32).astype(np.float64)
+    dgy = torch.from_numpy(ndhwc(gy).astype(np.float32)).cuda()
+    wt = torch.from_numpy(np.ascontiguousarray(np.transpose(wkrsc(w), (4, 1, 2, 3, 0))).astype(np.float32)).cuda()
+    prev = synthdata.rng(5).standard_normal((1, D, H, W, Cin - c1)).astype(np.float32)
+    g0 = torch.full((1, D, H, W, c1), float("nan"), device="cuda")
+    g1 = torch.from_numpy(prev.copy()).cuda()
+    lib.check(lib.lib.pooch_op_conv_dgrad2(C.byref(d), ptr(dgy), ptr(wt), ptr(g0), ptr(g1), 0, 1, None))
+    torch.cuda.synchronize()
+    dx_ref = ndhwc(L.conv3d_dgrad(gy, w, x.shape, 1, 1))
+    assert rel(g0.cpu().numpy(), dx_ref[..., :c1]) < TOL_X3
+    assert rel(g1.cpu().numpy(), dx_ref[..., c1:] + prev) < TOL_X3
+    wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(wsb // 4, 1), device="cuda")
+    gw = torch.full(dw.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_wgrad2(C.byref(d), ptr(x0), ptr(x1), ptr(dgy), ptr(gw), ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    assert rel(np.moveaxis(gw.cpu().numpy(), -1, 1), L.conv3d_wgrad(x, gy, w.shape, 1, 1)) < TOL_X3
+
+
+# ------------------------------------------------------------------ full U-Net step
+E, WIDTH, CLASSES = 16, 32, 2
+
+
+def _ctx(dev_bytes, host_bytes):
+    from paper_1907_05013_b200.executor import Context
+    ctx = Context.builtin("unet3d", 1, in_hw=E, classes=CLASSES, width=WIDTH)
+    dev = torch.empty(dev_bytes, dtype=torch.uint8, device="cuda")
+    host = torch.empty(host_bytes, dtype=torch.uint8, pin_memory=True) if host_bytes else None
+    ctx.set_budget(dev, dev_bytes, host, host_bytes)
+    ss = [torch.cuda.Stream() for _ in range(3)]
+    ctx.set_streams(*ss)
+    ctx._torch = (dev, host, ss)
+    return ctx
+
+
+def _put(ctx, x, labels):
+    dev = ctx._torch[0]
+    xp, lp = ctx.input_slot()
+    base = dev.data_ptr()
+    xt = torch.from_numpy(pad_input(x, 32)).reshape(-1).cuda()
+    lt = torch.from_numpy(labels.astype(np.int32).reshape(-1)).cuda()
+    dev[xp - base: xp - base + xt.numel() * 4].view(torch.float32).copy_(xt)
+    dev[lp - base: lp - base + lt.numel() * 4].view(torch.int32).copy_(lt)
+    torch.cuda.synchronize()
+
+
+@pytest.fixture(scope="module")
+def unet():
+    # ReLU-decision margin (DESIGN.md Reading 38): BN beta + 1, gamma x 0.5 put most ReLU inputs
+    # >= 1.6 sigma away from zero. At the default init the 16^3 U-Net flips a few ReLU / max-pool
+    # decisions between fp32 and fp64 forwards (the map error reaches 3e-5 through 18 BN layers)
+    # and the gradient moves by ~9e-3 (measured, tools/dbg_unet4.py) whatever the kernels do;
+    # with the margin the same kernels agree with the oracle to 4e-6.
+    net = nets.unet3d(in_d=E, width=WIDTH, classes=CLASSES)
+    params = nets.init_params(net, seed=21, bn_random=True)
+    for k in params:
+        if k.endswith(".beta"):
+            params[k] = (params[k] + 1.0).astype(np.float32)
+        elif k.endswith(".gamma"):
+            params[k] = (params[k] * 0.5).astype(np.float32)
+    g = synthdata.rng(22)
+    x = g.standard_normal((1, E, E, E, 1)).astype(np.float32)
+    t = g.integers(0, CLASSES, (1, E, E, E))
+    loss, grads, _ = nets.forward_backward(net, params, x, t)
+    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads)
+
+
+def _step(ctx, u, strategy):
+    load_params(ctx, u["params"])
+    _put(ctx, u["x"], u["t"])
+    cls, rep = ctx.plan(strategy)
+    loss = ctx.train_step(0.05)
+    torch.cuda.synchronize()
+    return loss, cls, rep
+
+
+def test_unet3d_step_matches_oracle(unet):
+    ctx = _ctx(1 << 30, 256 << 20)
+    ctx.profile(1)
+    loss, _, _ = _step(ctx, unet, "incore")
+    assert abs(loss - unet["loss"]) < 1e-3 * max(1.0, abs(unet["loss"]))
+    g = read_params(ctx, unet["params"], 1)
+    assert global_rel(g, unet["grads"]) < TOL
+    worst = max(rel(g[k], unet["grads"][k]) for k in unet["grads"] if np.linalg.norm(unet["grads"][k]) > 0)
+    assert worst < TOL_TENSOR
+    ctx.close()
+
+
+def test_unet3d_plan_bit_exact_below_incore(unet):
+    """Budget = resident + half the in-core peak of the maps: PoocH must move maps off the
+    device, stay in the arena and reproduce the in-core step bit for bit."""
+    ctx = _ctx(1 << 30, 256 << 20)
+    ctx.profile(1)
+    ref_loss, _, rep_in = _step(ctx, unet, "incore")
+    ref = [ctx.get_param(i, 1).view(np.uint32).copy() for i in range(len(ctx.params()))]
+    half = ctx.resident_bytes() + rep_in["peak_bytes"] // 2
+    half = (half + 255) // 256 * 256
+    dev, host, ss = ctx._torch
+    ctx.set_budget(dev, half, host, host.numel())
+    ctx.profile(1)
+    loss, cls, rep = _step(ctx, unet, "pooch")
+    assert rep["feasible"] and rep["arena_bytes"] <= half
+    assert cls != [0] * ctx.n
+    assert np.float32(loss).view(np.uint32) == np.float32(ref_loss).view(np.uint32)
+    got = [ctx.get_param(i, 1).view(np.uint32).copy() for i in range(len(ctx.params()))]
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
+    ctx.close()
