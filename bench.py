@@ -8,7 +8,11 @@ timed step is one full training iteration (forward, backward with swap-in /
 recompute, [allreduce], momentum SGD) -- the whole hot path of SURVEY.md 8(a).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--batch B] [--budget-gib G] [--workload cfg2|cfg3]
+                    [--batch B] [--budget-gib G] [--workload cfg2|cfg3|cfg4]
+
+--workload cfg4 runs BASELINE config 4 instead: the 3D U-Net (conv3d-BN-ReLU, widths
+256/512/1024/1024) at batch 1 on a 256^3 volume, whose 207 GB of maps exceed HBM; its
+in-core comparison is the same net at half the edge (the per-voxel rate).
 
 Under torchrun (N>1) every rank runs its own out-of-core executor on its own
 shard (weak scaling) with an NCCL gradient allreduce; the step time is the max
@@ -32,6 +36,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 METRIC = "ResNet-50 images/s at >HBM batch, 1/2/4/8 B200; overhead vs in-core; swap GB/s"
+METRIC_3D = "3D U-Net volumes/s at a >HBM footprint (batch 1, 256^3); overhead vs in-core per voxel; swap GB/s"
 
 
 def parse():
@@ -40,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--edge", type=int, default=None, help="cfg4: volume edge (default 256)")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--budget-gib", type=float, default=None)
     ap.add_argument("--li-cap", type=int, default=12)
@@ -57,17 +63,36 @@ def parse():
     return ap.parse_args()
 
 
+class Workload:
+    def __init__(self, net, batch, budget, name, in_hw, classes, width=32):
+        self.net, self.batch, self.budget, self.name = net, batch, budget, name
+        self.in_hw, self.classes, self.width = in_hw, classes, width
+        self.three = net == "unet3d"
+        self.unit = "volumes/s" if self.three else "images/s"
+        self.metric = METRIC_3D if self.three else METRIC
+
+    def context(self, device=0, in_hw=None):
+        from paper_1907_05013_b200.executor import Context
+        return Context.builtin(self.net, self.batch, in_hw=in_hw or self.in_hw, classes=self.classes,
+                               width=self.width, device=device)
+
+
 def workload(args):
     if args.workload == "cfg2":
         batch = args.batch or 640
         budget = int((args.budget_gib or 16.0) * (1 << 30))
         name = "cfg2: ResNet-50 v1.5 batch %d 224^2, device budget %.0f GiB (paper's 50 GB case)" % (
             batch, budget / (1 << 30))
-    else:
+        return Workload("resnet50", batch, budget, name, 224, 1000)
+    if args.workload == "cfg3":
         batch = args.batch or 2560
-        budget = None  # all free HBM
         name = "cfg3: ResNet-50 v1.5 batch %d 224^2, all free HBM" % batch
-    return batch, budget, name
+        return Workload("resnet50", batch, None, name, 224, 1000)
+    e = args.edge or 256
+    budget = int(args.budget_gib * (1 << 30)) if args.budget_gib else None
+    name = "cfg4: 3D U-Net (widths 256/512/1024/1024) batch 1, %d^3 volume, %s" % (
+        e, "all free HBM" if budget is None else "device budget %.0f GiB" % (budget / (1 << 30)))
+    return Workload("unet3d", 1, budget, name, e, 2, 256)
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -146,11 +171,34 @@ def cpu_sample(target_s=15.0, batch=1):
                 n_img // batch, batch)}
 
 
+def cpu_sample_3d(target_s=15.0, edge=16, width=32):
+    """The oracle as it stands on the 3D U-Net (fp64 NumPy) at a bounded size: per-voxel rate."""
+    import numpy as np
+    import synthdata
+    from oracle import nets
+    cores = len(os.sched_getaffinity(0))
+    net = nets.unet3d(in_d=edge, width=width, classes=2)
+    params = nets.init_params(net, seed=2)
+    g = synthdata.rng(0)
+    x = g.standard_normal((1, edge, edge, edge, 1))
+    t = g.integers(0, 2, (1, edge, edge, edge))
+    n, t0 = 0, time.time()
+    while True:
+        nets.forward_backward(net, params, x, t)
+        n += 1
+        if time.time() - t0 > target_s:
+            break
+    dt = time.time() - t0
+    return {"value": n * edge ** 3 / dt, "unit": "voxels/s", "cores": cores, "kind": "oracle",
+            "sample": "%d fp64 3D U-Net fwd+bwd step(s) at %d^3, width %d (NumPy, BLAS threads = cores)" % (
+                n, edge, width)}
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    batch, budget, name = workload(args)
+    name = workload(args).name
     per = []
     cs = None
     for i in range(args.warmup + args.steps):
@@ -185,8 +233,9 @@ def our_arm(args):
     dev_idx = local
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    batch, budget, wname = workload(args)
-    ctx = Context.builtin("resnet50", batch, in_hw=224, classes=1000, device=dev_idx)
+    W = workload(args)
+    batch, budget, wname = W.batch, W.budget, W.name
+    ctx = W.context(device=dev_idx)
     ctx.set_precision(args.precision)
     free, total = torch.cuda.mem_get_info()
     if budget is None:
@@ -223,9 +272,7 @@ def our_arm(args):
         else:
             ctx.set_param(i, np.zeros(numel, np.float32))
     xp, lp = ctx.input_slot()
-    x_host = torch.from_numpy(np.ascontiguousarray(pad4(synthdata.images(batch, 224, 224, 3, seed=0 + rank))))
-    x_host = x_host.reshape(-1).pin_memory()
-    l_host = torch.from_numpy(synthdata.labels(batch, 1000, seed=1 + rank)).pin_memory()
+    x_host, l_host = synth_batch(W, rank)
     base = dev.data_ptr()
     x_dev = dev[xp - base: xp - base + x_host.numel() * 4].view(torch.float32)
     l_dev = dev[lp - base: lp - base + l_host.numel() * 4].view(torch.int32)
@@ -316,19 +363,24 @@ def our_arm(args):
         ctx.plan("pooch", li_cap=args.li_cap)
 
     # ---- in-core comparison (the same kernels, every map kept) where it fits
+    # (after the out-of-core context and its arena are released: the in-core run needs the HBM)
     incore = None
     if not args.no_incore and world == 1:
-        incore = incore_run(ctx, dev, host, host_bytes, streams, args, free)
+        params_host = [ctx.get_param(i, 0) for i in range(len(ctx.params()))]
+        ctx.close()
+        dev = x_dev = l_dev = loss_dev = None  # noqa: F841 (drop the arena before the in-core run)
+        torch.cuda.empty_cache()
+        incore = incore_run(params_host, batch, streams, args)
 
     value = batch * world * 1000.0 / ms
     pk = peaks()
     roof = roofline(fam, pk)
     line = {
-        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "metric": W.metric, "value": value, "unit": W.unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32 (%s tensor-core contractions, fp32 accumulate/storage)" % ("3xtf32" if args.precision else "tf32"),
-        "data": "synthetic (x ~ N(0,1), labels U[0,1000), He-normal weights; seeded)",
+        "data": "synthetic (x ~ N(0,1), labels U[0,%d), He-normal weights; seeded)" % W.classes,
         "config": {"workload": wname, "global_batch": batch * world, "seq_len": None,
                    "parallelism": "dp%d" % world, "budget_bytes_per_gpu": budget,
                    "host_arena_bytes": host_bytes, "l2": "inputs > L2 (maps are GBs)",
@@ -336,7 +388,7 @@ def our_arm(args):
                    "profile_s": prof_s, "simulated_ms_per_step": rep["makespan_ns"] / 1e6,
                    "arena_high_water_bytes": rep["arena_bytes"], "L_O": rep["lo_size"], "L_I": rep["li_size"]},
         "clocks": clk.summary(),
-        "e2e": {"value": batch * world * 1000.0 / ms_e2e, "unit": "images/s",
+        "e2e": {"value": batch * world * 1000.0 / ms_e2e, "unit": W.unit,
                 "h2d_bytes_per_step": int(x_host.numel() * 4 + l_host.numel() * 4), "d2h_bytes_per_step": 4},
         "gpu_launches": launches,
         "roofline": roof,
@@ -345,12 +397,16 @@ def our_arm(args):
     }
     if ablation is not None:
         line["ablation"] = ablation
+    if W.three:
+        line["voxels_per_s"] = value * W.in_hw ** 3
     if incore is not None:
         line["incore"] = incore
-        if incore.get("images_per_s"):
+        if W.three and incore.get("voxels_per_s"):
+            line["overhead_vs_incore"] = 1.0 - line["voxels_per_s"] / incore["voxels_per_s"]
+        elif incore.get("images_per_s"):
             line["overhead_vs_incore"] = 1.0 - value / incore["images_per_s"]
     if rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_sample(15.0, batch=1)
+        line["cpu_baseline"] = cpu_sample_3d(15.0) if W.three else cpu_sample(15.0, batch=1)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -364,8 +420,23 @@ def pad4(x):
     return out
 
 
+def synth_batch(W, rank):
+    """Pinned host copies of the synthetic input and labels (seed 0 + rank / 1 + rank)."""
+    import numpy as np
+    import torch
+    import synthdata
+    if W.three:
+        e = W.in_hw
+        x = np.zeros((e * e * e, 32), np.float32)          # 1 channel padded to 32
+        x[:, 0] = synthdata.rng(0 + rank).standard_normal(e * e * e, dtype=np.float32)
+        lab = synthdata.rng(1 + rank).integers(0, W.classes, e * e * e).astype(np.int32)
+        return torch.from_numpy(x.reshape(-1)).pin_memory(), torch.from_numpy(lab).pin_memory()
+    x = torch.from_numpy(np.ascontiguousarray(pad4(synthdata.images(W.batch, 224, 224, 3, seed=0 + rank))))
+    return x.reshape(-1).pin_memory(), torch.from_numpy(synthdata.labels(W.batch, 1000, seed=1 + rank)).pin_memory()
+
+
 def ctx_map_bytes(ctx):
-    return [ctx.batch * l.cout * l.hout * l.wout * 4 for l in ctx.layers]
+    return [ctx.batch * l.cout * max(l.dout, 1) * l.hout * l.wout * 4 for l in ctx.layers]
 
 
 def name_out_channels(ctx, pname):
@@ -451,13 +522,14 @@ def swap_stats(fam, prof):
     return out
 
 
-def incore_run(ctx_ooc, dev, host, host_bytes, streams, args, free):
-    """Same kernels with every map kept: needs the full footprint in HBM."""
+def incore_run(params_host, batch, streams, args):
+    """Same kernels with every map kept: needs the full footprint in HBM. For the 3D U-Net
+    (cfg4, which cannot fit) the same net at half the volume edge gives the per-voxel rate."""
     import torch
-    from paper_1907_05013_b200.executor import Context
-    batch = ctx_ooc.batch
+    W = workload(args)
     try:
-        ctx = Context.builtin("resnet50", batch, in_hw=224, classes=1000)
+        edge = W.in_hw // 2 if W.three else None
+        ctx = W.context(in_hw=edge)
         ctx.set_precision(args.precision)
         need = int(ctx.resident_bytes() + sum(ctx_map_bytes(ctx)) * 1.4)
         free_now, _ = torch.cuda.mem_get_info()
@@ -467,7 +539,14 @@ def incore_run(ctx_ooc, dev, host, host_bytes, streams, args, free):
         ctx.set_budget(big, big.numel(), None, 0)
         ctx.set_streams(*streams)
         for i, (name, numel) in enumerate(ctx.params()):
-            ctx.set_param(i, ctx_ooc.get_param(i, 0))
+            ctx.set_param(i, params_host[i])
+        if W.three:  # its own input of the smaller volume
+            Wi = Workload(W.net, 1, None, W.name, edge, W.classes, W.width)
+            xh, lh = synth_batch(Wi, 0)
+            base = big.data_ptr()
+            xp, lp = ctx.input_slot()
+            big[xp - base: xp - base + xh.numel() * 4].view(torch.float32).copy_(xh)
+            big[lp - base: lp - base + lh.numel() * 4].view(torch.int32).copy_(lh)
         ctx.profile(1)
         ctx.plan("incore")
         for _ in range(2):
@@ -489,7 +568,10 @@ def incore_run(ctx_ooc, dev, host, host_bytes, streams, args, free):
         ctx.close()
         del big
         torch.cuda.empty_cache()
-        return {"images_per_s": batch * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+        out = {"images_per_s": batch * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+        if W.three:
+            out = {"volume_edge": edge, "voxels_per_s": edge ** 3 * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+        return out
     except Exception as e:  # report, never fake
         return {"images_per_s": None, "note": "in-core run failed: %s" % e}
 

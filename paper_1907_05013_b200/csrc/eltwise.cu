@@ -503,6 +503,64 @@ __global__ void mean_kernel(const float* __restrict__ v, int n, float* __restric
   if (threadIdx.x == 0) *out = (float)(sh[0] / n);
 }
 
+// Per-row softmax-CE for narrow rows (the voxel head: ld <= 8): one thread per row.
+__global__ void ce_rows_narrow_kernel(const float* __restrict__ z, const int32_t* __restrict__ lab, int64_t rows,
+                                      int classes, int ld, float* __restrict__ loss_rows, float* __restrict__ dz,
+                                      int write_dz) {
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < rows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const float* zr = z + (size_t)row * ld;
+    float m = -INFINITY;
+    for (int c = 0; c < classes; ++c) m = fmaxf(m, zr[c]);
+    float s = 0.f;
+    for (int c = 0; c < classes; ++c) s += expf(zr[c] - m);
+    const int t = lab[row];
+    if (!write_dz) {
+      loss_rows[row] = logf(s) + m - zr[t];
+      continue;
+    }
+    const float inv = 1.0f / (float)rows;
+    for (int c = 0; c < ld; ++c)
+      dz[(size_t)row * ld + c] = c < classes ? (expf(zr[c] - m) / s - (c == t ? 1.f : 0.f)) * inv : 0.f;
+  }
+}
+
+// Deterministic column sums of a tall, narrow matrix m [rows][ld] (ld <= 8): block b sums its
+// row range in a fixed thread / warp order (fp64), then one block adds the partials in order.
+constexpr int kColsumBlocks = 592;
+__global__ void colsum_partial_kernel(const float* __restrict__ m, int64_t rows, int ld, double* __restrict__ part) {
+  __shared__ double sh[8][8];
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < ld) acc[c] += (double)m[(size_t)r * ld + c];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  if (lane == 0)
+    for (int c = 0; c < 8; ++c) sh[w][c] = acc[c];
+  __syncthreads();
+  if (threadIdx.x < ld) {
+    double s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += sh[k][threadIdx.x];
+    part[(size_t)blockIdx.x * ld + threadIdx.x] = s;
+  }
+}
+
+// out[c] = sum_b part[b][c] * scale, in block order
+__global__ void colsum_final_kernel(const double* __restrict__ part, int blocks, int ld, double scale,
+                                    float* __restrict__ out) {
+  const int c = threadIdx.x;
+  if (c >= ld) return;
+  double s = 0;
+  for (int b = 0; b < blocks; ++b) s += part[(size_t)b * ld + c];
+  out[c] = (float)(s * scale);
+}
+
 __global__ void colsum_kernel(const float* __restrict__ m, int rows, int ld, float* __restrict__ out) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ld) return;
@@ -670,8 +728,21 @@ pooch_status avgpool_bwd(const float* gy, float* gx, int N, int HW, int C, cudaS
   return POOCH_OK;
 }
 
+// Narrow heads with many rows (the per-voxel CE): thread-per-row CE and two-stage reductions.
+static bool ce_narrow(int B, int ld) { return ld <= 8 && B >= 2048; }
+
 pooch_status ce_fwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* loss_rows, float* loss,
-                    cudaStream_t st) {
+                    cudaStream_t st, double* ws) {
+  if (ce_narrow(B, ld) && ws) {
+    count_launch();
+    ce_rows_narrow_kernel<<<grid_for(B, 256), 256, 0, st>>>(z, labels, B, classes, ld, loss_rows, nullptr, 0);
+    count_launch();
+    colsum_partial_kernel<<<kColsumBlocks, 256, 0, st>>>(loss_rows, B, 1, ws);
+    count_launch();
+    colsum_final_kernel<<<1, 32, 0, st>>>(ws, kColsumBlocks, 1, 1.0 / B, loss);
+    POOCH_CUDA(cudaGetLastError());
+    return POOCH_OK;
+  }
   count_launch();
   ce_rows_kernel<<<(B + 7) / 8, 256, 0, st>>>(z, labels, B, classes, ld, loss_rows, nullptr, 0);
   count_launch();
@@ -681,7 +752,17 @@ pooch_status ce_fwd(const float* z, const int32_t* labels, int B, int classes, i
 }
 
 pooch_status ce_bwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* dz, float* db,
-                    cudaStream_t st) {
+                    cudaStream_t st, double* ws) {
+  if (ce_narrow(B, ld) && ws) {
+    count_launch();
+    ce_rows_narrow_kernel<<<grid_for(B, 256), 256, 0, st>>>(z, labels, B, classes, ld, nullptr, dz, 1);
+    count_launch();
+    colsum_partial_kernel<<<kColsumBlocks, 256, 0, st>>>(dz, B, ld, ws);
+    count_launch();
+    colsum_final_kernel<<<1, 32, 0, st>>>(ws, kColsumBlocks, ld, 1.0, db);
+    POOCH_CUDA(cudaGetLastError());
+    return POOCH_OK;
+  }
   count_launch();
   ce_rows_kernel<<<(B + 7) / 8, 256, 0, st>>>(z, labels, B, classes, ld, nullptr, dz, 1);
   count_launch();
@@ -689,6 +770,8 @@ pooch_status ce_bwd(const float* z, const int32_t* labels, int B, int classes, i
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
+
+size_t ce_ws_bytes() { return (size_t)kColsumBlocks * 8 * sizeof(double); }
 
 pooch_status sgd_momentum(float* w, float* v, const float* g, int64_t n, float lr, float mu, float scale,
                           cudaStream_t st) {

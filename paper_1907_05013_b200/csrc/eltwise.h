@@ -59,10 +59,12 @@ pooch_status avgpool_bwd(const float* gy, float* gx, int N, int HW, int C, cudaS
 // ---- softmax cross-entropy over the first `classes` of `ld` logits per row.
 // fwd: loss_rows[n], loss = mean (single-block fixed order). bwd: dz = (softmax - onehot) / B
 // (padded columns get 0) and db[c] = sum_n dz[n][c].
+// ws (nullable): ce_ws_bytes() of device scratch for the two-stage reductions of narrow heads
 pooch_status ce_fwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* loss_rows, float* loss,
-                    cudaStream_t st);
+                    cudaStream_t st, double* ws = nullptr);
 pooch_status ce_bwd(const float* z, const int32_t* labels, int B, int classes, int ld, float* dz, float* db,
-                    cudaStream_t st);
+                    cudaStream_t st, double* ws = nullptr);
+size_t ce_ws_bytes();
 
 // ---- momentum SGD over n floats: v = mu*v + scale*g; w -= lr*v
 pooch_status sgd_momentum(float* w, float* v, const float* g, int64_t n, float lr, float mu, float scale,

@@ -154,7 +154,8 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
       POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, nullptr, nullptr, pw(c, R.b), st));
       if (!with_stats) return POOCH_OK;
       return ce_fwd(p.out, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), (int)R.rows, T.cout, R.cpad,
-                    fptr(c, c->off_lossrows), fptr(c, c->off_loss), st);
+                    fptr(c, c->off_lossrows), fptr(c, c->off_loss), st,
+                    reinterpret_cast<double*>(c->dev + c->off_cews));
     }
   }
   return fail(POOCH_EUSAGE, "bad task kind");
@@ -245,7 +246,7 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
     case POOCH_L_HEAD_CE: {
       float* dz = fptr(c, c->off_dz);
       POOCH_CHECK(ce_bwd(p.self, reinterpret_cast<const int32_t*>(c->dev + c->off_lab), (int)R.rows, T.cout, R.cpad,
-                         dz, pg(c, R.b), st));
+                         dz, pg(c, R.b), st, reinterpret_cast<double*>(c->dev + c->off_cews)));
       const ConvGeom& G = RG;
       double xb = 4.0 * G.N * G.C, yb = 4.0 * G.N * G.K, wb = 4.0 * G.K * G.C;
       if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
@@ -342,6 +343,7 @@ pooch_status layout_resident(pooch_ctx* c) {
   c->off_lab = take(ce_rows * 4);
   c->off_lossrows = take(ce_rows * 4);
   c->off_loss = take(16);
+  c->off_cews = take(ce_ws_bytes());
   c->off_dz = take(ce_rows * c->rt[n - 1].cpad * 4);
   c->resident_end = align_up(o, 1 << 20);
   return POOCH_OK;

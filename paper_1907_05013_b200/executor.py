@@ -97,6 +97,7 @@ class Context:
         if self.h:
             lib.pooch_destroy(self.h)
             self.h = None
+        self._keep = []          # release the caller's arenas held for the context's lifetime
 
     def __del__(self):
         try:
