@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--li-cap", type=int, default=12)
     ap.add_argument("--no-incore", action="store_true", help="skip the in-core comparison run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--profile-iters", type=int, default=2)
+    ap.add_argument("--profile-iters", type=int, default=3)
     ap.add_argument("--ablation", action="store_true",
                     help="also run the paper's strategies (Sec. 5.1-5.2) on the same executor and report each")
     ap.add_argument("--ncu-step", action="store_true",
@@ -342,6 +342,7 @@ def our_arm(args):
     ctx.set_timing(True)
     ctx.train_step(0.01, sync_loss=True)
     fam = ctx.family_stats()
+    segs = ctx.timing_segments()
     tim = ctx.last_timing()
     ctx.set_timing(False)
     launches = kernel_launches(ctx, args.steps)
@@ -374,7 +375,7 @@ def our_arm(args):
 
     value = batch * world * 1000.0 / ms
     pk = peaks()
-    roof = roofline(fam, pk)
+    roof = roofline(fam, pk, segs, args.precision)
     line = {
         "metric": W.metric, "value": value, "unit": W.unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -393,7 +394,7 @@ def our_arm(args):
         "gpu_launches": launches,
         "roofline": roof,
         "swap": swap_stats(fam, prof),
-        "families": families_table(fam, peaks()),
+        "families": families_table(fam, peaks(), segs, args.precision),
     }
     if ablation is not None:
         line["ablation"] = ablation
@@ -457,32 +458,62 @@ def kernel_launches(ctx, steps):
     return None
 
 
-def roofline(fam, pk):
-    """Dominant kernel family of the instrumented step vs its roof."""
-    cand = {k: v for k, v in fam.items() if k not in ("other", "stall", "swap_out", "swap_in") and v["ms"] > 0}
-    if not cand:
-        return None
-    k, v = max(cand.items(), key=lambda kv: kv[1]["ms"])
-    t = v["ms"] / 1e3
-    tf = pk["tf32_tflops_sustained"] * 1e12
-    bw = pk["hbm_gbs"] * 1e9
-    if v["flops"] / tf >= v["bytes"] / bw and v["flops"] > 0:
-        ach = v["flops"] / t / 1e12
-        return {"kernel": k, "bound": "tensor", "achieved": ach, "peak": pk["tf32_tflops_sustained"],
-                "unit": "TFLOP/s", "frac": ach / pk["tf32_tflops_sustained"], "traffic": traffic_for(k),
-                "launches": v["launches"], "peak_src": pk["src"] + " bf16 sustained x (1.1/2.25) nominal tf32 ratio"}
-    ach = v["bytes"] / t / 1e9
-    return {"kernel": k, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": ach / pk["hbm_gbs"], "traffic": traffic_for(k), "launches": v["launches"],
-            "peak_src": pk["src"]}
+def tensor_peak(pk, precision):
+    """Contraction roof in algorithmic FLOP/s for the precision the kernels compute in: TF32
+    (bf16 sustained x the guide's nominal 1.1/2.25 ratio), or 3xTF32 = TF32 / 3 (three TF32
+    MMAs per fp32 product)."""
+    return pk["tf32_tflops_sustained"] * 1e12 / (3.0 if precision else 1.0)
 
 
-def families_table(fam, pk):
-    """Per kernel family of the instrumented step: time, launches, achieved algorithmic
-    GB/s and TFLOP/s, and the fraction of the binding roof (HBM copy peak or TF32 peak)."""
+def seg_roof(segs, pk, precision):
+    """Per family: sum of launch times, of per-launch roofline times max(F / P_tensor, B / BW),
+    and of the time in launches whose binding roof is the tensor pipe."""
+    P, BW = tensor_peak(pk, precision), pk["hbm_gbs"] * 1e9
     out = {}
-    tf = pk["tf32_tflops_sustained"] * 1e12
-    bw = pk["hbm_gbs"] * 1e9
+    for f, ms, fl, by in segs:
+        if f in ("other", "stall", "swap_out", "swap_in", "allreduce") or ms <= 0:
+            continue
+        e = out.setdefault(f, {"t": 0.0, "bound": 0.0, "t_tensor": 0.0, "flops": 0.0, "bytes": 0.0})
+        t = ms / 1e3
+        tt, tb = fl / P, by / BW
+        e["t"] += t
+        e["bound"] += max(tt, tb)
+        e["t_tensor"] += t if tt >= tb and fl > 0 else 0.0
+        e["flops"] += fl
+        e["bytes"] += by
+    return out
+
+
+def roofline(fam, pk, segs=None, precision=1):
+    """Dominant kernel family of the instrumented step vs its roof:
+    achieved / peak on the family's binding roof, plus the per-launch roofline fraction
+    (sum of max(F / P_tensor, B / BW) over its launches / their measured time)."""
+    sr = seg_roof(segs or [], pk, precision)
+    if not sr:
+        return None
+    k, e = max(sr.items(), key=lambda kv: kv[1]["t"])
+    tensor = e["t_tensor"] >= 0.5 * e["t"]
+    P = tensor_peak(pk, precision)
+    src = pk["src"] + " bf16 sustained x (1.1/2.25) nominal tf32 ratio" + (" / 3 (3xTF32)" if precision else "")
+    launches = fam[k]["launches"] if k in fam else None
+    if tensor:
+        ach = e["flops"] / e["t"] / 1e12
+        return {"kernel": k, "bound": "tensor", "achieved": ach, "peak": P / 1e12, "unit": "TFLOP/s",
+                "frac": ach / (P / 1e12), "roofline_time_frac": e["bound"] / e["t"], "traffic": traffic_for(k),
+                "launches": launches, "peak_src": src}
+    ach = e["bytes"] / e["t"] / 1e9
+    return {"kernel": k, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": ach / pk["hbm_gbs"], "roofline_time_frac": e["bound"] / e["t"], "traffic": traffic_for(k),
+            "launches": launches, "peak_src": pk["src"]}
+
+
+def families_table(fam, pk, segs=None, precision=1):
+    """Per kernel family of the instrumented step: time, launches, achieved algorithmic
+    GB/s and TFLOP/s, the binding roof (the one most of the family's launch time is bound
+    by) with its fraction, and the per-launch roofline fraction."""
+    out = {}
+    sr = seg_roof(segs or [], pk, precision)
+    P, bw = tensor_peak(pk, precision), pk["hbm_gbs"] * 1e9
     for k, v in fam.items():
         if v["ms"] <= 0:
             continue
@@ -492,14 +523,12 @@ def families_table(fam, pk):
             e["gbs"] = round(v["bytes"] / t / 1e9, 1)
         if v["flops"] > 0:
             e["tflops"] = round(v["flops"] / t / 1e12, 2)
-        if k in ("swap_out", "swap_in"):
-            pass
-        elif v["flops"] / tf >= v["bytes"] / bw and v["flops"] > 0:
-            e["bound"] = "tensor"
-            e["frac"] = round(v["flops"] / t / tf, 4)
-        elif v["bytes"] > 0:
-            e["bound"] = "hbm"
-            e["frac"] = round(v["bytes"] / t / bw, 4)
+        if k in sr:
+            r = sr[k]
+            tensor = r["t_tensor"] >= 0.5 * r["t"]
+            e["bound"] = "tensor" if tensor else "hbm"
+            e["frac"] = round((r["flops"] / r["t"] / P) if tensor else (r["bytes"] / r["t"] / bw), 4)
+            e["roofline_time_frac"] = round(r["bound"] / r["t"], 4)
         out[k] = e
     return out
 
@@ -563,7 +592,7 @@ def incore_run(params_host, batch, streams, args):
         ctx.set_timing(True)
         ctx.train_step(0.01, sync_loss=False)
         torch.cuda.synchronize()
-        fam = families_table(ctx.family_stats(), peaks())
+        fam = families_table(ctx.family_stats(), peaks(), ctx.timing_segments(), args.precision)
         ctx.set_timing(False)
         ctx.close()
         del big

@@ -138,6 +138,13 @@ pooch_status pooch_set_streams(pooch_ctx* ctx, void* compute, void* d2h, void* h
  * caller (rank 0 creates it). The library creates its own communicator. Gradients are
  * summed across ranks and scaled by 1/world in the update. Marks the plan stale. */
 pooch_status pooch_set_comm(pooch_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t world);
+/* The gradient allreduce runs per bucket: reverse-layer groups of whole
+ * tasks' parameters of >= 26 MB, each one contiguous float range [lo, hi) of the gradient
+ * region, enqueued on the comm stream right after the backward of `close_task` (the bucket's
+ * lowest-index task) and overlapping the rest of backward; SGD waits for the last one. With
+ * world = 1 and a non-null id a 1-rank communicator runs the same path. Host-only query:
+ * *n in = capacity of lo / hi / close_task (nullable), out = bucket count. */
+pooch_status pooch_allreduce_buckets(pooch_ctx* ctx, int32_t* n, uint64_t* lo, uint64_t* hi, int32_t* close_task);
 
 /* Precision of the tensor-core contractions (conv fwd / dgrad / wgrad, FC):
  * 1 (default) = 3xTF32 split -- each fp32 operand x is fed as x and x - tf32(x), three TF32
@@ -308,6 +315,12 @@ pooch_status pooch_kernel_launches(pooch_ctx* ctx, int64_t* per_step);
  * algorithmic DRAM bytes. */
 pooch_status pooch_family_stats(pooch_ctx* ctx, int32_t family, double* time_ms, int64_t* launches,
                                 double* flops, double* bytes);
+/* The compute-stream segments of the last instrumented step (one per kernel launch group, in
+ * enqueue order): family, event time, algorithmic flops and bytes. *n in = capacity of the
+ * (nullable) arrays, out = segment count. Lets the caller put every launch against its own
+ * roof (bound time = max(flops / tensor peak, bytes / HBM peak)). */
+pooch_status pooch_timing_segments(pooch_ctx* ctx, int32_t* n, int32_t* family, double* time_ms, double* flops,
+                                   double* bytes);
 
 /* ---------------------------------------------------------------- kernel entry points */
 /* Single convolution passes on caller device buffers, launched on `stream` (cudaStream_t).

@@ -113,6 +113,8 @@ SIGNATURES = {
     "pooch_op_conv_wgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pooch_op_conv_wgrad_ws_bytes": (c_sz, [P(ConvDesc)]),
     "pooch_op_conv_stat_tiles": (c_i64, [P(ConvDesc)]),
+    "pooch_timing_segments": (c_i32, [c_vp, P(c_i32), c_vp, c_vp, c_vp, c_vp]),
+    "pooch_allreduce_buckets": (c_i32, [c_vp, P(c_i32), c_vp, c_vp, c_vp]),
     "pooch_op_conv_fwd2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pooch_op_conv_dgrad2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "pooch_op_conv_wgrad2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),

@@ -105,6 +105,7 @@ struct pooch_ctx {
   std::vector<std::pair<int, int>> tseg;  // (event index start, family), per segment
   std::vector<double> seg_flops, seg_bytes;
   std::vector<int> seg_task, seg_kind;  // task id and 'F','R','B','O','I','U'
+  std::vector<double> seg_ms_last;      // per-segment event time of the last instrumented step
   int t_used = 0;
   double fam_ms[pooch::FAM_COUNT] = {0};
   int64_t fam_launch[pooch::FAM_COUNT] = {0};
@@ -114,6 +115,17 @@ struct pooch_ctx {
   // dp
   void* nccl = nullptr;
   int rank = 0, world = 1;
+  // gradient allreduce buckets (reverse-layer order, ~26 MB): float range of the gradient
+  // region and the task whose backward completes it; events compute -> comm and comm -> update
+  struct Bucket {
+    size_t lo, hi;
+    int close_task;
+  };
+  std::vector<Bucket> buckets;
+  std::vector<int> bucket_at;            // task -> bucket index closed by its backward, or -1
+  std::vector<cudaEvent_t> ev_bucket;
+  cudaEvent_t ev_comm_done = nullptr;
+  cudaStream_t own_comm = nullptr;
   int64_t step_count = 0;
   int64_t last_launches = 0;
   int precision = 1;  // contractions: 0 TF32, 1 3xTF32 (default; DESIGN.md Reading 27)

@@ -572,6 +572,9 @@ extern "C" void pooch_destroy(pooch_ctx* c) {
   for (auto e : c->ev_start) cudaEventDestroy(e);
   for (auto e : c->tev) cudaEventDestroy(e);
   if (c->nccl && g_nccl.commDestroy) g_nccl.commDestroy(c->nccl);
+  for (cudaEvent_t e : c->ev_bucket) cudaEventDestroy(e);
+  if (c->ev_comm_done) cudaEventDestroy(c->ev_comm_done);
+  if (c->own_comm) cudaStreamDestroy(c->own_comm);
   if (c->own_streams)
     for (auto s : c->s)
       if (s) cudaStreamDestroy(s);
@@ -616,12 +619,69 @@ extern "C" pooch_status pooch_set_streams(pooch_ctx* c, void* compute, void* d2h
   return POOCH_OK;
 }
 
+// Gradient buckets for the allreduce: walk the tasks in backward order and
+// close a bucket once it holds >= 6.5 M floats (26 MB); a task's parameters are contiguous
+// in the region (appended per task), so every bucket is one contiguous float range, and it
+// is complete once the backward of its lowest-index task has run.
+static void build_buckets(pooch_ctx* c) {
+  const int n = c->g.n();
+  std::vector<size_t> lo(n, SIZE_MAX), hi(n, 0);
+  for (const ParamT& p : c->params) {
+    lo[p.task] = std::min(lo[p.task], p.off);
+    hi[p.task] = std::max(hi[p.task], p.off + (size_t)((p.numel + 3) / 4 * 4));
+  }
+  c->buckets.clear();
+  c->bucket_at.assign(n, -1);
+  constexpr size_t kBucketFloats = 6500000;
+  size_t b_lo = SIZE_MAX, b_hi = 0;
+  for (int t = n - 1; t >= 0; --t) {
+    if (hi[t] == 0) continue;
+    b_lo = std::min(b_lo, lo[t]);
+    b_hi = std::max(b_hi, hi[t]);
+    bool last = true;
+    for (int u = t - 1; u >= 0; --u)
+      if (hi[u] > 0) {
+        last = false;
+        break;
+      }
+    if (b_hi - b_lo >= kBucketFloats || last) {
+      c->bucket_at[t] = (int)c->buckets.size();
+      c->buckets.push_back({b_lo, b_hi, t});
+      b_lo = SIZE_MAX;
+      b_hi = 0;
+    }
+  }
+}
+
+static void create_bucket_events(pooch_ctx* c) {
+  for (cudaEvent_t e : c->ev_bucket) cudaEventDestroy(e);
+  c->ev_bucket.assign(c->buckets.size(), nullptr);
+  for (auto& e : c->ev_bucket) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (!c->ev_comm_done) cudaEventCreateWithFlags(&c->ev_comm_done, cudaEventDisableTiming);
+}
+
+extern "C" pooch_status pooch_allreduce_buckets(pooch_ctx* c, int32_t* n, uint64_t* lo, uint64_t* hi,
+                                                int32_t* close_task) {
+  if (!c || !n) return fail(POOCH_EUSAGE, "null argument");
+  build_buckets(c);
+  const int cap = *n;
+  *n = (int32_t)c->buckets.size();
+  for (int k = 0; k < std::min(cap, *n); ++k) {
+    if (lo) lo[k] = c->buckets[k].lo;
+    if (hi) hi[k] = c->buckets[k].hi;
+    if (close_task) close_task[k] = c->buckets[k].close_task;
+  }
+  return POOCH_OK;
+}
+
 extern "C" pooch_status pooch_set_comm(pooch_ctx* c, const void* uid, int32_t rank, int32_t world) {
   if (!c || world < 1 || rank < 0 || rank >= world) return fail(POOCH_EUSAGE, "bad rank / world");
   c->have_plan = false;
   c->rank = rank;
   c->world = world;
-  if (world == 1) return POOCH_OK;
+  // world 1 without an id: no communicator (nothing to exchange); with an id a 1-rank
+  // communicator runs the same bucketed path (used to test it on one GPU)
+  if (world == 1 && !uid) return POOCH_OK;
   if (!uid) return ctx_fail(c, fail(POOCH_EUSAGE, "nccl_unique_id is null"));
   std::string err;
   if (!g_nccl.load(err)) return ctx_fail(c, fail(POOCH_ENCCL, "%s", err.c_str()));
@@ -633,6 +693,31 @@ extern "C" pooch_status pooch_set_comm(pooch_ctx* c, const void* uid, int32_t ra
   if (r != 0)
     return ctx_fail(c, fail(POOCH_ENCCL, "ncclCommInitRank: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?"));
   c->nccl = comm;
+  POOCH_CUDA(cudaSetDevice(c->device));
+  build_buckets(c);
+  create_bucket_events(c);
+  return POOCH_OK;
+}
+
+// The comm stream: the caller's, else one the context owns.
+static cudaStream_t comm_stream(pooch_ctx* c) {
+  if (c->s[3]) return c->s[3];
+  if (!c->own_comm) cudaStreamCreateWithFlags(&c->own_comm, cudaStreamNonBlocking);
+  return c->own_comm;
+}
+
+// After the backward of task t: if it completes a bucket, the comm stream waits for it and
+// allreduces the bucket's gradient range (overlapping the rest of backward).
+static pooch_status enqueue_bucket(pooch_ctx* c, int t) {
+  if (!c->nccl || t < 0 || t >= (int)c->bucket_at.size() || c->bucket_at[t] < 0) return POOCH_OK;
+  const int k = c->bucket_at[t];
+  const pooch_ctx::Bucket& b = c->buckets[k];
+  cudaStream_t cs = comm_stream(c);
+  POOCH_CUDA(cudaEventRecord(c->ev_bucket[k], c->s[0]));
+  POOCH_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[k], 0));
+  int r = g_nccl.allReduce(fptr(c, c->off_g) + b.lo, fptr(c, c->off_g) + b.lo, b.hi - b.lo, /*ncclFloat32*/ 7,
+                           /*ncclSum*/ 0, c->nccl, cs);
+  if (r != 0) return fail(POOCH_ENCCL, "ncclAllReduce (bucket %d) failed: %d", k, r);
   return POOCH_OK;
 }
 
@@ -961,11 +1046,10 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
 // ====================================================================== training step
 static pooch_status enqueue_update(pooch_ctx* c, float lr, bool timing) {
   cudaStream_t st = c->s[0];
-  if (c->world > 1) {
+  if (c->nccl) {  // every bucket's allreduce was enqueued during backward; SGD waits for the last
     if (timing) mark_seg(c, FAM_ALLREDUCE, -1, 0, 2.0 * 4 * c->param_floats);
-    int r = g_nccl.allReduce(fptr(c, c->off_g), fptr(c, c->off_g), (size_t)c->param_floats, /*ncclFloat32*/ 7,
-                             /*ncclSum*/ 0, c->nccl, st);
-    if (r != 0) return fail(POOCH_ENCCL, "ncclAllReduce failed: %d", r);
+    POOCH_CUDA(cudaEventRecord(c->ev_comm_done, comm_stream(c)));
+    POOCH_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
   }
   if (timing) mark_seg(c, FAM_SGD, -1, 0, 20.0 * c->param_floats);
   return sgd_momentum(fptr(c, c->off_w), fptr(c, c->off_v), fptr(c, c->off_g), c->param_floats, lr, 0.9f,
@@ -1039,6 +1123,7 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
     }
     if (timing && o.lane == 0) op_seg_begin[i] = (int)c->tseg.size();
     POOCH_CHECK(run_op(c, o, timing));
+    if (o.lane == 0 && o.kind == 'B') POOCH_CHECK(enqueue_bucket(c, o.id));
     if (timing && o.lane != 0) {
       copy_ev[i].second = lt.get();
       POOCH_CUDA(cudaEventRecord(copy_ev[i].second, st));
@@ -1068,6 +1153,8 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
       cudaEventElapsedTime(&ms, c->tev[c->tseg[k].first], c->tev[c->tseg[k + 1].first]);
       seg_ms[k] = ms;
       int f = c->tseg[k].second;
+      if (k == 0) c->seg_ms_last.assign(c->tseg.size(), 0.0);
+      c->seg_ms_last[k] = ms;
       c->fam_ms[f] += ms;
       c->fam_launch[f] += 1;
       c->fam_flops[f] += c->seg_flops[k];
@@ -1144,6 +1231,21 @@ extern "C" pooch_status pooch_last_timing(pooch_ctx* c, int64_t* fwd, int64_t* b
   cp(d2h, c->last_d2h);
   cp(h2d, c->last_h2d);
   if (step_ns) *step_ns = c->last_step_ns;
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_timing_segments(pooch_ctx* c, int32_t* n, int32_t* family, double* time_ms,
+                                              double* flops, double* bytes) {
+  if (!c || !n) return fail(POOCH_EUSAGE, "null argument");
+  const int cap = *n;
+  const int m = (int)c->seg_ms_last.size();
+  *n = m;
+  for (int k = 0; k < std::min(cap, m); ++k) {
+    if (family) family[k] = c->tseg[k].second;
+    if (time_ms) time_ms[k] = c->seg_ms_last[k];
+    if (flops) flops[k] = c->seg_flops[k];
+    if (bytes) bytes[k] = c->seg_bytes[k];
+  }
   return POOCH_OK;
 }
 
@@ -1302,7 +1404,7 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
       float ms;
       POOCH_CUDA(cudaEventRecord(e0, st));
       POOCH_CHECK(enqueue_transposes(c));
-      if (c->world > 1) {
+      if (c->nccl) {
         int r = g_nccl.allReduce(fptr(c, c->off_g), fptr(c, c->off_g), 0, 7, 0, c->nccl, st);  // latency only
         (void)r;
       }

@@ -130,6 +130,15 @@ class Context:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         self._chk(lib.pooch_set_comm(self.h, buf, rank, world))
 
+    def allreduce_buckets(self):
+        """[(lo, hi, close_task)] float ranges of the gradient region allreduced per bucket."""
+        n = C.c_int32(0)
+        self._chk(lib.pooch_allreduce_buckets(self.h, C.byref(n), None, None, None))
+        lo, hi = np.zeros(n.value, np.uint64), np.zeros(n.value, np.uint64)
+        ct = np.zeros(n.value, np.int32)
+        self._chk(lib.pooch_allreduce_buckets(self.h, C.byref(n), lo.ctypes.data, hi.ctypes.data, ct.ctypes.data))
+        return [(int(a), int(b), int(t)) for a, b, t in zip(lo, hi, ct)]
+
     def input_slot(self):
         x, l = C.c_void_p(), C.c_void_p()
         self._chk(lib.pooch_input_slot(self.h, C.byref(x), C.byref(l)))
@@ -207,6 +216,15 @@ class Context:
         step = C.c_int64()
         self._chk(lib.pooch_last_timing(self.h, *[a.ctypes.data_as(P(C.c_int64)) for a in arrs], C.byref(step)))
         return dict(zip(("fwd", "bwd", "rec", "d2h", "h2d"), arrs), step_ns=step.value)
+
+    def timing_segments(self):
+        """Per-launch-group (family, ms, flops, bytes) of the last instrumented step."""
+        n = C.c_int32(0)
+        self._chk(lib.pooch_timing_segments(self.h, C.byref(n), None, None, None, None))
+        fam = np.zeros(n.value, np.int32)
+        arr = [np.zeros(n.value, np.float64) for _ in range(3)]
+        self._chk(lib.pooch_timing_segments(self.h, C.byref(n), fam.ctypes.data, *[a.ctypes.data for a in arr]))
+        return [(FAMILIES[int(f)], float(m), float(fl), float(b)) for f, m, fl, b in zip(fam, *arr)]
 
     def family_stats(self):
         out = {}

@@ -90,3 +90,18 @@ def test_unet3d_graph_matches_oracle_without_gpu():
     bad = build_net("unet3d", 32, 2, 32)
     with pytest.raises(Exception):
         Context(bad, 2, 32, 32, 32, 2, in_d=32)          # 3D networks run at batch 1
+
+
+def test_allreduce_buckets_partition_the_gradient_region():
+    """The per-bucket allreduce ranges tile the gradient region exactly (no gap, no overlap),
+    in reverse-layer order, each closed by the lowest-index task whose parameters it holds."""
+    from paper_1907_05013_b200.executor import Context, build_net
+    ctx = Context(build_net("resnet50", 224, 1000), 8, 4, 224, 224, 1000)
+    total = sum((numel + 3) // 4 * 4 for _, numel in ctx.params())
+    b = ctx.allreduce_buckets()
+    assert len(b) >= 3
+    assert b[0][1] == total and b[-1][0] == 0                 # first bucket = the network's tail
+    for (lo1, hi1, t1), (lo2, hi2, t2) in zip(b, b[1:]):
+        assert hi2 == lo1 and t2 < t1                         # contiguous, descending
+    assert all(hi - lo >= 6_500_000 for lo, hi, _ in b[:-1])
+    ctx.close()

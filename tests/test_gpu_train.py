@@ -176,3 +176,41 @@ def test_resnet50_plans_bit_exact(r50):
         assert np.float32(loss).view(np.uint32) == np.float32(ref_loss).view(np.uint32), strat
         for a, b in zip(_grads_bits(ctx), ref_g):
             assert np.array_equal(a, b), strat
+
+
+def _nccl_uid():
+    import ctypes
+    lib = ctypes.CDLL("libnccl.so.2")
+    raw = ctypes.create_string_buffer(128)
+    assert lib.ncclGetUniqueId(raw) == 0
+    return raw.raw
+
+
+@pytest.mark.parametrize("net", ["tiny", "resnet50"])
+def test_bucketed_allreduce_one_rank_is_identity(net):
+    """the gradient allreduce runs in reverse-layer buckets on the comm stream,
+    each gated by the backward that completes it, and SGD waits for the last one. With a 1-rank
+    NCCL communicator the sum is the identity, so the step must be bit-identical to the run
+    without a communicator -- this exercises the bucket boundaries, events and stream order
+    on one GPU (the multi-rank sum is NCCL's)."""
+    if net == "tiny":
+        model = nets.tiny_cnn()
+        batch, hw, classes, dev_b = 8, 32, 10, 256 << 20
+        x, t = synthdata.images(8, 32, 32, 3, seed=0), synthdata.labels(8, 10, seed=1)
+    else:
+        model = nets.resnet50(in_hw=64, classes=100)
+        batch, hw, classes, dev_b = 4, 64, 100, 2 << 30
+        x, t = synthdata.images(4, 64, 64, 3, seed=0), synthdata.labels(4, 100, seed=1)
+    params = nets.init_params(model, seed=2, bn_random=True)
+    out = []
+    for comm in (False, True):
+        ctx = _ctx_for(net, batch, hw, classes, dev_b, 64 << 20)
+        if comm:
+            ctx.set_comm(_nccl_uid(), 0, 1)
+        ctx.profile(1)
+        loss, cls, _ = _step(ctx, params, x, t, "incore")
+        out.append((np.float32(loss).view(np.uint32), _grads_bits(ctx), _params_bits(ctx)))
+        ctx.close()
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1] + out[0][2], out[1][1] + out[1][2]):
+        assert np.array_equal(a, b)
