@@ -18,10 +18,11 @@ B = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'KB': 1e3, 'MB': 1e6, 
 
 
 def key(k):
-    m = re.search(r'igemm_kernel<\(int\)(\d), \(int\)(\d+), \(int\)(\d), \(bool\)(\d)>', k)
+    m = re.search(r'igemm_kernel<\(int\)(\d), \(int\)(\d+), \(int\)(\d), \(bool\)(\d)(?:, \(bool\)(\d))?>', k)
     if m:
-        return 'igemm<%s,BN=%s,stages=%s,x3=%s>' % ({'0': 'FWD', '1': 'DGRAD', '2': 'WGRAD', '3': 'TEST'}[m.group(1)],
-                                                  m.group(2), m.group(3), m.group(4))
+        return 'igemm<%s,BN=%s,stages=%s,x3=%s,tma=%s>' % (
+            {'0': 'FWD', '1': 'DGRAD', '2': 'WGRAD', '3': 'TEST'}[m.group(1)],
+            m.group(2), m.group(3), m.group(4), m.group(5) or '0')
     k = re.sub(r'\(.*', '', k)
     return k.replace('void ', '').replace('pooch::', '').replace('(anonymous namespace)::', '').replace('<unnamed>::', '')
 
