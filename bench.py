@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--ncu-step", action="store_true",
                     help="profile/plan, 1 warm-up step, then exactly one step inside cudaProfilerStart/Stop "
                          "(for ncu --profile-from-start off); prints nothing")
+    ap.add_argument("--dump-profile", default=None,
+                    help="write the measured profile (+ plan classes) as JSON to this path (offline planning)")
     ap.add_argument("--precision", type=int, default=1, choices=[0, 1],
                     help="contractions: 1 = 3xTF32 (default, fp32-faithful), 0 = single TF32")
     return ap.parse_args()
@@ -290,6 +292,10 @@ def our_arm(args):
         ctx.set_profile(agreed["fwd"], agreed["bwd"], agreed["rec"], agreed["d2h"], agreed["h2d"], agreed["tail"])
     cls, rep = ctx.plan("pooch", li_cap=args.li_cap)
     counts = {"keep": cls.count(0), "swap": cls.count(1), "recompute": cls.count(2)}
+    if args.dump_profile and rank == 0:
+        with open(args.dump_profile, "w") as f:
+            json.dump({"workload": wname, "batch": batch, "budget": budget, "profile": prof, "classes": cls,
+                       "report": {k: (v if isinstance(v, (int, float)) else str(v)) for k, v in rep.items()}}, f)
 
     def barrier():
         if world > 1:

@@ -93,7 +93,10 @@ struct GemmSmem {
   static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
   static constexpr int SMALL_OFF = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 4 * BN * 4 * 2 + 1024;
+  static constexpr int RED_OFF = BAR_OFF + (3 * STAGES + 4) * 8 + 16;
+  // epilogue staging: per epilogue warp one 32 x 32 fp32 block (4 KB), 128-B aligned
+  static constexpr int STG_OFF = (RED_OFF + 4 * BN * 4 * 2 + 127) / 128 * 128;
+  static constexpr int TOTAL = STG_OFF + 4 * 4096 + 1024;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
   uint64_t* tempty = tfull + 2;       // [2]
   uint64_t* rawfull = tempty + 2;     // [STAGES] 3xTF32: raw operands landed (cp.async arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rawfull + STAGES);
-  float* red = reinterpret_cast<float*>(smem + SM::BAR_OFF + (3 * STAGES + 4) * 8 + 16);  // [4][BN] x2
+  float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);  // [4][BN] x2
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -736,32 +739,52 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Ng) ? __ldg(p.bias + nb + i) : 0.f;
           }
         }
-        if (rok) {
-          float* dst;
-          if constexpr (MODE == GEMM_TEST) {
-            dst = p.d + (size_t)z * p.M * p.ldd + (size_t)gm * p.ldd + nb;
-          } else if constexpr (MODE == CONV_WGRAD) {
-            dst = p.d + ((size_t)z * p.M + gm) * p.Ng + nb;
-          } else if (MODE == CONV_DGRAD && p.n_split > 0) {  // two-source input: split dx by channel
-            dst = nb < p.n_split ? p.d + (size_t)gm * p.n_split + nb
-                                 : p.d2 + (size_t)gm * (p.Ng - p.n_split) + (nb - p.n_split);
-          } else {
-            dst = p.d + (size_t)gm * p.Ng + nb;
-          }
-          const int accum = (p.n_split > 0 && nb >= p.n_split) ? p.accumulate2 : p.accumulate;
+        // Coalesced store: the warp stages its 32 rows x 32 columns in shared memory (16-B chunk j
+        // of row r at chunk j ^ (r & 7): conflict free both ways), then each instruction writes
+        // four whole 128-B row segments (lanes 8i..8i+7 = one row) instead of 32 scattered 16-B
+        // pieces. DGRAD accumulation reads the old values with the same pattern (same fp32 add).
+        {
+          const uint32_t stg = sbase + SM::STG_OFF + warp * 4096;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            if (nb + i < p.Ng) {
-              float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          for (int jj = 0; jj < 8; ++jj)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((jj ^ (lane & 7)) << 4)),
+                         "f"(v[4 * jj]), "f"(v[4 * jj + 1]), "f"(v[4 * jj + 2]), "f"(v[4 * jj + 3])
+                         : "memory");
+          __syncwarp();
+          const int q = lane & 7;
+          const int col = nb + 4 * q;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + (lane >> 3);
+            const int gmr = __shfl_sync(0xffffffffu, gm, r);
+            const int okr = __shfl_sync(0xffffffffu, rok ? 1 : 0, r);
+            float4 o;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w)
+                         : "r"(stg + r * 128 + ((q ^ (r & 7)) << 4)));
+            if (okr && col < p.Ng) {
+              float* dst;
+              if constexpr (MODE == GEMM_TEST) {
+                dst = p.d + (size_t)z * p.M * p.ldd + (size_t)gmr * p.ldd + col;
+              } else if constexpr (MODE == CONV_WGRAD) {
+                dst = p.d + ((size_t)z * p.M + gmr) * p.Ng + col;
+              } else if (MODE == CONV_DGRAD && p.n_split > 0) {  // two-source input: split dx by channel
+                dst = nb < p.n_split ? p.d + (size_t)gmr * p.n_split + col
+                                     : p.d2 + (size_t)gmr * (p.Ng - p.n_split) + (col - p.n_split);
+              } else {
+                dst = p.d + (size_t)gmr * p.Ng + col;
+              }
               if constexpr (MODE == CONV_DGRAD) {
+                const int accum = (p.n_split > 0 && nb >= p.n_split) ? p.accumulate2 : p.accumulate;
                 if (accum) {
-                  float4 q = *reinterpret_cast<const float4*>(dst + i);
-                  o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+                  float4 qv = *reinterpret_cast<const float4*>(dst);
+                  o.x += qv.x; o.y += qv.y; o.z += qv.z; o.w += qv.w;
                 }
               }
-              *reinterpret_cast<float4*>(dst + i) = o;
+              *reinterpret_cast<float4*>(dst) = o;
             }
           }
+          __syncwarp();
         }
         if constexpr (MODE == CONV_FWD) {
           if (stats) {

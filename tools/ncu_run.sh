@@ -9,11 +9,11 @@ timeout 1200 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram_
 echo "launch list rc=$?"
 # skip the stem (cp.async path) and take a spread of TMA forward convs
 timeout 1500 ncu --profile-from-start off --set full --clock-control none --import-source on \
-  -k regex:'igemm_kernel<0' -s 1 -c 6 -o gpurun_out/prof_fwd_step \
+  --kernel-name-base demangled -k regex:"igemm_kernel<\\(int\\)0" -s 1 -c 6 -o gpurun_out/prof_fwd_step \
   python bench.py --ncu-step --batch $B --profile-iters 1 > gpurun_out/ncu_full_fwd.log 2>&1
 echo "full fwd rc=$?"
 timeout 1200 ncu --profile-from-start off --set full --clock-control none --import-source on \
-  -k regex:'igemm_kernel<[12]' -c 6 -o gpurun_out/prof_bwd_step \
+  --kernel-name-base demangled -k regex:"igemm_kernel<\\(int\\)[12]" -c 6 -o gpurun_out/prof_bwd_step \
   python bench.py --ncu-step --batch $B --profile-iters 1 > gpurun_out/ncu_full_bwd.log 2>&1
 echo "full bwd rc=$?"
 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on \
