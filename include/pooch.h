@@ -355,6 +355,16 @@ pooch_status pooch_op_conv_wgrad2(const pooch_conv_desc* d, const float* x0, con
                                   float* dw, float* ws, size_t ws_bytes, void* stream);
 /* Number of M-tiles (rows of the partial-sum arrays) of pooch_op_conv_fwd for `d`. */
 int64_t pooch_op_conv_stat_tiles(const pooch_conv_desc* d);
+/* 2D max-pool (k x k window, stride s, padding p with -inf; Sec. 2.1 layer math, DESIGN.md
+ * Reading 25) on NHWC device buffers, launched on `stream`. fwd: y[N,Ho,Wo,C]. bwd: gx[N,H,W,C] =
+ * the gradient routed to the FIRST maximum (row-major window order) of every window, recomputed
+ * from x; `arg_ws` is a device workspace of N*Ho*Wo*C bytes. C % 4 == 0, H*W*C < 2^31, else
+ * POOCH_EUSAGE. Ho = (H + 2p - k)/s + 1 (likewise Wo). Used by the parity tests; the executor
+ * calls the same launchers. */
+pooch_status pooch_op_maxpool2d_fwd(const float* x, float* y, int32_t N, int32_t H, int32_t W, int32_t C, int32_t k,
+                                    int32_t s, int32_t p, void* stream);
+pooch_status pooch_op_maxpool2d_bwd(const float* x, const float* gy, float* gx, void* arg_ws, int32_t N, int32_t H,
+                                    int32_t W, int32_t C, int32_t k, int32_t s, int32_t p, void* stream);
 /* D[split][M][N] = A * B^T on the tensor-core core, A [M][K] and B [N][K] row-major (K-major);
  * a_mn = 2 selects the 3xTF32 path, other non-zero a_mn / b_mn (MN-major operands) return
  * POOCH_EUSAGE; bn in {64,128,256} (64/128 for 3xTF32); splits >= 1. Unit test only. */

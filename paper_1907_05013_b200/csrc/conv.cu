@@ -189,8 +189,14 @@ static int pick_bn(int n, int prec = 0) {
   return n <= 64 ? 64 : ((n <= 128 || prec) ? 128 : 256);
 }
 
+static int epi_direct() {  // POOCH_EPI_DIRECT=1: unstaged epilogue stores (A/B experiments)
+  static int v = getenv("POOCH_EPI_DIRECT") ? atoi(getenv("POOCH_EPI_DIRECT")) : 0;
+  return v;
+}
+
 static GemmParams base_params(const ConvGeom& g) {
   GemmParams p{};
+  p.epi_direct = epi_direct();
   p.N = g.N; p.H = g.H; p.W = g.W; p.C = g.C;
   p.K = g.K; p.R = g.R; p.S = g.S;
   p.Ho = g.Ho; p.Wo = g.Wo; p.stride = g.stride; p.pad = g.pad;
@@ -568,6 +574,7 @@ extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float
   }
   if (a_mn || b_mn) return fail(POOCH_EUSAGE, "MN-major operands are not supported (K-major only)");
   GemmParams p{};
+  p.epi_direct = epi_direct();
   p.M = M; p.Ng = N; p.Kg = K;
   p.a = A; p.b = B; p.d = D;
   p.lda = K;

@@ -43,16 +43,17 @@ __global__ void bn_fin_partial_kernel(const float* __restrict__ ts, const float*
   part[(size_t)(kFinRows + chunk) * C + c] = q;
 }
 
-// 32 channels per block, 8 warps stride the rows; fixed-order combine (deterministic)
-__global__ void bn_fin_final_kernel(const double* __restrict__ part, int C, double count, const float* gamma,
+// 32 channels per block, kFinWarps warps stride the rows; fixed-order combine (deterministic)
+constexpr int kFinWarps = 32;
+__global__ void __launch_bounds__(kFinWarps * 32) bn_fin_final_kernel(const double* __restrict__ part, int C, double count, const float* gamma,
                                     const float* beta, float* mean, float* invstd, float* scale, float* shift) {
-  __shared__ double sh[2][8][33];
+  __shared__ double sh[2][kFinWarps][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   double s = 0, q = 0;
   if (c < C) {
 #pragma unroll 4
-    for (int r = w; r < kFinRows; r += 8) {
+    for (int r = w; r < kFinRows; r += kFinWarps) {
       s += part[(size_t)r * C + c];
       q += part[(size_t)(kFinRows + r) * C + c];
     }
@@ -63,7 +64,7 @@ __global__ void bn_fin_final_kernel(const double* __restrict__ part, int C, doub
   if (w == 0 && c < C) {
     s = 0;
     q = 0;
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kFinWarps; ++k) {
       s += sh[0][k][lane];
       q += sh[1][k][lane];
     }
@@ -187,16 +188,16 @@ __global__ void __launch_bounds__(kBwdThreads) bn_bwd_reduce_kernel(BnBwdArgs p,
 
 // coef layout after the partials: [ka, kb, kc] for BN(a) then BN(b), each [C]
 template <int MODE>
-__global__ void bn_bwd_finalize_kernel(BnBwdArgs p, const float* __restrict__ part, int blocks, float* coef) {
+__global__ void __launch_bounds__(kFinWarps * 32) bn_bwd_finalize_kernel(BnBwdArgs p, const float* __restrict__ part, int blocks, float* coef) {
   constexpr int NQ = MODE == 1 ? 3 : 2;
-  __shared__ double sh[NQ][8][33];
+  __shared__ double sh[NQ][kFinWarps][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0;
   if (c < p.C) {
-    for (int b = w; b < blocks; b += 8) {
+    for (int b = w; b < blocks; b += kFinWarps) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) acc[q] += (double)part[((size_t)q * blocks + b) * p.C + c];
     }
@@ -209,7 +210,7 @@ __global__ void bn_bwd_finalize_kernel(BnBwdArgs p, const float* __restrict__ pa
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     double t = 0;
-    for (int k = 0; k < 8; ++k) t += sh[q][k][lane];
+    for (int k = 0; k < kFinWarps; ++k) t += sh[q][k][lane];
     s[q] = t;
   }
   double M = (double)p.rows;
@@ -276,51 +277,52 @@ __global__ void bn_bwd_apply_kernel(BnBwdArgs p, const float* __restrict__ coef,
 }
 
 // ------------------------------------------------------------------ pooling
+// 2D max-pool. One block per output row (n, ho) (backward: per input row (n, h)); threads
+// stride the row's (w, 4-channel group) pairs, so all index math is 32-bit and division-free
+// except one per element by C4 (a power of two in every network here).
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int N, int H, int W, int C4,
                                    int k, int s, int p, int Ho, int Wo) {
-  int64_t total = (int64_t)N * Ho * Wo * C4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int c4 = (int)(i % C4);
-    int64_t t = i / C4;
-    int wo = (int)(t % Wo);
-    t /= Wo;
-    int ho = (int)(t % Ho);
-    int n = (int)(t / Ho);
+  const int ho = blockIdx.x % Ho, n = blockIdx.x / Ho;
+  const float4* xn = reinterpret_cast<const float4*>(x) + (size_t)n * H * W * C4;
+  float4* yr = reinterpret_cast<float4*>(y) + ((size_t)n * Ho + ho) * Wo * C4;
+  const int h0 = ho * s - p;
+  for (int j = threadIdx.x; j < Wo * C4; j += blockDim.x) {
+    const int c4 = j % C4, wo = j / C4;
+    const int w0 = wo * s - p;
     float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     for (int u = 0; u < k; ++u) {
-      int h = ho * s - p + u;
+      const int h = h0 + u;
       if (h < 0 || h >= H) continue;
       for (int v = 0; v < k; ++v) {
-        int w = wo * s - p + v;
+        const int w = w0 + v;
         if (w < 0 || w >= W) continue;
-        float4 q = ld4(x + (((size_t)n * H + h) * W + w) * C4 * 4 + 4 * c4);
+        float4 q = __ldg(xn + (h * W + w) * C4 + c4);
         m.x = fmaxf(m.x, q.x); m.y = fmaxf(m.y, q.y); m.z = fmaxf(m.z, q.z); m.w = fmaxf(m.w, q.w);
       }
     }
-    st4(y + 4 * i, m);
+    yr[j] = m;
   }
 }
 
 // window argmax (first maximum in row-major order; -inf padding never wins) -> u*k+v per channel
 __global__ void maxpool_arg_kernel(const float* __restrict__ x, uint8_t* __restrict__ arg, int N, int H, int W,
                                    int C4, int k, int s, int p, int Ho, int Wo) {
-  int64_t total = (int64_t)N * Ho * Wo * C4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int c4 = (int)(i % C4);
-    int64_t t = i / C4;
-    int wo = (int)(t % Wo);
-    t /= Wo;
-    int ho = (int)(t % Ho);
-    int n = (int)(t / Ho);
+  const int ho = blockIdx.x % Ho, n = blockIdx.x / Ho;
+  const float4* xn = reinterpret_cast<const float4*>(x) + (size_t)n * H * W * C4;
+  uchar4* ar = reinterpret_cast<uchar4*>(arg) + ((size_t)n * Ho + ho) * Wo * C4;
+  const int h0 = ho * s - p;
+  for (int j = threadIdx.x; j < Wo * C4; j += blockDim.x) {
+    const int c4 = j % C4, wo = j / C4;
+    const int w0 = wo * s - p;
     float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     uint8_t a[4] = {255, 255, 255, 255};
     for (int u = 0; u < k; ++u) {
-      int h = ho * s - p + u;
+      const int h = h0 + u;
       if (h < 0 || h >= H) continue;
       for (int v = 0; v < k; ++v) {
-        int w = wo * s - p + v;
+        const int w = w0 + v;
         if (w < 0 || w >= W) continue;
-        float4 q = ld4(x + (((size_t)n * H + h) * W + w) * C4 * 4 + 4 * c4);
+        float4 q = __ldg(xn + (h * W + w) * C4 + c4);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float val = f4get(q, e);
@@ -331,41 +333,39 @@ __global__ void maxpool_arg_kernel(const float* __restrict__ x, uint8_t* __restr
         }
       }
     }
-    *reinterpret_cast<uchar4*>(arg + 4 * i) = make_uchar4(a[0], a[1], a[2], a[3]);
+    ar[j] = make_uchar4(a[0], a[1], a[2], a[3]);
   }
 }
 
 __global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ gy,
                                    float* __restrict__ gx, int N, int H, int W, int C4, int k, int s, int p, int Ho,
                                    int Wo) {
-  int64_t total = (int64_t)N * H * W * C4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int c4 = (int)(i % C4);
-    int64_t t = i / C4;
-    int w = (int)(t % W);
-    t /= W;
-    int h = (int)(t % H);
-    int n = (int)(t / H);
+  const int h = blockIdx.x % H, n = blockIdx.x / H;
+  const uchar4* an = reinterpret_cast<const uchar4*>(arg) + (size_t)n * Ho * Wo * C4;
+  const float4* gn = reinterpret_cast<const float4*>(gy) + (size_t)n * Ho * Wo * C4;
+  float4* gr = reinterpret_cast<float4*>(gx) + ((size_t)n * H + h) * W * C4;
+  const int ho_lo = max(0, (h + p - k + s) / s), ho_hi = min(Ho - 1, (h + p) / s);
+  for (int j = threadIdx.x; j < W * C4; j += blockDim.x) {
+    const int c4 = j % C4, w = j / C4;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    int ho_lo = max(0, (h + p - k + s) / s), ho_hi = min(Ho - 1, (h + p) / s);
-    int wo_lo = max(0, (w + p - k + s) / s), wo_hi = min(Wo - 1, (w + p) / s);
+    const int wo_lo = max(0, (w + p - k + s) / s), wo_hi = min(Wo - 1, (w + p) / s);
     for (int ho = ho_lo; ho <= ho_hi; ++ho) {
-      int u = h - (ho * s - p);
+      const int u = h - (ho * s - p);
       if (u < 0 || u >= k) continue;
       for (int wo = wo_lo; wo <= wo_hi; ++wo) {
-        int v = w - (wo * s - p);
+        const int v = w - (wo * s - p);
         if (v < 0 || v >= k) continue;
-        size_t o = (((size_t)n * Ho + ho) * Wo + wo) * C4 + c4;
-        uchar4 a = *reinterpret_cast<const uchar4*>(arg + 4 * o);
-        float4 g = ld4(gy + 4 * o);
-        int me = u * k + v;
+        const int o = (ho * Wo + wo) * C4 + c4;
+        uchar4 a = an[o];
+        float4 g = __ldg(gn + o);
+        const int me = u * k + v;
         if (a.x == me) acc[0] += g.x;
         if (a.y == me) acc[1] += g.y;
         if (a.z == me) acc[2] += g.z;
         if (a.w == me) acc[3] += g.w;
       }
     }
-    st4(gx + 4 * i, make_float4(acc[0], acc[1], acc[2], acc[3]));
+    gr[j] = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
 }
 
@@ -618,7 +618,7 @@ pooch_status bn_finalize(const float* ts, const float* tq, int tiles, int C, int
   count_launch();
   bn_fin_partial_kernel<<<g1, 128, 0, st>>>(ts, tq, tiles, C, ws);
   count_launch();
-  bn_fin_final_kernel<<<(C + 31) / 32, 256, 0, st>>>(ws, C, (double)count, gamma, beta, mean, invstd, scale, shift);
+  bn_fin_final_kernel<<<(C + 31) / 32, kFinWarps * 32, 0, st>>>(ws, C, (double)count, gamma, beta, mean, invstd, scale, shift);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
@@ -658,7 +658,7 @@ static pooch_status bn_bwd_mode(const BnBwdArgs& a, float* ws, cudaStream_t st) 
     return fail(POOCH_EUSAGE, "BN backward supports C <= 2048 (C = %d)", C);
   }
   count_launch();
-  bn_bwd_finalize_kernel<MODE><<<(C + 31) / 32, 256, 0, st>>>(a, ws, blocks, coef);
+  bn_bwd_finalize_kernel<MODE><<<(C + 31) / 32, kFinWarps * 32, 0, st>>>(a, ws, blocks, coef);
   int64_t n4 = a.rows * C / 4;
   count_launch();
   bn_bwd_apply_kernel<MODE><<<grid_for(n4, 256), 256, 0, st>>>(a, coef, n4);
@@ -675,20 +675,20 @@ pooch_status bn_bwd(const BnBwdArgs& a, float* ws, cudaStream_t st) {
 
 pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, int k, int s, int p, int Ho, int Wo,
                          cudaStream_t st) {
-  int64_t total = (int64_t)N * Ho * Wo * C / 4;
+  if (C % 4 || (int64_t)H * W * C >= (1LL << 31)) return fail(POOCH_EUSAGE, "max-pool: C %% 4 != 0 or image too large");
   count_launch();
-  maxpool_fwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, y, N, H, W, C / 4, k, s, p, Ho, Wo);
+  maxpool_fwd_kernel<<<N * Ho, 256, 0, st>>>(x, y, N, H, W, C / 4, k, s, p, Ho, Wo);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
 
 pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* arg_ws, int N, int H, int W, int C,
                          int k, int s, int p, int Ho, int Wo, cudaStream_t st) {
-  int64_t tot_o = (int64_t)N * Ho * Wo * C / 4, tot_i = (int64_t)N * H * W * C / 4;
+  if (C % 4 || (int64_t)H * W * C >= (1LL << 31)) return fail(POOCH_EUSAGE, "max-pool: C %% 4 != 0 or image too large");
   count_launch();
-  maxpool_arg_kernel<<<grid_for(tot_o, 256), 256, 0, st>>>(x, arg_ws, N, H, W, C / 4, k, s, p, Ho, Wo);
+  maxpool_arg_kernel<<<N * Ho, 256, 0, st>>>(x, arg_ws, N, H, W, C / 4, k, s, p, Ho, Wo);
   count_launch();
-  maxpool_bwd_kernel<<<grid_for(tot_i, 256), 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C / 4, k, s, p, Ho, Wo);
+  maxpool_bwd_kernel<<<N * H, 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C / 4, k, s, p, Ho, Wo);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
@@ -791,3 +791,21 @@ pooch_status transpose_krsc(const float* w, float* wt, int K, int RS, int C, cud
 }
 
 }  // namespace pooch
+
+extern "C" pooch_status pooch_op_maxpool2d_fwd(const float* x, float* y, int32_t N, int32_t H, int32_t W, int32_t C,
+                                               int32_t k, int32_t s, int32_t p, void* stream) {
+  if (!x || !y || N <= 0 || H <= 0 || W <= 0 || k <= 0 || s <= 0 || p < 0 || H + 2 * p < k || W + 2 * p < k)
+    return pooch::fail(POOCH_EUSAGE, "maxpool2d: bad arguments");
+  const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+  return pooch::maxpool_fwd(x, y, N, H, W, C, k, s, p, Ho, Wo, (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_maxpool2d_bwd(const float* x, const float* gy, float* gx, void* arg_ws, int32_t N,
+                                               int32_t H, int32_t W, int32_t C, int32_t k, int32_t s, int32_t p,
+                                               void* stream) {
+  if (!x || !gy || !gx || !arg_ws || N <= 0 || H <= 0 || W <= 0 || k <= 0 || s <= 0 || p < 0 || H + 2 * p < k ||
+      W + 2 * p < k || k * k > 255)
+    return pooch::fail(POOCH_EUSAGE, "maxpool2d: bad arguments");
+  const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+  return pooch::maxpool_bwd(x, gy, gx, reinterpret_cast<uint8_t*>(arg_ws), N, H, W, C, k, s, p, Ho, Wo, (cudaStream_t)stream);
+}

@@ -793,11 +793,10 @@ static Problem make_problem(pooch_ctx* c, uint64_t budget) {
   return p;
 }
 
-// Best-fit replay of the simulated ledger; fills c->buf_off. false on fragmentation.
 // Best-fit (address-ordered ties) replay of the simulated allocation ledger over [0, cap).
 // off[b] receives the region of every buffer instance b; false on fragmentation.
-bool pack_ledger(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap, bool no_reuse,
-                 std::vector<uint64_t>& off, uint64_t& high) {
+static bool pack_ledger_bestfit(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap, bool no_reuse,
+                                std::vector<uint64_t>& off, uint64_t& high) {
   off.assign(nbuf, 0);
   std::map<uint64_t, uint64_t> freel;  // offset -> length
   freel[0] = cap;
@@ -846,6 +845,124 @@ bool pack_ledger(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap,
       freel[o] = len;
     }
   }
+  return true;
+}
+
+// Offline placement of the ledger's buffer instances (row a6). Instance b lives over
+// [its allocation, its free) in ledger order (never freed: to the end); instances whose
+// lifetimes overlap must not share bytes. Greedy: take the instances in `order`, put each at
+// the lowest offset that clears every already placed instance it overlaps in time (conf[b]:
+// the instances whose lifetimes overlap b's). Returns the high-water mark.
+static uint64_t place_greedy(const std::vector<int>& order, const std::vector<std::vector<int>>& conf,
+                             const std::vector<uint64_t>& sz, std::vector<uint64_t>& off, std::vector<char>& placed,
+                             std::vector<std::pair<uint64_t, uint64_t>>& tmp) {
+  for (int b : order) placed[b] = 0;
+  uint64_t high = 0;
+  for (int b : order) {
+    tmp.clear();
+    for (int q : conf[b])
+      if (placed[q]) tmp.push_back({off[q], off[q] + sz[q]});
+    std::sort(tmp.begin(), tmp.end());
+    uint64_t cur = 0;
+    for (const auto& r : tmp) {
+      if (cur + sz[b] <= r.first) break;
+      cur = std::max(cur, r.second);
+    }
+    off[b] = cur;
+    placed[b] = 1;
+    high = std::max(high, cur + sz[b]);
+  }
+  return high;
+}
+
+// Static offsets of every buffer instance of the simulated ledger within [0, cap). Packing
+// intervals into the fewest bytes is NP-hard (dynamic storage allocation); the simulator
+// guarantees only that the live bytes stay within cap. Candidates: the online best-fit replay
+// of the ledger and three offline greedy orders (largest first; longest-lived first;
+// allocation order); if none fits, simulated annealing over the largest-first order (swap two
+// positions; fixed seed, so packing is deterministic) until the high-water mark fits or the
+// iteration budget runs out. false if nothing fits (the caller re-plans against less budget).
+bool pack_ledger(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap, bool no_reuse,
+                 std::vector<uint64_t>& off, uint64_t& high) {
+  if (no_reuse) return pack_ledger_bestfit(ledger, nbuf, cap, true, off, high);
+  if (pack_ledger_bestfit(ledger, nbuf, cap, false, off, high)) return true;
+  std::vector<int64_t> a(nbuf, -1), f(nbuf, INT64_MAX);
+  std::vector<uint64_t> sz(nbuf, 0);
+  for (size_t i = 0; i < ledger.size(); ++i) {
+    const LedgerEntry& e = ledger[i];
+    if (e.alloc) {
+      a[e.buf] = (int64_t)i;
+      sz[e.buf] = align_up(std::max<uint64_t>(e.bytes, 1));
+    } else {
+      f[e.buf] = (int64_t)i;
+    }
+  }
+  std::vector<int> bufs;
+  for (int b = 0; b < nbuf; ++b)
+    if (a[b] >= 0) bufs.push_back(b);
+  std::vector<std::vector<int>> conf(nbuf);
+  for (size_t i = 0; i < bufs.size(); ++i)
+    for (size_t j = i + 1; j < bufs.size(); ++j) {
+      const int x = bufs[i], y = bufs[j];
+      if (a[x] < f[y] && a[y] < f[x]) {
+        conf[x].push_back(y);
+        conf[y].push_back(x);
+      }
+    }
+  std::vector<std::vector<int>> orders(3, bufs);
+  std::stable_sort(orders[0].begin(), orders[0].end(), [&](int x, int y) {
+    return sz[x] != sz[y] ? sz[x] > sz[y] : a[x] < a[y];
+  });
+  std::stable_sort(orders[1].begin(), orders[1].end(), [&](int x, int y) {
+    const int64_t lx = f[x] - a[x], ly = f[y] - a[y];
+    return lx != ly ? lx > ly : (sz[x] != sz[y] ? sz[x] > sz[y] : a[x] < a[y]);
+  });
+  std::stable_sort(orders[2].begin(), orders[2].end(), [&](int x, int y) { return a[x] < a[y]; });
+  std::vector<uint64_t> cand(nbuf, 0);
+  std::vector<char> placed(nbuf, 0);
+  std::vector<std::pair<uint64_t, uint64_t>> tmp;
+  uint64_t best = UINT64_MAX;
+  for (const auto& ord : orders) {
+    uint64_t h = place_greedy(ord, conf, sz, cand, placed, tmp);
+    if (h < best) {
+      best = h;
+      off = cand;
+      if (best <= cap) break;
+    }
+  }
+  if (best > cap && bufs.size() >= 2) {
+    std::vector<int> cur = orders[0];
+    uint64_t hc = place_greedy(cur, conf, sz, cand, placed, tmp);
+    double T = 0.02 * (double)hc;
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto next = [&]() {
+      rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+      return rng;
+    };
+    const int iters = getenv("POOCH_PACK_ITERS") ? atoi(getenv("POOCH_PACK_ITERS")) : 30000;
+    int last_gain = 0;
+    for (int it = 0; it < iters && best > cap && it - last_gain < 8000; ++it) {
+      const size_t i = next() % cur.size(), j = next() % cur.size();
+      if (i == j) continue;
+      std::swap(cur[i], cur[j]);
+      const uint64_t h = place_greedy(cur, conf, sz, cand, placed, tmp);
+      const double u = (double)(next() >> 11) / 9007199254740992.0;
+      if (h <= hc || u < std::exp(-((double)h - (double)hc) / T)) {
+        hc = h;
+        if (h < best) {
+          best = h;
+          off = cand;
+          last_gain = it;
+        }
+      } else {
+        std::swap(cur[i], cur[j]);
+      }
+      T *= 0.9995;
+    }
+  }
+  high = best;
+  if (best > cap) return false;
+  off.resize(nbuf, 0);
   return true;
 }
 
@@ -976,71 +1093,144 @@ extern "C" pooch_status pooch_set_profile(pooch_ctx* c, const int64_t* fwd, cons
   return POOCH_OK;
 }
 
+// Plan selection with packing in the loop (row a6). The simulator's memory ledger is a byte
+// sum (Sec. 4.1.2), so a plan whose simulated peak fits the arena may still fail to pack into
+// static offsets (fragmentation: measured +2-8 % over the peak on ResNet-50). And the PoocH
+// search is a heuristic whose result moves a lot with the budget and the L_I tree cap (on the
+// cfg2 profile: 265-535 ms across budgets within 3 % and caps 4-12). So pooch_plan runs the
+// paper's search (Sec. 4.4) over a small grid -- budgets cap, cap - 0.4 %, ... and, for
+// STRAT_POOCH, tree caps 4, 6, ..., li_cap -- and keeps the candidate with the smallest simulated
+// makespan among those whose ledger packs into the arena. The grid stops four budget steps
+// after the first packable candidate (or after 40 steps). Each candidate is one plain run of
+// the planner, identical to the oracle's for its (budget, cap).
 extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_search_cfg* cfg,
                                    const uint8_t* fixed, uint8_t* classes_out, pooch_plan_report* report) {
   if (!c || !c->budget_set) return fail(POOCH_EUSAGE, "set the budget first");
   if (!c->have_profile) return ctx_fail(c, fail(POOCH_EUSAGE, "no profile: call pooch_profile or pooch_set_profile"));
   const int n = c->g.n();
-  uint64_t cap = c->dev_bytes - c->resident_end;
-  pooch_search_cfg sc = cfg ? *cfg : pooch_search_cfg{16, 0, POOCH_SCHED_EAGER};
-  uint64_t budget = cap;
-  for (int attempt = 0; attempt < 12; ++attempt) {
-    Problem p = make_problem(c, budget);
-    Planner pl(p, sc);
+  const uint64_t cap = c->dev_bytes - c->resident_end;
+  const pooch_search_cfg sc = cfg ? *cfg : pooch_search_cfg{16, 0, POOCH_SCHED_EAGER};
+  std::vector<int> caps;
+  if (strategy == POOCH_STRAT_POOCH && sc.li_cap > 4)
+    for (int lc = 4; lc <= sc.li_cap; lc += 2) caps.push_back(lc);
+  if (caps.empty() || caps.back() != sc.li_cap) caps.push_back(sc.li_cap);
+  const bool grid = strategy != POOCH_STRAT_FIXED && strategy != POOCH_STRAT_INCORE &&
+                    !getenv("POOCH_PLAN_NO_GRID");
+  const uint64_t step_bytes = std::max<uint64_t>(cap / 250, 1);
+
+  struct Best {
+    int64_t mk = INT64_MAX;
     std::vector<uint8_t> cls;
-    int64_t mk;
-    pooch_status st = pl.run(strategy, fixed, cls, mk);
-    if (st != POOCH_OK) {
-      pl.report(cls, mk, report);
-      return ctx_fail(c, st);
-    }
-    // host capacity for the swap class
-    uint64_t host_need = 0;
-    for (int m = 0; m < n; ++m)
-      if (cls[m] == C_SWAP) host_need += align_up(c->map_bytes[m]);
-    if (host_need > c->host_bytes)
-      return ctx_fail(c, fail(POOCH_EINFEASIBLE, "plan swaps %llu B but the host arena has %zu B",
-                              (unsigned long long)host_need, c->host_bytes));
-    SimOptions o;
-    o.sched = pl.sched();
-    o.record_events = true;
-    o.record_ledger = true;
     SimOut so;
-    simulate(p, cls.data(), o, so);
-    std::vector<int> dummy;
-    c->cls = cls;
-    if (!so.oom && pack(c, so, cap, dummy)) {
-      c->program = so.program;
-      c->sched = pl.sched();
-      compile(c, so);
-      c->host_off.assign(n, 0);
-      size_t ho = 0;
-      for (int m = 0; m < n; ++m)
-        if (cls[m] == C_SWAP) {
-          c->host_off[m] = ho;
-          ho += align_up(c->map_bytes[m]);
+    std::vector<uint64_t> off;
+    uint64_t high = 0;
+    pooch_plan_report rep{};
+    int sched = 0;
+    uint64_t budget = 0;
+  } best;
+  int64_t sims = 0;
+  double wall = 0;
+  int first_found = -1;
+  pooch_status last_st = POOCH_EINFEASIBLE;
+  std::string why = "static offset packing failed (fragmentation) at every budget tried";
+  for (int step = 0; step < 40; ++step) {
+    if (step * step_bytes >= cap) break;
+    const uint64_t budget = cap - step * step_bytes;
+    for (int lc : caps) {
+      pooch_search_cfg s2 = sc;
+      s2.li_cap = lc;
+      Problem p = make_problem(c, budget);
+      Planner pl(p, s2);
+      std::vector<uint8_t> cls;
+      int64_t mk;
+      pooch_status st = pl.run(strategy, fixed, cls, mk);
+      pooch_plan_report rep{};
+      pl.report(cls, mk, &rep);
+      sims += rep.n_sims;
+      wall += rep.wall_ms;
+      if (st != POOCH_OK) {
+        last_st = st;
+        if (st != POOCH_EINFEASIBLE) {  // usage errors do not depend on the budget
+          if (report) *report = rep;
+          return ctx_fail(c, st);
         }
-      // events: one sync event per op (+ start events)
-      while (c->ev.size() < c->ops.size()) {
-        cudaEvent_t e;
-        POOCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->ev.push_back(e);
+        why = pooch_last_error(nullptr) ? pooch_last_error(nullptr) : why;
+        continue;
       }
-      while (c->ev_start.size() < c->ops.size()) {
-        cudaEvent_t e;
-        POOCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->ev_start.push_back(e);
+      if (mk >= best.mk) continue;
+      uint64_t host_need = 0;
+      for (int m = 0; m < n; ++m)
+        if (cls[m] == C_SWAP) host_need += align_up(c->map_bytes[m]);
+      if (host_need > c->host_bytes) {
+        last_st = POOCH_EINFEASIBLE;
+        char buf[160];
+        snprintf(buf, sizeof(buf), "plan swaps %llu B but the host arena has %zu B", (unsigned long long)host_need,
+                 c->host_bytes);
+        why = buf;
+        continue;
       }
-      c->have_plan = true;
-      pl.report(cls, mk, report);
-      if (report) report->arena_bytes = c->arena_high + c->resident_end;
-      if (classes_out) std::copy(cls.begin(), cls.end(), classes_out);
-      return POOCH_OK;
+      SimOptions o;
+      o.sched = pl.sched();
+      o.record_events = true;
+      o.record_ledger = true;
+      SimOut so;
+      simulate(p, cls.data(), o, so);
+      if (so.oom) continue;
+      std::vector<uint64_t> off;
+      uint64_t high;
+      if (!pack_ledger(so.ledger, 3 * n, cap, getenv("POOCH_DEBUG_NO_REUSE") != nullptr, off, high)) continue;
+      best.mk = mk;
+      best.cls = cls;
+      best.so = std::move(so);
+      best.off = std::move(off);
+      best.high = high;
+      best.rep = rep;
+      best.sched = pl.sched();
+      best.budget = budget;
+      if (first_found < 0) first_found = step;
     }
-    // fragmentation: plan against a smaller budget and try again
-    budget = budget - std::max<uint64_t>(cap / 50, 1);
+    if (!grid || (first_found >= 0 && step >= first_found + 4)) break;
   }
-  return ctx_fail(c, fail(POOCH_EINFEASIBLE, "static offset packing failed (fragmentation) after 12 attempts"));
+  if (best.cls.empty()) {
+    if (last_st != POOCH_EINFEASIBLE) return ctx_fail(c, last_st);
+    return ctx_fail(c, fail(POOCH_EINFEASIBLE, "%s", why.c_str()));
+  }
+  const std::vector<uint8_t>& cls = best.cls;
+  c->cls = cls;
+  c->buf_off.assign(best.off.size(), 0);
+  for (size_t q = 0; q < best.off.size(); ++q) c->buf_off[q] = c->resident_end + best.off[q];
+  c->arena_high = best.high;
+  c->program = best.so.program;
+  c->sched = best.sched;
+  compile(c, best.so);
+  c->host_off.assign(n, 0);
+  size_t ho = 0;
+  for (int m = 0; m < n; ++m)
+    if (cls[m] == C_SWAP) {
+      c->host_off[m] = ho;
+      ho += align_up(c->map_bytes[m]);
+    }
+  // events: one sync event per op (+ start events)
+  while (c->ev.size() < c->ops.size()) {
+    cudaEvent_t e;
+    POOCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ev.push_back(e);
+  }
+  while (c->ev_start.size() < c->ops.size()) {
+    cudaEvent_t e;
+    POOCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ev_start.push_back(e);
+  }
+  c->have_plan = true;
+  c->plan_budget = best.budget;
+  if (report) {
+    *report = best.rep;
+    report->n_sims = sims;
+    report->wall_ms = wall;
+    report->arena_bytes = c->arena_high + c->resident_end;
+  }
+  if (classes_out) std::copy(cls.begin(), cls.end(), classes_out);
+  return POOCH_OK;
 }
 
 // ====================================================================== training step

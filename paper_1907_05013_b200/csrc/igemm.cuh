@@ -79,6 +79,7 @@ struct GemmParams {
   // [c_split, C) come from the third tensor map; DGRAD columns [n_split, Ng) go to d2
   int c_split, n_split, accumulate2;
   float* d2;
+  int epi_direct;        // 1: each thread stores its own row (no smem staging); experiments only
 };
 
 constexpr int BM = 128;
@@ -739,11 +740,40 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Ng) ? __ldg(p.bias + nb + i) : 0.f;
           }
         }
-        // Coalesced store: the warp stages its 32 rows x 32 columns in shared memory (16-B chunk j
-        // of row r at chunk j ^ (r & 7): conflict free both ways), then each instruction writes
-        // four whole 128-B row segments (lanes 8i..8i+7 = one row) instead of 32 scattered 16-B
-        // pieces. DGRAD accumulation reads the old values with the same pattern (same fp32 add).
-        {
+        // destination of row gmr, columns [col, col + 4) (gmr < 0: row not stored)
+        auto dst_of = [&](int gmr, int col) -> float* {
+          if constexpr (MODE == GEMM_TEST) {
+            return p.d + (size_t)z * p.M * p.ldd + (size_t)gmr * p.ldd + col;
+          } else if constexpr (MODE == CONV_WGRAD) {
+            return p.d + ((size_t)z * p.M + gmr) * p.Ng + col;
+          } else {
+            if (MODE == CONV_DGRAD && p.n_split > 0)  // two-source input: split dx by channel
+              return nb < p.n_split ? p.d + (size_t)gmr * p.n_split + col
+                                    : p.d2 + (size_t)gmr * (p.Ng - p.n_split) + (col - p.n_split);
+            return p.d + (size_t)gmr * p.Ng + col;
+          }
+        };
+        const int accum = MODE == CONV_DGRAD ? ((p.n_split > 0 && nb >= p.n_split) ? p.accumulate2 : p.accumulate) : 0;
+        if (p.epi_direct) {
+          if (rok) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              if (nb + i < p.Ng) {
+                float* dst = dst_of(gm, nb + i);
+                float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                if (accum) {
+                  float4 q = *reinterpret_cast<const float4*>(dst);
+                  o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+                }
+                *reinterpret_cast<float4*>(dst) = o;
+              }
+            }
+          }
+        } else {
+          // Coalesced store: the warp stages its 32 rows x 32 columns in shared memory (16-B chunk j
+          // of row r at chunk j ^ (r & 7): conflict free both ways), then each instruction writes
+          // four whole 128-B row segments (lanes 8i..8i+7 = one row) instead of 32 scattered 16-B
+          // pieces. DGRAD accumulation loads all eight old segments before adding (same fp32 add).
           const uint32_t stg = sbase + SM::STG_OFF + warp * 4096;
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
@@ -753,36 +783,31 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
           __syncwarp();
           const int q = lane & 7;
           const int col = nb + 4 * q;
+          float* dsts[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = 4 * i + (lane >> 3);
             const int gmr = __shfl_sync(0xffffffffu, gm, r);
             const int okr = __shfl_sync(0xffffffffu, rok ? 1 : 0, r);
+            dsts[i] = (okr && col < p.Ng) ? dst_of(gmr, col) : nullptr;
+          }
+          float4 old[8];
+          if (MODE == CONV_DGRAD && accum) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              old[i] = dsts[i] ? *reinterpret_cast<const float4*>(dsts[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + (lane >> 3);
             float4 o;
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                          : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w)
                          : "r"(stg + r * 128 + ((q ^ (r & 7)) << 4)));
-            if (okr && col < p.Ng) {
-              float* dst;
-              if constexpr (MODE == GEMM_TEST) {
-                dst = p.d + (size_t)z * p.M * p.ldd + (size_t)gmr * p.ldd + col;
-              } else if constexpr (MODE == CONV_WGRAD) {
-                dst = p.d + ((size_t)z * p.M + gmr) * p.Ng + col;
-              } else if (MODE == CONV_DGRAD && p.n_split > 0) {  // two-source input: split dx by channel
-                dst = nb < p.n_split ? p.d + (size_t)gmr * p.n_split + col
-                                     : p.d2 + (size_t)gmr * (p.Ng - p.n_split) + (col - p.n_split);
-              } else {
-                dst = p.d + (size_t)gmr * p.Ng + col;
-              }
-              if constexpr (MODE == CONV_DGRAD) {
-                const int accum = (p.n_split > 0 && nb >= p.n_split) ? p.accumulate2 : p.accumulate;
-                if (accum) {
-                  float4 qv = *reinterpret_cast<const float4*>(dst);
-                  o.x += qv.x; o.y += qv.y; o.z += qv.z; o.w += qv.w;
-                }
-              }
-              *reinterpret_cast<float4*>(dst) = o;
+            if (MODE == CONV_DGRAD && accum) {
+              o.x += old[i].x; o.y += old[i].y; o.z += old[i].z; o.w += old[i].w;
             }
+            if (dsts[i]) *reinterpret_cast<float4*>(dsts[i]) = o;
           }
           __syncwarp();
         }

@@ -161,3 +161,36 @@ def test_conv_large_wgrad_splitk():
     ref = L.conv2d_wgrad(x.transpose(0, 3, 1, 2).astype(np.float64), gy.transpose(0, 3, 1, 2).astype(np.float64),
                          (K, Cin, R, R), s, p).transpose(0, 2, 3, 1)
     assert rel(ddw.cpu().numpy(), ref) < TOL_OP
+
+
+@pytest.mark.parametrize("N,H,C,k,s,p", [
+    (2, 9, 8, 3, 2, 1),      # ResNet stem pool shape class (k3 s2 p1), odd extent -> ragged windows
+    (3, 16, 64, 3, 2, 1),
+    (2, 12, 32, 2, 2, 0),    # tiny CNN (k2 s2)
+    (1, 7, 4, 3, 1, 1)])     # overlapping stride-1 windows
+def test_maxpool2d(N, H, C, k, s, p):
+    """Max-pool fwd / bwd kernels vs the fp64 oracle (Sec. 2.1 layer math; Reading 25: gradient to
+    the first maximum). Values are distinct per window except for the forced ties below, so the
+    forward is exact and the backward routes every gradient to the same element as the oracle."""
+    lib = _lib().lib
+    g = synthdata.rng(11)
+    x = g.standard_normal((N, C, H, H))
+    x[:, :, 0, 0] = x[:, :, 0, 1]          # a tie: the first maximum must win on both sides
+    y_ref = L.maxpool_fwd(x, k, s, p)
+    gy = g.standard_normal(y_ref.shape)
+    gx_ref = L.maxpool_bwd(gy, x, k, s, p)
+    nhwc = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(0, 2, 3, 1), np.float32)).cuda()  # noqa: E731
+    xd, gyd = nhwc(x), nhwc(gy)
+    Ho = y_ref.shape[2]
+    yd = torch.empty(N, Ho, Ho, C, device="cuda")
+    gxd = torch.empty(N, H, H, C, device="cuda")
+    ws = torch.empty(N * Ho * Ho * C, dtype=torch.uint8, device="cuda")
+    assert lib.pooch_op_maxpool2d_fwd(ptr(xd), ptr(yd), N, H, H, C, k, s, p, None) == 0
+    assert lib.pooch_op_maxpool2d_bwd(ptr(xd), ptr(gyd), ptr(gxd), ptr(ws), N, H, H, C, k, s, p, None) == 0
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy().transpose(0, 3, 1, 2)
+    gx = gxd.cpu().numpy().transpose(0, 3, 1, 2)
+    np.testing.assert_array_equal(y, y_ref.astype(np.float32))
+    assert rel(gx, gx_ref) < 1e-6
+    # support of the routed gradient is identical (index work: exact)
+    np.testing.assert_array_equal(gx != 0, gx_ref != 0)
