@@ -48,10 +48,12 @@ static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 template <int MODE, int BN, bool X3 = false, bool TMA = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr) {
-  // deepest ring that fits 227 KB: TMA wgrad has the longest load -> MMA latency (TMA, then an
-  // in-place transpose by the auxiliary warps), so it gets every stage that fits
+  // deepest ring that fits 227 KB next to the epilogue staging / reduction buffers: a k-block's
+  // MMAs take only 0.2-0.4 us, less than the TMA -> (3xTF32 split / wgrad transpose) -> MMA
+  // latency, so the ring depth sets the throughput of the short-K and narrow (BN = 64) layers
   constexpr int STAGE_B = (BM + BN) * BK * 4 * (X3 ? 2 : 1);
-  constexpr int STAGES = (MODE == CONV_WGRAD && TMA) ? std::min(8, (200 * 1024) / STAGE_B) : (X3 ? 3 : 4);
+  constexpr int FIXED_B = GemmSmem<BN, 1, X3>::TOTAL - STAGE_B + 64;
+  constexpr int STAGES = std::max(2, std::min(8, (227 * 1024 - FIXED_B) / STAGE_B));
   constexpr int SMEM = GemmSmem<BN, STAGES, X3>::TOTAL;
   auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA>;
   static bool configured = false;
