@@ -19,6 +19,9 @@ and is always resident, Reading 2):
 * ``maxpool``   y = maxpool(x)                 bwd needs {x} (argmax from x)
 * ``avgpool``   y = mean_hw(x)                 bwd needs {}
 * ``fc_ce``     z = flat(x) W^T + b; CE loss   bwd needs {x, z} (sink task)
+* ``bnrelu_conv``  y = conv(relu(bn(c)), W)    bwd needs {c}  (the BN-ReLU
+  applied to the conv's operand on load, so relu(bn(c)) is never a map; built by
+  ``fuse_bnrelu`` from the plain graph, same function, same parameters)
 
 3D network (BASELINE.json config 4, "3D U-Net-style, conv3d-BN-ReLU"):
 
@@ -51,11 +54,12 @@ class Task:
     pad: int = 0
     k: int = 0              # conv/pool kernel size
     cin: int = 0            # conv input channels (true, unpadded)
+    bn: str = ""            # bnrelu_conv: name of the fused BN-ReLU (its gamma / beta)
 
     @property
     def needs(self):
         """Maps bwd(task) reads (see module docstring)."""
-        if self.kind in ("conv", "maxpool", "upconv"):
+        if self.kind in ("conv", "maxpool", "upconv", "bnrelu_conv"):
             return [i for i in self.inputs if i >= 0]
         if self.kind in ("bnrelu", "tail_proj", "tail_id"):
             return [i for i in self.inputs if i >= 0]
@@ -176,6 +180,38 @@ def unet3d(in_d: int = 256, width: int = 256, classes: int = 2, cin: int = 1) ->
     return net
 
 
+def fuse_bnrelu(net: Net) -> Net:
+    """merge every ``bnrelu`` whose only consumer is a single-input 2D conv with
+    32-multiple input channels (the B200 path's TMA-fed operand loader, which applies the
+    BN-ReLU on load) into that conv (kind ``bnrelu_conv``). Same function and parameters; the
+    merged BN-ReLU outputs stop being maps. Task order is kept; inputs are renumbered."""
+    n = len(net.tasks)
+    consumers = [[k for k in range(n) if i in net.tasks[k].inputs] for i in range(n)]
+    fused = set()
+    for i, t in enumerate(net.tasks):
+        if t.kind != "bnrelu" or len(consumers[i]) != 1 or net.dims != 2:
+            continue
+        k = consumers[i][0]
+        u = net.tasks[k]
+        if u.kind == "conv" and u.inputs == [i] and u.cin % 32 == 0 and u.stride <= 2:
+            fused.add(i)
+    out = Net(net.name + "_f2", net.in_chw, net.classes)
+    new_id = {}
+    for i, t in enumerate(net.tasks):
+        if i in fused:
+            continue
+        ins = []
+        for j in t.inputs:
+            ins.append(-1 if j < 0 else new_id[net.tasks[j].inputs[0] if j in fused else j])
+        if t.kind == "conv" and t.inputs[0] in fused:
+            bn = net.tasks[t.inputs[0]]
+            nt = Task(t.name, "bnrelu_conv", ins, t.out_chw, t.stride, t.pad, t.k, t.cin, bn=bn.name)
+        else:
+            nt = Task(t.name, t.kind, ins, t.out_chw, t.stride, t.pad, t.k, t.cin, t.bn)
+        new_id[i] = out.add(nt)
+    return out
+
+
 # -------------------------------------------------------------------- census
 def census(net: Net, batch: int):
     """[(name, bytes)] of every saved feature map (C2)."""
@@ -186,7 +222,10 @@ def param_shapes(net: Net):
     """Ordered {param name: shape}; conv weights OIHW, FC [O, I]."""
     shapes = {}
     for t in net.tasks:
-        if t.kind == "conv":
+        if t.kind == "bnrelu_conv":     # the fused BN's parameters first (the plain graph's order)
+            shapes[t.bn + ".gamma"] = (t.cin,)
+            shapes[t.bn + ".beta"] = (t.cin,)
+        if t.kind in ("conv", "bnrelu_conv"):
             shapes[t.name + ".w"] = (t.out_chw[0], t.cin) + (t.k,) * (len(t.out_chw) - 1)
         elif t.kind == "upconv":
             shapes[t.name + ".w"] = (t.cin, t.out_chw[0], 2, 2, 2)
@@ -238,6 +277,11 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             f = L.conv3d_fwd if three else L.conv2d_fwd
             y = f(q(conv_in(t)), q(P[t.name + ".w"]), t.stride, t.pad)
             cache = None
+        elif t.kind == "bnrelu_conv":
+            z, bc = L.bn_fwd(get(t.inputs[0]), P[t.bn + ".gamma"], P[t.bn + ".beta"])
+            r = L.relu_fwd(z)
+            y = L.conv2d_fwd(q(r), q(P[t.name + ".w"]), t.stride, t.pad)
+            cache = (bc, r)
         elif t.kind == "upconv":
             y = L.upconv3d_fwd(q(get(t.inputs[0])), q(P[t.name + ".w"]))
             cache = None
@@ -320,6 +364,16 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
                     cj = get(j).shape[1]
                     acc(j, dx[:, c0:c0 + cj])
                     c0 += cj
+        elif t.kind == "bnrelu_conv":
+            bc, r = cache
+            w = P[t.name + ".w"]
+            grads[t.name + ".w"] += L.conv2d_wgrad(q(r), q(dy), w.shape, t.stride, t.pad)
+            dr = L.conv2d_dgrad(q(dy), q(w), r.shape, t.stride, t.pad)
+            dz = L.relu_bwd(dr, r)
+            dx, dg, db = L.bn_bwd(dz, bc, P[t.bn + ".gamma"])
+            grads[t.bn + ".gamma"] += dg
+            grads[t.bn + ".beta"] += db
+            acc(t.inputs[0], dx)
         elif t.kind == "upconv":
             dx, dw = L.upconv3d_bwd(q(dy), q(get(t.inputs[0])), q(P[t.name + ".w"]))
             grads[t.name + ".w"] += dw
