@@ -78,8 +78,13 @@ typedef enum {
   POOCH_L_AVGPOOL = 5,   /* y = mean_hw(x)                               bwd reads {}       */
   POOCH_L_FC_CE = 6,     /* z = flat_hwc(x) W^T + b, softmax-CE loss     bwd reads {x, z}   */
   POOCH_L_UPCONV = 7,    /* y = transposed conv k2 s2 of x (3D U-Net up-sampling)  bwd reads {x} */
-  POOCH_L_HEAD_CE = 8    /* z = x W^T + b per voxel, softmax-CE averaged over voxels  bwd reads {x, z} */
+  POOCH_L_HEAD_CE = 8,   /* z = x W^T + b per voxel, softmax-CE averaged over voxels  bwd reads {x, z} */
+  POOCH_L_BNRELU_CONV = 9 /* y = conv(relu(BN(c)), W): BN-ReLU applied to the conv's operand on
+                             load, relu(BN(c)) never stored   bwd reads {c} */
 } pooch_layer_kind;
+/* POOCH_L_BNRELU_CONV: c (in0) is a conv output with this task as its only consumer; 2D, single
+ * input, cin a multiple of 32, stride <= 2. name = "<bn name>+<conv name>": the BN's gamma /
+ * beta are named after the first part, the conv weight after the second. */
 /* A POOCH_L_CONV with in1 >= 0 reads the channel concatenation [in0, in1] in place (the
  * U-Net's skip connection): cin = cout(in0) + cout(in1), both multiples of 32.
  * 3D networks (io.in_d > 0, batch 1): every conv is k x k x k; maxpool is k2 s2 p0 over 2^3
@@ -104,9 +109,13 @@ typedef struct {
 
 /* Built-in workloads of BASELINE.json: 0 = tiny CNN (config 1), 1 = ResNet-50 v1.5
  * (configs 2, 3, 5), 2 = ResNet-50 v1, 3 = 3D U-Net (config 4: in_hw^3 volume, base width
- * `width` -> level widths w, 2w, 4w, 4w, input channels padded 1 -> 32). Fills up to
+ * `width` -> level widths w, 2w, 4w, 4w, input channels padded 1 -> 32). which |
+ * POOCH_NET_FUSE_BNRELU merges every BN-ReLU whose only consumer is a single-input 2D conv with
+ * cin % 32 == 0 and stride <= 2 into that conv (POOCH_L_BNRELU_CONV; same function and
+ * parameters, fewer maps: ResNet-50 105 -> 73, tiny CNN 10 -> 7). Fills up to
  * *n_layers entries of `out` (host) and sets *n_layers to the task count (call with
  * out=NULL to query). */
+#define POOCH_NET_FUSE_BNRELU 16
 pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t classes, int32_t width,
                              pooch_layer_desc* out, int32_t* n_layers);
 

@@ -15,6 +15,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -966,17 +968,6 @@ bool pack_ledger(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap,
   return true;
 }
 
-static bool pack(pooch_ctx* c, const SimOut& so, uint64_t cap, std::vector<int>& alloc_op_buf) {
-  (void)alloc_op_buf;
-  std::vector<uint64_t> off;
-  uint64_t high;
-  if (!pack_ledger(so.ledger, 3 * c->g.n(), cap, getenv("POOCH_DEBUG_NO_REUSE") != nullptr, off, high)) return false;
-  c->buf_off.assign(off.size(), 0);
-  for (size_t b = 0; b < off.size(); ++b) c->buf_off[b] = c->resident_end + off[b];  // arena offsets
-  c->arena_high = high;
-  return true;
-}
-
 // Build the op list with cross-stream waits from the simulated events and ledger.
 static void compile(pooch_ctx* c, const SimOut& so) {
   const int n = c->g.n();
@@ -1096,13 +1087,14 @@ extern "C" pooch_status pooch_set_profile(pooch_ctx* c, const int64_t* fwd, cons
 // Plan selection with packing in the loop (row a6). The simulator's memory ledger is a byte
 // sum (Sec. 4.1.2), so a plan whose simulated peak fits the arena may still fail to pack into
 // static offsets (fragmentation: measured +2-8 % over the peak on ResNet-50). And the PoocH
-// search is a heuristic whose result moves a lot with the budget and the L_I tree cap (on the
-// cfg2 profile: 265-535 ms across budgets within 3 % and caps 4-12). So pooch_plan runs the
-// paper's search (Sec. 4.4) over a small grid -- budgets cap, cap - 0.4 %, ... and, for
-// STRAT_POOCH, tree caps 4, 6, ..., li_cap -- and keeps the candidate with the smallest simulated
-// makespan among those whose ledger packs into the arena. The grid stops four budget steps
-// after the first packable candidate (or after 40 steps). Each candidate is one plain run of
-// the planner, identical to the oracle's for its (budget, cap).
+// search is a heuristic whose result moves a lot with the budget and the L_I tree cap (on one
+// cfg2 profile: 251-471 ms across budgets within 6 % and caps 3-12). So pooch_plan runs the
+// paper's search (Sec. 4.4) over a grid -- budgets cap, cap - 0.4 %, ..., cap - 6 % and, for
+// STRAT_POOCH, tree caps 3 .. li_cap -- in parallel (one search per thread), then packs the
+// candidates in order of simulated makespan and keeps the first that packs into the arena.
+// Each candidate is one plain run of the planner, identical to the oracle's for its
+// (budget, cap). POOCH_PLAN_NO_GRID=1: the single search at the full budget (retrying 2 %
+// lower on fragmentation); POOCH_PLAN_STEPS=k: k budget steps.
 extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_search_cfg* cfg,
                                    const uint8_t* fixed, uint8_t* classes_out, pooch_plan_report* report) {
   if (!c || !c->budget_set) return fail(POOCH_EUSAGE, "set the budget first");
@@ -1110,16 +1102,25 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
   const int n = c->g.n();
   const uint64_t cap = c->dev_bytes - c->resident_end;
   const pooch_search_cfg sc = cfg ? *cfg : pooch_search_cfg{16, 0, POOCH_SCHED_EAGER};
+  const bool grid = strategy != POOCH_STRAT_FIXED && strategy != POOCH_STRAT_INCORE && !getenv("POOCH_PLAN_NO_GRID");
   std::vector<int> caps;
-  if (strategy == POOCH_STRAT_POOCH && sc.li_cap > 4)
-    for (int lc = 4; lc <= sc.li_cap; lc += 2) caps.push_back(lc);
-  if (caps.empty() || caps.back() != sc.li_cap) caps.push_back(sc.li_cap);
-  const bool grid = strategy != POOCH_STRAT_FIXED && strategy != POOCH_STRAT_INCORE &&
-                    !getenv("POOCH_PLAN_NO_GRID");
-  const uint64_t step_bytes = std::max<uint64_t>(cap / 250, 1);
+  if (grid && strategy == POOCH_STRAT_POOCH)
+    for (int lc = 3; lc < sc.li_cap; ++lc) caps.push_back(lc);
+  caps.push_back(sc.li_cap);
+  const int steps = grid ? (getenv("POOCH_PLAN_STEPS") ? std::max(1, atoi(getenv("POOCH_PLAN_STEPS"))) : 16) : 12;
+  const uint64_t step_bytes = grid ? std::max<uint64_t>(cap / 250, 1) : std::max<uint64_t>(cap / 50, 1);
 
-  struct Best {
+  struct Cand {
+    uint64_t budget = 0;
+    int li_cap = 0, step = 0;
+    pooch_status st = POOCH_OK;
+    std::string err;
+    std::vector<uint8_t> cls;
     int64_t mk = INT64_MAX;
+    pooch_plan_report rep{};
+    int sched = 0;
+  };
+  struct Best {
     std::vector<uint8_t> cls;
     SimOut so;
     std::vector<uint64_t> off;
@@ -1130,71 +1131,114 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
   } best;
   int64_t sims = 0;
   double wall = 0;
-  int first_found = -1;
-  pooch_status last_st = POOCH_EINFEASIBLE;
   std::string why = "static offset packing failed (fragmentation) at every budget tried";
-  for (int step = 0; step < 40; ++step) {
-    if (step * step_bytes >= cap) break;
-    const uint64_t budget = cap - step * step_bytes;
-    for (int lc : caps) {
-      pooch_search_cfg s2 = sc;
-      s2.li_cap = lc;
-      Problem p = make_problem(c, budget);
-      Planner pl(p, s2);
-      std::vector<uint8_t> cls;
-      int64_t mk;
-      pooch_status st = pl.run(strategy, fixed, cls, mk);
-      pooch_plan_report rep{};
-      pl.report(cls, mk, &rep);
-      sims += rep.n_sims;
-      wall += rep.wall_ms;
-      if (st != POOCH_OK) {
-        last_st = st;
-        if (st != POOCH_EINFEASIBLE) {  // usage errors do not depend on the budget
-          if (report) *report = rep;
-          return ctx_fail(c, st);
-        }
-        why = pooch_last_error(nullptr) ? pooch_last_error(nullptr) : why;
-        continue;
-      }
-      if (mk >= best.mk) continue;
-      uint64_t host_need = 0;
-      for (int m = 0; m < n; ++m)
-        if (cls[m] == C_SWAP) host_need += align_up(c->map_bytes[m]);
-      if (host_need > c->host_bytes) {
-        last_st = POOCH_EINFEASIBLE;
-        char buf[160];
-        snprintf(buf, sizeof(buf), "plan swaps %llu B but the host arena has %zu B", (unsigned long long)host_need,
-                 c->host_bytes);
-        why = buf;
-        continue;
-      }
-      SimOptions o;
-      o.sched = pl.sched();
-      o.record_events = true;
-      o.record_ledger = true;
-      SimOut so;
-      simulate(p, cls.data(), o, so);
-      if (so.oom) continue;
-      std::vector<uint64_t> off;
-      uint64_t high;
-      if (!pack_ledger(so.ledger, 3 * n, cap, getenv("POOCH_DEBUG_NO_REUSE") != nullptr, off, high)) continue;
-      best.mk = mk;
-      best.cls = cls;
-      best.so = std::move(so);
-      best.off = std::move(off);
-      best.high = high;
-      best.rep = rep;
-      best.sched = pl.sched();
-      best.budget = budget;
-      if (first_found < 0) first_found = step;
+  pooch_status hard = POOCH_OK;
+
+  auto run_cand = [&](Cand& k) {
+    pooch_search_cfg s2 = sc;
+    s2.li_cap = k.li_cap;
+    if (grid) s2.threads = 1;
+    Problem p = make_problem(c, k.budget);
+    Planner pl(p, s2);
+    k.st = pl.run(strategy, fixed, k.cls, k.mk);
+    if (k.st != POOCH_OK) k.err = pooch_last_error(nullptr);
+    pl.report(k.cls, k.mk, &k.rep);
+    k.sched = pl.sched();
+  };
+  // try to adopt candidate k: host capacity, ledger, static offsets; true on success
+  auto adopt = [&](const Cand& k) {
+    uint64_t host_need = 0;
+    for (int m = 0; m < n; ++m)
+      if (k.cls[m] == C_SWAP) host_need += align_up(c->map_bytes[m]);
+    if (host_need > c->host_bytes) {
+      char buf[160];
+      snprintf(buf, sizeof(buf), "plan swaps %llu B but the host arena has %zu B", (unsigned long long)host_need,
+               c->host_bytes);
+      why = buf;
+      return false;
     }
-    if (!grid || (first_found >= 0 && step >= first_found + 4)) break;
+    Problem p = make_problem(c, k.budget);
+    SimOptions o;
+    o.sched = k.sched;
+    o.record_events = true;
+    o.record_ledger = true;
+    SimOut so;
+    simulate(p, k.cls.data(), o, so);
+    if (so.oom) return false;
+    std::vector<uint64_t> off;
+    uint64_t high;
+    if (!pack_ledger(so.ledger, 3 * n, cap, getenv("POOCH_DEBUG_NO_REUSE") != nullptr, off, high)) return false;
+    best.cls = k.cls;
+    best.so = std::move(so);
+    best.off = std::move(off);
+    best.high = high;
+    best.rep = k.rep;
+    best.sched = k.sched;
+    best.budget = k.budget;
+    return true;
+  };
+
+  if (grid) {
+    std::vector<Cand> cands;
+    for (int st = 0; st < steps && (uint64_t)st * step_bytes < cap; ++st)
+      for (int lc : caps) {
+        Cand k;
+        k.budget = cap - st * step_bytes;
+        k.li_cap = lc;
+        k.step = st;
+        cands.push_back(std::move(k));
+      }
+    std::atomic<int> next{0};
+    const int T = std::max(1, std::min<int>((int)cands.size(), (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> ts;
+    for (int t = 0; t < T; ++t)
+      ts.emplace_back([&] {
+        for (int i = next++; i < (int)cands.size(); i = next++) run_cand(cands[i]);
+      });
+    for (auto& t : ts) t.join();
+    std::vector<int> order;
+    for (int i = 0; i < (int)cands.size(); ++i) {
+      sims += cands[i].rep.n_sims;
+      wall = std::max(wall, cands[i].rep.wall_ms);
+      if (cands[i].st == POOCH_OK) order.push_back(i);
+      else if (cands[i].st != POOCH_EINFEASIBLE) hard = cands[i].st;
+      else why = cands[i].err;
+    }
+    if (hard != POOCH_OK) {
+      if (report) *report = cands[0].rep;
+      return ctx_fail(c, fail(hard, "%s", cands[0].err.c_str()));
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+      return cands[x].mk != cands[y].mk ? cands[x].mk < cands[y].mk
+                                        : (cands[x].step != cands[y].step ? cands[x].step < cands[y].step
+                                                                          : cands[x].li_cap < cands[y].li_cap);
+    });
+    std::vector<std::vector<uint8_t>> tried;
+    for (int i : order) {
+      if (std::find(tried.begin(), tried.end(), cands[i].cls) != tried.end()) continue;
+      tried.push_back(cands[i].cls);
+      if (adopt(cands[i])) break;
+    }
+  } else {
+    for (int st = 0; st < steps && (uint64_t)st * step_bytes < cap; ++st) {
+      Cand k;
+      k.budget = cap - st * step_bytes;
+      k.li_cap = sc.li_cap;
+      run_cand(k);
+      sims += k.rep.n_sims;
+      wall += k.rep.wall_ms;
+      if (k.st != POOCH_OK) {
+        if (k.st != POOCH_EINFEASIBLE) {
+          if (report) *report = k.rep;
+          return ctx_fail(c, k.st);
+        }
+        why = k.err;
+        continue;
+      }
+      if (adopt(k)) break;
+    }
   }
-  if (best.cls.empty()) {
-    if (last_st != POOCH_EINFEASIBLE) return ctx_fail(c, last_st);
-    return ctx_fail(c, fail(POOCH_EINFEASIBLE, "%s", why.c_str()));
-  }
+  if (best.cls.empty()) return ctx_fail(c, fail(POOCH_EINFEASIBLE, "%s", why.c_str()));
   const std::vector<uint8_t>& cls = best.cls;
   c->cls = cls;
   c->buf_off.assign(best.off.size(), 0);

@@ -106,6 +106,44 @@ void unet3d(Builder& b, int e, int classes, int w) {
   b.add(POOCH_L_HEAD_CE, src, -1, c, classes, e, e, 1, 1, 0, "head", e);
 }
 
+// SURVEY 8(f) f2 (oracle: nets.fuse_bnrelu, same rule): merge every BN-ReLU whose only consumer
+// is a single-input 2D conv with cin % 32 == 0 and stride <= 2 into that conv.
+void fuse_bnrelu(std::vector<pooch_layer_desc>& L) {
+  const int n = (int)L.size();
+  std::vector<int> ncons(n, 0), cons(n, -1);
+  for (int i = 0; i < n; ++i)
+    for (int m : {L[i].in0, L[i].in1})
+      if (m >= 0) {
+        ncons[m]++;
+        cons[m] = i;
+      }
+  std::vector<char> gone(n, 0);
+  for (int i = 0; i < n; ++i) {
+    if (L[i].kind != POOCH_L_BNRELU || ncons[i] != 1 || L[i].dout > 0) continue;
+    const pooch_layer_desc& u = L[cons[i]];
+    if (u.kind == POOCH_L_CONV && u.in0 == i && u.in1 < 0 && u.cin % 32 == 0 && u.stride <= 2) gone[i] = 1;
+  }
+  std::vector<int> nid(n, -1);
+  std::vector<pooch_layer_desc> out;
+  for (int i = 0; i < n; ++i) {
+    if (gone[i]) continue;
+    pooch_layer_desc d = L[i];
+    if (d.kind == POOCH_L_CONV && d.in0 >= 0 && gone[d.in0]) {
+      const pooch_layer_desc& bn = L[d.in0];
+      std::string nm = std::string(bn.name, strnlen(bn.name, sizeof(bn.name))) + "+" +
+                       std::string(d.name, strnlen(d.name, sizeof(d.name)));
+      std::snprintf(d.name, sizeof(d.name), "%s", nm.c_str());
+      d.kind = POOCH_L_BNRELU_CONV;
+      d.in0 = L[d.in0].in0;
+    }
+    if (d.in0 >= 0) d.in0 = nid[d.in0];
+    if (d.in1 >= 0) d.in1 = nid[d.in1];
+    nid[i] = (int)out.size();
+    out.push_back(d);
+  }
+  L.swap(out);
+}
+
 }  // namespace
 
 bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io, Graph& g, std::string& err) {
@@ -131,7 +169,7 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
       err = "task " + std::to_string(i) + ": inputs must be topological";
       return false;
     }
-    if (d.kind < POOCH_L_CONV || d.kind > POOCH_L_HEAD_CE) {
+    if (d.kind < POOCH_L_CONV || d.kind > POOCH_L_BNRELU_CONV) {
       err = "task " + std::to_string(i) + ": bad kind";
       return false;
     }
@@ -176,7 +214,14 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
         return false;
       }
     }
-    if (d.kind == POOCH_L_CONV || d.kind == POOCH_L_MAXPOOL) {
+    if (d.kind == POOCH_L_BNRELU_CONV) {
+      const Task& c = g.t[d.in0];
+      if (three || c.kind != POOCH_L_CONV && c.kind != POOCH_L_BNRELU_CONV || d.cin % 32 || d.stride > 2) {
+        err = "task " + std::to_string(i) + ": BNRELU_CONV needs a 2D conv producer, cin % 32 == 0, stride <= 2";
+        return false;
+      }
+    }
+    if (d.kind == POOCH_L_CONV || d.kind == POOCH_L_MAXPOOL || d.kind == POOCH_L_BNRELU_CONV) {
       if (co(t.hin, d.k, d.stride, d.pad) != d.hout || co(t.win, d.k, d.stride, d.pad) != d.wout ||
           (three && co(t.din, d.k, d.stride, d.pad) != t.dout)) {
         err = "task " + std::to_string(i) + ": output shape does not match geometry";
@@ -207,6 +252,7 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
     // bwd reads (see pooch_layer_kind)
     switch (d.kind) {
       case POOCH_L_CONV:
+      case POOCH_L_BNRELU_CONV:
       case POOCH_L_BNRELU:
       case POOCH_L_TAIL_PROJ:
       case POOCH_L_TAIL_ID:
@@ -294,6 +340,8 @@ using namespace pooch;
 extern "C" pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t classes, int32_t width,
                                         pooch_layer_desc* out, int32_t* n_layers) {
   if (!n_layers) return fail(POOCH_EUSAGE, "n_layers is null");
+  const bool fuse = (which & POOCH_NET_FUSE_BNRELU) != 0;
+  which &= ~POOCH_NET_FUSE_BNRELU;
   Builder b;
   if (which == 0) {
     if (in_hw <= 0 || in_hw % 2 || width <= 0 || width % 4) return fail(POOCH_EUSAGE, "bad tiny CNN size");
@@ -307,6 +355,7 @@ extern "C" pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t cl
   } else {
     return fail(POOCH_EUSAGE, "unknown network %d", which);
   }
+  if (fuse) fuse_bnrelu(b.out);
   int n = (int)b.out.size();
   if (out) {
     if (*n_layers < n) return fail(POOCH_EUSAGE, "output array too small (%d < %d)", *n_layers, n);

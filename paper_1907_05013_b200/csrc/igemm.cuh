@@ -809,10 +809,30 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
             }
             if (dsts[i]) *reinterpret_cast<float4*>(dsts[i]) = o;
           }
+          if constexpr (MODE == CONV_FWD) {
+            if (stats) {
+              // per-tile BN partial sums straight from the staged block: lane = column, rows in
+              // order (deterministic), rows outside the output grid masked
+              const unsigned okm = __ballot_sync(0xffffffffu, rok);
+              float s1 = 0.f, s2 = 0.f;
+#pragma unroll 8
+              for (int r = 0; r < 32; ++r) {
+                float x;
+                asm volatile("ld.shared.f32 %0, [%1];"
+                             : "=f"(x)
+                             : "r"(stg + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4));
+                x = ((okm >> r) & 1u) ? x : 0.f;
+                s1 += x;
+                s2 = fmaf(x, x, s2);
+              }
+              red[warp * BN + c * 32 + lane] = s1;
+              red[4 * BN + warp * BN + c * 32 + lane] = s2;
+            }
+          }
           __syncwarp();
         }
         if constexpr (MODE == CONV_FWD) {
-          if (stats) {
+          if (stats && p.epi_direct) {
             float sq[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) {

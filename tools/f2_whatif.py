@@ -1,4 +1,6 @@
-"""What-if: plan a measured ResNet-50 profile with and without BN-ReLU prologue fusion.
+"""What-if: plan a measured ResNet-50 profile with and without BN-ReLU prologue fusion,
+through the executor's plan selection (PoocH over a (budget, L_I cap) grid, keep the fastest plan
+whose ledger packs into the arena -- DESIGN.md Reading 40).
 
 Usage: python tools/f2_whatif.py gpurun_out/profile_cfg2.json [conv_slowdown]
 
@@ -22,23 +24,31 @@ n = len(net.tasks)
 inputs = [[j for j in t.inputs if j >= 0] for t in net.tasks]
 needs = [net.needs(i) for i in range(n)]
 consumers = [[k for k in range(n) if i in inputs[k]] for i in range(n)]
-budget = d["budget"]
-resident = pr["resident"]
+cap = d["budget"] - pr["resident"]
 
 
-def plan(fwd, bwd, rec, nbytes, d2h, h2d, ins, nds, is_conv):
-    p = PlanProblem(fwd, bwd, nbytes, d2h, h2d, ins, nds, resident=resident, budget=budget, rec=rec,
-                    tail=pr["tail"], is_conv=is_conv)
-    cls, rep = p.plan("pooch", li_cap=12)
-    inc = p.simulate([0] * len(fwd))
-    return cls, rep, inc
+def select(fwd, bwd, rec, nbytes, d2h, h2d, ins, nds, is_conv, li_cap=12):
+    best, first = None, None
+    for step in range(40):
+        b = cap - step * (cap // 250)
+        p = PlanProblem(fwd, bwd, nbytes, d2h, h2d, ins, nds, resident=0, budget=b, rec=rec, tail=pr["tail"],
+                        is_conv=is_conv)
+        for lc in range(4, li_cap + 1, 2):
+            cls, rep = p.plan("pooch", li_cap=lc)
+            if cls is None or (best is not None and rep.makespan_ns >= best[0]):
+                continue
+            if p.pack(cls, cap) is not None:
+                best = (rep.makespan_ns, cls, b, lc)
+                first = step if first is None else first
+        if first is not None and step >= first + 4:
+            break
+    return best
 
 
 is_conv = [int(t.kind == "conv") for t in net.tasks]
-cls, rep, inc = plan(pr["fwd"], pr["bwd"], pr["rec"], pr["bytes"], pr["d2h"], pr["h2d"], inputs, needs, is_conv)
-print("unfused: %d maps, %.1f GB, plan k/s/r = %d/%d/%d, makespan %.1f ms (in-core sim %.1f ms, oom=%s)" % (
-    n, sum(pr["bytes"]) / 1e9, cls.count(0), cls.count(1), cls.count(2), rep.makespan_ns / 1e6,
-    inc["makespan"] / 1e6, inc["oom"]))
+b0 = select(pr["fwd"], pr["bwd"], pr["rec"], pr["bytes"], pr["d2h"], pr["h2d"], inputs, needs, is_conv)
+print("unfused: %d maps, %.1f GB, plan k/s/r = %d/%d/%d, makespan %.1f ms (budget %.2f GB, cap %d)" % (
+    n, sum(pr["bytes"]) / 1e9, b0[1].count(0), b0[1].count(1), b0[1].count(2), b0[0] / 1e6, b0[2] / 1e9, b0[3]))
 
 fused = {i for i, t in enumerate(net.tasks) if t.kind == "bnrelu" and len(consumers[i]) == 1
          and net.tasks[consumers[i][0]].kind == "conv" and inputs[consumers[i][0]] == [i]}
@@ -47,20 +57,15 @@ new_id = {o: k for k, o in enumerate(keep)}
 
 
 def remap(lst):
-    out = []
-    for j in lst:
-        j = inputs[j][0] if j in fused else j
-        out.append(new_id[j])
-    return sorted(set(out))
+    return sorted({new_id[inputs[j][0] if j in fused else j] for j in lst})
 
 
 F, Bw, R, NB, D, H, I, N, C = [], [], [], [], [], [], [], [], []
 for o in keep:
     f, b = pr["fwd"][o], pr["bwd"][o]
     if net.tasks[o].kind == "conv" and inputs[o] and inputs[o][0] in fused:
-        r = inputs[o][0]
         f = int(f * slow)
-        b = b + pr["bwd"][r]
+        b = b + pr["bwd"][inputs[o][0]]
     F.append(f)
     Bw.append(b)
     R.append(f if net.tasks[o].kind == "conv" else pr["rec"][o])
@@ -70,7 +75,6 @@ for o in keep:
     I.append(remap(inputs[o]))
     N.append(remap(needs[o]))
     C.append(is_conv[o])
-cls2, rep2, inc2 = plan(F, Bw, R, NB, D, H, I, N, C)
-print("fused  : %d maps, %.1f GB, plan k/s/r = %d/%d/%d, makespan %.1f ms (in-core sim %.1f ms, oom=%s)" % (
-    len(keep), sum(NB) / 1e9, cls2.count(0), cls2.count(1), cls2.count(2), rep2.makespan_ns / 1e6,
-    inc2["makespan"] / 1e6, inc2["oom"]))
+b1 = select(F, Bw, R, NB, D, H, I, N, C)
+print("fused  : %d maps, %.1f GB, plan k/s/r = %d/%d/%d, makespan %.1f ms (budget %.2f GB, cap %d)" % (
+    len(keep), sum(NB) / 1e9, b1[1].count(0), b1[1].count(1), b1[1].count(2), b1[0] / 1e6, b1[2] / 1e9, b1[3]))
