@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--ncu-step", action="store_true",
                     help="profile/plan, 1 warm-up step, then exactly one step inside cudaProfilerStart/Stop "
                          "(for ncu --profile-from-start off); prints nothing")
+    ap.add_argument("--fuse", type=int, default=0, choices=[0, 1],
+                    help="1: BN-ReLU applied on the consuming conv's operand load (SURVEY 8(f) f2; "
+                         "ResNet-50 105 -> 73 maps)")
     ap.add_argument("--dump-profile", default=None,
                     help="write the measured profile (+ plan classes) as JSON to this path (offline planning)")
     ap.add_argument("--precision", type=int, default=1, choices=[0, 1],
@@ -73,10 +76,12 @@ class Workload:
         self.unit = "volumes/s" if self.three else "images/s"
         self.metric = METRIC_3D if self.three else METRIC
 
+    fuse = False   # BN-ReLU prologue fusion, set from --fuse
+
     def context(self, device=0, in_hw=None):
         from paper_1907_05013_b200.executor import Context
         return Context.builtin(self.net, self.batch, in_hw=in_hw or self.in_hw, classes=self.classes,
-                               width=self.width, device=device)
+                               width=self.width, device=device, fuse=self.fuse)
 
 
 def workload(args):
@@ -92,6 +97,7 @@ def workload(args):
         return Workload("resnet50", batch, None, name, 224, 1000)
     e = args.edge or 256
     budget = int(args.budget_gib * (1 << 30)) if args.budget_gib else None
+    # (the 3D U-Net has no fusable BN-ReLU: fusion is 2D only)
     name = "cfg4: 3D U-Net (widths 256/512/1024/1024) batch 1, %d^3 volume, %s" % (
         e, "all free HBM" if budget is None else "device budget %.0f GiB" % (budget / (1 << 30)))
     return Workload("unet3d", 1, budget, name, e, 2, 256)
@@ -236,6 +242,9 @@ def our_arm(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     W = workload(args)
+    W.fuse = bool(args.fuse) and not W.three
+    if W.fuse:
+        W.name += ", BN-ReLU prologue fusion (f2)"
     batch, budget, wname = W.batch, W.budget, W.name
     ctx = W.context(device=dev_idx)
     ctx.set_precision(args.precision)
@@ -449,8 +458,9 @@ def ctx_map_bytes(ctx):
 def name_out_channels(ctx, pname):
     task = pname.rsplit(".", 1)[0]
     for l in ctx.layers:
-        if l.name.decode() == task:
-            return l.cout if l.kind == 0 else ((l.cout + 3) // 4 * 4)
+        name = l.name.decode()
+        if name == task or (l.kind == 9 and name.split("+", 1)[1] == task):   # 9: BNRELU_CONV "<bn>+<conv>"
+            return l.cout if l.kind in (0, 9) else ((l.cout + 3) // 4 * 4)
     raise KeyError(pname)
 
 
@@ -562,6 +572,7 @@ def incore_run(params_host, batch, streams, args):
     (cfg4, which cannot fit) the same net at half the volume edge gives the per-voxel rate."""
     import torch
     W = workload(args)
+    W.fuse = bool(args.fuse) and not W.three
     try:
         edge = W.in_hw // 2 if W.three else None
         ctx = W.context(in_hw=edge)

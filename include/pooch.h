@@ -362,6 +362,16 @@ pooch_status pooch_op_conv_dgrad2(const pooch_conv_desc* d, const float* dy, con
                                   int32_t accumulate0, int32_t accumulate1, void* stream);
 pooch_status pooch_op_conv_wgrad2(const pooch_conv_desc* d, const float* x0, const float* x1, const float* dy,
                                   float* dw, float* ws, size_t ws_bytes, void* stream);
+/* BN-ReLU applied to the activation operand on load (the POOCH_L_BNRELU_CONV
+ * kernels): the convolution's input is relu(scale[c] * x + shift[c]) (scale / shift: device [C],
+ * the BN's gamma * invstd and beta - mean * gamma * invstd), zero padding stays zero. 2D, one
+ * source, C % 32 == 0, stride <= 2 (TMA-fed kernels), else POOCH_EUSAGE. */
+pooch_status pooch_op_conv_fwd_bnrelu(const pooch_conv_desc* d, const float* x, const float* scale,
+                                      const float* shift, const float* w, float* y, float* stat_sum,
+                                      float* stat_sq, void* stream);
+pooch_status pooch_op_conv_wgrad_bnrelu(const pooch_conv_desc* d, const float* x, const float* scale,
+                                        const float* shift, const float* dy, float* dw, float* ws,
+                                        size_t ws_bytes, void* stream);
 /* Number of M-tiles (rows of the partial-sum arrays) of pooch_op_conv_fwd for `d`. */
 int64_t pooch_op_conv_stat_tiles(const pooch_conv_desc* d);
 /* 2D max-pool (k x k window, stride s, padding p with -inf; Sec. 2.1 layer math, DESIGN.md

@@ -45,7 +45,7 @@ bool conv_shape_ok(const ConvGeom& g) {
 
 static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
-template <int MODE, int BN, bool X3 = false, bool TMA = false>
+template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr) {
   // deepest ring that fits 227 KB next to the epilogue staging / reduction buffers: a k-block's
@@ -55,7 +55,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   constexpr int FIXED_B = GemmSmem<BN, 1, X3>::TOTAL - STAGE_B + 64;
   constexpr int STAGES = std::max(2, std::min(8, (227 * 1024 - FIXED_B) / STAGE_B));
   constexpr int SMEM = GemmSmem<BN, STAGES, X3>::TOTAL;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA>;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -66,7 +66,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   int64_t tiles = (int64_t)grid.x * grid.y * grid.z;
   int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
-  kern<<<ctas, igemm_threads(MODE, X3), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
+  kern<<<ctas, igemm_threads(MODE, X3, XF), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
                                                       tc ? *tc : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -76,6 +76,25 @@ template <int MODE, bool TMA = false>
 static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st, int prec = 0,
                               const CUtensorMap* ta = nullptr, const CUtensorMap* tb = nullptr,
                               const CUtensorMap* tc = nullptr) {
+  if constexpr (TMA && (MODE == CONV_FWD || MODE == CONV_WGRAD)) {
+    if (p.xf_scale) {  // BN-ReLU on load
+      if (prec) {
+        switch (bn) {
+          case 64: return launch_igemm<MODE, 64, true, true, true>(p, grid, st, ta, tb, tc);
+          case 128: return launch_igemm<MODE, 128, true, true, true>(p, grid, st, ta, tb, tc);
+        }
+      } else {
+        switch (bn) {
+          case 64: return launch_igemm<MODE, 64, false, true, true>(p, grid, st, ta, tb, tc);
+          case 128: return launch_igemm<MODE, 128, false, true, true>(p, grid, st, ta, tb, tc);
+          case 256: return launch_igemm<MODE, 256, false, true, true>(p, grid, st, ta, tb, tc);
+        }
+      }
+      return fail(POOCH_EUSAGE, "bad tile width %d", bn);
+    }
+  } else {
+    if (p.xf_scale) return fail(POOCH_EUSAGE, "BN-ReLU on load needs the TMA-fed fwd / wgrad kernels");
+  }
   if (prec) {
     switch (bn) {
       case 64: return launch_igemm<MODE, 64, true, TMA>(p, grid, st, ta, tb, tc);
@@ -223,8 +242,13 @@ int conv_stat_tiles(const ConvGeom& g) {
 }
 
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
-                             float* stat_sq, const float* bias, cudaStream_t st, const float* x1) {
+                             float* stat_sq, const float* bias, cudaStream_t st, const float* x1,
+                             const float* xf_scale, const float* xf_shift) {
   GemmParams p = base_params(g);
+  if (xf_scale && (!fwd_uses_tma(g) || g.is3d() || g.C1 > 0 || !xf_shift))
+    return fail(POOCH_EUSAGE, "BN-ReLU on load: 2D single-source conv with C %% 32 == 0 and stride <= 2 only");
+  p.xf_scale = xf_scale;
+  p.xf_shift = xf_shift;
   p.M = (int)out_pixels(g);
   p.Ng = g.K;
   p.Kg = g.T() * g.R * g.S * g.C;
@@ -435,9 +459,14 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ ws, float* __re
 }
 
 pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
-                               size_t ws_bytes, cudaStream_t st, const float* x1) {
+                               size_t ws_bytes, cudaStream_t st, const float* x1, const float* xf_scale,
+                               const float* xf_shift) {
   WgradPlan w = wgrad_plan(g);
   GemmParams p = base_params(g);
+  if (xf_scale && (!w.tma || g.is3d() || g.C1 > 0 || !xf_shift))
+    return fail(POOCH_EUSAGE, "BN-ReLU on load: TMA-fed 2D single-source wgrad only");
+  p.xf_scale = xf_scale;
+  p.xf_shift = xf_shift;
   const int rsc = g.T() * g.R * g.S * g.C;
   p.M = w.swap ? rsc : g.K;
   p.Ng = w.swap ? g.K : rsc;
@@ -586,6 +615,24 @@ extern "C" pooch_status pooch_op_gemm_test(const float* A, const float* B, float
   p.kb_per_split = (kb + splits - 1) / splits;
   dim3 grid((M + BM - 1) / BM, (N + bn - 1) / bn, splits);
   return launch_bn<GEMM_TEST>(bn, p, grid, (cudaStream_t)stream, b_mn == 0 && a_mn == 0 ? test_prec : 0);
+}
+
+extern "C" pooch_status pooch_op_conv_fwd_bnrelu(const pooch_conv_desc* d, const float* x, const float* scale,
+                                                 const float* shift, const float* w, float* y, float* stat_sum,
+                                                 float* stat_sq, void* stream) {
+  if (!d || !x || !scale || !shift || !w || !y) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  return launch_conv_fwd(g, x, w, y, stat_sum, stat_sq, nullptr, (cudaStream_t)stream, nullptr, scale, shift);
+}
+
+extern "C" pooch_status pooch_op_conv_wgrad_bnrelu(const pooch_conv_desc* d, const float* x, const float* scale,
+                                                   const float* shift, const float* dy, float* dw, float* ws,
+                                                   size_t ws_bytes, void* stream) {
+  if (!d || !x || !scale || !shift || !dy || !dw) return fail(POOCH_EUSAGE, "null argument");
+  ConvGeom g = conv_geom(*d);
+  if (!conv_shape_ok(g)) return fail(POOCH_EUSAGE, "unsupported conv shape");
+  return launch_conv_wgrad(g, x, dy, dw, ws, ws_bytes, (cudaStream_t)stream, nullptr, scale, shift);
 }
 
 extern "C" int64_t pooch_op_conv_stat_tiles(const pooch_conv_desc* d) {

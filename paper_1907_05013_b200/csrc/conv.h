@@ -20,14 +20,17 @@ ConvGeom conv_geom(const pooch_conv_desc& d);
 bool conv_shape_ok(const ConvGeom& g);
 
 // y = conv(x, w); bias (nullable) per output channel; stat_sum/sq nullable.
+// xf_scale / xf_shift (nullable): the operand is relu(scale[c] * x + shift[c]) (BN-ReLU on load)
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
-                             float* stat_sq, const float* bias, cudaStream_t st, const float* x1 = nullptr);
+                             float* stat_sq, const float* bias, cudaStream_t st, const float* x1 = nullptr,
+                             const float* xf_scale = nullptr, const float* xf_shift = nullptr);
 // dx (and, two-source, dx1 for channels [C1, C)); accumulate / accumulate1 per destination
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
                                cudaStream_t st, float* dx1 = nullptr, bool accumulate1 = false);
 size_t conv_wgrad_ws_bytes(const ConvGeom& g);
 pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
-                               size_t ws_bytes, cudaStream_t st, const float* x1 = nullptr);
+                               size_t ws_bytes, cudaStream_t st, const float* x1 = nullptr,
+                               const float* xf_scale = nullptr, const float* xf_shift = nullptr);
 // number of M-tiles of the forward pass = rows of its BN partial-sum arrays
 int conv_stat_tiles(const ConvGeom& g);
 inline int conv_mtiles(const ConvGeom& g) { return conv_stat_tiles(g); }

@@ -115,14 +115,22 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
   cudaStream_t st = c->s[0];
   const int B = c->g.io.batch;
   switch (T.kind) {
-    case POOCH_L_CONV: {
+    case POOCH_L_CONV:
+    case POOCH_L_BNRELU_CONV: {
       float* ts = nullptr;
       float* tq = nullptr;
       if (with_stats && R.has_stats) {
         ts = reinterpret_cast<float*>(c->dev + c->off_tile);
         tq = ts + (size_t)conv_mtiles(R.geom) * R.geom.K;
       }
-      POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, ts, tq, nullptr, st, p.in1));
+      const float* xs = nullptr;
+      const float* xh = nullptr;
+      if (T.kind == POOCH_L_BNRELU_CONV) {  // the producer's BN scale / shift (saved statistics)
+        const float* sa = fptr(c, c->off_stats) + c->rt[T.in0].stat_off;
+        xs = sa + 2 * T.cin;
+        xh = sa + 3 * T.cin;
+      }
+      POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, ts, tq, nullptr, st, p.in1, xs, xh));
       if (ts) {
         float* sp = fptr(c, c->off_stats) + R.stat_off;
         int C = R.geom.K;
@@ -198,6 +206,33 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
       }
       return POOCH_OK;
     }
+    case POOCH_L_BNRELU_CONV: {
+      // wgrad with relu(BN(c)) rebuilt on load; dgrad writes d relu(BN(c)) into c's gradient
+      // buffer (this task is c's only consumer), then the BN-ReLU backward runs in place on it
+      const ConvGeom& G = RG;
+      const float* sa = fptr(c, c->off_stats) + c->rt[T.in0].stat_off;
+      const int C = T.cin;
+      double xb = 4.0 * G.N * G.H * G.W * G.C, yb = 4.0 * R.rows * G.K, wb = 4.0 * G.K * G.R * G.S * G.C;
+      if (p.acc0) return fail(POOCH_EUSAGE, "BNRELU_CONV must be the only writer of its input's gradient");
+      if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
+      POOCH_CHECK(launch_conv_wgrad(G, p.in0, p.gy, pg(c, R.w), reinterpret_cast<float*>(c->dev + c->off_wgws),
+                                    c->wgws_bytes, st, nullptr, sa + 2 * C, sa + 3 * C));
+      if (mark) mark(c, FAM_CONV_DGRAD, t, R.flops, yb + xb + wb);
+      POOCH_CHECK(launch_conv_dgrad(G, p.gy, fptr(c, c->off_wt) + R.wt_off, p.g0, false, st));
+      if (mark) mark(c, FAM_BN_BWD, t, 0, 5.0 * xb);
+      BnBwdArgs a{};
+      a.a = p.in0;
+      a.gy = p.g0;
+      a.sa = sa + 2 * C; a.ta = sa + 3 * C; a.mean_a = sa; a.invstd_a = sa + C;
+      a.gamma_a = pw(c, R.g1);
+      a.dgamma_a = pg(c, R.g1);
+      a.dbeta_a = pg(c, R.b1);
+      a.ga = p.g0;
+      a.rows = c->rt[T.in0].rows;
+      a.C = C;
+      a.mode = 0;
+      return bn_bwd(a, reinterpret_cast<float*>(c->dev + c->off_bnws), st);
+    }
     case POOCH_L_UPCONV: {
       // equivalent conv: x = the up-sampled grid (its gradient gy), dy = the upconv input
       const ConvGeom& G = RG;
@@ -264,6 +299,7 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
 int fam_fwd(int kind) {
   switch (kind) {
     case POOCH_L_CONV:
+    case POOCH_L_BNRELU_CONV:
     case POOCH_L_UPCONV: return FAM_CONV_FWD;
     case POOCH_L_BNRELU:
     case POOCH_L_TAIL_PROJ:
@@ -276,6 +312,7 @@ int fam_fwd(int kind) {
 int fam_bwd(int kind) {
   switch (kind) {
     case POOCH_L_CONV:
+    case POOCH_L_BNRELU_CONV:
     case POOCH_L_UPCONV: return FAM_CONV_WGRAD;
     case POOCH_L_BNRELU:
     case POOCH_L_TAIL_PROJ:
@@ -293,7 +330,8 @@ double fwd_bytes(pooch_ctx* c, int t) {
   double e = (double)R.rows * T.cout;
   const double din = T.dout > 0 ? T.din : 1.0;
   switch (T.kind) {
-    case POOCH_L_CONV: return 4.0 * (R.geom.N * din * R.geom.H * R.geom.W * R.geom.C + e +
+    case POOCH_L_CONV:
+    case POOCH_L_BNRELU_CONV: return 4.0 * (R.geom.N * din * R.geom.H * R.geom.W * R.geom.C + e +
                                       (double)R.geom.K * R.geom.T() * R.geom.R * R.geom.S * R.geom.C);
     case POOCH_L_UPCONV: return 4.0 * (din * T.hin * T.win * T.cin + e + 8.0 * T.cin * T.cout);
     case POOCH_L_BNRELU: return 8.0 * e;
@@ -459,7 +497,7 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
     TaskRt& R = c->rt[t];
     const bool three = T.dout > 0;
     R.rows = (int64_t)B * T.hout * T.wout * (three ? T.dout : 1);
-    if (T.kind == POOCH_L_CONV) {
+    if (T.kind == POOCH_L_CONV || T.kind == POOCH_L_BNRELU_CONV) {
       R.is_conv = true;
       R.geom = ConvGeom{B, T.hin, T.win, T.cin, T.cout, T.k, T.k, T.stride, T.pad, T.hout, T.wout};
       if (three) {
@@ -472,7 +510,18 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
         delete c;
         return fail(POOCH_EUSAGE, "task %d: unsupported conv shape (3D / two-source convs need 32-channel multiples)", t);
       }
-      R.w = param_add(c, T.name + ".w", t, wn);
+      std::string wname = T.name;
+      if (T.kind == POOCH_L_BNRELU_CONV) {  // "<bn>+<conv>": the fused BN's parameters come first
+        const size_t plus = T.name.find('+');
+        if (plus == std::string::npos) {
+          delete c;
+          return fail(POOCH_EUSAGE, "task %d: BNRELU_CONV name must be \"<bn>+<conv>\"", t);
+        }
+        R.g1 = param_add(c, T.name.substr(0, plus) + ".gamma", t, T.cin);
+        R.b1 = param_add(c, T.name.substr(0, plus) + ".beta", t, T.cin);
+        wname = T.name.substr(plus + 1);
+      }
+      R.w = param_add(c, wname + ".w", t, wn);
       R.wt_off = wt;
       wt += (size_t)wn;
       R.flops = 2.0 * R.rows * wn;
@@ -518,14 +567,16 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
     } else if (T.kind == POOCH_L_MAXPOOL) {
       mparg = std::max(mparg, (size_t)R.rows * T.cout);
     }
-    if (T.kind == POOCH_L_BNRELU || T.kind == POOCH_L_TAIL_PROJ || T.kind == POOCH_L_TAIL_ID) {
-      bnws_c = std::max(bnws_c, T.cout);
+    if (T.kind == POOCH_L_BNRELU || T.kind == POOCH_L_TAIL_PROJ || T.kind == POOCH_L_TAIL_ID ||
+        T.kind == POOCH_L_BNRELU_CONV) {
+      bnws_c = std::max(bnws_c, T.kind == POOCH_L_BNRELU_CONV ? T.cin : T.cout);
       // the BN-consumed inputs must be conv outputs; they get statistics
       std::vector<std::pair<int, std::pair<int, int>>> bn_in = {{T.in0, {R.g1, R.b1}}};
       if (T.kind == POOCH_L_TAIL_PROJ) bn_in.push_back({T.in1, {R.g2, R.b2}});
       for (auto& q : bn_in) {
         int m = q.first;
-        if (m < 0 || g.t[m].kind != POOCH_L_CONV || g.t[m].consumers.size() != 1) {
+        if (m < 0 || (g.t[m].kind != POOCH_L_CONV && g.t[m].kind != POOCH_L_BNRELU_CONV) ||
+            g.t[m].consumers.size() != 1) {
           delete c;
           return fail(POOCH_EUSAGE, "task %d: BN input must be a conv output with a single consumer", t);
         }
@@ -786,7 +837,9 @@ static Problem make_problem(pooch_ctx* c, uint64_t budget) {
     p.needs[t] = c->g.t[t].needs;
   }
   p.is_conv.assign(n, 0);
-  for (int t = 0; t < n; ++t) p.is_conv[t] = (c->g.t[t].kind == POOCH_L_CONV || c->g.t[t].kind == POOCH_L_UPCONV) ? 1 : 0;
+  for (int t = 0; t < n; ++t)
+    p.is_conv[t] = (c->g.t[t].kind == POOCH_L_CONV || c->g.t[t].kind == POOCH_L_UPCONV ||
+                    c->g.t[t].kind == POOCH_L_BNRELU_CONV) ? 1 : 0;
   p.resident = 0;
   p.budget = budget;
   p.tail = c->tail_ns;
@@ -1027,7 +1080,8 @@ static void compile(pooch_ctx* c, const SimOut& so) {
       if (c->sched == SCHED_SN) {
         trig = n - 1;
         for (int q = need[o.id] - 1; q >= n; --q)
-          if (c->program[q].kind == 'B' && c->g.t[c->program[q].id].kind == POOCH_L_CONV) {
+          if (c->program[q].kind == 'B' && (c->g.t[c->program[q].id].kind == POOCH_L_CONV ||
+                                            c->g.t[c->program[q].id].kind == POOCH_L_BNRELU_CONV)) {
             trig = q;
             break;
           }

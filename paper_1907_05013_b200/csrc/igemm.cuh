@@ -80,6 +80,10 @@ struct GemmParams {
   int c_split, n_split, accumulate2;
   float* d2;
   int epi_direct;        // 1: each thread stores its own row (no smem staging); experiments only
+  // transform on load (XF kernels): the activation operand (FWD: A = x, WGRAD: x)
+  // is relu(xf_scale[c] * v + xf_shift[c]) of the stored tensor; zero padding stays zero
+  const float* xf_scale;
+  const float* xf_shift;
 };
 
 constexpr int BM = 128;
@@ -112,6 +116,9 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int j) {
 __device__ __forceinline__ float tf32_resid(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
+// BN-ReLU on load (XF): y = relu(fma(v, scale, shift)) -- the BN-apply kernel's arithmetic
+// (eltwise.cu bn_apply_kernel mode 0), so the fused and the stored paths agree bit for bit
+__device__ __forceinline__ float bnrelu1(float v, float sc, float sh) { return fmaxf(__fmaf_rn(v, sc, sh), 0.f); }
 __device__ __forceinline__ void split_chunk(uint32_t src, uint32_t dst) {
   float a, b, c, d;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(src));
@@ -351,14 +358,24 @@ __device__ __forceinline__ void transpose_block(uint32_t blk, int rot, uint32_t 
 // of 128-B row r sits at chunk j ^ (r & 7)) into the K-major SWIZZLE_128B operand layout (row =
 // channel, k = pixel). Lane l holds pixel l's row in registers, then writes column l of every
 // channel row: each store instruction covers one 128-B row, conflict free. X3: residuals -> +delta.
-template <bool X3>
-__device__ __forceinline__ void transpose32(uint32_t blk, int lane, uint32_t delta) {
+// XF: the block holds 32 channels of the activation; lane l's pixel is replaced by
+// relu(scale * v + shift) (scale / shift of channel c held by lane c), or 0 if !valid (padding).
+template <bool X3, bool XF = false>
+__device__ __forceinline__ void transpose32(uint32_t blk, int lane, uint32_t delta, bool valid = true,
+                                            float scl = 0.f, float shl = 0.f) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
                  : "r"(blk + lane * 128 + ((j ^ (lane & 7)) << 4)));
+  if constexpr (XF) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const float sc = __shfl_sync(0xffffffffu, scl, c), sh = __shfl_sync(0xffffffffu, shl, c);
+      v[c] = valid ? bnrelu1(v[c], sc, sh) : 0.f;
+    }
+  }
   __syncwarp();
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
@@ -392,10 +409,13 @@ __device__ __forceinline__ float warp_transpose_sum32(float* v, int lane) {
 constexpr int NUM_THREADS_P = 288;      // 4 epilogue + 4 producer + 1 MMA warps
 constexpr int NUM_THREADS_X3 = 416;     // + 4 residual ("split") warps for 3xTF32
 // the auxiliary warps 9-12 compute 3xTF32 residuals and / or transpose wgrad operands
-__host__ __device__ constexpr bool igemm_aux(int mode, bool x3) { return x3 || mode == CONV_WGRAD; }
-__host__ __device__ constexpr int igemm_threads(int mode, bool x3) {
-  return igemm_aux(mode, x3) ? NUM_THREADS_X3 : NUM_THREADS_P;
+__host__ __device__ constexpr bool igemm_aux(int mode, bool x3, bool xf = false) {
+  return x3 || xf || mode == CONV_WGRAD;
 }
+__host__ __device__ constexpr int igemm_threads(int mode, bool x3, bool xf = false) {
+  return igemm_aux(mode, x3, xf) ? NUM_THREADS_X3 : NUM_THREADS_P;
+}
+
 
 struct TileMap {
   int mt, nt, zt, kb_total, kbps;  // mt = M-tiles (TMA: tiles_n * tiles_h * tiles_w)
@@ -411,14 +431,15 @@ struct TileMap {
   }
 };
 
-template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false>
-__global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
+template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false>
+__global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c) {
   static_assert(!TMA || MODE != GEMM_TEST, "TMA path: conv fwd / dgrad / wgrad");
   // TMA tiles whose M rows are a box of output pixels (FWD / DGRAD); TMA wgrad boxes pixels along K
   constexpr bool PIXM = TMA && MODE != CONV_WGRAD;
-  constexpr bool AUX = igemm_aux(MODE, X3);
+  static_assert(!XF || (TMA && (MODE == CONV_FWD || MODE == CONV_WGRAD)), "XF: TMA-fed fwd / wgrad only");
+  constexpr bool AUX = igemm_aux(MODE, X3, XF);
   using SM = GemmSmem<BN, STAGES, X3>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -617,16 +638,90 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3), 1)
     // (3xTF32) write x - tf32(x) of every chunk, publish to the async proxy, arrive full[].
     const int stid = tid - 9 * 32;
     int it = 0;
+    // XF forward: this thread's A chunks are rows (stid >> 3) + 16 i, physical 16-B chunk stid & 7
+    // (logical chunk pj ^ (row & 7), the same for all eight rows); per tile the rows' top-left
+    // input coordinates (hb, wb) and whether the row is an output pixel at all
+    int hb[8], wb[8];
+    unsigned rowv = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int m0, n0, kb0, nkb;
       tm.decode(t, m0, n0, kb0, nkb, BN);
+      if constexpr (XF && MODE == CONV_FWD) {
+        const int mt_i = m0 / BM;
+        const int tw_i = mt_i % p.tiles_w, th_i = (mt_i / p.tiles_w) % p.tiles_h, tn_i = mt_i / (p.tiles_w * p.tiles_h);
+        const int per = p.tw * p.th;
+        rowv = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = (stid >> 3) + 16 * i;
+          const int nn = tn_i * p.tn + row / per, ho = th_i * p.th + (row / p.tw) % p.th, wo = tw_i * p.tw + row % p.tw;
+          if (row < per * p.tn && nn < p.n3 && ho < p.hout && wo < p.wout) rowv |= 1u << i;
+          hb[i] = ho * p.stride - p.pad;
+          wb[i] = wo * p.stride - p.pad;
+        }
+      }
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         int s = it % STAGES;
         ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
         if constexpr (MODE == CONV_WGRAD && TMA) {
           // (BM + BN) / 32 TMA boxes, A's then B's, 4 KB each; residuals at the same offsets + SMALL_OFF
-          for (int bi = warp - 9; bi < (BM + BN) / 32; bi += 4) transpose32<X3>(st + bi * 4096, lane, SM::SMALL_OFF);
+          for (int bi = warp - 9; bi < (BM + BN) / 32; bi += 4) {
+            if constexpr (XF) {
+              const bool in_a = bi < BM / 32;
+              if (in_a == (p.wg_a_is_x != 0)) {  // an activation block: BN-ReLU on load
+                const int row = in_a ? m0 + 32 * bi : n0 + 32 * (bi - BM / 32);
+                const int rs = row / p.C, ch = row - rs * p.C;
+                const int r = rs / p.S, sx = rs - r * p.S;
+                const int b = kb0 + kb;
+                const int ow = (b % p.tiles_w) * p.tw, oh = ((b / p.tiles_w) % p.tiles_h) * p.th,
+                          on = (b / (p.tiles_w * p.tiles_h)) * p.tn;
+                const int wo = ow + lane % p.tw, ho = oh + (lane / p.tw) % p.th, nn = on + lane / (p.tw * p.th);
+                const int hi = ho * p.stride - p.pad + r, wi = wo * p.stride - p.pad + sx;
+                const bool valid = nn < p.N && ho < p.Ho && wo < p.Wo && (unsigned)hi < (unsigned)p.H &&
+                                   (unsigned)wi < (unsigned)p.W;
+                const bool live = row < (in_a ? p.M : p.Ng);
+                const float scl = live ? __ldg(p.xf_scale + ch + lane) : 0.f;
+                const float shl = live ? __ldg(p.xf_shift + ch + lane) : 0.f;
+                transpose32<X3, true>(st + bi * 4096, lane, SM::SMALL_OFF, valid, scl, shl);
+                continue;
+              }
+            }
+            transpose32<X3>(st + bi * 4096, lane, SM::SMALL_OFF);
+          }
+        } else if constexpr (XF && MODE == CONV_FWD) {
+          // A: BN-ReLU on load (+ residual); B: residual only
+          const int k = kb0 + kb;
+          const int tap = k / p.cchunks, cc = k - tap * p.cchunks;
+          const int r = tap / p.S, sx = tap - r * p.S;
+          const int pj = stid & 7, jl = pj ^ ((stid >> 3) & 7);
+          const float4 sc = __ldg(reinterpret_cast<const float4*>(p.xf_scale + cc * 32 + 4 * jl));
+          const float4 sh = __ldg(reinterpret_cast<const float4*>(p.xf_shift + cc * 32 + 4 * jl));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int row = (stid >> 3) + 16 * i;
+            const int hi = hb[i] + r, wi = wb[i] + sx;
+            const bool valid = ((rowv >> i) & 1u) && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
+            const uint32_t a = st + row * 128 + (pj << 4);
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+            v.x = valid ? bnrelu1(v.x, sc.x, sh.x) : 0.f;
+            v.y = valid ? bnrelu1(v.y, sc.y, sh.y) : 0.f;
+            v.z = valid ? bnrelu1(v.z, sc.z, sh.z) : 0.f;
+            v.w = valid ? bnrelu1(v.w, sc.w, sh.w) : 0.f;
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                         : "memory");
+            if constexpr (X3)
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a + SM::SMALL_OFF), "f"(tf32_resid(v.x)),
+                           "f"(tf32_resid(v.y)), "f"(tf32_resid(v.z)), "f"(tf32_resid(v.w))
+                           : "memory");
+          }
+          if constexpr (X3) {
+            constexpr int BCH = BN * BK / 4;  // 16-B chunks of B
+#pragma unroll 4
+            for (int c = stid; c < BCH; c += 128)
+              split_chunk(st + SM::A_BYTES + c * 16, st + SM::A_BYTES + SM::SMALL_OFF + c * 16);
+          }
         } else if constexpr (MODE == CONV_WGRAD) {
           // 256 blocks in A (rows = Cout) and 256 in B (rows = R*S*C); block (g, j) = rows 4g..4g+3, k-chunk j
 #pragma unroll

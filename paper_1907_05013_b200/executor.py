@@ -15,17 +15,22 @@ from ._lib import P, IODesc, LayerDesc, PlanReport, ProfileT, SearchCfg, check, 
 from .planning import STRATEGIES
 
 NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2, "unet3d": 3}
-KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce", "upconv", "head_ce"]
+KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce", "upconv", "head_ce", "bnrelu_conv"]
 FAMILIES = ["conv_fwd", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd", "pool", "fc_ce", "sgd",
             "swap_out", "swap_in", "allreduce", "other", "stall"]
 
 
-def build_net(name: str, in_hw: int, classes: int, width: int = 32):
-    """Layer descriptors of a built-in workload (pooch_build_net)."""
+FUSE_BNRELU = 16   # POOCH_NET_FUSE_BNRELU: BN-ReLU on the consuming conv's operand load
+
+
+def build_net(name: str, in_hw: int, classes: int, width: int = 32, fuse: bool = False):
+    """Layer descriptors of a built-in workload (pooch_build_net); fuse=True merges every
+    conv-feeding BN-ReLU into its conv (POOCH_L_BNRELU_CONV)."""
+    which = NETS[name] | (FUSE_BNRELU if fuse else 0)
     n = C.c_int32(0)
-    check(lib.pooch_build_net(NETS[name], in_hw, classes, width, None, C.byref(n)))
+    check(lib.pooch_build_net(which, in_hw, classes, width, None, C.byref(n)))
     arr = (LayerDesc * n.value)()
-    check(lib.pooch_build_net(NETS[name], in_hw, classes, width, arr, C.byref(n)))
+    check(lib.pooch_build_net(which, in_hw, classes, width, arr, C.byref(n)))
     return arr
 
 
@@ -83,15 +88,15 @@ class Context:
         self._keep = []
 
     @classmethod
-    def builtin(cls, name, batch, in_hw=None, classes=None, width=32, device=0):
+    def builtin(cls, name, batch, in_hw=None, classes=None, width=32, device=0, fuse=False):
         if name == "unet3d":   # config 4: in_hw^3 volume, input channels padded 1 -> 32
             in_hw = in_hw or 256
             classes = classes or 2
-            return cls(build_net(name, in_hw, classes, width), batch, 32, in_hw, in_hw, classes, device,
+            return cls(build_net(name, in_hw, classes, width, fuse), batch, 32, in_hw, in_hw, classes, device,
                        in_d=in_hw)
         in_hw = in_hw or (32 if name == "tiny" else 224)
         classes = classes or (10 if name == "tiny" else 1000)
-        return cls(build_net(name, in_hw, classes, width), batch, 4, in_hw, in_hw, classes, device)
+        return cls(build_net(name, in_hw, classes, width, fuse), batch, 4, in_hw, in_hw, classes, device)
 
     def close(self):
         if self.h:

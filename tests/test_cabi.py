@@ -105,3 +105,26 @@ def test_allreduce_buckets_partition_the_gradient_region():
         assert hi2 == lo1 and t2 < t1                         # contiguous, descending
     assert all(hi - lo >= 6_500_000 for lo, hi, _ in b[:-1])
     ctx.close()
+
+
+def test_fused_build_net_matches_oracle_and_keeps_parameters():
+    """the C++ builder's BN-ReLU fusion (POOCH_NET_FUSE_BNRELU) produces the
+    oracle's fused graph (nets.fuse_bnrelu) task for task, and the fused context has exactly the
+    plain context's parameters in the same order (host-only, no device work)."""
+    from oracle import nets
+    from paper_1907_05013_b200.executor import KINDS, Context, build_net
+    for which, ref, hw, cls in (("resnet50", nets.resnet50(), 224, 1000), ("tiny", nets.tiny_cnn(), 32, 10)):
+        f = nets.fuse_bnrelu(ref)
+        layers = build_net(which, hw, cls, fuse=True)
+        assert len(layers) == len(f.tasks)
+        for l, t in zip(layers, f.tasks):
+            assert KINDS[l.kind] == t.kind
+            assert l.name.decode() == (t.bn + "+" + t.name if t.kind == "bnrelu_conv" else t.name)
+            assert [i for i in (l.in0, l.in1) if i >= 0] == [i for i in t.inputs if i >= 0]
+            assert (l.cout, l.hout, l.wout) == t.out_chw
+        a = Context(build_net(which, hw, cls), 2, 4, hw, hw, cls)
+        b = Context(layers, 2, 4, hw, hw, cls)
+        assert a.params() == b.params()
+        assert sum(n for _, n in a.params()) == sum(n for _, n in b.params())
+        a.close()
+        b.close()

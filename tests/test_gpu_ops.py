@@ -194,3 +194,50 @@ def test_maxpool2d(N, H, C, k, s, p):
     assert rel(gx, gx_ref) < 1e-6
     # support of the routed gradient is identical (index work: exact)
     np.testing.assert_array_equal(gx != 0, gx_ref != 0)
+
+
+BNRELU_CASES = [c for c in CONV_CASES if c[3] % 32 == 0 and c[6] <= 2] + [
+    (4, 14, 14, 64, 64, 3, 1, 1),     # stage-1-like 3x3, several M tiles
+    (3, 11, 11, 128, 64, 3, 2, 1),    # strided, ragged
+]
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("case", BNRELU_CASES)
+def test_conv_bnrelu_on_load(case, prec):
+    """conv fwd and wgrad with the operand relu(scale * x + shift) rebuilt on load
+    (pooch_op_conv_fwd_bnrelu / _wgrad_bnrelu) against the fp64 oracle conv of the stored
+    relu(bn(.)) -- padding must stay zero (shift != 0 makes a wrong pad visible)."""
+    lib = _lib()
+    N, H, W, Cin, K, R, s, p = case
+    x, w = _conv_inputs(N, H, W, Cin, K, R, sum(case) + 3)
+    g = synthdata.rng(sum(case) + 4)
+    scale = g.uniform(0.5, 1.5, Cin).astype(np.float32)
+    shift = g.uniform(-0.5, 0.5, Cin).astype(np.float32)
+    r = np.maximum(x.astype(np.float64) * scale + shift, 0.0)          # NHWC, fp64
+    ho, wo = L.conv_out_hw(H, W, R, R, s, p)
+    gy = g.standard_normal((N, ho, wo, K)).astype(np.float32)
+    d = lib.ConvDesc(N, H, W, Cin, K, R, R, s, p, prec)
+    mt = lib.lib.pooch_op_conv_stat_tiles(C.byref(d))
+    dx, dw = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    dsc, dsh = torch.from_numpy(scale).cuda(), torch.from_numpy(shift).cuda()
+    dy = torch.full((N, ho, wo, K), float("nan"), device="cuda")
+    s1 = torch.zeros((mt, K), device="cuda")
+    s2 = torch.zeros((mt, K), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_fwd_bnrelu(C.byref(d), ptr(dx), ptr(dsc), ptr(dsh), ptr(dw), ptr(dy), ptr(s1),
+                                               ptr(s2), None))
+    wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(wsb // 4, 1), device="cuda")
+    dgy = torch.from_numpy(gy).cuda()
+    ddw = torch.full((K, R, R, Cin), float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_wgrad_bnrelu(C.byref(d), ptr(dx), ptr(dsc), ptr(dsh), ptr(dgy), ptr(ddw), ptr(ws),
+                                                 wsb, None))
+    torch.cuda.synchronize()
+    rn = r.transpose(0, 3, 1, 2)
+    ref = L.conv2d_fwd(rn, w.transpose(0, 3, 1, 2).astype(np.float64), s, p).transpose(0, 2, 3, 1)
+    tol = TOL_X3 if prec else TOL_OP
+    assert rel(dy.cpu().numpy(), ref) < tol
+    flat = ref.reshape(-1, K)
+    assert rel(s1.cpu().numpy().astype(np.float64).sum(0), flat.sum(0)) < TOL_OP
+    refw = L.conv2d_wgrad(rn, gy.transpose(0, 3, 1, 2).astype(np.float64), (K, Cin, R, R), s, p).transpose(0, 2, 3, 1)
+    assert rel(ddw.cpu().numpy(), refw) < tol

@@ -96,7 +96,7 @@ def _net_profile(net, batch, link_gbs, budget, scale_ns=1.0):
     for i, t in enumerate(net.tasks):
         b = batch * net.map_bytes_per_image(i)
         nbytes.append(b)
-        if t.kind == "conv":
+        if t.kind in ("conv", "bnrelu_conv"):
             c, h, w = t.out_chw
             fl = 2 * batch * c * h * w * t.cin * t.k * t.k
             fwd.append(max(1, int(fl / 300e3 * scale_ns)))      # ~300 TFLOP/s
@@ -186,3 +186,27 @@ def test_host_budget_limits_swap_class(seed):
     assert cls == ref["cls"]
     assert sum(d["bytes"][m] for m in range(8) if cls[m] == OS.SWAP) <= hb
     assert pc.simulate([OS.SWAP] * 8)["oom"]          # all-swap needs more host memory than hb
+
+
+@pytest.mark.parametrize("link", [16.0, 75.0])
+def test_fused_graphs_profile_parity(link):
+    """the C++ planner matches the oracle on the BN-ReLU-fused graphs too (tiny CNN:
+    7 maps, full tree; ResNet-50: 73 maps, li_cap 3), and the tiny graph's PoocH plan is no better
+    than brute force over all 2 * 3^6 plans."""
+    tiny = nets.fuse_bnrelu(nets.tiny_cnn())
+    d = _net_profile(tiny, 8, link, 0)
+    total = sum(d["bytes"])
+    po, pc = both(d, resident=1_500_000, budget=1_500_000 + total // 2)
+    ref = OP.pooch(po, li_cap=16)
+    cls, _ = pc.plan("pooch")
+    assert cls == (ref["cls"] if ref["feasible"] else None)
+    bf = OP.brute_force(po)
+    if bf["cls"] is not None and ref["feasible"]:
+        assert ref["makespan"] >= bf["makespan"]
+    r50 = nets.fuse_bnrelu(nets.resnet50())
+    d = _net_profile(r50, 64, link, 0)
+    total = sum(d["bytes"])
+    po, pc = both(d, resident=200_000_000, budget=200_000_000 + int(total * 0.35))
+    ref = OP.pooch(po, li_cap=3)
+    cls, rep = pc.plan("pooch", li_cap=3)
+    assert cls == (ref["cls"] if ref["feasible"] else None)
