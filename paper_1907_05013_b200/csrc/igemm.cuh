@@ -662,53 +662,81 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
       }
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         int s = it % STAGES;
+        // XF: everything the transform needs that does not depend on the stage's data (scale /
+        // shift loads from L2, padding masks) is done before waiting for the stage, so the
+        // load latency overlaps the TMA instead of sitting between the TMA and the MMA
+        float4 xsc = make_float4(0.f, 0.f, 0.f, 0.f), xsh = xsc;
+        unsigned xvalid = 0;
+        constexpr int WQ = ((BM + BN) / 32 + 3) / 4;  // wgrad: 32x32 blocks per auxiliary warp
+        float wscl[WQ], wshl[WQ];
+        bool wval[WQ], wx[WQ];
+#pragma unroll
+        for (int q = 0; q < WQ; ++q) {
+          wscl[q] = wshl[q] = 0.f;
+          wval[q] = wx[q] = false;
+        }
+        if constexpr (XF && MODE == CONV_FWD) {
+          const int k = kb0 + kb;
+          const int tap = k / p.cchunks, cc = k - tap * p.cchunks;
+          const int r = tap / p.S, sx = tap - r * p.S;
+          const int jl = (stid & 7) ^ ((stid >> 3) & 7);
+          xsc = __ldg(reinterpret_cast<const float4*>(p.xf_scale + cc * 32 + 4 * jl));
+          xsh = __ldg(reinterpret_cast<const float4*>(p.xf_shift + cc * 32 + 4 * jl));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int hi = hb[i] + r, wi = wb[i] + sx;
+            if (((rowv >> i) & 1u) && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W) xvalid |= 1u << i;
+          }
+        }
+        if constexpr (XF && MODE == CONV_WGRAD) {
+          const int b = kb0 + kb;
+          const int ow = (b % p.tiles_w) * p.tw, oh = ((b / p.tiles_w) % p.tiles_h) * p.th,
+                    on = (b / (p.tiles_w * p.tiles_h)) * p.tn;
+          const int wo = ow + lane % p.tw, ho = oh + (lane / p.tw) % p.th, nn = on + lane / (p.tw * p.th);
+          const bool pix = nn < p.N && ho < p.Ho && wo < p.Wo;
+#pragma unroll
+          for (int q = 0; q < WQ; ++q) {
+            const int bi = warp - 9 + 4 * q;
+            const bool in_a = bi < BM / 32;
+            if (bi >= (BM + BN) / 32 || in_a != (p.wg_a_is_x != 0)) continue;
+            const int row = in_a ? m0 + 32 * bi : n0 + 32 * (bi - BM / 32);
+            if (row >= (in_a ? p.M : p.Ng)) continue;  // box not loaded: rows never stored
+            wx[q] = true;
+            const int rs = row / p.C, ch = row - rs * p.C;
+            const int r = rs / p.S, sx = rs - r * p.S;
+            const int hi = ho * p.stride - p.pad + r, wi = wo * p.stride - p.pad + sx;
+            wval[q] = pix && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
+            wscl[q] = __ldg(p.xf_scale + ch + lane);
+            wshl[q] = __ldg(p.xf_shift + ch + lane);
+          }
+        }
         ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
         if constexpr (MODE == CONV_WGRAD && TMA) {
           // (BM + BN) / 32 TMA boxes, A's then B's, 4 KB each; residuals at the same offsets + SMALL_OFF
-          for (int bi = warp - 9; bi < (BM + BN) / 32; bi += 4) {
-            if constexpr (XF) {
-              const bool in_a = bi < BM / 32;
-              if (in_a == (p.wg_a_is_x != 0)) {  // an activation block: BN-ReLU on load
-                const int row = in_a ? m0 + 32 * bi : n0 + 32 * (bi - BM / 32);
-                const int rs = row / p.C, ch = row - rs * p.C;
-                const int r = rs / p.S, sx = rs - r * p.S;
-                const int b = kb0 + kb;
-                const int ow = (b % p.tiles_w) * p.tw, oh = ((b / p.tiles_w) % p.tiles_h) * p.th,
-                          on = (b / (p.tiles_w * p.tiles_h)) * p.tn;
-                const int wo = ow + lane % p.tw, ho = oh + (lane / p.tw) % p.th, nn = on + lane / (p.tw * p.th);
-                const int hi = ho * p.stride - p.pad + r, wi = wo * p.stride - p.pad + sx;
-                const bool valid = nn < p.N && ho < p.Ho && wo < p.Wo && (unsigned)hi < (unsigned)p.H &&
-                                   (unsigned)wi < (unsigned)p.W;
-                const bool live = row < (in_a ? p.M : p.Ng);
-                const float scl = live ? __ldg(p.xf_scale + ch + lane) : 0.f;
-                const float shl = live ? __ldg(p.xf_shift + ch + lane) : 0.f;
-                transpose32<X3, true>(st + bi * 4096, lane, SM::SMALL_OFF, valid, scl, shl);
-                continue;
-              }
-            }
-            transpose32<X3>(st + bi * 4096, lane, SM::SMALL_OFF);
+#pragma unroll
+          for (int q = 0; q < WQ; ++q) {
+            const int bi = warp - 9 + 4 * q;
+            if (bi >= (BM + BN) / 32) break;
+            if (XF && wx[q])  // an activation block: BN-ReLU on load
+              transpose32<X3, XF>(st + bi * 4096, lane, SM::SMALL_OFF, wval[q], wscl[q], wshl[q]);
+            else
+              transpose32<X3>(st + bi * 4096, lane, SM::SMALL_OFF);
           }
         } else if constexpr (XF && MODE == CONV_FWD) {
           // A: BN-ReLU on load (+ residual); B: residual only
-          const int k = kb0 + kb;
-          const int tap = k / p.cchunks, cc = k - tap * p.cchunks;
-          const int r = tap / p.S, sx = tap - r * p.S;
-          const int pj = stid & 7, jl = pj ^ ((stid >> 3) & 7);
-          const float4 sc = __ldg(reinterpret_cast<const float4*>(p.xf_scale + cc * 32 + 4 * jl));
-          const float4 sh = __ldg(reinterpret_cast<const float4*>(p.xf_shift + cc * 32 + 4 * jl));
+          const int pj = stid & 7;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int row = (stid >> 3) + 16 * i;
-            const int hi = hb[i] + r, wi = wb[i] + sx;
-            const bool valid = ((rowv >> i) & 1u) && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
+            const bool valid = (xvalid >> i) & 1u;
             const uint32_t a = st + row * 128 + (pj << 4);
             float4 v;
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-            v.x = valid ? bnrelu1(v.x, sc.x, sh.x) : 0.f;
-            v.y = valid ? bnrelu1(v.y, sc.y, sh.y) : 0.f;
-            v.z = valid ? bnrelu1(v.z, sc.z, sh.z) : 0.f;
-            v.w = valid ? bnrelu1(v.w, sc.w, sh.w) : 0.f;
+            v.x = valid ? bnrelu1(v.x, xsc.x, xsh.x) : 0.f;
+            v.y = valid ? bnrelu1(v.y, xsc.y, xsh.y) : 0.f;
+            v.z = valid ? bnrelu1(v.z, xsc.z, xsh.z) : 0.f;
+            v.w = valid ? bnrelu1(v.w, xsc.w, xsh.w) : 0.f;
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                          : "memory");
             if constexpr (X3)
