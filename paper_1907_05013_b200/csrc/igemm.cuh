@@ -419,11 +419,20 @@ __host__ __device__ constexpr int igemm_threads(int mode, bool x3, bool xf = fal
 
 struct TileMap {
   int mt, nt, zt, kb_total, kbps;  // mt = M-tiles (TMA: tiles_n * tiles_h * tiles_w)
+  bool nfast;                      // N-tiles fastest: co-running CTAs share the A (activation) tile
   __device__ void decode(int t, int& m0, int& n0, int& kb0, int& nkb, int bn) const {
-    int m = t % mt;
-    int r = t / mt;
-    int n = r % nt;
-    int z = r / nt;
+    int m, n, z;
+    if (nfast) {
+      n = t % nt;
+      const int r = t / nt;
+      m = r % mt;
+      z = r / mt;
+    } else {
+      m = t % mt;
+      const int r = t / mt;
+      n = r % nt;
+      z = r / nt;
+    }
     m0 = m * BM;
     n0 = n * bn;
     kb0 = z * kbps;
@@ -461,6 +470,10 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
   tm.kb_total = (TMA && MODE == CONV_WGRAD) ? p.tiles_n * p.tiles_h * p.tiles_w : (p.Kg + BK - 1) / BK;
   tm.kbps = p.kb_per_split > 0 ? p.kb_per_split : max(tm.kb_total, 1);
   tm.zt = p.kb_per_split > 0 ? (tm.kb_total + tm.kbps - 1) / tm.kbps : 1;
+  // FWD / DGRAD: B is the (transposed) weight matrix -- at most a few MB, always L2-resident --
+  // while A is the activation stream; with N-tiles fastest the CTAs working on one M-tile run
+  // together and read its A rows from DRAM once instead of once per N-tile
+  tm.nfast = (MODE == CONV_FWD || MODE == CONV_DGRAD) && tm.nt > 1;
   const int ntiles = tm.mt * tm.nt * tm.zt;
 
   if (tid == 0) {
