@@ -47,7 +47,8 @@ static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
 template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
-                                 const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr) {
+                                 const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr,
+                                 const CUtensorMap* td = nullptr) {
   // deepest ring that fits 227 KB next to the epilogue staging / reduction buffers: a k-block's
   // MMAs take only 0.2-0.4 us, less than the TMA -> (3xTF32 split / wgrad transpose) -> MMA
   // latency, so the ring depth sets the throughput of the short-K and narrow (BN = 64) layers
@@ -67,7 +68,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
   kern<<<ctas, igemm_threads(MODE, X3, XF), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
-                                                      tc ? *tc : g_zero_map);
+                                                          tc ? *tc : g_zero_map, td ? *td : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
@@ -75,19 +76,19 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
 template <int MODE, bool TMA = false>
 static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream_t st, int prec = 0,
                               const CUtensorMap* ta = nullptr, const CUtensorMap* tb = nullptr,
-                              const CUtensorMap* tc = nullptr) {
+                              const CUtensorMap* tc = nullptr, const CUtensorMap* td = nullptr) {
   if constexpr (TMA && (MODE == CONV_FWD || MODE == CONV_WGRAD)) {
     if (p.xf_scale) {  // BN-ReLU on load
       if (prec) {
         switch (bn) {
-          case 64: return launch_igemm<MODE, 64, true, true, true>(p, grid, st, ta, tb, tc);
-          case 128: return launch_igemm<MODE, 128, true, true, true>(p, grid, st, ta, tb, tc);
+          case 64: return launch_igemm<MODE, 64, true, true, true>(p, grid, st, ta, tb, tc, td);
+          case 128: return launch_igemm<MODE, 128, true, true, true>(p, grid, st, ta, tb, tc, td);
         }
       } else {
         switch (bn) {
-          case 64: return launch_igemm<MODE, 64, false, true, true>(p, grid, st, ta, tb, tc);
-          case 128: return launch_igemm<MODE, 128, false, true, true>(p, grid, st, ta, tb, tc);
-          case 256: return launch_igemm<MODE, 256, false, true, true>(p, grid, st, ta, tb, tc);
+          case 64: return launch_igemm<MODE, 64, false, true, true>(p, grid, st, ta, tb, tc, td);
+          case 128: return launch_igemm<MODE, 128, false, true, true>(p, grid, st, ta, tb, tc, td);
+          case 256: return launch_igemm<MODE, 256, false, true, true>(p, grid, st, ta, tb, tc, td);
         }
       }
       return fail(POOCH_EUSAGE, "bad tile width %d", bn);
@@ -97,15 +98,15 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
   }
   if (prec) {
     switch (bn) {
-      case 64: return launch_igemm<MODE, 64, true, TMA>(p, grid, st, ta, tb, tc);
-      case 128: return launch_igemm<MODE, 128, true, TMA>(p, grid, st, ta, tb, tc);
+      case 64: return launch_igemm<MODE, 64, true, TMA>(p, grid, st, ta, tb, tc, td);
+      case 128: return launch_igemm<MODE, 128, true, TMA>(p, grid, st, ta, tb, tc, td);
     }
     return fail(POOCH_EUSAGE, "3xTF32 supports tile widths 64 / 128 (got %d)", bn);
   }
   switch (bn) {
-    case 64: return launch_igemm<MODE, 64, false, TMA>(p, grid, st, ta, tb, tc);
-    case 128: return launch_igemm<MODE, 128, false, TMA>(p, grid, st, ta, tb, tc);
-    case 256: return launch_igemm<MODE, 256, false, TMA>(p, grid, st, ta, tb, tc);
+    case 64: return launch_igemm<MODE, 64, false, TMA>(p, grid, st, ta, tb, tc, td);
+    case 128: return launch_igemm<MODE, 128, false, TMA>(p, grid, st, ta, tb, tc, td);
+    case 256: return launch_igemm<MODE, 256, false, TMA>(p, grid, st, ta, tb, tc, td);
   }
   return fail(POOCH_EUSAGE, "bad tile width %d", bn);
 }
@@ -169,6 +170,27 @@ static bool map_2d(CUtensorMap* m, const float* base, int rows, int cols, int bn
   cuuint32_t box[2] = {32, (cuuint32_t)bn};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// Epilogue stores through the TMA (POOCH_NO_TMA_STORE=1: per-thread stores, for A/B tests)
+static bool tma_store_enabled() {
+  static int on = getenv("POOCH_NO_TMA_STORE") ? 0 : 1;
+  return on != 0 && encode_fn() != nullptr;
+}
+
+// 4-D strided view {C, w, h, n} of an NHWC / NDHWC tensor for TMA stores: element (c, x, y, z)
+// at base + c + x * sw + y * sh + z * sn (floats); box {32, bw, bh, bn}, SWIZZLE_128B.
+static bool map_view4(CUtensorMap* m, float* base, int C, int w, int h, int n, int64_t sw, int64_t sh, int64_t sn,
+                      int bw, int bh, int bnn) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)sw * 4, (cuuint64_t)sh * 4, (cuuint64_t)sn * 4};
+  cuuint32_t box[4] = {32, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bnn};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
@@ -273,11 +295,18 @@ pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, 
         return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv fwd, second source)");
     }
     dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
-    return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb, g.C1 > 0 ? &tc : nullptr);
+    CUtensorMap td;
+    if (tma_store_enabled() &&
+        map_view4(&td, y, g.K, g.Wo, g.Ho, out3(g), g.K, (int64_t)g.Wo * g.K, (int64_t)g.Ho * g.Wo * g.K, b.tw, b.th, b.tn))
+      p.tma_store = 1;
+    return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb, g.C1 > 0 ? &tc : nullptr,
+                                     p.tma_store ? &td : nullptr);
   }
   if (g.is3d() || g.C1 > 0) return fail(POOCH_EUSAGE, "3D / two-source conv needs the TMA path");
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);
-  return launch_bn<CONV_FWD>(bn, p, grid, st, g.prec);
+  CUtensorMap td;
+  if (tma_store_enabled() && map_2d(&td, y, p.M, g.K, BM)) p.tma_store = 2;
+  return launch_bn<CONV_FWD>(bn, p, grid, st, g.prec, nullptr, nullptr, nullptr, p.tma_store ? &td : nullptr);
 }
 
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
@@ -330,7 +359,19 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
           if (!map_act(&ta, dy, out3(g), g.Ho, g.Wo, g.K, b.tw, b.th, b.tn, 1, 1))
             return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv dgrad)");
           dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
-          POOCH_CHECK((launch_bn<CONV_DGRAD, true>(bn, q, grid, st, g.prec, &ta, &tb)));
+          // this class's dx pixels as a strided 4-D view for the TMA store (plain, or fp32
+          // add-reduce when accumulating); the two-source split keeps the per-thread stores
+          CUtensorMap td;
+          q.tma_store = 0;
+          if (tma_store_enabled() && g.C1 == 0) {
+            const int64_t hw = (int64_t)g.H * g.W * g.C;
+            float* base = dx + ((int64_t)(g.is3d() ? cz : 0) * g.H + a) * g.W * g.C + (int64_t)bb * g.C;
+            if (map_view4(&td, base, g.C, wc, hc, dc, (int64_t)s_ * g.C, (int64_t)s_ * g.W * g.C,
+                          g.is3d() ? (int64_t)s3 * hw : hw, b.tw, b.th, b.tn))
+              q.tma_store = 1;
+          }
+          POOCH_CHECK((launch_bn<CONV_DGRAD, true>(bn, q, grid, st, g.prec, &ta, &tb, nullptr,
+                                                   q.tma_store ? &td : nullptr)));
         }
     return POOCH_OK;
   }

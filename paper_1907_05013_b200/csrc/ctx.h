@@ -93,6 +93,7 @@ struct pooch_ctx {
   std::vector<size_t> host_off;  // per map, swap class only
   uint64_t arena_high = 0;
   uint64_t plan_budget = 0;      // simulator budget of the chosen candidate (<= arena capacity)
+  bool refined = false, plan_refined = false;  // the plan came out of the local refinement (Reading 42)
   std::vector<pooch::Op> ops;
   std::vector<pooch::ProgTask> program;
   std::vector<int> first_writer;  // per map: task whose bwd writes (not accumulates) its gradient

@@ -938,7 +938,7 @@ static uint64_t place_greedy(const std::vector<int>& order, const std::vector<st
 // positions; fixed seed, so packing is deterministic) until the high-water mark fits or the
 // iteration budget runs out. false if nothing fits (the caller re-plans against less budget).
 bool pack_ledger(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap, bool no_reuse,
-                 std::vector<uint64_t>& off, uint64_t& high) {
+                 std::vector<uint64_t>& off, uint64_t& high, int sa_iters = -1) {
   if (no_reuse) return pack_ledger_bestfit(ledger, nbuf, cap, true, off, high);
   if (pack_ledger_bestfit(ledger, nbuf, cap, false, off, high)) return true;
   std::vector<int64_t> a(nbuf, -1), f(nbuf, INT64_MAX);
@@ -994,7 +994,7 @@ bool pack_ledger(const std::vector<LedgerEntry>& ledger, int nbuf, uint64_t cap,
       rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
       return rng;
     };
-    const int iters = getenv("POOCH_PACK_ITERS") ? atoi(getenv("POOCH_PACK_ITERS")) : 30000;
+    const int iters = sa_iters >= 0 ? sa_iters : (getenv("POOCH_PACK_ITERS") ? atoi(getenv("POOCH_PACK_ITERS")) : 30000);
     int last_gain = 0;
     for (int it = 0; it < iters && best > cap && it - last_gain < 8000; ++it) {
       const size_t i = next() % cur.size(), j = next() % cur.size();
@@ -1268,10 +1268,99 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
                                                                           : cands[x].li_cap < cands[y].li_cap);
     });
     std::vector<std::vector<uint8_t>> tried;
+    int adopted = -1;
     for (int i : order) {
       if (std::find(tried.begin(), tried.end(), cands[i].cls) != tried.end()) continue;
       tried.push_back(cands[i].cls);
-      if (adopt(cands[i])) break;
+      if (adopt(cands[i])) {
+        adopted = i;
+        break;
+      }
+    }
+    // Local refinement (Reading 42): single-map class changes under the same cost model, from the
+    // adopted plan and the fastest grid candidates (packable or not): first make the ledger pack
+    // (greedy high-water over the arena, lexicographically first), then lower the makespan.
+    if (strategy == POOCH_STRAT_POOCH && !getenv("POOCH_PLAN_NO_REFINE") && !order.empty()) {
+      const Problem pc = make_problem(c, cap);
+      const int sched = cands[order[0]].sched;
+      struct Eval { bool ok = false; int64_t mk = 0; uint64_t over = 0; };
+      auto eval = [&](const std::vector<uint8_t>& cl) {
+        Eval e;
+        uint64_t host_need = 0;
+        for (int m = 0; m < n; ++m)
+          if (cl[m] == C_SWAP) host_need += align_up(c->map_bytes[m]);
+        if (host_need > c->host_bytes) return e;
+        SimOptions o;
+        o.sched = sched;
+        o.record_ledger = true;
+        o.want_sets = false;
+        SimOut so;
+        simulate(pc, cl.data(), o, so);
+        if (so.oom) return e;
+        std::vector<uint64_t> off;
+        uint64_t high;
+        const bool fits = pack_ledger(so.ledger, 3 * n, cap, false, off, high, 0);
+        e.ok = true;
+        e.mk = so.makespan;
+        e.over = fits ? 0 : (high > cap ? high - cap : 1);
+        return e;
+      };
+      auto better = [](const Eval& a, const Eval& b) {  // a better than b
+        if (!a.ok) return false;
+        if (!b.ok) return true;
+        if (a.over != b.over) return a.over < b.over;
+        return a.mk < b.mk;
+      };
+      std::vector<std::vector<uint8_t>> starts;
+      if (adopted >= 0) starts.push_back(cands[adopted].cls);
+      for (int i : order) {
+        if ((int)starts.size() >= 7) break;
+        if (std::find(starts.begin(), starts.end(), cands[i].cls) == starts.end()) starts.push_back(cands[i].cls);
+      }
+      std::vector<std::vector<uint8_t>> res(starts.size());
+      std::vector<Eval> res_e(starts.size());
+      std::vector<std::thread> th;
+      for (size_t k = 0; k < starts.size(); ++k)
+        th.emplace_back([&, k] {
+          std::vector<uint8_t> cur = starts[k];
+          Eval ce = eval(cur);
+          for (int pass = 0; pass < 6 && ce.ok; ++pass) {
+            bool improved = false;
+            for (int m = 0; m < n; ++m)
+              for (uint8_t alt = C_KEEP; alt <= C_RECOMPUTE; ++alt) {
+                if (alt == cur[m] || (m == n - 1 && alt == C_RECOMPUTE)) continue;
+                const uint8_t was = cur[m];
+                cur[m] = alt;
+                const Eval e = eval(cur);
+                if (better(e, ce)) {
+                  ce = e;
+                  improved = true;
+                } else {
+                  cur[m] = was;
+                }
+              }
+            if (!improved) break;
+          }
+          res[k] = cur;
+          res_e[k] = ce;
+        });
+      for (auto& t : th) t.join();
+      int bk = -1;
+      for (size_t k = 0; k < res.size(); ++k)
+        if (res_e[k].ok && res_e[k].over == 0 && (bk < 0 || res_e[k].mk < res_e[bk].mk)) bk = (int)k;
+      const int64_t cur_best = adopted >= 0 ? cands[adopted].mk : INT64_MAX;
+      if (bk >= 0 && res_e[bk].mk < cur_best) {
+        Cand k;
+        k.budget = cap;
+        k.li_cap = sc.li_cap;
+        k.cls = res[bk];
+        k.mk = res_e[bk].mk;
+        k.sched = sched;
+        Planner pl(pc, sc);
+        pl.report(k.cls, k.mk, &k.rep);
+        adopt(k);
+        c->refined = true;
+      }
     }
   } else {
     for (int st = 0; st < steps && (uint64_t)st * step_bytes < cap; ++st) {
@@ -1293,6 +1382,8 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
     }
   }
   if (best.cls.empty()) return ctx_fail(c, fail(POOCH_EINFEASIBLE, "%s", why.c_str()));
+  c->plan_refined = c->refined;
+  c->refined = false;
   const std::vector<uint8_t>& cls = best.cls;
   c->cls = cls;
   c->buf_off.assign(best.off.size(), 0);

@@ -80,6 +80,9 @@ struct GemmParams {
   int c_split, n_split, accumulate2;
   float* d2;
   int epi_direct;        // 1: each thread stores its own row (no smem staging); experiments only
+  // epilogue stores through the TMA (tma_d): 1 = 4-D box of output pixels {32 ch, tw, th, tn}
+  // (PIXM, one dgrad class of stride 1), 2 = 2-D {32 cols, 128 rows} of a row-major [M][Ng]
+  int tma_store;
   // transform on load (XF kernels): the activation operand (FWD: A = x, WGRAD: x)
   // is relu(xf_scale[c] * v + xf_shift[c]) of the stored tensor; zero padding stays zero
   const float* xf_scale;
@@ -99,8 +102,9 @@ struct GemmSmem {
   static constexpr int SMALL_OFF = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int RED_OFF = BAR_OFF + (3 * STAGES + 4) * 8 + 16;
-  // epilogue staging: per epilogue warp one 32 x 32 fp32 block (4 KB), 128-B aligned
-  static constexpr int STG_OFF = (RED_OFF + 4 * BN * 4 * 2 + 127) / 128 * 128;
+  // epilogue staging: per epilogue warp one 32 x 32 fp32 block (4 KB); together the 128 x 32
+  // SWIZZLE_128B image of one column chunk of the tile (1024-B aligned for the TMA store)
+  static constexpr int STG_OFF = (RED_OFF + 4 * BN * 4 * 2 + 1023) / 1024 * 1024;
   static constexpr int TOTAL = STG_OFF + 4 * 4096 + 1024;
 };
 
@@ -443,7 +447,7 @@ struct TileMap {
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                 const __grid_constant__ CUtensorMap tma_c) {
+                 const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
   static_assert(!TMA || MODE != GEMM_TEST, "TMA path: conv fwd / dgrad / wgrad");
   // TMA tiles whose M rows are a box of output pixels (FWD / DGRAD); TMA wgrad boxes pixels along K
   constexpr bool PIXM = TMA && MODE != CONV_WGRAD;
@@ -890,7 +894,10 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
           }
         };
         const int accum = MODE == CONV_DGRAD ? ((p.n_split > 0 && nb >= p.n_split) ? p.accumulate2 : p.accumulate) : 0;
-        if (p.epi_direct) {
+        if (p.epi_direct == 2) {
+          // timing experiment only (POOCH_EPI_DIRECT=2): drain TMEM, store nothing
+          if (rok && v[0] == 12345.f) p.d[0] = v[1];
+        } else if (p.epi_direct) {
           if (rok) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
@@ -910,13 +917,35 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
           // of row r at chunk j ^ (r & 7): conflict free both ways), then each instruction writes
           // four whole 128-B row segments (lanes 8i..8i+7 = one row) instead of 32 scattered 16-B
           // pieces. DGRAD accumulation loads all eight old segments before adding (same fp32 add).
+          // With p.tma_store the four warps' blocks form the tile's 128 x 32 SWIZZLE_128B image and
+          // one thread hands it to the TMA (a plain store, or an fp32 add-reduce for accumulation).
           const uint32_t stg = sbase + SM::STG_OFF + warp * 4096;
+          if (p.tma_store) {  // the previous chunk's TMA store must have read the staging buffer
+            if (tid == 0) ptx::bulk_wait_read0();
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+          }
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((jj ^ (lane & 7)) << 4)),
                          "f"(v[4 * jj]), "f"(v[4 * jj + 1]), "f"(v[4 * jj + 2]), "f"(v[4 * jj + 3])
                          : "memory");
           __syncwarp();
+          if (p.tma_store) {
+            ptx::fence_proxy_async_smem();
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (tid == 0) {
+              const uint32_t img = sbase + SM::STG_OFF;
+              if (p.tma_store == 1) {
+                const int mt_i = m0 / BM;
+                const int tw_i = mt_i % p.tiles_w, th_i = (mt_i / p.tiles_w) % p.tiles_h, tn_i = mt_i / (p.tiles_w * p.tiles_h);
+                ptx::tma_store_4d(&tma_d, img, nb, tw_i * p.tw, th_i * p.th, tn_i * p.tn, accum);
+              } else {
+                ptx::tma_store_2d(&tma_d, img, nb, m0, accum);
+              }
+              ptx::bulk_commit();
+            }
+          }
+          if (!p.tma_store) {
           const int q = lane & 7;
           const int col = nb + 4 * q;
           float* dsts[8];
@@ -945,6 +974,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
             }
             if (dsts[i]) *reinterpret_cast<float4*>(dsts[i]) = o;
           }
+          }
           if constexpr (MODE == CONV_FWD) {
             if (stats) {
               // per-tile BN partial sums straight from the staged block: lane = column, rows in
@@ -968,7 +998,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
           __syncwarp();
         }
         if constexpr (MODE == CONV_FWD) {
-          if (stats && p.epi_direct) {
+          if (stats && p.epi_direct == 1) {
             float sq[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
@@ -1002,6 +1032,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
       }
     }
   }
+  if (tid == 0 && p.tma_store) ptx::bulk_wait0();  // the epilogue's TMA stores are complete
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 8) {
