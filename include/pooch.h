@@ -275,6 +275,16 @@ pooch_status pooch_plan_problem(const pooch_problem* prob, int32_t strategy, con
                                 const uint8_t* fixed_classes, uint8_t* classes_out,
                                 pooch_plan_report* report);
 
+/* The executor's plan refinement (DESIGN.md Reading 42; pooch_plan applies it to its best grid
+ * candidates): passes over the maps trying every other class of each (the sink never
+ * recompute), keeping a change when it lowers (greedy static-packing excess over `capacity`,
+ * simulated makespan) lexicographically, under the simulator of Sec. 4.1.2 with the problem's
+ * budget and host budget. classes_out (n) receives the result; makespan_ns (incl. tail) and
+ * packs (1 = its ledger packs into capacity) nullable. POOCH_EINFEASIBLE if the start runs out
+ * of memory or host arena. Host only. */
+pooch_status pooch_refine_problem(const pooch_problem* prob, const uint8_t* classes, int32_t sched,
+                                  uint64_t capacity, uint8_t* classes_out, int64_t* makespan_ns, int32_t* packs);
+
 /* Static arena offsets (replaces the paper's hooked allocator): simulate `classes`,
  * replay the allocation ledger best-fit over [0, capacity). Buffer instances b in [0, 3n):
  * b = m forward instance of map m, n + m its backward-phase (swapped-in / recomputed)

@@ -118,6 +118,7 @@ SIGNATURES = {
     "pooch_op_conv_fwd2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pooch_op_conv_dgrad2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "pooch_op_conv_wgrad2": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "pooch_refine_problem": (c_i32, [c_vp, c_vp, c_i32, c_u64, c_vp, P(c_i64), P(c_i32)]),
     "pooch_op_conv_fwd_bnrelu": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pooch_op_conv_wgrad_bnrelu": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pooch_op_maxpool2d_fwd": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),

@@ -1138,6 +1138,73 @@ extern "C" pooch_status pooch_set_profile(pooch_ctx* c, const int64_t* fwd, cons
   return POOCH_OK;
 }
 
+// Local refinement of a classification under the same cost model (Reading 42): repeated passes
+// over the maps, trying every other class of each map (the sink never recompute) and keeping a
+// change when it is better in (greedy-packing excess over the arena, simulated makespan) order:
+// first make the ledger pack into `cap`, then lower the makespan. Host capacity for the swap
+// class is a hard constraint. Returns the evaluation of the result (ok = false: the start itself
+// runs out of memory or host arena).
+struct RefineEval {
+  bool ok = false;
+  int64_t mk = 0;
+  uint64_t over = 0;  // 0: packs into cap
+};
+static RefineEval refine_eval(const Problem& p, int sched, uint64_t cap, const std::vector<uint64_t>& map_bytes,
+                              uint64_t host_bytes, const std::vector<uint8_t>& cl) {
+  RefineEval e;
+  const int n = p.n;
+  uint64_t host_need = 0;
+  for (int m = 0; m < n; ++m)
+    if (cl[m] == C_SWAP) host_need += align_up(map_bytes[m]);
+  if (host_need > host_bytes) return e;
+  SimOptions o;
+  o.sched = sched;
+  o.record_ledger = true;
+  o.want_sets = false;
+  SimOut so;
+  simulate(p, cl.data(), o, so);
+  if (so.oom) return e;
+  std::vector<uint64_t> off;
+  uint64_t high;
+  const bool fits = pack_ledger(so.ledger, 3 * n, cap, false, off, high, 0);
+  e.ok = true;
+  e.mk = so.makespan;
+  e.over = fits ? 0 : (high > cap ? high - cap : 1);
+  return e;
+}
+static bool refine_better(const RefineEval& a, const RefineEval& b) {
+  if (!a.ok) return false;
+  if (!b.ok) return true;
+  if (a.over != b.over) return a.over < b.over;
+  return a.mk < b.mk;
+}
+static RefineEval refine_plan(const Problem& p, int sched, uint64_t cap, const std::vector<uint64_t>& map_bytes,
+                              uint64_t host_bytes, const std::vector<uint8_t>& start, std::vector<uint8_t>& out,
+                              int max_passes = 6) {
+  const int n = p.n;
+  std::vector<uint8_t> cur = start;
+  RefineEval ce = refine_eval(p, sched, cap, map_bytes, host_bytes, cur);
+  for (int pass = 0; pass < max_passes && ce.ok; ++pass) {
+    bool improved = false;
+    for (int m = 0; m < n; ++m)
+      for (uint8_t alt = C_KEEP; alt <= C_RECOMPUTE; ++alt) {
+        if (alt == cur[m] || (m == n - 1 && alt == C_RECOMPUTE)) continue;
+        const uint8_t was = cur[m];
+        cur[m] = alt;
+        const RefineEval e = refine_eval(p, sched, cap, map_bytes, host_bytes, cur);
+        if (refine_better(e, ce)) {
+          ce = e;
+          improved = true;
+        } else {
+          cur[m] = was;
+        }
+      }
+    if (!improved) break;
+  }
+  out = cur;
+  return ce;
+}
+
 // Plan selection with packing in the loop (row a6). The simulator's memory ledger is a byte
 // sum (Sec. 4.1.2), so a plan whose simulated peak fits the arena may still fail to pack into
 // static offsets (fragmentation: measured +2-8 % over the peak on ResNet-50). And the PoocH
@@ -1277,40 +1344,10 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
         break;
       }
     }
-    // Local refinement (Reading 42): single-map class changes under the same cost model, from the
-    // adopted plan and the fastest grid candidates (packable or not): first make the ledger pack
-    // (greedy high-water over the arena, lexicographically first), then lower the makespan.
+    // Local refinement (Reading 42) from the adopted plan and the fastest grid candidates
     if (strategy == POOCH_STRAT_POOCH && !getenv("POOCH_PLAN_NO_REFINE") && !order.empty()) {
       const Problem pc = make_problem(c, cap);
       const int sched = cands[order[0]].sched;
-      struct Eval { bool ok = false; int64_t mk = 0; uint64_t over = 0; };
-      auto eval = [&](const std::vector<uint8_t>& cl) {
-        Eval e;
-        uint64_t host_need = 0;
-        for (int m = 0; m < n; ++m)
-          if (cl[m] == C_SWAP) host_need += align_up(c->map_bytes[m]);
-        if (host_need > c->host_bytes) return e;
-        SimOptions o;
-        o.sched = sched;
-        o.record_ledger = true;
-        o.want_sets = false;
-        SimOut so;
-        simulate(pc, cl.data(), o, so);
-        if (so.oom) return e;
-        std::vector<uint64_t> off;
-        uint64_t high;
-        const bool fits = pack_ledger(so.ledger, 3 * n, cap, false, off, high, 0);
-        e.ok = true;
-        e.mk = so.makespan;
-        e.over = fits ? 0 : (high > cap ? high - cap : 1);
-        return e;
-      };
-      auto better = [](const Eval& a, const Eval& b) {  // a better than b
-        if (!a.ok) return false;
-        if (!b.ok) return true;
-        if (a.over != b.over) return a.over < b.over;
-        return a.mk < b.mk;
-      };
       std::vector<std::vector<uint8_t>> starts;
       if (adopted >= 0) starts.push_back(cands[adopted].cls);
       for (int i : order) {
@@ -1318,32 +1355,10 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
         if (std::find(starts.begin(), starts.end(), cands[i].cls) == starts.end()) starts.push_back(cands[i].cls);
       }
       std::vector<std::vector<uint8_t>> res(starts.size());
-      std::vector<Eval> res_e(starts.size());
+      std::vector<RefineEval> res_e(starts.size());
       std::vector<std::thread> th;
       for (size_t k = 0; k < starts.size(); ++k)
-        th.emplace_back([&, k] {
-          std::vector<uint8_t> cur = starts[k];
-          Eval ce = eval(cur);
-          for (int pass = 0; pass < 6 && ce.ok; ++pass) {
-            bool improved = false;
-            for (int m = 0; m < n; ++m)
-              for (uint8_t alt = C_KEEP; alt <= C_RECOMPUTE; ++alt) {
-                if (alt == cur[m] || (m == n - 1 && alt == C_RECOMPUTE)) continue;
-                const uint8_t was = cur[m];
-                cur[m] = alt;
-                const Eval e = eval(cur);
-                if (better(e, ce)) {
-                  ce = e;
-                  improved = true;
-                } else {
-                  cur[m] = was;
-                }
-              }
-            if (!improved) break;
-          }
-          res[k] = cur;
-          res_e[k] = ce;
-        });
+        th.emplace_back([&, k] { res_e[k] = refine_plan(pc, sched, cap, c->map_bytes, c->host_bytes, starts[k], res[k]); });
       for (auto& t : th) t.join();
       int bk = -1;
       for (size_t k = 0; k < res.size(); ++k)
@@ -1857,6 +1872,26 @@ extern "C" pooch_status pooch_set_precision(pooch_ctx* c, int32_t precision) {
   c->precision = precision;
   c->have_profile = false;
   c->have_plan = false;
+  return POOCH_OK;
+}
+
+// host-only: the executor's plan refinement (Reading 42) on a planning problem, for tests
+extern "C" pooch_status pooch_refine_problem(const pooch_problem* prob, const uint8_t* classes, int32_t sched,
+                                             uint64_t capacity, uint8_t* classes_out, int64_t* makespan_ns,
+                                             int32_t* packs) {
+  if (!prob || !classes || !classes_out) return fail(POOCH_EUSAGE, "null argument");
+  Problem p;
+  std::string err;
+  if (!problem_from_c(*prob, p, err)) return fail(POOCH_EUSAGE, "%s", err.c_str());
+  const int sc = sched == POOCH_SCHED_NAIVE ? SCHED_NAIVE : (sched == POOCH_SCHED_SN ? SCHED_SN : SCHED_EAGER);
+  std::vector<uint64_t> mb(p.bytes.begin(), p.bytes.end());
+  const uint64_t host = p.host_budget ? p.host_budget : UINT64_MAX;
+  std::vector<uint8_t> start(classes, classes + p.n), out;
+  const RefineEval e = refine_plan(p, sc, capacity, mb, host, start, out);
+  if (!e.ok) return fail(POOCH_EINFEASIBLE, "the starting classification runs out of memory or host arena");
+  std::copy(out.begin(), out.end(), classes_out);
+  if (makespan_ns) *makespan_ns = e.mk + p.tail;
+  if (packs) *packs = e.over == 0 ? 1 : 0;
   return POOCH_OK;
 }
 

@@ -115,3 +115,13 @@ class PlanProblem:
             return None
         check(st)
         return dict(offsets=off, alloc=a, free=f, sizes=sz, high_water=hw.value)
+
+    def refine(self, classes, capacity, sched=EAGER):
+        """The executor's plan refinement (pooch_refine_problem): (classes, makespan_ns, packs)."""
+        cls = np.asarray(classes, np.uint8)
+        out = np.zeros(self.n, np.uint8)
+        mk = C.c_int64()
+        pk = C.c_int32()
+        check(lib.pooch_refine_problem(C.byref(self.c), cls.ctypes.data_as(P(C.c_uint8)), sched, int(capacity),
+                                       out.ctypes.data_as(P(C.c_uint8)), C.byref(mk), C.byref(pk)))
+        return [int(v) for v in out], int(mk.value), bool(pk.value)

@@ -1,0 +1,64 @@
+"""Plan refinement (DESIGN.md Reading 42, pooch_refine_problem): single-map class moves under the
+paper's simulator. Properties: the result is a valid classification (sink never recompute),
+never worse than a packable start, its reported makespan is the simulator's, and when it claims
+to pack, the executor's static packing of its ledger fits the arena."""
+import json
+import os
+
+import pytest
+
+import synthdata
+from oracle import nets
+from oracle.sim import RECOMPUTE, SWAP
+
+pp = pytest.importorskip("paper_1907_05013_b200.planning")
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _check(pc, start, cap):
+    s0 = pc.simulate(start)
+    p0 = pc.pack(start, cap) is not None
+    cls, mk, packs = pc.refine(start, cap)
+    assert len(cls) == pc.n and cls[-1] != RECOMPUTE and all(c in (0, 1, 2) for c in cls)
+    s1 = pc.simulate(cls)
+    assert not s1["oom"]
+    assert s1["makespan"] == mk                       # reported = simulated (problems here have no tail)
+    if packs:
+        assert pc.pack(cls, cap) is not None
+    if p0:
+        assert packs and mk <= s0["makespan"]
+    return cls, mk, packs
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_problems(seed):
+    g = synthdata.rng(7000 + seed)
+    n = int(g.integers(3, 11))
+    d = synthdata.random_profile(n, seed, dag=seed % 2 == 0, max_bytes=4096)
+    for frac in (0.6, 0.9, 1.5):
+        budget = int(sum(d["bytes"]) * frac)
+        pc = pp.PlanProblem.from_dict(d, resident=0, budget=budget)
+        for _ in range(4):
+            start = [int(v) for v in g.integers(0, 3, n)]
+            start[-1] = min(start[-1], SWAP)
+            if not pc.simulate(start)["oom"]:
+                _check(pc, start, budget)
+
+
+def test_measured_resnet50_profile():
+    """On the committed cfg2 profile (profiles/r01_profile_cfg2.json), refining the PoocH plan
+    planned at the full arena yields a plan that packs into the arena and is no slower than the
+    best packable plan of the budget grid's first steps."""
+    d = json.load(open(os.path.join(HERE, "..", "profiles", "r01_profile_cfg2.json")))
+    pr = d["profile"]
+    net = nets.resnet50()
+    n = len(net.tasks)
+    inputs = [[j for j in t.inputs if j >= 0] for t in net.tasks]
+    needs = [net.needs(i) for i in range(n)]
+    cap = d["budget"] - pr["resident"]
+    pc = pp.PlanProblem(pr["fwd"], pr["bwd"], pr["bytes"], pr["d2h"], pr["h2d"], inputs, needs, resident=0,
+                        budget=cap, rec=pr["rec"], tail=0, is_conv=[int(t.kind == "conv") for t in net.tasks])
+    start, rep = pc.plan("pooch", li_cap=6)
+    cls, mk, packs = _check(pc, start, cap)
+    assert packs
+    assert mk <= rep.makespan_ns
