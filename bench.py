@@ -252,6 +252,10 @@ def our_arm(args):
     if budget is None:
         budget = int(free - (3 << 30))
     budget = budget // 256 * 256
+    if world > 1:  # one budget for all ranks (free HBM can differ by a few MB): identical plans
+        t = torch.tensor([budget], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        budget = int(t.item())
     maps_total = sum(ctx_map_bytes(ctx))
     host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.6 * os.sysconf("SC_PAGE_SIZE") *
                          os.sysconf("SC_PHYS_PAGES") / max(1, world)))
