@@ -237,9 +237,15 @@ static int epi_direct() {  // POOCH_EPI_DIRECT=1: unstaged epilogue stores (A/B 
   return v;
 }
 
+static int early_ab() {
+  static int v = getenv("POOCH_EARLY_AB") ? atoi(getenv("POOCH_EARLY_AB")) : 0;
+  return v;
+}
+
 static GemmParams base_params(const ConvGeom& g) {
   GemmParams p{};
   p.epi_direct = epi_direct();
+  p.early_ab = early_ab();
   p.N = g.N; p.H = g.H; p.W = g.W; p.C = g.C;
   p.K = g.K; p.R = g.R; p.S = g.S;
   p.Ho = g.Ho; p.Wo = g.Wo; p.stride = g.stride; p.pad = g.pad;
