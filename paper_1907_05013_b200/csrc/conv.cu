@@ -176,7 +176,7 @@ static bool map_2d(CUtensorMap* m, const float* base, int rows, int cols, int bn
 
 // Epilogue stores through the TMA (POOCH_NO_TMA_STORE=1: per-thread stores, for A/B tests)
 static bool tma_store_enabled() {
-  static int on = getenv("POOCH_NO_TMA_STORE") ? 0 : 1;
+  static int on = (getenv("POOCH_NO_TMA_STORE") || (getenv("POOCH_EPI_DIRECT") && atoi(getenv("POOCH_EPI_DIRECT")) == 4)) ? 0 : 1;
   return on != 0 && encode_fn() != nullptr;
 }
 
@@ -237,15 +237,9 @@ static int epi_direct() {  // POOCH_EPI_DIRECT=1: unstaged epilogue stores (A/B 
   return v;
 }
 
-static int early_ab() {
-  static int v = getenv("POOCH_EARLY_AB") ? atoi(getenv("POOCH_EARLY_AB")) : 0;
-  return v;
-}
-
 static GemmParams base_params(const ConvGeom& g) {
   GemmParams p{};
   p.epi_direct = epi_direct();
-  p.early_ab = early_ab();
   p.N = g.N; p.H = g.H; p.W = g.W; p.C = g.C;
   p.K = g.K; p.R = g.R; p.S = g.S;
   p.Ho = g.Ho; p.Wo = g.Wo; p.stride = g.stride; p.pad = g.pad;

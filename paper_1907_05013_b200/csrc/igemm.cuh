@@ -83,7 +83,6 @@ struct GemmParams {
   // epilogue stores through the TMA (tma_d): 1 = 4-D box of output pixels {32 ch, tw, th, tn}
   // (PIXM, one dgrad class of stride 1), 2 = 2-D {32 cols, 128 rows} of a row-major [M][Ng]
   int tma_store;
-  int early_ab;          // experiments: 3xTF32 A*B issued before the residual pass (POOCH_EARLY_AB)
   // transform on load (XF kernels): the activation operand (FWD: A = x, WGRAD: x)
   // is relu(xf_scale[c] * v + xf_shift[c]) of the stored tensor; zero padding stays zero
   const float* xf_scale;
@@ -802,35 +801,6 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
       const uint32_t acc = tmem + ab * BN;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         int s = it % STAGES;
-        if constexpr (X3 && TMA && !XF && MODE != CONV_WGRAD) {
-          if (p.early_ab) {
-            // experiment (POOCH_EARLY_AB=1): A*B needs only the raw TMA tiles -- issue it when they
-            // land, overlapping the residual pass; A*Bs and As*B once the residuals are published
-            const uint32_t sa = sbase + s * SM::STAGE_BYTES, sb = sa + SM::A_BYTES;
-            ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
-            ptx::tc_fence_after();
-            if (lane == 0)
-#pragma unroll
-              for (int kk = 0; kk < BK / 8; ++kk)
-                ptx::mma_tf32(acc, ptx::smem_desc(sa + kk * 32, 16, 1024, 2), ptx::smem_desc(sb + kk * 32, 16, 1024, 2),
-                              IDESC, (kb | kk) != 0 ? 1u : 0u);
-            __syncwarp();
-            ptx::mbar_wait(&full[s], (it / STAGES) & 1);
-            ptx::tc_fence_after();
-            if (lane == 0) {
-#pragma unroll
-              for (int kk = 0; kk < BK / 8; ++kk) {
-                ptx::mma_tf32(acc, ptx::smem_desc(sa + SM::SMALL_OFF + kk * 32, 16, 1024, 2),
-                              ptx::smem_desc(sb + kk * 32, 16, 1024, 2), IDESC, 1u);
-                ptx::mma_tf32(acc, ptx::smem_desc(sa + kk * 32, 16, 1024, 2),
-                              ptx::smem_desc(sb + SM::SMALL_OFF + kk * 32, 16, 1024, 2), IDESC, 1u);
-              }
-              ptx::mma_commit(&empty[s]);
-            }
-            __syncwarp();
-            continue;
-          }
-        }
         ptx::mbar_wait(&full[s], (it / STAGES) & 1);
         ptx::tc_fence_after();
         if (lane == 0) {
@@ -892,7 +862,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
       const uint32_t taddr = tmem + ab * BN + ((uint32_t)(warp * 32) << 16);
       const int z = t / (tm.mt * tm.nt);
       bool stats = false;
-      if constexpr (MODE == CONV_FWD) stats = p.stat_sum != nullptr;
+      if constexpr (MODE == CONV_FWD) stats = p.stat_sum != nullptr && p.epi_direct != 3;  // 3: experiment
       if (stats) asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's reads of red[] done
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -927,7 +897,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
         if (p.epi_direct == 2) {
           // timing experiment only (POOCH_EPI_DIRECT=2): drain TMEM, store nothing
           if (rok && v[0] == 12345.f) p.d[0] = v[1];
-        } else if (p.epi_direct) {
+        } else if (p.epi_direct == 1) {
           if (rok) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
@@ -975,7 +945,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
               ptx::bulk_commit();
             }
           }
-          if (!p.tma_store) {
+          if (!p.tma_store && p.epi_direct != 4) {  // 4: experiment, no stores
           const int q = lane & 7;
           const int col = nb + 4 * q;
           float* dsts[8];

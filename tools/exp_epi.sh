@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-for m in 0 1 2; do POOCH_EPI_DIRECT=$m B=256 ONLY="l1.c3" OPS=fwd timeout 300 python tools/kbench.py > gpurun_out/exp_epi$m.log 2>&1; done
-for m in 0 2; do POOCH_EPI_DIRECT=$m B=256 ONLY="l3.c2" OPS=fwd,dgrad timeout 300 python tools/kbench.py > gpurun_out/exp2_epi$m.log 2>&1; done
-for m in 0 2; do POOCH_EPI_DIRECT=$m B=256 ONLY="l1.c2" OPS=fwd,dgrad timeout 300 python tools/kbench.py > gpurun_out/exp3_epi$m.log 2>&1; done
+for m in 0 2 3 4; do POOCH_EPI_DIRECT=$m B=256 ONLY="l1.c3" OPS=fwd timeout 300 python tools/kbench.py > gpurun_out/exp_epi$m.log 2>&1; done
+for m in 0 2 3 4; do POOCH_EPI_DIRECT=$m B=256 ONLY="l3.c3" OPS=fwd timeout 300 python tools/kbench.py > gpurun_out/exp4_epi$m.log 2>&1; done
