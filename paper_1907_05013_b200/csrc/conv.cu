@@ -226,6 +226,13 @@ static PixBox choose_box(int N3, int Ho, int Wo, int st, int st3, bool three) {
 }
 
 static bool fwd_uses_tma(const ConvGeom& g) { return tma_enabled() && g.C % 32 == 0 && g.stride <= 2; }
+// 4-channel 2D input (the stem, the tiny CNN's first conv) through TMA boxes of one tap each:
+// correct (parity-tested) but opt-in (POOCH_STEM_TMA=1) -- 16 TMA issues per k-block measured at
+// ~120 ns each make it 1.8x slower than the cp.async gathers (stem fwd, batch 256: 2.29 vs 1.25 ms)
+static bool fwd_uses_stem4(const ConvGeom& g) {
+  static int on = getenv("POOCH_STEM_TMA") ? atoi(getenv("POOCH_STEM_TMA")) : 0;
+  return on && tma_enabled() && g.C == 4 && !g.is3d() && g.C1 == 0 && g.stride <= 2;
+}
 static bool dgrad_uses_tma(const ConvGeom& g) { return tma_enabled() && g.K % 32 == 0 && g.stride <= 2; }
 
 static int pick_bn(int n, int prec = 0) {
@@ -256,7 +263,7 @@ static int out3(const ConvGeom& g) { return g.is3d() ? g.Do : g.N; }
 static int64_t out_pixels(const ConvGeom& g) { return (int64_t)out3(g) * g.Ho * g.Wo; }
 
 int conv_stat_tiles(const ConvGeom& g) {
-  if (fwd_uses_tma(g)) {
+  if (fwd_uses_tma(g) || fwd_uses_stem4(g)) {
     PixBox b = choose_box(out3(g), g.Ho, g.Wo, g.stride, g.is3d() ? g.stride : 1, g.is3d());
     return b.tiles_w * b.tiles_h * b.tiles_n;
   }
@@ -301,6 +308,40 @@ pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, 
       p.tma_store = 1;
     return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb, g.C1 > 0 ? &tc : nullptr,
                                      p.tma_store ? &td : nullptr);
+  }
+  if (fwd_uses_stem4(g) && !xf_scale) {
+    PixBox b = choose_box(g.N, g.Ho, g.Wo, g.stride, 1, false);
+    p.tw = b.tw; p.th = b.th; p.tn = b.tn;
+    p.tiles_w = b.tiles_w; p.tiles_h = b.tiles_h; p.tiles_n = b.tiles_n;
+    p.hout = g.Ho; p.wout = g.Wo; p.n3 = g.N;
+    p.stem4 = 1;
+    p.Kg = (g.R * g.S + 7) / 8 * 32;  // 8 taps per k-block; taps past R*S are zero boxes
+    p.cchunks = 1;
+    CUtensorMap ta, tb;
+    auto fn = encode_fn();
+    // A: {4 channels, W, H, N}, box {4, tw*st, th*st, tn}, traversal stride st, no swizzle
+    cuuint64_t dims[4] = {4, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    cuuint64_t strides[3] = {16, (cuuint64_t)g.W * 16, (cuuint64_t)g.H * g.W * 16};
+    cuuint32_t box[4] = {4, (cuuint32_t)(b.tw * g.stride), (cuuint32_t)(b.th * g.stride), (cuuint32_t)b.tn};
+    cuuint32_t es[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
+    // B: the [K][R*S*4] weight matrix, box {4 (one tap), bn rows}
+    cuuint64_t bd[2] = {(cuuint64_t)g.R * g.S * 4, (cuuint64_t)g.K};
+    cuuint64_t bs[1] = {(cuuint64_t)g.R * g.S * 16};
+    cuuint32_t bb[2] = {4, (cuuint32_t)bn};
+    cuuint32_t be[2] = {1, 1};
+    if (fn(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS ||
+        fn(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)w, bd, bs, bb, be, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+      return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (4-channel conv fwd)");
+    dim3 grid(b.tiles_w * b.tiles_h * b.tiles_n, (p.Ng + bn - 1) / bn, 1);
+    CUtensorMap td;
+    if (tma_store_enabled() &&
+        map_view4(&td, y, g.K, g.Wo, g.Ho, g.N, g.K, (int64_t)g.Wo * g.K, (int64_t)g.Ho * g.Wo * g.K, b.tw, b.th, b.tn))
+      p.tma_store = 1;
+    return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb, nullptr, p.tma_store ? &td : nullptr);
   }
   if (g.is3d() || g.C1 > 0) return fail(POOCH_EUSAGE, "3D / two-source conv needs the TMA path");
   dim3 grid((p.M + BM - 1) / BM, (p.Ng + bn - 1) / bn, 1);

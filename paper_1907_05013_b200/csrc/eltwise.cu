@@ -98,13 +98,9 @@ __global__ void bn_apply_kernel(const float* __restrict__ a, const float* __rest
   const int cstep = (int)(stride % C4);
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int cg = (int)(i % C4);  // channel group, advanced incrementally (no 64-bit modulo per element)
-  for (; i < n4; i += stride) {
-    int c = cg * 4;
-    cg += cstep;
-    if (cg >= C4) cg -= C4;
-    float4 av = ld4(a + 4 * i), s1 = ld4(sa + c), t1 = ld4(ta + c);
-    float4 bv = make_float4(0, 0, 0, 0), s2 = bv, t2 = bv;
-    if (MODE != 0) bv = ld4(b + 4 * i);
+  auto one = [&](int64_t k, int c, const float4& av, const float4& bv) {
+    const float4 s1 = ld4(sa + c), t1 = ld4(ta + c);
+    float4 s2 = make_float4(0, 0, 0, 0), t2 = s2;
     if (MODE == 1) {
       s2 = ld4(sb + c);
       t2 = ld4(tb + c);
@@ -114,7 +110,32 @@ __global__ void bn_apply_kernel(const float* __restrict__ a, const float* __rest
     o.y = fmaxf(pre_act<MODE>(av.y, s1.y, t1.y, bv.y, s2.y, t2.y), 0.f);
     o.z = fmaxf(pre_act<MODE>(av.z, s1.z, t1.z, bv.z, s2.z, t2.z), 0.f);
     o.w = fmaxf(pre_act<MODE>(av.w, s1.w, t1.w, bv.w, s2.w, t2.w), 0.f);
-    st4(y + 4 * i, o);
+    st4(y + 4 * k, o);
+  };
+  // two elements of the grid-stride loop per iteration, both loads issued before either store
+  for (; i + stride < n4; i += 2 * stride) {
+    const int c0 = cg * 4;
+    cg += cstep;
+    if (cg >= C4) cg -= C4;
+    const int c1 = cg * 4;
+    cg += cstep;
+    if (cg >= C4) cg -= C4;
+    const float4 a0 = ld4(a + 4 * i), a1 = ld4(a + 4 * (i + stride));
+    float4 b0 = make_float4(0, 0, 0, 0), b1 = b0;
+    if (MODE != 0) {
+      b0 = ld4(b + 4 * i);
+      b1 = ld4(b + 4 * (i + stride));
+    }
+    one(i, c0, a0, b0);
+    one(i + stride, c1, a1, b1);
+  }
+  for (; i < n4; i += stride) {
+    const int c = cg * 4;
+    cg += cstep;
+    if (cg >= C4) cg -= C4;
+    float4 bv = make_float4(0, 0, 0, 0);
+    if (MODE != 0) bv = ld4(b + 4 * i);
+    one(i, c, ld4(a + 4 * i), bv);
   }
 }
 
@@ -144,18 +165,16 @@ __global__ void __launch_bounds__(kBwdThreads) bn_bwd_reduce_kernel(BnBwdArgs p,
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[q][j][e] = 0.f;
   if (roff < rpi) {
-    for (int64_t r = r0 + roff; r < r1; r += rpi) {
 #pragma unroll
-      for (int j = 0; j < CGPT; ++j) {
-        int c = 4 * (cg0 + j * tpr);
-        size_t off = (size_t)r * C + c;
-        float4 av = ld4(p.a + off), g = ld4(p.gy + off);
-        float4 s1 = ld4(p.sa + c), t1 = ld4(p.ta + c), m1 = ld4(p.mean_a + c), i1 = ld4(p.invstd_a + c);
-        float4 bv = make_float4(0, 0, 0, 0), s2 = bv, t2 = bv, m2 = bv, i2 = bv;
-        if (MODE != 0) bv = ld4(p.b + off);
-        if (MODE == 1) {
-          s2 = ld4(p.sb + c); t2 = ld4(p.tb + c); m2 = ld4(p.mean_b + c); i2 = ld4(p.invstd_b + c);
-        }
+    for (int j = 0; j < CGPT; ++j) {
+      // per-channel parameters: loop-invariant, loaded once
+      const int c = 4 * (cg0 + j * tpr);
+      const float4 s1 = ld4(p.sa + c), t1 = ld4(p.ta + c), m1 = ld4(p.mean_a + c), i1 = ld4(p.invstd_a + c);
+      float4 s2 = make_float4(0, 0, 0, 0), t2 = s2, m2 = s2, i2 = s2;
+      if (MODE == 1) {
+        s2 = ld4(p.sb + c); t2 = ld4(p.tb + c); m2 = ld4(p.mean_b + c); i2 = ld4(p.invstd_b + c);
+      }
+      auto row = [&](const float4& av, const float4& g, const float4& bv) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float v = pre_act<MODE>(f4get(av, e), f4get(s1, e), f4get(t1, e), f4get(bv, e), f4get(s2, e), f4get(t2, e));
@@ -164,6 +183,26 @@ __global__ void __launch_bounds__(kBwdThreads) bn_bwd_reduce_kernel(BnBwdArgs p,
           acc[1][j][e] += dz * ((f4get(av, e) - f4get(m1, e)) * f4get(i1, e));
           if (MODE == 1) acc[2 % NQ][j][e] += dz * ((f4get(bv, e) - f4get(m2, e)) * f4get(i2, e));
         }
+      };
+      int64_t r = r0 + roff;
+      // two rows per iteration: all loads first (more bytes in flight), then the same
+      // accumulation order as one row at a time
+      for (; r + rpi < r1; r += 2 * rpi) {
+        const size_t o0 = (size_t)r * C + c, o1 = o0 + (size_t)rpi * C;
+        const float4 a0 = ld4(p.a + o0), g0 = ld4(p.gy + o0), a1 = ld4(p.a + o1), g1 = ld4(p.gy + o1);
+        float4 b0 = make_float4(0, 0, 0, 0), b1 = b0;
+        if (MODE != 0) {
+          b0 = ld4(p.b + o0);
+          b1 = ld4(p.b + o1);
+        }
+        row(a0, g0, b0);
+        row(a1, g1, b1);
+      }
+      for (; r < r1; r += rpi) {
+        const size_t o0 = (size_t)r * C + c;
+        float4 b0 = make_float4(0, 0, 0, 0);
+        if (MODE != 0) b0 = ld4(p.b + o0);
+        row(ld4(p.a + o0), ld4(p.gy + o0), b0);
       }
     }
   }

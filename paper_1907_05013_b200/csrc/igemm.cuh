@@ -83,6 +83,9 @@ struct GemmParams {
   // epilogue stores through the TMA (tma_d): 1 = 4-D box of output pixels {32 ch, tw, th, tn}
   // (PIXM, one dgrad class of stride 1), 2 = 2-D {32 cols, 128 rows} of a row-major [M][Ng]
   int tma_store;
+  // TMA-fed FWD over a 4-channel input (the stem): a k-block is 8 taps x 4 channels; per tap one
+  // 16-B-wide box of A (SWIZZLE_NONE, the K-major core-matrix layout) and one of B
+  int stem4;
   // transform on load (XF kernels): the activation operand (FWD: A = x, WGRAD: x)
   // is relu(xf_scale[c] * v + xf_shift[c]) of the stored tensor; zero padding stays zero
   const float* xf_scale;
@@ -619,6 +622,24 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
               chh = th_i * p.th + (p.dg_a + p.pad - r) / p.stride;
               c3 = tn_i * p.tn + (p.dg_c + p.pad3 - t3) / p.st3;
             }
+            if (MODE == CONV_FWD && p.stem4) {
+              // 8 taps of 4 channels: tap j's A box (16 B per output pixel) lands at j * BM * 16 and
+              // its B box at j * BN * 16 -- SWIZZLE_NONE core matrices, K-adjacent ones BM*16 / BN*16
+              // apart. Taps past R*S load fully out-of-bounds boxes: zeros, bytes still counted.
+              const int ntap = p.R * p.S;
+              ptx::mbar_arrive_expect_tx(bar, 8u * (16u * p.tw * p.th * p.tn + 16u * BN));
+#pragma unroll 1
+              for (int j = 0; j < 8; ++j) {
+                const int tp = 8 * k + j;
+                const bool live = tp < ntap;
+                const int r = live ? tp / p.S : 0, sx = live ? tp - (tp / p.S) * p.S : 0;
+                const int aw = live ? tw_i * p.tw * p.stride - p.pad + sx : -(1 << 20);
+                const int ah = th_i * p.th * p.stride - p.pad + r;
+                ptx::tma_load_4d(st + j * (BM * 16), &tma_a, bar, 0, aw, ah, tn_i * p.tn);
+                ptx::tma_load_2d(st + SM::A_BYTES + j * (BN * 16), &tma_b, bar, live ? 4 * tp : (1 << 20), n0);
+              }
+              continue;
+            }
             ptx::mbar_arrive_expect_tx(bar, bytes);
             if (MODE == CONV_FWD && p.c_split && cc * 32 >= p.c_split)
               ptx::tma_load_4d(st, &tma_c, bar, cc * 32 - p.c_split, cw, chh, c3);
@@ -806,12 +827,13 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
         if (lane == 0) {
           uint32_t sa = sbase + s * SM::STAGE_BYTES;
           uint32_t sb = sa + SM::A_BYTES;
+          const bool sw = TMA && !p.stem4;  // SWIZZLE_128B tiles, else the SWIZZLE_NONE core-matrix layout
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            // SWIZZLE_NONE (cp.async tiles): k-step = 2 core matrices; SWIZZLE_128B (TMA tiles):
+            // SWIZZLE_NONE (cp.async / stem tiles): k-step = 2 core matrices; SWIZZLE_128B (TMA tiles):
             // 128-B rows in 1024-B atoms (SBO), k-step = +32 B inside the row
-            const uint32_t ka = TMA ? kk * 32 : kk * 2 * A_LBO, kbo = TMA ? kk * 32 : kk * 2 * B_LBO;
-            const uint32_t la = TMA ? 16 : A_LBO, lb = TMA ? 16 : B_LBO, sbo = TMA ? 1024 : 128, lay = TMA ? 2 : 0;
+            const uint32_t ka = sw ? kk * 32 : kk * 2 * A_LBO, kbo = sw ? kk * 32 : kk * 2 * B_LBO;
+            const uint32_t la = sw ? 16 : A_LBO, lb = sw ? 16 : B_LBO, sbo = sw ? 1024 : 128, lay = sw ? 2 : 0;
             uint64_t ad = ptx::smem_desc(sa + ka, la, sbo, lay);
             uint64_t bd = ptx::smem_desc(sb + kbo, lb, sbo, lay);
             if constexpr (X3) {  // small terms first, then the big product
