@@ -1002,19 +1002,19 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
               // per-tile BN partial sums straight from the staged block: lane = column, rows in
               // order (deterministic), rows outside the output grid masked
               const unsigned okm = __ballot_sync(0xffffffffu, rok);
-              float s1 = 0.f, s2 = 0.f;
-#pragma unroll 8
+              float p1[4] = {0.f, 0.f, 0.f, 0.f}, p2[4] = {0.f, 0.f, 0.f, 0.f};  // 4 short chains
+#pragma unroll
               for (int r = 0; r < 32; ++r) {
                 float x;
                 asm volatile("ld.shared.f32 %0, [%1];"
                              : "=f"(x)
                              : "r"(stg + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4));
                 x = ((okm >> r) & 1u) ? x : 0.f;
-                s1 += x;
-                s2 = fmaf(x, x, s2);
+                p1[r & 3] += x;
+                p2[r & 3] = fmaf(x, x, p2[r & 3]);
               }
-              red[warp * BN + c * 32 + lane] = s1;
-              red[4 * BN + warp * BN + c * 32 + lane] = s2;
+              red[warp * BN + c * 32 + lane] = (p1[0] + p1[1]) + (p1[2] + p1[3]);
+              red[4 * BN + warp * BN + c * 32 + lane] = (p2[0] + p2[1]) + (p2[2] + p2[3]);
             }
           }
           __syncwarp();
