@@ -94,6 +94,13 @@ struct pooch_ctx {
   uint64_t arena_high = 0;
   uint64_t plan_budget = 0;      // simulator budget of the chosen candidate (<= arena capacity)
   bool refined = false, plan_refined = false;  // the plan came out of the local refinement (Reading 42)
+  // the step captured as one CUDA graph (re-captured when the plan, streams or lr change)
+  uint64_t plan_version = 0, graph_version = ~0ull;
+  float graph_lr = 0.f;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool graphs_off = false;
+  cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
   std::vector<pooch::Op> ops;
   std::vector<pooch::ProgTask> program;
   std::vector<int> first_writer;  // per map: task whose bwd writes (not accumulates) its gradient

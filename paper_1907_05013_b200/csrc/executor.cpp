@@ -619,8 +619,13 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
   return POOCH_OK;
 }
 
+static void drop_graph(pooch_ctx* c);
+
 extern "C" void pooch_destroy(pooch_ctx* c) {
   if (!c) return;
+  drop_graph(c);
+  for (cudaEvent_t e : c->ev_join)
+    if (e) cudaEventDestroy(e);
   for (auto e : c->ev) cudaEventDestroy(e);
   for (auto e : c->ev_start) cudaEventDestroy(e);
   for (auto e : c->tev) cudaEventDestroy(e);
@@ -665,6 +670,7 @@ extern "C" pooch_status pooch_set_budget(pooch_ctx* c, void* dev_base, size_t de
 
 extern "C" pooch_status pooch_set_streams(pooch_ctx* c, void* compute, void* d2h, void* h2d, void* comm) {
   if (!c || !compute || !d2h || !h2d) return fail(POOCH_EUSAGE, "compute, d2h and h2d streams are required");
+  c->plan_version++;  // a captured step graph belongs to the old streams
   c->s[0] = (cudaStream_t)compute;
   c->s[1] = (cudaStream_t)d2h;
   c->s[2] = (cudaStream_t)h2d;
@@ -1431,6 +1437,7 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
     c->ev_start.push_back(e);
   }
   c->have_plan = true;
+  c->plan_version++;
   c->plan_budget = best.budget;
   if (report) {
     *report = best.rep;
@@ -1596,13 +1603,75 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
   return POOCH_OK;
 }
 
+// The copy / comm streams rejoin the compute stream at the end of a step (a captured graph
+// must end joined; eagerly it makes every step a closed unit).
+static pooch_status join_streams(pooch_ctx* c) {
+  for (int k = 1; k <= 3; ++k) {
+    cudaStream_t s = k == 3 ? (c->nccl ? comm_stream(c) : nullptr) : c->s[k];
+    if (!s) continue;
+    if (!c->ev_join[k - 1]) POOCH_CUDA(cudaEventCreateWithFlags(&c->ev_join[k - 1], cudaEventDisableTiming));
+    POOCH_CUDA(cudaEventRecord(c->ev_join[k - 1], s));
+    POOCH_CUDA(cudaStreamWaitEvent(c->s[0], c->ev_join[k - 1], 0));
+  }
+  return POOCH_OK;
+}
+
+static void drop_graph(pooch_ctx* c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  c->gexec = nullptr;
+  c->graph = nullptr;
+  c->graph_version = ~0ull;
+}
+
+// One step as a CUDA graph (captured once per plan / lr): the ~650 kernels, ~20 copies and the
+// event edges of a step are replayed without per-launch host work. Any capture failure turns
+// graphs off for this context and the step runs eagerly (same kernels, same order).
+static pooch_status graph_step(pooch_ctx* c, float lr) {
+  if (!c->gexec || c->graph_version != c->plan_version || c->graph_lr != lr) {
+    drop_graph(c);
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(c->s[0], &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return POOCH_ECUDA;
+    if (cudaStreamBeginCapture(c->s[0], cudaStreamCaptureModeThreadLocal) != cudaSuccess) return POOCH_ECUDA;
+    pooch_status st = step_impl(c, lr, true);
+    if (st == POOCH_OK) st = join_streams(c);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->s[0], &g);
+    if (st != POOCH_OK || e != cudaSuccess || !g) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return POOCH_ECUDA;
+    }
+    if (cudaGraphInstantiate(&c->gexec, g, 0) != cudaSuccess) {
+      cudaGraphDestroy(g);
+      cudaGetLastError();
+      c->gexec = nullptr;
+      return POOCH_ECUDA;
+    }
+    c->graph = g;
+    c->graph_version = c->plan_version;
+    c->graph_lr = lr;
+  }
+  POOCH_CUDA(cudaGraphLaunch(c->gexec, c->s[0]));
+  return POOCH_OK;
+}
+
 extern "C" pooch_status pooch_train_step(pooch_ctx* c, float lr, float* loss_host) {
   if (!c) return fail(POOCH_EUSAGE, "null context");
   if (!c->have_plan) return ctx_fail(c, fail(POOCH_ENOPLAN, "no current plan (call pooch_plan)"));
   if (!c->s[0]) return ctx_fail(c, fail(POOCH_EUSAGE, "streams not set"));
   POOCH_CUDA(cudaSetDevice(c->device));
-  pooch_status st = step_impl(c, lr, true);
-  if (st != POOCH_OK) return ctx_fail(c, st);
+  static const bool no_graph = getenv("POOCH_NO_GRAPH") != nullptr;
+  bool done = false;
+  if (!c->timing && !no_graph && !c->graphs_off) {
+    if (graph_step(c, lr) == POOCH_OK) done = true;
+    else c->graphs_off = true;  // e.g. a stream the capture cannot follow: run eagerly from now on
+  }
+  if (!done) {
+    pooch_status st = step_impl(c, lr, true);
+    if (st == POOCH_OK) st = join_streams(c);
+    if (st != POOCH_OK) return ctx_fail(c, st);
+  }
   c->step_count++;
   if (loss_host) {
     POOCH_CUDA(cudaMemcpyAsync(loss_host, fptr(c, c->off_loss), 4, cudaMemcpyDeviceToHost, c->s[0]));

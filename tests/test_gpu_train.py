@@ -214,3 +214,24 @@ def test_bucketed_allreduce_one_rank_is_identity(net):
     assert out[0][0] == out[1][0]
     for a, b in zip(out[0][1] + out[0][2], out[1][1] + out[1][2]):
         assert np.array_equal(a, b)
+
+
+def test_graph_replay_bit_identical_to_eager(tiny):
+    """pooch_train_step replays the step as a captured CUDA graph; the instrumented (eager) step
+    runs the same kernels in the same order, so loss, gradients and updated weights agree bit for
+    bit -- for the step that captures the graph and for a later replay of it from the same state."""
+    ctx = tiny["ctx"]
+    _put_batch(ctx, tiny["x"], tiny["t"])
+    ctx.plan("pooch")
+    runs = []
+    for timing in (True, False, False):             # eager, capture + launch, replay
+        ctx.set_timing(timing)
+        load_params(ctx, tiny["params"])
+        loss = ctx.train_step(LR)
+        torch.cuda.synchronize()
+        runs.append((np.float32(loss).view(np.uint32), _grads_bits(ctx) + _params_bits(ctx)))
+    ctx.set_timing(False)
+    for loss, bits in runs[1:]:
+        assert loss == runs[0][0]
+        for a, b in zip(bits, runs[0][1]):
+            assert np.array_equal(a, b)
