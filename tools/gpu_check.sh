@@ -1,4 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 1500 python bench.py --dump-profile gpurun_out/profile_cfg2k.json > gpurun_out/bench_cfg2k.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_cfg2k.log
+timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ref_arm.log 2>&1; echo "rc=$?" >> gpurun_out/ref_arm.log
+/usr/bin/time -v timeout 1500 python bench.py --gpus 1 --steps 5 --warmup 3 > gpurun_out/bench_default.log 2> gpurun_out/bench_default.err; echo "rc=$?" >> gpurun_out/bench_default.log
