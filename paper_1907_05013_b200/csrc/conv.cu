@@ -45,18 +45,20 @@ bool conv_shape_ok(const ConvGeom& g) {
 
 static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
-template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false>
+template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr,
                                  const CUtensorMap* td = nullptr) {
   // deepest ring that fits 227 KB next to the epilogue staging / reduction buffers: a k-block's
   // MMAs take only 0.2-0.4 us, less than the TMA -> (3xTF32 split / wgrad transpose) -> MMA
   // latency, so the ring depth sets the throughput of the short-K and narrow (BN = 64) layers
-  constexpr int STAGE_B = (BM + BN) * BK * 4 * (X3 ? 2 : 1);
-  constexpr int FIXED_B = GemmSmem<BN, 1, X3>::TOTAL - STAGE_B + 64;
-  constexpr int STAGES = std::max(2, std::min(8, (227 * 1024 - FIXED_B) / STAGE_B));
-  constexpr int SMEM = GemmSmem<BN, STAGES, X3>::TOTAL;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF>;
+  constexpr int STAGE_B = GemmSmem<BN, 1, X3, AT>::STAGE_BYTES;
+  constexpr int FIXED_B = GemmSmem<BN, 1, X3, AT>::TOTAL - STAGE_B + 64;
+  constexpr int STAGES_SM = std::max(2, std::min(8, (227 * 1024 - FIXED_B) / STAGE_B));
+  // AT: each stage also holds 64 TMEM columns (A hi / lo) next to the two accumulators
+  constexpr int STAGES = AT ? std::min(STAGES_SM, (512 - 2 * BN) / 64) : STAGES_SM;
+  constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT>::TOTAL;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -71,6 +73,12 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
                                                           tc ? *tc : g_zero_map, td ? *td : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
+}
+
+// 3xTF32 TMA fwd / dgrad with the A operand in TMEM (POOCH_A_TMEM=0 disables)
+static bool a_in_tmem() {
+  static int on = getenv("POOCH_A_TMEM") ? atoi(getenv("POOCH_A_TMEM")) : 1;
+  return on != 0;
 }
 
 template <int MODE, bool TMA = false>
@@ -97,6 +105,14 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
     if (p.xf_scale) return fail(POOCH_EUSAGE, "BN-ReLU on load needs the TMA-fed fwd / wgrad kernels");
   }
   if (prec) {
+    if constexpr (TMA && (MODE == CONV_FWD || MODE == CONV_DGRAD)) {
+      if (a_in_tmem() && !p.stem4) {
+        switch (bn) {
+          case 64: return launch_igemm<MODE, 64, true, true, false, true>(p, grid, st, ta, tb, tc, td);
+          case 128: return launch_igemm<MODE, 128, true, true, false, true>(p, grid, st, ta, tb, tc, td);
+        }
+      }
+    }
     switch (bn) {
       case 64: return launch_igemm<MODE, 64, true, TMA>(p, grid, st, ta, tb, tc, td);
       case 128: return launch_igemm<MODE, 128, true, TMA>(p, grid, st, ta, tb, tc, td);

@@ -96,13 +96,15 @@ constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per k-block (128 B per row)
 constexpr int NUM_THREADS = 160;
 
-template <int BN, int STAGES, bool X3 = false>
+template <int BN, int STAGES, bool X3 = false, bool AT = false>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
-  // 3xTF32: the stage also holds the residuals As = A - tf32(A), Bs = B - tf32(B)
-  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
+  // 3xTF32: the stage also holds the residuals As = A - tf32(A), Bs = B - tf32(B) (AT: As lives
+  // in TMEM, the stage is [A][B][Bs])
+  static constexpr int STAGE_BYTES = AT ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
   static constexpr int SMALL_OFF = A_BYTES + B_BYTES;
+  static constexpr int BS_OFF = AT ? B_BYTES : SMALL_OFF;  // Bs relative to the B tile
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int RED_OFF = BAR_OFF + (3 * STAGES + 4) * 8 + 16;
   // epilogue staging: per epilogue warp one 32 x 32 fp32 block (4 KB); together the 128 x 32
@@ -447,7 +449,7 @@ struct TileMap {
   }
 };
 
-template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false>
+template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
@@ -455,8 +457,15 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
   // TMA tiles whose M rows are a box of output pixels (FWD / DGRAD); TMA wgrad boxes pixels along K
   constexpr bool PIXM = TMA && MODE != CONV_WGRAD;
   static_assert(!XF || (TMA && (MODE == CONV_FWD || MODE == CONV_WGRAD)), "XF: TMA-fed fwd / wgrad only");
+  // AT: 3xTF32 with the A operand in TMEM -- the auxiliary warps move each stage's A tile (hi =
+  // trunc_tf32(a), lo = a - hi) from shared memory into TMEM, so the three MMAs of a k-step read
+  // only B / Bs from shared memory (A is re-read by every MMA, the dominant smem traffic at BN = 64)
+  static_assert(!AT || (X3 && TMA && !XF && (MODE == CONV_FWD || MODE == CONV_DGRAD)), "AT: 3xTF32 TMA fwd / dgrad");
+  static_assert(!AT || 2 * BN + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
+  constexpr uint32_t TMEM_COLS = AT ? 512u : 2u * BN;
+  constexpr uint32_t A_TCOL = 2u * BN;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
   constexpr bool AUX = igemm_aux(MODE, X3, XF);
-  using SM = GemmSmem<BN, STAGES, X3>;
+  using SM = GemmSmem<BN, STAGES, X3, AT>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
@@ -496,7 +505,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&rawfull[s], TMA ? 1 : 128);
     ptx::fence_mbar_init();
   }
-  if (warp == 8) ptx::tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 8) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -797,6 +806,34 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
             uint32_t tile = st + (q < 2 ? 0 : SM::A_BYTES);
             transpose_block<X3>(tile + kmaj_off<128>(4 * g, j), (stid >> 1) & 3, SM::SMALL_OFF);
           }
+        } else if constexpr (AT) {
+          // A: warp w moves rows 32 (w % 4) .. +31 (its TMEM lane quadrant): lane = row, the row's 32
+          // k-values from the SWIZZLE_128B tile, then hi / lo into this stage's TMEM columns
+          {
+            const int row = 32 * (warp & 3) + lane;
+            float v[32], lo[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
+                           : "r"(st + row * 128 + ((j ^ (row & 7)) << 4)));
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float hi = __uint_as_float(__float_as_uint(v[i]) & 0xFFFFE000u);
+              lo[i] = v[i] - hi;
+              v[i] = hi;
+            }
+            const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + A_TCOL + 64u * s;
+            ptx::tmem_st32(ta, v);
+            ptx::tmem_st32(ta + 32, lo);
+          }
+          // B: residuals in shared memory, as in the plain 3xTF32 path
+          constexpr int BCH = BN * BK / 4;
+#pragma unroll 4
+          for (int c = stid; c < BCH; c += 128)
+            split_chunk(st + SM::A_BYTES + c * 16, st + SM::A_BYTES + SM::BS_OFF + c * 16);
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
         } else {
           constexpr int CHUNKS = (BM + BN) * BK / 4;  // 16-B chunks of A and B (contiguous)
 #pragma unroll 4
@@ -836,7 +873,14 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
             const uint32_t la = sw ? 16 : A_LBO, lb = sw ? 16 : B_LBO, sbo = sw ? 1024 : 128, lay = sw ? 2 : 0;
             uint64_t ad = ptx::smem_desc(sa + ka, la, sbo, lay);
             uint64_t bd = ptx::smem_desc(sb + kbo, lb, sbo, lay);
-            if constexpr (X3) {  // small terms first, then the big product
+            if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs from smem
+              const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
+              uint64_t bsd = ptx::smem_desc(sb + SM::BS_OFF + kbo, lb, sbo, lay);
+              ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+              ptx::mma_tf32_ts(acc, ta, bsd, IDESC, 1u);
+              ptx::mma_tf32_ts(acc, ta, bd, IDESC, 1u);
+              (void)ad;
+            } else if constexpr (X3) {  // small terms first, then the big product
               uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + ka, la, sbo, lay);
               uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + kbo, lb, sbo, lay);
               ptx::mma_tf32(acc, asd, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
@@ -1059,7 +1103,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
   __syncthreads();
   if (warp == 8) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 2 * BN);
+    ptx::tmem_dealloc(tmem, TMEM_COLS);
   }
 }
 

@@ -1,5 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ref_arm.log 2>&1; echo "rc=$?" >> gpurun_out/ref_arm.log
-/usr/bin/time -v timeout 1500 python bench.py --gpus 1 --steps 5 --warmup 3 > gpurun_out/bench_default.log 2> gpurun_out/bench_default.err; echo "rc=$?" >> gpurun_out/bench_default.log
+timeout 600 python -m pytest tests/test_gpu_ops.py -x -q > gpurun_out/pytest_ops.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_ops.log
+B=256 timeout 600 python tools/kbench_r50.py > gpurun_out/kb_r50_at.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1500 python bench.py --dump-profile gpurun_out/profile_cfg2l.json > gpurun_out/bench_cfg2l.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_cfg2l.log
