@@ -105,8 +105,10 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
     if (p.xf_scale) return fail(POOCH_EUSAGE, "BN-ReLU on load needs the TMA-fed fwd / wgrad kernels");
   }
   if (prec) {
-    if constexpr (TMA && (MODE == CONV_FWD || MODE == CONV_DGRAD)) {
-      if (a_in_tmem() && !p.stem4) {
+    if constexpr (TMA && MODE != GEMM_TEST) {
+      // wgrad: A in TMEM pays off at BN = 128 (stages 2-4: 3-12 % faster) but not at BN = 64
+      // (stage 1, 6-9 % slower: the extra read-back of the transposed A blocks)
+      if (a_in_tmem() && !p.stem4 && (MODE != CONV_WGRAD || bn == 128)) {
         switch (bn) {
           case 64: return launch_igemm<MODE, 64, true, true, false, true>(p, grid, st, ta, tb, tc, td);
           case 128: return launch_igemm<MODE, 128, true, true, false, true>(p, grid, st, ta, tb, tc, td);

@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
   // AT: 3xTF32 with the A operand in TMEM -- the auxiliary warps move each stage's A tile (hi =
   // trunc_tf32(a), lo = a - hi) from shared memory into TMEM, so the three MMAs of a k-step read
   // only B / Bs from shared memory (A is re-read by every MMA, the dominant smem traffic at BN = 64)
-  static_assert(!AT || (X3 && TMA && !XF && (MODE == CONV_FWD || MODE == CONV_DGRAD)), "AT: 3xTF32 TMA fwd / dgrad");
+  static_assert(!AT || (X3 && TMA && !XF && MODE != GEMM_TEST), "AT: 3xTF32 TMA fwd / dgrad / wgrad");
   static_assert(!AT || 2 * BN + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
   constexpr uint32_t TMEM_COLS = AT ? 512u : 2u * BN;
   constexpr uint32_t A_TCOL = 2u * BN;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
@@ -759,7 +759,40 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
         }
         ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
-        if constexpr (MODE == CONV_WGRAD && TMA) {
+        if constexpr (MODE == CONV_WGRAD && TMA && AT) {
+          // A in TMEM: warp w owns A block w & 3 (its TMEM lane quadrant): transpose it in place,
+          // read its rows back (lane = row) and store hi / lo into this stage's TMEM columns; the B
+          // blocks are transposed with their residuals into [B][Bs] as usual
+#pragma unroll
+          for (int q = 0; q < WQ; ++q) {
+            const int bi = (warp & 3) + 4 * q;
+            if (bi >= (BM + BN) / 32) break;
+            if (bi < BM / 32) {
+              const uint32_t blk = st + bi * 4096;
+              transpose32<false>(blk, lane, 0);
+              __syncwarp();
+              float v[32], lo[32];
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
+                             : "r"(blk + lane * 128 + ((j ^ (lane & 7)) << 4)));
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float hi = __uint_as_float(__float_as_uint(v[i]) & 0xFFFFE000u);
+                lo[i] = v[i] - hi;
+                v[i] = hi;
+              }
+              const uint32_t ta = tmem + ((uint32_t)(32 * bi) << 16) + A_TCOL + 64u * s;
+              ptx::tmem_st32(ta, v);
+              ptx::tmem_st32(ta + 32, lo);
+            } else {
+              transpose32<true>(st + bi * 4096, lane, SM::BS_OFF);
+            }
+          }
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+        } else if constexpr (MODE == CONV_WGRAD && TMA) {
           // (BM + BN) / 32 TMA boxes, A's then B's, 4 KB each; residuals at the same offsets + SMALL_OFF
 #pragma unroll
           for (int q = 0; q < WQ; ++q) {
