@@ -52,13 +52,16 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   // deepest ring that fits 227 KB next to the epilogue staging / reduction buffers: a k-block's
   // MMAs take only 0.2-0.4 us, less than the TMA -> (3xTF32 split / wgrad transpose) -> MMA
   // latency, so the ring depth sets the throughput of the short-K and narrow (BN = 64) layers
-  constexpr int STAGE_B = GemmSmem<BN, 1, X3, AT>::STAGE_BYTES;
-  constexpr int FIXED_B = GemmSmem<BN, 1, X3, AT>::TOTAL - STAGE_B + 64;
+  // AT fwd / dgrad: two epilogue staging images (the TMA store of one column chunk overlaps the
+  // staging of the next; more than 3-4 ring stages measured no faster, so the smem goes here)
+  constexpr int NSTG = (AT && MODE != CONV_WGRAD) ? 2 : 1;
+  constexpr int STAGE_B = GemmSmem<BN, 1, X3, AT, NSTG>::STAGE_BYTES;
+  constexpr int FIXED_B = GemmSmem<BN, 1, X3, AT, NSTG>::TOTAL - STAGE_B + 64;
   constexpr int STAGES_SM = std::max(2, std::min(8, (227 * 1024 - FIXED_B) / STAGE_B));
   // AT: each stage also holds 64 TMEM columns (A hi / lo) next to the two accumulators
   constexpr int STAGES = AT ? std::min(STAGES_SM, (512 - 2 * BN) / 64) : STAGES_SM;
-  constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT>::TOTAL;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT>;
+  constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT, NSTG>::TOTAL;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));

@@ -96,7 +96,7 @@ constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per k-block (128 B per row)
 constexpr int NUM_THREADS = 160;
 
-template <int BN, int STAGES, bool X3 = false, bool AT = false>
+template <int BN, int STAGES, bool X3 = false, bool AT = false, int NSTG = 1>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
@@ -110,7 +110,8 @@ struct GemmSmem {
   // epilogue staging: per epilogue warp one 32 x 32 fp32 block (4 KB); together the 128 x 32
   // SWIZZLE_128B image of one column chunk of the tile (1024-B aligned for the TMA store)
   static constexpr int STG_OFF = (RED_OFF + 4 * BN * 4 * 2 + 1023) / 1024 * 1024;
-  static constexpr int TOTAL = STG_OFF + 4 * 4096 + 1024;
+  // NSTG = 2: two staging images, so a column chunk is staged while the TMA still reads the last
+  static constexpr int TOTAL = STG_OFF + NSTG * 4 * 4096 + 1024;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -449,7 +450,8 @@ struct TileMap {
   }
 };
 
-template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false>
+template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false,
+          int NSTG = 1>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
@@ -465,7 +467,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
   constexpr uint32_t TMEM_COLS = AT ? 512u : 2u * BN;
   constexpr uint32_t A_TCOL = 2u * BN;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
   constexpr bool AUX = igemm_aux(MODE, X3, XF);
-  using SM = GemmSmem<BN, STAGES, X3, AT>;
+  using SM = GemmSmem<BN, STAGES, X3, AT, NSTG>;
   constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
@@ -937,6 +939,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
     // ------------------------------------------------------------------ epilogue
     const int row = warp * 32 + lane;
     int j = 0;
+    uint32_t chunk_seq = 0;  // column chunks staged so far (selects the staging image when NSTG = 2)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
       int m0, n0, kb0, nkb;
       tm.decode(t, m0, n0, kb0, nkb, BN);
@@ -1018,9 +1021,14 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
           // pieces. DGRAD accumulation loads all eight old segments before adding (same fp32 add).
           // With p.tma_store the four warps' blocks form the tile's 128 x 32 SWIZZLE_128B image and
           // one thread hands it to the TMA (a plain store, or an fp32 add-reduce for accumulation).
-          const uint32_t stg = sbase + SM::STG_OFF + warp * 4096;
-          if (p.tma_store) {  // the previous chunk's TMA store must have read the staging buffer
-            if (tid == 0) ptx::bulk_wait_read0();
+          const uint32_t img = sbase + SM::STG_OFF + (NSTG == 2 ? (chunk_seq & 1u) * 16384u : 0u);
+          ++chunk_seq;
+          const uint32_t stg = img + warp * 4096;
+          if (p.tma_store) {  // the TMA store that last used this staging image must have read it
+            if (tid == 0) {
+              if constexpr (NSTG == 2) ptx::bulk_wait_read1();
+              else ptx::bulk_wait_read0();
+            }
             asm volatile("bar.sync 2, 128;" ::: "memory");
           }
 #pragma unroll
@@ -1033,7 +1041,6 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
             ptx::fence_proxy_async_smem();
             asm volatile("bar.sync 2, 128;" ::: "memory");
             if (tid == 0) {
-              const uint32_t img = sbase + SM::STG_OFF;
               if (p.tma_store == 1) {
                 const int mt_i = m0 / BM;
                 const int tw_i = mt_i % p.tiles_w, th_i = (mt_i / p.tiles_w) % p.tiles_h, tn_i = mt_i / (p.tiles_w * p.tiles_h);
