@@ -150,6 +150,11 @@ struct KLoader {
   int nimg[RPT];
   bool valid[RPT];
   int lane, warp;
+  // FWD-A with C < 32 (the stem): the tap (tr, ts) and channel tc of this thread's two 16-B
+  // chunk columns for k-block cur, advanced incrementally (32 / C taps per k-block) instead of
+  // re-deriving them with runtime divisions every k-block
+  int tr[2], ts[2], tc[2];
+  int cur = -2;
 
   __device__ void init(const GemmParams& p, int row0, int tid) {
     warp = tid >> 5;
@@ -205,6 +210,46 @@ struct KLoader {
   }
 
   __device__ void load(const GemmParams& p, uint32_t sbase, int kb) {
+    if constexpr (IS_A && MODE == CONV_FWD) {
+      if (p.C < BK && BK % p.C == 0) {
+        if (kb == cur + 1) {  // next k-block: 32 / C more taps (at most a couple of row wraps)
+          const int adv = BK / p.C;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ts[h] += adv;
+            while (ts[h] >= p.S) {
+              ts[h] -= p.S;
+              ++tr[h];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int kk = kb * BK + ((lane >> 3) + 4 * h) * 4;
+            const int rs = kk / p.C;
+            tc[h] = kk - rs * p.C;
+            tr[h] = rs / p.S;
+            ts[h] = rs - tr[h] * p.S;
+          }
+        }
+        cur = kb;
+        const int WC = p.W * p.C;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = (lane >> 3) + 4 * h;
+          const bool kok = tr[h] < p.R * p.T;  // taps past R*S are the K padding of the last k-block
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const int hi = hi0[i] + tr[h], wi = wi0[i] + ts[h];
+            const bool ok = kok && valid[i] && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W;
+            const float* src = ok ? rowp[i] + (hi * WC + wi * p.C + tc[h]) : p.a;
+            const int row = warp * (ROWS / 4) + i * 8 + (lane & 7);
+            ptx::cp_async16(sbase + kmaj_off<ROWS>(row, j), src, ok ? 16 : 0);
+          }
+        }
+        return;
+      }
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       int j = (lane >> 3) + 4 * h;
