@@ -369,12 +369,18 @@ def our_arm(args):
     ablation = None
     if args.ablation:
         ablation = {}
-        for strat in ("swap_all_naive", "swap_all", "swap_opt", "superneurons", "pooch"):
+        # the paper's strategies (Sec. 5.1-5.2) on the same executor; "pooch_paper" is PoocH
+        # without the executor's local refinement (DESIGN.md Reading 42), "pooch" with it
+        for strat in ("swap_all_naive", "swap_all", "swap_opt", "superneurons", "pooch_paper", "pooch"):
             try:
-                c2, r2 = ctx.plan(strat, li_cap=args.li_cap)
+                if strat == "pooch_paper":
+                    os.environ["POOCH_PLAN_NO_REFINE"] = "1"
+                c2, r2 = ctx.plan("pooch" if strat == "pooch_paper" else strat, li_cap=args.li_cap)
             except Exception as e:  # infeasible plans are a result (superneurons OOM)
                 ablation[strat] = {"feasible": False, "why": str(e)[:160]}
                 continue
+            finally:
+                os.environ.pop("POOCH_PLAN_NO_REFINE", None)
             ctx.train_step(0.01, sync_loss=False)
             ms_s = timed(2)
             ablation[strat] = {"feasible": True, "ms_per_step": ms_s, "images_per_s": batch * world * 1000.0 / ms_s,

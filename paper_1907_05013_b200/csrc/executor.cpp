@@ -1234,8 +1234,11 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
   if (grid && strategy == POOCH_STRAT_POOCH)
     for (int lc = 3; lc < sc.li_cap; ++lc) caps.push_back(lc);
   caps.push_back(sc.li_cap);
-  const int steps = grid ? (getenv("POOCH_PLAN_STEPS") ? std::max(1, atoi(getenv("POOCH_PLAN_STEPS"))) : 16) : 12;
-  const uint64_t step_bytes = grid ? std::max<uint64_t>(cap / 250, 1) : std::max<uint64_t>(cap / 50, 1);
+  // PoocH: 0.4 % budget steps over 6 %; the other strategies (whose classification barely moves
+  // with the budget, e.g. all-swap) step 2 % at a time down to -24 % until their ledger packs
+  const bool fine = grid && strategy == POOCH_STRAT_POOCH;
+  const int steps = fine ? (getenv("POOCH_PLAN_STEPS") ? std::max(1, atoi(getenv("POOCH_PLAN_STEPS"))) : 16) : 12;
+  const uint64_t step_bytes = fine ? std::max<uint64_t>(cap / 250, 1) : std::max<uint64_t>(cap / 50, 1);
 
   struct Cand {
     uint64_t budget = 0;
