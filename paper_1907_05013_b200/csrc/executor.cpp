@@ -1343,11 +1343,15 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
                                         : (cands[x].step != cands[y].step ? cands[x].step < cands[y].step
                                                                           : cands[x].li_cap < cands[y].li_cap);
     });
-    std::vector<std::vector<uint8_t>> tried;
+    // the same classification at another budget is another candidate (the simulator's eager
+    // swap-in gating, hence the ledger, depends on the budget); at most 32 packing attempts
+    std::vector<std::pair<std::vector<uint8_t>, uint64_t>> tried;
     int adopted = -1;
     for (int i : order) {
-      if (std::find(tried.begin(), tried.end(), cands[i].cls) != tried.end()) continue;
-      tried.push_back(cands[i].cls);
+      const std::pair<std::vector<uint8_t>, uint64_t> key{cands[i].cls, cands[i].budget};
+      if (std::find(tried.begin(), tried.end(), key) != tried.end()) continue;
+      if (tried.size() >= 32) break;
+      tried.push_back(key);
       if (adopt(cands[i])) {
         adopted = i;
         break;
