@@ -319,20 +319,40 @@ __global__ void bn_bwd_apply_kernel(BnBwdArgs p, const float* __restrict__ coef,
 // 2D max-pool. One block per output row (n, ho) (backward: per input row (n, h)); threads
 // stride the row's (w, 4-channel group) pairs, so all index math is 32-bit and division-free
 // except one per element by C4 (a power of two in every network here).
+// K, S > 0: window / stride fixed at compile time (ResNet's 3x3 / 2; the loops unroll and the
+// divisions by the stride become shifts); 0: runtime k, s. cs >= 0: C4 = 1 << cs (j / C4 and
+// j % C4 are a shift and a mask), else a division.
+__device__ __forceinline__ void split_j(int j, int C4, int cs, int& c4, int& q) {
+  if (cs >= 0) {
+    c4 = j & (C4 - 1);
+    q = j >> cs;
+  } else {
+    c4 = j % C4;
+    q = j / C4;
+  }
+}
+
+template <int K, int S>
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int N, int H, int W, int C4,
-                                   int k, int s, int p, int Ho, int Wo) {
+                                   int cs, int k_, int s_, int p, int Ho, int Wo) {
+  const int k = K ? K : k_, s = S ? S : s_;
   const int ho = blockIdx.x % Ho, n = blockIdx.x / Ho;
   const float4* xn = reinterpret_cast<const float4*>(x) + (size_t)n * H * W * C4;
   float4* yr = reinterpret_cast<float4*>(y) + ((size_t)n * Ho + ho) * Wo * C4;
   const int h0 = ho * s - p;
   for (int j = threadIdx.x; j < Wo * C4; j += blockDim.x) {
-    const int c4 = j % C4, wo = j / C4;
+    int c4, wo;
+    split_j(j, C4, cs, c4, wo);
     const int w0 = wo * s - p;
     float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-    for (int u = 0; u < k; ++u) {
+#pragma unroll
+    for (int u = 0; u < (K ? K : 8); ++u) {
+      if (!K && u >= k) break;
       const int h = h0 + u;
       if (h < 0 || h >= H) continue;
-      for (int v = 0; v < k; ++v) {
+#pragma unroll
+      for (int v = 0; v < (K ? K : 8); ++v) {
+        if (!K && v >= k) break;
         const int w = w0 + v;
         if (w < 0 || w >= W) continue;
         float4 q = __ldg(xn + (h * W + w) * C4 + c4);
@@ -344,21 +364,28 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restric
 }
 
 // window argmax (first maximum in row-major order; -inf padding never wins) -> u*k+v per channel
+template <int K, int S>
 __global__ void maxpool_arg_kernel(const float* __restrict__ x, uint8_t* __restrict__ arg, int N, int H, int W,
-                                   int C4, int k, int s, int p, int Ho, int Wo) {
+                                   int C4, int cs, int k_, int s_, int p, int Ho, int Wo) {
+  const int k = K ? K : k_, s = S ? S : s_;
   const int ho = blockIdx.x % Ho, n = blockIdx.x / Ho;
   const float4* xn = reinterpret_cast<const float4*>(x) + (size_t)n * H * W * C4;
   uchar4* ar = reinterpret_cast<uchar4*>(arg) + ((size_t)n * Ho + ho) * Wo * C4;
   const int h0 = ho * s - p;
   for (int j = threadIdx.x; j < Wo * C4; j += blockDim.x) {
-    const int c4 = j % C4, wo = j / C4;
+    int c4, wo;
+    split_j(j, C4, cs, c4, wo);
     const int w0 = wo * s - p;
     float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     uint8_t a[4] = {255, 255, 255, 255};
-    for (int u = 0; u < k; ++u) {
+#pragma unroll
+    for (int u = 0; u < (K ? K : 8); ++u) {
+      if (!K && u >= k) break;
       const int h = h0 + u;
       if (h < 0 || h >= H) continue;
-      for (int v = 0; v < k; ++v) {
+#pragma unroll
+      for (int v = 0; v < (K ? K : 8); ++v) {
+        if (!K && v >= k) break;
         const int w = w0 + v;
         if (w < 0 || w >= W) continue;
         float4 q = __ldg(xn + (h * W + w) * C4 + c4);
@@ -376,16 +403,19 @@ __global__ void maxpool_arg_kernel(const float* __restrict__ x, uint8_t* __restr
   }
 }
 
+template <int K, int S>
 __global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ gy,
-                                   float* __restrict__ gx, int N, int H, int W, int C4, int k, int s, int p, int Ho,
-                                   int Wo) {
+                                   float* __restrict__ gx, int N, int H, int W, int C4, int cs, int k_, int s_, int p,
+                                   int Ho, int Wo) {
+  const int k = K ? K : k_, s = S ? S : s_;
   const int h = blockIdx.x % H, n = blockIdx.x / H;
   const uchar4* an = reinterpret_cast<const uchar4*>(arg) + (size_t)n * Ho * Wo * C4;
   const float4* gn = reinterpret_cast<const float4*>(gy) + (size_t)n * Ho * Wo * C4;
   float4* gr = reinterpret_cast<float4*>(gx) + ((size_t)n * H + h) * W * C4;
   const int ho_lo = max(0, (h + p - k + s) / s), ho_hi = min(Ho - 1, (h + p) / s);
   for (int j = threadIdx.x; j < W * C4; j += blockDim.x) {
-    const int c4 = j % C4, w = j / C4;
+    int c4, w;
+    split_j(j, C4, cs, c4, w);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     const int wo_lo = max(0, (w + p - k + s) / s), wo_hi = min(Wo - 1, (w + p) / s);
     for (int ho = ho_lo; ho <= ho_hi; ++ho) {
@@ -715,8 +745,12 @@ pooch_status bn_bwd(const BnBwdArgs& a, float* ws, cudaStream_t st) {
 pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, int k, int s, int p, int Ho, int Wo,
                          cudaStream_t st) {
   if (C % 4 || (int64_t)H * W * C >= (1LL << 31)) return fail(POOCH_EUSAGE, "max-pool: C %% 4 != 0 or image too large");
+  if (k > 8) return fail(POOCH_EUSAGE, "max-pool window > 8");
+  const int C4 = C / 4, cs = (C4 & (C4 - 1)) == 0 ? __builtin_ctz(C4) : -1;
   count_launch();
-  maxpool_fwd_kernel<<<N * Ho, 256, 0, st>>>(x, y, N, H, W, C / 4, k, s, p, Ho, Wo);
+  if (k == 3 && s == 2) maxpool_fwd_kernel<3, 2><<<N * Ho, 256, 0, st>>>(x, y, N, H, W, C4, cs, k, s, p, Ho, Wo);
+  else if (k == 2 && s == 2) maxpool_fwd_kernel<2, 2><<<N * Ho, 256, 0, st>>>(x, y, N, H, W, C4, cs, k, s, p, Ho, Wo);
+  else maxpool_fwd_kernel<0, 0><<<N * Ho, 256, 0, st>>>(x, y, N, H, W, C4, cs, k, s, p, Ho, Wo);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
@@ -724,10 +758,20 @@ pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, i
 pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* arg_ws, int N, int H, int W, int C,
                          int k, int s, int p, int Ho, int Wo, cudaStream_t st) {
   if (C % 4 || (int64_t)H * W * C >= (1LL << 31)) return fail(POOCH_EUSAGE, "max-pool: C %% 4 != 0 or image too large");
+  if (k > 8) return fail(POOCH_EUSAGE, "max-pool window > 8");
+  const int C4 = C / 4, cs = (C4 & (C4 - 1)) == 0 ? __builtin_ctz(C4) : -1;
   count_launch();
-  maxpool_arg_kernel<<<N * Ho, 256, 0, st>>>(x, arg_ws, N, H, W, C / 4, k, s, p, Ho, Wo);
   count_launch();
-  maxpool_bwd_kernel<<<N * H, 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C / 4, k, s, p, Ho, Wo);
+  if (k == 3 && s == 2) {
+    maxpool_arg_kernel<3, 2><<<N * Ho, 256, 0, st>>>(x, arg_ws, N, H, W, C4, cs, k, s, p, Ho, Wo);
+    maxpool_bwd_kernel<3, 2><<<N * H, 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C4, cs, k, s, p, Ho, Wo);
+  } else if (k == 2 && s == 2) {
+    maxpool_arg_kernel<2, 2><<<N * Ho, 256, 0, st>>>(x, arg_ws, N, H, W, C4, cs, k, s, p, Ho, Wo);
+    maxpool_bwd_kernel<2, 2><<<N * H, 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C4, cs, k, s, p, Ho, Wo);
+  } else {
+    maxpool_arg_kernel<0, 0><<<N * Ho, 256, 0, st>>>(x, arg_ws, N, H, W, C4, cs, k, s, p, Ho, Wo);
+    maxpool_bwd_kernel<0, 0><<<N * H, 256, 0, st>>>(arg_ws, gy, gx, N, H, W, C4, cs, k, s, p, Ho, Wo);
+  }
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
 }
