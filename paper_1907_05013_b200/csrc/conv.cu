@@ -91,6 +91,14 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
   if constexpr (TMA && (MODE == CONV_FWD || MODE == CONV_WGRAD)) {
     if (p.xf_scale) {  // BN-ReLU on load
       if (prec) {
+        if constexpr (MODE == CONV_FWD) {  // the A operand (rebuilt on load) goes to TMEM
+          if (a_in_tmem()) {
+            switch (bn) {
+              case 64: return launch_igemm<MODE, 64, true, true, true, true>(p, grid, st, ta, tb, tc, td);
+              case 128: return launch_igemm<MODE, 128, true, true, true, true>(p, grid, st, ta, tb, tc, td);
+            }
+          }
+        }
         switch (bn) {
           case 64: return launch_igemm<MODE, 64, true, true, true>(p, grid, st, ta, tb, tc, td);
           case 128: return launch_igemm<MODE, 128, true, true, true>(p, grid, st, ta, tb, tc, td);

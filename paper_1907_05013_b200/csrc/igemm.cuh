@@ -507,7 +507,8 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
   // AT: 3xTF32 with the A operand in TMEM -- the auxiliary warps move each stage's A tile (hi =
   // trunc_tf32(a), lo = a - hi) from shared memory into TMEM, so the three MMAs of a k-step read
   // only B / Bs from shared memory (A is re-read by every MMA, the dominant smem traffic at BN = 64)
-  static_assert(!AT || (X3 && TMA && !XF && MODE != GEMM_TEST), "AT: 3xTF32 TMA fwd / dgrad / wgrad");
+  static_assert(!AT || (X3 && TMA && MODE != GEMM_TEST && (!XF || MODE == CONV_FWD)),
+                "AT: 3xTF32 TMA fwd / dgrad / wgrad (with BN-ReLU on load: fwd only)");
   static_assert(!AT || 2 * BN + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
   constexpr uint32_t TMEM_COLS = AT ? 512u : 2u * BN;
   constexpr uint32_t A_TCOL = 2u * BN;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
@@ -746,8 +747,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
         const int per = p.tw * p.th;
         rowv = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = (stid >> 3) + 16 * i;
+        for (int i = 0; i < (AT ? 1 : 8); ++i) {
+          // AT: one row per thread (lane of the warp's TMEM quadrant); else 8 rows of a chunk column
+          const int row = AT ? 32 * (warp & 3) + lane : (stid >> 3) + 16 * i;
           const int nn = tn_i * p.tn + row / per, ho = th_i * p.th + (row / p.tw) % p.th, wo = tw_i * p.tw + row % p.tw;
           if (row < per * p.tn && nn < p.n3 && ho < p.hout && wo < p.wout) rowv |= 1u << i;
           hb[i] = ho * p.stride - p.pad;
@@ -773,13 +775,20 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
           const int k = kb0 + kb;
           const int tap = k / p.cchunks, cc = k - tap * p.cchunks;
           const int r = tap / p.S, sx = tap - r * p.S;
-          const int jl = (stid & 7) ^ ((stid >> 3) & 7);
-          xsc = __ldg(reinterpret_cast<const float4*>(p.xf_scale + cc * 32 + 4 * jl));
-          xsh = __ldg(reinterpret_cast<const float4*>(p.xf_shift + cc * 32 + 4 * jl));
+          if constexpr (AT) {  // lane-distributed: lane l holds channel cc*32 + l's scale / shift
+            xsc.x = __ldg(p.xf_scale + cc * 32 + lane);
+            xsh.x = __ldg(p.xf_shift + cc * 32 + lane);
+            const int hi = hb[0] + r, wi = wb[0] + sx;
+            if ((rowv & 1u) && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W) xvalid = 1u;
+          } else {
+            const int jl = (stid & 7) ^ ((stid >> 3) & 7);
+            xsc = __ldg(reinterpret_cast<const float4*>(p.xf_scale + cc * 32 + 4 * jl));
+            xsh = __ldg(reinterpret_cast<const float4*>(p.xf_shift + cc * 32 + 4 * jl));
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int hi = hb[i] + r, wi = wb[i] + sx;
-            if (((rowv >> i) & 1u) && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W) xvalid |= 1u << i;
+            for (int i = 0; i < 8; ++i) {
+              const int hi = hb[i] + r, wi = wb[i] + sx;
+              if (((rowv >> i) & 1u) && (unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W) xvalid |= 1u << i;
+            }
           }
         }
         if constexpr (XF && MODE == CONV_WGRAD) {
@@ -850,7 +859,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
             else
               transpose32<X3>(st + bi * 4096, lane, SM::SMALL_OFF);
           }
-        } else if constexpr (XF && MODE == CONV_FWD) {
+        } else if constexpr (XF && !AT && MODE == CONV_FWD) {
           // A: BN-ReLU on load (+ residual); B: residual only
           const int pj = stid & 7;
 #pragma unroll
@@ -897,6 +906,14 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
               asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                            : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
                            : "r"(st + row * 128 + ((j ^ (row & 7)) << 4)));
+            if constexpr (XF) {  // BN-ReLU on load: channel i's scale / shift from lane i
+              const bool valid = xvalid & 1u;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float sc = __shfl_sync(0xffffffffu, xsc.x, i), sh = __shfl_sync(0xffffffffu, xsh.x, i);
+                v[i] = valid ? bnrelu1(v[i], sc, sh) : 0.f;
+              }
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float hi = __uint_as_float(__float_as_uint(v[i]) & 0xFFFFE000u);
