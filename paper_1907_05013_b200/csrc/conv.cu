@@ -61,7 +61,10 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   // AT: each stage also holds 64 TMEM columns (A hi / lo) next to the two accumulators
   constexpr int STAGES = AT ? std::min(STAGES_SM, (512 - 2 * BN) / 64) : STAGES_SM;
   constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT, NSTG>::TOTAL;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG>;
+  // TMA wgrad at BN = 64 (3xTF32): six blocks of 32x32 per stage -> six auxiliary warps, one
+  // block each, instead of four warps doing one or two (the transposes bound these layers)
+  constexpr int NAUX = (MODE == CONV_WGRAD && TMA && X3 && BN == 64 && !AT && !XF) ? 6 : 4;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -72,7 +75,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   int64_t tiles = (int64_t)grid.x * grid.y * grid.z;
   int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
-  kern<<<ctas, igemm_threads(MODE, X3, XF), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
+  kern<<<ctas, igemm_threads(MODE, X3, XF, NAUX), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
                                                           tc ? *tc : g_zero_map, td ? *td : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;

@@ -467,8 +467,8 @@ constexpr int NUM_THREADS_X3 = 416;     // + 4 residual ("split") warps for 3xTF
 __host__ __device__ constexpr bool igemm_aux(int mode, bool x3, bool xf = false) {
   return x3 || xf || mode == CONV_WGRAD;
 }
-__host__ __device__ constexpr int igemm_threads(int mode, bool x3, bool xf = false) {
-  return igemm_aux(mode, x3, xf) ? NUM_THREADS_X3 : NUM_THREADS_P;
+__host__ __device__ constexpr int igemm_threads(int mode, bool x3, bool xf = false, int naux = 4) {
+  return igemm_aux(mode, x3, xf) ? NUM_THREADS_P + 32 * naux : NUM_THREADS_P;
 }
 
 
@@ -496,14 +496,16 @@ struct TileMap {
 };
 
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false,
-          int NSTG = 1>
-__global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
+          int NSTG = 1, int NAUX = 4>
+__global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
   static_assert(!TMA || MODE != GEMM_TEST, "TMA path: conv fwd / dgrad / wgrad");
   // TMA tiles whose M rows are a box of output pixels (FWD / DGRAD); TMA wgrad boxes pixels along K
   constexpr bool PIXM = TMA && MODE != CONV_WGRAD;
   static_assert(!XF || (TMA && (MODE == CONV_FWD || MODE == CONV_WGRAD)), "XF: TMA-fed fwd / wgrad only");
+  // NAUX > 4 auxiliary warps: only the TMA wgrad block loop distributes over them
+  static_assert(NAUX == 4 || (MODE == CONV_WGRAD && TMA && !AT && !XF), "NAUX: TMA wgrad only");
   // AT: 3xTF32 with the A operand in TMEM -- the auxiliary warps move each stage's A tile (hi =
   // trunc_tf32(a), lo = a - hi) from shared memory into TMEM, so the three MMAs of a k-step read
   // only B / Bs from shared memory (A is re-read by every MMA, the dominant smem traffic at BN = 64)
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // full: 128 producer (cp.async) or auxiliary-warp arrivals; 1 expect_tx arrival (TMA, no aux)
-      ptx::mbar_init(&full[s], (TMA && !AUX) ? 1 : 128);
+      ptx::mbar_init(&full[s], (TMA && !AUX) ? 1 : 32 * NAUX);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -763,7 +765,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
         // load latency overlaps the TMA instead of sitting between the TMA and the MMA
         float4 xsc = make_float4(0.f, 0.f, 0.f, 0.f), xsh = xsc;
         unsigned xvalid = 0;
-        constexpr int WQ = ((BM + BN) / 32 + 3) / 4;  // wgrad: 32x32 blocks per auxiliary warp
+        constexpr int WQ = ((BM + BN) / 32 + NAUX - 1) / NAUX;  // wgrad: 32x32 blocks per auxiliary warp
         float wscl[WQ], wshl[WQ];
         bool wval[WQ], wx[WQ];
 #pragma unroll
@@ -852,7 +854,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF), 1)
           // (BM + BN) / 32 TMA boxes, A's then B's, 4 KB each; residuals at the same offsets + SMALL_OFF
 #pragma unroll
           for (int q = 0; q < WQ; ++q) {
-            const int bi = warp - 9 + 4 * q;
+            const int bi = warp - 9 + NAUX * q;
             if (bi >= (BM + BN) / 32) break;
             if (XF && wx[q])  // an activation block: BN-ReLU on load
               transpose32<X3, XF>(st + bi * 4096, lane, SM::SMALL_OFF, wval[q], wscl[q], wshl[q]);
