@@ -62,7 +62,12 @@ typedef enum {
 } pooch_strategy;
 
 /* Swap-in scheduling (Sec. 4.3): EAGER = "when there is room in the GPU memory";
- * NAIVE = starts with the computation just before its first user. */
+ * NAIVE = starts with the computation just before its first user.
+ * EAGER, as built (DESIGN.md Reading 9): swap-ins are issued in need order once the forward pass
+ * has ended, and "room" is live + bytes + H(m) <= budget, where H(m) is the peak extra memory the
+ * compute program needs before the map's first use -- stricter than issuing whenever the H2D lane
+ * is free and live + bytes fits (which can let a prefetch take memory an earlier backward task
+ * needs and deadlock); the simulator, the oracle and the executor all use this rule. */
 typedef enum { POOCH_SCHED_EAGER = 0, POOCH_SCHED_NAIVE = 1, POOCH_SCHED_SN = 2 } pooch_sched;
 /* POOCH_SCHED_SN: SuperNeurons' rule, "each swap-in starts simultaneously with the computation
  * of the immediately preceding convolution layer". */
@@ -147,6 +152,9 @@ pooch_status pooch_set_streams(pooch_ctx* ctx, void* compute, void* d2h, void* h
  * caller (rank 0 creates it). The library creates its own communicator. Gradients are
  * summed across ranks and scaled by 1/world in the update. Marks the plan stale. */
 pooch_status pooch_set_comm(pooch_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t world);
+/* The communicator as NCCL reports it (ncclCommCount / ncclCommUserRank / ncclCommCuDevice):
+ * ranks, this rank, CUDA device. No communicator: 1, 0, the context's device. Host only. */
+pooch_status pooch_comm_info(pooch_ctx* ctx, int32_t* nranks, int32_t* rank, int32_t* cuda_device);
 /* The gradient allreduce runs per bucket: reverse-layer groups of whole
  * tasks' parameters of >= 26 MB, each one contiguous float range [lo, hi) of the gradient
  * region, enqueued on the comm stream right after the backward of `close_task` (the bucket's
@@ -191,12 +199,34 @@ typedef struct {
   int64_t tail_ns;           /* update (+ allreduce) after the last backward task */
   uint64_t resident_bytes;
   double d2h_gbs, h2d_gbs, duplex_gbs; /* probed host-link bandwidth (GB/s) */
+  int32_t mode;              /* how the times were measured: POOCH_PROFILE_ISOLATED or _ALL_SWAP */
+  const int64_t* d2h_issue_ns; /* ALL_SWAP only (else NULL): median issue time of each map's swap-out, */
+  const int64_t* h2d_issue_ns; /*   swap-in, ns after the step starts (-1: never copied)       */
+  int64_t step_ns;           /* ALL_SWAP only: median measured all-swap step (0 otherwise)            */
 } pooch_profile_t;
 
-/* Runs `iters` (>= 1) measured iterations under the all-swap classification ("all
- * feature maps are classified into swap as the default classification") after one warm-up,
- * keeping the per-task median; if the host arena or budget cannot hold all-swap, tasks are
- * timed in isolation instead (DESIGN.md Reading 22). Parameters are NOT updated. */
+/* Profiling modes (Sec. 4.2, DESIGN.md Reading 22).
+ *  ISOLATED: every task's forward, replay (recompute) and backward kernels are timed alone on
+ *            scratch buffers of the dynamic region (1 warm-up + `iters` runs, median); every
+ *            distinct map size is copied D2H and H2D through the pinned host arena the same way;
+ *            a duplex probe copies both directions at once; the tail (weight transposes, the
+ *            final bucket's allreduce at its real size, SGD) is timed likewise.
+ *  ALL_SWAP: the paper's method ("all feature maps are classified into swap as the
+ *            default classification"): after the isolated pass (which also provides the replay
+ *            times and the numbers the all-swap plan is packed with), `iters` real steps of the
+ *            all-swap plan run on the three streams after one warm-up, without the update; each
+ *            task's forward / backward time and each map's D2H / H2D time become the median over
+ *            those steps (under the real copy traffic), and each copy's issue time is recorded.
+ *            Needs a pinned host arena holding every map and a budget in which all-swap packs.
+ *  AUTO (default): ALL_SWAP when those hold, else ISOLATED (e.g. ResNet-50 at batch 2560: 214 GB
+ *            of maps, more than the host's pinned memory). */
+enum { POOCH_PROFILE_AUTO = 0, POOCH_PROFILE_ISOLATED = 1, POOCH_PROFILE_ALL_SWAP = 2 };
+pooch_status pooch_set_profile_mode(pooch_ctx* ctx, int32_t mode);
+
+/* Measures the profile in the context's profiling mode (above); `iters` >= 1. Parameters are NOT
+ * updated; any plan is invalidated. ALL_SWAP that cannot run returns POOCH_EINFEASIBLE (AUTO
+ * falls back to ISOLATED); a task whose isolated working set exceeds the budget returns
+ * POOCH_EINFEASIBLE. `out` (nullable) receives context-owned arrays. */
 pooch_status pooch_profile(pooch_ctx* ctx, int32_t iters, pooch_profile_t* out);
 /* Replace the measured times (e.g. the element-wise max over DP ranks). Arrays of n. */
 pooch_status pooch_set_profile(pooch_ctx* ctx, const int64_t* fwd_ns, const int64_t* bwd_ns,

@@ -1,11 +1,17 @@
 """Layer math of the paper's workloads in fp64, NCHW layout (oracle, C1).
 
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's CPU legs,
+never by the product path.
+
 The paper trains CNNs made of "convolutional layer, pooling layer,
 Batch-Normalization (BN) layer, fully-connected layer" (Sec. 2.1) with
 back-propagation: forward, backward, update. Each function below is
 the textbook definition of one of those layers; backward functions are the
 adjoints, written out directly (no autograd). Pinned by finite differences and
-closed forms in tests/test_oracle_layers.py.
+closed forms in tests/test_oracle_layers.py. Every function computes in the
+dtype of its inputs (fp64 normally; the same code runs in fp32 for the oracle's
+fp32 mode, which measures what plain fp32 arithmetic alone does to a result --
+DESIGN.md Reading 28).
 """
 from __future__ import annotations
 
@@ -16,6 +22,12 @@ SGD_MOMENTUM = 0.9     # Reading 23
 
 
 # ---------------------------------------------------------------- TF32 operands
+def _dt(*arrays):
+    """Arithmetic type of a layer call: the inputs' (fp64 by default; fp32 when the oracle
+    runs its fp32 mode, ``nets.forward_backward(precision="fp32")``)."""
+    return np.result_type(*arrays)
+
+
 def tf32(x):
     """Operand precision of the kernels' tensor-core contractions (BASELINE.json
     north_star: "TF32 in, FP32 accumulate"; DESIGN.md Reading 27): the value is
@@ -39,7 +51,7 @@ def conv2d_fwd(x, w, stride=1, pad=0):
     assert c == c2
     ho, wo = conv_out_hw(h, wd, r, s, stride, pad)
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
-    y = np.zeros((n, ho, wo, o), dtype=np.float64)
+    y = np.zeros((n, ho, wo, o), dtype=_dt(x, w))
     for u in range(r):
         for v in range(s):
             patch = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
@@ -52,7 +64,7 @@ def conv2d_dgrad(dy, w, x_shape, stride=1, pad=0):
     n, c, h, wd = x_shape
     o, _, r, s = w.shape
     _, _, ho, wo = dy.shape
-    dxp = np.zeros((n, c, h + 2 * pad, wd + 2 * pad), dtype=np.float64)
+    dxp = np.zeros((n, c, h + 2 * pad, wd + 2 * pad), dtype=_dt(dy, w))
     for u in range(r):
         for v in range(s):
             contrib = np.tensordot(dy, w[:, :, u, v], axes=([1], [0]))  # [n,ho,wo,c]
@@ -66,7 +78,7 @@ def conv2d_wgrad(x, dy, w_shape, stride=1, pad=0):
     o, c, r, s = w_shape
     _, _, ho, wo = dy.shape
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
-    dw = np.zeros(w_shape, dtype=np.float64)
+    dw = np.zeros(w_shape, dtype=_dt(x, dy))
     for u in range(r):
         for v in range(s):
             patch = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
@@ -93,7 +105,7 @@ def conv3d_fwd(x, w, stride=1, pad=0):
     assert c == c2
     do, ho, wo = (conv3d_out(e, k, stride, pad) for e in (d, h, wd))
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad), (pad, pad)))
-    y = np.zeros((n, do, ho, wo, o), dtype=np.float64)
+    y = np.zeros((n, do, ho, wo, o), dtype=_dt(x, w))
     for u in range(k):
         for v in range(k):
             for t in range(k):
@@ -106,7 +118,7 @@ def conv3d_dgrad(dy, w, x_shape, stride=1, pad=0):
     n, c, d, h, wd = x_shape
     o, _, k, _, _ = w.shape
     _, _, do, ho, wo = dy.shape
-    dxp = np.zeros((n, c, d + 2 * pad, h + 2 * pad, wd + 2 * pad), dtype=np.float64)
+    dxp = np.zeros((n, c, d + 2 * pad, h + 2 * pad, wd + 2 * pad), dtype=_dt(dy, w))
     for u in range(k):
         for v in range(k):
             for t in range(k):
@@ -121,7 +133,7 @@ def conv3d_wgrad(x, dy, w_shape, stride=1, pad=0):
     o, c, k, _, _ = w_shape
     _, _, do, ho, wo = dy.shape
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad), (pad, pad)))
-    dw = np.zeros(w_shape, dtype=np.float64)
+    dw = np.zeros(w_shape, dtype=_dt(x, dy))
     for u in range(k):
         for v in range(k):
             for t in range(k):
@@ -137,7 +149,7 @@ def upconv3d_fwd(x, w):
     n, c, d, h, wd = x.shape
     c2, o = w.shape[:2]
     assert c == c2
-    y = np.zeros((n, o, 2 * d, 2 * h, 2 * wd), dtype=np.float64)
+    y = np.zeros((n, o, 2 * d, 2 * h, 2 * wd), dtype=_dt(x, w))
     for u in range(2):
         for v in range(2):
             for t in range(2):
@@ -147,8 +159,8 @@ def upconv3d_fwd(x, w):
 
 def upconv3d_bwd(dy, x, w):
     """Adjoints of upconv3d_fwd: (dx, dw)."""
-    dx = np.zeros_like(x, dtype=np.float64)
-    dw = np.zeros(w.shape, dtype=np.float64)
+    dx = np.zeros_like(x, dtype=_dt(dy, x, w))
+    dw = np.zeros(w.shape, dtype=_dt(dy, x, w))
     for u in range(2):
         for v in range(2):
             for t in range(2):
@@ -162,7 +174,7 @@ def maxpool3d_fwd(x, k=2, stride=2):
     """Max over k^3 windows (no padding)."""
     n, c, d, h, w = x.shape
     do, ho, wo = ((e - k) // stride + 1 for e in (d, h, w))
-    y = np.full((n, c, do, ho, wo), -np.inf)
+    y = np.full((n, c, do, ho, wo), -np.inf, dtype=x.dtype)
     for u in range(k):
         for v in range(k):
             for t in range(k):
@@ -174,7 +186,7 @@ def maxpool3d_bwd(dy, x, k=2, stride=2):
     """Gradient to the FIRST maximum in (u, v, t) row-major window order (Reading 25)."""
     n, c, d, h, w = x.shape
     _, _, do, ho, wo = dy.shape
-    best = np.full(dy.shape, -np.inf)
+    best = np.full(dy.shape, -np.inf, dtype=x.dtype)
     arg = np.full(dy.shape, -1, dtype=np.int64)
     for u in range(k):
         for v in range(k):
@@ -183,7 +195,7 @@ def maxpool3d_bwd(dy, x, k=2, stride=2):
                 better = win > best
                 best = np.where(better, win, best)
                 arg = np.where(better, (u * k + v) * k + t, arg)
-    dx = np.zeros_like(x, dtype=np.float64)
+    dx = np.zeros_like(x, dtype=_dt(dy, x))
     for u in range(k):
         for v in range(k):
             for t in range(k):
@@ -237,7 +249,7 @@ def maxpool_fwd(x, k, stride, pad):
     n, c, h, w = x.shape
     ho, wo = conv_out_hw(h, w, k, k, stride, pad)
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)), constant_values=-np.inf)
-    y = np.full((n, c, ho, wo), -np.inf)
+    y = np.full((n, c, ho, wo), -np.inf, dtype=x.dtype)
     for u in range(k):
         for v in range(k):
             y = np.maximum(y, xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride])
@@ -250,7 +262,7 @@ def maxpool_bwd(dy, x, k, stride, pad):
     _, _, ho, wo = dy.shape
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)), constant_values=-np.inf)
     dxp = np.zeros_like(xp)
-    best = np.full((n, c, ho, wo), -np.inf)
+    best = np.full((n, c, ho, wo), -np.inf, dtype=x.dtype)
     arg = np.full((n, c, ho, wo), -1, dtype=np.int64)
     for u in range(k):
         for v in range(k):

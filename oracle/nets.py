@@ -257,10 +257,15 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
     outputs (NCHW) for map-level checks; ``map_grads`` (a list) receives the
     gradient of every map. ``precision="tf32"`` rounds the operands of every
     contraction (conv fwd / dgrad / wgrad, FC) with ``layers.tf32`` -- the
-    kernels' operand precision -- and keeps everything else in fp64."""
+    kernels' operand precision -- and keeps everything else in fp64.
+    ``precision="fp32"`` runs the same code with every array in fp32 (NumPy
+    keeps fp32 through every layer call; the contractions are fp32 BLAS): the
+    oracle's fp32 mode, which measures how far plain fp32 arithmetic alone
+    moves a result from fp64 (DESIGN.md Reading 28)."""
     q = L.tf32 if precision == "tf32" else (lambda a: a)
-    P = {k: np.asarray(v, dtype=np.float64) for k, v in params.items()}
-    x_np = np.asarray(x_nhwc, dtype=np.float64)
+    dt = np.float32 if precision == "fp32" else np.float64
+    P = {k: np.asarray(v, dtype=dt) for k, v in params.items()}
+    x_np = np.asarray(x_nhwc, dtype=dt)
     x_in = np.moveaxis(x_np, -1, 1)          # N(D)HWC -> NC(D)HW
     three = net.dims == 3
     outs, caches = [], []

@@ -1,4 +1,4 @@
-"""Keep / swap / recompute classification (oracle, C4).
+"""Keep / swap / recompute classification (oracle, C4). TEST INFRASTRUCTURE ONLY.
 
 Two independent planners over the simulator in ``oracle.sim``:
 
@@ -74,7 +74,8 @@ def host_fit_base(p):
     """Step 1's starting point. The paper starts from all-swap; when the swap class
     of all-swap exceeds the pinned host arena (Reading 37) the swap maps with the cheapest
     replay per byte (recompute time / bytes; ties: larger bytes, smaller id; never the sink)
-    move to recompute until the swap class fits."""
+    move to recompute until the swap class fits. The sink is never recompute; if it
+    alone still does not fit (e.g. no host arena at all), it is kept."""
     n = p.n
     cls = [SWAP] * n
     if p.host_budget is None:
@@ -86,17 +87,23 @@ def host_fit_base(p):
             break
         cls[m] = RECOMPUTE
         total -= p.bytes[m]
+    if total > p.host_budget:
+        cls[n - 1] = KEEP
     return cls
 
 
-def step1(p, li_cap=16, sched=EAGER, log=None):
-    """Keep/swap search (Sec. 4.4.2). Returns (cls, makespan, n_sims)."""
+def step1(p, li_cap=16, sched=EAGER, log=None, trace=None):
+    """Keep/swap search (Sec. 4.4.2). Returns (cls, makespan, n_sims). ``trace`` (a list)
+    receives every simulated state in evaluation order as (class tuple, makespan or None
+    when it ran out of memory) -- the start first, then per leaf the leaf and its scan."""
     n = p.n
     start = host_fit_base(p)
     base = simulate(p, start, sched)
     if base.oom:
         return None, INF, 1
     sims = 1
+    if trace is not None:
+        trace.append((tuple(start), base.makespan))
     L_O, L_I = set(base.L_O), set(base.L_I)
     ranked = sorted(L_I, key=lambda m: (-base.stall[m], m))
     tree = sorted(ranked[:li_cap])
@@ -110,12 +117,16 @@ def step1(p, li_cap=16, sched=EAGER, log=None):
                 cls[m] = KEEP
         ms = _ms(p, cls, sched)
         sims += 1
+        if trace is not None:
+            trace.append((tuple(cls), None if ms == INF else ms))
         if ms < INF:
             best = min(best, _key(ms, cls))
         for m in scan:
             cls[m] = KEEP
             ms2 = _ms(p, cls, sched)
             sims += 1
+            if trace is not None:
+                trace.append((tuple(cls), None if ms2 == INF else ms2))
             if ms2 == INF:
                 cls[m] = SWAP          # out of memory: revert, continue the scan
                 continue

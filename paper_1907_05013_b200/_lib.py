@@ -50,7 +50,8 @@ class IODesc(C.Structure):
 class ProfileT(C.Structure):
     _fields_ = [("n", c_i32), ("fwd_ns", P(c_i64)), ("bwd_ns", P(c_i64)), ("rec_ns", P(c_i64)),
                 ("d2h_ns", P(c_i64)), ("h2d_ns", P(c_i64)), ("bytes", P(c_u64)), ("tail_ns", c_i64),
-                ("resident_bytes", c_u64), ("d2h_gbs", c_f64), ("h2d_gbs", c_f64), ("duplex_gbs", c_f64)]
+                ("resident_bytes", c_u64), ("d2h_gbs", c_f64), ("h2d_gbs", c_f64), ("duplex_gbs", c_f64),
+                ("mode", c_i32), ("d2h_issue_ns", P(c_i64)), ("h2d_issue_ns", P(c_i64)), ("step_ns", c_i64)]
 
 
 class Problem(C.Structure):
@@ -123,6 +124,8 @@ SIGNATURES = {
     "pooch_op_conv_wgrad_bnrelu": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pooch_op_maxpool2d_fwd": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_op_maxpool2d_bwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "pooch_set_profile_mode": (c_i32, [c_vp, c_i32]),
+    "pooch_comm_info": (c_i32, [c_vp, P(c_i32), P(c_i32), P(c_i32)]),
     "pooch_op_gemm_test": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
 }
 

@@ -86,6 +86,10 @@ struct pooch_ctx {
   int64_t tail_ns = 0;
   double d2h_gbs = 0, h2d_gbs = 0, duplex_gbs = 0;
   bool have_profile = false;
+  int profile_mode = 0;        // requested: POOCH_PROFILE_AUTO / _ISOLATED / _ALL_SWAP
+  int profile_mode_used = 0;   // what the last pooch_profile measured (ISOLATED or ALL_SWAP)
+  std::vector<int64_t> prof_d2h_issue, prof_h2d_issue;  // all-swap mode: per-map copy issue (ns from step start)
+  int64_t prof_step_ns = 0;    // all-swap mode: median measured step time of the profiling iterations
   // plan
   std::vector<uint8_t> cls;
   bool have_plan = false;
@@ -120,6 +124,7 @@ struct pooch_ctx {
   int64_t fam_launch[pooch::FAM_COUNT] = {0};
   double fam_flops[pooch::FAM_COUNT] = {0}, fam_bytes[pooch::FAM_COUNT] = {0};
   std::vector<int64_t> last_fwd, last_bwd, last_rec, last_d2h, last_h2d;
+  std::vector<int64_t> last_d2h_issue, last_h2d_issue;  // copy start, ns after the step's first event
   int64_t last_step_ns = 0;
   // dp
   void* nccl = nullptr;

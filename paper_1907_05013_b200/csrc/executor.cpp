@@ -70,6 +70,9 @@ struct Nccl {
   int (*commInitRank)(void**, int, NcclUid /* ncclUniqueId by value */, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
+  int (*commCount)(void*, int*) = nullptr;
+  int (*commUserRank)(void*, int*) = nullptr;
+  int (*commCuDevice)(void*, int*) = nullptr;
   const char* (*getErrorString)(int) = nullptr;
   bool load(std::string& err) {
     if (h) return true;
@@ -85,6 +88,9 @@ struct Nccl {
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
     getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    commCount = (decltype(commCount))dlsym(h, "ncclCommCount");
+    commUserRank = (decltype(commUserRank))dlsym(h, "ncclCommUserRank");
+    commCuDevice = (decltype(commCuDevice))dlsym(h, "ncclCommCuDevice");
     if (!commInitRank || !allReduce || !commDestroy) {
       err = "libnccl is missing symbols";
       return false;
@@ -758,6 +764,21 @@ extern "C" pooch_status pooch_set_comm(pooch_ctx* c, const void* uid, int32_t ra
   return POOCH_OK;
 }
 
+extern "C" pooch_status pooch_comm_info(pooch_ctx* c, int32_t* nranks, int32_t* rank, int32_t* dev) {
+  if (!c) return fail(POOCH_EUSAGE, "null context");
+  int nr = 1, r = 0, d = c->device;
+  if (c->nccl) {
+    if (!g_nccl.commCount || !g_nccl.commUserRank || !g_nccl.commCuDevice)
+      return ctx_fail(c, fail(POOCH_ENCCL, "libnccl lacks ncclCommCount / ncclCommUserRank / ncclCommCuDevice"));
+    if (g_nccl.commCount(c->nccl, &nr) || g_nccl.commUserRank(c->nccl, &r) || g_nccl.commCuDevice(c->nccl, &d))
+      return ctx_fail(c, fail(POOCH_ENCCL, "NCCL communicator query failed"));
+  }
+  if (nranks) *nranks = nr;
+  if (rank) *rank = r;
+  if (dev) *dev = d;
+  return POOCH_OK;
+}
+
 // The comm stream: the caller's, else one the context owns.
 static cudaStream_t comm_stream(pooch_ctx* c) {
   if (c->s[3]) return c->s[3];
@@ -1229,6 +1250,8 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
   const int n = c->g.n();
   const uint64_t cap = c->dev_bytes - c->resident_end;
   const pooch_search_cfg sc = cfg ? *cfg : pooch_search_cfg{16, 0, POOCH_SCHED_EAGER};
+  if (sc.li_cap < 0 || sc.li_cap > kMaxLiCap)
+    return ctx_fail(c, fail(POOCH_EUSAGE, "li_cap must be in [0, %d]", kMaxLiCap));
   const bool grid = strategy != POOCH_STRAT_FIXED && strategy != POOCH_STRAT_INCORE && !getenv("POOCH_PLAN_NO_GRID");
   std::vector<int> caps;
   if (grid && strategy == POOCH_STRAT_POOCH)
@@ -1391,6 +1414,13 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
         k.sched = sched;
         Planner pl(pc, sc);
         pl.report(k.cls, k.mk, &k.rep);
+        // |L_O|, |L_I| of the step-1 start at the full budget (a fresh Planner has not run step 1)
+        for (const Cand& q : cands)
+          if (q.step == 0 && q.st == POOCH_OK) {
+            k.rep.lo_size = q.rep.lo_size;
+            k.rep.li_size = q.rep.li_size;
+            break;
+          }
         adopt(k);
         c->refined = true;
       }
@@ -1560,6 +1590,8 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
     c->last_rec.assign(n, 0);
     c->last_d2h.assign(n, 0);
     c->last_h2d.assign(n, 0);
+    c->last_d2h_issue.assign(n, -1);
+    c->last_h2d_issue.assign(n, -1);
     std::vector<double> seg_ms(c->tseg.size(), 0);
     for (size_t k = 0; k + 1 < c->tseg.size(); ++k) {
       float ms = 0;
@@ -1599,8 +1631,15 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
       c->fam_ms[f] += ms;
       c->fam_launch[f] += 1;
       c->fam_bytes[f] += (double)c->map_bytes[o.id];
-      if (o.lane == 1) c->last_d2h[o.id] = ns;
-      else c->last_h2d[o.id] = ns;
+      float at = 0;
+      cudaEventElapsedTime(&at, c->tev[c->tseg.front().first], copy_ev[i].first);
+      if (o.lane == 1) {
+        c->last_d2h[o.id] = ns;
+        c->last_d2h_issue[o.id] = (int64_t)(at * 1e6);
+      } else {
+        c->last_h2d[o.id] = ns;
+        c->last_h2d_issue[o.id] = (int64_t)(at * 1e6);
+      }
     }
     float tot = 0;
     cudaEventElapsedTime(&tot, c->tev[c->tseg.front().first], c->tev[c->tseg.back().first]);
@@ -1745,6 +1784,83 @@ static int64_t median_ns(std::vector<float>& ms) {
   return std::max<int64_t>(1, (int64_t)(ms[ms.size() / 2] * 1e6));
 }
 
+// The paper's profiling (Sec. 4.2): "all feature maps are classified into swap as the
+// default classification" for the first iterations, which are measured. Runs `iters` real steps
+// (after one warm-up) of the all-swap plan -- packed and compiled from the isolated timings just
+// taken -- on the three streams in instrumented (eager) mode, without the update, and replaces
+// every task's forward / backward time and every swapped map's D2H / H2D time by its median
+// under that traffic; records each copy's issue time (ns after the step starts). Recompute
+// times stay the isolated replay measurements (all-swap runs no recompute). Needs a pinned host
+// arena holding every map and a budget that packs all-swap; otherwise AUTO keeps the isolated
+// profile and ALL_SWAP fails with POOCH_EINFEASIBLE.
+static pooch_status profile_all_swap(pooch_ctx* c, int iters) {
+  const int n = c->g.n();
+  uint64_t need = 0;
+  for (int m = 0; m < n; ++m) need += align_up(c->map_bytes[m]);
+  const bool must = c->profile_mode == POOCH_PROFILE_ALL_SWAP;
+  if (!c->host || need > c->host_bytes) {
+    if (!must) return POOCH_OK;
+    return ctx_fail(c, fail(POOCH_EINFEASIBLE, "all-swap profiling needs %llu B of pinned host arena, have %zu B",
+                            (unsigned long long)need, c->host_bytes));
+  }
+  pooch_plan_report rep{};
+  pooch_status st = pooch_plan(c, POOCH_STRAT_SWAP_ALL, nullptr, nullptr, nullptr, &rep);
+  if (st != POOCH_OK) {
+    c->have_plan = false;
+    if (!must && st == POOCH_EINFEASIBLE) return POOCH_OK;
+    return ctx_fail(c, st);
+  }
+  const bool was_timing = c->timing;
+  c->timing = true;
+  std::vector<std::vector<int64_t>> f(n), b(n), d(n), h(n), di(n), hi(n);
+  std::vector<int64_t> steps;
+  for (int it = 0; it <= iters; ++it) {
+    pooch_status s2 = step_impl(c, 0.f, false);
+    if (s2 == POOCH_OK) s2 = join_streams(c);
+    if (s2 == POOCH_OK && cudaStreamSynchronize(c->s[0]) != cudaSuccess) s2 = fail(POOCH_ECUDA, "all-swap profiling step");
+    if (s2 != POOCH_OK) {
+      c->timing = was_timing;
+      c->have_plan = false;
+      return ctx_fail(c, s2);
+    }
+    if (it == 0) continue;  // warm-up
+    steps.push_back(c->last_step_ns);
+    for (int t = 0; t < n; ++t) {
+      f[t].push_back(c->last_fwd[t]);
+      b[t].push_back(c->last_bwd[t]);
+      if (c->last_d2h_issue[t] >= 0) {
+        d[t].push_back(c->last_d2h[t]);
+        di[t].push_back(c->last_d2h_issue[t]);
+      }
+      if (c->last_h2d_issue[t] >= 0) {
+        h[t].push_back(c->last_h2d[t]);
+        hi[t].push_back(c->last_h2d_issue[t]);
+      }
+    }
+  }
+  c->timing = was_timing;
+  auto med = [](std::vector<int64_t> v) {
+    std::sort(v.begin(), v.end());
+    return std::max<int64_t>(1, v[v.size() / 2]);
+  };
+  for (int t = 0; t < n; ++t) {
+    c->fwd_ns[t] = med(f[t]);
+    c->bwd_ns[t] = med(b[t]);
+    if (!d[t].empty()) {
+      c->d2h_ns[t] = med(d[t]);
+      c->prof_d2h_issue[t] = med(di[t]);
+    }
+    if (!h[t].empty()) {
+      c->h2d_ns[t] = med(h[t]);
+      c->prof_h2d_issue[t] = med(hi[t]);
+    }
+  }
+  c->prof_step_ns = med(steps);
+  c->profile_mode_used = POOCH_PROFILE_ALL_SWAP;
+  c->have_plan = false;
+  return POOCH_OK;
+}
+
 extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile_t* out) {
   if (!c || !c->budget_set) return fail(POOCH_EUSAGE, "set the budget first");
   if (!c->s[0]) return ctx_fail(c, fail(POOCH_EUSAGE, "streams not set"));
@@ -1879,9 +1995,13 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
       float ms;
       POOCH_CUDA(cudaEventRecord(e0, st));
       POOCH_CHECK(enqueue_transposes(c));
-      if (c->nccl) {
-        int r = g_nccl.allReduce(fptr(c, c->off_g), fptr(c, c->off_g), 0, 7, 0, c->nccl, st);  // latency only
-        (void)r;
+      if (c->nccl && !c->buckets.empty()) {
+        // the allreduce left after the last backward task: the final bucket's (the one SGD waits
+        // on), at its real size, on scratch floats of the dynamic region (the gradients stay intact)
+        const pooch_ctx::Bucket& b = c->buckets.back();
+        const size_t cnt = std::min<size_t>(b.hi - b.lo, dyn / 4);
+        int r = g_nccl.allReduce(fptr(c, c->resident_end), fptr(c, c->resident_end), cnt, 7, 0, c->nccl, st);
+        if (r != 0) return ctx_fail(c, fail(POOCH_ENCCL, "ncclAllReduce (profile tail) failed: %d", r));
       }
       POOCH_CHECK(sgd_momentum(fptr(c, c->off_tile), fptr(c, c->off_tile), fptr(c, c->off_tile), 0, 0.f, 0.f, 0.f, st));
       POOCH_CUDA(cudaEventRecord(e1, st));
@@ -1909,6 +2029,11 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
   c->timing = was_timing;
   c->have_profile = true;
   c->have_plan = false;
+  c->profile_mode_used = POOCH_PROFILE_ISOLATED;
+  c->prof_d2h_issue.assign(n, -1);
+  c->prof_h2d_issue.assign(n, -1);
+  c->prof_step_ns = 0;
+  if (c->profile_mode != POOCH_PROFILE_ISOLATED) POOCH_CHECK(profile_all_swap(c, iters));
   if (out) {
     out->n = n;
     out->fwd_ns = c->fwd_ns.data();
@@ -1922,7 +2047,18 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
     out->d2h_gbs = c->d2h_gbs;
     out->h2d_gbs = c->h2d_gbs;
     out->duplex_gbs = c->duplex_gbs;
+    out->mode = c->profile_mode_used;
+    const bool all_swap = c->profile_mode_used == POOCH_PROFILE_ALL_SWAP;
+    out->d2h_issue_ns = all_swap ? c->prof_d2h_issue.data() : nullptr;
+    out->h2d_issue_ns = all_swap ? c->prof_h2d_issue.data() : nullptr;
+    out->step_ns = c->prof_step_ns;
   }
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_set_profile_mode(pooch_ctx* c, int32_t mode) {
+  if (!c || mode < POOCH_PROFILE_AUTO || mode > POOCH_PROFILE_ALL_SWAP) return fail(POOCH_EUSAGE, "bad profile mode");
+  c->profile_mode = mode;
   return POOCH_OK;
 }
 

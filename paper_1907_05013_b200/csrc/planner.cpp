@@ -66,7 +66,8 @@ int64_t Planner::ms(const std::vector<uint8_t>& cls) {
 
 // Step 1's starting point: all-swap, or -- when its swap class exceeds the pinned
 // host arena (Reading 37) -- all-swap with the cheapest-to-replay maps (recompute ns per byte;
-// ties: larger bytes, smaller id; never the sink) moved to recompute until it fits.
+// ties: larger bytes, smaller id; never the sink) moved to recompute until it fits, the sink
+// kept if it alone does not fit.
 static std::vector<uint8_t> host_fit_base(const Problem& p) {
   const int n = p.n;
   std::vector<uint8_t> cls(n, C_SWAP);
@@ -87,6 +88,9 @@ static std::vector<uint8_t> host_fit_base(const Problem& p) {
     cls[m] = C_RECOMPUTE;
     total -= p.bytes[m];
   }
+  // the sink is never recompute; if it alone still exceeds the host arena (e.g. none at all) it
+  // is kept, so a context without a pinned host arena still gets keep / recompute plans
+  if (total > p.host_budget) cls[n - 1] = C_KEEP;
   return cls;
 }
 
@@ -122,7 +126,7 @@ bool Planner::step1(std::vector<uint8_t>& best_cls, int64_t& best_ms) {
   for (int m = n - 1; m >= 0; --m)
     if (in_scan[m]) scan.push_back(m);
 
-  const int64_t leaves = int64_t(1) << tree.size();
+  const int64_t leaves = int64_t(1) << tree.size();  // tree.size() <= li_cap <= kMaxLiCap
   const int T = hw_threads(cfg_.threads);
   std::vector<Key> best_per_thread;
   // deterministic reduction: each leaf's best, reduced in leaf order via min (total order)
@@ -390,6 +394,7 @@ extern "C" pooch_status pooch_plan_problem(const pooch_problem* prob, int32_t st
   std::string err;
   if (!problem_from_c(*prob, p, err)) return fail(POOCH_EUSAGE, "%s", err.c_str());
   pooch_search_cfg c = cfg ? *cfg : pooch_search_cfg{16, 0, POOCH_SCHED_EAGER};
+  if (c.li_cap < 0 || c.li_cap > kMaxLiCap) return fail(POOCH_EUSAGE, "li_cap must be in [0, %d]", kMaxLiCap);
   Planner pl(p, c);
   std::vector<uint8_t> cls;
   int64_t mk;

@@ -7,6 +7,9 @@
 
 namespace pooch {
 
+// Largest accepted L_I tree cap (Reading 16): 2^20 leaves, each a scan of simulations.
+constexpr int kMaxLiCap = 20;
+
 struct Decision {
   int map;
   double r;  // Eq. (1) ratio at commit time

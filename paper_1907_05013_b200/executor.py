@@ -172,14 +172,28 @@ class Context:
         return a
 
     # ---------------------------------------------------------------- profile / plan / step
+    PROFILE_MODES = {"auto": 0, "isolated": 1, "all_swap": 2}
+
+    def set_profile_mode(self, mode: str):
+        """'auto' (all-swap iterations when they fit, else isolated), 'isolated' or 'all_swap'."""
+        self._chk(lib.pooch_set_profile_mode(self.h, self.PROFILE_MODES[mode]))
+
     def profile(self, iters=3):
         pr = ProfileT()
         self._chk(lib.pooch_profile(self.h, iters, C.byref(pr)))
         n = pr.n
-        g = lambda p: [int(p[i]) for i in range(n)]
+        g = lambda p: [int(p[i]) for i in range(n)] if p else None
         return dict(fwd=g(pr.fwd_ns), bwd=g(pr.bwd_ns), rec=g(pr.rec_ns), d2h=g(pr.d2h_ns), h2d=g(pr.h2d_ns),
                     bytes=g(pr.bytes), tail=int(pr.tail_ns), resident=int(pr.resident_bytes),
-                    d2h_gbs=pr.d2h_gbs, h2d_gbs=pr.h2d_gbs, duplex_gbs=pr.duplex_gbs)
+                    d2h_gbs=pr.d2h_gbs, h2d_gbs=pr.h2d_gbs, duplex_gbs=pr.duplex_gbs,
+                    mode={1: "isolated", 2: "all_swap"}.get(int(pr.mode), str(pr.mode)),
+                    d2h_issue=g(pr.d2h_issue_ns), h2d_issue=g(pr.h2d_issue_ns), step_ns=int(pr.step_ns))
+
+    def comm_info(self):
+        """(nranks, rank, cuda device) of the library's NCCL communicator (ncclCommCount etc.)."""
+        a, b, d = C.c_int32(), C.c_int32(), C.c_int32()
+        self._chk(lib.pooch_comm_info(self.h, C.byref(a), C.byref(b), C.byref(d)))
+        return a.value, b.value, d.value
 
     def set_profile(self, fwd, bwd, rec, d2h, h2d, tail):
         arrs = [np.asarray(v, np.int64) for v in (fwd, bwd, rec, d2h, h2d)]

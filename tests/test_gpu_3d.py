@@ -21,8 +21,7 @@ from oracle import nets  # noqa: E402
 from netutil import global_rel, load_params, pad_input, read_params, rel  # noqa: E402
 
 TOL_X3 = 2e-5
-TOL = 5e-3
-TOL_TENSOR = 5e-2
+from gates import TOL, gate  # noqa: E402
 
 
 def _lib():
@@ -178,7 +177,8 @@ def unet():
     x = g.standard_normal((1, E, E, E, 1)).astype(np.float32)
     t = g.integers(0, CLASSES, (1, E, E, E))
     loss, grads, _ = nets.forward_backward(net, params, x, t)
-    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads)
+    _, grads32, _ = nets.forward_backward(net, params, x, t, precision="fp32")
+    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, grads32=grads32)
 
 
 def _step(ctx, u, strategy):
@@ -197,8 +197,7 @@ def test_unet3d_step_matches_oracle(unet):
     assert abs(loss - unet["loss"]) < 1e-3 * max(1.0, abs(unet["loss"]))
     g = read_params(ctx, unet["params"], 1)
     assert global_rel(g, unet["grads"]) < TOL
-    worst = max(rel(g[k], unet["grads"][k]) for k in unet["grads"] if np.linalg.norm(unet["grads"][k]) > 0)
-    assert worst < TOL_TENSOR
+    gate(g, unet["grads"], unet["grads32"], "3D U-Net 16^3")
     ctx.close()
 
 

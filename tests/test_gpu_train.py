@@ -20,8 +20,8 @@ import synthdata  # noqa: E402
 from oracle import nets  # noqa: E402
 from netutil import global_rel, load_params, pad_input, read_params, rel  # noqa: E402
 
-TOL = 5e-3          # rel-L2 of the whole gradient (north_star; DESIGN.md Reading 28)
-TOL_TENSOR = 5e-2   # per-tensor sanity bound (BN beta/gamma sums are ill-conditioned)
+from gates import FP32_X, TOL, gate  # noqa: E402
+
 LR = 0.05
 
 
@@ -73,9 +73,10 @@ def tiny():
     x = synthdata.images(8, 32, 32, 3, seed=0)
     t = synthdata.labels(8, 10, seed=1)
     loss, grads, _ = nets.forward_backward(net, params, x, t)
+    _, grads32, _ = nets.forward_backward(net, params, x, t, precision="fp32")
     ctx = _ctx_for("tiny", 8, 32, 10, 256 << 20, 64 << 20)
     ctx.profile(2)
-    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, ctx=ctx)
+    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, grads32=grads32, ctx=ctx)
 
 
 def test_tiny_cnn_gradients_match_oracle(tiny):
@@ -84,8 +85,7 @@ def test_tiny_cnn_gradients_match_oracle(tiny):
     assert abs(loss - tiny["loss"]) / abs(tiny["loss"]) < TOL
     g = read_params(ctx, tiny["params"], 1)
     assert global_rel(g, tiny["grads"]) < TOL
-    worst = max(rel(g[k], tiny["grads"][k]) for k in g)
-    assert worst < TOL_TENSOR, {k: rel(g[k], tiny["grads"][k]) for k in g}
+    gate(g, tiny["grads"], tiny["grads32"], "tiny CNN")
     # the update: v = g, w' = w - lr * g on the first step (momentum starts at 0)
     w = read_params(ctx, tiny["params"], 0)
     ref_w, _ = nets.sgd_step(tiny["params"], {k: np.zeros_like(v) for k, v in tiny["params"].items()},
@@ -136,19 +136,28 @@ def test_tiny_cnn_pooch_at_half_budget(tiny):
     assert peak > half
 
 
-@pytest.fixture(scope="module")
-def r50():
-    # 224^2 (the paper's input size) at batch 8; small-residual init (gamma3 ~ U(0.1, 0.3),
-    # DESIGN.md Reading 28): with gamma3 ~ 1 the random network is chaotic and fp32 rounding
-    # alone moves its gradients by ~4% against fp64 (measured), whatever the kernels do.
+def _r50_case(init):
     net = nets.resnet50(in_hw=224, classes=1000)
-    params = nets.init_params(net, seed=2, bn_random=True, residual_gamma=(0.1, 0.3))
+    if init == "small_residual":
+        params = nets.init_params(net, seed=2, bn_random=True, residual_gamma=(0.1, 0.3))
+    else:                                   # the bench's recipe: He-normal, gamma 1, beta 0
+        params = nets.init_params(net, seed=2)
     x = synthdata.images(8, 224, 224, 3, seed=0)
     t = synthdata.labels(8, 1000, seed=1)
     loss, grads, _ = nets.forward_backward(net, params, x, t)
+    _, grads32, _ = nets.forward_backward(net, params, x, t, precision="fp32")
+    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, grads32=grads32)
+
+
+@pytest.fixture(scope="module")
+def r50():
+    # 224^2 (the paper's input size) at batch 8; small-residual init (gamma3 ~ U(0.1, 0.3),
+    # DESIGN.md Reading 28), where plain fp32 stays within 1.3e-3 of fp64 (whole gradient)
+    d = _r50_case("small_residual")
     ctx = _ctx_for("resnet50", 8, 224, 1000, 4 << 30, 2 << 30)
     ctx.profile(1)
-    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, ctx=ctx)
+    d["ctx"] = ctx
+    return d
 
 
 def test_resnet50_gradients_match_oracle(r50):
@@ -156,11 +165,21 @@ def test_resnet50_gradients_match_oracle(r50):
     loss, cls, rep = _step(ctx, r50["params"], r50["x"], r50["t"], "incore")
     assert abs(loss - r50["loss"]) / abs(r50["loss"]) < TOL
     g = read_params(ctx, r50["params"], 1)
-    errs = {k: rel(g[k], r50["grads"][k]) for k in g}
-    print("global rel-L2 %.3e, worst tensor %s" % (global_rel(g, r50["grads"]), max(errs.items(), key=lambda kv: kv[1])))
     assert global_rel(g, r50["grads"]) < TOL
-    worst = max(errs.values())
-    assert worst < TOL_TENSOR, sorted(errs.items(), key=lambda kv: -kv[1])[:8]
+    gate(g, r50["grads"], r50["grads32"], "ResNet-50 224^2 b8, small-residual init")
+
+
+def test_resnet50_standard_init_gradients(r50):
+    """The bench's own initialisation (gamma = 1, beta = 0): a chaotic random network in which
+    plain fp32 alone moves the whole gradient ~2 % from fp64 (the fp32 oracle), so the gate is
+    the fp32 floor of every tensor (Reading 28); the loss still agrees to 5e-3."""
+    d = _r50_case("standard")
+    ctx = r50["ctx"]
+    loss, cls, rep = _step(ctx, d["params"], d["x"], d["t"], "incore")
+    assert abs(loss - d["loss"]) / abs(d["loss"]) < TOL
+    g = read_params(ctx, d["params"], 1)
+    assert global_rel(g, d["grads"]) <= max(TOL, FP32_X * global_rel(d["grads32"], d["grads"]))
+    gate(g, d["grads"], d["grads32"], "ResNet-50 224^2 b8, standard init")
 
 
 def test_resnet50_plans_bit_exact(r50):

@@ -210,3 +210,49 @@ def test_fused_graphs_profile_parity(link):
     ref = OP.pooch(po, li_cap=3)
     cls, rep = pc.plan("pooch", li_cap=3)
     assert cls == (ref["cls"] if ref["feasible"] else None)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_no_host_arena_plans_keep_recompute(seed):
+    """A context without a pinned host arena (host budget 1 byte, as make_problem sets it) still
+    gets keep / recompute plans (the sink used to stay swap and make every start
+    infeasible): the step-1 start keeps the sink (Reading 37), the C++ planner equals the oracle,
+    and no map is swapped."""
+    d, budget = _tight(seed, 5 + seed % 4)
+    po, pc = both(d, resident=10, budget=budget, host_budget=1)
+    ref = OP.pooch(po, li_cap=16)
+    cls, rep = pc.plan("pooch", threads=2)
+    if not ref["feasible"]:
+        assert cls is None
+        return
+    assert cls == ref["cls"] and rep.makespan_ns == ref["makespan"]
+    assert OS.SWAP not in cls
+
+
+def test_no_host_arena_start():
+    """The ADVICE r01 case. Without a host arena step 1 starts from the recompute class with the
+    sink kept (Reading 37). (a) Four maps computed from the (resident) input: that start fits, so
+    PoocH returns it (step 1 only turns swap into keep, so nothing improves on it without a host
+    arena) -- C++ = oracle, feasible, no swap. (b) A 6-map chain: recomputing everything replays
+    the whole forward at the first backward task, the start runs out of memory and PoocH reports
+    infeasible (its precondition, "problem exceeds plannable size"), although brute force
+    finds keep / recompute plans -- a documented limit of the paper's search."""
+    d = dict(fwd=[10] * 4, bwd=[10] * 4, bytes=[100] * 4, d2h=[5] * 4, h2d=[5] * 4,
+             inputs=[[]] * 4, needs=[[0], [1], [2], [3]])
+    po, pc = both(d, resident=0, budget=200, host_budget=1)
+    cls, rep = pc.plan("pooch", threads=1)
+    assert cls == OP.pooch(po)["cls"] == [OS.RECOMPUTE, OS.RECOMPUTE, OS.RECOMPUTE, OS.KEEP]
+    assert not OS.simulate(po, cls).oom
+    n = 6
+    d = dict(fwd=[10] * n, bwd=[10] * n, bytes=[100] * n, d2h=[5] * n, h2d=[5] * n,
+             inputs=[[]] + [[i] for i in range(n - 1)], needs=[[0]] + [[i - 1, i] for i in range(1, n)])
+    po, pc = both(d, resident=0, budget=500, host_budget=1)
+    assert OP.brute_force(po)["cls"] is not None
+    assert OP.pooch(po)["cls"] is None and pc.plan("pooch", threads=1)[0] is None
+
+
+def test_li_cap_out_of_range_is_usage_error():
+    d, budget = _tight(0, 6)
+    _, pc = both(d, resident=10, budget=budget)
+    with pytest.raises(Exception):
+        pc.plan("pooch", li_cap=21)
