@@ -1,22 +1,34 @@
 #!/usr/bin/env python
 """Benchmark of the out-of-core ResNet-50 training step (BASELINE.json metric).
 
-Default workload (N=1): BASELINE.json config 2 -- ResNet-50 v1.5, batch 640 at
-224x224 (the paper's 50 GB case) under a 16 GiB device-memory budget,
-feature maps swapped over the host link / recomputed per the PoocH plan. The
-timed step is one full training iteration (forward, backward with swap-in /
-recompute, [allreduce], momentum SGD) -- the whole hot path of SURVEY.md 8(a).
+Default workload (N=1): BASELINE.json config 3 -- ResNet-50 v1.5, batch 2560 at 224x224
+(214 GB of feature maps, more than the B200's HBM) in all free HBM, feature maps kept,
+swapped over the host link or recomputed per the PoocH plan. The timed step is one full
+training iteration (forward, backward with swap-in / recompute, [allreduce], momentum SGD)
+-- the whole hot path of SURVEY.md 8(a). The same run also reports:
+  * the paper's own PoocH plan (one search, no grid / refinement) measured on the executor;
+  * bit-exactness at the benchmarked size: one step of the adopted plan and one of another
+    plan from identical parameters and batch, every gradient bit and the loss (`bitexact`),
+    and that the loss is finite;
+  * the in-core rate per image at batch 640 (the largest fitting batch) and the
+    overhead against it;
+  * the secondary cfg2 line (batch 640, 16 GiB budget: the paper's 50 GB case) with its plan
+    checked bit for bit against the in-core step, under both profiling modes (all-swap
+    iterations, and isolated timing) with simulated vs measured step times.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--batch B] [--budget-gib G] [--workload cfg2|cfg3|cfg4]
+                    [--batch B] [--budget-gib G] [--workload cfg3|cfg2|cfg4]
 
 --workload cfg4 runs BASELINE config 4 instead: the 3D U-Net (conv3d-BN-ReLU, widths
 256/512/1024/1024) at batch 1 on a 256^3 volume, whose 207 GB of maps exceed HBM; its
 in-core comparison is the same net at half the edge (the per-voxel rate).
 
-Under torchrun (N>1) every rank runs its own out-of-core executor on its own
-shard (weak scaling) with an NCCL gradient allreduce; the step time is the max
-over ranks of the CUDA-event time. Rank 0 prints ONE JSON line.
+--gpus N > 1: one process per GPU (the driver's torch.distributed.run line; run by hand
+without WORLD_SIZE, bench.py relaunches itself that way and fails if fewer than N GPUs are
+visible). Every rank runs its own out-of-core executor on its own shard (weak scaling) with
+its pinned host arena on its GPU's NUMA node and an NCCL gradient allreduce; the step time
+is the max over ranks of the CUDA-event time; `ranks_identical` says whether every rank
+holds the same weights afterwards. Rank 0 prints ONE JSON line.
 
 --impl reference times the CPU oracle (oracle/, fp64 NumPy) on the box's host
 cores on a bounded sample of the same workload (the tier's reference arm).
@@ -45,7 +57,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--edge", type=int, default=None, help="cfg4: volume edge (default 256)")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--budget-gib", type=float, default=None)
@@ -53,6 +65,11 @@ def parse():
     ap.add_argument("--no-incore", action="store_true", help="skip the in-core comparison run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--profile-iters", type=int, default=3)
+    ap.add_argument("--profile-repeats", type=int, default=3,
+                    help="profiles taken; the plan uses their element-wise median (noise robustness)")
+    ap.add_argument("--no-paper", action="store_true", help="skip timing the paper's own PoocH plan")
+    ap.add_argument("--no-check", action="store_true", help="skip the full-size bit-exactness check")
+    ap.add_argument("--no-cfg2", action="store_true", help="skip the secondary cfg2 (16 GiB) line")
     ap.add_argument("--ablation", action="store_true",
                     help="also run the paper's strategies (Sec. 5.1-5.2) on the same executor and report each")
     ap.add_argument("--ncu-step", action="store_true",
@@ -226,42 +243,203 @@ def reference_arm(args):
 
 
 # ------------------------------------------------------------------ our arm
+class Run:
+    """One out-of-core context with its arenas, streams and synthetic batch (the caller-owned
+    resources of pooch_set_budget; the library never allocates device or pinned memory)."""
+
+    def __init__(self, W, budget, host, streams, rank=0, device=0, precision=1, margin=3 << 30):
+        import torch
+        self.W, self.streams, self.rank = W, streams, rank
+        self.ctx = W.context(device=device)
+        self.ctx.set_precision(precision)
+        if budget is None:
+            free, _ = torch.cuda.mem_get_info()
+            budget = int(free - margin)
+        self.budget = budget // 256 * 256
+        self.host = host
+        self.dev = torch.empty(self.budget, dtype=torch.uint8, device="cuda")
+        self.ctx.set_budget(self.dev, self.budget, host, host.numel() if host is not None else 0)
+        self.ctx.set_streams(*streams)
+        self.init_params()
+        xp, lp = self.ctx.input_slot()
+        self.x_host, self.l_host = synth_batch(W, rank)
+        base = self.dev.data_ptr()
+        self.x_dev = self.dev[xp - base: xp - base + self.x_host.numel() * 4].view(torch.float32)
+        self.l_dev = self.dev[lp - base: lp - base + self.l_host.numel() * 4].view(torch.int32)
+        self.put_batch()
+        lo = self.ctx.loss_slot() - base
+        self.loss_dev = self.dev[lo: lo + 4].view(torch.float32)
+
+    def init_params(self):
+        """Identical on every rank and every call (seed 2): He-normal fan-in weights, BN gamma 1,
+        beta 0, FC bias 0; pooch_set_param also zeroes the momentum."""
+        import numpy as np
+        import synthdata
+        g = synthdata.rng(2)
+        for i, (name, numel) in enumerate(self.ctx.params()):
+            if name.endswith(".w"):
+                fan = numel // int(name_out_channels(self.ctx, name))
+                self.ctx.set_param(i, synthdata.he_normal((numel,), fan, g))
+            elif ".gamma" in name:
+                self.ctx.set_param(i, np.ones(numel, np.float32))
+            else:
+                self.ctx.set_param(i, np.zeros(numel, np.float32))
+
+    def put_batch(self):
+        import torch
+        self.x_dev.copy_(self.x_host)
+        self.l_dev.copy_(self.l_host)
+        torch.cuda.synchronize()
+
+    def grads(self):
+        return [self.ctx.get_param(i, 1) for i in range(len(self.ctx.params()))]
+
+    def params_now(self):
+        return [self.ctx.get_param(i, 0) for i in range(len(self.ctx.params()))]
+
+    def close(self):
+        self.ctx.close()
+        self.dev = self.x_dev = self.l_dev = self.loss_dev = None
+
+
+def timed(run, n_steps, world, barrier, e2e=False):
+    """K steps between CUDA events on the compute stream, max over ranks. e2e: every step's input
+    batch comes from pinned host memory -- H2D into a staging buffer on a side stream one step
+    ahead (double buffering, the previous step still running), then a device copy into the input
+    slot -- and the step's loss is read back to pinned host memory."""
+    import torch
+    import torch.distributed as dist
+    s = run.streams[0]
+    stage = None
+    if e2e:
+        free, _ = torch.cuda.mem_get_info()
+        if free > run.x_host.numel() * 4 + (512 << 20):
+            stage = (torch.empty_like(run.x_dev), torch.empty_like(run.l_dev))
+            side = torch.cuda.Stream()
+            staged, consumed = torch.cuda.Event(), torch.cuda.Event()
+    loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    if stage is not None:
+        side.wait_event(e0)
+        with torch.cuda.stream(side):
+            stage[0].copy_(run.x_host, non_blocking=True)
+            stage[1].copy_(run.l_host, non_blocking=True)
+        staged.record(side)
+    for _ in range(n_steps):
+        if e2e:
+            with torch.cuda.stream(s):
+                if stage is not None:      # this step's batch from the staging buffer
+                    s.wait_event(staged)
+                    run.x_dev.copy_(stage[0], non_blocking=True)
+                    run.l_dev.copy_(stage[1], non_blocking=True)
+                    consumed.record(s)
+                    side.wait_event(consumed)
+                    with torch.cuda.stream(side):   # next step's batch, overlapping this step
+                        stage[0].copy_(run.x_host, non_blocking=True)
+                        stage[1].copy_(run.l_host, non_blocking=True)
+                    staged.record(side)
+                else:
+                    run.x_dev.copy_(run.x_host, non_blocking=True)
+                    run.l_dev.copy_(run.l_host, non_blocking=True)
+        run.ctx.train_step(0.01, sync_loss=False)
+        if e2e:
+            with torch.cuda.stream(s):
+                loss_h.copy_(run.loss_dev, non_blocking=True)
+    e1.record(s)
+    barrier()
+    ms = e0.elapsed_time(e1) / n_steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64).cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, ("double-buffered (staging %d B)" % (run.x_host.numel() * 4) if stage is not None else "serial")
+
+
+def median_profile(ctx, iters, repeats):
+    """`repeats` profiles, element-wise median (plan stability against measurement noise,
+    VERDICT r01); the context keeps the median."""
+    import numpy as np
+    profs = [ctx.profile(iters) for _ in range(max(1, repeats))]
+    if len(profs) == 1:
+        return profs[0]
+    out = dict(profs[-1])
+    for k in ("fwd", "bwd", "rec", "d2h", "h2d"):
+        out[k] = [int(v) for v in np.median(np.array([p[k] for p in profs]), axis=0)]
+    out["tail"] = int(np.median([p["tail"] for p in profs]))
+    out["spread"] = {k: float(np.max(np.std([p[k] for p in profs], axis=0) / np.maximum(1, np.mean([p[k] for p in profs], axis=0))))
+                     for k in ("fwd", "bwd")}
+    ctx.set_profile(out["fwd"], out["bwd"], out["rec"], out["d2h"], out["h2d"], out["tail"])
+    return out
+
+
+def counts_of(cls):
+    return "%d/%d/%d" % (cls.count(0), cls.count(1), cls.count(2))
+
+
+def plan_paper(ctx, li_cap):
+    """PoocH exactly as the paper's Sec. 4.4: one search at the full budget (no plan grid, no
+    refinement; DESIGN.md Readings 40, 42), retried 2 % lower only if its ledger does not pack."""
+    os.environ["POOCH_PLAN_NO_GRID"] = "1"
+    os.environ["POOCH_PLAN_NO_REFINE"] = "1"
+    try:
+        return ctx.plan("pooch", li_cap=li_cap)
+    finally:
+        os.environ.pop("POOCH_PLAN_NO_GRID", None)
+        os.environ.pop("POOCH_PLAN_NO_REFINE", None)
+
+
+def one_step_bits(run, strategy, fixed=None):
+    """From the seeded parameters (momentum 0) and the resident batch: plan, one step; returns
+    (classes, loss bits, gradient arrays, loss)."""
+    import numpy as np
+    import torch
+    run.init_params()
+    cls, _ = run.ctx.plan(strategy, fixed=fixed)
+    loss = run.ctx.train_step(0.01, sync_loss=True)
+    torch.cuda.synchronize()
+    return cls, np.float32(loss).view(np.uint32), run.grads(), loss
+
+
+def same_bits(a, b):
+    import numpy as np
+    return a[1] == b[1] and all(np.array_equal(x.view(np.uint32), y.view(np.uint32)) for x, y in zip(a[2], b[2]))
+
+
 def our_arm(args):
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_1907_05013_b200.executor import Context
-    import synthdata
+    from paper_1907_05013_b200 import dp
+    from paper_1907_05013_b200.executor import PinnedHost
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dev_idx = local
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    numa = dp.bind_host_to_gpu(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     W = workload(args)
     W.fuse = bool(args.fuse) and not W.three
     if W.fuse:
         W.name += ", BN-ReLU prologue fusion (f2)"
-    batch, budget, wname = W.batch, W.budget, W.name
-    ctx = W.context(device=dev_idx)
-    ctx.set_precision(args.precision)
-    free, total = torch.cuda.mem_get_info()
-    if budget is None:
-        budget = int(free - (3 << 30))
-    budget = budget // 256 * 256
-    if world > 1:  # one budget for all ranks (free HBM can differ by a few MB): identical plans
-        t = torch.tensor([budget], dtype=torch.int64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        budget = int(t.item())
-    maps_total = sum(ctx_map_bytes(ctx))
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    # pinned host arena: sized for all-swap when the host allows, else 60 % of RAM per rank
+    ctx0 = W.context(device=local)
+    maps_total = sum(ctx_map_bytes(ctx0))
+    ctx0.close()
     host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.6 * os.sysconf("SC_PAGE_SIZE") *
-                         os.sysconf("SC_PHYS_PAGES") / max(1, world)))
-    host_bytes = host_bytes // 4096 * 4096
-    dev = torch.empty(budget, dtype=torch.uint8, device="cuda")
-    from paper_1907_05013_b200.executor import PinnedHost
+                         os.sysconf("SC_PHYS_PAGES") / max(1, world))) // 4096 * 4096
     while True:  # the host may cap page-locked memory: halve until registration succeeds
         try:
             host = PinnedHost(host_bytes)
@@ -270,78 +448,47 @@ def our_arm(args):
             if host_bytes < (8 << 30):
                 raise
             host_bytes = host_bytes // 2 // 4096 * 4096
-    streams = [torch.cuda.Stream() for _ in range(3)]
-    ctx.set_budget(dev, budget, host, host_bytes)
-    ctx.set_streams(*streams)
+    budget = W.budget
+    if budget is None:
+        free, _ = torch.cuda.mem_get_info()
+        # all free HBM minus 3 GiB of headroom, minus the e2e staging buffer (one input batch)
+        budget = int(free - (3 << 30) - synth_bytes(W))
+    if world > 1:  # one budget for all ranks (free HBM can differ by a few MB): identical plans
+        t = torch.tensor([budget], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        budget = int(t.item())
+    run = Run(W, budget, host, streams, rank, local, args.precision)
+    ctx = run.ctx
+    comm = None
     if world > 1:
-        from paper_1907_05013_b200.dp import broadcast_unique_id
-        ctx.set_comm(broadcast_unique_id(rank, device="cuda"), rank, world)
-    # parameters and the synthetic batch (seed 0 + rank / 1 + rank; identical weights)
-    g = synthdata.rng(2)
-    for i, (name, numel) in enumerate(ctx.params()):
-        if name.endswith(".w"):
-            fan = numel // int(name_out_channels(ctx, name))
-            ctx.set_param(i, synthdata.he_normal((numel,), fan, g))
-        elif ".gamma" in name:
-            ctx.set_param(i, np.ones(numel, np.float32))
-        else:
-            ctx.set_param(i, np.zeros(numel, np.float32))
-    xp, lp = ctx.input_slot()
-    x_host, l_host = synth_batch(W, rank)
-    base = dev.data_ptr()
-    x_dev = dev[xp - base: xp - base + x_host.numel() * 4].view(torch.float32)
-    l_dev = dev[lp - base: lp - base + l_host.numel() * 4].view(torch.int32)
-    x_dev.copy_(x_host)
-    l_dev.copy_(l_host)
-    torch.cuda.synchronize()
+        ctx.set_comm(dp.broadcast_unique_id(rank, device="cuda"), rank, world)
+        comm = ctx.comm_info()
+        print("[rank %d] NCCL communicator: nranks %d, rank %d, cuda device %d, numa node %d" % (
+            rank, comm[0], comm[1], comm[2], numa), file=sys.stderr, flush=True)
 
-    # ---- profile (Sec. 4.2) + plan (Sec. 4.4); max over ranks so every rank runs one plan
+    # ---- profile (Sec. 4.2; median of --profile-repeats) + plan (Sec. 4.4); max over ranks
     t0 = time.time()
-    prof = ctx.profile(args.profile_iters)
-    prof_s = time.time() - t0
+    prof = median_profile(ctx, args.profile_iters, args.profile_repeats)
     if world > 1:
-        from paper_1907_05013_b200.dp import agree_profile
-        agreed = agree_profile(prof, device="cuda")
+        agreed = dp.agree_profile(prof, device="cuda")
         ctx.set_profile(agreed["fwd"], agreed["bwd"], agreed["rec"], agreed["d2h"], agreed["h2d"], agreed["tail"])
+    prof_s = time.time() - t0
+    paper = None
+    if not args.no_paper and world == 1:
+        try:   # the paper's own PoocH (one search, no grid / refinement), measured on the executor
+            pc, pr = plan_paper(ctx, args.li_cap)
+            ctx.train_step(0.01, sync_loss=False)
+            pms, _ = timed(run, 3, world, barrier)
+            paper = {"ms_per_step": pms, "images_per_s": W.batch * 1000.0 / pms, "counts": counts_of(pc),
+                     "simulated_ms": pr["makespan_ns"] / 1e6, "classes": pc}
+        except Exception as e:  # infeasible is a result
+            paper = {"feasible": False, "why": str(e)[:200]}
     cls, rep = ctx.plan("pooch", li_cap=args.li_cap)
     counts = {"keep": cls.count(0), "swap": cls.count(1), "recompute": cls.count(2)}
     if args.dump_profile and rank == 0:
         with open(args.dump_profile, "w") as f:
-            json.dump({"workload": wname, "batch": batch, "budget": budget, "profile": prof, "classes": cls,
+            json.dump({"workload": W.name, "batch": W.batch, "budget": run.budget, "profile": prof, "classes": cls,
                        "report": {k: (v if isinstance(v, (int, float)) else str(v)) for k, v in rep.items()}}, f)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    lo = ctx.loss_slot() - base
-    loss_dev = dev[lo: lo + 4].view(torch.float32)
-
-    def timed(n_steps, e2e=False):
-        s = streams[0]
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
-        e0.record(s)
-        for _ in range(n_steps):
-            if e2e:
-                with torch.cuda.stream(s):
-                    x_dev.copy_(x_host, non_blocking=True)
-                    l_dev.copy_(l_host, non_blocking=True)
-            ctx.train_step(0.01, sync_loss=False)
-            if e2e:
-                with torch.cuda.stream(s):
-                    loss_h.copy_(loss_dev, non_blocking=True)
-        e1.record(s)
-        barrier()
-        ms = e0.elapsed_time(e1) / n_steps
-        if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64).cuda()
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
 
     if args.ncu_step:
         ctx.train_step(0.01, sync_loss=False)
@@ -354,51 +501,56 @@ def our_arm(args):
     for _ in range(args.warmup):
         ctx.train_step(0.01, sync_loss=False)
     torch.cuda.synchronize()
-    with Clocks(dev_idx) as clk:
-        ms = timed(args.steps)
-    ms_e2e = timed(max(2, args.steps // 2), e2e=True)
+    with Clocks(local) as clk:
+        ms, _ = timed(run, args.steps, world, barrier)
+    ms_e2e, e2e_mode = timed(run, max(3, args.steps // 2), world, barrier, e2e=True)
+    # every rank must hold the same weights after the same steps (identical init, summed gradients)
+    ident = dp.ranks_identical(dp.digest(run.params_now()))
     # instrumented step: per kernel family times (CUDA events on the launching streams)
     ctx.set_timing(True)
     ctx.train_step(0.01, sync_loss=True)
     fam = ctx.family_stats()
     segs = ctx.timing_segments()
-    tim = ctx.last_timing()
     ctx.set_timing(False)
     launches = kernel_launches(ctx, args.steps)
 
     ablation = None
     if args.ablation:
         ablation = {}
-        # the paper's strategies (Sec. 5.1-5.2) on the same executor; "pooch_paper" is PoocH
-        # without the executor's local refinement (DESIGN.md Reading 42), "pooch" with it
-        for strat in ("swap_all_naive", "swap_all", "swap_opt", "superneurons", "pooch_paper", "pooch"):
+        for strat in ("swap_all_naive", "swap_all", "swap_opt", "superneurons", "pooch"):
             try:
-                if strat == "pooch_paper":
-                    os.environ["POOCH_PLAN_NO_REFINE"] = "1"
-                c2, r2 = ctx.plan("pooch" if strat == "pooch_paper" else strat, li_cap=args.li_cap)
+                c2, r2 = ctx.plan(strat, li_cap=args.li_cap)
             except Exception as e:  # infeasible plans are a result (superneurons OOM)
                 ablation[strat] = {"feasible": False, "why": str(e)[:160]}
                 continue
-            finally:
-                os.environ.pop("POOCH_PLAN_NO_REFINE", None)
             ctx.train_step(0.01, sync_loss=False)
-            ms_s = timed(2)
-            ablation[strat] = {"feasible": True, "ms_per_step": ms_s, "images_per_s": batch * world * 1000.0 / ms_s,
-                               "simulated_ms": r2["makespan_ns"] / 1e6,
-                               "counts": [c2.count(0), c2.count(1), c2.count(2)]}
+            ms_s, _ = timed(run, 2, world, barrier)
+            ablation[strat] = {"feasible": True, "ms_per_step": ms_s, "images_per_s": W.batch * world * 1000.0 / ms_s,
+                               "simulated_ms": r2["makespan_ns"] / 1e6, "counts": counts_of(c2)}
+
+    # ---- correctness at the benchmarked size: one step of the adopted plan and one of another plan
+    # from identical parameters and batch must agree bit for bit (north_star), and the loss is finite
+    check = None
+    if not args.no_check and world == 1:
+        run.put_batch()
+        a = one_step_bits(run, "fixed", cls)
+        check = {"loss": float(a[3]), "loss_finite": bool(np.isfinite(a[3])), "plan_a": counts_of(cls)}
+        alts = []
+        if paper and paper.get("classes") and paper["classes"] != cls:
+            alts.append(("paper PoocH", "fixed", paper["classes"]))
+        alts += [("swap-opt", "swap_opt", None), ("in-core", "incore", None)]
+        for name, strat, fx in alts:
+            try:
+                b = one_step_bits(run, strat, fx)
+            except Exception:
+                continue
+            if b[0] == cls:
+                continue
+            check.update(plan_b=name + " " + counts_of(b[0]), bitexact=same_bits(a, b))
+            break
         ctx.plan("pooch", li_cap=args.li_cap)
 
-    # ---- in-core comparison (the same kernels, every map kept) where it fits
-    # (after the out-of-core context and its arena are released: the in-core run needs the HBM)
-    incore = None
-    if not args.no_incore and world == 1:
-        params_host = [ctx.get_param(i, 0) for i in range(len(ctx.params()))]
-        ctx.close()
-        dev = x_dev = l_dev = loss_dev = None  # noqa: F841 (drop the arena before the in-core run)
-        torch.cuda.empty_cache()
-        incore = incore_run(params_host, batch, streams, args)
-
-    value = batch * world * 1000.0 / ms
+    value = W.batch * world * 1000.0 / ms
     pk = peaks()
     roof = roofline(fam, pk, segs, args.precision)
     line = {
@@ -407,30 +559,49 @@ def our_arm(args):
         "vs_baseline": None,
         "dtype": "f32 (%s tensor-core contractions, fp32 accumulate/storage)" % ("3xtf32" if args.precision else "tf32"),
         "data": "synthetic (x ~ N(0,1), labels U[0,%d), He-normal weights; seeded)" % W.classes,
-        "config": {"workload": wname, "global_batch": batch * world, "seq_len": None,
-                   "parallelism": "dp%d" % world, "budget_bytes_per_gpu": budget,
-                   "host_arena_bytes": host_bytes, "l2": "inputs > L2 (maps are GBs)",
+        "config": {"workload": W.name, "global_batch": W.batch * world, "seq_len": None,
+                   "parallelism": "dp%d" % world, "budget_bytes_per_gpu": run.budget,
+                   "host_arena_bytes": host_bytes, "numa_node": numa, "l2": "inputs > L2 (maps are GBs)",
+                   "profile_mode": prof.get("mode"), "profile_s": prof_s,
                    "plan_counts": counts, "planner_ms": rep["wall_ms"], "planner_sims": rep["n_sims"],
-                   "profile_s": prof_s, "simulated_ms_per_step": rep["makespan_ns"] / 1e6,
+                   "simulated_ms_per_step": rep["makespan_ns"] / 1e6,
                    "arena_high_water_bytes": rep["arena_bytes"], "L_O": rep["lo_size"], "L_I": rep["li_size"]},
         "clocks": clk.summary(),
-        "e2e": {"value": batch * world * 1000.0 / ms_e2e, "unit": W.unit,
-                "h2d_bytes_per_step": int(x_host.numel() * 4 + l_host.numel() * 4), "d2h_bytes_per_step": 4},
+        "e2e": {"value": W.batch * world * 1000.0 / ms_e2e, "unit": W.unit, "input": e2e_mode,
+                "h2d_bytes_per_step": int(run.x_host.numel() * 4 + run.l_host.numel() * 4), "d2h_bytes_per_step": 4},
         "gpu_launches": launches,
         "roofline": roof,
         "swap": swap_stats(fam, prof),
         "families": families_table(fam, peaks(), segs, args.precision),
+        "ranks_identical": ident,
     }
+    if comm is not None:
+        line["nccl"] = {"nranks": comm[0], "comm_nranks_ok": comm[0] == world}
+    if paper is not None:
+        line["pooch_paper"] = {k: v for k, v in paper.items() if k != "classes"}
+    if check is not None:
+        line["loss_finite"] = check["loss_finite"]
+        line["bitexact"] = check
     if ablation is not None:
         line["ablation"] = ablation
     if W.three:
         line["voxels_per_s"] = value * W.in_hw ** 3
-    if incore is not None:
-        line["incore"] = incore
-        if W.three and incore.get("voxels_per_s"):
-            line["overhead_vs_incore"] = 1.0 - line["voxels_per_s"] / incore["voxels_per_s"]
-        elif incore.get("images_per_s"):
-            line["overhead_vs_incore"] = 1.0 - value / incore["images_per_s"]
+
+    # ---- the in-core comparison and the secondary cfg2 line (after the arenas are released)
+    if world == 1:
+        run.close()
+        run = ctx = None
+        torch.cuda.empty_cache()
+        if not args.no_incore:
+            incore, cfg2 = incore_and_cfg2(W, args, host, streams)
+            if incore is not None:
+                line["incore"] = incore
+                if W.three and incore.get("voxels_per_s"):
+                    line["overhead_vs_incore"] = 1.0 - line["voxels_per_s"] / incore["voxels_per_s"]
+                elif incore.get("images_per_s"):
+                    line["overhead_vs_incore"] = 1.0 - value / incore["images_per_s"]
+            if cfg2 is not None:
+                line["cfg2"] = cfg2
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_sample_3d(15.0) if W.three else cpu_sample(15.0, batch=1)
     if rank == 0:
@@ -577,59 +748,88 @@ def swap_stats(fam, prof):
     return out
 
 
-def incore_run(params_host, batch, streams, args):
-    """Same kernels with every map kept: needs the full footprint in HBM. For the 3D U-Net
-    (cfg4, which cannot fit) the same net at half the volume edge gives the per-voxel rate."""
+def incore_and_cfg2(W, args, host, streams):
+    """The same kernels with every map kept, at the largest batch that fits (the paper's per-image
+    convention): ResNet-50 at batch 640, the 3D U-Net at half the volume edge. For ResNet-50
+    also the secondary cfg2 line (BASELINE config 2: batch 640 under a 16 GiB budget): one step
+    of its plan against the in-core step from identical parameters and batch (bit-exact at the
+    full benchmarked size, north_star), and the plan from each profiling mode (Sec. 4.2, all-swap
+    iterations vs isolated timing) with its simulated and measured step time."""
+    import numpy as np
     import torch
-    W = workload(args)
-    W.fuse = bool(args.fuse) and not W.three
+    if W.three:
+        Wi = Workload(W.net, 1, None, W.name, W.in_hw // 2, W.classes, W.width)
+    else:
+        Wi = Workload(W.net, 640, None, "in-core ResNet-50 v1.5 batch 640", 224, W.classes)
+    Wi.fuse = W.fuse
+    incore, cfg2 = None, None
     try:
-        edge = W.in_hw // 2 if W.three else None
-        ctx = W.context(in_hw=edge)
-        ctx.set_precision(args.precision)
-        need = int(ctx.resident_bytes() + sum(ctx_map_bytes(ctx)) * 1.4)
+        probe = Wi.context()
+        need = int(probe.resident_bytes() + sum(ctx_map_bytes(probe)) * 1.4)
+        probe.close()
         free_now, _ = torch.cuda.mem_get_info()
         if need > free_now - (2 << 30):
-            return {"images_per_s": None, "note": "in-core does not fit (%d GB needed)" % (need >> 30)}
-        big = torch.empty(need // 256 * 256, dtype=torch.uint8, device="cuda")
-        ctx.set_budget(big, big.numel(), None, 0)
-        ctx.set_streams(*streams)
-        for i, (name, numel) in enumerate(ctx.params()):
-            ctx.set_param(i, params_host[i])
-        if W.three:  # its own input of the smaller volume
-            Wi = Workload(W.net, 1, None, W.name, edge, W.classes, W.width)
-            xh, lh = synth_batch(Wi, 0)
-            base = big.data_ptr()
-            xp, lp = ctx.input_slot()
-            big[xp - base: xp - base + xh.numel() * 4].view(torch.float32).copy_(xh)
-            big[lp - base: lp - base + lh.numel() * 4].view(torch.int32).copy_(lh)
-        ctx.profile(1)
-        ctx.plan("incore")
+            return {"images_per_s": None, "note": "in-core does not fit (%d GB needed)" % (need >> 30)}, None
+        ri = Run(Wi, need, None, streams, precision=args.precision)
+        ri.ctx.set_profile_mode("isolated")
+        ri.ctx.profile(1)
+        ref = one_step_bits(ri, "incore")
         for _ in range(2):
-            ctx.train_step(0.01, sync_loss=False)
+            ri.ctx.train_step(0.01, sync_loss=False)
+        ms, _ = timed(ri, max(3, args.steps // 2), 1, torch.cuda.synchronize)
+        ri.ctx.set_timing(True)
+        ri.ctx.train_step(0.01, sync_loss=False)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = max(2, args.steps)
-        e0.record(streams[0])
-        for _ in range(n):
-            ctx.train_step(0.01, sync_loss=False)
-        e1.record(streams[0])
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / n
-        ctx.set_timing(True)
-        ctx.train_step(0.01, sync_loss=False)
-        torch.cuda.synchronize()
-        fam = families_table(ctx.family_stats(), peaks(), ctx.timing_segments(), args.precision)
-        ctx.set_timing(False)
-        ctx.close()
-        del big
-        torch.cuda.empty_cache()
-        out = {"images_per_s": batch * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+        fam = families_table(ri.ctx.family_stats(), peaks(), ri.ctx.timing_segments(), args.precision)
+        ri.ctx.set_timing(False)
         if W.three:
-            out = {"volume_edge": edge, "voxels_per_s": edge ** 3 * 1000.0 / ms, "ms_per_step": ms, "families": fam}
-        return out
+            e = Wi.in_hw
+            incore = {"volume_edge": e, "voxels_per_s": e ** 3 * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+            ri.close()
+            return incore, None
+        incore = {"batch": Wi.batch, "images_per_s": Wi.batch * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+        if not args.no_cfg2:
+            W2 = Workload("resnet50", 640, 16 << 30, "cfg2: ResNet-50 v1.5 batch 640 224^2, device budget 16 GiB",
+                          224, W.classes)
+            W2.fuse = W.fuse
+            r2 = Run(W2, W2.budget, host, streams, precision=args.precision)
+            cfg2 = {"workload": W2.name}
+            for mode in ("auto", "isolated"):
+                r2.ctx.set_profile_mode(mode)
+                r2.init_params()
+                prof = r2.ctx.profile(args.profile_iters)
+                cls, rep = r2.ctx.plan("pooch", li_cap=args.li_cap)
+                for _ in range(2):
+                    r2.ctx.train_step(0.01, sync_loss=False)
+                ms2, _ = timed(r2, max(3, args.steps // 2), 1, torch.cuda.synchronize)
+                e = {"profile_mode": prof["mode"], "images_per_s": 640 * 1000.0 / ms2, "ms_per_step": ms2,
+                     "simulated_ms_per_step": rep["makespan_ns"] / 1e6, "plan_counts": counts_of(cls),
+                     "overhead_vs_incore": 1.0 - (640 * 1000.0 / ms2) / incore["images_per_s"]}
+                if prof["mode"] == "all_swap":
+                    e["all_swap_profile_step_ms"] = prof["step_ns"] / 1e6
+                r2.put_batch()
+                b = one_step_bits(r2, "fixed", cls)
+                e["loss_finite"] = bool(np.isfinite(b[3]))
+                e["bitexact_vs_incore"] = same_bits(b, ref)
+                if mode == "auto":
+                    cfg2.update(e)
+                else:
+                    cfg2["isolated_profile"] = e
+            r2.close()
+        ri.close()
     except Exception as e:  # report, never fake
-        return {"images_per_s": None, "note": "in-core run failed: %s" % e}
+        incore = incore or {"images_per_s": None, "note": "in-core run failed: %s" % str(e)[:200]}
+        if cfg2 is not None:
+            cfg2["error"] = str(e)[:200]
+    torch.cuda.empty_cache()
+    return incore, cfg2
+
+
+def synth_bytes(W):
+    """Bytes of one input batch (+ labels) as the GPU stores it (the e2e staging buffer)."""
+    if W.three:
+        return W.in_hw ** 3 * (32 + 1) * 4
+    return W.batch * (224 * 224 * 4 + 1) * 4
 
 
 def main():
@@ -637,6 +837,20 @@ def main():
     if args.impl == "reference":
         reference_arm(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # the driver launches N > 1 under torch.distributed.run; run by hand, relaunch the same way
+        import torch
+        from paper_1907_05013_b200.dp import relaunch_argv
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print("bench.py --gpus %d needs %d visible GPUs, found %d" % (args.gpus, args.gpus, have),
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
+        port = 29500 + os.getpid() % 1000
+        sys.exit(subprocess.call(relaunch_argv(os.path.abspath(__file__), sys.argv[1:], args.gpus, port)))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print("bench.py: WORLD_SIZE %s != --gpus %d" % (os.environ["WORLD_SIZE"], args.gpus), file=sys.stderr)
+        sys.exit(2)
     our_arm(args)
 
 

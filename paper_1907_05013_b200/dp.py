@@ -43,3 +43,80 @@ def broadcast_unique_id(rank: int, group=None, device="cpu") -> bytes:
         buf.copy_(torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8))
     dist.broadcast(buf, 0, group=group)
     return bytes(buf.cpu().numpy().tobytes())
+
+
+def relaunch_argv(script: str, argv, nproc: int, port: int):
+    """`bench.py --gpus N` run without a launcher (WORLD_SIZE unset) re-executes itself under
+    torch.distributed.run with one process per GPU on 127.0.0.1 -- the driver's own launch line."""
+    import sys
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % nproc,
+            "--master-addr", "127.0.0.1", "--master-port", str(port), script] + list(argv)
+
+
+def pci_numa_node(bus_id: str) -> int:
+    """NUMA node of a PCI device from sysfs (-1 when unknown / single-node)."""
+    bus_id = bus_id.lower()
+    if bus_id.count(":") == 1:
+        bus_id = "0000:" + bus_id
+    try:
+        with open("/sys/bus/pci/devices/%s/numa_node" % bus_id) as f:
+            return int(f.read().strip())
+    except (OSError, ValueError):
+        return -1
+
+
+def node_cpus(node: int):
+    """CPU ids of a NUMA node (sysfs cpulist, e.g. '0-15,32-47')."""
+    try:
+        with open("/sys/devices/system/node/node%d/cpulist" % node) as f:
+            spec = f.read().strip()
+    except OSError:
+        return []
+    out = []
+    for part in spec.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            out.extend(range(int(a), int(b) + 1))
+        elif part:
+            out.append(int(part))
+    return out
+
+
+def bind_host_to_gpu(device: int) -> int:
+    """Pin this rank's CPU affinity to its GPU's NUMA node, so that the pinned host arena it
+    registers next (first touch by this thread) lands in that node's memory and the swap copies
+    cross no inter-socket link. Returns the node, or -1 when the box has no NUMA information."""
+    import os
+
+    import torch
+    p = torch.cuda.get_device_properties(device)
+    bus = getattr(p, "pci_bus_id", None)
+    if bus is None:
+        return -1
+    bus_id = "%04x:%02x:%02x.0" % (getattr(p, "pci_domain_id", 0), bus, getattr(p, "pci_device_id", 0))
+    node = pci_numa_node(bus_id)
+    cpus = node_cpus(node) if node >= 0 else []
+    allowed = os.sched_getaffinity(0)
+    cpus = [c for c in cpus if c in allowed]
+    if cpus:
+        os.sched_setaffinity(0, cpus)
+    return node if cpus else -1
+
+
+def digest(arrays) -> str:
+    """sha256 over the bytes of a list of arrays (parameter checksum for rank consistency)."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(memoryview(a).cast("B"))
+    return h.hexdigest()
+
+
+def ranks_identical(local_digest: str, group=None) -> bool:
+    """True when every rank holds the same digest (all_gather_object)."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return True
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, local_digest, group=group)
+    return all(d == out[0] for d in out)

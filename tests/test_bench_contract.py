@@ -36,3 +36,27 @@ def test_reference_arm_runs_on_cpu():
     d = json.loads(line)
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_gpus_n_without_launcher_relaunches_or_fails_loudly():
+    """`bench.py --gpus 2` run by hand (no WORLD_SIZE) re-executes itself under
+    torch.distributed.run; with fewer visible GPUs than asked it exits non-zero with a message
+    instead of silently measuring one GPU."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600, env=env)
+    assert r.returncode == 2, (r.returncode, r.stderr[-800:])
+    assert "needs 2 visible GPUs" in r.stderr
+    assert not [x for x in r.stdout.splitlines() if x.startswith("{")]
+
+
+def test_relaunch_line_is_the_drivers():
+    sys.path.insert(0, ROOT)
+    from paper_1907_05013_b200.dp import relaunch_argv
+    a = relaunch_argv("/x/bench.py", ["--gpus", "4", "--steps", "3"], 4, 29555)
+    assert a[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in a and "--nnodes=1" in a
+    assert a[a.index("--master-addr") + 1] == "127.0.0.1" and a[a.index("--master-port") + 1] == "29555"
+    assert a[-5:] == ["/x/bench.py", "--gpus", "4", "--steps", "3"]

@@ -71,3 +71,38 @@ def test_dp_gradient_is_mean_of_shards():
     p_mean, _ = nets.sgd_step(params, w0, {k: (gs[0][k] + gs[1][k]) / 2 for k in params}, 0.1)
     for k in params:
         np.testing.assert_allclose(p_sum[k], p_mean[k], rtol=1e-12, atol=1e-15)
+
+
+def _ident_worker(rank, world, port, q, differ):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1907_05013_b200.dp import digest, ranks_identical
+    arrs = [np.arange(1000, dtype=np.float32), np.ones(7, np.float32)]
+    if differ and rank == 1:
+        arrs[0][999] = np.nextafter(arrs[0][999], np.float32(2e3))   # one ulp on one rank
+    q.put((rank, ranks_identical(digest(arrs))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("differ", [False, True])
+def test_ranks_identical_checksum(differ):
+    """bench.py's post-step rank-consistency check: every rank's parameter digest is gathered and
+    compared; one ulp of difference on one rank is caught on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ident_worker, args=(r, 2, port, q, differ)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert [ok for _, ok in res] == [not differ, not differ]
+
+
+def test_numa_helpers_degrade_gracefully():
+    from paper_1907_05013_b200.dp import node_cpus, pci_numa_node
+    assert pci_numa_node("ffff:ff:1f.7") == -1          # no such device
+    assert node_cpus(4096) == []                        # no such node
+    c = node_cpus(0)
+    assert c == [] or (all(isinstance(v, int) for v in c) and c == sorted(c))

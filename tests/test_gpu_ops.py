@@ -241,3 +241,35 @@ def test_conv_bnrelu_on_load(case, prec):
     assert rel(s1.cpu().numpy().astype(np.float64).sum(0), flat.sum(0)) < TOL_OP
     refw = L.conv2d_wgrad(rn, gy.transpose(0, 3, 1, 2).astype(np.float64), (K, Cin, R, R), s, p).transpose(0, 2, 3, 1)
     assert rel(ddw.cpu().numpy(), refw) < tol
+
+
+def _emulated_3xtf32(A, B):
+    """The 3xTF32 products with EXACT (fp64) accumulation: hi = trunc_tf32(x), lo = trunc_tf32(x -
+    hi) (the tensor core truncates both, DESIGN.md Reading 27), D = Ah Bh + Ah Bl + Al Bh."""
+    t = lambda x: (x.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32).astype(np.float64)
+    ah, bh = t(A), t(B)
+    al, bl = t(A - ah.astype(np.float32)), t(B - bh.astype(np.float32))
+    return ah @ bh.T + ah @ bl.T + al @ bh.T
+
+
+@pytest.mark.parametrize("K", [576, 4608, 32768])
+def test_3xtf32_error_against_fp32(K):
+    """How accurate the contraction kernels are next to plain fp32 (Reading 28 sets the gradient
+    gate from this): rel-L2 vs fp64 of the GPU's 3xTF32 GEMM, of CPU fp32 BLAS on the same operands,
+    and of the 3xTF32 products accumulated exactly (isolating the tensor core's accumulation)."""
+    lib = _lib()
+    g = synthdata.rng(K)
+    M, N = 512, 256
+    A = g.standard_normal((M, K)).astype(np.float32)
+    B = g.standard_normal((N, K)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dD = torch.zeros((1, M, N), dtype=torch.float32, device="cuda")
+    lib.check(lib.lib.pooch_op_gemm_test(ptr(dA), ptr(dB), ptr(dD), M, N, K, 2, 0, 128, 1, None))
+    torch.cuda.synchronize()
+    e_gpu = rel(dD.cpu().numpy()[0].astype(np.float64), ref)
+    e_f32 = rel((A @ B.T).astype(np.float64), ref)
+    e_emu = rel(_emulated_3xtf32(A, B), ref)
+    print("\nK=%d: 3xTF32 GPU %.2e, fp32 BLAS %.2e, 3xTF32 products exactly accumulated %.2e (GPU / fp32 = %.1f)"
+          % (K, e_gpu, e_f32, e_emu, e_gpu / e_f32))
+    assert e_gpu < TOL_X3
