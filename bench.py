@@ -805,6 +805,13 @@ def incore_and_cfg2(W, args, host, streams):
                 e = {"profile_mode": prof["mode"], "images_per_s": 640 * 1000.0 / ms2, "ms_per_step": ms2,
                      "simulated_ms_per_step": rep["makespan_ns"] / 1e6, "plan_counts": counts_of(cls),
                      "overhead_vs_incore": 1.0 - (640 * 1000.0 / ms2) / incore["images_per_s"]}
+                if mode == "auto":   # per kernel family, against the in-core step's (same batch)
+                    r2.ctx.set_timing(True)
+                    r2.ctx.train_step(0.01, sync_loss=False)
+                    torch.cuda.synchronize()
+                    e["families"] = families_table(r2.ctx.family_stats(), peaks(), r2.ctx.timing_segments(),
+                                                   args.precision)
+                    r2.ctx.set_timing(False)
                 if prof["mode"] == "all_swap":
                     e["all_swap_profile_step_ms"] = prof["step_ns"] / 1e6
                 r2.put_batch()

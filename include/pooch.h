@@ -424,6 +424,33 @@ pooch_status pooch_op_maxpool2d_fwd(const float* x, float* y, int32_t N, int32_t
                                     int32_t s, int32_t p, void* stream);
 pooch_status pooch_op_maxpool2d_bwd(const float* x, const float* gy, float* gx, void* arg_ws, int32_t N, int32_t H,
                                     int32_t W, int32_t C, int32_t k, int32_t s, int32_t p, void* stream);
+/* Training-mode BN + ReLU passes the executor runs after a convolution (Sec. 2.1 layer math; the
+ * 3D U-Net's conv3d -> BN -> ReLU -> max-pool chain), on NDHWC / NHWC device buffers of `rows`
+ * pixels x C channels (C % 4 == 0; rows * C may exceed 2^31), launched on `stream`:
+ *   bn_finalize : per-channel mean, invstd = 1/sqrt(var + 1e-5), scale = gamma * invstd,
+ *                 shift = beta - mean * scale (each [C]) from the conv forward's per-M-tile column
+ *                 sums tile_sum / tile_sq [tiles][C] (pooch_op_conv_fwd's stat_sum / stat_sq) over
+ *                 `count` pixels, reduced in a fixed order in fp64; ws: pooch_op_bn_ws_bytes(C) B.
+ *   bn_relu_fwd : y = relu(fma(x, scale, shift)).
+ *   bn_relu_bwd : dz = gy * [relu input > 0] (recomputed from x, scale, shift exactly as the forward);
+ *                 dbeta = sum dz, dgamma = sum dz * xhat (per channel, fixed order);
+ *                 gx = gamma * invstd * (dz - dbeta / rows - xhat * dgamma / rows); ws as above.
+ * 3D max-pool, 2x2x2 windows, stride 2, no padding, over x [D][H][W][C] (batch 1):
+ *   maxpool3d_fwd : y [D/2][H/2][W/2][C];  maxpool3d_bwd : gx (=|+=) the gradient routed to the FIRST
+ *                 maximum of every window in (d, h, w) row-major order (Reading 25), argmax from x.
+ * POOCH_EUSAGE on null pointers or bad shapes. Used by the parity tests. */
+size_t pooch_op_bn_ws_bytes(int32_t C);
+pooch_status pooch_op_bn_finalize(const float* tile_sum, const float* tile_sq, int32_t tiles, int32_t C, int64_t count,
+                                  const float* gamma, const float* beta, float* mean, float* invstd, float* scale,
+                                  float* shift, void* ws, void* stream);
+pooch_status pooch_op_bn_relu_fwd(const float* x, const float* scale, const float* shift, float* y, int64_t rows,
+                                  int32_t C, void* stream);
+pooch_status pooch_op_bn_relu_bwd(const float* x, const float* gy, const float* scale, const float* shift,
+                                  const float* mean, const float* invstd, const float* gamma, float* dgamma,
+                                  float* dbeta, float* gx, int64_t rows, int32_t C, void* ws, void* stream);
+pooch_status pooch_op_maxpool3d_fwd(const float* x, float* y, int32_t D, int32_t H, int32_t W, int32_t C, void* stream);
+pooch_status pooch_op_maxpool3d_bwd(const float* x, const float* gy, float* gx, int32_t D, int32_t H, int32_t W,
+                                    int32_t C, int32_t accumulate, void* stream);
 /* D[split][M][N] = A * B^T on the tensor-core core, A [M][K] and B [N][K] row-major (K-major);
  * a_mn = 2 selects the 3xTF32 path, other non-zero a_mn / b_mn (MN-major operands) return
  * POOCH_EUSAGE; bn in {64,128,256} (64/128 for 3xTF32); splits >= 1. Unit test only. */

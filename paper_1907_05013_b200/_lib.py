@@ -124,6 +124,13 @@ SIGNATURES = {
     "pooch_op_conv_wgrad_bnrelu": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pooch_op_maxpool2d_fwd": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_op_maxpool2d_bwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "pooch_op_bn_ws_bytes": (c_sz, [c_i32]),
+    "pooch_op_bn_finalize": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pooch_op_bn_relu_fwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
+    "pooch_op_bn_relu_bwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp,
+                                     c_vp]),
+    "pooch_op_maxpool3d_fwd": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "pooch_op_maxpool3d_bwd": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_set_profile_mode": (c_i32, [c_vp, c_i32]),
     "pooch_comm_info": (c_i32, [c_vp, P(c_i32), P(c_i32), P(c_i32)]),
     "pooch_op_gemm_test": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),

