@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpooch.so")
+LIB_PATH = os.environ.get("POOCH_LIB") or os.path.join(_HERE, "libpooch.so")
 
 
 class PoochError(RuntimeError):

@@ -11,8 +11,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libpooch.so")
-OBJ = os.path.join(HERE, "build_obj")
+# POOCH_BUILD_VARIANT=tag builds an experiment variant (extra flags from POOCH_BUILD_FLAGS) into
+# libpooch_<tag>.so / build_obj_<tag>; load it with POOCH_LIB=<path> (A/B kernel timing only)
+_VARIANT = os.environ.get("POOCH_BUILD_VARIANT", "")
+OUT = os.path.join(HERE, "libpooch%s.so" % ("_" + _VARIANT if _VARIANT else ""))
+OBJ = os.path.join(HERE, "build_obj%s" % ("_" + _VARIANT if _VARIANT else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-lineinfo",
@@ -59,4 +62,5 @@ def build(jobs: int | None = None, extra=(), verbose=False) -> str:
 
 if __name__ == "__main__":
     extra = ["-Xptxas", "-v"] if "--ptxas" in sys.argv else []
+    extra += os.environ.get("POOCH_BUILD_FLAGS", "").split()
     print(build(extra=extra, verbose=True))

@@ -516,7 +516,6 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
   constexpr uint32_t A_TCOL = 2u * BN;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
   constexpr bool AUX = igemm_aux(MODE, X3, XF);
   using SM = GemmSmem<BN, STAGES, X3, AT, NSTG>;
-  constexpr int LAG = STAGES - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);

@@ -255,3 +255,34 @@ def test_graph_replay_bit_identical_to_eager(tiny):
         assert loss == runs[0][0]
         for a, b in zip(bits, runs[0][1]):
             assert np.array_equal(a, b)
+
+
+def test_profiling_modes(tiny):
+    """Sec. 4.2: with a host arena that holds every map, pooch_profile measures real all-swap
+    iterations (per-task times under the copy traffic, every swapped map's copy time and issue time);
+    with an undersized host arena AUTO falls back to isolated timing and ALL_SWAP refuses."""
+    from paper_1907_05013_b200._lib import PoochError
+    ctx = tiny["ctx"]
+    dev, host, ss = ctx._torch
+    _put_batch(ctx, tiny["x"], tiny["t"])
+    ctx.set_profile_mode("auto")
+    p = ctx.profile(2)
+    assert p["mode"] == "all_swap" and p["step_ns"] > 0
+    swapped = [m for m in range(ctx.n) if p["d2h_issue"][m] >= 0]
+    assert swapped and all(p["h2d_issue"][m] > p["d2h_issue"][m] for m in swapped)
+    assert all(v > 0 for v in p["fwd"] + p["bwd"])
+    cls, rep = ctx.plan("pooch")                 # plans from the all-swap profile
+    assert rep["feasible"]
+    small = 4096
+    ctx.set_budget(dev, dev.numel(), host, small)   # host arena far below the maps
+    load_params(ctx, tiny["params"])
+    _put_batch(ctx, tiny["x"], tiny["t"])
+    assert ctx.profile(1)["mode"] == "isolated"
+    ctx.set_profile_mode("all_swap")
+    with pytest.raises(PoochError) as e:
+        ctx.profile(1)
+    assert e.value.status == 2
+    ctx.set_profile_mode("auto")
+    ctx.set_budget(dev, dev.numel(), host, host.numel())
+    load_params(ctx, tiny["params"])
+    ctx.profile(2)
