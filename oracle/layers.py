@@ -315,3 +315,78 @@ def sgd_momentum(w, v, g, lr, mu=SGD_MOMENTUM, grad_scale=1.0):
     """v <- mu v + s g ; w <- w - lr v  (update step; s = 1/W under DP)."""
     v_new = mu * v + grad_scale * g
     return w - lr * v_new, v_new
+
+
+# -------------------------------------------------------- AlexNet layers (SURVEY 8(f) f3)
+# The paper's second image-recognition workload (P:L361, P:L386, P:L453) is AlexNet [alexnet] in
+# Chainer's single-tower form: conv (+bias) -> ReLU -> local response normalisation -> max-pool,
+# and fully-connected layers with ReLU and dropout.
+LRN_N, LRN_K, LRN_ALPHA, LRN_BETA = 5, 2.0, 1e-4, 0.75   # Krizhevsky et al. / Chainer defaults
+
+
+def conv2d_bias_fwd(x, w, b, stride=1, pad=0):
+    """conv2d_fwd plus a per-output-channel bias."""
+    return conv2d_fwd(x, w, stride, pad) + b.reshape(1, -1, 1, 1)
+
+
+def lrn_fwd(x, n=LRN_N, k=LRN_K, alpha=LRN_ALPHA, beta=LRN_BETA):
+    """Local response normalisation across channels (NCHW):
+    y[c] = x[c] / (k + alpha / n * sum_{c' = c - n//2 .. c + n//2} x[c']^2) ** beta
+    (channels outside [0, C) contribute nothing). Returns (y, s) with s the denominator base."""
+    C = x.shape[1]
+    sq = x * x
+    s = np.zeros_like(x)
+    for c in range(C):
+        lo, hi = max(0, c - n // 2), min(C, c + n // 2 + 1)
+        s[:, c] = sq[:, lo:hi].sum(axis=1)
+    s = k + (alpha / n) * s
+    return x * s ** (-beta), s
+
+
+def lrn_bwd(dy, x, n=LRN_N, k=LRN_K, alpha=LRN_ALPHA, beta=LRN_BETA):
+    """Adjoint of lrn_fwd: with s_j as above and t_j = dy_j x_j s_j^(-beta - 1),
+    dx_c = dy_c s_c^(-beta) - (2 alpha beta / n) x_c sum_{j : |j - c| <= n//2} t_j."""
+    _, s = lrn_fwd(x, n, k, alpha, beta)
+    t = dy * x * s ** (-beta - 1.0)
+    C = x.shape[1]
+    acc = np.zeros_like(x)
+    for c in range(C):
+        lo, hi = max(0, c - n // 2), min(C, c + n // 2 + 1)
+        acc[:, c] = t[:, lo:hi].sum(axis=1)
+    return dy * s ** (-beta) - (2.0 * alpha * beta / n) * x * acc
+
+
+def _fmix32(h):
+    """MurmurHash3's 32-bit finaliser on uint32 arrays (wrap-around arithmetic)."""
+    h = np.asarray(h, dtype=np.uint32).copy()
+    h ^= h >> np.uint32(16)
+    h *= np.uint32(0x85EBCA6B)
+    h ^= h >> np.uint32(13)
+    h *= np.uint32(0xC2B2AE35)
+    h ^= h >> np.uint32(16)
+    return h
+
+
+def dropout_keep(shape, ratio, seed, step, task):
+    """Counter-based dropout mask (the GPU implements the same generator; random numbers the
+    method draws are a function of (seed, step, task, element index), so a recomputed forward
+    reproduces its mask): key = fmix32(seed ^ fmix32(step * 0x9E3779B9 + task)), element i of the
+    row-major [rows, cols] output is kept iff fmix32(key ^ fmix32(i)) >= floor(ratio * 2^32)."""
+    with np.errstate(over="ignore"):
+        key = _fmix32(np.uint32(seed) ^ _fmix32(np.uint32(step) * np.uint32(0x9E3779B9) + np.uint32(task)))
+        idx = np.arange(int(np.prod(shape)), dtype=np.uint64).astype(np.uint32)
+        u = _fmix32(key ^ _fmix32(idx))
+    thresh = np.uint32(min(int(ratio * 4294967296.0), 4294967295))
+    return (u >= thresh).reshape(shape)
+
+
+def fc_relu_dropout_fwd(x, w, b, keep, ratio):
+    """y = keep * relu(x W^T + b) / (1 - ratio)  (inverted dropout, ratio = drop probability)."""
+    z = fc_fwd(x, w, b)
+    return np.where(keep, np.maximum(z, 0.0) / (1.0 - ratio), 0.0), z
+
+
+def fc_relu_dropout_bwd(dy, x, w, z, keep, ratio):
+    """Adjoint of fc_relu_dropout_fwd: dz = dy * keep * [z > 0] / (1 - ratio); (dx, dW, db)."""
+    dz = np.where(keep & (z > 0), dy / (1.0 - ratio), 0.0)
+    return fc_bwd(dz, x, w)

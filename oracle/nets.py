@@ -55,12 +55,15 @@ class Task:
     k: int = 0              # conv/pool kernel size
     cin: int = 0            # conv input channels (true, unpadded)
     bn: str = ""            # bnrelu_conv: name of the fused BN-ReLU (its gamma / beta)
+    ratio: float = 0.0      # fc_relu_drop: dropout probability
 
     @property
     def needs(self):
         """Maps bwd(task) reads (see module docstring)."""
-        if self.kind in ("conv", "maxpool", "upconv", "bnrelu_conv"):
+        if self.kind in ("conv", "maxpool", "upconv", "bnrelu_conv", "lrn"):
             return [i for i in self.inputs if i >= 0]
+        if self.kind in ("conv_relu", "fc_relu_drop"):
+            return None     # filled by Net (self id needed: the ReLU mask comes from the output)
         if self.kind in ("bnrelu", "tail_proj", "tail_id"):
             return [i for i in self.inputs if i >= 0]
         if self.kind == "avgpool":
@@ -87,7 +90,7 @@ class Net:
 
     def needs(self, i):
         t = self.tasks[i]
-        if t.kind in ("fc_ce", "head_ce"):
+        if t.kind in ("fc_ce", "head_ce", "conv_relu", "fc_relu_drop"):
             return sorted([j for j in t.inputs if j >= 0] + [i])
         return sorted(t.needs)
 
@@ -142,6 +145,39 @@ def resnet50(in_hw: int = 224, classes: int = 1000, v15: bool = True) -> Net:
             hw, cin = hw2, out
     a = net.add(Task("avgpool", "avgpool", [x], (cin, 1, 1)))
     net.add(Task("fc", "fc_ce", [a], (classes, 1, 1), cin=cin))
+    return net
+
+
+def alexnet(in_hw: int = 227, classes: int = 1000, drop: float = 0.5) -> Net:
+    """AlexNet [alexnet], the paper's compute-heavy workload, in the
+    single-tower form of Chainer's example: conv1 11x11/4 (96) -> ReLU -> LRN -> max-pool 3/2;
+    conv2 5x5 pad 2 (256) -> ReLU -> LRN -> max-pool 3/2; conv3 3x3 (384), conv4 3x3 (384),
+    conv5 3x3 (256) each -> ReLU, max-pool 3/2 after conv5; fc6 (4096), fc7 (4096) each -> ReLU ->
+    dropout; fc8 (classes) -> softmax CE. Convolutions and FC layers carry biases. Tasks:
+    ``conv_relu`` y = relu(conv(x) + b) (bwd needs {x, y}), ``lrn`` (bwd needs {x}), ``maxpool``,
+    ``fc_relu_drop`` y = dropout(relu(x W^T + b)) (bwd needs {x, y}), ``fc_ce``. 13 maps."""
+    net = Net("alexnet", (3, in_hw, in_hw), classes)
+
+    def co(h, k, s, p):
+        return (h + 2 * p - k) // s + 1
+
+    h = co(in_hw, 11, 4, 0)
+    x = net.add(Task("conv1", "conv_relu", [-1], (96, h, h), 4, 0, 11, 3))
+    x = net.add(Task("lrn1", "lrn", [x], (96, h, h)))
+    h = co(h, 3, 2, 0)
+    x = net.add(Task("pool1", "maxpool", [x], (96, h, h), 2, 0, 3))
+    x = net.add(Task("conv2", "conv_relu", [x], (256, h, h), 1, 2, 5, 96))
+    x = net.add(Task("lrn2", "lrn", [x], (256, h, h)))
+    h = co(h, 3, 2, 0)
+    x = net.add(Task("pool2", "maxpool", [x], (256, h, h), 2, 0, 3))
+    x = net.add(Task("conv3", "conv_relu", [x], (384, h, h), 1, 1, 3, 256))
+    x = net.add(Task("conv4", "conv_relu", [x], (384, h, h), 1, 1, 3, 384))
+    x = net.add(Task("conv5", "conv_relu", [x], (256, h, h), 1, 1, 3, 384))
+    h = co(h, 3, 2, 0)
+    x = net.add(Task("pool5", "maxpool", [x], (256, h, h), 2, 0, 3))
+    x = net.add(Task("fc6", "fc_relu_drop", [x], (4096, 1, 1), cin=256 * h * h, ratio=drop))
+    x = net.add(Task("fc7", "fc_relu_drop", [x], (4096, 1, 1), cin=4096, ratio=drop))
+    net.add(Task("fc8", "fc_ce", [x], (classes, 1, 1), cin=4096))
     return net
 
 
@@ -225,8 +261,13 @@ def param_shapes(net: Net):
         if t.kind == "bnrelu_conv":     # the fused BN's parameters first (the plain graph's order)
             shapes[t.bn + ".gamma"] = (t.cin,)
             shapes[t.bn + ".beta"] = (t.cin,)
-        if t.kind in ("conv", "bnrelu_conv"):
+        if t.kind in ("conv", "bnrelu_conv", "conv_relu"):
             shapes[t.name + ".w"] = (t.out_chw[0], t.cin) + (t.k,) * (len(t.out_chw) - 1)
+            if t.kind == "conv_relu":
+                shapes[t.name + ".b"] = (t.out_chw[0],)
+        elif t.kind == "fc_relu_drop":
+            shapes[t.name + ".w"] = (t.out_chw[0], t.cin)
+            shapes[t.name + ".b"] = (t.out_chw[0],)
         elif t.kind == "upconv":
             shapes[t.name + ".w"] = (t.cin, t.out_chw[0], 2, 2, 2)
         elif t.kind == "bnrelu":
@@ -250,7 +291,7 @@ def _flat_hwc(x):
 
 
 def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndarray, map_grads=None,
-                     precision: str = "fp64"):
+                     precision: str = "fp64", rng=(0, 0)):
     """One fp64 fwd + bwd of ``net``. ``x_nhwc`` is the (unpadded)
     input batch in NHWC; params are promoted to fp64. Returns (loss, grads,
     outputs) with grads keyed like ``params`` and outputs the fp64 task
@@ -258,7 +299,8 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
     gradient of every map. ``precision="tf32"`` rounds the operands of every
     contraction (conv fwd / dgrad / wgrad, FC) with ``layers.tf32`` -- the
     kernels' operand precision -- and keeps everything else in fp64.
-    ``precision="fp32"`` runs the same code with every array in fp32 (NumPy
+    ``rng`` = (seed, step) of the counter-based dropout masks (``layers.dropout_keep``, salted
+    with the task id). ``precision="fp32"`` runs the same code with every array in fp32 (NumPy
     keeps fp32 through every layer call; the contractions are fp32 BLAS): the
     oracle's fp32 mode, which measures how far plain fp32 arithmetic alone
     moves a result from fp64 (DESIGN.md Reading 28)."""
@@ -313,6 +355,19 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             y = (L.maxpool3d_fwd(get(t.inputs[0]), t.k, t.stride) if three
                  else L.maxpool_fwd(get(t.inputs[0]), t.k, t.stride, t.pad))
             cache = None
+        elif t.kind == "conv_relu":
+            y = L.relu_fwd(L.conv2d_bias_fwd(q(get(t.inputs[0])), q(P[t.name + ".w"]), P[t.name + ".b"],
+                                             t.stride, t.pad))
+            cache = None
+        elif t.kind == "lrn":
+            y, _ = L.lrn_fwd(get(t.inputs[0]))
+            cache = None
+        elif t.kind == "fc_relu_drop":
+            xf = _flat_hwc(get(t.inputs[0]))
+            keep = L.dropout_keep((xf.shape[0], t.out_chw[0]), t.ratio, rng[0], rng[1], len(outs))
+            yf, z = L.fc_relu_dropout_fwd(q(xf), q(P[t.name + ".w"]), P[t.name + ".b"], keep, t.ratio)
+            y = yf[:, :, None, None]
+            cache = (xf, z, keep)
         elif t.kind == "avgpool":
             y = L.avgpool_fwd(get(t.inputs[0]))[:, :, None, None]
             cache = None
@@ -405,6 +460,24 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
         elif t.kind == "maxpool":
             acc(t.inputs[0], L.maxpool3d_bwd(dy, get(t.inputs[0]), t.k, t.stride) if three
                 else L.maxpool_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad))
+        elif t.kind == "conv_relu":
+            dz = L.relu_bwd(dy, outs[i])
+            xin = get(t.inputs[0])
+            w = P[t.name + ".w"]
+            grads[t.name + ".w"] += L.conv2d_wgrad(q(xin), q(dz), w.shape, t.stride, t.pad)
+            grads[t.name + ".b"] += dz.sum(axis=(0, 2, 3))
+            if t.inputs[0] >= 0:
+                acc(t.inputs[0], L.conv2d_dgrad(q(dz), q(w), xin.shape, t.stride, t.pad))
+        elif t.kind == "lrn":
+            acc(t.inputs[0], L.lrn_bwd(dy, get(t.inputs[0])))
+        elif t.kind == "fc_relu_drop":
+            xf, z, keep = caches[i]
+            dxf, dw, db = L.fc_relu_dropout_bwd(q(dy[:, :, 0, 0]), q(xf), q(P[t.name + ".w"]), z, keep, t.ratio)
+            grads[t.name + ".w"] += dw
+            grads[t.name + ".b"] += db
+            src = get(t.inputs[0])
+            n, c, h, w = src.shape
+            acc(t.inputs[0], dxf.reshape(n, h, w, c).transpose(0, 3, 1, 2))
         elif t.kind == "avgpool":
             acc(t.inputs[0], L.avgpool_bwd(dy[:, :, 0, 0], get(t.inputs[0]).shape))
     if map_grads is not None:
