@@ -48,6 +48,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 METRIC = "ResNet-50 images/s at >HBM batch, 1/2/4/8 B200; overhead vs in-core; swap GB/s"
+METRIC_ALEX = "AlexNet images/s at a batch exceeding the device budget; overhead vs in-core; swap GB/s"
 METRIC_3D = "3D U-Net volumes/s at a >HBM footprint (batch 1, 256^3); overhead vs in-core per voxel; swap GB/s"
 
 
@@ -57,7 +58,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg4", "alexnet"])
     ap.add_argument("--edge", type=int, default=None, help="cfg4: volume edge (default 256)")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--budget-gib", type=float, default=None)
@@ -91,7 +92,7 @@ class Workload:
         self.in_hw, self.classes, self.width = in_hw, classes, width
         self.three = net == "unet3d"
         self.unit = "volumes/s" if self.three else "images/s"
-        self.metric = METRIC_3D if self.three else METRIC
+        self.metric = METRIC_3D if self.three else (METRIC_ALEX if net == "alexnet" else METRIC)
 
     fuse = False   # BN-ReLU prologue fusion, set from --fuse
 
@@ -112,6 +113,12 @@ def workload(args):
         batch = args.batch or 2560
         name = "cfg3: ResNet-50 v1.5 batch %d 224^2, all free HBM" % batch
         return Workload("resnet50", batch, None, name, 224, 1000)
+    if args.workload == "alexnet":
+        batch = args.batch or 4096
+        budget = int((args.budget_gib or 16.0) * (1 << 30))
+        name = ("alexnet: AlexNet (single tower, LRN, dropout 0.5) batch %d 227^2, device budget %.0f GiB "
+                "(the paper's compute-heavy workload, P:L453; SURVEY 8(f) f3)" % (batch, budget / (1 << 30)))
+        return Workload("alexnet", batch, budget, name, 227, 1000)
     e = args.edge or 256
     budget = int(args.budget_gib * (1 << 30)) if args.budget_gib else None
     # (the 3D U-Net has no fusable BN-ReLU: fusion is 2D only)
@@ -196,6 +203,27 @@ def cpu_sample(target_s=15.0, batch=1):
                 n_img // batch, batch)}
 
 
+def cpu_sample_alex(target_s=15.0, batch=4):
+    """The oracle as it stands on AlexNet (fp64 NumPy, 227^2) on host cores."""
+    import synthdata
+    from oracle import nets
+    cores = len(os.sched_getaffinity(0))
+    net = nets.alexnet()
+    params = nets.init_params(net, seed=2)
+    x = synthdata.images(batch, 227, 227, 3, seed=0)
+    t = synthdata.labels(batch, 1000, seed=1)
+    n_img, t0 = 0, time.time()
+    while True:
+        nets.forward_backward(net, params, x, t)
+        n_img += batch
+        if time.time() - t0 > target_s:
+            break
+    dt = time.time() - t0
+    return {"value": n_img / dt, "unit": "images/s", "cores": cores, "kind": "oracle",
+            "sample": "%d fp64 AlexNet fwd+bwd step(s) at batch %d, 227^2 (NumPy, BLAS threads = cores)" % (
+                n_img // batch, batch)}
+
+
 def cpu_sample_3d(target_s=15.0, edge=16, width=32):
     """The oracle as it stands on the 3D U-Net (fp64 NumPy) at a bounded size: per-voxel rate."""
     import numpy as np
@@ -223,21 +251,24 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    name = workload(args).name
+    W = workload(args)
+    name = W.name
+    alex = W.net == "alexnet"
     per = []
     cs = None
     for i in range(args.warmup + args.steps):
-        s = cpu_sample(target_s=0.0, batch=1)
+        s = cpu_sample_alex(target_s=0.0, batch=1) if alex else cpu_sample(target_s=0.0, batch=1)
         if i >= args.warmup:
             per.append(s["value"])
         cs = s
     v = statistics.median(per)
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": W.metric, "value": v, "unit": "images/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": name + " -- oracle sample: 1 image per step"},
             "cpu_baseline": {"value": v, "unit": "images/s", "cores": cs["cores"], "kind": "oracle",
-                             "sample": "1 fp64 ResNet-50 fwd+bwd image per step, 224^2"},
+                             "sample": "1 fp64 %s fwd+bwd image per step, %d^2" % (
+                                 "AlexNet" if alex else "ResNet-50", W.in_hw)},
             "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -603,7 +634,8 @@ def our_arm(args):
             if cfg2 is not None:
                 line["cfg2"] = cfg2
     if rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_sample_3d(15.0) if W.three else cpu_sample(15.0, batch=1)
+        line["cpu_baseline"] = (cpu_sample_3d(15.0) if W.three else
+                                cpu_sample_alex(15.0) if W.net == "alexnet" else cpu_sample(15.0, batch=1))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -628,7 +660,7 @@ def synth_batch(W, rank):
         x[:, 0] = synthdata.rng(0 + rank).standard_normal(e * e * e, dtype=np.float32)
         lab = synthdata.rng(1 + rank).integers(0, W.classes, e * e * e).astype(np.int32)
         return torch.from_numpy(x.reshape(-1)).pin_memory(), torch.from_numpy(lab).pin_memory()
-    x = torch.from_numpy(np.ascontiguousarray(pad4(synthdata.images(W.batch, 224, 224, 3, seed=0 + rank))))
+    x = torch.from_numpy(np.ascontiguousarray(pad4(synthdata.images(W.batch, W.in_hw, W.in_hw, 3, seed=0 + rank))))
     return x.reshape(-1).pin_memory(), torch.from_numpy(synthdata.labels(W.batch, 1000, seed=1 + rank)).pin_memory()
 
 
@@ -641,7 +673,7 @@ def name_out_channels(ctx, pname):
     for l in ctx.layers:
         name = l.name.decode()
         if name == task or (l.kind == 9 and name.split("+", 1)[1] == task):   # 9: BNRELU_CONV "<bn>+<conv>"
-            return l.cout if l.kind in (0, 9) else ((l.cout + 3) // 4 * 4)
+            return l.cout if l.kind in (0, 9, 10, 12) else ((l.cout + 3) // 4 * 4)
     raise KeyError(pname)
 
 
@@ -759,6 +791,8 @@ def incore_and_cfg2(W, args, host, streams):
     import torch
     if W.three:
         Wi = Workload(W.net, 1, None, W.name, W.in_hw // 2, W.classes, W.width)
+    elif W.net == "alexnet":   # in-core fits at the benchmarked batch: the same step, every map kept
+        Wi = Workload(W.net, W.batch, None, "in-core AlexNet batch %d" % W.batch, W.in_hw, W.classes)
     else:
         Wi = Workload(W.net, 640, None, "in-core ResNet-50 v1.5 batch 640", 224, W.classes)
     Wi.fuse = W.fuse
@@ -788,7 +822,7 @@ def incore_and_cfg2(W, args, host, streams):
             ri.close()
             return incore, None
         incore = {"batch": Wi.batch, "images_per_s": Wi.batch * 1000.0 / ms, "ms_per_step": ms, "families": fam}
-        if not args.no_cfg2:
+        if not args.no_cfg2 and W.net == "resnet50":
             W2 = Workload("resnet50", 640, 16 << 30, "cfg2: ResNet-50 v1.5 batch 640 224^2, device budget 16 GiB",
                           224, W.classes)
             W2.fuse = W.fuse
@@ -836,7 +870,7 @@ def synth_bytes(W):
     """Bytes of one input batch (+ labels) as the GPU stores it (the e2e staging buffer)."""
     if W.three:
         return W.in_hw ** 3 * (32 + 1) * 4
-    return W.batch * (224 * 224 * 4 + 1) * 4
+    return W.batch * (W.in_hw * W.in_hw * 4 + 1) * 4
 
 
 def main():

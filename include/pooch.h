@@ -84,8 +84,15 @@ typedef enum {
   POOCH_L_FC_CE = 6,     /* z = flat_hwc(x) W^T + b, softmax-CE loss     bwd reads {x, z}   */
   POOCH_L_UPCONV = 7,    /* y = transposed conv k2 s2 of x (3D U-Net up-sampling)  bwd reads {x} */
   POOCH_L_HEAD_CE = 8,   /* z = x W^T + b per voxel, softmax-CE averaged over voxels  bwd reads {x, z} */
-  POOCH_L_BNRELU_CONV = 9 /* y = conv(relu(BN(c)), W): BN-ReLU applied to the conv's operand on
+  POOCH_L_BNRELU_CONV = 9, /* y = conv(relu(BN(c)), W): BN-ReLU applied to the conv's operand on
                              load, relu(BN(c)) never stored   bwd reads {c} */
+  /* AlexNet: */
+  POOCH_L_CONV_RELU = 10,   /* y = relu(conv(x, W) + b), bias per output channel   bwd reads {x, y} */
+  POOCH_L_LRN = 11,         /* y = x / (2 + 1e-4 / 5 * sum_{|c'-c| <= 2} x_c'^2)^0.75 (local response
+                               normalisation across channels)                      bwd reads {x}    */
+  POOCH_L_FC_RELU_DROP = 12 /* y = dropout(relu(flat_hwc(x) W^T + b)), inverted dropout with a
+                               counter-based mask (pooch_set_rng); k = drop probability in percent,
+                               output [batch][cout] (hout = wout = 1)           bwd reads {x, y}    */
 } pooch_layer_kind;
 /* POOCH_L_BNRELU_CONV: c (in0) is a conv output with this task as its only consumer; 2D, single
  * input, cin a multiple of 32, stride <= 2. name = "<bn name>+<conv name>": the BN's gamma /
@@ -114,7 +121,9 @@ typedef struct {
 
 /* Built-in workloads of BASELINE.json: 0 = tiny CNN (config 1), 1 = ResNet-50 v1.5
  * (configs 2, 3, 5), 2 = ResNet-50 v1, 3 = 3D U-Net (config 4: in_hw^3 volume, base width
- * `width` -> level widths w, 2w, 4w, 4w, input channels padded 1 -> 32). which |
+ * `width` -> level widths w, 2w, 4w, 4w, input channels padded 1 -> 32), 4 = AlexNet (the
+ * paper's second workload: single-tower, in_hw 227, dropout 0.5; width unused;
+ * 13 maps, 62,378,344 parameters). which |
  * POOCH_NET_FUSE_BNRELU merges every BN-ReLU whose only consumer is a single-input 2D conv with
  * cin % 32 == 0 and stride <= 2 into that conv (POOCH_L_BNRELU_CONV; same function and
  * parameters, fewer maps: ResNet-50 105 -> 73, tiny CNN 10 -> 7). Fills up to
@@ -169,6 +178,13 @@ pooch_status pooch_allreduce_buckets(pooch_ctx* ctx, int32_t* n, uint64_t* lo, u
  * 0 = plain TF32 (one MMA, operands truncated to TF32 by the tensor core). Invalidates the
  * profile and the plan. */
 pooch_status pooch_set_precision(pooch_ctx* ctx, int32_t precision);
+
+/* Counter-based generator of the dropout masks (POOCH_L_FC_RELU_DROP): element i of task t's
+ * output is kept iff fmix32(key ^ fmix32(i)) >= floor(p * 2^32), key = fmix32(seed ^
+ * fmix32(step * 0x9E3779B9 + t)) (fmix32 = MurmurHash3's finaliser), so a recomputed forward
+ * reproduces its mask. (seed, step) live in device memory; every train step advances step by
+ * one after the update. Sets both; synchronises the compute stream. Valid after pooch_set_budget. */
+pooch_status pooch_set_rng(pooch_ctx* ctx, uint32_t seed, uint32_t step);
 
 /* Input slot inside the device arena: x_dev [batch, in_h, in_w, in_c] fp32 (3D networks:
  * [batch, in_d, in_h, in_w, in_c]), labels_dev [batch] int32 (POOCH_L_HEAD_CE networks: one
@@ -440,6 +456,11 @@ pooch_status pooch_op_maxpool2d_bwd(const float* x, const float* gy, float* gx, 
  *                 maximum of every window in (d, h, w) row-major order (Reading 25), argmax from x.
  * POOCH_EUSAGE on null pointers or bad shapes. Used by the parity tests. */
 size_t pooch_op_bn_ws_bytes(int32_t C);
+/* AlexNet's local response normalisation over the C (<= 1024) channels of `pixels` NHWC pixels:
+ * lrn_fwd y = x * s^-0.75, s = 2 + 1e-4 / 5 * sum_{|c'-c| <= 2} x_c'^2; lrn_bwd gx = its adjoint
+ * applied to gy (written, not accumulated). */
+pooch_status pooch_op_lrn_fwd(const float* x, float* y, int64_t pixels, int32_t C, void* stream);
+pooch_status pooch_op_lrn_bwd(const float* x, const float* gy, float* gx, int64_t pixels, int32_t C, void* stream);
 pooch_status pooch_op_bn_finalize(const float* tile_sum, const float* tile_sq, int32_t tiles, int32_t C, int64_t count,
                                   const float* gamma, const float* beta, float* mean, float* invstd, float* scale,
                                   float* shift, void* ws, void* stream);

@@ -304,8 +304,9 @@ int conv_stat_tiles(const ConvGeom& g) {
 
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
                              float* stat_sq, const float* bias, cudaStream_t st, const float* x1,
-                             const float* xf_scale, const float* xf_shift) {
+                             const float* xf_scale, const float* xf_shift, bool relu) {
   GemmParams p = base_params(g);
+  p.relu = relu ? 1 : 0;
   if (xf_scale && (!fwd_uses_tma(g) || g.is3d() || g.C1 > 0 || !xf_shift))
     return fail(POOCH_EUSAGE, "BN-ReLU on load: 2D single-source conv with C %% 32 == 0 and stride <= 2 only");
   p.xf_scale = xf_scale;

@@ -21,9 +21,10 @@ bool conv_shape_ok(const ConvGeom& g);
 
 // y = conv(x, w); bias (nullable) per output channel; stat_sum/sq nullable.
 // xf_scale / xf_shift (nullable): the operand is relu(scale[c] * x + shift[c]) (BN-ReLU on load)
+// relu: the epilogue applies max(v, 0) after the bias (y = relu(conv(x, w) + b)).
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
                              float* stat_sq, const float* bias, cudaStream_t st, const float* x1 = nullptr,
-                             const float* xf_scale = nullptr, const float* xf_shift = nullptr);
+                             const float* xf_scale = nullptr, const float* xf_shift = nullptr, bool relu = false);
 // dx (and, two-source, dx1 for channels [C1, C)); accumulate / accumulate1 per destination
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
                                cudaStream_t st, float* dx1 = nullptr, bool accumulate1 = false);

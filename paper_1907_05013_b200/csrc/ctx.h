@@ -75,7 +75,7 @@ struct pooch_ctx {
   std::vector<pooch::TaskRt> rt;
   size_t off_w = 0, off_g = 0, off_v = 0, off_wt = 0, off_stats = 0, off_tile = 0, off_fin = 0, off_bnws = 0,
          off_wgws = 0, off_mparg = 0, off_x = 0, off_lab = 0, off_lossrows = 0, off_loss = 0, off_dz = 0,
-         off_cews = 0;  // off_cews: CE two-stage reduction scratch (narrow heads)
+         off_cews = 0, off_rng = 0;  // off_cews: CE two-stage reduction scratch; off_rng: dropout {seed, step}
   size_t wt_floats = 0, stats_floats = 0, tile_bytes = 0, fin_bytes = 0, bnws_bytes = 0, wgws_bytes = 0,
          mparg_bytes = 0;
   size_t resident_end = 0;
@@ -143,4 +143,5 @@ struct pooch_ctx {
   int64_t step_count = 0;
   int64_t last_launches = 0;
   int precision = 1;  // contractions: 0 TF32, 1 3xTF32 (default; DESIGN.md Reading 27)
+  bool has_dropout = false;  // an FC_RELU_DROP task with p > 0: the step counter advances per step
 };

@@ -23,6 +23,7 @@
 #include <map>
 #include <numeric>
 
+#include "alex.h"
 #include "common.h"
 #include "ctx.h"
 #include "eltwise.h"
@@ -159,6 +160,16 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
       if (T.dout > 0)
         return maxpool3d_fwd(p.in0, p.out, T.din, T.hin, T.win, T.cin, st);
       return maxpool_fwd(p.in0, p.out, B, T.hin, T.win, T.cin, T.k, T.stride, T.pad, T.hout, T.wout, st);
+    case POOCH_L_CONV_RELU:   // bias + ReLU in the tensor-core epilogue
+      return launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, nullptr, nullptr, pw(c, R.b), st, nullptr, nullptr,
+                             nullptr, true);
+    case POOCH_L_LRN:
+      return lrn_fwd(p.in0, p.out, R.rows, T.cout, st);
+    case POOCH_L_FC_RELU_DROP:
+      POOCH_CHECK(launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, nullptr, nullptr, pw(c, R.b), st, nullptr, nullptr,
+                                  nullptr, true));
+      return dropout_fwd(p.out, R.rows * T.cout, reinterpret_cast<const uint32_t*>(c->dev + c->off_rng), t,
+                         T.k / 100.f, st);
     case POOCH_L_AVGPOOL:
       return avgpool_fwd(p.in0, p.out, B, T.hin * T.win, T.cin, st);
     case POOCH_L_UPCONV:
@@ -285,6 +296,30 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
                          T.k, T.stride, T.pad, T.hout, T.wout, st);
     case POOCH_L_AVGPOOL:
       return avgpool_bwd(p.gy, p.g0, B, T.hin * T.win, T.cin, st);
+    case POOCH_L_CONV_RELU:
+    case POOCH_L_FC_RELU_DROP: {
+      // dz = dy [y > 0] / (1 - p) in place on this task's output gradient (kept dropout units are
+      // exactly the positive outputs), db = column sums of dz; then wgrad and dgrad with dz
+      const ConvGeom& G = RG;
+      const float scale = T.kind == POOCH_L_FC_RELU_DROP ? 1.f / (1.f - T.k / 100.f) : 1.f;
+      float* dz = const_cast<float*>(p.gy);
+      double eb = 4.0 * R.rows * T.cout;
+      if (mark) mark(c, FAM_BN_BWD, t, 0, 4.0 * eb);
+      POOCH_CHECK(relu_mask_sum(dz, p.self, R.rows, T.cout, scale, pg(c, R.b), reinterpret_cast<float*>(c->dev + c->off_bnws),
+                                st));
+      double xb = 4.0 * G.N * G.H * G.W * G.C, wb = 4.0 * G.K * G.R * G.S * G.C;
+      if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + eb + wb);
+      POOCH_CHECK(launch_conv_wgrad(G, p.in0 ? p.in0 : reinterpret_cast<const float*>(c->dev + c->off_x), dz,
+                                    pg(c, R.w), reinterpret_cast<float*>(c->dev + c->off_wgws), c->wgws_bytes, st));
+      if (T.in0 >= 0) {
+        if (mark) mark(c, FAM_CONV_DGRAD, t, R.flops, eb + xb * (p.acc0 ? 2 : 1) + wb);
+        POOCH_CHECK(launch_conv_dgrad(G, dz, fptr(c, c->off_wt) + R.wt_off, p.g0, p.acc0, st));
+      }
+      return POOCH_OK;
+    }
+    case POOCH_L_LRN:
+      if (p.acc0) return fail(POOCH_EUSAGE, "LRN must be the only writer of its input's gradient");
+      return lrn_bwd(p.in0, p.gy, p.g0, R.rows, T.cin, st);
     case POOCH_L_FC_CE:
     case POOCH_L_HEAD_CE: {
       float* dz = fptr(c, c->off_dz);
@@ -306,9 +341,11 @@ int fam_fwd(int kind) {
   switch (kind) {
     case POOCH_L_CONV:
     case POOCH_L_BNRELU_CONV:
+    case POOCH_L_CONV_RELU:
     case POOCH_L_UPCONV: return FAM_CONV_FWD;
     case POOCH_L_BNRELU:
     case POOCH_L_TAIL_PROJ:
+    case POOCH_L_LRN:
     case POOCH_L_TAIL_ID: return FAM_BN_FWD;
     case POOCH_L_MAXPOOL:
     case POOCH_L_AVGPOOL: return FAM_POOL;
@@ -319,9 +356,11 @@ int fam_bwd(int kind) {
   switch (kind) {
     case POOCH_L_CONV:
     case POOCH_L_BNRELU_CONV:
+    case POOCH_L_CONV_RELU:
     case POOCH_L_UPCONV: return FAM_CONV_WGRAD;
     case POOCH_L_BNRELU:
     case POOCH_L_TAIL_PROJ:
+    case POOCH_L_LRN:
     case POOCH_L_TAIL_ID: return FAM_BN_BWD;
     case POOCH_L_MAXPOOL:
     case POOCH_L_AVGPOOL: return FAM_POOL;
@@ -337,8 +376,10 @@ double fwd_bytes(pooch_ctx* c, int t) {
   const double din = T.dout > 0 ? T.din : 1.0;
   switch (T.kind) {
     case POOCH_L_CONV:
+    case POOCH_L_CONV_RELU:
     case POOCH_L_BNRELU_CONV: return 4.0 * (R.geom.N * din * R.geom.H * R.geom.W * R.geom.C + e +
                                       (double)R.geom.K * R.geom.T() * R.geom.R * R.geom.S * R.geom.C);
+    case POOCH_L_LRN: return 8.0 * e;
     case POOCH_L_UPCONV: return 4.0 * (din * T.hin * T.win * T.cin + e + 8.0 * T.cin * T.cout);
     case POOCH_L_BNRELU: return 8.0 * e;
     case POOCH_L_TAIL_PROJ:
@@ -359,6 +400,7 @@ double bwd_bytes(pooch_ctx* c, int t) {
     case POOCH_L_MAXPOOL:
       return 4.0 * (2.0 * c->g.io.batch * (T.dout > 0 ? T.din : 1) * T.hin * T.win * T.cin + e) + e;
     case POOCH_L_AVGPOOL: return 4.0 * ((double)c->g.io.batch * T.hin * T.win * T.cin + e);
+    case POOCH_L_LRN: return 12.0 * e;          // read x, gy; write gx
     default: return 0;
   }
 }
@@ -391,6 +433,7 @@ pooch_status layout_resident(pooch_ctx* c) {
   c->off_loss = take(16);
   c->off_cews = take(ce_ws_bytes());
   c->off_dz = take(ce_rows * c->rt[n - 1].cpad * 4);
+  c->off_rng = take(16);   // dropout generator {seed, step} (pooch_set_rng)
   c->resident_end = align_up(o, 1 << 20);
   return POOCH_OK;
 }
@@ -433,7 +476,9 @@ BwdPtrs bwd_ptrs(pooch_ctx* c, int t) {
   BwdPtrs p;
   p.in0 = T.in0 >= 0 ? map_bwd(c, T.in0) : nullptr;
   p.in1 = T.in1 >= 0 ? map_bwd(c, T.in1) : nullptr;
-  if (T.kind == POOCH_L_FC_CE || T.kind == POOCH_L_HEAD_CE) p.self = map_bwd(c, t);
+  if (T.kind == POOCH_L_FC_CE || T.kind == POOCH_L_HEAD_CE || T.kind == POOCH_L_CONV_RELU ||
+      T.kind == POOCH_L_FC_RELU_DROP)
+    p.self = map_bwd(c, t);
   if (t != n - 1) p.gy = buf(c, 2 * n + t);
   if (T.in0 >= 0) {
     p.g0 = buf(c, 2 * n + T.in0);
@@ -532,6 +577,27 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
       wt += (size_t)wn;
       R.flops = 2.0 * R.rows * wn;
       wg = std::max(wg, conv_wgrad_ws_bytes(R.geom));
+    } else if (T.kind == POOCH_L_CONV_RELU || T.kind == POOCH_L_FC_RELU_DROP) {
+      R.is_conv = true;
+      if (T.kind == POOCH_L_CONV_RELU) {
+        R.geom = ConvGeom{B, T.hin, T.win, T.cin, T.cout, T.k, T.k, T.stride, T.pad, T.hout, T.wout};
+      } else {   // one GEMM row per image over the flattened (h, w, c) input
+        R.rows = B;
+        R.geom = ConvGeom{B, 1, 1, T.cin, T.cout, 1, 1, 1, 0, 1, 1};
+        c->has_dropout = c->has_dropout || T.k > 0;
+      }
+      if (!conv_shape_ok(R.geom)) {
+        delete c;
+        return fail(POOCH_EUSAGE, "task %d: unsupported conv / FC shape", t);
+      }
+      const int64_t wn = (int64_t)T.cout * R.geom.R * R.geom.S * T.cin;
+      R.w = param_add(c, T.name + ".w", t, wn);
+      R.b = param_add(c, T.name + ".b", t, T.cout);
+      R.wt_off = wt;
+      wt += (size_t)wn;
+      R.flops = 2.0 * R.rows * wn;
+      wg = std::max(wg, conv_wgrad_ws_bytes(R.geom));
+      bnws_c = std::max(bnws_c, T.cout);
     } else if (T.kind == POOCH_L_UPCONV) {
       // the equivalent k2 s2 conv maps the up-sampled grid (cout channels) to the input grid (cin)
       R.is_conv = true;
@@ -602,6 +668,7 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
     for (int k = 0; k < (int)T.inputs.size(); ++k) {
       int m = T.inputs[k];
       bool can_acc = T.kind == POOCH_L_CONV || T.kind == POOCH_L_FC_CE || T.kind == POOCH_L_HEAD_CE ||
+                     T.kind == POOCH_L_CONV_RELU || T.kind == POOCH_L_FC_RELU_DROP ||
                      (T.kind == POOCH_L_TAIL_ID && k == 1) || (T.kind == POOCH_L_MAXPOOL && T.dout > 0);
       if (!can_acc && c->first_writer[m] != t) {
         delete c;
@@ -613,7 +680,7 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
   c->stats_floats = stats;
   c->tile_bytes = std::max<size_t>(tile, 256);
   c->fin_bytes = bn_finalize_ws_bytes(2048);
-  c->bnws_bytes = bn_bwd_ws_bytes(bnws_c);
+  c->bnws_bytes = std::max(bn_bwd_ws_bytes(bnws_c), relu_mask_sum_ws_bytes(bnws_c));
   c->wgws_bytes = std::max<size_t>(wg, 256);
   c->mparg_bytes = std::max<size_t>(mparg, 256);
   c->map_bytes.resize(n);
@@ -798,6 +865,15 @@ static pooch_status enqueue_bucket(pooch_ctx* c, int t) {
   int r = g_nccl.allReduce(fptr(c, c->off_g) + b.lo, fptr(c, c->off_g) + b.lo, b.hi - b.lo, /*ncclFloat32*/ 7,
                            /*ncclSum*/ 0, c->nccl, cs);
   if (r != 0) return fail(POOCH_ENCCL, "ncclAllReduce (bucket %d) failed: %d", k, r);
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_set_rng(pooch_ctx* c, uint32_t seed, uint32_t step) {
+  if (!c || !c->budget_set || !c->s[0]) return fail(POOCH_EUSAGE, "set the budget and streams first");
+  const uint32_t v[4] = {seed, step, 0u, 0u};
+  POOCH_CUDA(cudaSetDevice(c->device));
+  POOCH_CUDA(cudaMemcpyAsync(c->dev + c->off_rng, v, sizeof(v), cudaMemcpyHostToDevice, c->s[0]));
+  POOCH_CUDA(cudaStreamSynchronize(c->s[0]));
   return POOCH_OK;
 }
 
@@ -1495,8 +1571,10 @@ static pooch_status enqueue_update(pooch_ctx* c, float lr, bool timing) {
     POOCH_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
   }
   if (timing) mark_seg(c, FAM_SGD, -1, 0, 20.0 * c->param_floats);
-  return sgd_momentum(fptr(c, c->off_w), fptr(c, c->off_v), fptr(c, c->off_g), c->param_floats, lr, 0.9f,
-                      1.0f / (float)c->world, st);
+  POOCH_CHECK(sgd_momentum(fptr(c, c->off_w), fptr(c, c->off_v), fptr(c, c->off_g), c->param_floats, lr, 0.9f,
+                           1.0f / (float)c->world, st));
+  if (c->has_dropout) POOCH_CHECK(rng_advance(reinterpret_cast<uint32_t*>(c->dev + c->off_rng), st));
+  return POOCH_OK;
 }
 
 static pooch_status enqueue_transposes(pooch_ctx* c) {

@@ -1,4 +1,4 @@
-// graph.cpp -- network builders (tiny CNN, ResNet-50) and task-graph derivation.
+// graph.cpp -- network builders (tiny CNN, ResNet-50, 3D U-Net, AlexNet) and task-graph derivation.
 //
 // Feature maps are the task outputs retained for backward (Sec. 2.1; P:L160,
 // Sec. 4.1.1). For ResNet-50 the census is 53 conv + 49 BN(+add)+ReLU + maxpool + avgpool
@@ -73,6 +73,28 @@ void resnet50(Builder& b, int in_hw, int classes, bool v15) {
   }
   int a = b.add(POOCH_L_AVGPOOL, x, -1, cin, cin, 1, 1, 0, 1, 0, "avgpool");
   b.add(POOCH_L_FC_CE, a, -1, cin, classes, 1, 1, 0, 1, 0, "fc");
+}
+
+// AlexNet (oracle nets.alexnet, same tasks): conv+bias+ReLU, LRN, 3/2 max-pool,
+// FC+ReLU+dropout, FC+CE; input 227x227, channels padded 3 -> 4.
+void alexnet(Builder& b, int in_hw, int classes) {
+  int h = co(in_hw, 11, 4, 0);
+  int x = b.add(POOCH_L_CONV_RELU, -1, -1, 4, 96, h, h, 11, 4, 0, "conv1");
+  x = b.add(POOCH_L_LRN, x, -1, 96, 96, h, h, 0, 1, 0, "lrn1");
+  h = co(h, 3, 2, 0);
+  x = b.add(POOCH_L_MAXPOOL, x, -1, 96, 96, h, h, 3, 2, 0, "pool1");
+  x = b.add(POOCH_L_CONV_RELU, x, -1, 96, 256, h, h, 5, 1, 2, "conv2");
+  x = b.add(POOCH_L_LRN, x, -1, 256, 256, h, h, 0, 1, 0, "lrn2");
+  h = co(h, 3, 2, 0);
+  x = b.add(POOCH_L_MAXPOOL, x, -1, 256, 256, h, h, 3, 2, 0, "pool2");
+  x = b.add(POOCH_L_CONV_RELU, x, -1, 256, 384, h, h, 3, 1, 1, "conv3");
+  x = b.add(POOCH_L_CONV_RELU, x, -1, 384, 384, h, h, 3, 1, 1, "conv4");
+  x = b.add(POOCH_L_CONV_RELU, x, -1, 384, 256, h, h, 3, 1, 1, "conv5");
+  h = co(h, 3, 2, 0);
+  x = b.add(POOCH_L_MAXPOOL, x, -1, 256, 256, h, h, 3, 2, 0, "pool5");
+  x = b.add(POOCH_L_FC_RELU_DROP, x, -1, 256 * h * h, 4096, 1, 1, 50, 1, 0, "fc6");
+  x = b.add(POOCH_L_FC_RELU_DROP, x, -1, 4096, 4096, 1, 1, 50, 1, 0, "fc7");
+  b.add(POOCH_L_FC_CE, x, -1, 4096, classes, 1, 1, 0, 1, 0, "fc8");
 }
 
 // 3D U-Net of BASELINE config 4: 4 levels of widths w, 2w, 4w, 4w, each
@@ -169,14 +191,15 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
       err = "task " + std::to_string(i) + ": inputs must be topological";
       return false;
     }
-    if (d.kind < POOCH_L_CONV || d.kind > POOCH_L_BNRELU_CONV) {
+    if (d.kind < POOCH_L_CONV || d.kind > POOCH_L_FC_RELU_DROP) {
       err = "task " + std::to_string(i) + ": bad kind";
       return false;
     }
     if (d.in0 >= 0) t.inputs.push_back(d.in0);
     if (d.in1 >= 0) t.inputs.push_back(d.in1);
     const bool two = d.kind == POOCH_L_TAIL_PROJ || d.kind == POOCH_L_TAIL_ID || (d.kind == POOCH_L_CONV && d.in1 >= 0);
-    if (two != (d.in1 >= 0) || ((d.kind != POOCH_L_CONV || two) && d.in0 < 0)) {
+    const bool may_read_input = (d.kind == POOCH_L_CONV && !two) || d.kind == POOCH_L_CONV_RELU;
+    if (two != (d.in1 >= 0) || (!may_read_input && d.in0 < 0)) {
       err = "task " + std::to_string(i) + ": wrong number of inputs";
       return false;
     }
@@ -186,7 +209,7 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
       t.win = g.t[d.in0].wout;
       t.din = g.t[d.in0].dout;
       int cprev = g.t[d.in0].cout;
-      if (d.kind == POOCH_L_FC_CE) cprev *= t.hin * t.win;
+      if (d.kind == POOCH_L_FC_CE || d.kind == POOCH_L_FC_RELU_DROP) cprev *= t.hin * t.win;
       if (d.kind == POOCH_L_CONV && d.in1 >= 0) {  // two-source conv: same grid, channels concatenated
         const Task& o = g.t[d.in1];
         if (o.hout != t.hin || o.wout != t.win || o.dout != t.din || cprev % 32 || o.cout % 32) {
@@ -221,7 +244,20 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
         return false;
       }
     }
-    if (d.kind == POOCH_L_CONV || d.kind == POOCH_L_MAXPOOL || d.kind == POOCH_L_BNRELU_CONV) {
+    if ((d.kind == POOCH_L_CONV_RELU || d.kind == POOCH_L_LRN || d.kind == POOCH_L_FC_RELU_DROP) && three) {
+      err = "task " + std::to_string(i) + ": the AlexNet kinds are 2D";
+      return false;
+    }
+    if (d.kind == POOCH_L_LRN && (d.cout != d.cin || d.hout != t.hin || d.wout != t.win || d.cin > 1024)) {
+      err = "task " + std::to_string(i) + ": LRN keeps the shape (C <= 1024)";
+      return false;
+    }
+    if (d.kind == POOCH_L_FC_RELU_DROP && (d.hout != 1 || d.wout != 1 || d.k < 0 || d.k >= 100)) {
+      err = "task " + std::to_string(i) + ": FC_RELU_DROP outputs [batch][cout]; k = drop percent in [0, 100)";
+      return false;
+    }
+    if (d.kind == POOCH_L_CONV || d.kind == POOCH_L_MAXPOOL || d.kind == POOCH_L_BNRELU_CONV ||
+        d.kind == POOCH_L_CONV_RELU) {
       if (co(t.hin, d.k, d.stride, d.pad) != d.hout || co(t.win, d.k, d.stride, d.pad) != d.wout ||
           (three && co(t.din, d.k, d.stride, d.pad) != t.dout)) {
         err = "task " + std::to_string(i) + ": output shape does not match geometry";
@@ -257,8 +293,14 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
       case POOCH_L_TAIL_PROJ:
       case POOCH_L_TAIL_ID:
       case POOCH_L_UPCONV:
-      case POOCH_L_MAXPOOL: t.needs = t.inputs; break;
+      case POOCH_L_MAXPOOL:
+      case POOCH_L_LRN: t.needs = t.inputs; break;
       case POOCH_L_AVGPOOL: break;
+      case POOCH_L_CONV_RELU:
+      case POOCH_L_FC_RELU_DROP:   // the ReLU mask comes from the task's own output
+        t.needs = t.inputs;
+        t.needs.push_back(i);
+        break;
       case POOCH_L_FC_CE:
       case POOCH_L_HEAD_CE:
         t.needs = t.inputs;
@@ -352,6 +394,9 @@ extern "C" pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t cl
   } else if (which == 3) {
     if (in_hw < 16 || in_hw % 16 || width <= 0 || width % 32) return fail(POOCH_EUSAGE, "bad 3D U-Net size");
     unet3d(b, in_hw, classes, width);
+  } else if (which == 4) {
+    if (in_hw < 67) return fail(POOCH_EUSAGE, "AlexNet input too small (>= 67)");
+    alexnet(b, in_hw, classes);
   } else {
     return fail(POOCH_EUSAGE, "unknown network %d", which);
   }

@@ -90,6 +90,7 @@ struct GemmParams {
   // is relu(xf_scale[c] * v + xf_shift[c]) of the stored tensor; zero padding stays zero
   const float* xf_scale;
   const float* xf_shift;
+  int relu;              // FWD: the epilogue applies max(v, 0) after the bias (AlexNet conv / FC)
 };
 
 constexpr int BM = 128;
@@ -1043,6 +1044,10 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
           if (p.bias != nullptr) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += (nb + i < p.Ng) ? __ldg(p.bias + nb + i) : 0.f;
+          }
+          if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
           }
         }
         // destination of row gmr, columns [col, col + 4) (gmr < 0: row not stored)

@@ -14,8 +14,9 @@ import numpy as np
 from ._lib import P, IODesc, LayerDesc, PlanReport, ProfileT, SearchCfg, check, lib
 from .planning import STRATEGIES
 
-NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2, "unet3d": 3}
-KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce", "upconv", "head_ce", "bnrelu_conv"]
+NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2, "unet3d": 3, "alexnet": 4}
+KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce", "upconv", "head_ce", "bnrelu_conv",
+         "conv_relu", "lrn", "fc_relu_drop"]
 FAMILIES = ["conv_fwd", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd", "pool", "fc_ce", "sgd",
             "swap_out", "swap_in", "allreduce", "other", "stall"]
 
@@ -94,7 +95,7 @@ class Context:
             classes = classes or 2
             return cls(build_net(name, in_hw, classes, width, fuse), batch, 32, in_hw, in_hw, classes, device,
                        in_d=in_hw)
-        in_hw = in_hw or (32 if name == "tiny" else 224)
+        in_hw = in_hw or {"tiny": 32, "alexnet": 227}.get(name, 224)
         classes = classes or (10 if name == "tiny" else 1000)
         return cls(build_net(name, in_hw, classes, width, fuse), batch, 4, in_hw, in_hw, classes, device)
 
@@ -143,6 +144,10 @@ class Context:
         ct = np.zeros(n.value, np.int32)
         self._chk(lib.pooch_allreduce_buckets(self.h, C.byref(n), lo.ctypes.data, hi.ctypes.data, ct.ctypes.data))
         return [(int(a), int(b), int(t)) for a, b, t in zip(lo, hi, ct)]
+
+    def set_rng(self, seed: int, step: int):
+        """(seed, step) of the counter-based dropout masks (pooch_set_rng)."""
+        self._chk(lib.pooch_set_rng(self.h, seed & 0xFFFFFFFF, step & 0xFFFFFFFF))
 
     def input_slot(self):
         x, l = C.c_void_p(), C.c_void_p()

@@ -65,6 +65,8 @@ CONV_CASES = [
     (3, 6, 6, 256, 64, 1, 1, 0),      # 1x1 reduce to 64 (wgrad: transposed orientation)
     (2, 6, 6, 64, 256, 1, 1, 0),      # 1x1 expand from 64 (wgrad: 64-wide B tile)
     (5, 7, 7, 64, 96, 3, 1, 1),       # odd batch, ragged pixel boxes
+    (2, 67, 67, 4, 96, 11, 4, 0),     # AlexNet conv1 (11x11 stride 4, Cin padded 3->4)
+    (2, 13, 13, 96, 256, 5, 1, 2),    # AlexNet conv2 shape (5x5 pad 2), 96 channels
 ]
 
 
