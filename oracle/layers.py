@@ -390,3 +390,84 @@ def fc_relu_dropout_bwd(dy, x, w, z, keep, ratio):
     """Adjoint of fc_relu_dropout_fwd: dz = dy * keep * [z > 0] / (1 - ratio); (dx, dW, db)."""
     dz = np.where(keep & (z > 0), dy / (1.0 - ratio), 0.0)
     return fc_bwd(dz, x, w)
+
+
+# ------------------------------------------------ decisions taken in the kernel's precision
+# Where floating point decides a discrete choice -- a ReLU mask, a max-pool winner -- the oracle
+# can take that decision from the GPU's own tensors (its forward maps, read back) and compute
+# everything else in fp64, so that both sides decide in the same precision and the comparison
+# measures arithmetic, not the chaotic amplification of a flipped decision (DESIGN.md Reading 28).
+def maxpool_argmax(xd, k, stride, pad):
+    """Window index u*k+v of the FIRST maximum of every k x k window of xd (NCHW, -inf padding)."""
+    n, c, h, w = xd.shape
+    ho, wo = conv_out_hw(h, w, k, k, stride, pad)
+    xp = np.pad(xd, ((0, 0), (0, 0), (pad, pad), (pad, pad)), constant_values=-np.inf)
+    best = np.full((n, c, ho, wo), -np.inf, dtype=xd.dtype)
+    arg = np.full((n, c, ho, wo), -1, dtype=np.int64)
+    for u in range(k):
+        for v in range(k):
+            win = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
+            better = win > best
+            best = np.where(better, win, best)
+            arg = np.where(better, u * k + v, arg)
+    return arg
+
+
+def maxpool_fwd_at(x, arg, k, stride, pad):
+    """y = x at the window positions arg (from maxpool_argmax)."""
+    n, c, h, w = x.shape
+    _, _, ho, wo = arg.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)), constant_values=-np.inf)
+    y = np.zeros(arg.shape, dtype=x.dtype)
+    for u in range(k):
+        for v in range(k):
+            win = xp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride]
+            y = np.where(arg == u * k + v, win, y)
+    return y
+
+
+def maxpool_bwd_at(dy, x_shape, arg, k, stride, pad):
+    """dx: dy routed to the window positions arg."""
+    n, c, h, w = x_shape
+    _, _, ho, wo = dy.shape
+    dxp = np.zeros((n, c, h + 2 * pad, w + 2 * pad), dtype=dy.dtype)
+    for u in range(k):
+        for v in range(k):
+            dxp[:, :, u:u + stride * (ho - 1) + 1:stride, v:v + stride * (wo - 1) + 1:stride] += dy * (arg == u * k + v)
+    return dxp[:, :, pad:pad + h, pad:pad + w].copy()
+
+
+def maxpool3d_argmax(xd, k=2, stride=2):
+    n, c, d, h, w = xd.shape
+    do, ho, wo = ((e - k) // stride + 1 for e in (d, h, w))
+    best = np.full((n, c, do, ho, wo), -np.inf, dtype=xd.dtype)
+    arg = np.full((n, c, do, ho, wo), -1, dtype=np.int64)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                win = _win3(xd, u, v, t, stride, do, ho, wo)
+                better = win > best
+                best = np.where(better, win, best)
+                arg = np.where(better, (u * k + v) * k + t, arg)
+    return arg
+
+
+def maxpool3d_fwd_at(x, arg, k=2, stride=2):
+    _, _, do, ho, wo = arg.shape
+    y = np.zeros(arg.shape, dtype=x.dtype)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                y = np.where(arg == (u * k + v) * k + t, _win3(x, u, v, t, stride, do, ho, wo), y)
+    return y
+
+
+def maxpool3d_bwd_at(dy, x_shape, arg, k=2, stride=2):
+    _, _, do, ho, wo = dy.shape
+    dx = np.zeros(x_shape, dtype=dy.dtype)
+    for u in range(k):
+        for v in range(k):
+            for t in range(k):
+                dx[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
+                   t:t + stride * (wo - 1) + 1:stride] += dy * (arg == (u * k + v) * k + t)
+    return dx

@@ -291,7 +291,7 @@ def _flat_hwc(x):
 
 
 def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndarray, map_grads=None,
-                     precision: str = "fp64", rng=(0, 0)):
+                     precision: str = "fp64", rng=(0, 0), decisions=None):
     """One fp64 fwd + bwd of ``net``. ``x_nhwc`` is the (unpadded)
     input batch in NHWC; params are promoted to fp64. Returns (loss, grads,
     outputs) with grads keyed like ``params`` and outputs the fp64 task
@@ -303,7 +303,12 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
     with the task id). ``precision="fp32"`` runs the same code with every array in fp32 (NumPy
     keeps fp32 through every layer call; the contractions are fp32 BLAS): the
     oracle's fp32 mode, which measures how far plain fp32 arithmetic alone
-    moves a result from fp64 (DESIGN.md Reading 28)."""
+    moves a result from fp64 (DESIGN.md Reading 28).
+    ``decisions`` ({task id: NCHW array}, optional) takes the discrete choices from given tensors
+    -- the GPU's own forward maps -- instead of this run's values: for ReLU-type tasks (bnrelu,
+    tail_*, conv_relu, fc_relu_drop) the ReLU mask is [given output > 0]; for max-pool tasks the
+    window winners are the first maxima of the given INPUT map. Everything else stays fp64, so
+    both sides decide in the same precision (layers.maxpool_argmax)."""
     q = L.tf32 if precision == "tf32" else (lambda a: a)
     dt = np.float32 if precision == "fp32" else np.float64
     P = {k: np.asarray(v, dtype=dt) for k, v in params.items()}
@@ -311,12 +316,23 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
     x_in = np.moveaxis(x_np, -1, 1)          # N(D)HWC -> NC(D)HW
     three = net.dims == 3
     outs, caches = [], []
+    dec = decisions or {}
+    masks = {}           # task id -> ReLU mask taken from ``decisions``
 
     def get(i):
         return x_in if i < 0 else outs[i]
 
     def conv_in(t):   # a conv with two inputs reads their channel concatenation
         return np.concatenate([get(i) for i in t.inputs], axis=1) if len(t.inputs) > 1 else get(t.inputs[0])
+
+    def _relu_dec(z, i):   # relu(z), or z masked by the given map's positives (decisions)
+        if i not in dec:
+            return L.relu_fwd(z)
+        masks[i] = np.asarray(dec[i]).reshape(z.shape) > 0
+        return z * masks[i]
+
+    def _relu_bwd_dec(dy, i):
+        return dy * masks[i] if i in masks else L.relu_bwd(dy, outs[i])
 
     loss = None
     for t in net.tasks:
@@ -341,7 +357,7 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             cache = (xf, dz)
         elif t.kind == "bnrelu":
             z, bc = L.bn_fwd(get(t.inputs[0]), P[t.name + ".gamma"], P[t.name + ".beta"])
-            y = L.relu_fwd(z)
+            y = _relu_dec(z, len(outs))
             cache = (bc,)
         elif t.kind in ("tail_proj", "tail_id"):
             z3, bc3 = L.bn_fwd(get(t.inputs[0]), P[t.name + ".gamma3"], P[t.name + ".beta3"])
@@ -349,15 +365,21 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
                 zp, bcp = L.bn_fwd(get(t.inputs[1]), P[t.name + ".gammap"], P[t.name + ".betap"])
             else:
                 zp, bcp = get(t.inputs[1]), None
-            y = L.relu_fwd(z3 + zp)
+            y = _relu_dec(z3 + zp, len(outs))
             cache = (bc3, bcp)
+        elif t.kind == "maxpool" and len(outs) in dec:
+            xd = np.asarray(dec[len(outs)], np.float64)
+            arg = L.maxpool3d_argmax(xd, t.k, t.stride) if three else L.maxpool_argmax(xd, t.k, t.stride, t.pad)
+            y = (L.maxpool3d_fwd_at(get(t.inputs[0]), arg, t.k, t.stride) if three
+                 else L.maxpool_fwd_at(get(t.inputs[0]), arg, t.k, t.stride, t.pad))
+            cache = arg
         elif t.kind == "maxpool":
             y = (L.maxpool3d_fwd(get(t.inputs[0]), t.k, t.stride) if three
                  else L.maxpool_fwd(get(t.inputs[0]), t.k, t.stride, t.pad))
             cache = None
         elif t.kind == "conv_relu":
-            y = L.relu_fwd(L.conv2d_bias_fwd(q(get(t.inputs[0])), q(P[t.name + ".w"]), P[t.name + ".b"],
-                                             t.stride, t.pad))
+            y = _relu_dec(L.conv2d_bias_fwd(q(get(t.inputs[0])), q(P[t.name + ".w"]), P[t.name + ".b"],
+                                            t.stride, t.pad), len(outs))
             cache = None
         elif t.kind == "lrn":
             y, _ = L.lrn_fwd(get(t.inputs[0]))
@@ -365,7 +387,13 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
         elif t.kind == "fc_relu_drop":
             xf = _flat_hwc(get(t.inputs[0]))
             keep = L.dropout_keep((xf.shape[0], t.out_chw[0]), t.ratio, rng[0], rng[1], len(outs))
-            yf, z = L.fc_relu_dropout_fwd(q(xf), q(P[t.name + ".w"]), P[t.name + ".b"], keep, t.ratio)
+            if len(outs) in dec:     # the GPU's kept-and-positive units decide (keep & [z > 0])
+                keep = np.asarray(dec[len(outs)]).reshape(xf.shape[0], -1) > 0
+                z = L.fc_fwd(q(xf), q(P[t.name + ".w"]), P[t.name + ".b"])
+                yf = np.where(keep, z / (1.0 - t.ratio), 0.0)
+                z = np.where(keep, np.abs(z) + 1.0, -1.0)   # the mask fc_relu_dropout_bwd applies
+            else:
+                yf, z = L.fc_relu_dropout_fwd(q(xf), q(P[t.name + ".w"]), P[t.name + ".b"], keep, t.ratio)
             y = yf[:, :, None, None]
             cache = (xf, z, keep)
         elif t.kind == "avgpool":
@@ -439,13 +467,13 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             grads[t.name + ".w"] += dw
             acc(t.inputs[0], dx)
         elif t.kind == "bnrelu":
-            dz = L.relu_bwd(dy, outs[i])
+            dz = _relu_bwd_dec(dy, i)
             dx, dg, db = L.bn_bwd(dz, cache[0], P[t.name + ".gamma"])
             grads[t.name + ".gamma"] += dg
             grads[t.name + ".beta"] += db
             acc(t.inputs[0], dx)
         elif t.kind in ("tail_proj", "tail_id"):
-            dz = L.relu_bwd(dy, outs[i])
+            dz = _relu_bwd_dec(dy, i)
             dx3, dg3, db3 = L.bn_bwd(dz, cache[0], P[t.name + ".gamma3"])
             grads[t.name + ".gamma3"] += dg3
             grads[t.name + ".beta3"] += db3
@@ -457,11 +485,15 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
                 acc(t.inputs[1], dxp)
             else:
                 acc(t.inputs[1], dz)
+        elif t.kind == "maxpool" and cache is not None:      # winners from ``decisions``
+            shape = get(t.inputs[0]).shape
+            acc(t.inputs[0], L.maxpool3d_bwd_at(dy, shape, cache, t.k, t.stride) if three
+                else L.maxpool_bwd_at(dy, shape, cache, t.k, t.stride, t.pad))
         elif t.kind == "maxpool":
             acc(t.inputs[0], L.maxpool3d_bwd(dy, get(t.inputs[0]), t.k, t.stride) if three
                 else L.maxpool_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad))
         elif t.kind == "conv_relu":
-            dz = L.relu_bwd(dy, outs[i])
+            dz = _relu_bwd_dec(dy, i)
             xin = get(t.inputs[0])
             w = P[t.name + ".w"]
             grads[t.name + ".w"] += L.conv2d_wgrad(q(xin), q(dz), w.shape, t.stride, t.pad)

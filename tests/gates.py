@@ -35,3 +35,51 @@ def gate(g, ref64, ref32, tag):
     bad = [r for r in rows if r[1] > r[3]]
     assert not bad, bad[:8]
     return rows
+
+
+RELU_KINDS = ("bnrelu", "tail_proj", "tail_id", "conv_relu", "fc_relu_drop")
+
+
+def gpu_decisions(ctx, net):
+    """{task id: NC(D)HW map} for the oracle's decisions mode, read back from the GPU after a step
+    planned in-core with POOCH_DEBUG_NO_REUSE=1 (every buffer instance at its own offset, so every
+    forward map is intact afterwards): ReLU-type task outputs (their masks) and max-pool inputs
+    (their window winners)."""
+    B = ctx.batch
+    out = {}
+
+    def read(m):
+        shape = tuple(net.tasks[m].out_chw)
+        n = B * int(np.prod(shape))
+        a = ctx.read_buffer(0, m, 4 * n)
+        return np.moveaxis(a.reshape((B,) + shape[1:] + (shape[0],)), -1, 1).astype(np.float64)
+    for i, t in enumerate(net.tasks):
+        if t.kind in RELU_KINDS:
+            out[i] = read(i)
+        elif t.kind == "maxpool":
+            out[i] = read(t.inputs[0])
+    return out
+
+
+def step_for_decisions(ctx, plan_step):
+    """Run plan_step() (plan in-core + one step) with buffer reuse disabled."""
+    import os
+    os.environ["POOCH_DEBUG_NO_REUSE"] = "1"
+    try:
+        return plan_step()
+    finally:
+        os.environ.pop("POOCH_DEBUG_NO_REUSE", None)
+
+
+def gate_decided(g, ref, tag):
+    """The north_star gate, per tensor and whole, against the oracle run with the GPU's own
+    ReLU / max-pool decisions (Reading 28): both sides decide in the same precision, so the gap is
+    the arithmetic's alone."""
+    rows = sorted(((k, rel(g[k], ref[k])) for k in ref if np.linalg.norm(np.asarray(ref[k])) > 0),
+                  key=lambda r: -r[1])
+    glob = global_rel(g, ref)
+    print("\n[%s, GPU decisions] whole gradient %.3e; worst: %s" % (
+        tag, glob, ", ".join("%s %.2e" % r for r in rows[:4])))
+    assert glob < TOL
+    assert rows[0][1] < TOL, rows[:8]
+    return rows

@@ -16,7 +16,13 @@ import synthdata  # noqa: E402
 from oracle import layers as L  # noqa: E402
 
 TOL_OP = 3e-3
-TOL_X3 = 2e-5     # 3xTF32 split: ~fp32 accumulation error
+TOL_X3 = 2e-5     # 3xTF32 split: ~fp32 accumulation error at K <~ 2000 ...
+
+
+def tol_x3(K):
+    """... growing ~linearly with the reduction length: the tensor core's accumulation bias
+    (Reading 43; test_3xtf32_error_against_fp32 measures 3.3e-5 at K = 4608)."""
+    return max(TOL_X3, 1e-8 * K)
 
 
 def _lib():
@@ -96,7 +102,7 @@ def test_conv_fwd_and_stats(case, prec):
     ref = L.conv2d_fwd(x.transpose(0, 3, 1, 2).astype(np.float64), w.transpose(0, 3, 1, 2).astype(np.float64), s, p)
     ref = ref.transpose(0, 2, 3, 1)
     y = dy.cpu().numpy()
-    assert rel(y, ref) < (TOL_X3 if prec else TOL_OP)
+    assert rel(y, ref) < (tol_x3(R * R * Cin) if prec else TOL_OP)
     # per-tile partial sums add up to the column sums of y (checked against the oracle output)
     flat = ref.reshape(-1, K)
     assert rel(s1.cpu().numpy().astype(np.float64).sum(0), flat.sum(0)) < TOL_OP
@@ -123,7 +129,7 @@ def test_conv_dgrad(case, accumulate, prec):
                          (N, Cin, H, W), s, p).transpose(0, 2, 3, 1)
     if accumulate:
         ref = ref + prev
-    assert rel(ddx.cpu().numpy(), ref) < (TOL_X3 if prec else TOL_OP)
+    assert rel(ddx.cpu().numpy(), ref) < (tol_x3(R * R * K) if prec else TOL_OP)
 
 
 @pytest.mark.parametrize("prec", [0, 1])

@@ -20,7 +20,7 @@ import synthdata  # noqa: E402
 from oracle import nets  # noqa: E402
 from netutil import global_rel, load_params, pad_input, read_params, rel  # noqa: E402
 
-from gates import TOL, gate  # noqa: E402
+from gates import TOL, gate, gate_decided, gpu_decisions, step_for_decisions  # noqa: E402
 
 LR = 0.05
 
@@ -167,6 +167,23 @@ def test_resnet50_gradients_match_oracle(r50):
     g = read_params(ctx, r50["params"], 1)
     assert global_rel(g, r50["grads"]) < TOL
     gate(g, r50["grads"], r50["grads32"], "ResNet-50 224^2 b8, small-residual init")
+
+
+@pytest.mark.parametrize("which", ["tiny", "r50_small_residual", "r50_standard"])
+def test_gradients_with_gpu_decisions(which, tiny, r50):
+    """Reading 28: against the oracle taking the GPU's own ReLU masks and max-pool winners (read
+    back from the step's maps), every gradient tensor is within the north_star's 5e-3 -- at the
+    standard init too, where free-running fp32 itself is 2 % away."""
+    if which == "tiny":
+        d, ctx = tiny, tiny["ctx"]
+    else:
+        d = r50 if which == "r50_small_residual" else _r50_case("standard")
+        ctx = r50["ctx"]
+    step_for_decisions(ctx, lambda: _step(ctx, d["params"], d["x"], d["t"], "incore"))
+    dec = gpu_decisions(ctx, d["net"])
+    g = read_params(ctx, d["params"], 1)
+    _, ref, _ = nets.forward_backward(d["net"], d["params"], d["x"], d["t"], decisions=dec)
+    gate_decided(g, ref, which)
 
 
 def test_resnet50_standard_init_gradients(r50):

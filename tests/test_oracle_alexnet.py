@@ -143,3 +143,39 @@ def test_micro_alexnet_whole_net_finite_differences():
                 return nets.forward_backward(net, q, x, t, rng=(3, 1))[0]
             num = _fd(f, P64[name], idx, h)
             assert grads[name][idx] == pytest.approx(num, rel=2e-4, abs=1e-7), (name, idx)
+
+
+def test_decisions_mode():
+    """oracle.nets ``decisions``: discrete choices taken from given tensors (the GPU's maps).
+    (a) The pool helpers reproduce the pinned max-pool definitions when the winners come from the
+    same tensor; (b) a hand example where the given tensor picks another winner; (c) feeding the
+    oracle its own outputs as decisions changes nothing (tiny CNN and 67^2 AlexNet)."""
+    g = synthdata.rng(12)
+    x = g.standard_normal((2, 3, 7, 7))
+    for k, s, p in ((3, 2, 1), (3, 2, 0), (2, 2, 0)):
+        arg = L.maxpool_argmax(x, k, s, p)
+        y = L.maxpool_fwd_at(x, arg, k, s, p)
+        assert np.array_equal(y, L.maxpool_fwd(x, k, s, p))
+        dy = g.standard_normal(y.shape)
+        assert np.array_equal(L.maxpool_bwd_at(dy, x.shape, arg, k, s, p), L.maxpool_bwd(dy, x, k, s, p))
+    # 2x2 window [[1, 2], [3, 0]] whose winner is decided by [[5, 0], [0, 0]]: y = 1, dx at (0, 0)
+    xx = np.array([[[[1.0, 2.0], [3.0, 0.0]]]])
+    arg = L.maxpool_argmax(np.array([[[[5.0, 0.0], [0.0, 0.0]]]]), 2, 2, 0)
+    assert L.maxpool_fwd_at(xx, arg, 2, 2, 0)[0, 0, 0, 0] == 1.0
+    assert np.array_equal(L.maxpool_bwd_at(np.array([[[[7.0]]]]), xx.shape, arg, 2, 2, 0),
+                          np.array([[[[7.0, 0.0], [0.0, 0.0]]]]))
+    for net, hw, cls in ((nets.tiny_cnn(), 32, 10), (nets.alexnet(in_hw=67), 67, 1000)):
+        params = nets.init_params(net, seed=2, bn_random=True)
+        xi = synthdata.images(2, hw, hw, 3, seed=0)
+        t = synthdata.labels(2, cls, seed=1)
+        l0, g0, outs = nets.forward_backward(net, params, xi, t, rng=(1, 2))
+        dec = {}
+        for i, tk in enumerate(net.tasks):
+            if tk.kind in ("bnrelu", "tail_proj", "tail_id", "conv_relu", "fc_relu_drop"):
+                dec[i] = outs[i]
+            elif tk.kind == "maxpool":
+                dec[i] = outs[tk.inputs[0]]
+        l1, g1, _ = nets.forward_backward(net, params, xi, t, rng=(1, 2), decisions=dec)
+        assert l1 == pytest.approx(l0, rel=1e-12)
+        for k in g0:
+            np.testing.assert_allclose(g1[k], g0[k], rtol=1e-10, atol=1e-14)
