@@ -114,7 +114,10 @@ def workload(args):
         name = "cfg3: ResNet-50 v1.5 batch %d 224^2, all free HBM" % batch
         return Workload("resnet50", batch, None, name, 224, 1000)
     if args.workload == "alexnet":
-        batch = args.batch or 4096
+        # the largest batch whose widest task (conv1 / LRN1: input, output and both gradients,
+        # 4 x 1.16 MB per image) still fits the 16 GiB budget next to the resident input slot;
+        # 12.9 GB of maps plus gradients and the resident set exceed 16 GiB (in-core does not fit)
+        batch = args.batch or 2560
         budget = int((args.budget_gib or 16.0) * (1 << 30))
         name = ("alexnet: AlexNet (single tower, LRN, dropout 0.5) batch %d 227^2, device budget %.0f GiB "
                 "(the paper's compute-heavy workload, P:L453; SURVEY 8(f) f3)" % (batch, budget / (1 << 30)))
