@@ -431,6 +431,7 @@ def one_step_bits(run, strategy, fixed=None):
     import numpy as np
     import torch
     run.init_params()
+    run.ctx.set_rng(0, 0)       # the same dropout masks for every compared step
     cls, _ = run.ctx.plan(strategy, fixed=fixed)
     loss = run.ctx.train_step(0.01, sync_loss=True)
     torch.cuda.synchronize()
@@ -439,7 +440,8 @@ def one_step_bits(run, strategy, fixed=None):
 
 def same_bits(a, b):
     import numpy as np
-    return a[1] == b[1] and all(np.array_equal(x.view(np.uint32), y.view(np.uint32)) for x, y in zip(a[2], b[2]))
+    return bool(a[1] == b[1]) and all(bool(np.array_equal(x.view(np.uint32), y.view(np.uint32)))
+                                      for x, y in zip(a[2], b[2]))
 
 
 def our_arm(args):
@@ -640,7 +642,7 @@ def our_arm(args):
         line["cpu_baseline"] = (cpu_sample_3d(15.0) if W.three else
                                 cpu_sample_alex(15.0) if W.net == "alexnet" else cpu_sample(15.0, batch=1))
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
