@@ -11,11 +11,18 @@ REQUIRED = ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step
             "vs_baseline", "dtype", "data", "config", "clocks", "e2e", "gpu_launches", "roofline", "cpu_baseline"]
 
 
-def test_committed_cfg2_line_has_the_contract_keys():
-    d = json.load(open(os.path.join(ROOT, "profiles", "r01_bench_cfg2.json")))
+def test_committed_headline_line_has_the_contract_keys():
+    """The committed default line (r02: BASELINE config 3, the metric's >HBM batch) carries every
+    contract key plus the round-2 evidence: the full-size bit-exact check, a finite loss, the
+    in-core comparison and the secondary cfg2 line checked against in-core."""
+    d = json.load(open(os.path.join(ROOT, "profiles", "r02_bench_cfg3.json")))
     for k in REQUIRED:
         assert k in d, k
-    assert d["config"]["workload"].startswith("cfg2")
+    assert d["config"]["workload"].startswith("cfg3")
+    assert d["bitexact"]["bitexact"] is True and d["loss_finite"] is True
+    assert d["incore"]["images_per_s"] > 0 and "overhead_vs_incore" in d
+    assert d["cfg2"]["bitexact_vs_incore"] is True and d["cfg2"]["isolated_profile"]["bitexact_vs_incore"] is True
+    assert d["config"]["L_O"] > 0 and d["config"]["L_I"] > 0 and d["config"]["profile_mode"] in ("isolated", "all_swap")
     assert d["warmup"] >= 3 and d["n_gpus"] == 1 and d["higher_is_better"] is True
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in d["roofline"], k

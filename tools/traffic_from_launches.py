@@ -21,7 +21,7 @@ for r in rows[hi + 1:]:
         names[r[iID]] = r[iK]
 fam = collections.defaultdict(list)
 for i, m in per.items():
-    mm = re.search(r"igemm_kernel<\(int\)(\d)", names[i])
+    mm = re.search(r"igemm_kernel<(?:\(int\))?(\d)", names[i])
     if not mm:
         continue
     f = {"0": "conv_fwd", "1": "conv_dgrad", "2": "conv_wgrad"}.get(mm.group(1))
