@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--no-paper", action="store_true", help="skip timing the paper's own PoocH plan")
     ap.add_argument("--no-check", action="store_true", help="skip the full-size bit-exactness check")
     ap.add_argument("--no-cfg2", action="store_true", help="skip the secondary cfg2 (16 GiB) line")
+    ap.add_argument("--trace", default=None,
+                    help="write the plan's simulated and the instrumented step's measured timelines as one "
+                         "Chrome trace (pid 0 simulated, pid 1 measured) to this path")
     ap.add_argument("--ablation", action="store_true",
                     help="also run the paper's strategies (Sec. 5.1-5.2) on the same executor and report each")
     ap.add_argument("--ncu-step", action="store_true",
@@ -547,6 +550,12 @@ def our_arm(args):
     ctx.train_step(0.01, sync_loss=True)
     fam = ctx.family_stats()
     segs = ctx.timing_segments()
+    if args.trace and rank == 0:
+        from paper_1907_05013_b200.planning import chrome_trace
+        names = [l.name.decode() for l in ctx.layers]
+        with open(args.trace, "w") as f:
+            json.dump(chrome_trace(ctx.last_trace(simulated=True), names, 0, "simulated") +
+                      chrome_trace(ctx.last_trace(), names, 1, "measured"), f)
     ctx.set_timing(False)
     launches = kernel_launches(ctx, args.steps)
 

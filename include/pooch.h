@@ -370,6 +370,17 @@ pooch_status pooch_set_timing(pooch_ctx* ctx, int32_t enable);
 pooch_status pooch_last_timing(pooch_ctx* ctx, int64_t* fwd_ns, int64_t* bwd_ns, int64_t* rec_ns,
                                int64_t* d2h_ns, int64_t* h2d_ns, int64_t* step_ns);
 
+/* The measured timeline of the last instrumented step (pooch_set_timing), the executed counterpart
+ * of pooch_simulate's event list: per op its lane (0 compute, 1 D2H, 2 H2D), kind ('F', 'R', 'B',
+ * 'O', 'I'), task / map id and start / end in ns after the step's first event (compute ops span
+ * their kernels; copies their own events). *n in = capacity of the nullable arrays, out = count. */
+pooch_status pooch_last_trace(pooch_ctx* ctx, int32_t* n, int32_t* lane, int32_t* kind, int32_t* id, int64_t* start_ns,
+                              int64_t* end_ns);
+/* The current plan's simulated timeline (the event list its static offsets were packed from),
+ * same layout as pooch_last_trace. POOCH_ENOPLAN without a plan. Host only. */
+pooch_status pooch_plan_trace(pooch_ctx* ctx, int32_t* n, int32_t* lane, int32_t* kind, int32_t* id, int64_t* start_ns,
+                              int64_t* end_ns);
+
 /* Number of CUDA kernels this library launched in the last pooch_train_step (all streams;
  * copies and NCCL calls not counted). */
 pooch_status pooch_kernel_launches(pooch_ctx* ctx, int64_t* per_step);

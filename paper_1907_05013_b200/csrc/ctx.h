@@ -107,6 +107,7 @@ struct pooch_ctx {
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
   std::vector<pooch::Op> ops;
   std::vector<pooch::ProgTask> program;
+  std::vector<pooch::SimEvent> plan_events;  // the adopted plan's simulated timeline
   std::vector<int> first_writer;  // per map: task whose bwd writes (not accumulates) its gradient
   // events
   std::vector<cudaEvent_t> ev;    // one per op (sync events)
@@ -125,6 +126,13 @@ struct pooch_ctx {
   double fam_flops[pooch::FAM_COUNT] = {0}, fam_bytes[pooch::FAM_COUNT] = {0};
   std::vector<int64_t> last_fwd, last_bwd, last_rec, last_d2h, last_h2d;
   std::vector<int64_t> last_d2h_issue, last_h2d_issue;  // copy start, ns after the step's first event
+  struct TraceEv {
+    int lane;
+    char kind;
+    int id;
+    int64_t start, end;
+  };
+  std::vector<TraceEv> trace;  // measured timeline of the last instrumented step
   int64_t last_step_ns = 0;
   // dp
   void* nccl = nullptr;

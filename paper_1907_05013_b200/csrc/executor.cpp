@@ -1529,6 +1529,7 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
   for (size_t q = 0; q < best.off.size(); ++q) c->buf_off[q] = c->resident_end + best.off[q];
   c->arena_high = best.high;
   c->program = best.so.program;
+  c->plan_events = best.so.events;
   c->sched = best.sched;
   compile(c, best.so);
   c->host_off.assign(n, 0);
@@ -1687,10 +1688,21 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
     std::vector<int> comp;
     for (size_t i = 0; i < c->ops.size(); ++i)
       if (c->ops[i].lane == 0) comp.push_back((int)i);
+    // measured timeline of this step (ns after its first event): compute ops from their first
+    // segment mark to the next op's, copies from their own start / end events
+    c->trace.clear();
+    auto at_ns = [&](cudaEvent_t e) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, c->tev[c->tseg.front().first], e);
+      return (int64_t)(ms * 1e6);
+    };
     for (size_t j = 0; j < comp.size(); ++j) {
       const Op& o = c->ops[comp[j]];
       size_t k0 = op_seg_begin[comp[j]];
       size_t k1 = j + 1 < comp.size() ? (size_t)op_seg_begin[comp[j + 1]] : (size_t)seg_end_compute;
+      if (k0 < c->tseg.size())
+        c->trace.push_back({0, o.kind, o.id, at_ns(c->tev[c->tseg[k0].first]),
+                            at_ns(c->tev[c->tseg[std::min(k1, c->tseg.size() - 1)].first])});
       double ms = 0;
       for (size_t k = k0; k < k1 && k < seg_ms.size(); ++k)
         if (c->tseg[k].second != FAM_STALL) ms += seg_ms[k];
@@ -1711,6 +1723,7 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
       c->fam_bytes[f] += (double)c->map_bytes[o.id];
       float at = 0;
       cudaEventElapsedTime(&at, c->tev[c->tseg.front().first], copy_ev[i].first);
+      c->trace.push_back({o.lane, o.kind, o.id, (int64_t)(at * 1e6), (int64_t)(at * 1e6) + ns});
       if (o.lane == 1) {
         c->last_d2h[o.id] = ns;
         c->last_d2h_issue[o.id] = (int64_t)(at * 1e6);
@@ -1823,6 +1836,39 @@ extern "C" pooch_status pooch_last_timing(pooch_ctx* c, int64_t* fwd, int64_t* b
   cp(d2h, c->last_d2h);
   cp(h2d, c->last_h2d);
   if (step_ns) *step_ns = c->last_step_ns;
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_plan_trace(pooch_ctx* c, int32_t* n, int32_t* lane, int32_t* kind, int32_t* id,
+                                         int64_t* start_ns, int64_t* end_ns) {
+  if (!c || !n) return fail(POOCH_EUSAGE, "null argument");
+  if (!c->have_plan) return ctx_fail(c, fail(POOCH_ENOPLAN, "no current plan"));
+  const int cap = *n, m = (int)c->plan_events.size();
+  *n = m;
+  for (int k = 0; k < std::min(cap, m); ++k) {
+    const SimEvent& e = c->plan_events[k];
+    if (lane) lane[k] = e.lane;
+    if (kind) kind[k] = e.kind;
+    if (id) id[k] = e.id;
+    if (start_ns) start_ns[k] = e.start;
+    if (end_ns) end_ns[k] = e.end;
+  }
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_last_trace(pooch_ctx* c, int32_t* n, int32_t* lane, int32_t* kind, int32_t* id,
+                                         int64_t* start_ns, int64_t* end_ns) {
+  if (!c || !n) return fail(POOCH_EUSAGE, "null argument");
+  const int cap = *n, m = (int)c->trace.size();
+  *n = m;
+  for (int k = 0; k < std::min(cap, m); ++k) {
+    const auto& e = c->trace[k];
+    if (lane) lane[k] = e.lane;
+    if (kind) kind[k] = e.kind;
+    if (id) id[k] = e.id;
+    if (start_ns) start_ns[k] = e.start;
+    if (end_ns) end_ns[k] = e.end;
+  }
   return POOCH_OK;
 }
 

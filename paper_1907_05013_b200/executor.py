@@ -241,6 +241,17 @@ class Context:
         self._chk(lib.pooch_last_timing(self.h, *[a.ctypes.data_as(P(C.c_int64)) for a in arrs], C.byref(step)))
         return dict(zip(("fwd", "bwd", "rec", "d2h", "h2d"), arrs), step_ns=step.value)
 
+    def last_trace(self, simulated=False):
+        """Measured timeline of the last instrumented step (simulated=True: the current plan's
+        simulated one): [(lane, kind, id, start_ns, end_ns)]."""
+        fn = lib.pooch_plan_trace if simulated else lib.pooch_last_trace
+        n = C.c_int32(0)
+        self._chk(fn(self.h, C.byref(n), None, None, None, None, None))
+        a = [np.zeros(n.value, np.int32) for _ in range(3)] + [np.zeros(n.value, np.int64) for _ in range(2)]
+        self._chk(fn(self.h, C.byref(n), *[x.ctypes.data for x in a]))
+        lanes = ("COMPUTE", "D2H", "H2D")
+        return [(lanes[int(l)], chr(int(k)), int(i), int(s), int(e)) for l, k, i, s, e in zip(*a)]
+
     def timing_segments(self):
         """Per-launch-group (family, ms, flops, bytes) of the last instrumented step."""
         n = C.c_int32(0)

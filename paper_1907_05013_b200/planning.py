@@ -125,3 +125,18 @@ class PlanProblem:
         check(lib.pooch_refine_problem(C.byref(self.c), cls.ctypes.data_as(P(C.c_uint8)), sched, int(capacity),
                                        out.ctypes.data_as(P(C.c_uint8)), C.byref(mk), C.byref(pk)))
         return [int(v) for v in out], int(mk.value), bool(pk.value)
+
+
+def chrome_trace(events, names=None, pid=0, label=""):
+    """Timeline events [(lane, kind, id, start_ns, end_ns)] -- pooch_simulate's (simulated) or
+    pooch_last_trace's (measured) -- in the Chrome trace event format: complete events
+    ("ph": "X") with ts / dur in microseconds, tid 0 = COMPUTE, 1 = D2H, 2 = H2D. Open the JSON in
+    chrome://tracing or Perfetto; pass two timelines with different pids to overlay them."""
+    tid = {"COMPUTE": 0, "D2H": 1, "H2D": 2}
+    what = {"F": "fwd", "R": "recompute", "B": "bwd", "O": "swap-out", "I": "swap-in"}
+    out = []
+    for lane, kind, i, s, e in events:
+        nm = names[i] if names is not None and 0 <= i < len(names) else str(i)
+        out.append({"name": "%s %s" % (what.get(kind, kind), nm), "ph": "X", "ts": s / 1e3, "dur": max(e - s, 0) / 1e3,
+                    "pid": pid, "tid": tid.get(lane, lane), "args": {"label": label}})
+    return out

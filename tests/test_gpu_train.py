@@ -303,3 +303,44 @@ def test_profiling_modes(tiny):
     ctx.set_budget(dev, dev.numel(), host, host.numel())
     load_params(ctx, tiny["params"])
     ctx.profile(2)
+
+
+def test_measured_trace_and_plan_from_a_faster_link(tiny):
+    """(1) pooch_last_trace: the executed timeline of an instrumented step -- compute ops in
+    program order without overlap, each swap-in after its swap-out. (2) The paper's portability
+    experiment (a plan made for the faster POWER9 link ran out of memory on x86): a plan
+    made from a profile claiming an 8x faster host link, executed on the real one, cannot overrun
+    the arena (static offsets + event-ordered reuse) and reproduces the in-core step bit for bit;
+    it is only slower than its simulation promised."""
+    ctx = tiny["ctx"]
+    ref, _, rep_in = _step(ctx, tiny["params"], tiny["x"], tiny["t"], "incore")
+    ref_g = _grads_bits(ctx)
+    dev, host, ss = ctx._torch
+    half = (ctx.resident_bytes() + rep_in["peak_bytes"] // 2 + 255) // 256 * 256
+    ctx.set_budget(dev, half, host, host.numel())
+    load_params(ctx, tiny["params"])
+    _put_batch(ctx, tiny["x"], tiny["t"])
+    ctx.set_profile_mode("isolated")
+    p = ctx.profile(2)
+    fast = [max(1, v // 8) for v in p["d2h"]], [max(1, v // 8) for v in p["h2d"]]
+    ctx.set_profile(p["fwd"], p["bwd"], p["rec"], fast[0], fast[1], p["tail"])
+    load_params(ctx, tiny["params"])
+    cls, rep = ctx.plan("swap_all")
+    assert rep["arena_bytes"] <= half
+    ctx.set_timing(True)
+    loss = ctx.train_step(LR)
+    torch.cuda.synchronize()
+    tr = ctx.last_trace()
+    ctx.set_timing(False)
+    assert np.float32(loss).view(np.uint32) == np.float32(ref).view(np.uint32)
+    for a, b in zip(_grads_bits(ctx), ref_g):
+        assert np.array_equal(a, b)
+    comp = [e for e in tr if e[0] == "COMPUTE"]
+    assert all(a[4] <= b[3] + 1000 for a, b in zip(comp, comp[1:]))   # serial on the compute lane
+    outs = {e[2]: e for e in tr if e[1] == "O"}
+    ins = {e[2]: e for e in tr if e[1] == "I"}
+    assert ins and all(ins[m][3] >= outs[m][4] - 1000 for m in ins)   # swap-in after its swap-out
+    ctx.set_profile_mode("auto")
+    ctx.set_budget(dev, dev.numel(), host, host.numel())
+    load_params(ctx, tiny["params"])
+    ctx.profile(2)

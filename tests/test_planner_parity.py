@@ -256,3 +256,16 @@ def test_li_cap_out_of_range_is_usage_error():
     _, pc = both(d, resident=10, budget=budget)
     with pytest.raises(Exception):
         pc.plan("pooch", li_cap=21)
+
+
+def test_chrome_trace_of_the_fig11_timeline():
+    """S:L168 timeline export: complete events, microseconds, one tid per lane."""
+    f = json.load(open(os.path.join(G, "fig11_chain.json")))
+    _, pc = both(f)
+    ev = pc.simulate([OS.SWAP] * 8, events=True)["events"]
+    tr = pp.chrome_trace(ev, names=["l%d" % i for i in range(8)])
+    assert len(tr) == len(ev) and all(e["ph"] == "X" for e in tr)
+    json.loads(json.dumps(tr))
+    f7 = [e for e in tr if e["name"] == "fwd l7"][0]
+    assert (f7["ts"], f7["dur"], f7["tid"]) == (70e-3, 10e-3, 0)       # F7 = [70, 80] ns
+    assert sorted({e["tid"] for e in tr}) == [0, 1, 2]
