@@ -542,6 +542,7 @@ def our_arm(args):
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         ms, _ = timed(run, args.steps, world, barrier)
+    graph_used = ctx.step_was_graph()
     ms_e2e, e2e_mode = timed(run, max(3, args.steps // 2), world, barrier, e2e=True)
     # every rank must hold the same weights after the same steps (identical init, summed gradients)
     ident = dp.ranks_identical(dp.digest(run.params_now()))
@@ -619,6 +620,7 @@ def our_arm(args):
         "swap": swap_stats(fam, prof),
         "families": families_table(fam, peaks(), segs, args.precision),
         "ranks_identical": ident,
+        "cuda_graph": graph_used,
     }
     if comm is not None:
         line["nccl"] = {"nranks": comm[0], "comm_nranks_ok": comm[0] == world}
@@ -825,6 +827,7 @@ def incore_and_cfg2(W, args, host, streams):
         for _ in range(2):
             ri.ctx.train_step(0.01, sync_loss=False)
         ms, _ = timed(ri, max(3, args.steps // 2), 1, torch.cuda.synchronize)
+        graph_in = ri.ctx.step_was_graph()
         ri.ctx.set_timing(True)
         ri.ctx.train_step(0.01, sync_loss=False)
         torch.cuda.synchronize()
@@ -835,7 +838,8 @@ def incore_and_cfg2(W, args, host, streams):
             incore = {"volume_edge": e, "voxels_per_s": e ** 3 * 1000.0 / ms, "ms_per_step": ms, "families": fam}
             ri.close()
             return incore, None
-        incore = {"batch": Wi.batch, "images_per_s": Wi.batch * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+        incore = {"batch": Wi.batch, "images_per_s": Wi.batch * 1000.0 / ms, "ms_per_step": ms, "families": fam,
+                  "cuda_graph": graph_in}
         if not args.no_cfg2 and W.net == "resnet50":
             W2 = Workload("resnet50", 640, 16 << 30, "cfg2: ResNet-50 v1.5 batch 640 224^2, device budget 16 GiB",
                           224, W.classes)

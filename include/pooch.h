@@ -353,6 +353,10 @@ pooch_status pooch_plan(pooch_ctx* ctx, int32_t strategy, const pooch_search_cfg
  * cross-entropy loss; if NULL the call only enqueues work on the caller's streams. */
 pooch_status pooch_train_step(pooch_ctx* ctx, float lr, float* loss_host);
 
+/* *graph = 1 if the last pooch_train_step ran as one captured CUDA graph launch, 0 if eagerly
+ * (timing mode, POOCH_NO_GRAPH, or a capture that failed). Host only. */
+pooch_status pooch_step_graph(const pooch_ctx* ctx, int32_t* graph);
+
 /* Device address of the step's mean loss (fp32 scalar inside the arena), for callers that
  * read it back asynchronously on their own stream. */
 pooch_status pooch_loss_slot(pooch_ctx* ctx, float** loss_dev);

@@ -135,6 +135,7 @@ SIGNATURES = {
     "pooch_set_rng": (c_i32, [c_vp, C.c_uint32, C.c_uint32]),
     "pooch_last_trace": (c_i32, [c_vp, P(c_i32), c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pooch_plan_trace": (c_i32, [c_vp, P(c_i32), c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pooch_step_graph": (c_i32, [c_vp, P(c_i32)]),
     "pooch_op_lrn_fwd": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),
     "pooch_op_lrn_bwd": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "pooch_comm_info": (c_i32, [c_vp, P(c_i32), P(c_i32), P(c_i32)]),

@@ -104,6 +104,7 @@ struct pooch_ctx {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   bool graphs_off = false;
+  bool last_step_graph = false;  // the last pooch_train_step ran as a CUDA graph launch
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
   std::vector<pooch::Op> ops;
   std::vector<pooch::ProgTask> program;

@@ -1743,9 +1743,13 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
 // The copy / comm streams rejoin the compute stream at the end of a step (a captured graph
 // must end joined; eagerly it makes every step a closed unit).
 static pooch_status join_streams(pooch_ctx* c) {
+  // only the streams this step gave work: a plan without copies leaves the copy streams outside
+  // a graph capture, and waiting on an event recorded there would invalidate the capture
+  bool used[4] = {true, false, false, c->nccl != nullptr};
+  for (const Op& o : c->ops) used[o.lane] = true;
   for (int k = 1; k <= 3; ++k) {
     cudaStream_t s = k == 3 ? (c->nccl ? comm_stream(c) : nullptr) : c->s[k];
-    if (!s) continue;
+    if (!s || !used[k]) continue;
     if (!c->ev_join[k - 1]) POOCH_CUDA(cudaEventCreateWithFlags(&c->ev_join[k - 1], cudaEventDisableTiming));
     POOCH_CUDA(cudaEventRecord(c->ev_join[k - 1], s));
     POOCH_CUDA(cudaStreamWaitEvent(c->s[0], c->ev_join[k - 1], 0));
@@ -1804,6 +1808,7 @@ extern "C" pooch_status pooch_train_step(pooch_ctx* c, float lr, float* loss_hos
     if (graph_step(c, lr) == POOCH_OK) done = true;
     else c->graphs_off = true;  // e.g. a stream the capture cannot follow: run eagerly from now on
   }
+  c->last_step_graph = done;
   if (!done) {
     pooch_status st = step_impl(c, lr, true);
     if (st == POOCH_OK) st = join_streams(c);
@@ -1814,6 +1819,12 @@ extern "C" pooch_status pooch_train_step(pooch_ctx* c, float lr, float* loss_hos
     POOCH_CUDA(cudaMemcpyAsync(loss_host, fptr(c, c->off_loss), 4, cudaMemcpyDeviceToHost, c->s[0]));
     POOCH_CUDA(cudaStreamSynchronize(c->s[0]));
   }
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_step_graph(const pooch_ctx* c, int32_t* graph) {
+  if (!c || !graph) return fail(POOCH_EUSAGE, "null argument");
+  *graph = c->last_step_graph ? 1 : 0;
   return POOCH_OK;
 }
 

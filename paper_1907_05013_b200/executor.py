@@ -222,6 +222,12 @@ class Context:
         self._chk(lib.pooch_train_step(self.h, lr, None))
         return None
 
+    def step_was_graph(self) -> bool:
+        """Whether the last train_step ran as one captured CUDA graph launch."""
+        v = C.c_int32()
+        self._chk(lib.pooch_step_graph(self.h, C.byref(v)))
+        return bool(v.value)
+
     def read_buffer(self, which, m, nbytes):
         a = np.empty(nbytes // 4, np.float32)
         self._chk(lib.pooch_read_buffer(self.h, which, m, a.ctypes.data, nbytes))

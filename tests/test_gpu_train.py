@@ -267,6 +267,7 @@ def test_graph_replay_bit_identical_to_eager(tiny):
         loss = ctx.train_step(LR)
         torch.cuda.synchronize()
         runs.append((np.float32(loss).view(np.uint32), _grads_bits(ctx) + _params_bits(ctx)))
+        assert ctx.step_was_graph() == (not timing)     # the replays really are graph launches
     ctx.set_timing(False)
     for loss, bits in runs[1:]:
         assert loss == runs[0][0]
