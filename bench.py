@@ -598,7 +598,7 @@ def our_arm(args):
 
     value = W.batch * world * 1000.0 / ms
     pk = peaks()
-    roof = roofline(fam, pk, segs, args.precision)
+    roof = roofline(fam, pk, segs, args.precision, W.name)
     line = {
         "metric": W.metric, "value": value, "unit": W.unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -729,7 +729,7 @@ def seg_roof(segs, pk, precision):
     return out
 
 
-def roofline(fam, pk, segs=None, precision=1):
+def roofline(fam, pk, segs=None, precision=1, workload=""):
     """Dominant kernel family of the instrumented step vs its roof:
     achieved / peak on the family's binding roof, plus the per-launch roofline fraction
     (sum of max(F / P_tensor, B / BW) over its launches / their measured time)."""
@@ -744,11 +744,11 @@ def roofline(fam, pk, segs=None, precision=1):
     if tensor:
         ach = e["flops"] / e["t"] / 1e12
         return {"kernel": k, "bound": "tensor", "achieved": ach, "peak": P / 1e12, "unit": "TFLOP/s",
-                "frac": ach / (P / 1e12), "roofline_time_frac": e["bound"] / e["t"], "traffic": traffic_for(k),
+                "frac": ach / (P / 1e12), "roofline_time_frac": e["bound"] / e["t"], "traffic": traffic_for(k, workload),
                 "launches": launches, "peak_src": src}
     ach = e["bytes"] / e["t"] / 1e9
     return {"kernel": k, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": ach / pk["hbm_gbs"], "roofline_time_frac": e["bound"] / e["t"], "traffic": traffic_for(k),
+            "frac": ach / pk["hbm_gbs"], "roofline_time_frac": e["bound"] / e["t"], "traffic": traffic_for(k, workload),
             "launches": launches, "peak_src": pk["src"]}
 
 
@@ -778,11 +778,15 @@ def families_table(fam, pk, segs=None, precision=1):
     return out
 
 
-def traffic_for(family):
+def traffic_for(family, workload=""):
+    """DRAM bytes per launch of `family` from the committed ncu capture of the same workload
+    (profiles/ncu_traffic.json), else None."""
     try:
         d = json.load(open(os.path.join(HERE, "profiles", "ncu_traffic.json")))
         e = d.get(family)
-        return None if e is None else e["dram_bytes_per_launch"]
+        if e is None or not workload.startswith(e.get("workload", "?")):
+            return None
+        return e["dram_bytes_per_launch"]
     except Exception:
         return None
 
