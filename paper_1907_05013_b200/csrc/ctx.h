@@ -51,6 +51,7 @@ struct Op {
   bool record = false;     // another lane waits on this op's completion
   bool record_start = false;  // another lane waits on this op's start (naive / SN swap-in triggers)
   std::vector<int> start_waits;  // compute ops whose START must precede this op
+  std::vector<int> frees;        // POOCH_DEBUG_POISON: buffer instances this op frees (NaN-filled after it)
 };
 
 struct pooch_ctx_impl;
@@ -105,6 +106,7 @@ struct pooch_ctx {
   cudaGraphExec_t gexec = nullptr;
   bool graphs_off = false;
   bool last_step_graph = false;  // the last pooch_train_step ran as a CUDA graph launch
+  bool poison = false;           // POOCH_DEBUG_POISON at the last compile
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
   std::vector<pooch::Op> ops;
   std::vector<pooch::ProgTask> program;

@@ -1198,6 +1198,13 @@ static void compile(pooch_ctx* c, const SimOut& so) {
   std::vector<int> free_op(3 * n, -1);
   for (const LedgerEntry& e : so.ledger)
     if (!e.alloc) free_op[e.buf] = opof(e.kind, e.id);
+  // debug mode (POOCH_DEBUG_POISON=1): every freed buffer instance is filled with NaN on the
+  // freeing op's stream right after that op, so a read after the free (a missing cross-stream
+  // wait, a wrong offset) turns the step's loss / gradients into NaN
+  c->poison = getenv("POOCH_DEBUG_POISON") != nullptr;
+  if (c->poison)
+    for (int b = 0; b < 3 * n; ++b)
+      if (free_op[b] >= 0) c->ops[free_op[b]].frees.push_back(b);
   std::map<size_t, std::pair<size_t, int>> paint;  // start -> (end, buffer)
   for (const LedgerEntry& e : so.ledger) {
     if (!e.alloc) continue;
@@ -1646,6 +1653,8 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
     if (timing && o.lane == 0) op_seg_begin[i] = (int)c->tseg.size();
     POOCH_CHECK(run_op(c, o, timing));
     if (o.lane == 0 && o.kind == 'B') POOCH_CHECK(enqueue_bucket(c, o.id));
+    for (int b : o.frees)  // POOCH_DEBUG_POISON: NaN-fill what this op freed
+      POOCH_CUDA(cudaMemsetAsync(buf(c, b), 0xFF, align_up(std::max<uint64_t>(c->map_bytes[b % n], 1)), st));
     if (timing && o.lane != 0) {
       copy_ev[i].second = lt.get();
       POOCH_CUDA(cudaEventRecord(copy_ev[i].second, st));

@@ -345,3 +345,43 @@ def test_measured_trace_and_plan_from_a_faster_link(tiny):
     ctx.set_budget(dev, dev.numel(), host, host.numel())
     load_params(ctx, tiny["params"])
     ctx.profile(2)
+
+
+def test_poisoned_frees_stay_bit_exact(tiny):
+    """SURVEY 5 debug mode: with POOCH_DEBUG_POISON=1 every freed buffer instance is NaN-filled on
+    its stream right after the freeing op, so any read after a free (a missing cross-stream wait,
+    an overlapping offset) would poison the step. Every plan of the bit-exactness test, including
+    PoocH at half the in-core peak, still reproduces the unpoisoned in-core step bit for bit."""
+    import os
+    ctx = tiny["ctx"]
+    n = ctx.n
+    ref_loss, _, rep_in = _step(ctx, tiny["params"], tiny["x"], tiny["t"], "incore")
+    ref_g = _grads_bits(ctx)
+    g = synthdata.rng(13)
+    plans = [("swap_all", None), ("fixed", [2] * (n - 1) + [1])]
+    for _ in range(3):
+        f = [int(v) for v in g.integers(0, 3, n)]
+        f[-1] = min(f[-1], 1)
+        plans.append(("fixed", f))
+    os.environ["POOCH_DEBUG_POISON"] = "1"
+    try:
+        for strat, fixed in plans:
+            loss, cls, rep = _step(ctx, tiny["params"], tiny["x"], tiny["t"], strat, fixed)
+            assert np.float32(loss).view(np.uint32) == np.float32(ref_loss).view(np.uint32), (strat, cls)
+            for a, b in zip(_grads_bits(ctx), ref_g):
+                assert np.array_equal(a, b), (strat, cls)
+        dev, host, ss = ctx._torch
+        half = (ctx.resident_bytes() + rep_in["peak_bytes"] // 2 + 255) // 256 * 256
+        ctx.set_budget(dev, half, host, host.numel())
+        load_params(ctx, tiny["params"])
+        _put_batch(ctx, tiny["x"], tiny["t"])
+        ctx.profile(2)
+        loss, cls, rep = _step(ctx, tiny["params"], tiny["x"], tiny["t"], "pooch")
+        assert np.float32(loss).view(np.uint32) == np.float32(ref_loss).view(np.uint32)
+        for a, b in zip(_grads_bits(ctx), ref_g):
+            assert np.array_equal(a, b)
+    finally:
+        os.environ.pop("POOCH_DEBUG_POISON", None)
+    ctx.set_budget(dev, dev.numel(), host, host.numel())
+    load_params(ctx, tiny["params"])
+    ctx.profile(2)
