@@ -84,6 +84,8 @@ def parse():
                          "ResNet-50 105 -> 73 maps)")
     ap.add_argument("--dump-profile", default=None,
                     help="write the measured profile (+ plan classes) as JSON to this path (offline planning)")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: gradient allreduce over peer memory (libpooch's own, default) or NCCL")
     ap.add_argument("--precision", type=int, default=1, choices=[0, 1],
                     help="contractions: 1 = 3xTF32 (default, fp32-faithful), 0 = single TF32")
     return ap.parse_args()
@@ -458,9 +460,20 @@ def our_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # POOCH_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 over a gloo process group, the
+    # gradients exchanged through peer.cu between processes of one GPU -- exercises the N > 1
+    # path on a one-GPU box; its timings mean nothing
+    share = os.environ.get("POOCH_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
+        if args.comm != "peer":
+            raise SystemExit("POOCH_BENCH_SHARE_GPU needs --comm peer (NCCL refuses two ranks on one GPU)")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     numa = dp.bind_host_to_gpu(local)
 
     def barrier():
@@ -476,6 +489,9 @@ def our_arm(args):
     # pinned host arena: sized for all-swap when the host allows, else 60 % of RAM per rank
     ctx0 = W.context(device=local)
     maps_total = sum(ctx_map_bytes(ctx0))
+    # the peer-memory allreduce's exchange buffer lives outside the arena: 64 KB + the gradient
+    peer_reserve = (65536 + 4 * sum((n + 3) // 4 * 4 for _, n in ctx0.params())
+                    if world > 1 and args.comm == "peer" else 0)
     ctx0.close()
     host_bytes = int(min(maps_total * 1.02 + (64 << 20), 0.6 * os.sysconf("SC_PAGE_SIZE") *
                          os.sysconf("SC_PHYS_PAGES") / max(1, world))) // 4096 * 4096
@@ -491,7 +507,7 @@ def our_arm(args):
     if budget is None:
         free, _ = torch.cuda.mem_get_info()
         # all free HBM minus 3 GiB of headroom, minus the e2e staging buffer (one input batch)
-        budget = int(free - (3 << 30) - synth_bytes(W))
+        budget = int(free - (3 << 30) - synth_bytes(W) - peer_reserve)
     if world > 1:  # one budget for all ranks (free HBM can differ by a few MB): identical plans
         t = torch.tensor([budget], dtype=torch.int64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
@@ -499,11 +515,16 @@ def our_arm(args):
     run = Run(W, budget, host, streams, rank, local, args.precision)
     ctx = run.ctx
     comm = None
-    if world > 1:
+    if world > 1 and args.comm == "nccl":
         ctx.set_comm(dp.broadcast_unique_id(rank, device="cuda"), rank, world)
         comm = ctx.comm_info()
         print("[rank %d] NCCL communicator: nranks %d, rank %d, cuda device %d, numa node %d" % (
             rank, comm[0], comm[1], comm[2], numa), file=sys.stderr, flush=True)
+    elif world > 1:   # the library's own allreduce over NVLink peer memory (peer.cu)
+        nb = dp.setup_peers(ctx, rank, world)
+        comm = ctx.comm_info()
+        print("[rank %d] peer-memory allreduce: nranks %d, rank %d, cuda device %d, exchange buffer %d B, "
+              "numa node %d" % (rank, comm[0], comm[1], comm[2], nb, numa), file=sys.stderr, flush=True)
 
     # ---- profile (Sec. 4.2; median of --profile-repeats) + plan (Sec. 4.4); max over ranks
     t0 = time.time()
@@ -623,7 +644,7 @@ def our_arm(args):
         "cuda_graph": graph_used,
     }
     if comm is not None:
-        line["nccl"] = {"nranks": comm[0], "comm_nranks_ok": comm[0] == world}
+        line["comm"] = {"kind": args.comm, "nranks": comm[0], "comm_nranks_ok": comm[0] == world}
     if paper is not None:
         line["pooch_paper"] = {k: v for k, v in paper.items() if k != "classes"}
     if check is not None:
@@ -905,7 +926,7 @@ def main():
         import torch
         from paper_1907_05013_b200.dp import relaunch_argv
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and os.environ.get("POOCH_BENCH_SHARE_GPU") != "1":
             print("bench.py --gpus %d needs %d visible GPUs, found %d" % (args.gpus, args.gpus, have),
                   file=sys.stderr, flush=True)
             sys.exit(2)

@@ -161,6 +161,20 @@ pooch_status pooch_set_streams(pooch_ctx* ctx, void* compute, void* d2h, void* h
  * caller (rank 0 creates it). The library creates its own communicator. Gradients are
  * summed across ranks and scaled by 1/world in the update. Marks the plan stale. */
 pooch_status pooch_set_comm(pooch_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t world);
+/* Data parallelism over peer memory (the library's own allreduce, no NCCL): allocates this
+ * rank's exchange buffer (cudaMalloc, OUTSIDE the budget arena: 64 KB of flags + one float per
+ * gradient float; its size in *bytes) and writes its 64-byte cudaIpcMemHandle to handle64.
+ * The caller all-gathers the handles (rank order) and passes them to pooch_set_peers, which
+ * maps every other rank's buffer (cudaIpcOpenMemHandle: NVLink / NVSwitch peer memory, or the
+ * same GPU when ranks share one). Each gradient bucket is then summed on the comm stream:
+ * copy into the stage, barrier, rank r sums its 1/W share over all stages in rank order and
+ * writes the sum into every stage, barrier, copy back -- every rank gets identical bits.
+ * Gradients are scaled by 1/world in the update. Exclusive with pooch_set_comm. world <= 16.
+ * A barrier whose peer never arrives traps the kernel after 120 s (a CUDA error, not a hang).
+ * Marks the plan stale. Definition of the exchange: P:L12 (Sec. 1, data parallelism);
+ * SURVEY 8(e). */
+pooch_status pooch_peer_open(pooch_ctx* ctx, int32_t rank, int32_t world, void* handle64, uint64_t* bytes);
+pooch_status pooch_set_peers(pooch_ctx* ctx, const void* handles64);
 /* The communicator as NCCL reports it (ncclCommCount / ncclCommUserRank / ncclCommCuDevice):
  * ranks, this rank, CUDA device. No communicator: 1, 0, the context's device. Host only. */
 pooch_status pooch_comm_info(pooch_ctx* ctx, int32_t* nranks, int32_t* rank, int32_t* cuda_device);

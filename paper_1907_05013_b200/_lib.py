@@ -89,6 +89,8 @@ SIGNATURES = {
     "pooch_resident_bytes": (c_i32, [c_vp, P(c_u64)]),
     "pooch_set_streams": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pooch_set_comm": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
+    "pooch_peer_open": (c_i32, [c_vp, c_i32, c_i32, c_vp, P(C.c_uint64)]),
+    "pooch_set_peers": (c_i32, [c_vp, c_vp]),
     "pooch_input_slot": (c_i32, [c_vp, P(c_vp), P(c_vp)]),
     "pooch_num_params": (c_i32, [c_vp, P(c_i32)]),
     "pooch_param_info": (c_i32, [c_vp, c_i32, C.c_char_p, P(c_i64)]),

@@ -140,6 +140,11 @@ struct pooch_ctx {
   // dp
   void* nccl = nullptr;
   int rank = 0, world = 1;
+  // peer-memory allreduce (peer.cu): own IPC-exported exchange buffer, every rank's mapped base
+  void* peer_own = nullptr;
+  std::vector<void*> peer_base;
+  size_t peer_floats = 0;
+  int sm_count = 148;
   // gradient allreduce buckets (reverse-layer order, ~26 MB): float range of the gradient
   // region and the task whose backward completes it; events compute -> comm and comm -> update
   struct Bucket {
@@ -156,3 +161,15 @@ struct pooch_ctx {
   int precision = 1;  // contractions: 0 TF32, 1 3xTF32 (default; DESIGN.md Reading 27)
   bool has_dropout = false;  // an FC_RELU_DROP task with p > 0: the step counter advances per step
 };
+
+namespace pooch {
+// peer.cu: allreduce (sum) of src[0, hi - lo) through stage range [lo, hi) of the exchange
+// buffers; `slot` numbers the barrier pair (buckets 0..n-1, the profile tail n)
+pooch_status peer_allreduce(pooch_ctx* c, float* src, size_t lo, size_t hi, int slot, cudaStream_t st);
+void peer_close(pooch_ctx* c);
+int peer_max_slots();
+// executor.cpp: buckets + events for the comm stream
+void peer_setup_buckets(pooch_ctx* c);
+// the step exchanges gradients (NCCL communicator or peer-memory buffers)
+inline bool has_comm(const pooch_ctx* c) { return c->nccl != nullptr || !c->peer_base.empty(); }
+}  // namespace pooch

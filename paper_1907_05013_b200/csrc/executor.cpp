@@ -703,6 +703,7 @@ extern "C" void pooch_destroy(pooch_ctx* c) {
   for (auto e : c->ev_start) cudaEventDestroy(e);
   for (auto e : c->tev) cudaEventDestroy(e);
   if (c->nccl && g_nccl.commDestroy) g_nccl.commDestroy(c->nccl);
+  peer_close(c);
   for (cudaEvent_t e : c->ev_bucket) cudaEventDestroy(e);
   if (c->ev_comm_done) cudaEventDestroy(c->ev_comm_done);
   if (c->own_comm) cudaStreamDestroy(c->own_comm);
@@ -808,6 +809,7 @@ extern "C" pooch_status pooch_allreduce_buckets(pooch_ctx* c, int32_t* n, uint64
 
 extern "C" pooch_status pooch_set_comm(pooch_ctx* c, const void* uid, int32_t rank, int32_t world) {
   if (!c || world < 1 || rank < 0 || rank >= world) return fail(POOCH_EUSAGE, "bad rank / world");
+  if (c->peer_own) return ctx_fail(c, fail(POOCH_EUSAGE, "context already exchanges over peer memory"));
   c->have_plan = false;
   c->rank = rank;
   c->world = world;
@@ -831,9 +833,20 @@ extern "C" pooch_status pooch_set_comm(pooch_ctx* c, const void* uid, int32_t ra
   return POOCH_OK;
 }
 
+namespace pooch {
+void peer_setup_buckets(pooch_ctx* c) {
+  build_buckets(c);
+  create_bucket_events(c);
+}
+}  // namespace pooch
+
 extern "C" pooch_status pooch_comm_info(pooch_ctx* c, int32_t* nranks, int32_t* rank, int32_t* dev) {
   if (!c) return fail(POOCH_EUSAGE, "null context");
   int nr = 1, r = 0, d = c->device;
+  if (!c->peer_base.empty()) {  // peer-memory exchange: the ranks this context mapped
+    nr = c->world;
+    r = c->rank;
+  }
   if (c->nccl) {
     if (!g_nccl.commCount || !g_nccl.commUserRank || !g_nccl.commCuDevice)
       return ctx_fail(c, fail(POOCH_ENCCL, "libnccl lacks ncclCommCount / ncclCommUserRank / ncclCommCuDevice"));
@@ -856,12 +869,13 @@ static cudaStream_t comm_stream(pooch_ctx* c) {
 // After the backward of task t: if it completes a bucket, the comm stream waits for it and
 // allreduces the bucket's gradient range (overlapping the rest of backward).
 static pooch_status enqueue_bucket(pooch_ctx* c, int t) {
-  if (!c->nccl || t < 0 || t >= (int)c->bucket_at.size() || c->bucket_at[t] < 0) return POOCH_OK;
+  if (!has_comm(c) || t < 0 || t >= (int)c->bucket_at.size() || c->bucket_at[t] < 0) return POOCH_OK;
   const int k = c->bucket_at[t];
   const pooch_ctx::Bucket& b = c->buckets[k];
   cudaStream_t cs = comm_stream(c);
   POOCH_CUDA(cudaEventRecord(c->ev_bucket[k], c->s[0]));
   POOCH_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[k], 0));
+  if (!c->nccl) return peer_allreduce(c, fptr(c, c->off_g) + b.lo, b.lo, b.hi, k, cs);
   int r = g_nccl.allReduce(fptr(c, c->off_g) + b.lo, fptr(c, c->off_g) + b.lo, b.hi - b.lo, /*ncclFloat32*/ 7,
                            /*ncclSum*/ 0, c->nccl, cs);
   if (r != 0) return fail(POOCH_ENCCL, "ncclAllReduce (bucket %d) failed: %d", k, r);
@@ -1573,7 +1587,7 @@ extern "C" pooch_status pooch_plan(pooch_ctx* c, int32_t strategy, const pooch_s
 // ====================================================================== training step
 static pooch_status enqueue_update(pooch_ctx* c, float lr, bool timing) {
   cudaStream_t st = c->s[0];
-  if (c->nccl) {  // every bucket's allreduce was enqueued during backward; SGD waits for the last
+  if (has_comm(c)) {  // every bucket's allreduce was enqueued during backward; SGD waits for the last
     if (timing) mark_seg(c, FAM_ALLREDUCE, -1, 0, 2.0 * 4 * c->param_floats);
     POOCH_CUDA(cudaEventRecord(c->ev_comm_done, comm_stream(c)));
     POOCH_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
@@ -1754,10 +1768,10 @@ static pooch_status step_impl(pooch_ctx* c, float lr, bool update) {
 static pooch_status join_streams(pooch_ctx* c) {
   // only the streams this step gave work: a plan without copies leaves the copy streams outside
   // a graph capture, and waiting on an event recorded there would invalidate the capture
-  bool used[4] = {true, false, false, c->nccl != nullptr};
+  bool used[4] = {true, false, false, has_comm(c)};
   for (const Op& o : c->ops) used[o.lane] = true;
   for (int k = 1; k <= 3; ++k) {
-    cudaStream_t s = k == 3 ? (c->nccl ? comm_stream(c) : nullptr) : c->s[k];
+    cudaStream_t s = k == 3 ? (has_comm(c) ? comm_stream(c) : nullptr) : c->s[k];
     if (!s || !used[k]) continue;
     if (!c->ev_join[k - 1]) POOCH_CUDA(cudaEventCreateWithFlags(&c->ev_join[k - 1], cudaEventDisableTiming));
     POOCH_CUDA(cudaEventRecord(c->ev_join[k - 1], s));
@@ -2139,13 +2153,17 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
       float ms;
       POOCH_CUDA(cudaEventRecord(e0, st));
       POOCH_CHECK(enqueue_transposes(c));
-      if (c->nccl && !c->buckets.empty()) {
+      if (has_comm(c) && !c->buckets.empty()) {
         // the allreduce left after the last backward task: the final bucket's (the one SGD waits
         // on), at its real size, on scratch floats of the dynamic region (the gradients stay intact)
         const pooch_ctx::Bucket& b = c->buckets.back();
-        const size_t cnt = std::min<size_t>(b.hi - b.lo, dyn / 4);
-        int r = g_nccl.allReduce(fptr(c, c->resident_end), fptr(c, c->resident_end), cnt, 7, 0, c->nccl, st);
-        if (r != 0) return ctx_fail(c, fail(POOCH_ENCCL, "ncclAllReduce (profile tail) failed: %d", r));
+        const size_t cnt = std::min<size_t>(b.hi - b.lo, dyn / 4) / 4 * 4;
+        if (c->nccl) {
+          int r = g_nccl.allReduce(fptr(c, c->resident_end), fptr(c, c->resident_end), cnt, 7, 0, c->nccl, st);
+          if (r != 0) return ctx_fail(c, fail(POOCH_ENCCL, "ncclAllReduce (profile tail) failed: %d", r));
+        } else {  // its own barrier slots (after the buckets'), same stage range
+          CTX_CHECK(c, peer_allreduce(c, fptr(c, c->resident_end), b.lo, b.lo + cnt, (int)c->buckets.size(), st));
+        }
       }
       POOCH_CHECK(sgd_momentum(fptr(c, c->off_tile), fptr(c, c->off_tile), fptr(c, c->off_tile), 0, 0.f, 0.f, 0.f, st));
       POOCH_CUDA(cudaEventRecord(e1, st));

@@ -45,6 +45,21 @@ def broadcast_unique_id(rank: int, group=None, device="cpu") -> bytes:
     return bytes(buf.cpu().numpy().tobytes())
 
 
+def setup_peers(ctx, rank: int, world: int, group=None):
+    """Peer-memory allreduce (libpooch's own, peer.cu): each rank exports its exchange buffer,
+    the 64-byte IPC handles are all-gathered over the (gloo / nccl) process group, every rank
+    maps every other rank's buffer. Returns the exchange buffer's bytes (outside the arena)."""
+    import torch.distributed as dist
+    h = ctx.peer_open(rank, world)
+    handles = [None] * world
+    if world > 1:
+        dist.all_gather_object(handles, h, group=group)
+    else:
+        handles = [h]
+    ctx.set_peers(handles)
+    return ctx.peer_bytes
+
+
 def relaunch_argv(script: str, argv, nproc: int, port: int):
     """`bench.py --gpus N` run without a launcher (WORLD_SIZE unset) re-executes itself under
     torch.distributed.run with one process per GPU on 127.0.0.1 -- the driver's own launch line."""

@@ -136,6 +136,20 @@ class Context:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         self._chk(lib.pooch_set_comm(self.h, buf, rank, world))
 
+    def peer_open(self, rank: int, world: int) -> bytes:
+        """Allocate this rank's IPC-exported exchange buffer for the peer-memory allreduce;
+        returns its 64-byte cudaIpcMemHandle (all-gather them, then set_peers)."""
+        h = C.create_string_buffer(64)
+        nb = C.c_uint64(0)
+        self._chk(lib.pooch_peer_open(self.h, int(rank), int(world), h, C.byref(nb)))
+        self.peer_bytes = nb.value
+        return bytes(h.raw)
+
+    def set_peers(self, handles):
+        """Map every rank's exchange buffer (handles in rank order)."""
+        buf = C.create_string_buffer(b"".join(bytes(x) for x in handles), 64 * len(handles))
+        self._chk(lib.pooch_set_peers(self.h, buf))
+
     def allreduce_buckets(self):
         """[(lo, hi, close_task)] float ranges of the gradient region allreduced per bucket."""
         n = C.c_int32(0)
