@@ -170,38 +170,128 @@ def upconv3d_bwd(dy, x, w):
     return dx, dw
 
 
-def maxpool3d_fwd(x, k=2, stride=2):
-    """Max over k^3 windows (no padding)."""
+def _pad3(x, pad, value=0.0):
+    return np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad), (pad, pad)), constant_values=value) if pad else x
+
+
+def maxpool3d_fwd(x, k=2, stride=2, pad=0):
+    """Max over k^3 windows, -inf padding (the U-Net's 2^3 / 2 has none; ResNeXt-101 (3D)'s
+    3^3 / 2 pads 1)."""
     n, c, d, h, w = x.shape
-    do, ho, wo = ((e - k) // stride + 1 for e in (d, h, w))
+    do, ho, wo = (conv3d_out(e, k, stride, pad) for e in (d, h, w))
+    xp = _pad3(x, pad, -np.inf)
     y = np.full((n, c, do, ho, wo), -np.inf, dtype=x.dtype)
     for u in range(k):
         for v in range(k):
             for t in range(k):
-                y = np.maximum(y, _win3(x, u, v, t, stride, do, ho, wo))
+                y = np.maximum(y, _win3(xp, u, v, t, stride, do, ho, wo))
     return y
 
 
-def maxpool3d_bwd(dy, x, k=2, stride=2):
+def maxpool3d_bwd(dy, x, k=2, stride=2, pad=0):
     """Gradient to the FIRST maximum in (u, v, t) row-major window order (Reading 25)."""
     n, c, d, h, w = x.shape
     _, _, do, ho, wo = dy.shape
+    xp = _pad3(x, pad, -np.inf)
     best = np.full(dy.shape, -np.inf, dtype=x.dtype)
     arg = np.full(dy.shape, -1, dtype=np.int64)
     for u in range(k):
         for v in range(k):
             for t in range(k):
-                win = _win3(x, u, v, t, stride, do, ho, wo)
+                win = _win3(xp, u, v, t, stride, do, ho, wo)
                 better = win > best
                 best = np.where(better, win, best)
                 arg = np.where(better, (u * k + v) * k + t, arg)
-    dx = np.zeros_like(x, dtype=_dt(dy, x))
+    dxp = np.zeros(xp.shape, dtype=_dt(dy, x))
     for u in range(k):
         for v in range(k):
             for t in range(k):
-                dx[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
-                   t:t + stride * (wo - 1) + 1:stride] += dy * (arg == (u * k + v) * k + t)
-    return dx
+                dxp[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
+                    t:t + stride * (wo - 1) + 1:stride] += dy * (arg == (u * k + v) * k + t)
+    return dxp[:, :, pad:pad + d, pad:pad + h, pad:pad + w].copy()
+
+
+# ------------------------------------------------------ ResNeXt-101 (3D), SURVEY 8(f) f4
+# "we computed ResNext101 (3D) [resnext] for various input data sizes with batch size of 1.
+# ResNext101 (3D) is an extension of ResNext101 for video recognition based on [3dnn]"
+# (P:L386, Sec. 5.2). Its bottleneck's 3^3 convolution is GROUPED (ResNeXt's aggregated
+# transformation, cardinality 32 [resnext]) and its stem strides (1, 2, 2) [3dnn]: a grouped
+# convolution with a per-axis stride, written out below from its definition.
+def _s3(stride):
+    return (stride,) * 3 if isinstance(stride, int) else tuple(int(v) for v in stride)
+
+
+def _win3s(xp, u, v, t, s3, do, ho, wo):
+    sd, sh, sw = s3
+    return xp[:, :, u:u + sd * (do - 1) + 1:sd, v:v + sh * (ho - 1) + 1:sh, t:t + sw * (wo - 1) + 1:sw]
+
+
+def gconv3d_out(dhw, k, stride, pad):
+    return tuple(conv3d_out(e, k, s, pad) for e, s in zip(dhw, _s3(stride)))
+
+
+def gconv3d_fwd(x, w, stride=1, pad=0, groups=1):
+    """Grouped 3D convolution, zero padded, stride (sd, sh, sw):
+    y[n, g*Og+o, a, i, j] = sum_{c < Cg, u, v, t} x[n, g*Cg+c, sd*a+u-p, sh*i+v-p, sw*j+t-p]
+                                                  * w[g*Og+o, c, u, v, t]
+    with Cg = C / groups, Og = O / groups; w is [O, Cg, k, k, k] (groups = 1: conv3d_fwd)."""
+    n, c, d, h, wd = x.shape
+    o, cg, k, _, _ = w.shape
+    assert c == cg * groups and o % groups == 0
+    og = o // groups
+    s3 = _s3(stride)
+    do, ho, wo = gconv3d_out((d, h, wd), k, s3, pad)
+    xp = _pad3(x, pad)
+    y = np.zeros((n, o, do, ho, wo), dtype=_dt(x, w))
+    for g in range(groups):
+        xg = xp[:, g * cg:(g + 1) * cg]
+        wg = w[g * og:(g + 1) * og]
+        acc = np.zeros((n, do, ho, wo, og), dtype=y.dtype)
+        for u in range(k):
+            for v in range(k):
+                for t in range(k):
+                    acc += np.tensordot(_win3s(xg, u, v, t, s3, do, ho, wo), wg[:, :, u, v, t], axes=([1], [1]))
+        y[:, g * og:(g + 1) * og] = acc.transpose(0, 4, 1, 2, 3)
+    return y
+
+
+def gconv3d_dgrad(dy, w, x_shape, stride=1, pad=0, groups=1):
+    """dx = adjoint of gconv3d_fwd w.r.t. x."""
+    n, c, d, h, wd = x_shape
+    o, cg, k, _, _ = w.shape
+    og = o // groups
+    sd, sh, sw = _s3(stride)
+    _, _, do, ho, wo = dy.shape
+    dxp = np.zeros((n, c, d + 2 * pad, h + 2 * pad, wd + 2 * pad), dtype=_dt(dy, w))
+    for g in range(groups):
+        dyg = dy[:, g * og:(g + 1) * og]
+        wg = w[g * og:(g + 1) * og]
+        for u in range(k):
+            for v in range(k):
+                for t in range(k):
+                    contrib = np.tensordot(dyg, wg[:, :, u, v, t], axes=([1], [0]))   # [n,do,ho,wo,cg]
+                    dxp[:, g * cg:(g + 1) * cg, u:u + sd * (do - 1) + 1:sd, v:v + sh * (ho - 1) + 1:sh,
+                        t:t + sw * (wo - 1) + 1:sw] += contrib.transpose(0, 4, 1, 2, 3)
+    return dxp[:, :, pad:pad + d, pad:pad + h, pad:pad + wd].copy()
+
+
+def gconv3d_wgrad(x, dy, w_shape, stride=1, pad=0, groups=1):
+    """dw = adjoint of gconv3d_fwd w.r.t. w."""
+    o, cg, k, _, _ = w_shape
+    og = o // groups
+    s3 = _s3(stride)
+    _, _, do, ho, wo = dy.shape
+    xp = _pad3(x, pad)
+    dw = np.zeros(w_shape, dtype=_dt(x, dy))
+    for g in range(groups):
+        xg = xp[:, g * cg:(g + 1) * cg]
+        dyg = dy[:, g * og:(g + 1) * og]
+        for u in range(k):
+            for v in range(k):
+                for t in range(k):
+                    dw[g * og:(g + 1) * og, :, u, v, t] = np.tensordot(
+                        dyg, _win3s(xg, u, v, t, s3, do, ho, wo), axes=([0, 2, 3, 4], [0, 2, 3, 4]))
+    return dw
 
 
 # ----------------------------------------------------------------------------- BN
@@ -278,13 +368,13 @@ def maxpool_bwd(dy, x, k, stride, pad):
 
 
 def avgpool_fwd(x):
-    """Global average pool: [n,c,h,w] -> [n,c]."""
-    return x.mean(axis=(2, 3))
+    """Global average pool: [n,c,h,w] (or [n,c,d,h,w]) -> [n,c]."""
+    return x.mean(axis=tuple(range(2, x.ndim)))
 
 
 def avgpool_bwd(dy, x_shape):
-    n, c, h, w = x_shape
-    return np.broadcast_to(dy[:, :, None, None] / (h * w), x_shape).copy()
+    sp = int(np.prod(x_shape[2:]))
+    return np.broadcast_to(dy.reshape(dy.shape[:2] + (1,) * (len(x_shape) - 2)) / sp, x_shape).copy()
 
 
 # ----------------------------------------------------------------------------- FC
@@ -437,37 +527,40 @@ def maxpool_bwd_at(dy, x_shape, arg, k, stride, pad):
     return dxp[:, :, pad:pad + h, pad:pad + w].copy()
 
 
-def maxpool3d_argmax(xd, k=2, stride=2):
+def maxpool3d_argmax(xd, k=2, stride=2, pad=0):
     n, c, d, h, w = xd.shape
-    do, ho, wo = ((e - k) // stride + 1 for e in (d, h, w))
+    do, ho, wo = (conv3d_out(e, k, stride, pad) for e in (d, h, w))
+    xp = _pad3(xd, pad, -np.inf)
     best = np.full((n, c, do, ho, wo), -np.inf, dtype=xd.dtype)
     arg = np.full((n, c, do, ho, wo), -1, dtype=np.int64)
     for u in range(k):
         for v in range(k):
             for t in range(k):
-                win = _win3(xd, u, v, t, stride, do, ho, wo)
+                win = _win3(xp, u, v, t, stride, do, ho, wo)
                 better = win > best
                 best = np.where(better, win, best)
                 arg = np.where(better, (u * k + v) * k + t, arg)
     return arg
 
 
-def maxpool3d_fwd_at(x, arg, k=2, stride=2):
+def maxpool3d_fwd_at(x, arg, k=2, stride=2, pad=0):
     _, _, do, ho, wo = arg.shape
+    xp = _pad3(x, pad, -np.inf)
     y = np.zeros(arg.shape, dtype=x.dtype)
     for u in range(k):
         for v in range(k):
             for t in range(k):
-                y = np.where(arg == (u * k + v) * k + t, _win3(x, u, v, t, stride, do, ho, wo), y)
+                y = np.where(arg == (u * k + v) * k + t, _win3(xp, u, v, t, stride, do, ho, wo), y)
     return y
 
 
-def maxpool3d_bwd_at(dy, x_shape, arg, k=2, stride=2):
+def maxpool3d_bwd_at(dy, x_shape, arg, k=2, stride=2, pad=0):
     _, _, do, ho, wo = dy.shape
-    dx = np.zeros(x_shape, dtype=dy.dtype)
+    n, c, d, h, w = x_shape
+    dxp = np.zeros((n, c, d + 2 * pad, h + 2 * pad, w + 2 * pad), dtype=dy.dtype)
     for u in range(k):
         for v in range(k):
             for t in range(k):
-                dx[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
-                   t:t + stride * (wo - 1) + 1:stride] += dy * (arg == (u * k + v) * k + t)
-    return dx
+                dxp[:, :, u:u + stride * (do - 1) + 1:stride, v:v + stride * (ho - 1) + 1:stride,
+                    t:t + stride * (wo - 1) + 1:stride] += dy * (arg == (u * k + v) * k + t)
+    return dxp[:, :, pad:pad + d, pad:pad + h, pad:pad + w].copy()

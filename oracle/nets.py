@@ -56,6 +56,12 @@ class Task:
     cin: int = 0            # conv input channels (true, unpadded)
     bn: str = ""            # bnrelu_conv: name of the fused BN-ReLU (its gamma / beta)
     ratio: float = 0.0      # fc_relu_drop: dropout probability
+    groups: int = 1         # conv: grouped convolution (ResNeXt's cardinality), w is [O, cin/groups, k..]
+    stride_d: int = 0       # 3D conv: stride along depth (0: = stride); ResNeXt-101 (3D)'s stem is (1, 2, 2)
+
+    @property
+    def stride3(self):
+        return (self.stride_d or self.stride, self.stride, self.stride)
 
     @property
     def needs(self):
@@ -216,6 +222,53 @@ def unet3d(in_d: int = 256, width: int = 256, classes: int = 2, cin: int = 1) ->
     return net
 
 
+def resnext3d(in_dhw=(16, 112, 112), classes: int = 400, depth: int = 101, cardinality: int = 32,
+              cin: int = 3, widths=(128, 256, 512, 1024), blocks=None, stem: int = 64) -> Net:
+    """ResNeXt-101 (3D), the paper's third workload (Sec. 5.2; SURVEY 8(f)
+    f4), as [3dnn] builds it from ResNeXt [resnext]: conv 7^3 (stride (1, 2, 2), pad 3, 64) ->
+    BN -> ReLU -> max-pool 3^3 / 2 (pad 1); four stages of [3, 4, 23, 3] bottleneck blocks of
+    widths 128 / 256 / 512 / 1024 (= cardinality 32 x 4 / 8 / 16 / 32 channels per group):
+    conv 1^3 -> BN -> ReLU -> GROUPED conv 3^3 (32 groups; stride 2 in the first block of stages
+    2-4) -> BN -> ReLU -> conv 1^3 to twice the width -> BN, plus the shortcut (a 1^3 projection
+    conv + BN in each stage's first block, "shortcut type B"), -> add -> ReLU; global average
+    pool; FC to ``classes``. Task kinds are ResNet-50's (the bottleneck's tails, BN-ReLU
+    groups, pools); only the 3D geometry and the groups differ. depth 50: [3, 4, 6, 3].
+    ``widths`` / ``blocks`` / ``stem`` / ``cardinality`` shrink it for the finite-difference
+    pins (tests only)."""
+    blocks = blocks or {50: [3, 4, 6, 3], 101: [3, 4, 23, 3]}[depth]
+    d, h, w = in_dhw
+    net = Net("resnext%d_3d" % depth, (cin,) + tuple(in_dhw), classes)
+
+    def out3(dhw, k, s3, p):
+        return L.gconv3d_out(dhw, k, s3, p)
+    e = out3((d, h, w), 7, (1, 2, 2), 3)
+    c = net.add(Task("conv1", "conv", [-1], (stem,) + e, 2, 3, 7, cin, stride_d=1))
+    x = net.add(Task("bn1", "bnrelu", [c], (stem,) + e))
+    e = out3(e, 3, 2, 1)
+    x = net.add(Task("maxpool", "maxpool", [x], (stem,) + e, 2, 1, 3))
+    cin_ = stem
+    for si, (nb, mid) in enumerate(zip(blocks, widths)):
+        out = 2 * mid
+        for b in range(nb):
+            s = 2 if (b == 0 and si > 0) else 1
+            pre = f"layer{si + 1}.{b}"
+            c1 = net.add(Task(pre + ".conv1", "conv", [x], (mid,) + e, 1, 0, 1, cin_))
+            y1 = net.add(Task(pre + ".bn1", "bnrelu", [c1], (mid,) + e))
+            e2 = out3(e, 3, s, 1)
+            c2 = net.add(Task(pre + ".conv2", "conv", [y1], (mid,) + e2, s, 1, 3, mid, groups=cardinality))
+            y2 = net.add(Task(pre + ".bn2", "bnrelu", [c2], (mid,) + e2))
+            c3 = net.add(Task(pre + ".conv3", "conv", [y2], (out,) + e2, 1, 0, 1, mid))
+            if b == 0:
+                p = net.add(Task(pre + ".downsample", "conv", [x], (out,) + e2, s, 0, 1, cin_))
+                x = net.add(Task(pre + ".tail", "tail_proj", [c3, p], (out,) + e2))
+            else:
+                x = net.add(Task(pre + ".tail", "tail_id", [c3, x], (out,) + e2))
+            e, cin_ = e2, out
+    a = net.add(Task("avgpool", "avgpool", [x], (cin_, 1, 1)))
+    net.add(Task("fc", "fc_ce", [a], (classes, 1, 1), cin=cin_))
+    return net
+
+
 def fuse_bnrelu(net: Net) -> Net:
     """merge every ``bnrelu`` whose only consumer is a single-input 2D conv with
     32-multiple input channels (the B200 path's TMA-fed operand loader, which applies the
@@ -262,7 +315,7 @@ def param_shapes(net: Net):
             shapes[t.bn + ".gamma"] = (t.cin,)
             shapes[t.bn + ".beta"] = (t.cin,)
         if t.kind in ("conv", "bnrelu_conv", "conv_relu"):
-            shapes[t.name + ".w"] = (t.out_chw[0], t.cin) + (t.k,) * (len(t.out_chw) - 1)
+            shapes[t.name + ".w"] = (t.out_chw[0], t.cin // t.groups) + (t.k,) * (len(t.out_chw) - 1)
             if t.kind == "conv_relu":
                 shapes[t.name + ".b"] = (t.out_chw[0],)
         elif t.kind == "fc_relu_drop":
@@ -336,7 +389,10 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
 
     loss = None
     for t in net.tasks:
-        if t.kind == "conv":
+        if t.kind == "conv" and three and (t.groups > 1 or t.stride_d):
+            y = L.gconv3d_fwd(q(conv_in(t)), q(P[t.name + ".w"]), t.stride3, t.pad, t.groups)
+            cache = None
+        elif t.kind == "conv":
             f = L.conv3d_fwd if three else L.conv2d_fwd
             y = f(q(conv_in(t)), q(P[t.name + ".w"]), t.stride, t.pad)
             cache = None
@@ -369,12 +425,13 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             cache = (bc3, bcp)
         elif t.kind == "maxpool" and len(outs) in dec:
             xd = np.asarray(dec[len(outs)], np.float64)
-            arg = L.maxpool3d_argmax(xd, t.k, t.stride) if three else L.maxpool_argmax(xd, t.k, t.stride, t.pad)
-            y = (L.maxpool3d_fwd_at(get(t.inputs[0]), arg, t.k, t.stride) if three
+            arg = (L.maxpool3d_argmax(xd, t.k, t.stride, t.pad) if three
+                   else L.maxpool_argmax(xd, t.k, t.stride, t.pad))
+            y = (L.maxpool3d_fwd_at(get(t.inputs[0]), arg, t.k, t.stride, t.pad) if three
                  else L.maxpool_fwd_at(get(t.inputs[0]), arg, t.k, t.stride, t.pad))
             cache = arg
         elif t.kind == "maxpool":
-            y = (L.maxpool3d_fwd(get(t.inputs[0]), t.k, t.stride) if three
+            y = (L.maxpool3d_fwd(get(t.inputs[0]), t.k, t.stride, t.pad) if three
                  else L.maxpool_fwd(get(t.inputs[0]), t.k, t.stride, t.pad))
             cache = None
         elif t.kind == "conv_relu":
@@ -397,7 +454,7 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
             y = yf[:, :, None, None]
             cache = (xf, z, keep)
         elif t.kind == "avgpool":
-            y = L.avgpool_fwd(get(t.inputs[0]))[:, :, None, None]
+            y = L.avgpool_fwd(get(t.inputs[0]))[:, :, None, None]     # 3D nets too: [n, c, 1, 1]
             cache = None
         elif t.kind == "fc_ce":
             xf = _flat_hwc(get(t.inputs[0]))
@@ -443,7 +500,12 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
         if t.kind == "conv":
             xin = conv_in(t)
             w = P[t.name + ".w"]
-            fw, fd = (L.conv3d_wgrad, L.conv3d_dgrad) if three else (L.conv2d_wgrad, L.conv2d_dgrad)
+            if three and (t.groups > 1 or t.stride_d):
+                g_, s_ = t.groups, t.stride3
+                fw = lambda a, b, sh, st, pd: L.gconv3d_wgrad(a, b, sh, s_, pd, g_)  # noqa: E731
+                fd = lambda a, b, sh, st, pd: L.gconv3d_dgrad(a, b, sh, s_, pd, g_)  # noqa: E731
+            else:
+                fw, fd = (L.conv3d_wgrad, L.conv3d_dgrad) if three else (L.conv2d_wgrad, L.conv2d_dgrad)
             grads[t.name + ".w"] += fw(q(xin), q(dy), w.shape, t.stride, t.pad)
             if t.inputs[0] >= 0:
                 dx = fd(q(dy), q(w), xin.shape, t.stride, t.pad)
@@ -487,10 +549,10 @@ def forward_backward(net: Net, params: dict, x_nhwc: np.ndarray, labels: np.ndar
                 acc(t.inputs[1], dz)
         elif t.kind == "maxpool" and cache is not None:      # winners from ``decisions``
             shape = get(t.inputs[0]).shape
-            acc(t.inputs[0], L.maxpool3d_bwd_at(dy, shape, cache, t.k, t.stride) if three
+            acc(t.inputs[0], L.maxpool3d_bwd_at(dy, shape, cache, t.k, t.stride, t.pad) if three
                 else L.maxpool_bwd_at(dy, shape, cache, t.k, t.stride, t.pad))
         elif t.kind == "maxpool":
-            acc(t.inputs[0], L.maxpool3d_bwd(dy, get(t.inputs[0]), t.k, t.stride) if three
+            acc(t.inputs[0], L.maxpool3d_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad) if three
                 else L.maxpool_bwd(dy, get(t.inputs[0]), t.k, t.stride, t.pad))
         elif t.kind == "conv_relu":
             dz = _relu_bwd_dec(dy, i)
