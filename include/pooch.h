@@ -110,6 +110,8 @@ typedef struct {
   int32_t k, stride, pad;   /* conv / pool geometry */
   char name[48];
   int32_t dout;             /* output depth of a 3D network's map (0 in 2D networks) */
+  int32_t groups;           /* POOCH_L_CONV: 0 / 1 dense, > 1 grouped (see pooch_conv_desc.groups) */
+  int32_t stride_d;         /* 3D POOCH_L_CONV: depth stride (0 = stride) */
 } pooch_layer_desc;
 
 typedef struct {
@@ -123,7 +125,9 @@ typedef struct {
  * (configs 2, 3, 5), 2 = ResNet-50 v1, 3 = 3D U-Net (config 4: in_hw^3 volume, base width
  * `width` -> level widths w, 2w, 4w, 4w, input channels padded 1 -> 32), 4 = AlexNet (the
  * paper's second workload: single-tower, in_hw 227, dropout 0.5; width unused;
- * 13 maps, 62,378,344 parameters). which |
+ * 13 maps, 62,378,344 parameters), 5 = ResNeXt-101 (3D) (the paper's third workload, SURVEY 8(f)
+ * f4: input [1, D = width, H = W = in_hw, 3 -> 32 channels], 207 maps, grouped 3^3 convs), 6 = its
+ * depth-50 variant ([3, 4, 6, 3] blocks; tests). which |
  * POOCH_NET_FUSE_BNRELU merges every BN-ReLU whose only consumer is a single-input 2D conv with
  * cin % 32 == 0 and stride <= 2 into that conv (POOCH_L_BNRELU_CONV; same function and
  * parameters, fewer maps: ResNet-50 105 -> 73, tiny CNN 10 -> 7). Fills up to
@@ -430,6 +434,12 @@ typedef struct {
                          weights [K,R,R,R,C]; requires C, K multiples of 32 (TMA-fed kernels) */
   int32_t C1;         /* 0: one input. > 0: the input is the channel concatenation of two
                          tensors x0 [..,C1] and x1 [..,C-C1] (the *2 entry points); C1 % 32 == 0 */
+  int32_t groups;     /* 0 / 1: dense. > 1: grouped 3D conv (ResNeXt-101 (3D), SURVEY 8(f) f4;
+                         definition: oracle layers.gconv3d_fwd, the aggregated transformation of
+                         P:L386's ResNeXt): D > 0, C == K, C / groups in {4, 8, 16, 32}, K % 32 == 0,
+                         R == S in {1, 3}, strides <= 2; weights [K][R][R][R][C/groups], and dgrad
+                         reads that same (untransposed) layout as `wt`. FP32 on the CUDA cores. */
+  int32_t stride_d;   /* 3D: stride along depth; 0 = `stride` (ResNeXt-101 (3D)'s stem: 1, 2, 2) */
 } pooch_conv_desc;
 
 pooch_status pooch_op_conv_fwd(const pooch_conv_desc* d, const float* x, const float* w, float* y,
@@ -501,6 +511,16 @@ pooch_status pooch_op_bn_relu_bwd(const float* x, const float* gy, const float* 
 pooch_status pooch_op_maxpool3d_fwd(const float* x, float* y, int32_t D, int32_t H, int32_t W, int32_t C, void* stream);
 pooch_status pooch_op_maxpool3d_bwd(const float* x, const float* gy, float* gx, int32_t D, int32_t H, int32_t W,
                                     int32_t C, int32_t accumulate, void* stream);
+/* 3D max-pool with any k / s / p (-inf padding; ResNeXt-101 (3D)'s 3^3 / 2 pad 1):
+ * y [Do][Ho][Wo][C], Do = (D + 2p - k)/s + 1; bwd gx (=|+=) the gradient routed to the first
+ * maximum of every window in (d, h, w) row-major order (Reading 25), gathered from the input side
+ * (overlapping windows add in output order); arg_ws: device workspace of Do*Ho*Wo*C bytes.
+ * k2 s2 p0 runs the tiling kernels above (arg_ws unused). C % 4 == 0, 1 <= k <= 6, p < k. */
+pooch_status pooch_op_maxpool3d_fwd_k(const float* x, float* y, int32_t D, int32_t H, int32_t W, int32_t C, int32_t k,
+                                      int32_t s, int32_t p, void* stream);
+pooch_status pooch_op_maxpool3d_bwd_k(const float* x, const float* gy, float* gx, void* arg_ws, int32_t D, int32_t H,
+                                      int32_t W, int32_t C, int32_t k, int32_t s, int32_t p, int32_t accumulate,
+                                      void* stream);
 /* D[split][M][N] = A * B^T on the tensor-core core, A [M][K] and B [N][K] row-major (K-major);
  * a_mn = 2 selects the 3xTF32 path, other non-zero a_mn / b_mn (MN-major operands) return
  * POOCH_EUSAGE; bn in {64,128,256} (64/128 for 3xTF32); splits >= 1. Unit test only. */

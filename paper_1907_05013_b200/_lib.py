@@ -33,13 +33,14 @@ P = C.POINTER
 
 
 class ConvDesc(C.Structure):
-    _fields_ = [(n, c_i32) for n in ("N", "H", "W", "C", "K", "R", "S", "stride", "pad", "precision", "D", "C1")]
+    _fields_ = [(n, c_i32) for n in ("N", "H", "W", "C", "K", "R", "S", "stride", "pad", "precision", "D", "C1",
+                                     "groups", "stride_d")]
 
 
 class LayerDesc(C.Structure):
     _fields_ = [("kind", c_i32), ("in0", c_i32), ("in1", c_i32), ("cin", c_i32), ("cout", c_i32),
                 ("hout", c_i32), ("wout", c_i32), ("k", c_i32), ("stride", c_i32), ("pad", c_i32),
-                ("name", C.c_char * 48), ("dout", c_i32)]
+                ("name", C.c_char * 48), ("dout", c_i32), ("groups", c_i32), ("stride_d", c_i32)]
 
 
 class IODesc(C.Structure):
@@ -124,6 +125,9 @@ SIGNATURES = {
     "pooch_refine_problem": (c_i32, [c_vp, c_vp, c_i32, c_u64, c_vp, P(c_i64), P(c_i32)]),
     "pooch_op_conv_fwd_bnrelu": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pooch_op_conv_wgrad_bnrelu": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "pooch_op_maxpool3d_fwd_k": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "pooch_op_maxpool3d_bwd_k": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                         c_i32, c_vp]),
     "pooch_op_maxpool2d_fwd": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_op_maxpool2d_bwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_op_bn_ws_bytes": (c_sz, [c_i32]),

@@ -25,14 +25,18 @@ ConvGeom conv_geom(const pooch_conv_desc& d) {
   g.Ho = (d.H + 2 * d.pad - d.R) / d.stride + 1;
   g.Wo = (d.W + 2 * d.pad - d.S) / d.stride + 1;
   g.D = d.D;
-  g.Do = d.D > 0 ? (d.D + 2 * d.pad - d.R) / d.stride + 1 : 0;
   g.C1 = d.C1;
+  g.groups = d.groups > 1 ? d.groups : 1;
+  g.stride_d = d.D > 0 ? d.stride_d : 0;
+  g.Do = d.D > 0 ? (d.D + 2 * d.pad - d.R) / g.sd() + 1 : 0;
   return g;
 }
 
 bool conv_shape_ok(const ConvGeom& g) {
   bool ok = g.N > 0 && g.H > 0 && g.W > 0 && g.C > 0 && g.K > 0 && g.R > 0 && g.S > 0 && g.stride > 0 &&
             g.pad >= 0 && g.C % 4 == 0 && g.K % 4 == 0 && g.Ho > 0 && g.Wo > 0;
+  if (g.groups > 1) return ok && g.C1 == 0 && gconv_shape_ok(g);
+  if (g.stride_d > 0 && g.sd() > 2) return false;
   if (g.is3d() || g.C1 > 0) {
     // the 3D / two-source convs run only on the TMA-fed kernels (the launchers fail with
     // POOCH_EUSAGE if the driver offers no tensor maps); this check is structural
@@ -283,7 +287,7 @@ static GemmParams base_params(const ConvGeom& g) {
   p.K = g.K; p.R = g.R; p.S = g.S;
   p.Ho = g.Ho; p.Wo = g.Wo; p.stride = g.stride; p.pad = g.pad;
   p.T = g.T();
-  p.st3 = g.is3d() ? g.stride : 1;
+  p.st3 = g.sd();
   p.pad3 = g.is3d() ? g.pad : 0;
   p.dg_nt = 1;
   return p;
@@ -295,8 +299,9 @@ static int out3(const ConvGeom& g) { return g.is3d() ? g.Do : g.N; }
 static int64_t out_pixels(const ConvGeom& g) { return (int64_t)out3(g) * g.Ho * g.Wo; }
 
 int conv_stat_tiles(const ConvGeom& g) {
+  if (g.groups > 1) return gconv_stat_tiles(g);
   if (fwd_uses_tma(g) || fwd_uses_stem4(g)) {
-    PixBox b = choose_box(out3(g), g.Ho, g.Wo, g.stride, g.is3d() ? g.stride : 1, g.is3d());
+    PixBox b = choose_box(out3(g), g.Ho, g.Wo, g.stride, g.sd(), g.is3d());
     return b.tiles_w * b.tiles_h * b.tiles_n;
   }
   return (int)((out_pixels(g) + 127) / 128);
@@ -305,6 +310,10 @@ int conv_stat_tiles(const ConvGeom& g) {
 pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
                              float* stat_sq, const float* bias, cudaStream_t st, const float* x1,
                              const float* xf_scale, const float* xf_shift, bool relu) {
+  if (g.groups > 1) {
+    if (bias || x1 || xf_scale || relu) return fail(POOCH_EUSAGE, "grouped conv: plain fwd only");
+    return gconv_fwd(g, x, w, y, stat_sum, stat_sq, st);
+  }
   GemmParams p = base_params(g);
   p.relu = relu ? 1 : 0;
   if (xf_scale && (!fwd_uses_tma(g) || g.is3d() || g.C1 > 0 || !xf_shift))
@@ -385,6 +394,10 @@ pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, 
 
 pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* wt, float* dx, bool accumulate,
                                cudaStream_t st, float* dx1, bool accumulate1) {
+  if (g.groups > 1) {  // wt: the plain [K][taps][C / groups] weight (no transpose)
+    if (dx1) return fail(POOCH_EUSAGE, "grouped conv: one source");
+    return gconv_dgrad(g, dy, wt, dx, accumulate, st);
+  }
   GemmParams p = base_params(g);
   p.M = (int)((int64_t)in3(g) * g.H * g.W);
   p.Ng = g.C;
@@ -499,7 +512,7 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
   int M = g.K, Ng = rsc;
   w.bn = 128;
   if (w.tma) {
-    w.box = choose_kbox(out3(g), g.Ho, g.Wo, g.stride, g.is3d() ? g.stride : 1);
+    w.box = choose_kbox(out3(g), g.Ho, g.Wo, g.stride, g.sd());
     if (const char* e = getenv("POOCH_KBOX")) {  // profiling experiments only
       int a = 0, b = 0, c = 0;
       if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && a * b * c == 32)
@@ -545,6 +558,7 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
 }
 
 size_t conv_wgrad_ws_bytes(const ConvGeom& g) {
+  if (g.groups > 1) return gconv_wgrad_ws_bytes(g);
   WgradPlan w = wgrad_plan(g);
   return (w.splits > 1 || w.swap) ? (size_t)w.splits * g.K * g.T() * g.R * g.S * g.C * sizeof(float) : 0;
 }
@@ -588,6 +602,10 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ ws, float* __re
 pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws,
                                size_t ws_bytes, cudaStream_t st, const float* x1, const float* xf_scale,
                                const float* xf_shift) {
+  if (g.groups > 1) {
+    if (x1 || xf_scale) return fail(POOCH_EUSAGE, "grouped conv: plain wgrad only");
+    return gconv_wgrad(g, x, dy, dw, ws, ws_bytes, st);
+  }
   WgradPlan w = wgrad_plan(g);
   GemmParams p = base_params(g);
   if (xf_scale && (!w.tma || g.is3d() || g.C1 > 0 || !xf_shift))

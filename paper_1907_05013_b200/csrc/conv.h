@@ -13,7 +13,12 @@ struct ConvGeom {
   int D = 0, Do = 0;
   // two-source input: x = concat_c(x0 [.., C1], x1 [.., C - C1]); 0 = one source
   int C1 = 0;
+  // grouped convolution (ResNeXt; gconv.cu): groups > 1, C == K, C / groups in {4, 8, 16, 32}
+  int groups = 1;
+  // 3D: stride along depth (0 = stride); ResNeXt-101 (3D)'s stem strides (1, 2, 2)
+  int stride_d = 0;
   bool is3d() const { return D > 0; }
+  int sd() const { return D > 0 ? (stride_d > 0 ? stride_d : stride) : 1; }
   int T() const { return D > 0 ? R : 1; }
 };
 ConvGeom conv_geom(const pooch_conv_desc& d);
@@ -35,5 +40,17 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
 // number of M-tiles of the forward pass = rows of its BN partial-sum arrays
 int conv_stat_tiles(const ConvGeom& g);
 inline int conv_mtiles(const ConvGeom& g) { return conv_stat_tiles(g); }
+
+// grouped 3D convolution on the CUDA cores (gconv.cu); the launch_conv_* entry points dispatch
+// to these when g.groups > 1. dgrad reads the weights in their own [K][taps][C/groups] layout.
+bool gconv_shape_ok(const ConvGeom& g);
+int gconv_stat_tiles(const ConvGeom& g);
+size_t gconv_wgrad_ws_bytes(const ConvGeom& g);
+pooch_status gconv_fwd(const ConvGeom& g, const float* x, const float* w, float* y, float* stat_sum,
+                       float* stat_sq, cudaStream_t st);
+pooch_status gconv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
+                         cudaStream_t st);
+pooch_status gconv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes,
+                         cudaStream_t st);
 
 }  // namespace pooch

@@ -776,7 +776,108 @@ pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* ar
   return POOCH_OK;
 }
 
-pooch_status maxpool3d_fwd(const float* x, float* y, int D, int H, int W, int C, cudaStream_t st) {
+// General 3D max-pool (k, s, p; -inf padding): ResNeXt-101 (3D)'s 3^3 / 2 pad 1. Windows overlap,
+// so the backward pass records each output's first-maximum window index (uint8, (u*k+v)*k+t)
+// and then gathers on the INPUT side: every input voxel sums, in (od, oh, ow) order, the dy of
+// the windows that cover it and chose it -- one writer per element, deterministic.
+namespace {
+
+struct Pool3 {
+  int D, H, W, C4, Do, Ho, Wo, k, s, p;
+};
+
+__global__ void maxpool3d_gen_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,  // y / arg nullable
+                                         uchar4* __restrict__ arg, Pool3 q) {
+  const int64_t total = (int64_t)q.Do * q.Ho * q.Wo * q.C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = (int)(i % q.C4);
+    int64_t t = i / q.C4;
+    const int wo = (int)(t % q.Wo);
+    t /= q.Wo;
+    const int ho = (int)(t % q.Ho);
+    const int dz = (int)(t / q.Ho);
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int a[4] = {0, 0, 0, 0};
+    for (int u = 0; u < q.k; ++u) {
+      const int zi = dz * q.s - q.p + u;
+      if (zi < 0 || zi >= q.D) continue;
+      for (int v = 0; v < q.k; ++v) {
+        const int hi = ho * q.s - q.p + v;
+        if (hi < 0 || hi >= q.H) continue;
+        for (int w = 0; w < q.k; ++w) {
+          const int wi = wo * q.s - q.p + w;
+          if (wi < 0 || wi >= q.W) continue;
+          const float4 v4 = ld4(x + ((((int64_t)zi * q.H + hi) * q.W + wi) * q.C4 + c4) * 4);
+          const float va[4] = {v4.x, v4.y, v4.z, v4.w};
+          const int e = (u * q.k + v) * q.k + w;
+          for (int j = 0; j < 4; ++j)
+            if (va[j] > best[j]) {  // strict: the first maximum wins
+              best[j] = va[j];
+              a[j] = e;
+            }
+        }
+      }
+    }
+    if (y) st4(y + 4 * i, make_float4(best[0], best[1], best[2], best[3]));
+    if (arg) arg[i] = make_uchar4((unsigned char)a[0], (unsigned char)a[1], (unsigned char)a[2], (unsigned char)a[3]);
+  }
+}
+
+__global__ void maxpool3d_gen_bwd_kernel(const uchar4* __restrict__ arg, const float* __restrict__ gy,
+                                         float* __restrict__ gx, Pool3 q, int accumulate) {
+  const int64_t total = (int64_t)q.D * q.H * q.W * q.C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = (int)(i % q.C4);
+    int64_t t = i / q.C4;
+    const int wi = (int)(t % q.W);
+    t /= q.W;
+    const int hi = (int)(t % q.H);
+    const int zi = (int)(t / q.H);
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    // outputs whose window covers this voxel: od*s - p <= zi <= od*s - p + k - 1
+    const int d0 = max(0, (zi + q.p - q.k + q.s) / q.s), d1 = min(q.Do - 1, (zi + q.p) / q.s);
+    const int h0 = max(0, (hi + q.p - q.k + q.s) / q.s), h1 = min(q.Ho - 1, (hi + q.p) / q.s);
+    const int w0 = max(0, (wi + q.p - q.k + q.s) / q.s), w1 = min(q.Wo - 1, (wi + q.p) / q.s);
+    for (int od = d0; od <= d1; ++od)
+      for (int oh = h0; oh <= h1; ++oh)
+        for (int ow = w0; ow <= w1; ++ow) {
+          const int e = ((zi - (od * q.s - q.p)) * q.k + (hi - (oh * q.s - q.p))) * q.k + (wi - (ow * q.s - q.p));
+          const int64_t oi = (((int64_t)od * q.Ho + oh) * q.Wo + ow) * q.C4 + c4;
+          const uchar4 a = arg[oi];
+          const float4 g = ld4(gy + 4 * oi);
+          if (a.x == e) o[0] += g.x;
+          if (a.y == e) o[1] += g.y;
+          if (a.z == e) o[2] += g.z;
+          if (a.w == e) o[3] += g.w;
+        }
+    float* dst = gx + 4 * i;
+    if (accumulate) {
+      const float4 q4 = ld4(dst);
+      o[0] += q4.x; o[1] += q4.y; o[2] += q4.z; o[3] += q4.w;
+    }
+    st4(dst, make_float4(o[0], o[1], o[2], o[3]));
+  }
+}
+
+}  // namespace
+
+static Pool3 pool3(int D, int H, int W, int C, int k, int s, int p) {
+  Pool3 q{D, H, W, C / 4, (D + 2 * p - k) / s + 1, (H + 2 * p - k) / s + 1, (W + 2 * p - k) / s + 1, k, s, p};
+  return q;
+}
+
+pooch_status maxpool3d_fwd(const float* x, float* y, int D, int H, int W, int C, cudaStream_t st, int k, int s,
+                           int p) {
+  if (!(k == 2 && s == 2 && p == 0)) {
+    if (C % 4 || k < 1 || k > 6 || s < 1 || p < 0 || p >= k || D + 2 * p < k || H + 2 * p < k || W + 2 * p < k)
+      return fail(POOCH_EUSAGE, "3D max-pool: bad k / s / p or C %% 4 != 0");
+    const Pool3 q = pool3(D, H, W, C, k, s, p);
+    const int64_t total = (int64_t)q.Do * q.Ho * q.Wo * q.C4;
+    count_launch();
+    maxpool3d_gen_fwd_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, y, nullptr, q);
+    POOCH_CUDA(cudaGetLastError());
+    return POOCH_OK;
+  }
   if (D % 2 || H % 2 || W % 2 || C % 4) return fail(POOCH_EUSAGE, "3D max-pool needs even extents, C % 4 == 0");
   int64_t total = (int64_t)(D / 2) * (H / 2) * (W / 2) * C / 4;
   count_launch();
@@ -786,7 +887,22 @@ pooch_status maxpool3d_fwd(const float* x, float* y, int D, int H, int W, int C,
 }
 
 pooch_status maxpool3d_bwd(const float* x, const float* gy, float* gx, int D, int H, int W, int C, bool accumulate,
-                           cudaStream_t st) {
+                           cudaStream_t st, int k, int s, int p, uint8_t* arg_ws) {
+  if (!(k == 2 && s == 2 && p == 0)) {
+    if (C % 4 || k < 1 || k > 6 || s < 1 || p < 0 || p >= k || !arg_ws)
+      return fail(POOCH_EUSAGE, "3D max-pool bwd: bad k / s / p, C %% 4 != 0 or no argmax workspace");
+    const Pool3 q = pool3(D, H, W, C, k, s, p);
+    const int64_t nout = (int64_t)q.Do * q.Ho * q.Wo * q.C4, nin = (int64_t)D * H * W * q.C4;
+    // the window winners, recomputed from x (the forward kernel storing only arg)
+    count_launch();
+    maxpool3d_gen_fwd_kernel<<<grid_for(nout, 256), 256, 0, st>>>(x, nullptr, reinterpret_cast<uchar4*>(arg_ws), q);
+    POOCH_CUDA(cudaGetLastError());
+    count_launch();
+    maxpool3d_gen_bwd_kernel<<<grid_for(nin, 256), 256, 0, st>>>(reinterpret_cast<const uchar4*>(arg_ws), gy, gx, q,
+                                                                  accumulate ? 1 : 0);
+    POOCH_CUDA(cudaGetLastError());
+    return POOCH_OK;
+  }
   if (D % 2 || H % 2 || W % 2 || C % 4) return fail(POOCH_EUSAGE, "3D max-pool needs even extents, C % 4 == 0");
   int64_t total = (int64_t)(D / 2) * (H / 2) * (W / 2) * C / 4;
   count_launch();
@@ -944,6 +1060,20 @@ extern "C" pooch_status pooch_op_maxpool3d_fwd(const float* x, float* y, int32_t
                                                void* stream) {
   if (!x || !y || D < 2 || H < 2 || W < 2 || C <= 0 || C % 4) return pooch::fail(POOCH_EUSAGE, "maxpool3d: bad arguments");
   return pooch::maxpool3d_fwd(x, y, D, H, W, C, (cudaStream_t)stream);
+}
+
+extern "C" pooch_status pooch_op_maxpool3d_fwd_k(const float* x, float* y, int32_t D, int32_t H, int32_t W,
+                                                 int32_t C, int32_t k, int32_t s, int32_t p, void* stream) {
+  if (!x || !y || D < 1 || H < 1 || W < 1 || C <= 0) return pooch::fail(POOCH_EUSAGE, "maxpool3d: bad arguments");
+  return pooch::maxpool3d_fwd(x, y, D, H, W, C, (cudaStream_t)stream, k, s, p);
+}
+
+extern "C" pooch_status pooch_op_maxpool3d_bwd_k(const float* x, const float* gy, float* gx, void* arg_ws, int32_t D,
+                                                 int32_t H, int32_t W, int32_t C, int32_t k, int32_t s, int32_t p,
+                                                 int32_t accumulate, void* stream) {
+  if (!x || !gy || !gx || D < 1 || H < 1 || W < 1 || C <= 0) return pooch::fail(POOCH_EUSAGE, "maxpool3d: bad arguments");
+  return pooch::maxpool3d_bwd(x, gy, gx, D, H, W, C, accumulate != 0, (cudaStream_t)stream, k, s, p,
+                              static_cast<uint8_t*>(arg_ws));
 }
 
 extern "C" pooch_status pooch_op_maxpool3d_bwd(const float* x, const float* gy, float* gx, int32_t D, int32_t H,

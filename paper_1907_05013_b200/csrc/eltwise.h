@@ -48,9 +48,13 @@ pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, i
 // gx = gradient routed to the first maximum of every window (argmax recomputed from x)
 // arg_ws: N*Ho*Wo*C bytes of scratch for the window argmax indices
 // 3D max-pool k2 s2 p0 over x [D][H][W][C] (batch 1); bwd re-derives the first-max argmax from x
-pooch_status maxpool3d_fwd(const float* x, float* y, int D, int H, int W, int C, cudaStream_t st);
+// 3D max-pool over x [D][H][W][C] (batch 1): k2 s2 p0 (the U-Net's, windows tile the input) or
+// any k / s / p with -inf padding (ResNeXt-101 (3D)'s k3 s2 p1; bwd then takes arg_ws of
+// Do*Ho*Wo*C bytes: the first-maximum index per output, gathered from the input side).
+pooch_status maxpool3d_fwd(const float* x, float* y, int D, int H, int W, int C, cudaStream_t st, int k = 2,
+                           int s = 2, int p = 0);
 pooch_status maxpool3d_bwd(const float* x, const float* gy, float* gx, int D, int H, int W, int C, bool accumulate,
-                           cudaStream_t st);
+                           cudaStream_t st, int k = 2, int s = 2, int p = 0, uint8_t* arg_ws = nullptr);
 pooch_status maxpool_bwd(const float* x, const float* gy, float* gx, uint8_t* arg_ws, int N, int H, int W, int C,
                          int k, int s, int p, int Ho, int Wo, cudaStream_t st);
 pooch_status avgpool_fwd(const float* x, float* y, int N, int HW, int C, cudaStream_t st);

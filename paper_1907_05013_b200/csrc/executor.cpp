@@ -158,7 +158,7 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
     }
     case POOCH_L_MAXPOOL:
       if (T.dout > 0)
-        return maxpool3d_fwd(p.in0, p.out, T.din, T.hin, T.win, T.cin, st);
+        return maxpool3d_fwd(p.in0, p.out, T.din, T.hin, T.win, T.cin, st, T.k, T.stride, T.pad);
       return maxpool_fwd(p.in0, p.out, B, T.hin, T.win, T.cin, T.k, T.stride, T.pad, T.hout, T.wout, st);
     case POOCH_L_CONV_RELU:   // bias + ReLU in the tensor-core epilogue
       return launch_conv_fwd(RG, p.in0, pw(c, R.w), p.out, nullptr, nullptr, pw(c, R.b), st, nullptr, nullptr,
@@ -171,7 +171,7 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
       return dropout_fwd(p.out, R.rows * T.cout, reinterpret_cast<const uint32_t*>(c->dev + c->off_rng), t,
                          T.k / 100.f, st);
     case POOCH_L_AVGPOOL:
-      return avgpool_fwd(p.in0, p.out, B, T.hin * T.win, T.cin, st);
+      return avgpool_fwd(p.in0, p.out, B, std::max(T.din, 1) * T.hin * T.win, T.cin, st);
     case POOCH_L_UPCONV:
       // transposed conv = the input-gradient pass of the equivalent k2 s2 conv (weights KTRSC
       // [cin][2][2][2][cout]), run through the parity-class dgrad with the transposed weights
@@ -219,7 +219,9 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
                                     p.in1));
       if (T.in0 >= 0) {
         if (mark) mark(c, FAM_CONV_DGRAD, t, R.flops, yb + xb * (p.acc0 ? 2 : 1) + wb);
-        POOCH_CHECK(launch_conv_dgrad(G, p.gy, fptr(c, c->off_wt) + R.wt_off, p.g0, p.acc0, st, p.g1, p.acc1));
+        // grouped convs read their weights untransposed (gconv.cu)
+        const float* wt = G.groups > 1 ? pw(c, R.w) : fptr(c, c->off_wt) + R.wt_off;
+        POOCH_CHECK(launch_conv_dgrad(G, p.gy, wt, p.g0, p.acc0, st, p.g1, p.acc1));
       }
       return POOCH_OK;
     }
@@ -291,11 +293,12 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
     }
     case POOCH_L_MAXPOOL:
       if (T.dout > 0)
-        return maxpool3d_bwd(p.in0, p.gy, p.g0, T.din, T.hin, T.win, T.cin, p.acc0, st);
+        return maxpool3d_bwd(p.in0, p.gy, p.g0, T.din, T.hin, T.win, T.cin, p.acc0, st, T.k, T.stride, T.pad,
+                             reinterpret_cast<uint8_t*>(c->dev + c->off_mparg));
       return maxpool_bwd(p.in0, p.gy, p.g0, reinterpret_cast<uint8_t*>(c->dev + c->off_mparg), B, T.hin, T.win, T.cin,
                          T.k, T.stride, T.pad, T.hout, T.wout, st);
     case POOCH_L_AVGPOOL:
-      return avgpool_bwd(p.gy, p.g0, B, T.hin * T.win, T.cin, st);
+      return avgpool_bwd(p.gy, p.g0, B, std::max(T.din, 1) * T.hin * T.win, T.cin, st);
     case POOCH_L_CONV_RELU:
     case POOCH_L_FC_RELU_DROP: {
       // dz = dy [y > 0] / (1 - p) in place on this task's output gradient (kept dropout units are
@@ -378,14 +381,15 @@ double fwd_bytes(pooch_ctx* c, int t) {
     case POOCH_L_CONV:
     case POOCH_L_CONV_RELU:
     case POOCH_L_BNRELU_CONV: return 4.0 * (R.geom.N * din * R.geom.H * R.geom.W * R.geom.C + e +
-                                      (double)R.geom.K * R.geom.T() * R.geom.R * R.geom.S * R.geom.C);
+                                      (double)R.geom.K * R.geom.T() * R.geom.R * R.geom.S * R.geom.C /
+                                          R.geom.groups);
     case POOCH_L_LRN: return 8.0 * e;
     case POOCH_L_UPCONV: return 4.0 * (din * T.hin * T.win * T.cin + e + 8.0 * T.cin * T.cout);
     case POOCH_L_BNRELU: return 8.0 * e;
     case POOCH_L_TAIL_PROJ:
     case POOCH_L_TAIL_ID: return 12.0 * e;
     case POOCH_L_MAXPOOL: return 4.0 * ((double)c->g.io.batch * din * T.hin * T.win * T.cin + e);
-    case POOCH_L_AVGPOOL: return 4.0 * ((double)c->g.io.batch * T.hin * T.win * T.cin + e);
+    case POOCH_L_AVGPOOL: return 4.0 * ((double)c->g.io.batch * std::max(T.din, 1) * T.hin * T.win * T.cin + e);
     default: return 4.0 * (R.geom.N * (double)R.geom.C + R.geom.N * (double)R.geom.K + (double)R.geom.K * R.geom.C);
   }
 }
@@ -399,7 +403,7 @@ double bwd_bytes(pooch_ctx* c, int t) {
     case POOCH_L_TAIL_ID: return 4.0 * 8 * e;
     case POOCH_L_MAXPOOL:
       return 4.0 * (2.0 * c->g.io.batch * (T.dout > 0 ? T.din : 1) * T.hin * T.win * T.cin + e) + e;
-    case POOCH_L_AVGPOOL: return 4.0 * ((double)c->g.io.batch * T.hin * T.win * T.cin + e);
+    case POOCH_L_AVGPOOL: return 4.0 * ((double)c->g.io.batch * std::max(T.din, 1) * T.hin * T.win * T.cin + e);
     case POOCH_L_LRN: return 12.0 * e;          // read x, gy; write gx
     default: return 0;
   }
@@ -554,9 +558,11 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
       if (three) {
         R.geom.D = T.din;
         R.geom.Do = T.dout;
+        R.geom.stride_d = T.stride_d;
       }
+      R.geom.groups = T.groups;
       if (T.in1 >= 0) R.geom.C1 = g.t[T.in0].cout;
-      const int64_t wn = (int64_t)T.cout * R.geom.T() * T.k * T.k * T.cin;
+      const int64_t wn = (int64_t)T.cout * R.geom.T() * T.k * T.k * (T.cin / T.groups);
       if (!conv_shape_ok(R.geom)) {
         delete c;
         return fail(POOCH_EUSAGE, "task %d: unsupported conv shape (3D / two-source convs need 32-channel multiples)", t);
@@ -1602,7 +1608,7 @@ static pooch_status enqueue_update(pooch_ctx* c, float lr, bool timing) {
 static pooch_status enqueue_transposes(pooch_ctx* c) {
   for (int t = 0; t < c->g.n(); ++t) {
     const TaskRt& R = c->rt[t];
-    if (!R.is_conv) continue;
+    if (!R.is_conv || R.geom.groups > 1) continue;   // grouped: dgrad reads w itself
     const ConvGeom& G = R.geom;
     POOCH_CHECK(transpose_krsc(pw(c, R.w), fptr(c, c->off_wt) + R.wt_off, G.K, G.T() * G.R * G.S, G.C, c->s[0]));
   }

@@ -16,10 +16,10 @@ namespace {
 struct Builder {
   std::vector<pooch_layer_desc> out;
   int add(int kind, int in0, int in1, int cin, int cout, int h, int w, int k, int s, int p, const std::string& nm,
-          int dout = 0) {
+          int dout = 0, int groups = 0, int stride_d = 0) {
     pooch_layer_desc d{};
     d.kind = kind; d.in0 = in0; d.in1 = in1; d.cin = cin; d.cout = cout; d.hout = h; d.wout = w;
-    d.k = k; d.stride = s; d.pad = p; d.dout = dout;
+    d.k = k; d.stride = s; d.pad = p; d.dout = dout; d.groups = groups; d.stride_d = stride_d;
     std::snprintf(d.name, sizeof(d.name), "%s", nm.c_str());
     out.push_back(d);
     return (int)out.size() - 1;
@@ -128,6 +128,47 @@ void unet3d(Builder& b, int e, int classes, int w) {
   b.add(POOCH_L_HEAD_CE, src, -1, c, classes, e, e, 1, 1, 0, "head", e);
 }
 
+// ResNeXt-101 (3D) (oracle nets.resnext3d, same tasks): conv 7^3 stride
+// (1, 2, 2) pad 3 -> BN-ReLU -> max-pool 3^3 / 2 pad 1; [3, 4, 23, 3] bottlenecks of widths 128 /
+// 256 / 512 / 1024 with a grouped (32) 3^3 conv, 2x expansion, projection shortcut in each stage's
+// first block; global average pool; FC. Input [1, D, H, W, 3 -> 32 channels].
+void resnext3d(Builder& b, int d, int hw, int classes, int depth) {
+  const int n101[4] = {3, 4, 23, 3}, n50[4] = {3, 4, 6, 3};
+  const int* nb = depth == 50 ? n50 : n101;
+  const int mids[4] = {128, 256, 512, 1024};
+  int e = d, h = co(hw, 7, 2, 3);
+  int c = b.add(POOCH_L_CONV, -1, -1, 32, 64, h, h, 7, 2, 3, "conv1", e, 0, 1);
+  int x = b.add(POOCH_L_BNRELU, c, -1, 64, 64, h, h, 0, 1, 0, "bn1", e);
+  e = co(e, 3, 2, 1);
+  h = co(h, 3, 2, 1);
+  x = b.add(POOCH_L_MAXPOOL, x, -1, 64, 64, h, h, 3, 2, 1, "maxpool", e);
+  int cin = 64;
+  for (int si = 0; si < 4; ++si) {
+    const int mid = mids[si], out = 2 * mid;
+    for (int bi = 0; bi < nb[si]; ++bi) {
+      const int s = (bi == 0 && si > 0) ? 2 : 1;
+      const std::string pre = "layer" + std::to_string(si + 1) + "." + std::to_string(bi);
+      int c1 = b.add(POOCH_L_CONV, x, -1, cin, mid, h, h, 1, 1, 0, pre + ".conv1", e);
+      int y1 = b.add(POOCH_L_BNRELU, c1, -1, mid, mid, h, h, 0, 1, 0, pre + ".bn1", e);
+      const int e2 = co(e, 3, s, 1), h2 = co(h, 3, s, 1);
+      int c2 = b.add(POOCH_L_CONV, y1, -1, mid, mid, h2, h2, 3, s, 1, pre + ".conv2", e2, 32);
+      int y2 = b.add(POOCH_L_BNRELU, c2, -1, mid, mid, h2, h2, 0, 1, 0, pre + ".bn2", e2);
+      int c3 = b.add(POOCH_L_CONV, y2, -1, mid, out, h2, h2, 1, 1, 0, pre + ".conv3", e2);
+      if (bi == 0) {
+        int p = b.add(POOCH_L_CONV, x, -1, cin, out, h2, h2, 1, s, 0, pre + ".downsample", e2);
+        x = b.add(POOCH_L_TAIL_PROJ, c3, p, out, out, h2, h2, 0, 1, 0, pre + ".tail", e2);
+      } else {
+        x = b.add(POOCH_L_TAIL_ID, c3, x, out, out, h2, h2, 0, 1, 0, pre + ".tail", e2);
+      }
+      e = e2;
+      h = h2;
+      cin = out;
+    }
+  }
+  int a = b.add(POOCH_L_AVGPOOL, x, -1, cin, cin, 1, 1, 0, 1, 0, "avgpool", 1);
+  b.add(POOCH_L_FC_CE, a, -1, cin, classes, 1, 1, 0, 1, 0, "fc", 1);
+}
+
 // SURVEY 8(f) f2 (oracle: nets.fuse_bnrelu, same rule): merge every BN-ReLU whose only consumer
 // is a single-input 2D conv with cin % 32 == 0 and stride <= 2 into that conv.
 void fuse_bnrelu(std::vector<pooch_layer_desc>& L) {
@@ -186,6 +227,13 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
     t.kind = d.kind; t.in0 = d.in0; t.in1 = d.in1; t.cin = d.cin; t.cout = d.cout; t.hout = d.hout;
     t.wout = d.wout; t.k = d.k; t.stride = d.stride; t.pad = d.pad;
     t.dout = three ? d.dout : 0;
+    t.groups = d.groups > 1 ? d.groups : 1;
+    t.stride_d = three ? d.stride_d : 0;
+    if ((t.groups > 1 && (d.kind != POOCH_L_CONV || !three || d.cin != d.cout || d.cin % t.groups)) ||
+        (t.stride_d > 0 && d.kind != POOCH_L_CONV)) {
+      err = "task " + std::to_string(i) + ": groups / depth stride are for 3D convs (grouped: cin == cout)";
+      return false;
+    }
     t.name = std::string(d.name, strnlen(d.name, sizeof(d.name)));
     if (d.in0 >= i || d.in1 >= i || d.in0 < -1 || d.in1 < -1) {
       err = "task " + std::to_string(i) + ": inputs must be topological";
@@ -258,14 +306,16 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
     }
     if (d.kind == POOCH_L_CONV || d.kind == POOCH_L_MAXPOOL || d.kind == POOCH_L_BNRELU_CONV ||
         d.kind == POOCH_L_CONV_RELU) {
+      const int sd = t.stride_d > 0 ? t.stride_d : d.stride;
       if (co(t.hin, d.k, d.stride, d.pad) != d.hout || co(t.win, d.k, d.stride, d.pad) != d.wout ||
-          (three && co(t.din, d.k, d.stride, d.pad) != t.dout)) {
+          (three && co(t.din, d.k, sd, d.pad) != t.dout)) {
         err = "task " + std::to_string(i) + ": output shape does not match geometry";
         return false;
       }
     }
-    if (three && d.kind == POOCH_L_MAXPOOL && (d.k != 2 || d.stride != 2 || d.pad != 0)) {
-      err = "task " + std::to_string(i) + ": 3D max-pool is k2 s2 p0";
+    if (three && d.kind == POOCH_L_MAXPOOL &&
+        !((d.k == 2 && d.stride == 2 && d.pad == 0) || (d.k == 3 && d.stride == 2 && d.pad == 1))) {
+      err = "task " + std::to_string(i) + ": 3D max-pool is k2 s2 p0 (U-Net) or k3 s2 p1 (ResNeXt)";
       return false;
     }
     if (d.kind == POOCH_L_UPCONV && (!three || d.k != 2 || d.stride != 2 || d.hout != 2 * t.hin ||
@@ -277,8 +327,8 @@ bool build_graph(const pooch_layer_desc* layers, int n, const pooch_io_desc& io,
       err = "task " + std::to_string(i) + ": the head keeps the grid";
       return false;
     }
-    if (d.kind == POOCH_L_AVGPOOL && three) {
-      err = "task " + std::to_string(i) + ": 3D networks have no global average pool";
+    if ((d.kind == POOCH_L_AVGPOOL || d.kind == POOCH_L_FC_CE) && three && (d.dout != 1 || d.hout != 1 || d.wout != 1)) {
+      err = "task " + std::to_string(i) + ": a 3D global average pool / FC outputs one voxel (dout = hout = wout = 1)";
       return false;
     }
     if ((d.kind == POOCH_L_FC_CE || d.kind == POOCH_L_HEAD_CE) && i != n - 1) {
@@ -397,6 +447,9 @@ extern "C" pooch_status pooch_build_net(int32_t which, int32_t in_hw, int32_t cl
   } else if (which == 4) {
     if (in_hw < 67) return fail(POOCH_EUSAGE, "AlexNet input too small (>= 67)");
     alexnet(b, in_hw, classes);
+  } else if (which == 5 || which == 6) {
+    if (in_hw < 32 || width < 8) return fail(POOCH_EUSAGE, "ResNeXt (3D) input too small (H = W >= 32, D >= 8)");
+    resnext3d(b, width, in_hw, classes, which == 5 ? 101 : 50);
   } else {
     return fail(POOCH_EUSAGE, "unknown network %d", which);
   }

@@ -15,6 +15,8 @@ struct Task {
   int cin, cout, hout, wout, k, stride, pad;
   int hin, win;        // derived: input spatial dims (conv / pool)
   int din, dout;       // 3D networks: input / output depth (0 in 2D networks)
+  int groups = 1;      // grouped conv (ResNeXt-101 (3D)); 1 = dense
+  int stride_d = 0;    // 3D conv: depth stride (0 = stride)
   std::string name;
   std::vector<int> inputs;  // map inputs (ids >= 0)
   std::vector<int> needs;   // maps bwd(task) reads

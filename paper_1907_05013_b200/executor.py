@@ -14,7 +14,7 @@ import numpy as np
 from ._lib import P, IODesc, LayerDesc, PlanReport, ProfileT, SearchCfg, check, lib
 from .planning import STRATEGIES
 
-NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2, "unet3d": 3, "alexnet": 4}
+NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2, "unet3d": 3, "alexnet": 4, "resnext3d": 5, "resnext50_3d": 6}
 KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce", "upconv", "head_ce", "bnrelu_conv",
          "conv_relu", "lrn", "fc_relu_drop"]
 FAMILIES = ["conv_fwd", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd", "pool", "fc_ce", "sgd",
@@ -95,6 +95,10 @@ class Context:
             classes = classes or 2
             return cls(build_net(name, in_hw, classes, width, fuse), batch, 32, in_hw, in_hw, classes, device,
                        in_d=in_hw)
+        if name in ("resnext3d", "resnext50_3d"):   # in_hw = H = W, width = D; input channels 3 -> 32
+            classes = classes or 400
+            return cls(build_net(name, in_hw, classes, width, fuse), batch, 32, in_hw, in_hw, classes, device,
+                       in_d=width)
         in_hw = in_hw or {"tiny": 32, "alexnet": 227}.get(name, 224)
         classes = classes or (10 if name == "tiny" else 1000)
         return cls(build_net(name, in_hw, classes, width, fuse), batch, 4, in_hw, in_hw, classes, device)

@@ -1,0 +1,266 @@
+"""GPU parity of the ResNeXt-101 (3D) path against the fp64
+oracle, through the C ABI:
+
+* grouped conv3d forward (+ BN partial sums) / dgrad (written and accumulated) / wgrad for every
+  group width the network has (4, 8, 16, 32 channels per group; 32 groups), stride 1 and 2,
+  ragged extents -- element-wise rel-L2 against oracle layers.gconv3d_* (FP32 on the CUDA cores,
+  so the tolerance is fp32 accumulation's, not 3xTF32's);
+* the (1, 2, 2)-strided 7^3 stem and the strided 1^3 projection on the tensor-core kernels;
+* the padded 3^3 / 2 max-pool (values exact, gradient routing exact);
+* one training step of ResNeXt-50 (3D) (the same blocks as 101, [3, 4, 6, 3]) at 32 x 64 x 64
+  against oracle nets.resnext3d (loss, per-tensor gate), and PoocH's plan below the in-core
+  peak bit-exact against the in-core run.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synthdata  # noqa: E402
+from oracle import layers as L  # noqa: E402
+from oracle import nets  # noqa: E402
+from netutil import global_rel, load_params, pad_input, read_params, rel  # noqa: E402
+from gates import TOL, gate  # noqa: E402
+
+TOL_FP32 = 2e-6      # fp32 FMA chains of <= 864 terms against fp64
+TOL_X3 = 2e-5
+
+
+def _lib():
+    from paper_1907_05013_b200 import _lib
+    return _lib
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def ndhwc(a):
+    return np.ascontiguousarray(np.moveaxis(a, 1, -1))
+
+
+def ncdhw(a):
+    return np.moveaxis(a, -1, 1)
+
+
+def wkrsc(w):
+    return np.ascontiguousarray(np.moveaxis(w, 1, -1))
+
+
+GCASES = [
+    # D, H, W, C, groups, k, stride   (ResNeXt-101 (3D) group widths 4 / 8 / 16 / 32)
+    (4, 6, 5, 128, 32, 3, 1),
+    (5, 7, 6, 128, 32, 3, 2),
+    (3, 5, 9, 256, 32, 3, 2),
+    (4, 4, 4, 512, 32, 3, 1),
+    (3, 4, 5, 1024, 32, 3, 2),
+    (2, 3, 3, 1024, 32, 3, 1),
+    (6, 6, 6, 64, 16, 3, 1),      # 4 per group, 16 groups
+    (3, 4, 4, 64, 4, 1, 1),       # 1^3 grouped (16 per group)
+]
+
+
+@pytest.mark.parametrize("case", GCASES)
+def test_grouped_conv3d_fwd_dgrad_wgrad(case):
+    lib = _lib()
+    D, H, W, Cc, G, k, s = case
+    g = synthdata.rng(sum(case))
+    x = g.standard_normal((1, Cc, D, H, W)).astype(np.float32).astype(np.float64)
+    w = (g.standard_normal((Cc, Cc // G, k, k, k)) / np.sqrt(Cc // G * k ** 3)).astype(np.float32).astype(np.float64)
+    p = k // 2
+    y_ref = L.gconv3d_fwd(x, w, s, p, G)
+    d = lib.ConvDesc(1, H, W, Cc, Cc, k, k, s, p, 1, D, 0, G, 0)
+    dx = torch.from_numpy(ndhwc(x).astype(np.float32)).cuda()
+    dw = torch.from_numpy(wkrsc(w).astype(np.float32)).cuda()
+    dy = torch.full((1,) + y_ref.shape[2:] + (Cc,), float("nan"), device="cuda")
+    mt = lib.lib.pooch_op_conv_stat_tiles(C.byref(d))
+    s1 = torch.full((mt, Cc), float("nan"), device="cuda")
+    s2 = torch.full((mt, Cc), float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_fwd(C.byref(d), ptr(dx), ptr(dw), ptr(dy), ptr(s1), ptr(s2), None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(dy.cpu().numpy()), y_ref) < TOL_FP32
+    flat = ndhwc(y_ref).reshape(-1, Cc)
+    assert rel(s1.cpu().numpy().astype(np.float64).sum(0), flat.sum(0)) < 1e-5
+    assert rel(s2.cpu().numpy().astype(np.float64).sum(0), (flat ** 2).sum(0)) < 1e-5
+    # dgrad: written, then accumulated onto a known tensor
+    gy = synthdata.rng(3).standard_normal(y_ref.shape).astype(np.float32).astype(np.float64)
+    dgy = torch.from_numpy(ndhwc(gy).astype(np.float32)).cuda()
+    dx_ref = L.gconv3d_dgrad(gy, w, x.shape, s, p, G)
+    gx = torch.full(dx.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_dgrad(C.byref(d), ptr(dgy), ptr(dw), ptr(gx), 0, None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(gx.cpu().numpy()), dx_ref) < TOL_FP32
+    base = synthdata.rng(4).standard_normal(dx.shape).astype(np.float32)
+    gx2 = torch.from_numpy(base).cuda()
+    lib.check(lib.lib.pooch_op_conv_dgrad(C.byref(d), ptr(dgy), ptr(dw), ptr(gx2), 1, None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(gx2.cpu().numpy()), dx_ref + ncdhw(base.astype(np.float64))) < TOL_FP32
+    # wgrad
+    wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(wsb // 4, 1), device="cuda")
+    gw = torch.full(dw.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(dx), ptr(dgy), ptr(gw), ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    assert rel(np.moveaxis(gw.cpu().numpy(), -1, 1), L.gconv3d_wgrad(x, gy, w.shape, s, p, G)) < TOL_FP32
+
+
+def test_grouped_conv3d_rejects_unsupported():
+    lib = _lib()
+    for d in (lib.ConvDesc(1, 4, 4, 96, 96, 3, 3, 1, 1, 1, 4, 0, 32, 0),     # 3 channels per group
+              lib.ConvDesc(1, 4, 4, 128, 256, 3, 3, 1, 1, 1, 4, 0, 32, 0),   # C != K
+              lib.ConvDesc(2, 4, 4, 128, 128, 3, 3, 1, 1, 1, 0, 0, 32, 0)):  # 2D
+        t = torch.zeros(1 << 16, device="cuda")
+        assert lib.lib.pooch_op_conv_fwd(C.byref(d), ptr(t), ptr(t), ptr(t), None, None, None) != 0
+
+
+@pytest.mark.parametrize("case", [
+    # D, H, W, C, K, k, stride, stride_d, pad: the stem (7^3, (1, 2, 2), pad 3, 3 -> 32 channels)
+    # and the strided 1^3 projection
+    (6, 12, 10, 32, 64, 7, 2, 1, 3),
+    (5, 7, 6, 64, 128, 1, 2, 0, 0),
+    (4, 6, 6, 256, 512, 1, 2, 0, 0),
+])
+def test_stem_and_projection_conv3d(case):
+    lib = _lib()
+    D, H, W, Cc, K, k, s, sd, p = case
+    g = synthdata.rng(sum(case) + 7)
+    x = g.standard_normal((1, Cc, D, H, W)).astype(np.float32).astype(np.float64)
+    if Cc == 32:
+        x[:, 3:] = 0.0          # the stem's input: 3 channels padded to 32
+    w = (g.standard_normal((K, Cc, k, k, k)) / np.sqrt(Cc * k ** 3)).astype(np.float32).astype(np.float64)
+    s3 = (sd or s, s, s)
+    y_ref = L.gconv3d_fwd(x, w, s3, p, 1)
+    d = lib.ConvDesc(1, H, W, Cc, K, k, k, s, p, 1, D, 0, 0, sd)
+    dx = torch.from_numpy(ndhwc(x).astype(np.float32)).cuda()
+    dw = torch.from_numpy(wkrsc(w).astype(np.float32)).cuda()
+    dy = torch.full((1,) + y_ref.shape[2:] + (K,), float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_fwd(C.byref(d), ptr(dx), ptr(dw), ptr(dy), None, None, None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(dy.cpu().numpy()), y_ref) < TOL_X3
+    gy = synthdata.rng(5).standard_normal(y_ref.shape).astype(np.float32).astype(np.float64)
+    dgy = torch.from_numpy(ndhwc(gy).astype(np.float32)).cuda()
+    wt = torch.from_numpy(np.ascontiguousarray(np.transpose(wkrsc(w), (4, 1, 2, 3, 0))).astype(np.float32)).cuda()
+    gx = torch.full(dx.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_dgrad(C.byref(d), ptr(dgy), ptr(wt), ptr(gx), 0, None))
+    torch.cuda.synchronize()
+    assert rel(ncdhw(gx.cpu().numpy()), L.gconv3d_dgrad(gy, w, x.shape, s3, p, 1)) < TOL_X3
+    wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
+    ws = torch.empty(max(wsb // 4, 1), device="cuda")
+    gw = torch.full(dw.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(dx), ptr(dgy), ptr(gw), ptr(ws), wsb, None))
+    torch.cuda.synchronize()
+    assert rel(np.moveaxis(gw.cpu().numpy(), -1, 1), L.gconv3d_wgrad(x, gy, w.shape, s3, p, 1)) < TOL_X3
+
+
+@pytest.mark.parametrize("shape", [(5, 7, 6, 64), (8, 8, 8, 32), (3, 4, 9, 16)])
+def test_maxpool3d_k3s2p1(shape):
+    lib = _lib()
+    D, H, W, Cc = shape
+    g = synthdata.rng(D * H * W + Cc)
+    x = g.standard_normal((1, Cc, D, H, W)).astype(np.float32).astype(np.float64)
+    y_ref = L.maxpool3d_fwd(x, 3, 2, 1)
+    dx = torch.from_numpy(ndhwc(x).astype(np.float32)).cuda()
+    dy = torch.full((1,) + y_ref.shape[2:] + (Cc,), float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_maxpool3d_fwd_k(ptr(dx), ptr(dy), D, H, W, Cc, 3, 2, 1, None))
+    torch.cuda.synchronize()
+    assert np.array_equal(ncdhw(dy.cpu().numpy()), y_ref.astype(np.float32))
+    gy = synthdata.rng(9).standard_normal(y_ref.shape).astype(np.float32).astype(np.float64)
+    dgy = torch.from_numpy(ndhwc(gy).astype(np.float32)).cuda()
+    arg = torch.empty(int(np.prod(y_ref.shape)), dtype=torch.uint8, device="cuda")
+    gx = torch.full(dx.shape, float("nan"), device="cuda")
+    lib.check(lib.lib.pooch_op_maxpool3d_bwd_k(ptr(dx), ptr(dgy), ptr(gx), ptr(arg), D, H, W, Cc, 3, 2, 1, 0, None))
+    torch.cuda.synchronize()
+    # fp32 sums of at most 8 routed gradients (overlapping windows) in output order
+    assert rel(ncdhw(gx.cpu().numpy()), L.maxpool3d_bwd(gy, x, 3, 2, 1)) < 1e-7
+
+
+DHW = (32, 64, 64)
+CLASSES = 10
+
+
+def _ctx(dev_bytes, host_bytes):
+    from paper_1907_05013_b200.executor import Context
+    ctx = Context.builtin("resnext50_3d", 1, in_hw=DHW[1], classes=CLASSES, width=DHW[0])
+    dev = torch.empty(dev_bytes, dtype=torch.uint8, device="cuda")
+    host = torch.empty(host_bytes, dtype=torch.uint8, pin_memory=True)
+    ctx.set_budget(dev, dev_bytes, host, host_bytes)
+    ss = [torch.cuda.Stream() for _ in range(3)]
+    ctx.set_streams(*ss)
+    ctx._torch = (dev, host, ss)
+    return ctx
+
+
+def _put(ctx, x, labels):
+    dev = ctx._torch[0]
+    xp, lp = ctx.input_slot()
+    base = dev.data_ptr()
+    xt = torch.from_numpy(pad_input(x, 32)).reshape(-1).cuda()
+    lt = torch.from_numpy(labels.astype(np.int32).reshape(-1)).cuda()
+    dev[xp - base: xp - base + xt.numel() * 4].view(torch.float32).copy_(xt)
+    dev[lp - base: lp - base + lt.numel() * 4].view(torch.int32).copy_(lt)
+    torch.cuda.synchronize()
+
+
+@pytest.fixture(scope="module")
+def rx():
+    net = nets.resnext3d(DHW, classes=CLASSES, depth=50)
+    params = nets.init_params(net, seed=31, bn_random=True)
+    g = synthdata.rng(32)
+    x = g.standard_normal((1,) + DHW + (3,)).astype(np.float32)
+    t = np.array([3])
+    loss, grads, _ = nets.forward_backward(net, params, x, t)
+    _, grads32, _ = nets.forward_backward(net, params, x, t, precision="fp32")
+    return dict(net=net, params=params, x=x, t=t, loss=loss, grads=grads, grads32=grads32)
+
+
+def _step(ctx, r, strategy):
+    load_params(ctx, r["params"])
+    _put(ctx, r["x"], r["t"])
+    cls, rep = ctx.plan(strategy)
+    loss = ctx.train_step(0.05)
+    torch.cuda.synchronize()
+    return loss, cls, rep
+
+
+def test_resnext3d_graph_matches_oracle(rx):
+    from paper_1907_05013_b200.executor import Context
+    ctx = _ctx(2 << 30, 64 << 20)
+    assert ctx.n == len(rx["net"].tasks)
+    names = [n for n, _ in ctx.params()]
+    shapes = nets.param_shapes(rx["net"])
+    assert set(names) == set(shapes)
+    ctx.close()
+
+
+def test_resnext3d_step_matches_oracle(rx):
+    ctx = _ctx(2 << 30, 64 << 20)
+    ctx.profile(1)
+    loss, _, _ = _step(ctx, rx, "incore")
+    assert abs(loss - rx["loss"]) < 1e-3 * max(1.0, abs(rx["loss"]))
+    g = read_params(ctx, rx["params"], 1)
+    assert global_rel(g, rx["grads"]) < TOL
+    gate(g, rx["grads"], rx["grads32"], "ResNeXt-50 (3D) 32x64x64")
+    ctx.close()
+
+
+def test_resnext3d_plan_bit_exact_below_incore(rx):
+    ctx = _ctx(2 << 30, 256 << 20)
+    ctx.profile(1)
+    ref_loss, _, rep_in = _step(ctx, rx, "incore")
+    ref = [ctx.get_param(i, 1).view(np.uint32).copy() for i in range(len(ctx.params()))]
+    half = ctx.resident_bytes() + rep_in["peak_bytes"] // 2
+    half = (half + 255) // 256 * 256
+    dev, host, ss = ctx._torch
+    ctx.set_budget(dev, half, host, host.numel())
+    ctx.profile(1)
+    loss, cls, rep = _step(ctx, rx, "pooch")
+    assert rep["feasible"] and rep["arena_bytes"] <= half
+    assert cls != [0] * ctx.n
+    assert np.float32(loss).view(np.uint32) == np.float32(ref_loss).view(np.uint32)
+    got = [ctx.get_param(i, 1).view(np.uint32).copy() for i in range(len(ctx.params()))]
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
+    ctx.close()

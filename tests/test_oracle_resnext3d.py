@@ -182,3 +182,23 @@ def test_resnext101_3d_census():
     shp = {t.name: t.out_chw for t in net.tasks}
     assert shp["conv1"] == (64, 16, 56, 56) and shp["maxpool"] == (64, 8, 28, 28)
     assert shp["layer1.2.tail"] == (256, 8, 28, 28) and shp["layer4.2.tail"] == (2048, 1, 4, 4)
+
+
+@pytest.mark.parametrize("which,depth,dhw", [("resnext3d", 101, (16, 112, 112)), ("resnext50_3d", 50, (32, 64, 64))])
+def test_builtin_resnext3d_graph_equals_oracle(which, depth, dhw):
+    """pooch_build_net(5 / 6) (host only) builds the oracle's task list: kinds, inputs, output
+    shapes (C, D, H, W), kernel / stride / depth stride / padding and groups, task by task."""
+    from paper_1907_05013_b200.executor import KINDS, build_net
+    layers = build_net(which, dhw[1], 400, dhw[0])
+    net = nets.resnext3d(dhw, classes=400, depth=depth)
+    assert len(layers) == len(net.tasks)
+    for d, t in zip(layers, net.tasks):
+        assert KINDS[d.kind] == t.kind, t.name
+        assert d.name.decode() == t.name
+        assert [i for i in (d.in0, d.in1) if i >= 0] == [i for i in t.inputs if i >= 0], t.name
+        shape = (d.cout, d.dout, d.hout, d.wout) if t.kind not in ("avgpool", "fc_ce") else (d.cout, 1, 1)
+        assert shape == tuple(t.out_chw), t.name
+        if t.kind in ("conv", "maxpool"):
+            assert (d.k, d.stride, d.pad) == (t.k, t.stride, t.pad), t.name
+            assert (d.stride_d or d.stride) == t.stride3[0], t.name
+            assert max(d.groups, 1) == t.groups, t.name
