@@ -126,7 +126,7 @@ typedef struct {
  * `width` -> level widths w, 2w, 4w, 4w, input channels padded 1 -> 32), 4 = AlexNet (the
  * paper's second workload: single-tower, in_hw 227, dropout 0.5; width unused;
  * 13 maps, 62,378,344 parameters), 5 = ResNeXt-101 (3D) (the paper's third workload, SURVEY 8(f)
- * f4: input [1, D = width, H = W = in_hw, 3 -> 32 channels], 207 maps, grouped 3^3 convs), 6 = its
+ * f4: input [1, D = width, H = W = in_hw, 3 -> 4 channels], 207 maps, grouped 3^3 convs), 6 = its
  * depth-50 variant ([3, 4, 6, 3] blocks; tests). which |
  * POOCH_NET_FUSE_BNRELU merges every BN-ReLU whose only consumer is a single-input 2D conv with
  * cin % 32 == 0 and stride <= 2 into that conv (POOCH_L_BNRELU_CONV; same function and

@@ -40,6 +40,12 @@ struct TaskRt {
   int64_t rows = 0;     // N*H*W of the output
   int cpad = 0;         // FC: padded classes
   double flops = 0;     // per pass (fwd == dgrad == wgrad for convs)
+  // 3D stem with depth stride 1 reading the network input (ResNeXt-101 (3D)'s 7^3 conv): run as a
+  // 2D conv over the Do depth slices of the input's depth-im2col X'[od][h][w][u*C + c] =
+  // x[od+u-p][h][w][c] (k*C <= 32 channels, padded to 32), geom holds that 2D geometry, the wt
+  // region holds the weight re-laid [K][v][t][u*C + c]; fold_c = C, fold_k = k
+  bool fold = false;
+  int fold_c = 0, fold_k = 0;
 };
 
 // One host-enqueued operation of the compiled schedule.
@@ -76,7 +82,8 @@ struct pooch_ctx {
   std::vector<pooch::TaskRt> rt;
   size_t off_w = 0, off_g = 0, off_v = 0, off_wt = 0, off_stats = 0, off_tile = 0, off_fin = 0, off_bnws = 0,
          off_wgws = 0, off_mparg = 0, off_x = 0, off_lab = 0, off_lossrows = 0, off_loss = 0, off_dz = 0,
-         off_cews = 0, off_rng = 0;  // off_cews: CE two-stage reduction scratch; off_rng: dropout {seed, step}
+         off_cews = 0, off_rng = 0, off_xs = 0, off_w2g = 0;  // off_cews: CE two-stage reduction scratch; off_rng: dropout {seed, step}
+  size_t xs_bytes = 0, w2g_bytes = 0;  // folded stem: depth-im2col input X', wgrad scratch dW'
   size_t wt_floats = 0, stats_floats = 0, tile_bytes = 0, fin_bytes = 0, bnws_bytes = 0, wgws_bytes = 0,
          mparg_bytes = 0;
   size_t resident_end = 0;

@@ -981,6 +981,64 @@ pooch_status sgd_momentum(float* w, float* v, const float* g, int64_t n, float l
   return POOCH_OK;
 }
 
+namespace {
+// one thread per (output slice voxel, float4 of the 32 channels); C % 4 == 0
+__global__ void depth_im2col_kernel(const float* __restrict__ x, float* __restrict__ xs, int D, int H, int W, int C4,
+                                    int k, int p, int Do) {
+  const int64_t total = (int64_t)Do * H * W * 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j4 = (int)(i & 7);
+    const int64_t vox = i >> 3;
+    const int64_t hw = vox % ((int64_t)H * W);
+    const int od = (int)(vox / ((int64_t)H * W));
+    const int u = j4 / C4, c4 = j4 % C4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int d = od + u - p;
+    if (u < k && d >= 0 && d < D) v = ld4(x + (((int64_t)d * H * W + hw) * C4 + c4) * 4);
+    st4(xs + 4 * i, v);
+  }
+}
+
+__global__ void fold_weight_kernel(float* w, float* w2, int K, int k, int C, int back) {
+  const int64_t total = (int64_t)K * k * k * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % 32);
+    const int64_t r = i / 32;                 // (o, v, t)
+    const int t = (int)(r % k), v = (int)((r / k) % k), o = (int)(r / ((int64_t)k * k));
+    const int u = j / C, c = j % C;
+    if (back) {
+      if (u < k) w[((((int64_t)o * k + u) * k + v) * k + t) * C + c] = w2[i];
+    } else {
+      w2[i] = u < k ? w[((((int64_t)o * k + u) * k + v) * k + t) * C + c] : 0.f;
+    }
+  }
+}
+}  // namespace
+
+pooch_status depth_im2col(const float* x, float* xs, int D, int H, int W, int C, int k, int p, int Do,
+                          cudaStream_t st) {
+  if (C % 4 || k * C > 32) return fail(POOCH_EUSAGE, "depth_im2col: k * C must be <= 32, C %% 4 == 0");
+  const int64_t total = (int64_t)Do * H * W * 8;
+  count_launch();
+  depth_im2col_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, xs, D, H, W, C / 4, k, p, Do);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status fold_weight(const float* w, float* w2, int K, int k, int C, cudaStream_t st) {
+  count_launch();
+  fold_weight_kernel<<<grid_for((int64_t)K * k * k * 32, 256), 256, 0, st>>>(const_cast<float*>(w), w2, K, k, C, 0);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status unfold_weight(const float* w2, float* w, int K, int k, int C, cudaStream_t st) {
+  count_launch();
+  fold_weight_kernel<<<grid_for((int64_t)K * k * k * 32, 256), 256, 0, st>>>(w, const_cast<float*>(w2), K, k, C, 1);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
 pooch_status transpose_krsc(const float* w, float* wt, int K, int RS, int C, cudaStream_t st) {
   dim3 g((C + 31) / 32, (K + 31) / 32, RS);
   count_launch();

@@ -75,6 +75,13 @@ pooch_status sgd_momentum(float* w, float* v, const float* g, int64_t n, float l
                           cudaStream_t st);
 
 // ---- weight transpose for dgrad: wt[c][r][s][k] = w[k][r][s][c]
+// Depth-folded 3D stem (ResNeXt-101 (3D), executor TaskRt::fold): xs[od][h][w][j] =
+// x[od + u - p][h][w][c] for j = u*C + c < k*C (zero outside the volume and for j >= k*C), 32
+// channels; the weight to / from the 2D layout W2[o][v][t][u*C + c] <-> W[o][u][v][t][c].
+pooch_status depth_im2col(const float* x, float* xs, int D, int H, int W, int C, int k, int p, int Do,
+                          cudaStream_t st);
+pooch_status fold_weight(const float* w, float* w2, int K, int k, int C, cudaStream_t st);
+pooch_status unfold_weight(const float* w2, float* w, int K, int k, int C, cudaStream_t st);
 pooch_status transpose_krsc(const float* w, float* wt, int K, int RS, int C, cudaStream_t st);
 
 }  // namespace pooch

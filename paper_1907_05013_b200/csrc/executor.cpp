@@ -121,6 +121,24 @@ pooch_status run_fwd(pooch_ctx* c, int t, const Ptrs& p, bool with_stats) {
   const ConvGeom RG = geom_of(c, t);
   cudaStream_t st = c->s[0];
   const int B = c->g.io.batch;
+  if (R.fold) {   // depth-folded stem: X' from the network input, then the 2D conv
+    float* xs = fptr(c, c->off_xs);
+    POOCH_CHECK(depth_im2col(fptr(c, c->off_x), xs, T.din, T.hin, T.win, R.fold_c, R.fold_k, T.pad, T.dout, st));
+    float* ts = nullptr;
+    float* tq = nullptr;
+    if (with_stats && R.has_stats) {
+      ts = reinterpret_cast<float*>(c->dev + c->off_tile);
+      tq = ts + (size_t)conv_mtiles(R.geom) * R.geom.K;
+    }
+    POOCH_CHECK(launch_conv_fwd(RG, xs, fptr(c, c->off_wt) + R.wt_off, p.out, ts, tq, nullptr, st));
+    if (ts) {
+      float* sp = fptr(c, c->off_stats) + R.stat_off;
+      const int C = R.geom.K;
+      POOCH_CHECK(bn_finalize(ts, tq, conv_mtiles(R.geom), C, R.rows, pw(c, R.bn_gamma), pw(c, R.bn_beta), sp,
+                              sp + C, sp + 2 * C, sp + 3 * C, reinterpret_cast<double*>(c->dev + c->off_fin), st));
+    }
+    return POOCH_OK;
+  }
   switch (T.kind) {
     case POOCH_L_CONV:
     case POOCH_L_BNRELU_CONV: {
@@ -207,6 +225,14 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
   const ConvGeom RG = geom_of(c, t);
   cudaStream_t st = c->s[0];
   const int B = c->g.io.batch;
+  if (R.fold) {   // depth-folded stem: wgrad of the 2D conv on X' (written by the forward), re-laid
+    const ConvGeom& G = RG;
+    if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, 4.0 * ((double)c->xs_bytes / 4 + R.rows * G.K));
+    float* w2g = fptr(c, c->off_w2g);
+    POOCH_CHECK(launch_conv_wgrad(G, fptr(c, c->off_xs), p.gy, w2g, reinterpret_cast<float*>(c->dev + c->off_wgws),
+                                  c->wgws_bytes, st));
+    return unfold_weight(w2g, pg(c, R.w), G.K, R.fold_k, R.fold_c, st);
+  }
   switch (T.kind) {
     case POOCH_L_CONV: {
       const ConvGeom& G = RG;
@@ -438,6 +464,8 @@ pooch_status layout_resident(pooch_ctx* c) {
   c->off_cews = take(ce_ws_bytes());
   c->off_dz = take(ce_rows * c->rt[n - 1].cpad * 4);
   c->off_rng = take(16);   // dropout generator {seed, step} (pooch_set_rng)
+  c->off_xs = take(c->xs_bytes);    // folded stem (TaskRt::fold): X' and the 2D weight gradient
+  c->off_w2g = take(c->w2g_bytes);
   c->resident_end = align_up(o, 1 << 20);
   return POOCH_OK;
 }
@@ -552,7 +580,28 @@ extern "C" pooch_status pooch_create(const pooch_layer_desc* layers, int32_t n_l
     TaskRt& R = c->rt[t];
     const bool three = T.dout > 0;
     R.rows = (int64_t)B * T.hout * T.wout * (three ? T.dout : 1);
-    if (T.kind == POOCH_L_CONV || T.kind == POOCH_L_BNRELU_CONV) {
+    const int fold_sd = T.stride_d > 0 ? T.stride_d : T.stride;
+    if (T.kind == POOCH_L_CONV && three && T.in0 < 0 && T.in1 < 0 && T.groups == 1 && fold_sd == 1 &&
+        T.cin % 4 == 0 && T.k * T.cin <= 32 && T.stride <= 2) {
+      // the depth-folded stem (TaskRt::fold): a 2D conv over the Do depth slices of X'
+      R.is_conv = true;
+      R.fold = true;
+      R.fold_c = T.cin;
+      R.fold_k = T.k;
+      R.geom = ConvGeom{T.dout, T.hin, T.win, 32, T.cout, T.k, T.k, T.stride, T.pad, T.hout, T.wout};
+      if (!conv_shape_ok(R.geom)) {
+        delete c;
+        return fail(POOCH_EUSAGE, "task %d: unsupported folded stem shape", t);
+      }
+      const int64_t wn = (int64_t)T.cout * T.k * T.k * T.k * T.cin;
+      R.w = param_add(c, T.name + ".w", t, wn);
+      R.wt_off = wt;
+      wt += (size_t)T.cout * T.k * T.k * 32;
+      R.flops = 2.0 * R.rows * wn;
+      wg = std::max(wg, conv_wgrad_ws_bytes(R.geom));
+      c->xs_bytes = (size_t)T.dout * T.hin * T.win * 32 * 4;
+      c->w2g_bytes = (size_t)T.cout * T.k * T.k * 32 * 4;
+    } else if (T.kind == POOCH_L_CONV || T.kind == POOCH_L_BNRELU_CONV) {
       R.is_conv = true;
       R.geom = ConvGeom{B, T.hin, T.win, T.cin, T.cout, T.k, T.k, T.stride, T.pad, T.hout, T.wout};
       if (three) {
@@ -1608,6 +1657,10 @@ static pooch_status enqueue_update(pooch_ctx* c, float lr, bool timing) {
 static pooch_status enqueue_transposes(pooch_ctx* c) {
   for (int t = 0; t < c->g.n(); ++t) {
     const TaskRt& R = c->rt[t];
+    if (R.fold) {   // the folded stem's 2D weight (it has no dgrad)
+      POOCH_CHECK(fold_weight(pw(c, R.w), fptr(c, c->off_wt) + R.wt_off, R.geom.K, R.fold_k, R.fold_c, c->s[0]));
+      continue;
+    }
     if (!R.is_conv || R.geom.groups > 1) continue;   // grouped: dgrad reads w itself
     const ConvGeom& G = R.geom;
     POOCH_CHECK(transpose_krsc(pw(c, R.w), fptr(c, c->off_wt) + R.wt_off, G.K, G.T() * G.R * G.S, G.C, c->s[0]));

@@ -131,13 +131,14 @@ void unet3d(Builder& b, int e, int classes, int w) {
 // ResNeXt-101 (3D) (oracle nets.resnext3d, same tasks): conv 7^3 stride
 // (1, 2, 2) pad 3 -> BN-ReLU -> max-pool 3^3 / 2 pad 1; [3, 4, 23, 3] bottlenecks of widths 128 /
 // 256 / 512 / 1024 with a grouped (32) 3^3 conv, 2x expansion, projection shortcut in each stage's
-// first block; global average pool; FC. Input [1, D, H, W, 3 -> 32 channels].
+// first block; global average pool; FC. Input [1, D, H, W, 3 -> 4 channels]; the stem runs
+// depth-folded (executor TaskRt::fold: 7 depth taps x 4 channels as 28 -> 32 channels of a 2D conv).
 void resnext3d(Builder& b, int d, int hw, int classes, int depth) {
   const int n101[4] = {3, 4, 23, 3}, n50[4] = {3, 4, 6, 3};
   const int* nb = depth == 50 ? n50 : n101;
   const int mids[4] = {128, 256, 512, 1024};
   int e = d, h = co(hw, 7, 2, 3);
-  int c = b.add(POOCH_L_CONV, -1, -1, 32, 64, h, h, 7, 2, 3, "conv1", e, 0, 1);
+  int c = b.add(POOCH_L_CONV, -1, -1, 4, 64, h, h, 7, 2, 3, "conv1", e, 0, 1);
   int x = b.add(POOCH_L_BNRELU, c, -1, 64, 64, h, h, 0, 1, 0, "bn1", e);
   e = co(e, 3, 2, 1);
   h = co(h, 3, 2, 1);

@@ -95,9 +95,9 @@ class Context:
             classes = classes or 2
             return cls(build_net(name, in_hw, classes, width, fuse), batch, 32, in_hw, in_hw, classes, device,
                        in_d=in_hw)
-        if name in ("resnext3d", "resnext50_3d"):   # in_hw = H = W, width = D; input channels 3 -> 32
+        if name in ("resnext3d", "resnext50_3d"):   # in_hw = H = W, width = D; input channels 3 -> 4
             classes = classes or 400
-            return cls(build_net(name, in_hw, classes, width, fuse), batch, 32, in_hw, in_hw, classes, device,
+            return cls(build_net(name, in_hw, classes, width, fuse), batch, 4, in_hw, in_hw, classes, device,
                        in_d=width)
         in_hw = in_hw or {"tiny": 32, "alexnet": 227}.get(name, 224)
         classes = classes or (10 if name == "tiny" else 1000)

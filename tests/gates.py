@@ -71,15 +71,31 @@ def step_for_decisions(ctx, plan_step):
         os.environ.pop("POOCH_DEBUG_NO_REUSE", None)
 
 
-def gate_decided(g, ref, tag):
+# the measured error ratio of a 3xTF32 tensor-core GEMM to an fp32 BLAS GEMM at K = 576
+# (test_gpu_ops.py::test_3xtf32_error_against_fp32: 14.5, growing with K; Reading 43)
+X3_OVER_FP32 = 15.0
+
+
+def gate_decided(g, ref, tag, ref32=None, factor=FP32_X):
     """The north_star gate, per tensor and whole, against the oracle run with the GPU's own
     ReLU / max-pool decisions (Reading 28): both sides decide in the same precision, so the gap is
-    the arithmetic's alone."""
-    rows = sorted(((k, rel(g[k], ref[k])) for k in ref if np.linalg.norm(np.asarray(ref[k])) > 0),
-                  key=lambda r: -r[1])
+    the arithmetic's alone. With ``ref32`` (the same decided oracle run in fp32) the BN gamma /
+    beta tensors -- sums over every voxel of a map with cancelling signs -- are gated at
+    max(5e-3, factor x their fp32 error), the floor the verdict asked to state per tensor; conv and
+    FC weights and the whole gradient keep 5e-3."""
+    rows = []
+    for k in ref:
+        if np.linalg.norm(np.asarray(ref[k])) == 0:
+            continue
+        e = rel(g[k], ref[k])
+        lim = TOL
+        if ref32 is not None and (".gamma" in k or ".beta" in k):
+            lim = max(TOL, factor * rel(ref32[k], ref[k]))
+        rows.append((k, e, lim))
+    rows.sort(key=lambda r: -r[1] / r[2])
     glob = global_rel(g, ref)
-    print("\n[%s, GPU decisions] whole gradient %.3e; worst: %s" % (
-        tag, glob, ", ".join("%s %.2e" % r for r in rows[:4])))
+    print("\n[%s, GPU decisions] whole gradient %.3e; worst (error, limit): %s" % (
+        tag, glob, ", ".join("%s %.2e %.2e" % r for r in rows[:4])))
     assert glob < TOL
-    assert rows[0][1] < TOL, rows[:8]
+    assert rows[0][1] < rows[0][2], rows[:8]
     return rows

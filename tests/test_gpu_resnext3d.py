@@ -7,7 +7,7 @@ oracle, through the C ABI:
   so the tolerance is fp32 accumulation's, not 3xTF32's);
 * the (1, 2, 2)-strided 7^3 stem and the strided 1^3 projection on the tensor-core kernels;
 * the padded 3^3 / 2 max-pool (values exact, gradient routing exact);
-* one training step of ResNeXt-50 (3D) (the same blocks as 101, [3, 4, 6, 3]) at 32 x 64 x 64
+* one training step of ResNeXt-50 (3D) (the same blocks as 101, [3, 4, 6, 3]) at 32 x 128 x 128
   against oracle nets.resnext3d (loss, per-tensor gate), and PoocH's plan below the in-core
   peak bit-exact against the in-core run.
 """
@@ -23,10 +23,15 @@ import synthdata  # noqa: E402
 from oracle import layers as L  # noqa: E402
 from oracle import nets  # noqa: E402
 from netutil import global_rel, load_params, pad_input, read_params, rel  # noqa: E402
-from gates import TOL, gate  # noqa: E402
+from gates import TOL, X3_OVER_FP32, gate_decided, gpu_decisions, step_for_decisions  # noqa: E402
 
 TOL_FP32 = 2e-6      # fp32 FMA chains of <= 864 terms against fp64
 TOL_X3 = 2e-5
+
+
+def tol_x3(K):
+    """3xTF32 tolerance growing with the reduction length (Reading 43; test_gpu_ops.tol_x3)."""
+    return max(TOL_X3, 1e-8 * K)
 
 
 def _lib():
@@ -139,20 +144,20 @@ def test_stem_and_projection_conv3d(case):
     dy = torch.full((1,) + y_ref.shape[2:] + (K,), float("nan"), device="cuda")
     lib.check(lib.lib.pooch_op_conv_fwd(C.byref(d), ptr(dx), ptr(dw), ptr(dy), None, None, None))
     torch.cuda.synchronize()
-    assert rel(ncdhw(dy.cpu().numpy()), y_ref) < TOL_X3
+    assert rel(ncdhw(dy.cpu().numpy()), y_ref) < tol_x3(Cc * k ** 3)
     gy = synthdata.rng(5).standard_normal(y_ref.shape).astype(np.float32).astype(np.float64)
     dgy = torch.from_numpy(ndhwc(gy).astype(np.float32)).cuda()
     wt = torch.from_numpy(np.ascontiguousarray(np.transpose(wkrsc(w), (4, 1, 2, 3, 0))).astype(np.float32)).cuda()
     gx = torch.full(dx.shape, float("nan"), device="cuda")
     lib.check(lib.lib.pooch_op_conv_dgrad(C.byref(d), ptr(dgy), ptr(wt), ptr(gx), 0, None))
     torch.cuda.synchronize()
-    assert rel(ncdhw(gx.cpu().numpy()), L.gconv3d_dgrad(gy, w, x.shape, s3, p, 1)) < TOL_X3
+    assert rel(ncdhw(gx.cpu().numpy()), L.gconv3d_dgrad(gy, w, x.shape, s3, p, 1)) < tol_x3(K * k ** 3)
     wsb = lib.lib.pooch_op_conv_wgrad_ws_bytes(C.byref(d))
     ws = torch.empty(max(wsb // 4, 1), device="cuda")
     gw = torch.full(dw.shape, float("nan"), device="cuda")
     lib.check(lib.lib.pooch_op_conv_wgrad(C.byref(d), ptr(dx), ptr(dgy), ptr(gw), ptr(ws), wsb, None))
     torch.cuda.synchronize()
-    assert rel(np.moveaxis(gw.cpu().numpy(), -1, 1), L.gconv3d_wgrad(x, gy, w.shape, s3, p, 1)) < TOL_X3
+    assert rel(np.moveaxis(gw.cpu().numpy(), -1, 1), L.gconv3d_wgrad(x, gy, w.shape, s3, p, 1)) < tol_x3(gy[0, 0].size)
 
 
 @pytest.mark.parametrize("shape", [(5, 7, 6, 64), (8, 8, 8, 32), (3, 4, 9, 16)])
@@ -177,7 +182,7 @@ def test_maxpool3d_k3s2p1(shape):
     assert rel(ncdhw(gx.cpu().numpy()), L.maxpool3d_bwd(gy, x, 3, 2, 1)) < 1e-7
 
 
-DHW = (32, 64, 64)
+DHW = (32, 128, 128)
 CLASSES = 10
 
 
@@ -197,7 +202,7 @@ def _put(ctx, x, labels):
     dev = ctx._torch[0]
     xp, lp = ctx.input_slot()
     base = dev.data_ptr()
-    xt = torch.from_numpy(pad_input(x, 32)).reshape(-1).cuda()
+    xt = torch.from_numpy(pad_input(x, 4)).reshape(-1).cuda()
     lt = torch.from_numpy(labels.astype(np.int32).reshape(-1)).cuda()
     dev[xp - base: xp - base + xt.numel() * 4].view(torch.float32).copy_(xt)
     dev[lp - base: lp - base + lt.numel() * 4].view(torch.int32).copy_(lt)
@@ -236,13 +241,36 @@ def test_resnext3d_graph_matches_oracle(rx):
 
 
 def test_resnext3d_step_matches_oracle(rx):
+    """Free-running against the fp64 oracle: the loss to 1e-3, the whole gradient within 10x what
+    plain fp32 arithmetic alone does to it (the fp32 oracle: 2.4 % at batch 1, where stage 4's BN
+    sees 32 voxels and flips ReLU decisions -- Reading 28's conditioning floor)."""
     ctx = _ctx(2 << 30, 64 << 20)
     ctx.profile(1)
     loss, _, _ = _step(ctx, rx, "incore")
     assert abs(loss - rx["loss"]) < 1e-3 * max(1.0, abs(rx["loss"]))
     g = read_params(ctx, rx["params"], 1)
-    assert global_rel(g, rx["grads"]) < TOL
-    gate(g, rx["grads"], rx["grads32"], "ResNeXt-50 (3D) 32x64x64")
+    e32 = global_rel(rx["grads32"], rx["grads"])
+    print("\n[ResNeXt-50 (3D)] whole gradient GPU %.3e, fp32 oracle %.3e" % (global_rel(g, rx["grads"]), e32))
+    assert global_rel(g, rx["grads"]) < max(TOL, 10 * e32)
+    ctx.close()
+
+
+def test_resnext3d_gradients_with_gpu_decisions(rx):
+    """Reading 28's strict gate: against the oracle taking the GPU's own ReLU masks and max-pool
+    winners (padded 3^3 / 2 windows included), every conv / FC weight gradient and the whole
+    gradient within 5e-3; BN gamma / beta within max(5e-3, 15x the decided fp32 oracle's error) --
+    15 = the measured error ratio of a 3xTF32 GEMM to an fp32 BLAS GEMM (Reading 43): the stem BN's
+    beta is a sum over 2^17 voxels with cancelling signs whose plain-fp32 error is already 6e-4
+    (GPU 7.3e-3, DESIGN.md Reading 28)."""
+    ctx = _ctx(2 << 30, 64 << 20)
+    ctx.profile(1)
+    step_for_decisions(ctx, lambda: _step(ctx, rx, "incore"))
+    dec = gpu_decisions(ctx, rx["net"])
+    g = read_params(ctx, rx["params"], 1)
+    _, ref, _ = nets.forward_backward(rx["net"], rx["params"], rx["x"], rx["t"], decisions=dec)
+    _, ref32, _ = nets.forward_backward(rx["net"], rx["params"], rx["x"], rx["t"], decisions=dec, precision="fp32")
+    rows = gate_decided(g, ref, "ResNeXt-50 (3D) 32x128x128", ref32, factor=X3_OVER_FP32)
+    assert max(r[1] for r in rows if r[0].endswith(".w")) < TOL
     ctx.close()
 
 
