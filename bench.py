@@ -50,6 +50,8 @@ sys.path.insert(0, HERE)
 METRIC = "ResNet-50 images/s at >HBM batch, 1/2/4/8 B200; overhead vs in-core; swap GB/s"
 METRIC_ALEX = "AlexNet images/s at a batch exceeding the device budget; overhead vs in-core; swap GB/s"
 METRIC_3D = "3D U-Net volumes/s at a >HBM footprint (batch 1, 256^3); overhead vs in-core per voxel; swap GB/s"
+METRIC_RX = ("ResNeXt-101 (3D) volumes/s at batch 1 with maps exceeding the device budget; overhead vs in-core at "
+             "the same volume; swap GB/s")
 
 
 def parse():
@@ -58,7 +60,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg4", "alexnet"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg4", "alexnet", "resnext3d"])
+    ap.add_argument("--dhw", default=None, help="resnext3d: input D x H (= W), e.g. 64x512 (default)")
     ap.add_argument("--edge", type=int, default=None, help="cfg4: volume edge (default 256)")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--budget-gib", type=float, default=None)
@@ -95,9 +98,15 @@ class Workload:
     def __init__(self, net, batch, budget, name, in_hw, classes, width=32):
         self.net, self.batch, self.budget, self.name = net, batch, budget, name
         self.in_hw, self.classes, self.width = in_hw, classes, width
-        self.three = net == "unet3d"
+        self.three = net in ("unet3d", "resnext3d")
+        self.rx = net == "resnext3d"     # in_hw = H = W, width = D, input 3 -> 4 channels, one label
         self.unit = "volumes/s" if self.three else "images/s"
-        self.metric = METRIC_3D if self.three else (METRIC_ALEX if net == "alexnet" else METRIC)
+        self.metric = (METRIC_RX if self.rx else METRIC_3D) if self.three else (
+            METRIC_ALEX if net == "alexnet" else METRIC)
+
+    @property
+    def voxels(self):
+        return self.width * self.in_hw * self.in_hw if self.rx else self.in_hw ** 3
 
     fuse = False   # BN-ReLU prologue fusion, set from --fuse
 
@@ -127,6 +136,15 @@ def workload(args):
         name = ("alexnet: AlexNet (single tower, LRN, dropout 0.5) batch %d 227^2, device budget %.0f GiB "
                 "(the paper's compute-heavy workload, P:L453; SURVEY 8(f) f3)" % (batch, budget / (1 << 30)))
         return Workload("alexnet", batch, budget, name, 227, 1000)
+    if args.workload == "resnext3d":
+        # the paper's third workload (batch 1, inputs whose maps exceed the 16 GB
+        # V100): ResNeXt-101 (3D) under a 16 GiB budget at a volume whose 207 maps take 16 GB (64 x
+        # 512^2; in-core fits the B200 at the same volume -> overhead at equal work)
+        d, h = (int(v) for v in (args.dhw or "64x512").split("x"))
+        budget = int((args.budget_gib or 16.0) * (1 << 30))
+        name = ("resnext3d: ResNeXt-101 (3D) (cardinality 32) batch 1, %d x %d x %d volume, device budget %.0f GiB "
+                "(the paper's 3D workload, P:L386; SURVEY 8(f) f4)" % (d, h, h, budget / (1 << 30)))
+        return Workload("resnext3d", 1, budget, name, h, 400, d)
     e = args.edge or 256
     budget = int(args.budget_gib * (1 << 30)) if args.budget_gib else None
     # (the 3D U-Net has no fusable BN-ReLU: fusion is 2D only)
@@ -253,6 +271,30 @@ def cpu_sample_3d(target_s=15.0, edge=16, width=32):
     return {"value": n * edge ** 3 / dt, "unit": "voxels/s", "cores": cores, "kind": "oracle",
             "sample": "%d fp64 3D U-Net fwd+bwd step(s) at %d^3, width %d (NumPy, BLAS threads = cores)" % (
                 n, edge, width)}
+
+
+def cpu_sample_rx(target_s=15.0, dhw=(8, 32, 32)):
+    """The oracle as it stands on ResNeXt-101 (3D) (fp64 NumPy) at a bounded volume: per-voxel rate."""
+    import numpy as np
+    import synthdata
+    from oracle import nets
+    cores = len(os.sched_getaffinity(0))
+    net = nets.resnext3d(dhw, classes=400)
+    params = nets.init_params(net, seed=2)
+    g = synthdata.rng(0)
+    x = g.standard_normal((1,) + tuple(dhw) + (3,))
+    t = g.integers(0, 400, (1,))
+    n, t0 = 0, time.time()
+    while True:
+        nets.forward_backward(net, params, x, t)
+        n += 1
+        if time.time() - t0 > target_s:
+            break
+    dt = time.time() - t0
+    vox = int(np.prod(dhw))
+    return {"value": n * vox / dt, "unit": "voxels/s", "cores": cores, "kind": "oracle",
+            "sample": "%d fp64 ResNeXt-101 (3D) fwd+bwd step(s) at %dx%dx%d (NumPy, BLAS threads = cores)" % (
+                (n,) + tuple(dhw))}
 
 
 def reference_arm(args):
@@ -653,7 +695,7 @@ def our_arm(args):
     if ablation is not None:
         line["ablation"] = ablation
     if W.three:
-        line["voxels_per_s"] = value * W.in_hw ** 3
+        line["voxels_per_s"] = value * W.voxels
 
     # ---- the in-core comparison and the secondary cfg2 line (after the arenas are released)
     if world == 1:
@@ -671,7 +713,7 @@ def our_arm(args):
             if cfg2 is not None:
                 line["cfg2"] = cfg2
     if rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = (cpu_sample_3d(15.0) if W.three else
+        line["cpu_baseline"] = (cpu_sample_rx(15.0) if W.rx else cpu_sample_3d(15.0) if W.three else
                                 cpu_sample_alex(15.0) if W.net == "alexnet" else cpu_sample(15.0, batch=1))
     if rank == 0:
         print(json.dumps(line, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
@@ -691,6 +733,12 @@ def synth_batch(W, rank):
     import numpy as np
     import torch
     import synthdata
+    if W.rx:
+        n = W.voxels
+        x = np.zeros((n, 4), np.float32)                     # 3 channels padded to 4
+        x[:, :3] = synthdata.rng(0 + rank).standard_normal((n, 3), dtype=np.float32)
+        lab = synthdata.rng(1 + rank).integers(0, W.classes, 1).astype(np.int32)
+        return torch.from_numpy(x.reshape(-1)).pin_memory(), torch.from_numpy(lab).pin_memory()
     if W.three:
         e = W.in_hw
         x = np.zeros((e * e * e, 32), np.float32)          # 1 channel padded to 32
@@ -830,7 +878,9 @@ def incore_and_cfg2(W, args, host, streams):
     iterations vs isolated timing) with its simulated and measured step time."""
     import numpy as np
     import torch
-    if W.three:
+    if W.rx:   # in-core fits at the benchmarked volume: the same step, every map kept
+        Wi = Workload(W.net, 1, None, "in-core " + W.name.split(",")[0], W.in_hw, W.classes, W.width)
+    elif W.three:
         Wi = Workload(W.net, 1, None, W.name, W.in_hw // 2, W.classes, W.width)
     elif W.net == "alexnet":   # in-core fits at the benchmarked batch: the same step, every map kept
         Wi = Workload(W.net, W.batch, None, "in-core AlexNet batch %d" % W.batch, W.in_hw, W.classes)
@@ -860,7 +910,12 @@ def incore_and_cfg2(W, args, host, streams):
         ri.ctx.set_timing(False)
         if W.three:
             e = Wi.in_hw
-            incore = {"volume_edge": e, "voxels_per_s": e ** 3 * 1000.0 / ms, "ms_per_step": ms, "families": fam}
+            incore = {"volume_edge": e, "voxels_per_s": Wi.voxels * 1000.0 / ms, "ms_per_step": ms, "families": fam,
+                      "cuda_graph": graph_in}
+            if W.rx:
+                incore = {"volume": [Wi.width, e, e], "volumes_per_s": 1000.0 / ms,
+                          "voxels_per_s": Wi.voxels * 1000.0 / ms, "ms_per_step": ms, "families": fam,
+                          "cuda_graph": graph_in}
             ri.close()
             return incore, None
         incore = {"batch": Wi.batch, "images_per_s": Wi.batch * 1000.0 / ms, "ms_per_step": ms, "families": fam,
@@ -911,6 +966,8 @@ def incore_and_cfg2(W, args, host, streams):
 
 def synth_bytes(W):
     """Bytes of one input batch (+ labels) as the GPU stores it (the e2e staging buffer)."""
+    if W.rx:
+        return W.voxels * 4 * 4 + 4
     if W.three:
         return W.in_hw ** 3 * (32 + 1) * 4
     return W.batch * (W.in_hw * W.in_hw * 4 + 1) * 4
