@@ -437,7 +437,8 @@ typedef struct {
   int32_t groups;     /* 0 / 1: dense. > 1: grouped 3D conv (ResNeXt-101 (3D), SURVEY 8(f) f4;
                          definition: oracle layers.gconv3d_fwd, the aggregated transformation of
                          P:L386's ResNeXt): D > 0, C == K, C / groups in {4, 8, 16, 32}, K % 32 == 0,
-                         R == S in {1, 3}, strides <= 2; weights [K][R][R][R][C/groups], and dgrad
+                         R == S in {1, 3}, one stride (1 or 2) on all three axes; weights
+                         [K][R][R][R][C/groups], and dgrad
                          reads that same (untransposed) layout as `wt`. FP32 on the CUDA cores. */
   int32_t stride_d;   /* 3D: stride along depth; 0 = `stride` (ResNeXt-101 (3D)'s stem: 1, 2, 2) */
 } pooch_conv_desc;
@@ -521,6 +522,49 @@ pooch_status pooch_op_maxpool3d_fwd_k(const float* x, float* y, int32_t D, int32
 pooch_status pooch_op_maxpool3d_bwd_k(const float* x, const float* gy, float* gx, void* arg_ws, int32_t D, int32_t H,
                                       int32_t W, int32_t C, int32_t k, int32_t s, int32_t p, int32_t accumulate,
                                       void* stream);
+/* ---------------------------------------------------------------- intra-layer division */
+/* ooc_cuDNN-style division of a single layer whose maps exceed the device (P:L495,
+ * Sec. 6: "ooc_cuDNN performs data-swapping after dividing each computation and data ... supports
+ * NNs where memory consumption of a single layer exceeds the GPU memory capacity"). Tensors are
+ * HOST-resident (pinned, NDHWC, batch 1); the layer runs in chunks of depth rows through the
+ * caller's device workspace `ws` of ws_bytes (the chunk size is the largest that fits two buffer
+ * sets), the copies of one chunk overlapping the kernels of the next on three streams (`streams`:
+ * compute, H2D, D2H cudaStream_t). A convolution chunk loads its input rows plus the halo rows
+ * (zero rows at the volume's faces) and runs the undivided kernels on the slab, padded in H / W
+ * only, so conv fwd / dgrad outputs equal the undivided launch bit for bit; BN statistics and
+ * wgrad partials are summed over chunks in chunk order (fp64 / fp32). Synchronous: returns when
+ * done; *info (nullable) gets the chunking, the device time and the bytes moved. POOCH_EINFEASIBLE
+ * when one row does not fit ws; POOCH_EUSAGE for unsupported shapes (3D dense single-source
+ * convs, one stride on all axes, kernel >= stride). */
+typedef struct {
+  int32_t chunks, rows_per_chunk;
+  double ms;
+  uint64_t h2d_bytes, d2h_bytes;
+} pooch_div_info;
+/* y = conv3d(x, w) (x [D][H][W][C] host, w device KTRSC, y [Do][Ho][Wo][K] host). With `stats`
+ * (device [4K]: mean, invstd, scale, shift) the training-mode BN statistics of y are computed
+ * (bn_finalize's formula, eps 1e-5) for gamma / beta (device [K]). */
+pooch_status pooch_div_conv3d_fwd(const pooch_conv_desc* d, const float* x_host, const float* w_dev, float* y_host,
+                                  const float* gamma, const float* beta, float* stats, void* ws, size_t ws_bytes,
+                                  void* const* streams, pooch_div_info* info);
+/* y = relu(scale[c] c + shift[c]) over rows x row_floats (row_floats = H W C) host floats. */
+pooch_status pooch_div_bn_relu_fwd(const float* c_host, const float* stats, float* y_host, int64_t rows,
+                                   int64_t row_floats, int32_t C, void* ws, size_t ws_bytes, void* const* streams,
+                                   pooch_div_info* info);
+/* BN-ReLU backward in two passes over the chunks: dbeta = sum dz, dgamma = sum dz xhat (device [C]),
+ * gx = gamma invstd (dz - dbeta / M - xhat dgamma / M), dz = gy [relu input > 0]. */
+pooch_status pooch_div_bn_relu_bwd(const float* c_host, const float* gy_host, const float* stats, const float* gamma,
+                                   float* dgamma, float* dbeta, float* gx_host, int64_t rows, int64_t row_floats,
+                                   int32_t C, void* ws, size_t ws_bytes, void* const* streams, pooch_div_info* info);
+/* gx = conv3d^T(gy, wt) (wt device [C][T][R][S][K], as pooch_op_conv_dgrad), host in / out. */
+pooch_status pooch_div_conv3d_dgrad(const pooch_conv_desc* d, const float* gy_host, const float* wt_dev,
+                                    float* gx_host, void* ws, size_t ws_bytes, void* const* streams,
+                                    pooch_div_info* info);
+/* dw (device KTRSC) = sum over chunks of the chunk's wgrad (x, gy host). */
+pooch_status pooch_div_conv3d_wgrad(const pooch_conv_desc* d, const float* x_host, const float* gy_host,
+                                    float* dw_dev, void* ws, size_t ws_bytes, void* const* streams,
+                                    pooch_div_info* info);
+
 /* D[split][M][N] = A * B^T on the tensor-core core, A [M][K] and B [N][K] row-major (K-major);
  * a_mn = 2 selects the 3xTF32 path, other non-zero a_mn / b_mn (MN-major operands) return
  * POOCH_EUSAGE; bn in {64,128,256} (64/128 for 3xTF32); splits >= 1. Unit test only. */

@@ -37,6 +37,11 @@ class ConvDesc(C.Structure):
                                      "groups", "stride_d")]
 
 
+class DivInfo(C.Structure):
+    _fields_ = [("chunks", c_i32), ("rows_per_chunk", c_i32), ("ms", c_f64), ("h2d_bytes", c_u64),
+                ("d2h_bytes", c_u64)]
+
+
 class LayerDesc(C.Structure):
     _fields_ = [("kind", c_i32), ("in0", c_i32), ("in1", c_i32), ("cin", c_i32), ("cout", c_i32),
                 ("hout", c_i32), ("wout", c_i32), ("k", c_i32), ("stride", c_i32), ("pad", c_i32),
@@ -128,6 +133,12 @@ SIGNATURES = {
     "pooch_op_maxpool3d_fwd_k": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_op_maxpool3d_bwd_k": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                                          c_i32, c_vp]),
+    "pooch_div_conv3d_fwd": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
+    "pooch_div_bn_relu_fwd": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_sz, c_vp, c_vp]),
+    "pooch_div_bn_relu_bwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_sz,
+                                      c_vp, c_vp]),
+    "pooch_div_conv3d_dgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
+    "pooch_div_conv3d_wgrad": (c_i32, [P(ConvDesc), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
     "pooch_op_maxpool2d_fwd": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_op_maxpool2d_bwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pooch_op_bn_ws_bytes": (c_sz, [c_i32]),

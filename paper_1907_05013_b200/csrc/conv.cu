@@ -288,7 +288,7 @@ static GemmParams base_params(const ConvGeom& g) {
   p.Ho = g.Ho; p.Wo = g.Wo; p.stride = g.stride; p.pad = g.pad;
   p.T = g.T();
   p.st3 = g.sd();
-  p.pad3 = g.is3d() ? g.pad : 0;
+  p.pad3 = g.pd();
   p.dg_nt = 1;
   return p;
 }
@@ -431,7 +431,7 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
           q.dg_a = a; q.dg_b = bb; q.dg_c = cz;
           q.dg_r0 = first_tap(a, g.pad, s_);
           q.dg_s0 = first_tap(bb, g.pad, s_);
-          q.dg_t0 = g.is3d() ? first_tap(cz, g.pad, s3) : 0;
+          q.dg_t0 = g.is3d() ? first_tap(cz, g.pd(), s3) : 0;
           q.dg_nr = ntaps(q.dg_r0, g.R, s_);
           q.dg_ns = ntaps(q.dg_s0, g.S, s_);
           q.dg_nt = g.is3d() ? ntaps(q.dg_t0, g.R, s3) : 1;

@@ -19,6 +19,10 @@ struct ConvGeom {
   int stride_d = 0;
   bool is3d() const { return D > 0; }
   int sd() const { return D > 0 ? (stride_d > 0 ? stride_d : stride) : 1; }
+  // 3D: padding along depth (-1 = pad); the divided layers (divide.cu) run depth slabs whose halo
+  // rows are real or zero-filled rows, so their sub-convolutions pad only H and W
+  int pad_d = -1;
+  int pd() const { return D > 0 ? (pad_d >= 0 ? pad_d : pad) : 0; }
   int T() const { return D > 0 ? R : 1; }
 };
 ConvGeom conv_geom(const pooch_conv_desc& d);

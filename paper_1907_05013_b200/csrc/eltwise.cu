@@ -735,6 +735,112 @@ static pooch_status bn_bwd_mode(const BnBwdArgs& a, float* ws, cudaStream_t st) 
   return POOCH_OK;
 }
 
+// ---- BN-ReLU backward in pieces (divided layers, divide.cu): per-chunk partial sums accumulated
+// in fp64 across chunks in order, one finalize, per-chunk apply
+namespace {
+__global__ void acc_partials_kernel(const float* __restrict__ part, int blocks, int C, int nq, double* __restrict__ acc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  for (int q = 0; q < nq; ++q) {
+    double s = 0;
+    for (int b = 0; b < blocks; ++b) s += (double)part[((size_t)q * blocks + b) * C + c];
+    acc[(size_t)q * C + c] += s;
+  }
+}
+
+__global__ void bn_bwd_finalize_sums_kernel(BnBwdArgs p, const double* __restrict__ acc, double M, float* coef) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= p.C) return;
+  p.dbeta_a[c] = (float)acc[c];
+  p.dgamma_a[c] = (float)acc[p.C + c];
+  coef[c] = p.gamma_a[c] * p.invstd_a[c];
+  coef[p.C + c] = (float)(acc[c] / M);
+  coef[2 * p.C + c] = (float)(acc[p.C + c] / M);
+}
+
+__global__ void acc_tiles_kernel(const float* __restrict__ ts, const float* __restrict__ tq, int tiles, int C,
+                                 double* __restrict__ acc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0, q = 0;
+  for (int t = 0; t < tiles; ++t) {
+    s += (double)ts[(size_t)t * C + c];
+    q += (double)tq[(size_t)t * C + c];
+  }
+  acc[c] += s;
+  acc[C + c] += q;
+}
+
+__global__ void bn_finalize_sums_kernel(const double* __restrict__ acc, int C, double count, const float* gamma,
+                                        const float* beta, float* mean, float* invstd, float* scale, float* shift) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double mu = acc[c] / count;
+  double var = acc[C + c] / count - mu * mu;
+  if (var < 0) var = 0;
+  const float is = (float)(1.0 / sqrt(var + 1e-5));
+  const float m = (float)mu;
+  mean[c] = m;
+  invstd[c] = is;
+  const float sc = gamma[c] * is;
+  scale[c] = sc;
+  shift[c] = __fsub_rn(beta[c], __fmul_rn(m, sc));
+}
+}  // namespace
+
+pooch_status bn_relu_bwd_partial(const BnBwdArgs& a, float* ws, double* acc, cudaStream_t st) {
+  const int C = a.C, C4 = C / 4;
+  if (a.mode != 0 || C % 4 || C > 2048) return fail(POOCH_EUSAGE, "divided BN-ReLU backward: mode 0, C %% 4 == 0, C <= 2048");
+  const int blocks = bwd_blocks(a.rows);
+  const int cgpt = C4 > kBwdThreads ? C4 / kBwdThreads : 1;
+  const int rpi = kBwdThreads / (C4 / cgpt);
+  const size_t smem = (size_t)2 * rpi * C * sizeof(float);
+  count_launch();
+  if (cgpt == 1) {
+    if (smem > 48 * 1024) POOCH_CUDA(cudaFuncSetAttribute(bn_bwd_reduce_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bn_bwd_reduce_kernel<0, 1><<<blocks, kBwdThreads, smem, st>>>(a, ws);
+  } else {
+    if (smem > 48 * 1024) POOCH_CUDA(cudaFuncSetAttribute(bn_bwd_reduce_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bn_bwd_reduce_kernel<0, 2><<<blocks, kBwdThreads, smem, st>>>(a, ws);
+  }
+  count_launch();
+  acc_partials_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, blocks, C, 2, acc);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status bn_relu_bwd_finalize(const BnBwdArgs& a, const double* acc, int64_t total_rows, float* coef,
+                                  cudaStream_t st) {
+  count_launch();
+  bn_bwd_finalize_sums_kernel<<<(a.C + 127) / 128, 128, 0, st>>>(a, acc, (double)total_rows, coef);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status bn_relu_bwd_apply(const BnBwdArgs& a, const float* coef, cudaStream_t st) {
+  const int64_t n4 = a.rows * a.C / 4;
+  count_launch();
+  bn_bwd_apply_kernel<0><<<grid_for(n4, 256), 256, 0, st>>>(a, coef, n4);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status bn_acc_tiles(const float* ts, const float* tq, int tiles, int C, double* acc, cudaStream_t st) {
+  count_launch();
+  acc_tiles_kernel<<<(C + 127) / 128, 128, 0, st>>>(ts, tq, tiles, C, acc);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
+pooch_status bn_finalize_sums(const double* acc, int C, int64_t count, const float* gamma, const float* beta,
+                              float* mean, float* invstd, float* scale, float* shift, cudaStream_t st) {
+  count_launch();
+  bn_finalize_sums_kernel<<<(C + 127) / 128, 128, 0, st>>>(acc, C, (double)count, gamma, beta, mean, invstd, scale,
+                                                           shift);
+  POOCH_CUDA(cudaGetLastError());
+  return POOCH_OK;
+}
+
 pooch_status bn_bwd(const BnBwdArgs& a, float* ws, cudaStream_t st) {
   if (a.C % 4 != 0 || a.C > 2048 || a.C < 4) return fail(POOCH_EUSAGE, "BN backward: bad C %d", a.C);
   if (a.mode == 0) return bn_bwd_mode<0>(a, ws, st);

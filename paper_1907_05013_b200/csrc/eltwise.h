@@ -41,6 +41,17 @@ struct BnBwdArgs {
 };
 size_t bn_bwd_ws_bytes(int C);
 pooch_status bn_bwd(const BnBwdArgs& a, float* ws, cudaStream_t st);
+// BN(-ReLU) in pieces for the divided layers (divide.cu): partial sums of a chunk (mode 0)
+// accumulated into acc[2][C] (fp64, chunk order); finalize dbeta / dgamma / coef (3C floats) from
+// acc over total_rows; apply on a chunk. Forward: tile partials of a chunk's conv epilogue into
+// acc[2][C], then mean / invstd / scale / shift from acc (bn_finalize's formula).
+pooch_status bn_relu_bwd_partial(const BnBwdArgs& a, float* ws, double* acc, cudaStream_t st);
+pooch_status bn_relu_bwd_finalize(const BnBwdArgs& a, const double* acc, int64_t total_rows, float* coef,
+                                  cudaStream_t st);
+pooch_status bn_relu_bwd_apply(const BnBwdArgs& a, const float* coef, cudaStream_t st);
+pooch_status bn_acc_tiles(const float* ts, const float* tq, int tiles, int C, double* acc, cudaStream_t st);
+pooch_status bn_finalize_sums(const double* acc, int C, int64_t count, const float* gamma, const float* beta,
+                              float* mean, float* invstd, float* scale, float* shift, cudaStream_t st);
 
 // ---- pooling (NHWC)
 pooch_status maxpool_fwd(const float* x, float* y, int N, int H, int W, int C, int k, int s, int p, int Ho, int Wo,

@@ -12,17 +12,19 @@
 // every kernel here register-blocks 32 accumulators per thread so one shared-memory or global
 // load feeds 4-32 FMAs, and all reductions run in a fixed order (plans stay bit-exact).
 //
-// fwd  : one thread = one output voxel x 32 output channels (NG = 32 / Kg groups); a block = 128
-//        voxels x one 32-channel group block; weights of those groups transposed into shared
-//        memory [group][tap][c][o]; BN partial sums per block in a fixed order.
-// dgrad: one thread = one input voxel x 32 input channels; the taps whose output position is an
-//        integer (stride 2: one or two per axis) gather dy; weights in smem [group][tap][o][c].
-// wgrad: a block = a chunk of output voxels x a group block x a slice of taps; 32-voxel tiles of
-//        dy and of the tap-shifted x are staged in smem; every thread owns 4 x 4 (o, c) blocks of
-//        dw; per-chunk partials are summed over the chunks in order by a second kernel.
+// fwd  : a block = 128 output voxels x one 32-channel block (32 / Cg groups); a thread = 4 voxels
+//        x one channel quad, so a warp-wide 128-bit load covers 4 voxels' 128 contiguous bytes and
+//        one shared-memory weight quad feeds 16 FMAs; weights staged [tap][c][o]; BN partial sums
+//        per block in a fixed order.
+// dgrad: the same layout over input voxels; the taps whose output position is an integer gather
+//        dy (stride 2: each warp owns one W parity, so its lanes skip the same taps).
+// wgrad: a block = a chunk of output voxels x a 32-channel block x a slice of taps; 16 / 32-voxel
+//        tiles of dy and of the tap-shifted x are staged in smem; every thread owns 4 x 4 (o, c)
+//        blocks of dw; per-chunk partials are summed over the chunks in order by a second kernel.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 
 #include "common.h"
 #include "conv.h"
@@ -31,9 +33,8 @@ namespace pooch {
 
 namespace {
 
-constexpr int kFwdThreads = 128;
-constexpr int kWgV = 32;          // voxels per wgrad smem tile
-constexpr int kWgThreads = 256;
+constexpr int kThreads = 256;     // every kernel: 8 warps
+constexpr int kVoxBlk = 128;      // fwd / dgrad: voxels per block (8 warps x 4 voxel lanes x kV)
 
 struct GArgs {
   const float* x;    // [D][H][W][C]
@@ -51,234 +52,300 @@ struct GArgs {
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
+// the output position o of input coordinate i through tap u (stride S, padding pad), if integral
+template <int S>
+__device__ __forceinline__ bool tap_ok(int i, int u, int pad, int n_out, int& o) {
+  const int q = i + pad - u;
+  if (q < 0 || (S == 2 && (q & 1))) return false;
+  o = S == 2 ? q >> 1 : q;
+  return o < n_out;
+}
+
 // ------------------------------------------------------------------------------ forward
-template <int CG>  // channels per group (in == out); NG = 32 / CG groups per block
-__global__ void __launch_bounds__(kFwdThreads) gconv_fwd_kernel(GArgs a) {
-  constexpr int NG = 32 / CG;
-  extern __shared__ float ws[];  // [NG][taps][CG (c)][CG (o)]
+// Thread layout shared by fwd and dgrad: lane = (vs, q) with q = lane & 7 the channel quad (4
+// channels of the block's 32) and vs = lane >> 3; a thread owns kV voxels, so one warp-wide
+// 128-bit access covers 4 voxels x 128 contiguous bytes, and one shared-memory weight quad
+// (broadcast to the lanes of equal q, conflict-free across q) feeds 4 x kV FMAs.
+constexpr int kV = 4;
+
+__device__ __forceinline__ float f4c(const float4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void fma4(float4& acc, float s, const float4& w) {
+  acc.x = fmaf(s, w.x, acc.x);
+  acc.y = fmaf(s, w.y, acc.y);
+  acc.z = fmaf(s, w.z, acc.z);
+  acc.w = fmaf(s, w.w, acc.w);
+}
+
+template <int CG>  // channels per group (in == out)
+__global__ void __launch_bounds__(kThreads) gconv_fwd_kernel(GArgs a) {
+  extern __shared__ float4 smem4[];
+  float* ws = reinterpret_cast<float*>(smem4);  // [taps][CG (c)][32 (o of the block)]
   const int taps = a.k * a.k * a.k;
-  const int gb = blockIdx.y;     // 32-channel block: groups gb*NG .. gb*NG+NG-1
-  for (int i = threadIdx.x; i < NG * taps * CG * CG; i += blockDim.x) {
-    // i -> (j, tap, c, o) in smem order; the global weight is [K][taps][CG]
-    const int o = i % CG, c = (i / CG) % CG, tap = (i / (CG * CG)) % taps, j = i / (CG * CG * taps);
-    ws[i] = a.w[((int64_t)(gb * 32 + j * CG + o) * taps + tap) * CG + c];
+  const int gb = blockIdx.y;
+  for (int i = threadIdx.x; i < taps * CG * 32; i += kThreads) {
+    const int o = i & 31, c = (i >> 5) % CG, tap = i / (32 * CG);
+    ws[i] = a.w[((int64_t)(gb * 32 + o) * taps + tap) * CG + c];
   }
   __syncthreads();
-  const int64_t m = (int64_t)blockIdx.x * kFwdThreads + threadIdx.x;
-  float acc[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 7, vs = lane >> 3;
+  const int cin0 = gb * 32 + ((4 * q) / CG) * CG;  // first input channel of this thread's group
+  int64_t m[kV];
+  int od[kV], oh[kV], ow[kV];
+  bool ok[kV];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-  const bool valid = m < a.M;
-  if (valid) {
-    const int ow = (int)(m % a.Wo);
-    const int oh = (int)((m / a.Wo) % a.Ho);
-    const int od = (int)(m / ((int64_t)a.Wo * a.Ho));
-    int tap = 0;
-    for (int u = 0; u < a.k; ++u) {
-      const int zi = od * a.sd - a.pad + u;
-      for (int v = 0; v < a.k; ++v) {
-        const int hi = oh * a.s - a.pad + v;
-        for (int t = 0; t < a.k; ++t, ++tap) {
-          const int wi = ow * a.s - a.pad + t;
-          if (zi < 0 || zi >= a.D || hi < 0 || hi >= a.H || wi < 0 || wi >= a.W) continue;
-          const float* xp = a.x + (((int64_t)zi * a.H + hi) * a.W + wi) * a.C + gb * 32;
+  for (int i = 0; i < kV; ++i) {
+    m[i] = (int64_t)blockIdx.x * kVoxBlk + warp * 16 + vs + 4 * i;
+    ok[i] = m[i] < a.M;
+    ow[i] = (int)(m[i] % a.Wo);
+    oh[i] = (int)((m[i] / a.Wo) % a.Ho);
+    od[i] = (int)(m[i] / ((int64_t)a.Wo * a.Ho));
+  }
+  float4 acc[kV];
 #pragma unroll
-          for (int j = 0; j < NG; ++j) {
-            float xv[CG];
+  for (int i = 0; i < kV; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int u = 0; u < a.k; ++u) {
+    for (int v = 0; v < a.k; ++v) {
+      const float* rp[kV];
+      bool rv[kV];
 #pragma unroll
-            for (int c4 = 0; c4 < CG / 4; ++c4) {
-              const float4 q = ldg4(xp + j * CG + 4 * c4);
-              xv[4 * c4] = q.x; xv[4 * c4 + 1] = q.y; xv[4 * c4 + 2] = q.z; xv[4 * c4 + 3] = q.w;
-            }
-            const float* wr = ws + ((j * taps + tap) * CG) * CG;
+      for (int i = 0; i < kV; ++i) {
+        const int zi = od[i] * a.sd - a.pad + u, hi = oh[i] * a.s - a.pad + v;
+        rv[i] = ok[i] && zi >= 0 && zi < a.D && hi >= 0 && hi < a.H;
+        rp[i] = a.x + ((int64_t)(rv[i] ? zi : 0) * a.H + (rv[i] ? hi : 0)) * a.W * a.C + cin0;
+      }
+      for (int t = 0; t < a.k; ++t) {
+        const float* wt = ws + ((u * a.k + v) * a.k + t) * CG * 32 + 4 * q;
+        const float* xp[kV];
+        bool xv_ok[kV];
 #pragma unroll
-            for (int c = 0; c < CG; ++c) {
+        for (int i = 0; i < kV; ++i) {
+          const int wi = ow[i] * a.s - a.pad + t;
+          xv_ok[i] = rv[i] && wi >= 0 && wi < a.W;
+          xp[i] = rp[i] + (int64_t)(xv_ok[i] ? wi : 0) * a.C;
+        }
 #pragma unroll
-              for (int o4 = 0; o4 < CG / 4; ++o4) {
-                const float4 wv = *reinterpret_cast<const float4*>(wr + c * CG + 4 * o4);
-                float* ac = acc + j * CG + 4 * o4;
-                ac[0] = fmaf(xv[c], wv.x, ac[0]);
-                ac[1] = fmaf(xv[c], wv.y, ac[1]);
-                ac[2] = fmaf(xv[c], wv.z, ac[2]);
-                ac[3] = fmaf(xv[c], wv.w, ac[3]);
-              }
-            }
+        for (int c4 = 0; c4 < CG / 4; ++c4) {
+          float4 xv[kV];
+#pragma unroll
+          for (int i = 0; i < kV; ++i) xv[i] = xv_ok[i] ? ldg4(xp[i] + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const float4 w4 = *reinterpret_cast<const float4*>(wt + (4 * c4 + cc) * 32);
+#pragma unroll
+            for (int i = 0; i < kV; ++i) fma4(acc[i], f4c(xv[i], cc), w4);
           }
         }
       }
     }
-    float* yp = a.out + m * a.K + gb * 32;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      *reinterpret_cast<float4*>(yp + 4 * i) = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
   }
+#pragma unroll
+  for (int i = 0; i < kV; ++i)
+    if (ok[i]) *reinterpret_cast<float4*>(a.out + m[i] * a.K + gb * 32 + 4 * q) = acc[i];
   if (!a.stat_sum) return;
-  // BN partial sums of this block's 128 voxels x 32 channels: warp shuffles, then the four
-  // warps in order (invalid voxels contribute zeros)
-  __shared__ float red[2][kFwdThreads / 32][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // BN partial sums of the block's 128 voxels: the thread's kV voxels, the four voxel lanes of
+  // its quad (shuffles), then the eight warps in order (invalid voxels hold zeros)
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f), sq = s;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float sv = acc[i], qv = acc[i] * acc[i];
+  for (int i = 0; i < kV; ++i) {
+    s.x += acc[i].x; s.y += acc[i].y; s.z += acc[i].z; s.w += acc[i].w;
+    sq.x = fmaf(acc[i].x, acc[i].x, sq.x); sq.y = fmaf(acc[i].y, acc[i].y, sq.y);
+    sq.z = fmaf(acc[i].z, acc[i].z, sq.z); sq.w = fmaf(acc[i].w, acc[i].w, sq.w);
+  }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      sv += __shfl_xor_sync(0xffffffffu, sv, off);
-      qv += __shfl_xor_sync(0xffffffffu, qv, off);
-    }
-    if (lane == i) {
-      red[0][warp][i] = sv;
-      red[1][warp][i] = qv;
-    }
+  for (int off = 8; off < 32; off <<= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, off); s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+    s.z += __shfl_xor_sync(0xffffffffu, s.z, off); s.w += __shfl_xor_sync(0xffffffffu, s.w, off);
+    sq.x += __shfl_xor_sync(0xffffffffu, sq.x, off); sq.y += __shfl_xor_sync(0xffffffffu, sq.y, off);
+    sq.z += __shfl_xor_sync(0xffffffffu, sq.z, off); sq.w += __shfl_xor_sync(0xffffffffu, sq.w, off);
+  }
+  __shared__ float4 red[2][kThreads / 32][8];
+  if (vs == 0) {
+    red[0][warp][q] = s;
+    red[1][warp][q] = sq;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float sv = 0.f, qv = 0.f;
-    for (int w = 0; w < kFwdThreads / 32; ++w) {
-      sv += red[0][w][threadIdx.x];
-      qv += red[1][w][threadIdx.x];
+  if (threadIdx.x < 16) {
+    const int which = threadIdx.x >> 3, qq = threadIdx.x & 7;
+    float4 r = red[which][0][qq];
+    for (int w = 1; w < kThreads / 32; ++w) {
+      const float4 e = red[which][w][qq];
+      r.x += e.x; r.y += e.y; r.z += e.z; r.w += e.w;
     }
-    a.stat_sum[(int64_t)blockIdx.x * a.K + gb * 32 + threadIdx.x] = sv;
-    a.stat_sq[(int64_t)blockIdx.x * a.K + gb * 32 + threadIdx.x] = qv;
+    float* dst = (which ? a.stat_sq : a.stat_sum) + (int64_t)blockIdx.x * a.K + gb * 32 + 4 * qq;
+    *reinterpret_cast<float4*>(dst) = r;
   }
 }
 
 // ------------------------------------------------------------------------------ dgrad
-// first tap index u (0 <= u < k) with (i + pad - u) % s == 0, and the output position
-__device__ __forceinline__ bool tap_ok(int i, int u, int pad, int s, int n_out, int& o) {
-  const int q = i + pad - u;
-  if (q < 0 || q % s) return false;
-  o = q / s;
-  return o < n_out;
-}
-
-template <int CG>
-__global__ void __launch_bounds__(kFwdThreads) gconv_dgrad_kernel(GArgs a) {
-  constexpr int NG = 32 / CG;
-  extern __shared__ float ws[];  // [NG][taps][CG (o)][CG (c)]: the global layout per group
+// dx[in voxel][c] = sum over taps whose output position is an integer, sum_o dy[out][o] w[o][tap][c].
+// Strides are uniform (1 or 2, S2). Stride 2: a warp owns 16 input voxels of one parity along W
+// (every other voxel of 32), so its lanes skip the same taps.
+template <int CG, bool S2>
+__global__ void __launch_bounds__(kThreads) gconv_dgrad_kernel(GArgs a) {
+  extern __shared__ float4 smem4[];
+  float* wd = reinterpret_cast<float*>(smem4);  // [taps][CG (o)][32 (c of the block)]
   const int taps = a.k * a.k * a.k;
   const int gb = blockIdx.y;
-  for (int i = threadIdx.x; i < NG * taps * CG * CG; i += blockDim.x) {
-    const int c = i % CG, o = (i / CG) % CG, tap = (i / (CG * CG)) % taps, j = i / (CG * CG * taps);
-    ws[i] = a.w[((int64_t)(gb * 32 + j * CG + o) * taps + tap) * CG + c];
+  for (int i = threadIdx.x; i < taps * CG * 32; i += kThreads) {
+    const int c32 = i & 31, o = (i >> 5) % CG, tap = i / (32 * CG);
+    wd[i] = a.w[((int64_t)(gb * 32 + (c32 / CG) * CG + o) * taps + tap) * CG + (c32 % CG)];
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 7, vs = lane >> 3;
+  const int o0 = gb * 32 + ((4 * q) / CG) * CG;  // first dy channel of this thread's group
   const int64_t n_in = (int64_t)a.D * a.H * a.W;
-  const int64_t m = (int64_t)blockIdx.x * kFwdThreads + threadIdx.x;
-  if (m >= n_in) return;
-  const int wi = (int)(m % a.W);
-  const int hi = (int)((m / a.W) % a.H);
-  const int zi = (int)(m / ((int64_t)a.W * a.H));
-  float acc[32];
+  int64_t m[kV];
+  int zi[kV], hi[kV], wi[kV];
+  bool ok[kV];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+  for (int i = 0; i < kV; ++i) {
+    m[i] = S2 ? (int64_t)blockIdx.x * kVoxBlk + (warp >> 1) * 32 + (warp & 1) + 2 * (vs + 4 * i)
+              : (int64_t)blockIdx.x * kVoxBlk + warp * 16 + vs + 4 * i;
+    ok[i] = m[i] < n_in;
+    wi[i] = (int)(m[i] % a.W);
+    hi[i] = (int)((m[i] / a.W) % a.H);
+    zi[i] = (int)(m[i] / ((int64_t)a.W * a.H));
+  }
+  float4 acc[kV];
+#pragma unroll
+  for (int i = 0; i < kV; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int u = 0; u < a.k; ++u) {
-    int od;
-    if (!tap_ok(zi, u, a.pad, a.sd, a.Do, od)) continue;
+    int odv[kV];
+    bool zv[kV], any_z = false;
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      zv[i] = ok[i] && tap_ok<(S2 ? 2 : 1)>(zi[i], u, a.pad, a.Do, odv[i]);
+      any_z |= zv[i];
+    }
+    if (!any_z) continue;
     for (int v = 0; v < a.k; ++v) {
-      int oh;
-      if (!tap_ok(hi, v, a.pad, a.s, a.Ho, oh)) continue;
+      int ohv[kV];
+      bool hv[kV], any_h = false;
+#pragma unroll
+      for (int i = 0; i < kV; ++i) {
+        hv[i] = zv[i] && tap_ok<(S2 ? 2 : 1)>(hi[i], v, a.pad, a.Ho, ohv[i]);
+        any_h |= hv[i];
+      }
+      if (!any_h) continue;
       for (int t = 0; t < a.k; ++t) {
-        int ow;
-        if (!tap_ok(wi, t, a.pad, a.s, a.Wo, ow)) continue;
-        const int tap = (u * a.k + v) * a.k + t;
-        const float* gp = a.dy + (((int64_t)od * a.Ho + oh) * a.Wo + ow) * a.K + gb * 32;
+        const float* gp[kV];
+        bool gv_ok[kV], any_w = false;
 #pragma unroll
-        for (int j = 0; j < NG; ++j) {
-          float gv[CG];
+        for (int i = 0; i < kV; ++i) {
+          int owv = 0;
+          gv_ok[i] = hv[i] && tap_ok<(S2 ? 2 : 1)>(wi[i], t, a.pad, a.Wo, owv);
+          any_w |= gv_ok[i];
+          gp[i] = a.dy + (gv_ok[i] ? (((int64_t)odv[i] * a.Ho + ohv[i]) * a.Wo + owv) * a.K : 0) + o0;
+        }
+        if (!any_w) continue;
+        const float* wt = wd + ((u * a.k + v) * a.k + t) * CG * 32 + 4 * q;
 #pragma unroll
-          for (int o4 = 0; o4 < CG / 4; ++o4) {
-            const float4 q = ldg4(gp + j * CG + 4 * o4);
-            gv[4 * o4] = q.x; gv[4 * o4 + 1] = q.y; gv[4 * o4 + 2] = q.z; gv[4 * o4 + 3] = q.w;
-          }
-          const float* wr = ws + ((j * taps + tap) * CG) * CG;
+        for (int o4 = 0; o4 < CG / 4; ++o4) {
+          float4 gv[kV];
 #pragma unroll
-          for (int o = 0; o < CG; ++o) {
+          for (int i = 0; i < kV; ++i) gv[i] = gv_ok[i] ? ldg4(gp[i] + 4 * o4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int c4 = 0; c4 < CG / 4; ++c4) {
-              const float4 wv = *reinterpret_cast<const float4*>(wr + o * CG + 4 * c4);
-              float* ac = acc + j * CG + 4 * c4;
-              ac[0] = fmaf(gv[o], wv.x, ac[0]);
-              ac[1] = fmaf(gv[o], wv.y, ac[1]);
-              ac[2] = fmaf(gv[o], wv.z, ac[2]);
-              ac[3] = fmaf(gv[o], wv.w, ac[3]);
-            }
+          for (int oo = 0; oo < 4; ++oo) {
+            const float4 w4 = *reinterpret_cast<const float4*>(wt + (4 * o4 + oo) * 32);
+#pragma unroll
+            for (int i = 0; i < kV; ++i) fma4(acc[i], f4c(gv[i], oo), w4);
           }
         }
       }
     }
   }
-  float* xp = a.out + m * a.C + gb * 32;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    float4 r = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+  for (int i = 0; i < kV; ++i) {
+    if (!ok[i]) continue;
+    float* xp = a.out + m[i] * a.C + gb * 32 + 4 * q;
+    float4 r = acc[i];
     if (a.accumulate) {
-      const float4 q = *reinterpret_cast<const float4*>(xp + 4 * i);
-      r.x += q.x; r.y += q.y; r.z += q.z; r.w += q.w;
+      const float4 e = *reinterpret_cast<const float4*>(xp);
+      r.x += e.x; r.y += e.y; r.z += e.z; r.w += e.w;
     }
-    *reinterpret_cast<float4*>(xp + 4 * i) = r;
+    *reinterpret_cast<float4*>(xp) = r;
   }
 }
 
 // ------------------------------------------------------------------------------ wgrad
-// grid (chunks, K / 32, tap slices); ws[chunk][K][taps][CG] partials (or dw itself, one chunk)
-template <int CG, int TZ>  // TZ taps per slice
-__global__ void __launch_bounds__(kWgThreads) gconv_wgrad_kernel(GArgs a) {
+// grid (chunks, K / 32, tap slices); out = ws[chunk][K][taps][CG] partials (or dw, one chunk).
+// Per V-voxel tile: dy [V][32] and the TZ tap-shifted x tiles [TZ][V][32] are staged in
+// shared memory (one thread per (voxel, quad), coordinates decoded once per tile, the taps from
+// a table); then every thread accumulates its 4 x 4 (o, c) blocks over the tile's voxels. The
+// block index puts the input-channel quad fastest, so a warp's x reads are whole 128-byte rows.
+template <int CG, int TZ>
+__global__ void __launch_bounds__(kThreads) gconv_wgrad_kernel(GArgs a) {
   constexpr int NG = 32 / CG;
-  constexpr int NB4 = NG * TZ * (CG / 4) * (CG / 4);   // 4x4 (o, c) blocks of this CTA
-  constexpr int PER = (NB4 + kWgThreads - 1) / kWgThreads;
-  extern __shared__ __align__(16) float wsm[];   // dy tile [V][32], then x tiles [TZ][V][32]
-  float(*dys)[32] = reinterpret_cast<float(*)[32]>(wsm);
-  float(*xs)[kWgV][32] = reinterpret_cast<float(*)[kWgV][32]>(wsm + kWgV * 32);
+  constexpr int Q = CG / 4;
+  constexpr int NB4 = NG * TZ * Q * Q;
+  constexpr int PER = (NB4 + kThreads - 1) / kThreads;
+  constexpr int V = TZ > 9 ? 16 : 32;   // voxels per tile (smem: (1 + TZ) x V x 128 B)
+  extern __shared__ float4 smem4[];
+  float(*dys)[32] = reinterpret_cast<float(*)[32]>(smem4);
+  float(*xs)[V][32] = reinterpret_cast<float(*)[V][32]>(reinterpret_cast<float*>(smem4) + V * 32);
+  __shared__ int tap_uvt[TZ][3];
+  __shared__ int vox_c[V][3];
   const int taps = a.k * a.k * a.k;
   const int gb = blockIdx.y;
   const int tap0 = blockIdx.z * TZ;
+  if (threadIdx.x < TZ) {
+    const int tap = tap0 + threadIdx.x;
+    tap_uvt[threadIdx.x][0] = tap < taps ? tap / (a.k * a.k) : -1;
+    tap_uvt[threadIdx.x][1] = (tap / a.k) % a.k;
+    tap_uvt[threadIdx.x][2] = tap % a.k;
+  }
   const int64_t m0 = (int64_t)blockIdx.x * a.chunk, m1 = min(a.M, m0 + a.chunk);
   float acc[PER][16];
 #pragma unroll
   for (int p = 0; p < PER; ++p)
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[p][i] = 0.f;
-  for (int64_t mt = m0; mt < m1; mt += kWgV) {
-    // stage dy [V][32] and x [TZ][V][32] (zero outside the tile / the padding)
-    for (int i = threadIdx.x; i < kWgV * 8; i += kWgThreads) {
+  for (int64_t mt = m0; mt < m1; mt += V) {
+    if (threadIdx.x < V) {
+      const int64_t m = mt + threadIdx.x;
+      vox_c[threadIdx.x][0] = m < m1 ? (int)(m / ((int64_t)a.Wo * a.Ho)) * a.sd - a.pad : INT_MIN / 2;
+      vox_c[threadIdx.x][1] = (int)((m / a.Wo) % a.Ho) * a.s - a.pad;
+      vox_c[threadIdx.x][2] = (int)(m % a.Wo) * a.s - a.pad;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < V * 8; i += kThreads) {
       const int v = i >> 3, c4 = i & 7;
       const int64_t m = mt + v;
-      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < m1) q = ldg4(a.dy + m * a.K + gb * 32 + 4 * c4);
-      *reinterpret_cast<float4*>(&dys[v][4 * c4]) = q;
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m < m1) g = ldg4(a.dy + m * a.K + gb * 32 + 4 * c4);
+      *reinterpret_cast<float4*>(&dys[v][4 * c4]) = g;
     }
-    for (int i = threadIdx.x; i < TZ * kWgV * 8; i += kWgThreads) {
-      const int c4 = i & 7, v = (i >> 3) % kWgV, tz = i / (8 * kWgV);
-      const int tap = tap0 + tz;
-      const int64_t m = mt + v;
-      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < m1 && tap < taps) {
-        const int ow = (int)(m % a.Wo), oh = (int)((m / a.Wo) % a.Ho), od = (int)(m / ((int64_t)a.Wo * a.Ho));
-        const int u = tap / (a.k * a.k), vv = (tap / a.k) % a.k, t = tap % a.k;
-        const int zi = od * a.sd - a.pad + u, hi = oh * a.s - a.pad + vv, wi = ow * a.s - a.pad + t;
+    for (int i = threadIdx.x; i < TZ * V * 8; i += kThreads) {
+      const int c4 = i & 7, v = (i >> 3) % V, tz = i / (8 * V);
+      float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int u = tap_uvt[tz][0];
+      if (u >= 0) {
+        const int zi = vox_c[v][0] + u, hi = vox_c[v][1] + tap_uvt[tz][1], wi = vox_c[v][2] + tap_uvt[tz][2];
         if (zi >= 0 && zi < a.D && hi >= 0 && hi < a.H && wi >= 0 && wi < a.W)
-          q = ldg4(a.x + (((int64_t)zi * a.H + hi) * a.W + wi) * a.C + gb * 32 + 4 * c4);
+          xv = ldg4(a.x + (((int64_t)zi * a.H + hi) * a.W + wi) * a.C + gb * 32 + 4 * c4);
       }
-      *reinterpret_cast<float4*>(&xs[tz][v][4 * c4]) = q;
+      *reinterpret_cast<float4*>(&xs[tz][v][4 * c4]) = xv;
     }
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < PER; ++p) {
-      const int b = threadIdx.x + p * kWgThreads;
+      const int b = threadIdx.x + p * kThreads;
       if (b < NB4) {
-        // b -> (j, tz, o4, c4)
-        const int c4 = b % (CG / 4), o4 = (b / (CG / 4)) % (CG / 4), tz = (b / ((CG / 4) * (CG / 4))) % TZ,
-                  j = b / ((CG / 4) * (CG / 4) * TZ);
+        const int c4 = b % Q, o4 = (b / Q) % Q, j = (b / (Q * Q)) % NG, tz = b / (Q * Q * NG);
         const int oc = j * CG + 4 * o4, xc = j * CG + 4 * c4;
-#pragma unroll 8
-        for (int v = 0; v < kWgV; ++v) {
+#pragma unroll 4
+        for (int v = 0; v < V; ++v) {
           const float4 g = *reinterpret_cast<const float4*>(&dys[v][oc]);
           const float4 xv = *reinterpret_cast<const float4*>(&xs[tz][v][xc]);
-          const float ga[4] = {g.x, g.y, g.z, g.w}, xa[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
           for (int oo = 0; oo < 4; ++oo)
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) acc[p][oo * 4 + cc] = fmaf(ga[oo], xa[cc], acc[p][oo * 4 + cc]);
+            for (int cc = 0; cc < 4; ++cc)
+              acc[p][oo * 4 + cc] = fmaf(f4c(g, oo), f4c(xv, cc), acc[p][oo * 4 + cc]);
         }
       }
     }
@@ -287,10 +354,9 @@ __global__ void __launch_bounds__(kWgThreads) gconv_wgrad_kernel(GArgs a) {
   float* dst = a.out + (int64_t)blockIdx.x * a.K * taps * CG;
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
-    const int b = threadIdx.x + p * kWgThreads;
+    const int b = threadIdx.x + p * kThreads;
     if (b >= NB4) continue;
-    const int c4 = b % (CG / 4), o4 = (b / (CG / 4)) % (CG / 4), tz = (b / ((CG / 4) * (CG / 4))) % TZ,
-              j = b / ((CG / 4) * (CG / 4) * TZ);
+    const int c4 = b % Q, o4 = (b / Q) % Q, j = (b / (Q * Q)) % NG, tz = b / (Q * Q * NG);
     const int tap = tap0 + tz;
     if (tap >= taps) continue;
 #pragma unroll
@@ -328,20 +394,34 @@ int cg_of(const ConvGeom& g) { return g.C / g.groups; }
 // taps per wgrad slice: the CTA's 4x4 blocks (NG * TZ * (CG/4)^2) fit two per thread
 int wgrad_tz(int cg) { return cg == 32 ? 3 : (cg == 16 ? 9 : 27); }
 
+int wgrad_v(int cg) { return wgrad_tz(cg) > 9 ? 16 : 32; }
+
 int wgrad_chunks(const ConvGeom& g) {
   const int taps = g.R * g.R * g.R;
   const int tz = wgrad_tz(cg_of(g));
   const int per_chunk = (g.K / 32) * ((taps + tz - 1) / tz);
   const int64_t M = (int64_t)g.Do * g.Ho * g.Wo;
-  // ~2 waves of 148 SMs, at least 4 tiles of 32 voxels per chunk
-  int64_t ch = std::max<int64_t>(1, (2 * 148 + per_chunk - 1) / per_chunk);
-  ch = std::min<int64_t>(ch, std::max<int64_t>(1, M / (4 * kWgV)));
-  return (int)std::min<int64_t>(ch, 256);
+  // ~4 waves of 148 SMs, at least 8 tiles per chunk
+  int64_t ch = std::max<int64_t>(1, (4 * 148 + per_chunk - 1) / per_chunk);
+  ch = std::min<int64_t>(ch, std::max<int64_t>(1, M / (8 * wgrad_v(cg_of(g)))));
+  return (int)std::min<int64_t>(ch, 512);
 }
 
 template <typename Kern>
 pooch_status set_smem(Kern k, int bytes) {
   if (bytes > 48 * 1024) POOCH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return POOCH_OK;
+}
+
+template <int CG>
+pooch_status launch_dgrad(dim3 grid, int smem, cudaStream_t st, const GArgs& a, bool s2) {
+  if (s2) {
+    POOCH_CHECK(set_smem(gconv_dgrad_kernel<CG, true>, smem));
+    gconv_dgrad_kernel<CG, true><<<grid, kThreads, smem, st>>>(a);
+  } else {
+    POOCH_CHECK(set_smem(gconv_dgrad_kernel<CG, false>, smem));
+    gconv_dgrad_kernel<CG, false><<<grid, kThreads, smem, st>>>(a);
+  }
   return POOCH_OK;
 }
 
@@ -351,11 +431,11 @@ bool gconv_shape_ok(const ConvGeom& g) {
   const int cg = g.groups > 0 ? g.C / g.groups : 0;
   return g.is3d() && g.groups > 1 && g.C == g.K && g.C % g.groups == 0 &&
          (cg == 4 || cg == 8 || cg == 16 || cg == 32) && g.K % 32 == 0 && (g.R == 1 || g.R == 3) && g.R == g.S &&
-         g.stride >= 1 && g.stride <= 2 && g.sd() >= 1 && g.sd() <= 2 && g.N == 1;
+         g.stride >= 1 && g.stride <= 2 && g.sd() == g.stride && g.N == 1;
 }
 
 int gconv_stat_tiles(const ConvGeom& g) {
-  return (int)(((int64_t)g.Do * g.Ho * g.Wo + kFwdThreads - 1) / kFwdThreads);
+  return (int)(((int64_t)g.Do * g.Ho * g.Wo + kVoxBlk - 1) / kVoxBlk);
 }
 
 size_t gconv_wgrad_ws_bytes(const ConvGeom& g) {
@@ -375,10 +455,10 @@ pooch_status gconv_fwd(const ConvGeom& g, const float* x, const float* w, float*
   if (a.M == 0) return POOCH_OK;
   count_launch();
   switch (cg) {
-    case 4: POOCH_CHECK(set_smem(gconv_fwd_kernel<4>, smem)); gconv_fwd_kernel<4><<<grid, kFwdThreads, smem, st>>>(a); break;
-    case 8: POOCH_CHECK(set_smem(gconv_fwd_kernel<8>, smem)); gconv_fwd_kernel<8><<<grid, kFwdThreads, smem, st>>>(a); break;
-    case 16: POOCH_CHECK(set_smem(gconv_fwd_kernel<16>, smem)); gconv_fwd_kernel<16><<<grid, kFwdThreads, smem, st>>>(a); break;
-    case 32: POOCH_CHECK(set_smem(gconv_fwd_kernel<32>, smem)); gconv_fwd_kernel<32><<<grid, kFwdThreads, smem, st>>>(a); break;
+    case 4: POOCH_CHECK(set_smem(gconv_fwd_kernel<4>, smem)); gconv_fwd_kernel<4><<<grid, kThreads, smem, st>>>(a); break;
+    case 8: POOCH_CHECK(set_smem(gconv_fwd_kernel<8>, smem)); gconv_fwd_kernel<8><<<grid, kThreads, smem, st>>>(a); break;
+    case 16: POOCH_CHECK(set_smem(gconv_fwd_kernel<16>, smem)); gconv_fwd_kernel<16><<<grid, kThreads, smem, st>>>(a); break;
+    case 32: POOCH_CHECK(set_smem(gconv_fwd_kernel<32>, smem)); gconv_fwd_kernel<32><<<grid, kThreads, smem, st>>>(a); break;
   }
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -392,14 +472,15 @@ pooch_status gconv_dgrad(const ConvGeom& g, const float* dy, const float* w, flo
   const int taps = g.R * g.R * g.R, cg = cg_of(g);
   const int smem = 32 * taps * cg * (int)sizeof(float);
   const int64_t n_in = (int64_t)g.D * g.H * g.W;
-  dim3 grid((unsigned)((n_in + kFwdThreads - 1) / kFwdThreads), g.C / 32);
+  dim3 grid((unsigned)((n_in + kVoxBlk - 1) / kVoxBlk), g.C / 32);
+  const bool s2 = g.stride == 2;
   if (n_in == 0) return POOCH_OK;
   count_launch();
   switch (cg) {
-    case 4: POOCH_CHECK(set_smem(gconv_dgrad_kernel<4>, smem)); gconv_dgrad_kernel<4><<<grid, kFwdThreads, smem, st>>>(a); break;
-    case 8: POOCH_CHECK(set_smem(gconv_dgrad_kernel<8>, smem)); gconv_dgrad_kernel<8><<<grid, kFwdThreads, smem, st>>>(a); break;
-    case 16: POOCH_CHECK(set_smem(gconv_dgrad_kernel<16>, smem)); gconv_dgrad_kernel<16><<<grid, kFwdThreads, smem, st>>>(a); break;
-    case 32: POOCH_CHECK(set_smem(gconv_dgrad_kernel<32>, smem)); gconv_dgrad_kernel<32><<<grid, kFwdThreads, smem, st>>>(a); break;
+    case 4: POOCH_CHECK(launch_dgrad<4>(grid, smem, st, a, s2)); break;
+    case 8: POOCH_CHECK(launch_dgrad<8>(grid, smem, st, a, s2)); break;
+    case 16: POOCH_CHECK(launch_dgrad<16>(grid, smem, st, a, s2)); break;
+    case 32: POOCH_CHECK(launch_dgrad<32>(grid, smem, st, a, s2)); break;
   }
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -416,13 +497,13 @@ pooch_status gconv_wgrad(const ConvGeom& g, const float* x, const float* dy, flo
   a.chunk = (a.M + chunks - 1) / chunks;
   const int taps = g.R * g.R * g.R, cg = cg_of(g), tz = wgrad_tz(cg);
   dim3 grid(chunks, g.K / 32, (taps + tz - 1) / tz);
-  const int smem = (1 + tz) * kWgV * 32 * (int)sizeof(float);
+  const int smem = (1 + tz) * wgrad_v(cg) * 32 * (int)sizeof(float);
   count_launch();
   switch (cg) {
-    case 4: POOCH_CHECK(set_smem(gconv_wgrad_kernel<4, 27>, smem)); gconv_wgrad_kernel<4, 27><<<grid, kWgThreads, smem, st>>>(a); break;
-    case 8: POOCH_CHECK(set_smem(gconv_wgrad_kernel<8, 27>, smem)); gconv_wgrad_kernel<8, 27><<<grid, kWgThreads, smem, st>>>(a); break;
-    case 16: POOCH_CHECK(set_smem(gconv_wgrad_kernel<16, 9>, smem)); gconv_wgrad_kernel<16, 9><<<grid, kWgThreads, smem, st>>>(a); break;
-    case 32: POOCH_CHECK(set_smem(gconv_wgrad_kernel<32, 3>, smem)); gconv_wgrad_kernel<32, 3><<<grid, kWgThreads, smem, st>>>(a); break;
+    case 4: POOCH_CHECK(set_smem(gconv_wgrad_kernel<4, 27>, smem)); gconv_wgrad_kernel<4, 27><<<grid, kThreads, smem, st>>>(a); break;
+    case 8: POOCH_CHECK(set_smem(gconv_wgrad_kernel<8, 27>, smem)); gconv_wgrad_kernel<8, 27><<<grid, kThreads, smem, st>>>(a); break;
+    case 16: POOCH_CHECK(set_smem(gconv_wgrad_kernel<16, 9>, smem)); gconv_wgrad_kernel<16, 9><<<grid, kThreads, smem, st>>>(a); break;
+    case 32: POOCH_CHECK(set_smem(gconv_wgrad_kernel<32, 3>, smem)); gconv_wgrad_kernel<32, 3><<<grid, kThreads, smem, st>>>(a); break;
   }
   POOCH_CUDA(cudaGetLastError());
   if (chunks > 1) {
