@@ -283,12 +283,13 @@ extern "C" pooch_status pooch_div_bn_relu_bwd(const float* c_host, const float* 
   if (!c_host || !gy_host || !stats || !gamma || !dgamma || !dbeta || !gx_host || !ws || !streams || rows <= 0 ||
       C <= 0 || C % 4 || C > 2048 || row_floats % C)
     return fail(POOCH_EUSAGE, "divided BN-ReLU backward: bad arguments");
-  const size_t fixed = bn_bwd_ws_bytes(C) + (size_t)2 * C * 8 + (size_t)3 * C * 4 + 1024;
+  const int64_t pix_row = row_floats / C;
   auto need = [&](int64_t r) {
     const size_t s = (size_t)r * row_floats * 4;
-    return Carve::need({s, s, s, s, s, s, bn_bwd_ws_bytes(C), (size_t)2 * C * 8, (size_t)3 * C * 4});
+    return Carve::need({s, s, s, s, s, s, bn_relu_bwd_partial_ws_bytes(r * pix_row, C), (size_t)2 * C * 8,
+                        (size_t)3 * C * 4});
   };
-  int64_t r = std::min<int64_t>(rows, (int64_t)(ws_bytes > fixed ? (ws_bytes - fixed) / (6 * (size_t)row_floats * 4) : 0));
+  int64_t r = std::min<int64_t>(rows, (int64_t)(ws_bytes / (6 * (size_t)row_floats * 4)));
   while (r > 0 && need(r) > ws_bytes) --r;
   if (r <= 0) return fail(POOCH_EINFEASIBLE, "divided BN-ReLU backward: one row does not fit the workspace");
   Carve cv{static_cast<char*>(ws), ws_bytes};
@@ -296,7 +297,7 @@ extern "C" pooch_status pooch_div_bn_relu_bwd(const float* c_host, const float* 
   float* cin[2] = {(float*)cv.take(cf * 4), (float*)cv.take(cf * 4)};
   float* gin[2] = {(float*)cv.take(cf * 4), (float*)cv.take(cf * 4)};
   float* gout[2] = {(float*)cv.take(cf * 4), (float*)cv.take(cf * 4)};
-  float* bws = (float*)cv.take(bn_bwd_ws_bytes(C));
+  float* bws = (float*)cv.take(bn_relu_bwd_partial_ws_bytes(r * pix_row, C));
   double* acc = (double*)cv.take((size_t)2 * C * 8);
   float* coef = (float*)cv.take((size_t)3 * C * 4);
   BnBwdArgs a{};
@@ -356,13 +357,25 @@ static void dgrad_span(const ConvGeom& g, int a, int ri, int& o0, int& o1) {
   o1 = std::min(g.Do, (a + ri - 1 + p) / s + 1);
 }
 
+// the largest dy-row and dx-row counts any chunk of ri input rows needs (exact, over all chunks)
+static void dgrad_rows(const ConvGeom& g, int ri, int& dy_rows, int& dx_rows) {
+  dy_rows = 1;
+  dx_rows = ri;
+  for (int a = 0; a < g.D; a += ri) {
+    const int n = std::min(ri, g.D - a);
+    int o0, o1;
+    dgrad_span(g, a, n, o0, o1);
+    if (o1 <= o0) continue;
+    const int slab0 = o0 * g.sd() - g.pd(), dp = (o1 - o0 - 1) * g.sd() + g.R;
+    dy_rows = std::max(dy_rows, o1 - o0);
+    dx_rows = std::max(dx_rows, std::max(dp, (a - slab0) + n));
+  }
+}
+
 static size_t dgrad_need(const ConvGeom& g, int ri) {
-  int o0, o1;
-  // the widest span of any chunk start (interior chunks)
-  dgrad_span(g, g.D / 2, ri, o0, o1);
-  const int n_out = std::max(1, o1 - o0 + 2);
-  const size_t dy = (size_t)n_out * g.Ho * g.Wo * g.K * 4;
-  const size_t dx = (size_t)((n_out - 1) * g.sd() + g.R + ri) * g.H * g.W * g.C * 4;
+  int dyr, dxr;
+  dgrad_rows(g, ri, dyr, dxr);
+  const size_t dy = (size_t)dyr * g.Ho * g.Wo * g.K * 4, dx = (size_t)dxr * g.H * g.W * g.C * 4;
   return Carve::need({dy, dy, dx, dx});
 }
 
@@ -375,11 +388,10 @@ extern "C" pooch_status pooch_div_conv3d_dgrad(const pooch_conv_desc* d, const f
   int ri = g.D;
   while (ri > 0 && dgrad_need(g, ri) > ws_bytes) --ri;
   if (ri == 0) return fail(POOCH_EINFEASIBLE, "divided dgrad: one input row does not fit the workspace");
-  int o0, o1;
-  dgrad_span(g, g.D / 2, ri, o0, o1);
-  const int n_out_max = std::max(1, o1 - o0 + 2);
-  const size_t dy_f = (size_t)n_out_max * g.Ho * g.Wo * g.K;
-  const size_t dx_f = (size_t)((n_out_max - 1) * g.sd() + g.R + ri) * g.H * g.W * g.C;
+  int o0, o1, dyr, dxr;
+  dgrad_rows(g, ri, dyr, dxr);
+  const size_t dy_f = (size_t)dyr * g.Ho * g.Wo * g.K;
+  const size_t dx_f = (size_t)dxr * g.H * g.W * g.C;
   Carve cv{static_cast<char*>(ws), ws_bytes};
   float* dyb[2] = {(float*)cv.take(dy_f * 4), (float*)cv.take(dy_f * 4)};
   float* dxb[2] = {(float*)cv.take(dx_f * 4), (float*)cv.take(dx_f * 4)};

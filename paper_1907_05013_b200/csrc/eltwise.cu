@@ -788,6 +788,8 @@ __global__ void bn_finalize_sums_kernel(const double* __restrict__ acc, int C, d
 }
 }  // namespace
 
+size_t bn_relu_bwd_partial_ws_bytes(int64_t rows, int C) { return (size_t)2 * bwd_blocks(rows) * C * sizeof(float); }
+
 pooch_status bn_relu_bwd_partial(const BnBwdArgs& a, float* ws, double* acc, cudaStream_t st) {
   const int C = a.C, C4 = C / 4;
   if (a.mode != 0 || C % 4 || C > 2048) return fail(POOCH_EUSAGE, "divided BN-ReLU backward: mode 0, C %% 4 == 0, C <= 2048");

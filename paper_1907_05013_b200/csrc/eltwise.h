@@ -45,6 +45,7 @@ pooch_status bn_bwd(const BnBwdArgs& a, float* ws, cudaStream_t st);
 // accumulated into acc[2][C] (fp64, chunk order); finalize dbeta / dgamma / coef (3C floats) from
 // acc over total_rows; apply on a chunk. Forward: tile partials of a chunk's conv epilogue into
 // acc[2][C], then mean / invstd / scale / shift from acc (bn_finalize's formula).
+size_t bn_relu_bwd_partial_ws_bytes(int64_t rows, int C);   // ws of bn_relu_bwd_partial for `rows` rows
 pooch_status bn_relu_bwd_partial(const BnBwdArgs& a, float* ws, double* acc, cudaStream_t st);
 pooch_status bn_relu_bwd_finalize(const BnBwdArgs& a, const double* acc, int64_t total_rows, float* coef,
                                   cudaStream_t st);
