@@ -99,9 +99,11 @@ __global__ void __launch_bounds__(kThreads) gconv_fwd_kernel(GArgs a) {
   for (int i = 0; i < kV; ++i) {
     m[i] = (int64_t)blockIdx.x * kVoxBlk + warp * 16 + vs + 4 * i;
     ok[i] = m[i] < a.M;
-    ow[i] = (int)(m[i] % a.Wo);
-    oh[i] = (int)((m[i] / a.Wo) % a.Ho);
-    od[i] = (int)(m[i] / ((int64_t)a.Wo * a.Ho));
+    // voxel counts < 2^31 (gconv_shape_ok): 32-bit divisions
+    const unsigned mu = (unsigned)m[i], q1 = mu / (unsigned)a.Wo;
+    ow[i] = (int)(mu - q1 * (unsigned)a.Wo);
+    oh[i] = (int)(q1 % (unsigned)a.Ho);
+    od[i] = (int)(q1 / (unsigned)a.Ho);
   }
   float4 acc[kV];
 #pragma unroll
@@ -206,9 +208,10 @@ __global__ void __launch_bounds__(kThreads) gconv_dgrad_kernel(GArgs a) {
     m[i] = S2 ? (int64_t)blockIdx.x * kVoxBlk + (warp >> 1) * 32 + (warp & 1) + 2 * (vs + 4 * i)
               : (int64_t)blockIdx.x * kVoxBlk + warp * 16 + vs + 4 * i;
     ok[i] = m[i] < n_in;
-    wi[i] = (int)(m[i] % a.W);
-    hi[i] = (int)((m[i] / a.W) % a.H);
-    zi[i] = (int)(m[i] / ((int64_t)a.W * a.H));
+    const unsigned mu = (unsigned)m[i], q1 = mu / (unsigned)a.W;
+    wi[i] = (int)(mu - q1 * (unsigned)a.W);
+    hi[i] = (int)(q1 % (unsigned)a.H);
+    zi[i] = (int)(q1 / (unsigned)a.H);
   }
   float4 acc[kV];
 #pragma unroll
@@ -307,9 +310,10 @@ __global__ void __launch_bounds__(kThreads) gconv_wgrad_kernel(GArgs a) {
   for (int64_t mt = m0; mt < m1; mt += V) {
     if (threadIdx.x < V) {
       const int64_t m = mt + threadIdx.x;
-      vox_c[threadIdx.x][0] = m < m1 ? (int)(m / ((int64_t)a.Wo * a.Ho)) * a.sd - a.pad : INT_MIN / 2;
-      vox_c[threadIdx.x][1] = (int)((m / a.Wo) % a.Ho) * a.s - a.pad;
-      vox_c[threadIdx.x][2] = (int)(m % a.Wo) * a.s - a.pad;
+      const unsigned mu = (unsigned)m, q1 = mu / (unsigned)a.Wo;
+      vox_c[threadIdx.x][0] = m < m1 ? (int)(q1 / (unsigned)a.Ho) * a.sd - a.pad : INT_MIN / 2;
+      vox_c[threadIdx.x][1] = (int)(q1 % (unsigned)a.Ho) * a.s - a.pad;
+      vox_c[threadIdx.x][2] = (int)(mu - q1 * (unsigned)a.Wo) * a.s - a.pad;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < V * 8; i += kThreads) {
@@ -368,6 +372,66 @@ __global__ void __launch_bounds__(kThreads) gconv_wgrad_kernel(GArgs a) {
   }
 }
 
+// wgrad for narrow groups (Cg = 4, 8; 3^3 taps): a staged x tile would be consumed by exactly one
+// (or two) threads, so each thread -- one (tap, group, o quad, c quad) 4 x 4 block of dw -- streams
+// its own tap-shifted x rows and the dy rows straight from L1 / L2 over the block's voxel chunk:
+// a warp (4 taps x 8 channel quads, Cg = 4) reads one 128-byte dy row and four 128-byte x rows per
+// voxel for 16 FMAs each, with no shared memory and no barriers.
+template <int CG>
+__global__ void __launch_bounds__(CG == 4 ? 224 : 448) gconv_wgrad_direct_kernel(GArgs a) {
+  constexpr int NG = 32 / CG, Q = CG / 4, NB = NG * 27 * Q * Q;
+  const int b = threadIdx.x;
+  if (b >= NB) return;
+  const int c4 = b % Q, o4 = (b / Q) % Q, j = (b / (Q * Q)) % NG, tap = b / (Q * Q * NG);
+  const int u = tap / 9, v = (tap / 3) % 3, t = tap % 3;
+  const int gb = blockIdx.y;
+  const int oc = gb * 32 + j * CG + 4 * o4, xc = gb * 32 + j * CG + 4 * c4;
+  const int64_t m0 = (int64_t)blockIdx.x * a.chunk, m1 = min(a.M, m0 + a.chunk);
+  float acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+  if (m0 < m1) {
+    const unsigned q1 = (unsigned)m0 / (unsigned)a.Wo;
+    int ow = (int)((unsigned)m0 - q1 * (unsigned)a.Wo), oh = (int)(q1 % (unsigned)a.Ho), od = (int)(q1 / (unsigned)a.Ho);
+    int zi = od * a.sd - a.pad + u, hi = oh * a.s - a.pad + v;
+    bool rv = zi >= 0 && zi < a.D && hi >= 0 && hi < a.H;
+    const float* xrow = a.x + ((int64_t)(rv ? zi : 0) * a.H + (rv ? hi : 0)) * a.W * a.C + xc;
+    const float* gp = a.dy + m0 * a.K + oc;
+#pragma unroll 4
+    for (int64_t m = m0; m < m1; ++m) {
+      const int wi = ow * a.s - a.pad + t;
+      const bool ok = rv && wi >= 0 && wi < a.W;
+      const float4 g = ldg4(gp);
+      const float4 xr = ldg4(xrow + (int64_t)(ok ? wi : 0) * a.C);
+      const float4 xv = ok ? xr : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float ga[4] = {g.x, g.y, g.z, g.w}, xa[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int oo = 0; oo < 4; ++oo)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) acc[oo * 4 + cc] = fmaf(ga[oo], xa[cc], acc[oo * 4 + cc]);
+      gp += a.K;
+      if (++ow == a.Wo) {   // next output row: new input row for this tap
+        ow = 0;
+        if (++oh == a.Ho) {
+          oh = 0;
+          ++od;
+        }
+        zi = od * a.sd - a.pad + u;
+        hi = oh * a.s - a.pad + v;
+        rv = zi >= 0 && zi < a.D && hi >= 0 && hi < a.H;
+        xrow = a.x + ((int64_t)(rv ? zi : 0) * a.H + (rv ? hi : 0)) * a.W * a.C + xc;
+      }
+    }
+  }
+  float* dst = a.out + (int64_t)blockIdx.x * a.K * 27 * CG;
+#pragma unroll
+  for (int oo = 0; oo < 4; ++oo) {
+    const int o = gb * 32 + j * CG + 4 * o4 + oo;
+    *reinterpret_cast<float4*>(dst + ((int64_t)o * 27 + tap) * CG + 4 * c4) =
+        make_float4(acc[oo * 4], acc[oo * 4 + 1], acc[oo * 4 + 2], acc[oo * 4 + 3]);
+  }
+}
+
 __global__ void gconv_chunk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ dw, int64_t n4,
                                           int chunks) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -396,10 +460,12 @@ int wgrad_tz(int cg) { return cg == 32 ? 3 : (cg == 16 ? 9 : 27); }
 
 int wgrad_v(int cg) { return wgrad_tz(cg) > 9 ? 16 : 32; }
 
+bool wgrad_direct(const ConvGeom& g) { return g.R == 3 && cg_of(g) == 4; }   // Cg = 8: the staged tile (measured faster)
+
 int wgrad_chunks(const ConvGeom& g) {
   const int taps = g.R * g.R * g.R;
   const int tz = wgrad_tz(cg_of(g));
-  const int per_chunk = (g.K / 32) * ((taps + tz - 1) / tz);
+  const int per_chunk = (g.K / 32) * (wgrad_direct(g) ? 1 : (taps + tz - 1) / tz);
   const int64_t M = (int64_t)g.Do * g.Ho * g.Wo;
   // ~4 waves of 148 SMs, at least 8 tiles per chunk
   int64_t ch = std::max<int64_t>(1, (4 * 148 + per_chunk - 1) / per_chunk);
@@ -430,6 +496,7 @@ pooch_status launch_dgrad(dim3 grid, int smem, cudaStream_t st, const GArgs& a, 
 bool gconv_shape_ok(const ConvGeom& g) {
   const int cg = g.groups > 0 ? g.C / g.groups : 0;
   return g.is3d() && g.groups > 1 && g.C == g.K && g.C % g.groups == 0 &&
+         (int64_t)g.D * g.H * g.W < (1ll << 31) && (int64_t)g.Do * g.Ho * g.Wo < (1ll << 31) &&
          (cg == 4 || cg == 8 || cg == 16 || cg == 32) && g.K % 32 == 0 && (g.R == 1 || g.R == 3) && g.R == g.S &&
          g.stride >= 1 && g.stride <= 2 && g.sd() == g.stride && g.N == 1;
 }
@@ -499,7 +566,13 @@ pooch_status gconv_wgrad(const ConvGeom& g, const float* x, const float* dy, flo
   dim3 grid(chunks, g.K / 32, (taps + tz - 1) / tz);
   const int smem = (1 + tz) * wgrad_v(cg) * 32 * (int)sizeof(float);
   count_launch();
-  switch (cg) {
+  if (wgrad_direct(g)) {
+    grid.z = 1;
+    if (cg == 4)
+      gconv_wgrad_direct_kernel<4><<<grid, 224, 0, st>>>(a);
+    else
+      gconv_wgrad_direct_kernel<8><<<grid, 448, 0, st>>>(a);
+  } else switch (cg) {
     case 4: POOCH_CHECK(set_smem(gconv_wgrad_kernel<4, 27>, smem)); gconv_wgrad_kernel<4, 27><<<grid, kThreads, smem, st>>>(a); break;
     case 8: POOCH_CHECK(set_smem(gconv_wgrad_kernel<8, 27>, smem)); gconv_wgrad_kernel<8, 27><<<grid, kThreads, smem, st>>>(a); break;
     case 16: POOCH_CHECK(set_smem(gconv_wgrad_kernel<16, 9>, smem)); gconv_wgrad_kernel<16, 9><<<grid, kThreads, smem, st>>>(a); break;

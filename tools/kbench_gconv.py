@@ -34,7 +34,11 @@ def clock_mhz():
         return 1965.0
 
 
-def timeit(fn, reps=10):
+REPS = int(os.environ.get("POOCH_KB_REPS", "10"))
+PICK = [int(v) for v in os.environ.get("POOCH_KB_SHAPES", "").split(",") if v]
+
+
+def timeit(fn, reps=REPS):
     fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -50,7 +54,9 @@ def main():
     lib = _lib
     peak = 148 * 128 * 2 * clock_mhz() * 1e6 / 1e12
     rows = []
-    for name, D, H, W, Cc, s in SHAPES:
+    for si, (name, D, H, W, Cc, s) in enumerate(SHAPES):
+        if PICK and si not in PICK:
+            continue
         d = lib.ConvDesc(1, H, W, Cc, Cc, 3, 3, s, 1, 1, D, 0, 32, 0)
         Do, Ho, Wo = (D - 1) // s + 1, (H - 1) // s + 1, (W - 1) // s + 1
         x = torch.randn(D * H * W * Cc, device="cuda")
