@@ -386,22 +386,23 @@ __global__ void __launch_bounds__(CG == 4 ? 224 : 448) gconv_wgrad_direct_kernel
   const int u = tap / 9, v = (tap / 3) % 3, t = tap % 3;
   const int gb = blockIdx.y;
   const int oc = gb * 32 + j * CG + 4 * o4, xc = gb * 32 + j * CG + 4 * c4;
-  const int64_t m0 = (int64_t)blockIdx.x * a.chunk, m1 = min(a.M, m0 + a.chunk);
+  // this block's output rows (od, oh) [r0, r1): a.chunk rows each
+  const int64_t rows = (int64_t)a.Do * a.Ho;
+  const int64_t r0 = (int64_t)blockIdx.x * a.chunk, r1 = min(rows, r0 + a.chunk);
   float acc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-  if (m0 < m1) {
-    const unsigned q1 = (unsigned)m0 / (unsigned)a.Wo;
-    int ow = (int)((unsigned)m0 - q1 * (unsigned)a.Wo), oh = (int)(q1 % (unsigned)a.Ho), od = (int)(q1 / (unsigned)a.Ho);
-    int zi = od * a.sd - a.pad + u, hi = oh * a.s - a.pad + v;
-    bool rv = zi >= 0 && zi < a.D && hi >= 0 && hi < a.H;
-    const float* xrow = a.x + ((int64_t)(rv ? zi : 0) * a.H + (rv ? hi : 0)) * a.W * a.C + xc;
-    const float* gp = a.dy + m0 * a.K + oc;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int od = (int)(r / a.Ho), oh = (int)(r - (int64_t)od * a.Ho);
+    const int zi = od * a.sd - a.pad + u, hi = oh * a.s - a.pad + v;
+    if (zi < 0 || zi >= a.D || hi < 0 || hi >= a.H) continue;   // this tap reads padding: no term
+    const float* xrow = a.x + ((int64_t)zi * a.H + hi) * a.W * a.C + xc;
+    const float* gp = a.dy + r * a.Wo * a.K + oc;
 #pragma unroll 4
-    for (int64_t m = m0; m < m1; ++m) {
+    for (int ow = 0; ow < a.Wo; ++ow) {
       const int wi = ow * a.s - a.pad + t;
-      const bool ok = rv && wi >= 0 && wi < a.W;
-      const float4 g = ldg4(gp);
+      const bool ok = wi >= 0 && wi < a.W;
+      const float4 g = ldg4(gp + (int64_t)ow * a.K);
       const float4 xr = ldg4(xrow + (int64_t)(ok ? wi : 0) * a.C);
       const float4 xv = ok ? xr : make_float4(0.f, 0.f, 0.f, 0.f);
       const float ga[4] = {g.x, g.y, g.z, g.w}, xa[4] = {xv.x, xv.y, xv.z, xv.w};
@@ -409,18 +410,6 @@ __global__ void __launch_bounds__(CG == 4 ? 224 : 448) gconv_wgrad_direct_kernel
       for (int oo = 0; oo < 4; ++oo)
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) acc[oo * 4 + cc] = fmaf(ga[oo], xa[cc], acc[oo * 4 + cc]);
-      gp += a.K;
-      if (++ow == a.Wo) {   // next output row: new input row for this tap
-        ow = 0;
-        if (++oh == a.Ho) {
-          oh = 0;
-          ++od;
-        }
-        zi = od * a.sd - a.pad + u;
-        hi = oh * a.s - a.pad + v;
-        rv = zi >= 0 && zi < a.D && hi >= 0 && hi < a.H;
-        xrow = a.x + ((int64_t)(rv ? zi : 0) * a.H + (rv ? hi : 0)) * a.W * a.C + xc;
-      }
     }
   }
   float* dst = a.out + (int64_t)blockIdx.x * a.K * 27 * CG;
@@ -470,6 +459,7 @@ int wgrad_chunks(const ConvGeom& g) {
   // ~4 waves of 148 SMs, at least 8 tiles per chunk
   int64_t ch = std::max<int64_t>(1, (4 * 148 + per_chunk - 1) / per_chunk);
   ch = std::min<int64_t>(ch, std::max<int64_t>(1, M / (8 * wgrad_v(cg_of(g)))));
+  if (wgrad_direct(g)) ch = std::min<int64_t>(ch, (int64_t)g.Do * g.Ho);   // whole rows per chunk
   return (int)std::min<int64_t>(ch, 512);
 }
 
@@ -561,7 +551,8 @@ pooch_status gconv_wgrad(const ConvGeom& g, const float* x, const float* dy, flo
     return fail(POOCH_EUSAGE, "grouped wgrad workspace too small: %zu < %zu", ws_bytes, gconv_wgrad_ws_bytes(g));
   GArgs a = gargs(g);
   a.x = x; a.dy = dy; a.out = chunks > 1 ? ws : dw;
-  a.chunk = (a.M + chunks - 1) / chunks;
+  // voxels per chunk; the direct kernel takes whole output rows (od, oh) per chunk
+  a.chunk = wgrad_direct(g) ? ((int64_t)g.Do * g.Ho + chunks - 1) / chunks : (a.M + chunks - 1) / chunks;
   const int taps = g.R * g.R * g.R, cg = cg_of(g), tz = wgrad_tz(cg);
   dim3 grid(chunks, g.K / 32, (taps + tz - 1) / tz);
   const int smem = (1 + tz) * wgrad_v(cg) * 32 * (int)sizeof(float);
