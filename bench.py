@@ -779,14 +779,22 @@ def tensor_peak(pk, precision):
     return pk["tf32_tflops_sustained"] * 1e12 / (3.0 if precision else 1.0)
 
 
+def alu_peak():
+    """FP32 FMA roof of the CUDA cores (grouped conv3d, DESIGN.md Reading 47): 148 SMs x 128 FMA
+    lanes x 2 flop x the SM clock (the boost clock, 1.965 GHz; B200_PROFILING.md unit counts)."""
+    return 148 * 128 * 2 * 1.965e9
+
+
 def seg_roof(segs, pk, precision):
-    """Per family: sum of launch times, of per-launch roofline times max(F / P_tensor, B / BW),
-    and of the time in launches whose binding roof is the tensor pipe."""
-    P, BW = tensor_peak(pk, precision), pk["hbm_gbs"] * 1e9
+    """Per family: sum of launch times, of per-launch roofline times max(F / P, B / BW) -- P the
+    tensor roof, or the ALU roof for the grouped-conv families -- and of the time in launches
+    whose binding roof is the compute pipe."""
+    BW = pk["hbm_gbs"] * 1e9
     out = {}
     for f, ms, fl, by in segs:
         if f in ("other", "stall", "swap_out", "swap_in", "allreduce") or ms <= 0:
             continue
+        P = alu_peak() if f.startswith("gconv") else tensor_peak(pk, precision)
         e = out.setdefault(f, {"t": 0.0, "bound": 0.0, "t_tensor": 0.0, "flops": 0.0, "bytes": 0.0})
         t = ms / 1e3
         tt, tb = fl / P, by / BW
@@ -810,6 +818,12 @@ def roofline(fam, pk, segs=None, precision=1, workload=""):
     P = tensor_peak(pk, precision)
     src = pk["src"] + " bf16 sustained x (1.1/2.25) nominal tf32 ratio" + (" / 3 (3xTF32)" if precision else "")
     launches = fam[k]["launches"] if k in fam else None
+    if tensor and k.startswith("gconv"):
+        ach = e["flops"] / e["t"] / 1e12
+        return {"kernel": k, "bound": "alu", "achieved": ach, "peak": alu_peak() / 1e12, "unit": "TFLOP/s",
+                "frac": ach / (alu_peak() / 1e12), "roofline_time_frac": e["bound"] / e["t"],
+                "traffic": traffic_for(k, workload), "launches": launches,
+                "peak_src": "148 SMs x 128 FP32 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md unit counts)"}
     if tensor:
         ach = e["flops"] / e["t"] / 1e12
         return {"kernel": k, "bound": "tensor", "achieved": ach, "peak": P / 1e12, "unit": "TFLOP/s",
@@ -840,8 +854,10 @@ def families_table(fam, pk, segs=None, precision=1):
         if k in sr:
             r = sr[k]
             tensor = r["t_tensor"] >= 0.5 * r["t"]
-            e["bound"] = "tensor" if tensor else "hbm"
-            e["frac"] = round((r["flops"] / r["t"] / P) if tensor else (r["bytes"] / r["t"] / bw), 4)
+            alu = k.startswith("gconv")
+            e["bound"] = ("alu" if alu else "tensor") if tensor else "hbm"
+            Pk = alu_peak() if alu else P
+            e["frac"] = round((r["flops"] / r["t"] / Pk) if tensor else (r["bytes"] / r["t"] / bw), 4)
             e["roofline_time_frac"] = round(r["bound"] / r["t"], 4)
         out[k] = e
     return out

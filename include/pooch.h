@@ -409,7 +409,8 @@ pooch_status pooch_kernel_launches(pooch_ctx* ctx, int64_t* per_step);
 
 /* Kernel-family accounting of the last instrumented step: for family f (0 conv-fwd,
  * 1 conv-dgrad, 2 conv-wgrad, 3 bn-fwd, 4 bn-bwd, 5 pool, 6 fc/ce, 7 sgd, 8 swap-out,
- * 9 swap-in, 10 allreduce, 11 other, 12 compute-stream stall waiting on a copy stream) the summed event time, launch count, algorithmic flops and
+ * 9 swap-in, 10 allreduce, 11 other, 12 compute-stream stall waiting on a copy stream, 13-15 grouped
+ * conv3d fwd / dgrad / wgrad on the CUDA cores) the summed event time, launch count, algorithmic flops and
  * algorithmic DRAM bytes. */
 pooch_status pooch_family_stats(pooch_ctx* ctx, int32_t family, double* time_ms, int64_t* launches,
                                 double* flops, double* bytes);

@@ -16,7 +16,9 @@ namespace pooch {
 
 enum Family {
   FAM_CONV_FWD = 0, FAM_CONV_DGRAD, FAM_CONV_WGRAD, FAM_BN_FWD, FAM_BN_BWD, FAM_POOL, FAM_FC_CE, FAM_SGD,
-  FAM_SWAP_OUT, FAM_SWAP_IN, FAM_ALLREDUCE, FAM_OTHER, FAM_STALL, FAM_COUNT
+  FAM_SWAP_OUT, FAM_SWAP_IN, FAM_ALLREDUCE, FAM_OTHER, FAM_STALL,
+  FAM_GCONV_FWD, FAM_GCONV_DGRAD, FAM_GCONV_WGRAD,  // grouped conv3d on the CUDA cores (ALU roof)
+  FAM_COUNT
 };
 
 struct ParamT {

@@ -239,12 +239,13 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
       const double din = G.is3d() ? G.D : 1.0;
       double xb = 4.0 * G.N * din * G.H * G.W * G.C, yb = 4.0 * R.rows * G.K,
              wb = 4.0 * G.K * G.T() * G.R * G.S * G.C;
-      if (mark) mark(c, FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
+      const bool grp = G.groups > 1;
+      if (mark) mark(c, grp ? FAM_GCONV_WGRAD : FAM_CONV_WGRAD, t, R.flops, xb + yb + wb);
       POOCH_CHECK(launch_conv_wgrad(G, p.in0 ? p.in0 : reinterpret_cast<const float*>(c->dev + c->off_x), p.gy,
                                     pg(c, R.w), reinterpret_cast<float*>(c->dev + c->off_wgws), c->wgws_bytes, st,
                                     p.in1));
       if (T.in0 >= 0) {
-        if (mark) mark(c, FAM_CONV_DGRAD, t, R.flops, yb + xb * (p.acc0 ? 2 : 1) + wb);
+        if (mark) mark(c, grp ? FAM_GCONV_DGRAD : FAM_CONV_DGRAD, t, R.flops, yb + xb * (p.acc0 ? 2 : 1) + wb);
         // grouped convs read their weights untransposed (gconv.cu)
         const float* wt = G.groups > 1 ? pw(c, R.w) : fptr(c, c->off_wt) + R.wt_off;
         POOCH_CHECK(launch_conv_dgrad(G, p.gy, wt, p.g0, p.acc0, st, p.g1, p.acc1));
@@ -364,6 +365,11 @@ pooch_status run_bwd(pooch_ctx* c, int t, const BwdPtrs& p, MarkFn mark) {
     }
   }
   return fail(POOCH_EUSAGE, "bad task kind");
+}
+
+int fam_fwd(int kind);
+int fam_fwd_task(pooch_ctx* c, int t) {
+  return c->rt[t].geom.groups > 1 ? FAM_GCONV_FWD : fam_fwd(c->g.t[t].kind);
 }
 
 int fam_fwd(int kind) {
@@ -1672,11 +1678,11 @@ static pooch_status run_op(pooch_ctx* c, const Op& o, bool timing) {
   const int n = c->g.n();
   switch (o.kind) {
     case 'F':
-      if (timing) mark_seg(c, fam_fwd(c->g.t[o.id].kind), o.id,
+      if (timing) mark_seg(c, fam_fwd_task(c, o.id), o.id,
                            c->rt[o.id].is_conv ? c->rt[o.id].flops : 0, fwd_bytes(c, o.id));
       return run_fwd(c, o.id, fwd_ptrs(c, o.id, false), true);
     case 'R':
-      if (timing) mark_seg(c, fam_fwd(c->g.t[o.id].kind), o.id,
+      if (timing) mark_seg(c, fam_fwd_task(c, o.id), o.id,
                            c->rt[o.id].is_conv ? c->rt[o.id].flops : 0, fwd_bytes(c, o.id));
       return run_fwd(c, o.id, fwd_ptrs(c, o.id, true), false);
     case 'B':

@@ -18,7 +18,7 @@ NETS = {"tiny": 0, "resnet50": 1, "resnet50v1": 2, "unet3d": 3, "alexnet": 4, "r
 KINDS = ["conv", "bnrelu", "tail_proj", "tail_id", "maxpool", "avgpool", "fc_ce", "upconv", "head_ce", "bnrelu_conv",
          "conv_relu", "lrn", "fc_relu_drop"]
 FAMILIES = ["conv_fwd", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd", "pool", "fc_ce", "sgd",
-            "swap_out", "swap_in", "allreduce", "other", "stall"]
+            "swap_out", "swap_in", "allreduce", "other", "stall", "gconv_fwd", "gconv_dgrad", "gconv_wgrad"]
 
 
 FUSE_BNRELU = 16   # POOCH_NET_FUSE_BNRELU: BN-ReLU on the consuming conv's operand load
