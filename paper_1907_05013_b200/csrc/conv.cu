@@ -49,7 +49,7 @@ bool conv_shape_ok(const ConvGeom& g) {
 
 static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
-template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false>
+template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false, bool MNW = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr,
                                  const CUtensorMap* td = nullptr) {
@@ -67,8 +67,8 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT, NSTG>::TOTAL;
   // TMA wgrad at BN = 64 (3xTF32): six blocks of 32x32 per stage -> six auxiliary warps, one
   // block each, instead of four warps doing one or two (the transposes bound these layers)
-  constexpr int NAUX = (MODE == CONV_WGRAD && TMA && X3 && BN == 64 && !AT && !XF) ? 6 : 4;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX>;
+  constexpr int NAUX = (MODE == CONV_WGRAD && TMA && X3 && BN == 64 && !AT && !XF && !MNW) ? 6 : 4;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX, MNW>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -83,6 +83,12 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
                                                           tc ? *tc : g_zero_map, td ? *td : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
+}
+
+// TMA wgrad with MN-major operands, no transposes (POOCH_WGRAD_MN=0: the transposing kernels)
+static bool mn_wgrad() {
+  static int on = getenv("POOCH_WGRAD_MN") ? atoi(getenv("POOCH_WGRAD_MN")) : 1;
+  return on != 0;
 }
 
 // 3xTF32 TMA fwd / dgrad with the A operand in TMEM (POOCH_A_TMEM=0 disables)
@@ -185,16 +191,18 @@ static bool map_act(CUtensorMap* m, const float* base, int N3, int H, int W, int
 // outermost, stride 128 B); box {32, tw*st, th*st, tn*st3, cb} lands as cb consecutive
 // [pixel][32] blocks.
 static bool map_act_chunks(CUtensorMap* m, const float* base, int N3, int H, int W, int C, int tw, int th, int tn,
-                           int st, int st3, int cb) {
+                           int st, int st3, int cb, bool mn = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[5] = {32, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N3, (cuuint64_t)(C / 32)};
   cuuint64_t strides[4] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4, 128};
   cuuint32_t box[5] = {32, (cuuint32_t)(tw * st), (cuuint32_t)(th * st), (cuuint32_t)(tn * st3), (cuuint32_t)cb};
   cuuint32_t es[5] = {1, (cuuint32_t)st, (cuuint32_t)st, (cuuint32_t)st3, 1};
+  // mn: the MN-major tf32 operand layout of the transpose-free wgrad (128-B rows swizzled in
+  // 32-B atoms; igemm.cuh MNW), else SWIZZLE_128B for the in-place transposes
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
+            mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // 2-D row-major matrix [rows][cols]: box {32 cols, bn rows}
@@ -643,18 +651,33 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
     p.wg_cba = w.swap ? cb_x : cb_dy;
     p.wg_cbb = w.swap ? cb_dy : cb_x;
     const int c0 = g.C1 > 0 ? g.C1 : g.C;
+    // transpose-free MN-major operands (igemm.cuh MNW) unless BN-ReLU-on-load rewrites them
+    const bool mn = mn_wgrad() && !p.xf_scale;
     CUtensorMap tdy, tx, tx1;
-    if (!map_act_chunks(&tdy, dy, out3(g), g.Ho, g.Wo, g.K, w.box.tw, w.box.th, w.box.tn, 1, 1, cb_dy) ||
-        !map_act_chunks(&tx, x, in3(g), g.H, g.W, c0, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x))
+    if (!map_act_chunks(&tdy, dy, out3(g), g.Ho, g.Wo, g.K, w.box.tw, w.box.th, w.box.tn, 1, 1, cb_dy, mn) ||
+        !map_act_chunks(&tx, x, in3(g), g.H, g.W, c0, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x, mn))
       return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv wgrad)");
     if (g.C1 > 0) {
       p.c_split = g.C1;
-      if (!map_act_chunks(&tx1, x1, in3(g), g.H, g.W, g.C - g.C1, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x))
+      if (!map_act_chunks(&tx1, x1, in3(g), g.H, g.W, g.C - g.C1, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x,
+                          mn))
         return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv wgrad, second source)");
     }
     const CUtensorMap* ta = w.swap ? &tx : &tdy;
     const CUtensorMap* tb = w.swap ? &tdy : &tx;
-    POOCH_CHECK((launch_bn<CONV_WGRAD, true>(w.bn, p, grid, st, g.prec, ta, tb, g.C1 > 0 ? &tx1 : nullptr)));
+    const CUtensorMap* tc = g.C1 > 0 ? &tx1 : nullptr;
+    if (mn) {
+      if (g.prec) {
+        if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
+        else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
+      } else {
+        if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, false, true, false, false, true>(p, grid, st, ta, tb, tc)));
+        else if (w.bn == 128) POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, false, true, false, false, true>(p, grid, st, ta, tb, tc)));
+        else POOCH_CHECK((launch_igemm<CONV_WGRAD, 256, false, true, false, false, true>(p, grid, st, ta, tb, tc)));
+      }
+    } else {
+      POOCH_CHECK((launch_bn<CONV_WGRAD, true>(w.bn, p, grid, st, g.prec, ta, tb, tc)));
+    }
   } else if (g.is3d() || g.C1 > 0) {
     return fail(POOCH_EUSAGE, "3D / two-source conv needs the TMA path");
   } else if (g.prec) {

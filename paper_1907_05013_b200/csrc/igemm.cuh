@@ -497,7 +497,7 @@ struct TileMap {
 };
 
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false,
-          int NSTG = 1, int NAUX = 4>
+          int NSTG = 1, int NAUX = 4, bool MNW = false>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
@@ -507,6 +507,11 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
   static_assert(!XF || (TMA && (MODE == CONV_FWD || MODE == CONV_WGRAD)), "XF: TMA-fed fwd / wgrad only");
   // NAUX > 4 auxiliary warps: only the TMA wgrad block loop distributes over them
   static_assert(NAUX == 4 || (MODE == CONV_WGRAD && TMA && !AT && !XF), "NAUX: TMA wgrad only");
+  // MNW: TMA wgrad with both operands MN-major in shared memory -- the boxes land as [pixel][32
+  // channels] rows in the SWIZZLE_128B_ATOM_32B layout, the only MN-major layout tcgen05 accepts
+  // for tf32 (layout type SWIZZLE_128B_BASE32B), so no transposes:
+  // the auxiliary warps only write the 3xTF32 residuals
+  static_assert(!MNW || (MODE == CONV_WGRAD && TMA && !AT && !XF && NAUX == 4), "MNW: plain TMA wgrad");
   // AT: 3xTF32 with the A operand in TMEM -- the auxiliary warps move each stage's A tile (hi =
   // trunc_tf32(a), lo = a - hi) from shared memory into TMEM, so the three MMAs of a k-step read
   // only B / Bs from shared memory (A is re-read by every MMA, the dominant smem traffic at BN = 64)
@@ -817,7 +822,15 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
         }
         ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
-        if constexpr (MODE == CONV_WGRAD && TMA && AT) {
+        if constexpr (MNW) {
+          // MN-major operands: the residual of every element at the same offset + SMALL_OFF (the
+          // layout is the same for both, so no index arithmetic)
+          if constexpr (X3) {
+            constexpr int CHUNKS = (BM + BN) * BK / 4;
+#pragma unroll 4
+            for (int c = stid; c < CHUNKS; c += 128) split_chunk(st + c * 16, st + SM::SMALL_OFF + c * 16);
+          }
+        } else if constexpr (MODE == CONV_WGRAD && TMA && AT) {
           // A in TMEM: warp w owns A block w & 3 (its TMEM lane quadrant): transpose it in place,
           // read its rows back (lane = row) and store hi / lo into this stage's TMEM columns; the B
           // blocks are transposed with their residuals into [B][Bs] as usual
@@ -964,6 +977,27 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
           uint32_t sa = sbase + s * SM::STAGE_BYTES;
           uint32_t sb = sa + SM::A_BYTES;
           const bool sw = TMA && !p.stem4;  // SWIZZLE_128B tiles, else the SWIZZLE_NONE core-matrix layout
+          if constexpr (MNW) {
+            // MN-major SWIZZLE_128B_BASE32B: a 4 KB block per 32 rows of A / B (LBO = 4096 between
+            // them), pixel rows of 128 B, 4-row K groups 512 B apart (SBO); a k-step of 8 pixels
+            // advances 8 rows = 1024 B
+            constexpr uint32_t IDESC_MN = ptx::idesc_tf32(BM, BN, true, true);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t ko = kk * 1024;
+              const uint64_t ad = ptx::smem_desc(sa + ko, 4096, 512, 1);
+              const uint64_t bd = ptx::smem_desc(sb + ko, 4096, 512, 1);
+              if constexpr (X3) {
+                const uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + ko, 4096, 512, 1);
+                const uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + ko, 4096, 512, 1);
+                ptx::mma_tf32(acc, asd, bd, IDESC_MN, (kb | kk) != 0 ? 1u : 0u);
+                ptx::mma_tf32(acc, ad, bsd, IDESC_MN, 1u);
+                ptx::mma_tf32(acc, ad, bd, IDESC_MN, 1u);
+              } else {
+                ptx::mma_tf32(acc, ad, bd, IDESC_MN, (kb | kk) != 0 ? 1u : 0u);
+              }
+            }
+          } else {
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             // SWIZZLE_NONE (cp.async / stem tiles): k-step = 2 core matrices; SWIZZLE_128B (TMA tiles):
@@ -989,6 +1023,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
               ptx::mma_tf32(acc, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
             }
           }
+          }  // MNW
           ptx::mma_commit(&empty[s]);
         }
         __syncwarp();
