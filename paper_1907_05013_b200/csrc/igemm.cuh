@@ -20,13 +20,15 @@
 //   CONV_DGRAD: A = dy gathered by the transposed-conv rule [M=N*H*W, K=R*S*Cout],
 //               B = Wt [C, R*S*Cout]; epilogue stores (or accumulates into) dx.
 //   CONV_WGRAD: A = dy^T [Cout, K=N*Ho*Wo], B = im2col(x)^T [R*S*C, K]; both are strided along
-//               K in NHWC: producers cp.async 16-B (4-channel) chunks into their 4x4 blocks and
-//               the auxiliary warps transpose each block in place (WLoader / transpose_block);
+//               K in NHWC: the TMA path loads them MN-major (MNW: fed to the MMA as loaded; XF:
+//               transposed in place by the auxiliary warps); the cp.async path gathers 16-B
+//               (4-channel) chunks into 4x4 blocks that the auxiliary warps transpose
+//               (WLoader / transpose_block);
 //               split-K over pixels, the epilogue stores the split's partial dW (KRSC).
 //   GEMM_TEST : plain K-major A [M][K], B [N][K], for unit tests of the core.
-// (All smem operands are K-major SWIZZLE_NONE. MN-major tf32 operands -- transpose bits 15/16
-//  of the instruction descriptor -- produced all-zero results on B200 in our tests, see
-//  DESIGN.md "MN-major tf32".)
+// (Operands are K-major -- SWIZZLE_NONE core matrices or SWIZZLE_128B TMA tiles -- except the
+//  MNW wgrad, whose TMA boxes stay MN-major in the SWIZZLE_128B_BASE32B layout, the one MN-major
+//  layout tcgen05 accepts for tf32.)
 #pragma once
 #include <cuda.h>
 
