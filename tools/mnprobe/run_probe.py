@@ -15,6 +15,7 @@ if not os.path.exists(so):
                            "-shared", "-Xcompiler", "-fPIC", "-o", so, os.path.join(HERE, "mnprobe.cu"), "-lcuda"])
 lib = C.CDLL(so)
 lib.mnprobe_run.argtypes = [C.c_void_p] * 3 + [C.c_uint32] * 4 + [C.c_int] * 2
+lib.mnprobe_halo.argtypes = [C.c_void_p] * 3 + [C.c_uint32] * 2
 
 K, M, N = 32, 128, 128
 g = np.random.default_rng(0)
@@ -41,3 +42,17 @@ for name, lbo, sbo, layout, swz in [
     out = dd.cpu().numpy().astype(np.float64)
     err = np.linalg.norm(out - ref) / np.linalg.norm(ref)
     print("%-30s rc %d  rel err %.3e  |D| %.3e" % (name, rc, err, np.linalg.norm(out)), flush=True)
+
+# probe 2: A chunk q = the 40-row halo shifted by q (+ start) rows (LBO = 128 B)
+halo = g.standard_normal((40, 32)).astype(np.float32)
+dh = torch.from_numpy(halo).cuda()
+for start in (0, 1, 2, 3, 5):
+    A = np.zeros((M, K))
+    for q in range(4):
+        A[q * 32:(q + 1) * 32, :] = tf32_trunc(halo[start + q:start + q + K, :]).T.astype(np.float64)
+    ref2 = A @ tf32_trunc(b).astype(np.float64)
+    dd.zero_()
+    rc = lib.mnprobe_halo(C.c_void_p(dh.data_ptr()), C.c_void_p(db.data_ptr()), C.c_void_p(dd.data_ptr()), 128, start)
+    out = dd.cpu().numpy().astype(np.float64)
+    print("halo start %d LBO 128: rc %d  rel err %.3e" % (start, rc, np.linalg.norm(out - ref2) / np.linalg.norm(ref2)),
+          flush=True)
