@@ -91,6 +91,12 @@ static bool mn_wgrad() {
   return on != 0;
 }
 
+// the transpose-free 3xTF32 wgrad with its A operand in TMEM (POOCH_WGRAD_AT=1 enables)
+static bool mn_wgrad_at() {
+  static int on = getenv("POOCH_WGRAD_AT") ? atoi(getenv("POOCH_WGRAD_AT")) : 0;
+  return on != 0;
+}
+
 // 3xTF32 TMA fwd / dgrad with the A operand in TMEM (POOCH_A_TMEM=0 disables)
 static bool a_in_tmem() {
   static int on = getenv("POOCH_A_TMEM") ? atoi(getenv("POOCH_A_TMEM")) : 1;
@@ -668,7 +674,11 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
     const CUtensorMap* tc = g.C1 > 0 ? &tx1 : nullptr;
     if (mn) {
       if (g.prec) {
-        if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
+        // A in TMEM (hi / lo gathered from the MN-major blocks) unless POOCH_WGRAD_AT=0
+        if (mn_wgrad_at()) {
+          if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, true, true>(p, grid, st, ta, tb, tc)));
+          else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true, true, false, true, true>(p, grid, st, ta, tb, tc)));
+        } else if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
         else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
       } else {
         if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, false, true, false, false, true>(p, grid, st, ta, tb, tc)));

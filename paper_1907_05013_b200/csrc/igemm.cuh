@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
   // channels] rows in the SWIZZLE_128B_ATOM_32B layout, the only MN-major layout tcgen05 accepts
   // for tf32 (layout type SWIZZLE_128B_BASE32B), so no transposes:
   // the auxiliary warps only write the 3xTF32 residuals
-  static_assert(!MNW || (MODE == CONV_WGRAD && TMA && !AT && !XF && NAUX == 4), "MNW: plain TMA wgrad");
+  static_assert(!MNW || (MODE == CONV_WGRAD && TMA && !XF && NAUX == 4), "MNW: plain TMA wgrad");
   // AT: 3xTF32 with the A operand in TMEM -- the auxiliary warps move each stage's A tile (hi =
   // trunc_tf32(a), lo = a - hi) from shared memory into TMEM, so the three MMAs of a k-step read
   // only B / Bs from shared memory (A is re-read by every MMA, the dominant smem traffic at BN = 64)
@@ -824,7 +824,42 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
         }
         ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
-        if constexpr (MNW) {
+        if constexpr (MNW && AT) {
+          // A in TMEM from MN-major blocks: warp w owns A block w & 3 (its TMEM lane quadrant);
+          // lane m gathers its 32 K values straight from the block's column m (row k at k * 128,
+          // 32-B granule (m / 8) ^ (k & 3): conflict-free across the lanes), splits hi / lo and
+          // stores both into this stage's TMEM columns; the B blocks get their residuals in place
+          // (+ BS_OFF, same MN-major layout)
+#pragma unroll
+          for (int q = 0; q < WQ; ++q) {
+            const int bi = (warp & 3) + 4 * q;
+            if (bi >= (BM + BN) / 32) break;
+            const uint32_t blk = st + bi * 4096;
+            if (bi < BM / 32) {
+              float v[32], lo[32];
+#pragma unroll
+              for (int k = 0; k < 32; ++k)
+                asm volatile("ld.shared.f32 %0, [%1];"
+                             : "=f"(v[k])
+                             : "r"(blk + k * 128 + ((((lane >> 3) ^ (k & 3))) << 5) + (lane & 7) * 4));
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float hi = __uint_as_float(__float_as_uint(v[i]) & 0xFFFFE000u);
+                lo[i] = v[i] - hi;
+                v[i] = hi;
+              }
+              const uint32_t ta = tmem + ((uint32_t)(32 * bi) << 16) + A_TCOL + 64u * s;
+              ptx::tmem_st32(ta, v);
+              ptx::tmem_st32(ta + 32, lo);
+            } else {
+              const uint32_t bblk = st + SM::A_BYTES + (bi - BM / 32) * 4096;
+#pragma unroll
+              for (int c = lane; c < 256; c += 32) split_chunk(bblk + c * 16, bblk + SM::BS_OFF + c * 16);
+            }
+          }
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+        } else if constexpr (MNW) {
           // MN-major operands: the residual of every element at the same offset + SMALL_OFF (the
           // layout is the same for both, so no index arithmetic)
           if constexpr (X3) {
@@ -984,12 +1019,20 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
             // them), pixel rows of 128 B, 4-row K groups 512 B apart (SBO); a k-step of 8 pixels
             // advances 8 rows = 1024 B
             constexpr uint32_t IDESC_MN = ptx::idesc_tf32(BM, BN, true, true);
+            constexpr uint32_t IDESC_TMN = ptx::idesc_tf32(BM, BN, false, true);  // A K-major in TMEM
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint32_t ko = kk * 1024;
               const uint64_t ad = ptx::smem_desc(sa + ko, 4096, 512, 1);
               const uint64_t bd = ptx::smem_desc(sb + ko, 4096, 512, 1);
-              if constexpr (X3) {
+              if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs MN-major
+                const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
+                const uint64_t bsd = ptx::smem_desc(sb + SM::BS_OFF + ko, 4096, 512, 1);
+                ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_TMN, (kb | kk) != 0 ? 1u : 0u);
+                ptx::mma_tf32_ts(acc, ta, bsd, IDESC_TMN, 1u);
+                ptx::mma_tf32_ts(acc, ta, bd, IDESC_TMN, 1u);
+                (void)ad;
+              } else if constexpr (X3) {
                 const uint64_t asd = ptx::smem_desc(sa + SM::SMALL_OFF + ko, 4096, 512, 1);
                 const uint64_t bsd = ptx::smem_desc(sb + SM::SMALL_OFF + ko, 4096, 512, 1);
                 ptx::mma_tf32(acc, asd, bd, IDESC_MN, (kb | kk) != 0 ? 1u : 0u);

@@ -63,7 +63,7 @@ def _run(tmp_path, world, strategy, net="tiny"):
 
 
 @pytest.mark.parametrize("world,strategy,net", [(2, "incore", "tiny"), (2, "pooch", "tiny"), (3, "pooch", "tiny"),
-                                                (2, "incore", "resnet50")])
+                                                (4, "incore", "tiny"), (2, "incore", "resnet50")])
 def test_peer_allreduce_sum_bit_exact(tmp_path, world, strategy, net):
     """ResNet-50 (25.6 M parameters) spans four gradient buckets, each its own barrier pair."""
     res, load = _run(tmp_path, world, strategy, net)
