@@ -583,44 +583,70 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
         ptx::tma_prefetch_desc(&tma_b);
         if (p.c_split) ptx::tma_prefetch_desc(&tma_c);
         int it = 0;
+        // per tile, the (at most (BM + BN) / 32) boxes' maps and tap offsets are fixed: decode them
+        // once; per k-block only the pixel box moves (walked incrementally, no divisions), so the
+        // single issuing thread keeps up with the MMAs of narrow (BN = 64) tiles
+        constexpr int NBOX = (BM + BN) / 32;
+        const CUtensorMap* bmap[NBOX];
+        uint32_t bdst[NBOX];
+        int bdx[NBOX], bdy[NBOX], bdz[NBOX], bch[NBOX];
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
           int m0, n0, kb0, nkb;
           tm.decode(t, m0, n0, kb0, nkb, BN);
           uint32_t bytes = 0;
-          for (int q = 0; q < BM / 32; q += p.wg_cba) bytes += (m0 + 32 * q < p.M) ? 4096u * p.wg_cba : 0u;
-          for (int q = 0; q < BN / 32; q += p.wg_cbb) bytes += (n0 + 32 * q < p.Ng) ? 4096u * p.wg_cbb : 0u;
+          int nbox = 0;
+          // one box = cb consecutive 32-channel chunks of the same tap over the pixel box; the
+          // 5-D map puts the chunk index outermost, so the box lands as cb consecutive 4-KB blocks
+          auto add_box = [&](uint32_t dst_off, const CUtensorMap* map, bool is_x, int row, int cb) {
+            bdst[nbox] = dst_off;
+            bytes += 4096u * cb;
+            if (is_x) {
+              // row = ((t * R + r) * S + s) * C + c; channels past c_split come from the second source
+              const int rs = row / p.C;
+              int c = row - rs * p.C;
+              const int t3 = rs / (p.R * p.S), r2 = rs - t3 * p.R * p.S;
+              const int r = r2 / p.S, sx = r2 - r * p.S;
+              if (p.c_split && c >= p.c_split) {
+                map = &tma_c;
+                c -= p.c_split;
+              }
+              bmap[nbox] = map;
+              bdx[nbox] = sx - p.pad;
+              bdy[nbox] = r - p.pad;
+              bdz[nbox] = t3 - p.pad3;
+              bch[nbox] = c >> 5;
+            } else {
+              bmap[nbox] = map;
+              bdx[nbox] = bdy[nbox] = bdz[nbox] = 0x40000000;   // marks a dy box (no stride / offset)
+              bch[nbox] = row >> 5;
+            }
+            ++nbox;
+          };
+          for (int q = 0; q < BM / 32; q += p.wg_cba)
+            if (m0 + 32 * q < p.M) add_box(q * 4096, &tma_a, p.wg_a_is_x != 0, m0 + 32 * q, p.wg_cba);
+          for (int q = 0; q < BN / 32; q += p.wg_cbb)
+            if (n0 + 32 * q < p.Ng) add_box(SM::A_BYTES + q * 4096, &tma_b, p.wg_a_is_x == 0, n0 + 32 * q, p.wg_cbb);
+          int bw = kb0 % p.tiles_w, bh = (kb0 / p.tiles_w) % p.tiles_h, bn = kb0 / (p.tiles_w * p.tiles_h);
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             int s = it % STAGES;
             if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
             uint32_t st = sbase + s * SM::STAGE_BYTES;
-            const int b = kb0 + kb;
-            const int ow = (b % p.tiles_w) * p.tw;
-            const int oh = ((b / p.tiles_w) % p.tiles_h) * p.th;
-            const int on = (b / (p.tiles_w * p.tiles_h)) * p.tn;
+            const int ow = bw * p.tw, oh = bh * p.th, on = bn * p.tn;
             ptx::mbar_arrive_expect_tx(&rawfull[s], bytes);
-            // one box = cb consecutive 32-channel chunks of the same tap over the pixel box; the
-            // 5-D map puts the chunk index outermost, so the box lands as cb consecutive 4-KB blocks
-            auto box = [&](uint32_t dst, const CUtensorMap* map, bool is_x, int row) {
-              if (is_x) {
-                // row = ((t * R + r) * S + s) * C + c; channels past c_split come from the second source
-                const int rs = row / p.C;
-                int c = row - rs * p.C;
-                const int t3 = rs / (p.R * p.S), r2 = rs - t3 * p.R * p.S;
-                const int r = r2 / p.S, sx = r2 - r * p.S;
-                if (p.c_split && c >= p.c_split) {
-                  map = &tma_c;
-                  c -= p.c_split;
-                }
-                ptx::tma_load_5d(dst, map, &rawfull[s], 0, ow * p.stride - p.pad + sx, oh * p.stride - p.pad + r,
-                                 on * p.st3 - p.pad3 + t3, c >> 5);
-              } else {
-                ptx::tma_load_5d(dst, map, &rawfull[s], 0, ow, oh, on, row >> 5);
+            for (int i = 0; i < nbox; ++i) {
+              if (bdx[i] == 0x40000000)
+                ptx::tma_load_5d(st + bdst[i], bmap[i], &rawfull[s], 0, ow, oh, on, bch[i]);
+              else
+                ptx::tma_load_5d(st + bdst[i], bmap[i], &rawfull[s], 0, ow * p.stride + bdx[i], oh * p.stride + bdy[i],
+                                 on * p.st3 + bdz[i], bch[i]);
+            }
+            if (++bw == p.tiles_w) {
+              bw = 0;
+              if (++bh == p.tiles_h) {
+                bh = 0;
+                ++bn;
               }
-            };
-            for (int q = 0; q < BM / 32; q += p.wg_cba)
-              if (m0 + 32 * q < p.M) box(st + q * 4096, &tma_a, p.wg_a_is_x != 0, m0 + 32 * q);
-            for (int q = 0; q < BN / 32; q += p.wg_cbb)
-              if (n0 + 32 * q < p.Ng) box(st + SM::A_BYTES + q * 4096, &tma_b, p.wg_a_is_x == 0, n0 + 32 * q);
+            }
           }
         }
       }
@@ -664,29 +690,60 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
           const int tw_i = mt_i % p.tiles_w;
           const int th_i = (mt_i / p.tiles_w) % p.tiles_h;
           const int tn_i = mt_i / (p.tiles_w * p.tiles_h);
+          // the k-block walks (tap, 32-channel chunk) with the chunk fastest: decode k = kb0 once per
+          // tile, then advance incrementally (no per-k-block divisions in the single issuing thread,
+          // which otherwise paces the narrow BN = 64 tiles)
+          int cc = kb0 % p.cchunks, tap0 = kb0 / p.cchunks;
+          int wt3, wr, ws;   // FWD: (t3, r, s) of the tap; DGRAD: the class-tap indices (tt, tr, ts)
+          if (MODE == CONV_FWD) {
+            wt3 = tap0 / (p.R * p.S);
+            const int r2 = tap0 - wt3 * p.R * p.S;
+            wr = r2 / p.S;
+            ws = r2 - wr * p.S;
+          } else {
+            wt3 = tap0 / (p.dg_nr * p.dg_ns);
+            const int t2 = tap0 - wt3 * p.dg_nr * p.dg_ns;
+            wr = t2 / p.dg_ns;
+            ws = t2 - wr * p.dg_ns;
+          }
+          // FWD: cw = cw0 + s; DGRAD: cw = cw0 - ts (the class selects taps whose offsets divide
+          // exactly by the stride)
+          const int cw0 = MODE == CONV_FWD ? tw_i * p.tw * p.stride - p.pad
+                                           : tw_i * p.tw + (p.dg_b + p.pad - p.dg_s0) / p.stride;
+          const int ch0 = MODE == CONV_FWD ? th_i * p.th * p.stride - p.pad
+                                           : th_i * p.th + (p.dg_a + p.pad - p.dg_r0) / p.stride;
+          const int c30 = MODE == CONV_FWD ? tn_i * p.tn * p.st3 - p.pad3
+                                           : tn_i * p.tn + (p.dg_c + p.pad3 - p.dg_t0) / p.st3;
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             int s = it % STAGES;
             if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
             uint32_t st = sbase + s * SM::STAGE_BYTES;
             uint64_t* bar = AUX ? &rawfull[s] : &full[s];
             const int k = kb0 + kb;
-            const int tap = k / p.cchunks, cc = k - tap * p.cchunks;
             int cw, chh, c3, rs;
             if (MODE == CONV_FWD) {  // tap = (t * R + r) * S + s over the [K][T][R][S][C] weights
-              const int t3 = tap / (p.R * p.S), r2 = tap - t3 * p.R * p.S;
-              const int r = r2 / p.S, sx = r2 - r * p.S;
-              rs = tap;
-              cw = tw_i * p.tw * p.stride - p.pad + sx;
-              chh = th_i * p.th * p.stride - p.pad + r;
-              c3 = tn_i * p.tn * p.st3 - p.pad3 + t3;
+              rs = (wt3 * p.R + wr) * p.S + ws;
+              cw = cw0 + ws;
+              chh = ch0 + wr;
+              c3 = c30 + wt3;
             } else {
-              const int tt = tap / (p.dg_nr * p.dg_ns), t2 = tap - tt * p.dg_nr * p.dg_ns;
-              const int tr = t2 / p.dg_ns, ts = t2 - tr * p.dg_ns;
-              const int r = p.dg_r0 + p.stride * tr, sx = p.dg_s0 + p.stride * ts, t3 = p.dg_t0 + p.st3 * tt;
+              const int r = p.dg_r0 + p.stride * wr, sx = p.dg_s0 + p.stride * ws, t3 = p.dg_t0 + p.st3 * wt3;
               rs = (t3 * p.R + r) * p.S + sx;
-              cw = tw_i * p.tw + (p.dg_b + p.pad - sx) / p.stride;   // exact: the class selects the taps
-              chh = th_i * p.th + (p.dg_a + p.pad - r) / p.stride;
-              c3 = tn_i * p.tn + (p.dg_c + p.pad3 - t3) / p.st3;
+              cw = cw0 - ws;
+              chh = ch0 - wr;
+              c3 = c30 - wt3;
+            }
+            const int cck = cc;
+            if (++cc == p.cchunks) {   // next tap
+              cc = 0;
+              const int ns = MODE == CONV_FWD ? p.S : p.dg_ns, nr = MODE == CONV_FWD ? p.R : p.dg_nr;
+              if (++ws == ns) {
+                ws = 0;
+                if (++wr == nr) {
+                  wr = 0;
+                  ++wt3;
+                }
+              }
             }
             if (MODE == CONV_FWD && p.stem4) {
               // 8 taps of 4 channels: tap j's A box (16 B per output pixel) lands at j * BM * 16 and
@@ -707,11 +764,11 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
               continue;
             }
             ptx::mbar_arrive_expect_tx(bar, bytes);
-            if (MODE == CONV_FWD && p.c_split && cc * 32 >= p.c_split)
-              ptx::tma_load_4d(st, &tma_c, bar, cc * 32 - p.c_split, cw, chh, c3);
+            if (MODE == CONV_FWD && p.c_split && cck * 32 >= p.c_split)
+              ptx::tma_load_4d(st, &tma_c, bar, cck * 32 - p.c_split, cw, chh, c3);
             else
-              ptx::tma_load_4d(st, &tma_a, bar, cc * 32, cw, chh, c3);
-            ptx::tma_load_2d(st + SM::A_BYTES, &tma_b, bar, rs * cred + cc * 32, n0);
+              ptx::tma_load_4d(st, &tma_a, bar, cck * 32, cw, chh, c3);
+            ptx::tma_load_2d(st + SM::A_BYTES, &tma_b, bar, rs * cred + cck * 32, n0);
           }
         }
       }
