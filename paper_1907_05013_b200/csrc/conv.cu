@@ -91,9 +91,9 @@ static bool mn_wgrad() {
   return on != 0;
 }
 
-// the transpose-free 3xTF32 wgrad with its A operand in TMEM (POOCH_WGRAD_AT=1 enables)
+// the transpose-free 3xTF32 wgrad with its A operand in TMEM (POOCH_WGRAD_AT=0: A in smem)
 static bool mn_wgrad_at() {
-  static int on = getenv("POOCH_WGRAD_AT") ? atoi(getenv("POOCH_WGRAD_AT")) : 0;
+  static int on = getenv("POOCH_WGRAD_AT") ? atoi(getenv("POOCH_WGRAD_AT")) : 1;
   return on != 0;
 }
 
