@@ -201,14 +201,22 @@ extern "C" pooch_status pooch_set_peers(pooch_ctx* c, const void* handles) {
     cudaError_t e = cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) {
       cudaGetLastError();
+      // leave no half-mapped peer set behind (has_comm() would route the step through it)
+      for (int r = 0; r < p; ++r)
+        if (c->peer_base[r] && c->peer_base[r] != c->peer_own) cudaIpcCloseMemHandle(c->peer_base[r]);
+      c->peer_base.clear();
       return ctx_fail(c, fail(POOCH_ECUDA, "cudaIpcOpenMemHandle (rank %d): %s", p, cudaGetErrorString(e)));
     }
     c->peer_base[p] = q;
   }
   c->have_plan = false;
   peer_setup_buckets(c);
-  if ((int)c->buckets.size() + 1 > peer_max_slots())
+  if ((int)c->buckets.size() + 1 > peer_max_slots()) {
+    for (int r = 0; r < c->world; ++r)
+      if (c->peer_base[r] && c->peer_base[r] != c->peer_own) cudaIpcCloseMemHandle(c->peer_base[r]);
+    c->peer_base.clear();
     return ctx_fail(c, fail(POOCH_EUSAGE, "%zu allreduce buckets exceed the %d barrier slots", c->buckets.size(),
                             peer_max_slots() - 1));
+  }
   return POOCH_OK;
 }
