@@ -49,7 +49,8 @@ bool conv_shape_ok(const ConvGeom& g) {
 
 static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
-template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false, bool MNW = false>
+template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false, bool MNW = false,
+          bool E2 = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr,
                                  const CUtensorMap* td = nullptr) {
@@ -58,17 +59,20 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   // latency, so the ring depth sets the throughput of the short-K and narrow (BN = 64) layers
   // AT fwd / dgrad: two epilogue staging images (the TMA store of one column chunk overlaps the
   // staging of the next; more than 3-4 ring stages measured no faster, so the smem goes here)
-  constexpr int NSTG = (AT && MODE != CONV_WGRAD) ? 2 : 1;
-  constexpr int STAGE_B = GemmSmem<BN, 1, X3, AT, NSTG>::STAGE_BYTES;
-  constexpr int FIXED_B = GemmSmem<BN, 1, X3, AT, NSTG>::TOTAL - STAGE_B + 64;
+  // E2 (two epilogue warp groups, each with its own images): one image per group at BN = 64
+  // (one column chunk per group per tile), so the ring keeps its depth
+  constexpr int NEG = E2 ? 2 : 1;
+  constexpr int NSTG = (AT && MODE != CONV_WGRAD) ? ((E2 && BN == 64) ? 1 : 2) : 1;
+  constexpr int STAGE_B = GemmSmem<BN, 1, X3, AT, NSTG, NEG>::STAGE_BYTES;
+  constexpr int FIXED_B = GemmSmem<BN, 1, X3, AT, NSTG, NEG>::TOTAL - STAGE_B + 64;
   constexpr int STAGES_SM = std::max(2, std::min(8, (227 * 1024 - FIXED_B) / STAGE_B));
   // AT: each stage also holds 64 TMEM columns (A hi / lo) next to the two accumulators
   constexpr int STAGES = AT ? std::min(STAGES_SM, (512 - 2 * BN) / 64) : STAGES_SM;
-  constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT, NSTG>::TOTAL;
+  constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT, NSTG, NEG>::TOTAL;
   // TMA wgrad at BN = 64 (3xTF32): six blocks of 32x32 per stage -> six auxiliary warps, one
   // block each, instead of four warps doing one or two (the transposes bound these layers)
   constexpr int NAUX = (MODE == CONV_WGRAD && TMA && X3 && BN == 64 && !AT && !XF && !MNW) ? 6 : 4;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX, MNW>;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX, MNW, E2>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -79,7 +83,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   int64_t tiles = (int64_t)grid.x * grid.y * grid.z;
   int ctas = (int)std::min<int64_t>(tiles, 148);
   count_launch();
-  kern<<<ctas, igemm_threads(MODE, X3, XF, NAUX), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
+  kern<<<ctas, igemm_threads(MODE, X3, XF, NAUX, E2), SMEM, st>>>(p, ta ? *ta : g_zero_map, tb ? *tb : g_zero_map,
                                                           tc ? *tc : g_zero_map, td ? *td : g_zero_map);
   POOCH_CUDA(cudaGetLastError());
   return POOCH_OK;
@@ -101,6 +105,14 @@ static bool mn_wgrad_at() {
 static bool a_in_tmem() {
   static int on = getenv("POOCH_A_TMEM") ? atoi(getenv("POOCH_A_TMEM")) : 1;
   return on != 0;
+}
+
+// two epilogue warp groups for the AT fwd / dgrad kernels (POOCH_EPI2: 0 off, 1 BN = 128 only,
+// 2 all tile widths, the default: 1x1 expand fwd 23 % and 1x1 reduce dgrad 20 % faster, the
+// rest 0-4 %; profiles/r02_kernel_experiments.md)
+static int epi2() {
+  static int on = getenv("POOCH_EPI2") ? atoi(getenv("POOCH_EPI2")) : 2;
+  return on;
 }
 
 template <int MODE, bool TMA = false>
@@ -139,6 +151,10 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
       // wgrad: A in TMEM pays off at BN = 128 (stages 2-4: 3-12 % faster) but not at BN = 64
       // (stage 1, 6-9 % slower: the extra read-back of the transposed A blocks)
       if (a_in_tmem() && !p.stem4 && (MODE != CONV_WGRAD || bn == 128)) {
+        if constexpr (MODE != CONV_WGRAD) {
+          if (epi2() >= 2 && bn == 64) return launch_igemm<MODE, 64, true, true, false, true, false, true>(p, grid, st, ta, tb, tc, td);
+          if (epi2() >= 1 && bn == 128) return launch_igemm<MODE, 128, true, true, false, true, false, true>(p, grid, st, ta, tb, tc, td);
+        }
         switch (bn) {
           case 64: return launch_igemm<MODE, 64, true, true, false, true>(p, grid, st, ta, tb, tc, td);
           case 128: return launch_igemm<MODE, 128, true, true, false, true>(p, grid, st, ta, tb, tc, td);

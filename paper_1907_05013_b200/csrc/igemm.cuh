@@ -3,16 +3,22 @@
 // One CTA computes a 128 x BN fp32 tile D = A * B^T with tcgen05.mma kind::tf32
 // (TF32 in, FP32 accumulate in TMEM), K consumed in blocks of 32 elements.
 //
-//   warps 0-3 : producers -- gather A/B chunks (16 B = 4 fp32) straight from the NHWC
-//               tensors with cp.async (zero-fill for padding / tails) into the canonical
-//               SWIZZLE_NONE core-matrix layout, then become the epilogue warps
-//               (tcgen05.ld TMEM -> registers -> fused epilogue -> global).
-//   warp 4    : TMEM allocator + single-thread MMA issuer (tcgen05.mma, tcgen05.commit).
+// Persistent and warp-specialised (igemm_kernel below): each CTA walks tiles with a stride of
+// the grid and two TMEM accumulators, so the epilogue of tile i overlaps the mainloop of i+1.
+//   warps 0-3  : epilogue -- tcgen05.ld TMEM -> registers -> fused epilogue (bias / ReLU, BN
+//                partial sums) -> swizzled smem staging -> TMA store (or coalesced stores).
+//                E2: warps 4-7 form a second epilogue group that drains the other half of the
+//                accumulator's columns (a warp may only read TMEM lane quadrant warp % 4).
+//   warps 4-7  : producers -- cp.async gathers of 16-B chunks into SWIZZLE_NONE core matrices,
+//                or (TMA) one elected thread issuing the tensor-memory-accelerator boxes
+//                (E2: that thread is warp 13).
+//   warp 8     : TMEM allocator + single-thread MMA issuer (tcgen05.mma, tcgen05.commit).
+//   warps 9-12 : auxiliary (3xTF32 residuals, wgrad transposes, AT: A hi / lo into TMEM).
 //
-// Pipeline: STAGES smem slots, mbarrier full/empty ring. A producer thread commits its
-// cp.async group per k-block and, LAG = STAGES-1 blocks later, waits for it, issues
-// fence.proxy.async and arrives on full[]; the MMA thread's tcgen05.commit arrives on
-// empty[] when the tensor core is done reading the slot.
+// Pipeline: STAGES smem slots, mbarrier full/empty ring (TMA: expect-tx arrivals; 3xTF32: the
+// auxiliary warps publish each stage after writing its residuals); the MMA thread's
+// tcgen05.commit arrives on empty[] when the tensor core is done reading the slot and on
+// tfull[] when an accumulator is complete.
 //
 // Modes (which tensors A and B are, and what the epilogue does):
 //   CONV_FWD  : A = im2col(x) [M=N*Ho*Wo, K=R*S*C] (K-major gather), B = W [Cout, R*S*C];
@@ -99,7 +105,7 @@ constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per k-block (128 B per row)
 constexpr int NUM_THREADS = 160;
 
-template <int BN, int STAGES, bool X3 = false, bool AT = false, int NSTG = 1>
+template <int BN, int STAGES, bool X3 = false, bool AT = false, int NSTG = 1, int NEG = 1>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
@@ -113,8 +119,9 @@ struct GemmSmem {
   // epilogue staging: per epilogue warp one 32 x 32 fp32 block (4 KB); together the 128 x 32
   // SWIZZLE_128B image of one column chunk of the tile (1024-B aligned for the TMA store)
   static constexpr int STG_OFF = (RED_OFF + 4 * BN * 4 * 2 + 1023) / 1024 * 1024;
-  // NSTG = 2: two staging images, so a column chunk is staged while the TMA still reads the last
-  static constexpr int TOTAL = STG_OFF + NSTG * 4 * 4096 + 1024;
+  // NSTG = 2: two staging images, so a column chunk is staged while the TMA still reads the last;
+  // NEG = 2 epilogue warp groups, each with its own NSTG images
+  static constexpr int TOTAL = STG_OFF + NEG * NSTG * 4 * 4096 + 1024;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -470,8 +477,9 @@ constexpr int NUM_THREADS_X3 = 416;     // + 4 residual ("split") warps for 3xTF
 __host__ __device__ constexpr bool igemm_aux(int mode, bool x3, bool xf = false) {
   return x3 || xf || mode == CONV_WGRAD;
 }
-__host__ __device__ constexpr int igemm_threads(int mode, bool x3, bool xf = false, int naux = 4) {
-  return igemm_aux(mode, x3, xf) ? NUM_THREADS_P + 32 * naux : NUM_THREADS_P;
+// E2: a second epilogue warp group (warps 4-7, the TMA producer moves to warp 13)
+__host__ __device__ constexpr int igemm_threads(int mode, bool x3, bool xf = false, int naux = 4, bool e2 = false) {
+  return (igemm_aux(mode, x3, xf) ? NUM_THREADS_P + 32 * naux : NUM_THREADS_P) + (e2 ? 32 : 0);
 }
 
 
@@ -499,8 +507,8 @@ struct TileMap {
 };
 
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false,
-          int NSTG = 1, int NAUX = 4, bool MNW = false>
-__global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
+          int NSTG = 1, int NAUX = 4, bool MNW = false, bool E2 = false>
+__global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
   static_assert(!TMA || MODE != GEMM_TEST, "TMA path: conv fwd / dgrad / wgrad");
@@ -520,10 +528,17 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
   static_assert(!AT || (X3 && TMA && MODE != GEMM_TEST && (!XF || MODE == CONV_FWD)),
                 "AT: 3xTF32 TMA fwd / dgrad / wgrad (with BN-ReLU on load: fwd only)");
   static_assert(!AT || 2 * BN + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
+  // E2: two epilogue warp groups drain each accumulator, one per half of its columns (the
+  // 1x1 expand convs are epilogue-bound: TMEM -> smem staging -> BN partial sums -> TMA store);
+  // warps 4-7 (idle besides the one TMA-issuing thread) become group 1, and the TMA producer
+  // moves to warp 13 -- the TMEM lane quadrant a warp may read is warp % 4, so 4-7 cover all four
+  static_assert(!E2 || (PIXM && X3 && NAUX == 4), "E2: 3xTF32 TMA fwd / dgrad");
+  constexpr int NEG = E2 ? 2 : 1;
+  constexpr int PW = E2 ? 13 : 4;  // first producer warp
   constexpr uint32_t TMEM_COLS = AT ? 512u : 2u * BN;
   constexpr uint32_t A_TCOL = 2u * BN;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
   constexpr bool AUX = igemm_aux(MODE, X3, XF);
-  using SM = GemmSmem<BN, STAGES, X3, AT, NSTG>;
+  using SM = GemmSmem<BN, STAGES, X3, AT, NSTG, NEG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
@@ -557,7 +572,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 128);
+      ptx::mbar_init(&tempty[a], 128 * NEG);
     }
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&rawfull[s], TMA ? 1 : 128);
     ptx::fence_mbar_init();
@@ -569,9 +584,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = ptx::smem_u32(smem);
 
-  if (warp >= 4 && warp < 8) {
+  if (E2 ? warp == PW : (warp >= 4 && warp < 8)) {
     // ------------------------------------------------------------------ producers
-    const int ptid = tid - 128;
+    const int ptid = tid - 32 * PW;
     if constexpr (MODE == CONV_WGRAD && TMA) {
       // one elected thread: per k-block (a box of 32 output pixels) one 4-D TMA box per 32 rows
       // of each operand -- dy: 32 output channels x the pixel box; x: the 32 input channels of
@@ -793,7 +808,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
       }
       ptx::cp_async_wait<0>();
     }
-  } else if (AUX && warp >= 9) {
+  } else if (AUX && warp >= 9 && warp < 13) {
     // ------------------------------------------------------------------ auxiliary warps
     // Per stage: wait for the raw operands, (wgrad) transpose every 4x4 block in place,
     // (3xTF32) write x - tf32(x) of every chunk, publish to the async proxy, arrive full[].
@@ -1138,7 +1153,13 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
     }
   } else {
     // ------------------------------------------------------------------ epilogue
-    const int row = warp * 32 + lane;
+    // group eg (E2: warps 0-3 / 4-7) drains column chunks [eg * CPG, (eg + 1) * CPG) of the
+    // accumulator; q4 = the warp's TMEM lane quadrant, etid = thread index within the group
+    const int q4 = warp & 3;
+    const int eg = E2 ? (warp >> 2) : 0;
+    const int etid = tid - 128 * eg;
+    constexpr int CPG = BN / 32 / NEG;
+    const int row = q4 * 32 + lane;
     int j = 0;
     uint32_t chunk_seq = 0;  // column chunks staged so far (selects the staging image when NSTG = 2)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
@@ -1162,13 +1183,91 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
         else
           gm = (nn * p.hout + hh) * p.wout + ww;
       }
-      const uint32_t taddr = tmem + ab * BN + ((uint32_t)(warp * 32) << 16);
+      const uint32_t taddr = tmem + ab * BN + ((uint32_t)(q4 * 32) << 16);
       const int z = t / (tm.mt * tm.nt);
       bool stats = false;
       if constexpr (MODE == CONV_FWD) stats = p.stat_sum != nullptr && p.epi_direct != 3;  // 3: experiment
-      if (stats) asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's reads of red[] done
+      if (stats) ptx::named_bar_sync(1 + 2 * eg, 128);  // previous tile's reads of red[] done
+      // E2 at BN = 128: the group's two column chunks in one pass -- one 64-column TMEM load, both
+      // staging images filled behind one pair of barriers, two TMA stores in one bulk group, then
+      // the BN partial sums of both (the per-chunk loop below pays its barriers / fence per chunk)
+      const bool batched = E2 && CPG == 2 && NSTG == 2 && p.tma_store && p.epi_direct == 0;
+      if (batched) {
+        float v[64];
+        const int c0 = eg * CPG;
+        if (nkb > 0) {
+          ptx::tmem_ld64(taddr + c0 * 32, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) v[i] = 0.f;
+        }
+        if constexpr (MODE == CONV_FWD) {
+          if (p.bias != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] += (n0 + c0 * 32 + i < p.Ng) ? __ldg(p.bias + n0 + c0 * 32 + i) : 0.f;
+          }
+          if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+        }
+        const uint32_t img0 = sbase + SM::STG_OFF + eg * (NSTG * 16384u);
+        if (etid == 0) ptx::bulk_wait_read0();  // this group's previous stores have read both images
+        ptx::named_bar_sync(2 + 2 * eg, 128);
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const uint32_t stg = img0 + cc * 16384u + q4 * 4096;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((jj ^ (lane & 7)) << 4)),
+                         "f"(v[32 * cc + 4 * jj]), "f"(v[32 * cc + 4 * jj + 1]), "f"(v[32 * cc + 4 * jj + 2]),
+                         "f"(v[32 * cc + 4 * jj + 3])
+                         : "memory");
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(2 + 2 * eg, 128);
+        if (etid == 0) {
+          const int mt_i = m0 / BM;
+          const int tw_i = mt_i % p.tiles_w, th_i = (mt_i / p.tiles_w) % p.tiles_h, tn_i = mt_i / (p.tiles_w * p.tiles_h);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int nb = n0 + (c0 + cc) * 32;
+            const int accum = MODE == CONV_DGRAD ? ((p.n_split > 0 && nb >= p.n_split) ? p.accumulate2 : p.accumulate) : 0;
+            if (nb < p.Ng) {
+              if (p.tma_store == 1)
+                ptx::tma_store_4d(&tma_d, img0 + cc * 16384u, nb, tw_i * p.tw, th_i * p.th, tn_i * p.tn, accum);
+              else
+                ptx::tma_store_2d(&tma_d, img0 + cc * 16384u, nb, m0, accum);
+            }
+          }
+          ptx::bulk_commit();
+        }
+        if constexpr (MODE == CONV_FWD) {
+          if (stats) {
+            const unsigned okm = __ballot_sync(0xffffffffu, rok);
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              const uint32_t stg = img0 + cc * 16384u + q4 * 4096;
+              float p1[4] = {0.f, 0.f, 0.f, 0.f}, p2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+              for (int r = 0; r < 32; ++r) {
+                float x;
+                asm volatile("ld.shared.f32 %0, [%1];"
+                             : "=f"(x)
+                             : "r"(stg + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4));
+                x = ((okm >> r) & 1u) ? x : 0.f;
+                p1[r & 3] += x;
+                p2[r & 3] = fmaf(x, x, p2[r & 3]);
+              }
+              red[q4 * BN + (c0 + cc) * 32 + lane] = (p1[0] + p1[1]) + (p1[2] + p1[3]);
+              red[4 * BN + q4 * BN + (c0 + cc) * 32 + lane] = (p2[0] + p2[1]) + (p2[2] + p2[3]);
+            }
+          }
+        }
+        __syncwarp();
+      }
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = eg * CPG; c < (batched ? eg * CPG : (eg + 1) * CPG); ++c) {
         float v[32];
         if (nkb > 0) {
           ptx::tmem_ld32(taddr + c * 32, v);
@@ -1226,15 +1325,15 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
           // pieces. DGRAD accumulation loads all eight old segments before adding (same fp32 add).
           // With p.tma_store the four warps' blocks form the tile's 128 x 32 SWIZZLE_128B image and
           // one thread hands it to the TMA (a plain store, or an fp32 add-reduce for accumulation).
-          const uint32_t img = sbase + SM::STG_OFF + (NSTG == 2 ? (chunk_seq & 1u) * 16384u : 0u);
+          const uint32_t img = sbase + SM::STG_OFF + eg * (NSTG * 16384u) + (NSTG == 2 ? (chunk_seq & 1u) * 16384u : 0u);
           ++chunk_seq;
-          const uint32_t stg = img + warp * 4096;
+          const uint32_t stg = img + q4 * 4096;
           if (p.tma_store) {  // the TMA store that last used this staging image must have read it
-            if (tid == 0) {
+            if (etid == 0) {
               if constexpr (NSTG == 2) ptx::bulk_wait_read1();
               else ptx::bulk_wait_read0();
             }
-            asm volatile("bar.sync 2, 128;" ::: "memory");
+            ptx::named_bar_sync(2 + 2 * eg, 128);
           }
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
@@ -1244,8 +1343,8 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
           __syncwarp();
           if (p.tma_store) {
             ptx::fence_proxy_async_smem();
-            asm volatile("bar.sync 2, 128;" ::: "memory");
-            if (tid == 0) {
+            ptx::named_bar_sync(2 + 2 * eg, 128);
+            if (etid == 0) {
               if (p.tma_store == 1) {
                 const int mt_i = m0 / BM;
                 const int tw_i = mt_i % p.tiles_w, th_i = (mt_i / p.tiles_w) % p.tiles_h, tn_i = mt_i / (p.tiles_w * p.tiles_h);
@@ -1302,8 +1401,8 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
                 p1[r & 3] += x;
                 p2[r & 3] = fmaf(x, x, p2[r & 3]);
               }
-              red[warp * BN + c * 32 + lane] = (p1[0] + p1[1]) + (p1[2] + p1[3]);
-              red[4 * BN + warp * BN + c * 32 + lane] = (p2[0] + p2[1]) + (p2[2] + p2[3]);
+              red[q4 * BN + c * 32 + lane] = (p1[0] + p1[1]) + (p1[2] + p1[3]);
+              red[4 * BN + q4 * BN + c * 32 + lane] = (p2[0] + p2[1]) + (p2[2] + p2[3]);
             }
           }
           __syncwarp();
@@ -1318,8 +1417,8 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
             }
             float s1 = warp_transpose_sum32(v, lane);
             float s2 = warp_transpose_sum32(sq, lane);
-            red[warp * BN + c * 32 + lane] = s1;
-            red[4 * BN + warp * BN + c * 32 + lane] = s2;
+            red[q4 * BN + c * 32 + lane] = s1;
+            red[4 * BN + q4 * BN + c * 32 + lane] = s2;
           }
         }
       }
@@ -1328,9 +1427,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
       ptx::mbar_arrive(&tempty[ab]);
       if constexpr (MODE == CONV_FWD) {
         if (stats) {
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          ptx::named_bar_sync(1 + 2 * eg, 128);
           const int mt_idx = m0 / BM;
-          for (int jj = tid; jj < BN; jj += 128) {
+          for (int jj = eg * (BN / NEG) + etid; jj < (eg + 1) * (BN / NEG); jj += 128) {
             int n = n0 + jj;
             if (n < p.Ng) {
               float a = ((red[jj] + red[BN + jj]) + red[2 * BN + jj]) + red[3 * BN + jj];
@@ -1343,7 +1442,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX), 1)
       }
     }
   }
-  if (tid == 0 && p.tma_store) ptx::bulk_wait0();  // the epilogue's TMA stores are complete
+  if ((tid == 0 || (E2 && tid == 128)) && p.tma_store) ptx::bulk_wait0();  // the epilogue's TMA stores are complete
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 8) {
