@@ -50,7 +50,7 @@ bool conv_shape_ok(const ConvGeom& g) {
 static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
 template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false, bool MNW = false,
-          bool E2 = false>
+          bool E2 = false, bool SP = false, bool W2 = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr,
                                  const CUtensorMap* td = nullptr) {
@@ -63,16 +63,16 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   // (one column chunk per group per tile), so the ring keeps its depth
   constexpr int NEG = E2 ? 2 : 1;
   constexpr int NSTG = (AT && MODE != CONV_WGRAD) ? ((E2 && BN == 64) ? 1 : 2) : 1;
-  constexpr int STAGE_B = GemmSmem<BN, 1, X3, AT, NSTG, NEG>::STAGE_BYTES;
-  constexpr int FIXED_B = GemmSmem<BN, 1, X3, AT, NSTG, NEG>::TOTAL - STAGE_B + 64;
-  constexpr int STAGES_SM = std::max(2, std::min(8, (227 * 1024 - FIXED_B) / STAGE_B));
+  constexpr int STAGE_B = GemmSmem<BN, 1, X3, AT, NSTG, NEG, SP>::STAGE_BYTES;
+  constexpr int FIXED_B = GemmSmem<BN, 1, X3, AT, NSTG, NEG, SP>::TOTAL - STAGE_B + 64;
+  constexpr int STAGES_SM = SP ? 8 : std::max(2, std::min(8, (227 * 1024 - FIXED_B) / std::max(STAGE_B, 1)));
   // AT: each stage also holds 64 TMEM columns (A hi / lo) next to the two accumulators
-  constexpr int STAGES = AT ? std::min(STAGES_SM, (512 - 2 * BN) / 64) : STAGES_SM;
-  constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT, NSTG, NEG>::TOTAL;
+  constexpr int STAGES = AT ? std::min(STAGES_SM, (512 - 2 * BN * (W2 ? 2 : 1)) / 64) : STAGES_SM;
+  constexpr int SMEM = GemmSmem<BN, STAGES, X3, AT, NSTG, NEG, SP>::TOTAL;
   // TMA wgrad at BN = 64 (3xTF32): six blocks of 32x32 per stage -> six auxiliary warps, one
   // block each, instead of four warps doing one or two (the transposes bound these layers)
   constexpr int NAUX = (MODE == CONV_WGRAD && TMA && X3 && BN == 64 && !AT && !XF && !MNW) ? 6 : 4;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX, MNW, E2>;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX, MNW, E2, SP, W2>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -110,6 +110,13 @@ static bool a_in_tmem() {
 // two epilogue warp groups for the AT fwd / dgrad kernels (POOCH_EPI2: 0 off, 1 BN = 128 only,
 // 2 all tile widths, the default: 1x1 expand fwd 23 % and 1x1 reduce dgrad 20 % faster, the
 // rest 0-4 %; profiles/r02_kernel_experiments.md)
+// BN = 64 AT fwd / dgrad with two N = 128 MMAs per k-step over [B; Bs] (igemm.cuh W2;
+// POOCH_W2=0: three N = 64 MMAs)
+static bool w2() {
+  static int on = getenv("POOCH_W2") ? atoi(getenv("POOCH_W2")) : 1;
+  return on != 0;
+}
+
 static int epi2() {
   static int on = getenv("POOCH_EPI2") ? atoi(getenv("POOCH_EPI2")) : 2;
   return on;
@@ -150,9 +157,19 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
     if constexpr (TMA && MODE != GEMM_TEST) {
       // wgrad: A in TMEM pays off at BN = 128 (stages 2-4: 3-12 % faster) but not at BN = 64
       // (stage 1, 6-9 % slower: the extra read-back of the transposed A blocks)
+      if constexpr (MODE == CONV_FWD) {
+        if (p.stem4 == 2) {  // the patch-gather stem (AT, one output tile width of 64)
+          if (bn != 64) return fail(POOCH_EUSAGE, "patch stem: tile width 64 only (got %d)", bn);
+          if (w2()) return launch_igemm<MODE, 64, true, true, false, true, false, true, true, true>(p, grid, st, ta, tb, tc, td);
+          return launch_igemm<MODE, 64, true, true, false, true, false, true, true>(p, grid, st, ta, tb, tc, td);
+        }
+      }
       if (a_in_tmem() && !p.stem4 && (MODE != CONV_WGRAD || bn == 128)) {
         if constexpr (MODE != CONV_WGRAD) {
-          if (epi2() >= 2 && bn == 64) return launch_igemm<MODE, 64, true, true, false, true, false, true>(p, grid, st, ta, tb, tc, td);
+          if (epi2() >= 2 && bn == 64) {
+            if (w2()) return launch_igemm<MODE, 64, true, true, false, true, false, true, false, true>(p, grid, st, ta, tb, tc, td);
+            return launch_igemm<MODE, 64, true, true, false, true, false, true>(p, grid, st, ta, tb, tc, td);
+          }
           if (epi2() >= 1 && bn == 128) return launch_igemm<MODE, 128, true, true, false, true, false, true>(p, grid, st, ta, tb, tc, td);
         }
         switch (bn) {
@@ -301,6 +318,25 @@ static bool fwd_uses_stem4(const ConvGeom& g) {
 }
 static bool dgrad_uses_tma(const ConvGeom& g) { return tma_enabled() && g.K % 32 == 0 && g.stride <= 2; }
 
+// The patch-gather stem (igemm.cuh SP): a 4-channel 2D input, 3xTF32, at most 64 output channels,
+// and the patch under a 16 x 8 output box within 13 KB (the ResNet stem's 7x7 / 2: 37 x 21 pixels,
+// 12.4 KB). POOCH_STEM_PATCH=0 disables it (then the cp.async gathers).
+struct StemBox { int tw, th, pw, ph; };
+static StemBox stem_box(const ConvGeom& g) {
+  StemBox b{16, 8, 0, 0};
+  if (g.Wo <= 8) { b.tw = 8; b.th = 16; }
+  b.pw = (b.tw - 1) * g.stride + g.S;
+  b.ph = (b.th - 1) * g.stride + g.R;
+  return b;
+}
+static bool fwd_uses_stem_patch(const ConvGeom& g) {
+  static int on = getenv("POOCH_STEM_PATCH") ? atoi(getenv("POOCH_STEM_PATCH")) : 1;
+  if (!on || !tma_enabled() || g.C != 4 || g.is3d() || g.C1 > 0 || g.groups > 1 || !g.prec || g.K > 64) return false;
+  const StemBox b = stem_box(g);
+  // the patch within 16 KB; the weight matrix resident (at most 8 k-blocks of 8 taps)
+  return b.pw * b.ph * 16 <= 13312 && b.pw <= 256 && b.ph <= 256 && g.R * g.S <= 64;
+}
+
 static int pick_bn(int n, int prec = 0) {
   return n <= 64 ? 64 : ((n <= 128 || prec) ? 128 : 256);
 }
@@ -330,6 +366,10 @@ static int64_t out_pixels(const ConvGeom& g) { return (int64_t)out3(g) * g.Ho * 
 
 int conv_stat_tiles(const ConvGeom& g) {
   if (g.groups > 1) return gconv_stat_tiles(g);
+  if (fwd_uses_stem_patch(g)) {
+    const StemBox sb = stem_box(g);
+    return ((g.Wo + sb.tw - 1) / sb.tw) * ((g.Ho + sb.th - 1) / sb.th) * g.N;
+  }
   if (fwd_uses_tma(g) || fwd_uses_stem4(g)) {
     PixBox b = choose_box(out3(g), g.Ho, g.Wo, g.stride, g.sd(), g.is3d());
     return b.tiles_w * b.tiles_h * b.tiles_n;
@@ -380,6 +420,42 @@ pooch_status launch_conv_fwd(const ConvGeom& g, const float* x, const float* w, 
       p.tma_store = 1;
     return launch_bn<CONV_FWD, true>(bn, p, grid, st, g.prec, &ta, &tb, g.C1 > 0 ? &tc : nullptr,
                                      p.tma_store ? &td : nullptr);
+  }
+  if (fwd_uses_stem_patch(g) && !xf_scale) {
+    const StemBox sb = stem_box(g);
+    p.tw = sb.tw; p.th = sb.th; p.tn = 1;
+    p.tiles_w = (g.Wo + sb.tw - 1) / sb.tw; p.tiles_h = (g.Ho + sb.th - 1) / sb.th; p.tiles_n = g.N;
+    p.hout = g.Ho; p.wout = g.Wo; p.n3 = g.N;
+    p.stem4 = 2;
+    p.patch_w = sb.pw;
+    p.Kg = g.R * g.S * 4;
+    p.cchunks = 1;
+    CUtensorMap ta, tb;
+    auto fn = encode_fn();
+    // A: the input patch, box {4 channels, pw, ph, 1 image}, no swizzle (16 B per pixel, dense)
+    cuuint64_t dims[4] = {4, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    cuuint64_t strides[3] = {16, (cuuint64_t)g.W * 16, (cuuint64_t)g.H * g.W * 16};
+    cuuint32_t box[4] = {4, (cuuint32_t)sb.pw, (cuuint32_t)sb.ph, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    // B: the [K][R*S*4] weight matrix, box {32 k, 64 rows}, SWIZZLE_128B (K-major); the last
+    // k-block's columns past R*S*4 are zero-filled
+    cuuint64_t bd[2] = {(cuuint64_t)g.R * g.S * 4, (cuuint64_t)g.K};
+    cuuint64_t bs[1] = {(cuuint64_t)g.R * g.S * 16};
+    cuuint32_t bb[2] = {32, 64};
+    cuuint32_t be[2] = {1, 1};
+    if (fn(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS ||
+        fn(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)w, bd, bs, bb, be, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+      return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (patch stem)");
+    dim3 grid(p.tiles_w * p.tiles_h * p.tiles_n, 1, 1);
+    CUtensorMap td;
+    if (tma_store_enabled() &&
+        map_view4(&td, y, g.K, g.Wo, g.Ho, g.N, g.K, (int64_t)g.Wo * g.K, (int64_t)g.Ho * g.Wo * g.K, sb.tw, sb.th, 1))
+      p.tma_store = 1;
+    return launch_bn<CONV_FWD, true>(64, p, grid, st, g.prec, &ta, &tb, nullptr, p.tma_store ? &td : nullptr);
   }
   if (fwd_uses_stem4(g) && !xf_scale) {
     PixBox b = choose_box(g.N, g.Ho, g.Wo, g.stride, 1, false);

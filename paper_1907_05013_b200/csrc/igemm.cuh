@@ -92,8 +92,11 @@ struct GemmParams {
   // (PIXM, one dgrad class of stride 1), 2 = 2-D {32 cols, 128 rows} of a row-major [M][Ng]
   int tma_store;
   // TMA-fed FWD over a 4-channel input (the stem): a k-block is 8 taps x 4 channels; per tap one
-  // 16-B-wide box of A (SWIZZLE_NONE, the K-major core-matrix layout) and one of B
+  // 16-B-wide box of A (SWIZZLE_NONE, the K-major core-matrix layout) and one of B (stem4 = 1);
+  // stem4 = 2 (SP kernels): one input patch per tile, the A rows gathered from it (patch_w = its
+  // width in pixels)
   int stem4;
+  int patch_w;
   // transform on load (XF kernels): the activation operand (FWD: A = x, WGRAD: x)
   // is relu(xf_scale[c] * v + xf_shift[c]) of the stored tensor; zero padding stays zero
   const float* xf_scale;
@@ -105,23 +108,30 @@ constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per k-block (128 B per row)
 constexpr int NUM_THREADS = 160;
 
-template <int BN, int STAGES, bool X3 = false, bool AT = false, int NSTG = 1, int NEG = 1>
+template <int BN, int STAGES, bool X3 = false, bool AT = false, int NSTG = 1, int NEG = 1, bool SP = false>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   // 3xTF32: the stage also holds the residuals As = A - tf32(A), Bs = B - tf32(B) (AT: As lives
   // in TMEM, the stage is [A][B][Bs])
-  static constexpr int STAGE_BYTES = AT ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
+  // SP: no smem stages (A goes to TMEM from the patch); the whole weight matrix (<= 8 k-blocks)
+  // and its residuals stay resident at offset 0: B of k-block kb at kb * B_BYTES, Bs at + BS_OFF
+  static constexpr int SP_KB = 8;
+  static constexpr int STAGE_BYTES = SP ? 0 : (AT ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * (X3 ? 2 : 1));
   static constexpr int SMALL_OFF = A_BYTES + B_BYTES;
-  static constexpr int BS_OFF = AT ? B_BYTES : SMALL_OFF;  // Bs relative to the B tile
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int RED_OFF = BAR_OFF + (3 * STAGES + 4) * 8 + 16;
+  static constexpr int BS_OFF = SP ? SP_KB * B_BYTES : (AT ? B_BYTES : SMALL_OFF);  // Bs relative to the B tile
+  static constexpr int BAR_OFF = SP ? 2 * SP_KB * B_BYTES : STAGES * STAGE_BYTES;
+  static constexpr int RED_OFF = BAR_OFF + (3 * STAGES + 16) * 8 + 16;
   // epilogue staging: per epilogue warp one 32 x 32 fp32 block (4 KB); together the 128 x 32
   // SWIZZLE_128B image of one column chunk of the tile (1024-B aligned for the TMA store)
   static constexpr int STG_OFF = (RED_OFF + 4 * BN * 4 * 2 + 1023) / 1024 * 1024;
   // NSTG = 2: two staging images, so a column chunk is staged while the TMA still reads the last;
   // NEG = 2 epilogue warp groups, each with its own NSTG images
-  static constexpr int TOTAL = STG_OFF + NEG * NSTG * 4 * 4096 + 1024;
+  // SP: NPB input-patch buffers of up to 13 KB, loaded NPB - 1 tiles ahead
+  static constexpr int NPB = 4;
+  static constexpr int PATCH_BYTES = 13312;
+  static constexpr int PATCH_OFF = STG_OFF + NEG * NSTG * 4 * 4096;
+  static constexpr int TOTAL = PATCH_OFF + (SP ? NPB * PATCH_BYTES : 0) + 1024;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -507,7 +517,7 @@ struct TileMap {
 };
 
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false,
-          int NSTG = 1, int NAUX = 4, bool MNW = false, bool E2 = false>
+          int NSTG = 1, int NAUX = 4, bool MNW = false, bool E2 = false, bool SP = false, bool W2 = false>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
@@ -527,18 +537,32 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
   // only B / Bs from shared memory (A is re-read by every MMA, the dominant smem traffic at BN = 64)
   static_assert(!AT || (X3 && TMA && MODE != GEMM_TEST && (!XF || MODE == CONV_FWD)),
                 "AT: 3xTF32 TMA fwd / dgrad / wgrad (with BN-ReLU on load: fwd only)");
-  static_assert(!AT || 2 * BN + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
+  // W2 (BN = 64, A in TMEM): the weight tile and its residual, adjacent in shared memory, form one
+  // 128-row B operand, so a k-step is two N = 128 MMAs -- lo * [B; Bs] and hi * [B; Bs] -- instead
+  // of three N = 64 ones (an N = 64 tcgen05.mma runs at ~2/3 of the per-flop rate of N = 128, and
+  // each k-block's barrier wait in the issuing thread stalls the narrow ones longer:
+  // tools/mmaprobe). The accumulator is [A*B | A*Bs] (2 * BN columns); the epilogue adds the halves.
+  static_assert(!W2 || (AT && BN == 64 && MODE != CONV_WGRAD && !MNW), "W2: AT fwd / dgrad at BN = 64");
+  constexpr uint32_t ACC_COLS = W2 ? 2u * BN : (uint32_t)BN;  // columns of one accumulator
+  static_assert(!AT || 2 * ACC_COLS + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
   // E2: two epilogue warp groups drain each accumulator, one per half of its columns (the
   // 1x1 expand convs are epilogue-bound: TMEM -> smem staging -> BN partial sums -> TMA store);
   // warps 4-7 (idle besides the one TMA-issuing thread) become group 1, and the TMA producer
   // moves to warp 13 -- the TMEM lane quadrant a warp may read is warp % 4, so 4-7 cover all four
   static_assert(!E2 || (PIXM && X3 && NAUX == 4), "E2: 3xTF32 TMA fwd / dgrad");
   constexpr int NEG = E2 ? 2 : 1;
+  // SP (stem patch, 4-channel input): per tile the producer loads the input patch under the
+  // tile's output box once ((tw - 1) * stride + S wide, (th - 1) * stride + R high, 16 B per pixel,
+  // zero-filled padding) and per k-block only the weight tile; the auxiliary warps gather each
+  // A row's 8 taps x 4 channels from the patch straight into TMEM (hi / lo) -- instead of 16
+  // narrow TMA boxes per k-block (stem4 = 1) or 16-B cp.async gathers
+  static_assert(!SP || (AT && MODE == CONV_FWD && !XF), "SP: AT fwd");
   constexpr int PW = E2 ? 13 : 4;  // first producer warp
   constexpr uint32_t TMEM_COLS = AT ? 512u : 2u * BN;
-  constexpr uint32_t A_TCOL = 2u * BN;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
+  constexpr uint32_t A_TCOL = 2u * ACC_COLS;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
   constexpr bool AUX = igemm_aux(MODE, X3, XF);
-  using SM = GemmSmem<BN, STAGES, X3, AT, NSTG, NEG>;
+  using SM = GemmSmem<BN, STAGES, X3, AT, NSTG, NEG, SP>;
+  static_assert(!W2 || SP || SM::BS_OFF == SM::B_BYTES, "W2: Bs directly after B");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
@@ -546,7 +570,10 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint64_t* rawfull = tempty + 2;     // [STAGES] 3xTF32: raw operands landed (cp.async arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rawfull + STAGES);
+  uint64_t* pfull = rawfull + STAGES;  // [NPB] SP: input patch landed
+  uint64_t* pempty = pfull + SM::NPB;  // [NPB] SP: the auxiliary warps are done with the patch
+  uint64_t* bfull = pempty + SM::NPB;  // SP: the resident weight tiles landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 2);
   float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);  // [4][BN] x2
 
   const int tid = threadIdx.x;
@@ -575,6 +602,11 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
       ptx::mbar_init(&tempty[a], 128 * NEG);
     }
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&rawfull[s], TMA ? 1 : 128);
+    for (int a = 0; a < SM::NPB; ++a) {
+      ptx::mbar_init(&pfull[a], 1);
+      ptx::mbar_init(&pempty[a], 128);
+    }
+    ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 8) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -697,14 +729,48 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
         const uint32_t a_bytes = 32u * p.tw * p.th * p.tn * 4u;
         const uint32_t bytes = a_bytes + (uint32_t)BN * 32u * 4u;
         const int cred = MODE == CONV_FWD ? p.C : p.K;  // reduced channels
-        int it = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int it = 0, jt = 0, jn = 0;
+        if constexpr (SP) {  // the whole weight matrix, once: k-block kb's 64 x 32 tile at kb * B_BYTES
+          ptx::mbar_arrive_expect_tx(bfull, (uint32_t)tm.kb_total * SM::B_BYTES);
+          for (int kb = 0; kb < tm.kb_total; ++kb)
+            ptx::tma_load_2d(sbase + kb * SM::B_BYTES * (W2 ? 2 : 1), &tma_b, bfull, kb * 32, 0);
+        }
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++jt) {
           int m0, n0, kb0, nkb;
           tm.decode(t, m0, n0, kb0, nkb, BN);
           const int mt_i = m0 / BM;
           const int tw_i = mt_i % p.tiles_w;
           const int th_i = (mt_i / p.tiles_w) % p.tiles_h;
           const int tn_i = mt_i / (p.tiles_w * p.tiles_h);
+          if constexpr (SP) {
+            // input patches (box {4, patch_w, patch_h, 1} of the tensor map, zero-filled outside
+            // the image) run NPB - 1 tiles ahead of the k-block relay
+            while (jn <= jt + SM::NPB - 1) {
+              const int tq = blockIdx.x + jn * gridDim.x;
+              if (tq < ntiles) {
+                int qm0, qn0, qkb0, qnkb;
+                tm.decode(tq, qm0, qn0, qkb0, qnkb, BN);
+                const int qi = qm0 / BM;
+                const int qw = qi % p.tiles_w, qh = (qi / p.tiles_w) % p.tiles_h, qn = qi / (p.tiles_w * p.tiles_h);
+                const int pb = jn % SM::NPB;
+                if (jn >= SM::NPB) ptx::mbar_wait(&pempty[pb], ((jn / SM::NPB) - 1) & 1);
+                ptx::mbar_arrive_expect_tx(&pfull[pb], (uint32_t)p.patch_w * ((p.th - 1) * p.stride + p.R) * 16u);
+                ptx::tma_load_4d(sbase + SM::PATCH_OFF + pb * SM::PATCH_BYTES, &tma_a, &pfull[pb], 0,
+                                 qw * p.tw * p.stride - p.pad, qh * p.th * p.stride - p.pad, qn);
+              }
+              ++jn;
+            }
+            (void)tw_i; (void)th_i; (void)tn_i;
+#ifdef POOCH_SP_RELAY
+            // (experiment) per k-block a relay: TMEM stage s is free again once its MMAs are done
+            for (int kb = 0; kb < nkb; ++kb, ++it) {
+              const int s = it % STAGES;
+              if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+              ptx::mbar_arrive(&rawfull[s]);
+            }
+#endif
+            continue;
+          }
           // the k-block walks (tap, 32-channel chunk) with the chunk fastest: decode k = kb0 once per
           // tile, then advance incrementally (no per-k-block divisions in the single issuing thread,
           // which otherwise paces the narrow BN = 64 tiles)
@@ -819,9 +885,27 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
     // input coordinates (hb, wb) and whether the row is an output pixel at all
     int hb[8], wb[8];
     unsigned rowv = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int jt = 0;
+    if constexpr (SP) {  // residuals of the resident weight tiles, once
+      ptx::mbar_wait(bfull, 0);
+      // W2: B of k-block kb at kb * 2 * B_BYTES and its residual right after it; else Bs at + BS_OFF
+      const int nch = tm.kb_total * SM::B_BYTES / 16, cpb = SM::B_BYTES / 16;
+      for (int c = stid; c < nch; c += 128) {
+        const uint32_t src = W2 ? sbase + (c / cpb) * 2 * SM::B_BYTES + (c % cpb) * 16 : sbase + c * 16;
+        split_chunk(src, W2 ? src + SM::B_BYTES : src + SM::BS_OFF);
+      }
+    }
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++jt) {
       int m0, n0, kb0, nkb;
       tm.decode(t, m0, n0, kb0, nkb, BN);
+      // SP: this thread's A row = output pixel (ph, pw) of the tile box; its taps read patch pixels
+      // (ph * stride + r, pw * stride + s); (tr, ts) walks the taps of the k-block incrementally
+      const int sp_row = 32 * (warp & 3) + lane;
+      const bool sp_ok = sp_row < p.tw * p.th;
+      const uint32_t sp_base = sbase + SM::PATCH_OFF + (jt % SM::NPB) * SM::PATCH_BYTES +
+                               (uint32_t)(((sp_row / p.tw) * p.stride * p.patch_w + (sp_row % p.tw) * p.stride) * 16);
+      int tr = 0, ts = 0, tap = 0;
+      if constexpr (SP) ptx::mbar_wait(&pfull[jt % SM::NPB], (jt / SM::NPB) & 1);
       if constexpr (XF && MODE == CONV_FWD) {
         const int mt_i = m0 / BM;
         const int tw_i = mt_i % p.tiles_w, th_i = (mt_i / p.tiles_w) % p.tiles_h, tn_i = mt_i / (p.tiles_w * p.tiles_h);
@@ -894,6 +978,11 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
             wshl[q] = __ldg(p.xf_shift + ch + lane);
           }
         }
+#ifndef POOCH_SP_RELAY
+        if constexpr (SP) {  // TMEM stage s is free once the MMAs that read it are done (no relay)
+          if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        } else
+#endif
         ptx::mbar_wait(&rawfull[s], (it / STAGES) & 1);
         uint32_t st = sbase + s * SM::STAGE_BYTES;
         if constexpr (MNW && AT) {
@@ -1025,11 +1114,30 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
           {
             const int row = 32 * (warp & 3) + lane;
             float v[32], lo[32];
+            if constexpr (SP) {  // taps 8 (kb0 + kb) .. +7 of this row from the patch (zeros past R*S)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (sp_ok && tap < p.R * p.S && p.epi_direct != 6) {  // 6: timing experiment, no gathers
+                  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                               : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
+                               : "r"(sp_base + (uint32_t)((tr * p.patch_w + ts) * 16)));
+                } else {
+                  v[4 * j] = v[4 * j + 1] = v[4 * j + 2] = v[4 * j + 3] = 0.f;
+                }
+                ++tap;
+                if (++ts == p.S) {
+                  ts = 0;
+                  ++tr;
+                }
+              }
+              if (kb == nkb - 1) ptx::mbar_arrive(&pempty[jt % SM::NPB]);  // the patch is in registers
+            } else {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                            : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
                            : "r"(st + row * 128 + ((j ^ (row & 7)) << 4)));
+            }
             if constexpr (XF) {  // BN-ReLU on load: channel i's scale / shift from lane i
               const bool valid = xvalid & 1u;
 #pragma unroll
@@ -1045,14 +1153,18 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
               v[i] = hi;
             }
             const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + A_TCOL + 64u * s;
-            ptx::tmem_st32(ta, v);
-            ptx::tmem_st32(ta + 32, lo);
+            if (!SP || p.epi_direct < 7) {  // 7 / 8: timing experiments (SP), no TMEM writes
+              ptx::tmem_st32(ta, v);
+              ptx::tmem_st32(ta + 32, lo);
+            }
           }
-          // B: residuals in shared memory, as in the plain 3xTF32 path
+          // B: residuals in shared memory, as in the plain 3xTF32 path (SP: resident, split once)
           constexpr int BCH = BN * BK / 4;
+          if constexpr (!SP) {
 #pragma unroll 4
-          for (int c = stid; c < BCH; c += 128)
-            split_chunk(st + SM::A_BYTES + c * 16, st + SM::A_BYTES + SM::BS_OFF + c * 16);
+            for (int c = stid; c < BCH; c += 128)
+              split_chunk(st + SM::A_BYTES + c * 16, st + SM::A_BYTES + SM::BS_OFF + c * 16);
+          }
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
         } else {
@@ -1077,15 +1189,15 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
       const int ab = j & 1;
       if (j >= 2) ptx::mbar_wait(&tempty[ab], ((j >> 1) - 1) & 1);
       ptx::tc_fence_after();
-      const uint32_t acc = tmem + ab * BN;
+      const uint32_t acc = tmem + ab * ACC_COLS;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         int s = it % STAGES;
         ptx::mbar_wait(&full[s], (it / STAGES) & 1);
         ptx::tc_fence_after();
         if (lane == 0) {
           uint32_t sa = sbase + s * SM::STAGE_BYTES;
-          uint32_t sb = sa + SM::A_BYTES;
-          const bool sw = TMA && !p.stem4;  // SWIZZLE_128B tiles, else the SWIZZLE_NONE core-matrix layout
+          uint32_t sb = SP ? sbase + (kb0 + kb) * SM::B_BYTES * (W2 ? 2 : 1) : sa + SM::A_BYTES;
+          const bool sw = TMA && p.stem4 != 1;  // SWIZZLE_128B tiles, else the SWIZZLE_NONE core-matrix layout
           if constexpr (MNW) {
             // MN-major SWIZZLE_128B_BASE32B: a 4 KB block per 32 rows of A / B (LBO = 4096 between
             // them), pixel rows of 128 B, 4-row K groups 512 B apart (SBO); a k-step of 8 pixels
@@ -1123,7 +1235,13 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
             const uint32_t la = sw ? 16 : A_LBO, lb = sw ? 16 : B_LBO, sbo = sw ? 1024 : 128, lay = sw ? 2 : 0;
             uint64_t ad = ptx::smem_desc(sa + ka, la, sbo, lay);
             uint64_t bd = ptx::smem_desc(sb + kbo, lb, sbo, lay);
-            if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs from smem
+            if constexpr (W2) {  // [B; Bs] as one 128-row operand: lo first, then hi
+              constexpr uint32_t IDESC_W2 = ptx::idesc_tf32(BM, 2 * BN, false, false);
+              const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
+              ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_W2, (kb | kk) != 0 ? 1u : 0u);
+              ptx::mma_tf32_ts(acc, ta, bd, IDESC_W2, 1u);
+              (void)ad;
+            } else if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs from smem
               const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
               uint64_t bsd = ptx::smem_desc(sb + SM::BS_OFF + kbo, lb, sbo, lay);
               ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
@@ -1168,6 +1286,11 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
       const int ab = j & 1;
       ptx::mbar_wait_sleep(&tfull[ab], (j >> 1) & 1);
       ptx::tc_fence_after();
+      if (p.epi_direct == 8) {  // timing experiment: hand the accumulator straight back
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[ab]);
+        continue;
+      }
       int gm = m0 + row;
       bool rok = gm < p.M;
       if constexpr (PIXM) {  // row -> (n, h, w) of the tile's pixel box
@@ -1183,7 +1306,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
         else
           gm = (nn * p.hout + hh) * p.wout + ww;
       }
-      const uint32_t taddr = tmem + ab * BN + ((uint32_t)(q4 * 32) << 16);
+      const uint32_t taddr = tmem + ab * ACC_COLS + ((uint32_t)(q4 * 32) << 16);
       const int z = t / (tm.mt * tm.nt);
       bool stats = false;
       if constexpr (MODE == CONV_FWD) stats = p.stat_sum != nullptr && p.epi_direct != 3;  // 3: experiment
@@ -1271,6 +1394,12 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
         float v[32];
         if (nkb > 0) {
           ptx::tmem_ld32(taddr + c * 32, v);
+          if constexpr (W2) {  // + the A * Bs half
+            float v2[32];
+            ptx::tmem_ld32(taddr + BN + c * 32, v2);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += v2[i];
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
