@@ -266,6 +266,12 @@ pooch_status pooch_profile(pooch_ctx* ctx, int32_t iters, pooch_profile_t* out);
 pooch_status pooch_set_profile(pooch_ctx* ctx, const int64_t* fwd_ns, const int64_t* bwd_ns,
                                const int64_t* rec_ns, const int64_t* d2h_ns, const int64_t* h2d_ns,
                                int64_t tail_ns);
+/* Replace the probed host-link rates (GB/s; e.g. the most pessimistic over DP ranks, so every
+ * rank plans the same). d2h / h2d: one direction alone; duplex: each direction while both run.
+ * The planner's link model uses duplex / d2h and duplex / h2d (DESIGN.md Reading 51); duplex = 0
+ * turns it off (independent lanes). Any plan is invalidated. EUSAGE on a negative rate, or
+ * d2h / h2d <= 0 with duplex > 0. */
+pooch_status pooch_set_link(pooch_ctx* ctx, double d2h_gbs, double h2d_gbs, double duplex_gbs);
 
 /* ----------------------------------------------------------------- host-only planning */
 /* A planning problem in plain arrays (host memory): the simulator's input (Sec. 4.1.2).
@@ -288,6 +294,12 @@ typedef struct {
   int64_t tail_ns;
   const uint8_t* is_conv;    /* nullable: 1 for convolution tasks (SuperNeurons rule only) */
   uint64_t host_budget_bytes; /* pinned host bytes for the swap class; 0 = unlimited */
+  /* Shared host link (DESIGN.md Reading 51): the rate, per mille of its profiled (one-direction)
+   * rate, at which a D2H / H2D copy progresses while the other copy lane is busy -- the probed
+   * duplex bandwidth over the single-direction one. 0 or 1000 = independent lanes (each copy takes
+   * exactly its profiled time, the plain reading of P:L165-167); valid range 1..1000. */
+  int32_t duplex_d2h_permille;
+  int32_t duplex_h2d_permille;
 } pooch_problem;
 
 typedef struct {

@@ -10,6 +10,14 @@ source (Readings are numbered as in DESIGN.md):
 
 Lanes: COMPUTE, D2H, H2D, one task at a time each (Reading 10).
 
+Shared host link (Reading 51): a copy's profiled time is its duration with
+  the other copy lane idle; while both copy lanes are busy the D2H copy
+  progresses at duplex_d2h / 1000 and the H2D copy at duplex_h2d / 1000 of
+  that rate (the probed duplex over single-direction bandwidth, per mille).
+  Work is kept in integer ns x 1000; a copy ends at the first integer ns at
+  which its remaining work is <= 0. duplex = 1000 (the default) is the plain
+  model in which each copy takes exactly its profiled time.
+
 COMPUTE program: F(0..n-1) in topological order; then for o = n-1..0 the
   recompute tasks bwd(o) needs that are not yet regenerated (recursively,
   P:L114-116 "recomputation recursively"; inputs before outputs), then B(o).
@@ -65,7 +73,8 @@ class Profile:
     swap-out/in ns, graph (inputs, needs), resident base, budget, tail."""
 
     def __init__(self, fwd, bwd, nbytes, d2h, h2d, inputs, needs, resident=0,
-                 budget=1 << 62, rec=None, tail=0, is_conv=None, host_budget=None):
+                 budget=1 << 62, rec=None, tail=0, is_conv=None, host_budget=None,
+                 duplex=(1000, 1000)):
         self.n = len(fwd)
         self.fwd, self.bwd, self.bytes = list(fwd), list(bwd), list(nbytes)
         self.d2h, self.h2d = list(d2h), list(h2d)
@@ -75,6 +84,8 @@ class Profile:
         self.resident, self.budget, self.tail = resident, budget, tail
         self.is_conv = [False] * self.n if is_conv is None else [bool(v) for v in is_conv]
         self.host_budget = host_budget      # pinned host bytes for the swap class (None: unlimited)
+        self.duplex_d2h, self.duplex_h2d = int(duplex[0]), int(duplex[1])   # Reading 51
+        assert 0 < self.duplex_d2h <= 1000 and 0 < self.duplex_h2d <= 1000
         for i in range(self.n):
             assert all(j < i for j in self.inputs[i]), "inputs must be topological"
             assert self.fwd[i] > 0 and self.bwd[i] > 0 and self.rec[i] > 0
@@ -195,10 +206,10 @@ def simulate(p: Profile, cls, sched=EAGER, budget=None) -> Result:
     c_run = None          # (q, end)
     start_of = [None] * P
     end_of = [None] * P
-    d_run = None          # (m, end)
+    d_run = None          # [m, remaining work (ns x 1000), event index]
     d_ready = {}          # m -> ready time
     out_end = {}
-    h_run = None
+    h_run = None          # [m, remaining work (ns x 1000), event index]
     hq = 0
     in_end = {}
     fwd_done = 0
@@ -230,13 +241,15 @@ def simulate(p: Profile, cls, sched=EAGER, budget=None) -> Result:
                     d_ready[m] = t
                 if fwd_done == n:
                     fwd_end = t
-        if d_run is not None and d_run[1] == t:
+        if d_run is not None and d_run[1] <= 0:
             m = d_run[0]
             live -= size[m]
             out_end[m] = t
+            res.events[d_run[2]] = res.events[d_run[2]][:4] + (t,)
             d_run = None
-        if h_run is not None and h_run[1] == t:
+        if h_run is not None and h_run[1] <= 0:
             in_end[h_run[0]] = t
+            res.events[h_run[2]] = res.events[h_run[2]][:4] + (t,)
             h_run = None
         # ---- starts at t (COMPUTE, D2H, H2D)
         if c_run is None and pc < P:
@@ -256,8 +269,8 @@ def simulate(p: Profile, cls, sched=EAGER, budget=None) -> Result:
         if d_run is None and d_ready:
             m = min(d_ready, key=lambda k: (d_ready[k], k))
             del d_ready[m]
-            d_run = (m, t + p.d2h[m])
-            res.events.append(("D2H", "O", m, t, t + p.d2h[m]))
+            d_run = [m, 1000 * p.d2h[m], len(res.events)]
+            res.events.append(("D2H", "O", m, t, None))     # end set at completion
         if h_run is None and hq < len(fifo):
             m = fifo[hq]
             if sched == EAGER:
@@ -271,16 +284,30 @@ def simulate(p: Profile, cls, sched=EAGER, budget=None) -> Result:
                     live + size[m] + headroom(m) <= budget:
                 live += size[m]
                 peak = max(peak, live)
-                h_run = (m, t + p.h2d[m])
-                res.events.append(("H2D", "I", m, t, t + p.h2d[m]))
+                h_run = [m, 1000 * p.h2d[m], len(res.events)]
+                res.events.append(("H2D", "I", m, t, None))
                 hq += 1
-        # ---- advance
-        ends = [x[1] for x in (c_run, d_run, h_run) if x is not None]
+        # ---- advance (copy rates: Reading 51)
+        both = d_run is not None and h_run is not None
+        rd = p.duplex_d2h if both else 1000
+        rh = p.duplex_h2d if both else 1000
+        ends = []
+        if c_run is not None:
+            ends.append(c_run[1])
+        if d_run is not None:
+            ends.append(t + -(-d_run[1] // rd))       # ceil(remaining / rate)
+        if h_run is not None:
+            ends.append(t + -(-h_run[1] // rh))
         if not ends:
             if pc < P or hq < len(fifo) or d_ready:
                 res.oom = True
             break
-        t = min(ends)
+        t_next = min(ends)
+        if d_run is not None:
+            d_run[1] -= (t_next - t) * rd
+        if h_run is not None:
+            h_run[1] -= (t_next - t) * rh
+        t = t_next
 
     res.peak = peak
     if res.oom:

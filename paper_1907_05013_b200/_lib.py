@@ -65,7 +65,8 @@ class Problem(C.Structure):
                 ("d2h_ns", P(c_i64)), ("h2d_ns", P(c_i64)), ("bytes", P(c_u64)),
                 ("in_ptr", P(c_i32)), ("in_idx", P(c_i32)), ("need_ptr", P(c_i32)), ("need_idx", P(c_i32)),
                 ("resident_bytes", c_u64), ("budget_bytes", c_u64), ("tail_ns", c_i64), ("is_conv", P(C.c_uint8)),
-                ("host_budget_bytes", c_u64)]
+                ("host_budget_bytes", c_u64), ("duplex_d2h_permille", C.c_int32),
+                ("duplex_h2d_permille", C.c_int32)]
 
 
 class SimResult(C.Structure):
@@ -104,6 +105,7 @@ SIGNATURES = {
     "pooch_set_param": (c_i32, [c_vp, c_i32, c_i32, P(c_f32), c_i64]),
     "pooch_profile": (c_i32, [c_vp, c_i32, P(ProfileT)]),
     "pooch_set_profile": (c_i32, [c_vp, P(c_i64), P(c_i64), P(c_i64), P(c_i64), P(c_i64), c_i64]),
+    "pooch_set_link": (c_i32, [c_vp, c_f64, c_f64, c_f64]),
     "pooch_simulate": (c_i32, [P(Problem), P(C.c_uint8), c_i32, P(SimResult)]),
     "pooch_plan_problem": (c_i32, [P(Problem), c_i32, P(SearchCfg), P(C.c_uint8), P(C.c_uint8), P(PlanReport)]),
     "pooch_pack_problem": (c_i32, [P(Problem), P(C.c_uint8), c_i32, c_u64, P(c_u64), P(c_i32), P(c_i32), P(c_u64),

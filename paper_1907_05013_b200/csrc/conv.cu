@@ -131,6 +131,12 @@ static pooch_status launch_bn(int bn, const GemmParams& p, dim3 grid, cudaStream
       if (prec) {
         if constexpr (MODE == CONV_FWD) {  // the A operand (rebuilt on load) goes to TMEM
           if (a_in_tmem()) {
+            // the plain AT kernels' epilogue groups and BN = 64 MMA split (E2, W2), so the fused
+            // step stays bit-identical to the plain one (W2 sums A*B and A*Bs separately)
+            if (epi2() >= 2 && bn == 64 && w2())
+              return launch_igemm<MODE, 64, true, true, true, true, false, true, false, true>(p, grid, st, ta, tb, tc, td);
+            if (epi2() >= 1 && bn == 128)
+              return launch_igemm<MODE, 128, true, true, true, true, false, true>(p, grid, st, ta, tb, tc, td);
             switch (bn) {
               case 64: return launch_igemm<MODE, 64, true, true, true, true>(p, grid, st, ta, tb, tc, td);
               case 128: return launch_igemm<MODE, 128, true, true, true, true>(p, grid, st, ta, tb, tc, td);

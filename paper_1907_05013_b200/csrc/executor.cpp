@@ -1023,6 +1023,14 @@ static Problem make_problem(pooch_ctx* c, uint64_t budget) {
   p.tail = c->tail_ns;
   // pinned host arena (each swapped map padded to 256 B); 1 = no host arena at all
   p.host_budget = c->host_bytes > (uint64_t)n * 256 ? c->host_bytes - (uint64_t)n * 256 : 1;
+  // shared host link (Reading 51): each direction's rate while the other is busy, from the probe
+  // (POOCH_DUPLEX=0: independent lanes)
+  static const int duplex_on = getenv("POOCH_DUPLEX") ? atoi(getenv("POOCH_DUPLEX")) : 1;
+  if (duplex_on && c->duplex_gbs > 0 && c->d2h_gbs > 0 && c->h2d_gbs > 0) {
+    auto permille = [](double r) { return (int)std::max(1.0, std::min(1000.0, std::floor(1000.0 * r))); };
+    p.duplex_d2h = permille(c->duplex_gbs / c->d2h_gbs);
+    p.duplex_h2d = permille(c->duplex_gbs / c->h2d_gbs);
+  }
   return p;
 }
 
@@ -1319,6 +1327,17 @@ extern "C" pooch_status pooch_set_profile(pooch_ctx* c, const int64_t* fwd, cons
       return ctx_fail(c, fail(POOCH_EUSAGE, "profile times must be positive"));
   c->tail_ns = tail_ns;
   c->have_profile = true;
+  c->have_plan = false;
+  return POOCH_OK;
+}
+
+extern "C" pooch_status pooch_set_link(pooch_ctx* c, double d2h_gbs, double h2d_gbs, double duplex_gbs) {
+  if (!c) return fail(POOCH_EUSAGE, "null context");
+  if (d2h_gbs < 0 || h2d_gbs < 0 || duplex_gbs < 0 || (duplex_gbs > 0 && (d2h_gbs <= 0 || h2d_gbs <= 0)))
+    return fail(POOCH_EUSAGE, "bad link rates %g / %g / %g GB/s", d2h_gbs, h2d_gbs, duplex_gbs);
+  c->d2h_gbs = d2h_gbs;
+  c->h2d_gbs = h2d_gbs;
+  c->duplex_gbs = duplex_gbs;
   c->have_plan = false;
   return POOCH_OK;
 }
@@ -2190,6 +2209,12 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
   for (int m = 0; m < n; ++m)
     if (c->map_bytes[m] * 2 <= std::min<size_t>(c->host_bytes, dyn)) big = std::max<uint64_t>(big, c->map_bytes[m]);
   if (big > 0) {
+    // median of three (the rate enters the simulator's link model, Reading 51)
+    std::vector<float> tms;
+    cudaEvent_t a, b2;
+    POOCH_CUDA(cudaEventCreate(&a));
+    POOCH_CUDA(cudaEventCreate(&b2));
+    for (int rep = 0; rep < 3; ++rep) {
     float ms;
     POOCH_CUDA(cudaEventRecord(e0, st));
     POOCH_CUDA(cudaStreamWaitEvent(c->s[1], e0, 0));
@@ -2197,9 +2222,6 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
     POOCH_CUDA(cudaMemcpyAsync(c->host, c->dev + c->resident_end, big, cudaMemcpyDeviceToHost, c->s[1]));
     POOCH_CUDA(cudaMemcpyAsync(c->dev + c->resident_end + align_up(big), c->host + align_up(big), big,
                                cudaMemcpyHostToDevice, c->s[2]));
-    cudaEvent_t a, b2;
-    POOCH_CUDA(cudaEventCreate(&a));
-    POOCH_CUDA(cudaEventCreate(&b2));
     POOCH_CUDA(cudaEventRecord(a, c->s[1]));
     POOCH_CUDA(cudaEventRecord(b2, c->s[2]));
     POOCH_CUDA(cudaStreamWaitEvent(st, a, 0));
@@ -2207,7 +2229,10 @@ extern "C" pooch_status pooch_profile(pooch_ctx* c, int32_t iters, pooch_profile
     POOCH_CUDA(cudaEventRecord(e1, st));
     POOCH_CUDA(cudaEventSynchronize(e1));
     POOCH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    c->duplex_gbs = big / (ms * 1e6);
+    tms.push_back(ms);
+    }
+    std::sort(tms.begin(), tms.end());
+    c->duplex_gbs = big / (tms[1] * 1e6);
     cudaEventDestroy(a);
     cudaEventDestroy(b2);
   }

@@ -420,6 +420,13 @@ bool problem_from_c(const pooch_problem& p, Problem& o, std::string& err) {
   o.budget = p.budget_bytes;
   o.tail = p.tail_ns;
   o.host_budget = p.host_budget_bytes;
+  if (p.duplex_d2h_permille < 0 || p.duplex_d2h_permille > 1000 || p.duplex_h2d_permille < 0 ||
+      p.duplex_h2d_permille > 1000) {
+    err = "duplex_*_permille must be in 0..1000";
+    return false;
+  }
+  o.duplex_d2h = p.duplex_d2h_permille > 0 ? p.duplex_d2h_permille : 1000;
+  o.duplex_h2d = p.duplex_h2d_permille > 0 ? p.duplex_h2d_permille : 1000;
   o.is_conv.assign(p.n, 0);
   if (p.is_conv)
     for (int i = 0; i < p.n; ++i) o.is_conv[i] = p.is_conv[i] ? 1 : 0;

@@ -42,6 +42,9 @@ struct Problem {
   std::vector<uint8_t> is_conv;
   uint64_t resident = 0, budget = 0;
   uint64_t host_budget = 0;  // 0: unlimited
+  // shared host link (Reading 51): per-mille rate of a D2H / H2D copy while the other copy lane is
+  // busy (probed duplex / single-direction bandwidth); 1000 (or 0) = independent lanes
+  int duplex_d2h = 1000, duplex_h2d = 1000;
   int64_t tail = 0;
 };
 

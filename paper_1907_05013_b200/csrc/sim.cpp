@@ -176,13 +176,18 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
   int64_t c_end = 0;
   s.start_of.assign(P, -1);
   s.end_of.assign(P, -1);
+  // copy lanes: remaining work in ns x 1000 and the start event's index (its end is set at
+  // completion); while both lanes are busy each progresses at its duplex rate (Reading 51)
   int d_m = -1;
-  int64_t d_end = 0;
+  int64_t d_rem = 0;
+  size_t d_ev = 0;
   s.d_ready.assign(n, -1);
   int n_ready = 0;
   s.out_end.assign(n, -1);
   int h_m = -1;
-  int64_t h_end = 0;
+  int64_t h_rem = 0;
+  size_t h_ev = 0;
+  const int64_t dx_d = p.duplex_d2h > 0 ? p.duplex_d2h : 1000, dx_h = p.duplex_h2d > 0 ? p.duplex_h2d : 1000;
   size_t hq = 0;
   s.in_end.assign(n, -1);
   int fwd_done = 0;
@@ -209,14 +214,16 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
         if (fwd_done == n) fwd_end = t;
       }
     }
-    if (d_m >= 0 && d_end == t) {
+    if (d_m >= 0 && d_rem <= 0) {
       live -= s.size[d_m];
       s.out_end[d_m] = t;
+      if (E) ev[d_ev].end = t;
       if (L) led.push_back({t, d_m, false, 0, 1, 'O', d_m});
       d_m = -1;
     }
-    if (h_m >= 0 && h_end == t) {
+    if (h_m >= 0 && h_rem <= 0) {
       s.in_end[h_m] = t;
+      if (E) ev[h_ev].end = t;
       h_m = -1;
     }
     // starts at t: COMPUTE, D2H, H2D
@@ -247,8 +254,9 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
       d_m = best;
       s.d_ready[best] = -1;
       --n_ready;
-      d_end = t + p.d2h[best];
-      if (E) ev.push_back({1, 'O', best, t, d_end});
+      d_rem = 1000 * p.d2h[best];
+      d_ev = ev.size();
+      if (E) ev.push_back({1, 'O', best, t, -1});
     }
     if (h_m < 0 && hq < s.fifo.size()) {
       int m = s.fifo[hq];
@@ -273,22 +281,27 @@ void simulate(const Problem& p, const uint8_t* cls, const SimOptions& opt, SimOu
           live += s.size[m];
           peak = std::max(peak, live);
           h_m = m;
-          h_end = t + p.h2d[m];
-          if (E) ev.push_back({2, 'I', m, t, h_end});
+          h_rem = 1000 * p.h2d[m];
+          h_ev = ev.size();
+          if (E) ev.push_back({2, 'I', m, t, -1});
           if (L) led.push_back({t, n + m, true, 0, 2, 'I', m});
           ++hq;
         }
       }
     }
     // advance
+    const bool both = d_m >= 0 && h_m >= 0;
+    const int64_t rd = both ? dx_d : 1000, rh = both ? dx_h : 1000;
     int64_t nxt = INT64_MAX;
     if (c_q >= 0) nxt = std::min(nxt, c_end);
-    if (d_m >= 0) nxt = std::min(nxt, d_end);
-    if (h_m >= 0) nxt = std::min(nxt, h_end);
+    if (d_m >= 0) nxt = std::min(nxt, t + (d_rem + rd - 1) / rd);
+    if (h_m >= 0) nxt = std::min(nxt, t + (h_rem + rh - 1) / rh);
     if (nxt == INT64_MAX) {
       if (pc < P || hq < s.fifo.size() || n_ready > 0) out.oom = true;
       break;
     }
+    if (d_m >= 0) d_rem -= (nxt - t) * rd;
+    if (h_m >= 0) h_rem -= (nxt - t) * rh;
     t = nxt;
   }
 

@@ -25,6 +25,12 @@ def agree_profile(prof: dict, group=None, device="cpu") -> dict:
     for i, k in enumerate(KEYS):
         out[k] = a[i]
     out["tail"] = a[len(KEYS)][0]
+    # host-link rates (Reading 51): the most pessimistic duplex factor, the same on every rank
+    if "duplex_gbs" in prof:
+        r = torch.tensor([-float(prof["duplex_gbs"]), float(prof["d2h_gbs"]), float(prof["h2d_gbs"])],
+                         dtype=torch.float64, device=device)
+        dist.all_reduce(r, op=dist.ReduceOp.MAX, group=group)
+        out["duplex_gbs"], out["d2h_gbs"], out["h2d_gbs"] = -float(r[0]), float(r[1]), float(r[2])
     return out
 
 

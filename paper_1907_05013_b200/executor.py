@@ -222,6 +222,10 @@ class Context:
         arrs = [np.asarray(v, np.int64) for v in (fwd, bwd, rec, d2h, h2d)]
         self._chk(lib.pooch_set_profile(self.h, *[a.ctypes.data_as(P(C.c_int64)) for a in arrs], int(tail)))
 
+    def set_link(self, d2h_gbs, h2d_gbs, duplex_gbs):
+        """Override the probed host-link rates (GB/s) the planner's link model uses (Reading 51)."""
+        self._chk(lib.pooch_set_link(self.h, float(d2h_gbs), float(h2d_gbs), float(duplex_gbs)))
+
     def plan(self, strategy="pooch", li_cap=16, threads=0, sched=0, fixed=None):
         out = np.zeros(self.n, np.uint8)
         rep = PlanReport()

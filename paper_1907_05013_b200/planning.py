@@ -29,7 +29,7 @@ class PlanProblem:
     """Owns the arrays a pooch_problem points at."""
 
     def __init__(self, fwd, bwd, nbytes, d2h, h2d, inputs, needs, resident=0, budget=(1 << 62),
-                 rec=None, tail=0, is_conv=None, host_budget=None):
+                 rec=None, tail=0, is_conv=None, host_budget=None, duplex=(1000, 1000)):
         self.n = len(fwd)
         self._a = {
             "fwd": np.asarray(fwd, np.int64), "bwd": np.asarray(bwd, np.int64),
@@ -47,7 +47,7 @@ class PlanProblem:
                          a["in_ptr"].ctypes.data_as(P(C.c_int32)), a["in_idx"].ctypes.data_as(P(C.c_int32)),
                          a["need_ptr"].ctypes.data_as(P(C.c_int32)), a["need_idx"].ctypes.data_as(P(C.c_int32)),
                          int(resident), int(budget), int(tail), a["is_conv"].ctypes.data_as(P(C.c_uint8)),
-                         0 if host_budget is None else int(host_budget))
+                         0 if host_budget is None else int(host_budget), int(duplex[0]), int(duplex[1]))
 
     @staticmethod
     def from_dict(d, **kw):

@@ -33,13 +33,17 @@ def _worker(rank, world, port, q):
     g = synthdata.rng(10 + rank)          # rank-specific measurements
     prof = {k: [int(v) for v in g.integers(1000, 50000, n)] for k in ("fwd", "bwd", "rec", "d2h", "h2d")}
     prof["tail"] = int(g.integers(100, 1000))
+    prof.update(d2h_gbs=50.0 + rank, h2d_gbs=55.0 - rank, duplex_gbs=40.0 + 2 * rank)
     agreed = agree_profile(prof)
     nbytes = [8 * net.map_bytes_per_image(i) for i in range(n)]
     pp = PlanProblem(agreed["fwd"], agreed["bwd"], nbytes, agreed["d2h"], agreed["h2d"],
                      [[j for j in t.inputs if j >= 0] for t in net.tasks], [net.needs(i) for i in range(n)],
-                     resident=0, budget=sum(nbytes) // 2, rec=agreed["rec"], tail=agreed["tail"])
+                     resident=0, budget=sum(nbytes) // 2, rec=agreed["rec"], tail=agreed["tail"],
+                     duplex=(int(1000 * agreed["duplex_gbs"] / agreed["d2h_gbs"]),
+                             int(1000 * agreed["duplex_gbs"] / agreed["h2d_gbs"])))
     cls, rep = pp.plan("pooch")
-    q.put((rank, cls, agreed["fwd"][:3], prof["fwd"][:3]))
+    link = (agreed["d2h_gbs"], agreed["h2d_gbs"], agreed["duplex_gbs"])
+    q.put((rank, cls, agreed["fwd"][:3], prof["fwd"][:3], link))
     dist.destroy_process_group()
 
 
@@ -53,8 +57,9 @@ def test_two_ranks_agree_on_one_plan():
     res = sorted(q.get(timeout=120) for _ in ps)
     for p in ps:
         p.join(timeout=60)
-    (r0, c0, a0, p0), (r1, c1, a1, p1) = res
+    (r0, c0, a0, p0, l0), (r1, c1, a1, p1, l1) = res
     assert c0 is not None and c0 == c1
+    assert l0 == l1 == (51.0, 55.0, 40.0)     # slowest link figures over the ranks (Reading 51)
     assert a0 == a1 == [max(x, y) for x, y in zip(p0, p1)]
 
 

@@ -167,3 +167,47 @@ def test_host_fit_base_by_hand():
     assert planner.host_fit_base(prof(9)) == [SWAP, RECOMPUTE, RECOMPUTE, SWAP]
     assert planner.host_fit_base(prof(3)) == [RECOMPUTE, RECOMPUTE, RECOMPUTE, KEEP]
     assert planner.host_fit_base(prof(0)) == [RECOMPUTE, RECOMPUTE, RECOMPUTE, KEEP]
+
+
+# ---- shared host link (Reading 51), hand-traced on a 4-task DAG where a swap-in overlaps a
+# swap-out. Tasks: F0 -> map 0; F1 reads 0 -> map 1; F2 reads 1 -> map 2; F3 reads 2 and 0 ->
+# map 3 (sink). bwd(3) needs {2}, bwd(2) needs {1}, bwd(1) needs {0}. All fwd / bwd 10 ns;
+# maps 0 and 1 swap (d2h 100 / 30, h2d 10 / 40), maps 2, 3 keep; unlimited memory.
+#   F0 [0,10] F1 [10,20] F2 [20,30] F3 [30,40]; forward ends at 40.
+#   O1 ready at 30 (last forward use F2): D2H [30, 60] alone. O0 ready at 40 (F3): waits for the lane.
+#   At 60 O0 starts and I1 starts (eager: forward over, O1 done): both lanes busy.
+#   Independent lanes (1000): I1 [60,100], O0 [60,160], I0 [160,170]; B3 [40,50], B2 [100,110],
+#     B1 [170,180], B0 [180,190]: makespan 190.
+#   duplex (500, 500): I1 needs 40 ns of work at 1/2 -> [60,140]; O0 has done 40 of 100 by 140,
+#     the remaining 60 alone -> ends 200; I0 [200,210]; B2 [140,150], B1 [210,220], B0 [220,230]: 230.
+#   duplex (800, 500): I1 [60,140] (O0 still running at 0.8: would need 125 ns); O0 has done
+#     80 x 0.8 = 64 by 140, 36 alone -> 176; I0 [176,186]; B2 [140,150], B1 [186,196], B0 [196,206].
+#   duplex (1000, 333): I1 work 40000 at 333 per ns -> ceil(40000 / 333) = 121 -> [60,181]; O0 at
+#     full rate ends at 160 first, so at 160 I1 has 40000 - 100 x 333 = 6700 left, alone at 1000 per
+#     ns -> ceil(6.7) = 7 -> ends 167; O0 [60,160]; I0 waits for the H2D lane: [167,177];
+#     B2 [167,177], B1 [177,187], B0 [187,197]: 197.
+def _link_dag(duplex):
+    return Profile([10] * 4, [10] * 4, [1] * 4, [100, 30, 5, 5], [10, 40, 5, 5],
+                   [[], [0], [1], [2, 0]], [[0], [0], [1], [2]], duplex=duplex)
+
+
+@pytest.mark.parametrize("duplex,io,b,makespan", [
+    ((1000, 1000), {"O1": (30, 60), "O0": (60, 160), "I1": (60, 100), "I0": (160, 170)},
+     {3: (40, 50), 2: (100, 110), 1: (170, 180), 0: (180, 190)}, 190),
+    ((500, 500), {"O1": (30, 60), "O0": (60, 200), "I1": (60, 140), "I0": (200, 210)},
+     {2: (140, 150), 1: (210, 220), 0: (220, 230)}, 230),
+    ((800, 500), {"O0": (60, 176), "I1": (60, 140), "I0": (176, 186)},
+     {2: (140, 150), 1: (186, 196), 0: (196, 206)}, 206),
+    ((1000, 333), {"O0": (60, 160), "I1": (60, 167), "I0": (167, 177)},
+     {2: (167, 177), 1: (177, 187), 0: (187, 197)}, 197),
+])
+def test_shared_link_hand_trace(duplex, io, b, makespan):
+    r = simulate(_link_dag(duplex), [SWAP, SWAP, KEEP, KEEP], EAGER)
+    assert not r.oom
+    got = {(k + str(m)): (s, e) for lane, k, m, s, e in r.events if lane != "COMPUTE"}
+    for key, span in io.items():
+        assert got[key] == span, key
+    bw = {m: (s, e) for lane, k, m, s, e in r.events if lane == "COMPUTE" and k == "B"}
+    for m, span in b.items():
+        assert bw[m] == span, m
+    assert r.makespan == makespan

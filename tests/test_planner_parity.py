@@ -58,6 +58,37 @@ def test_sim_differential(seed):
             _cmp_sim(po, pc, cls, sched)
 
 
+@pytest.mark.parametrize("seed", range(40))
+def test_sim_differential_shared_link(seed):
+    """Reading 51: copies slowed while both copy lanes are busy -- same timelines, tolerance 0."""
+    g = synthdata.rng(700 + seed)
+    n = int(g.integers(1, 9))
+    d = synthdata.random_profile(n, seed, dag=seed % 2 == 1)
+    budget = int(10 + sum(d["bytes"]) * g.uniform(0.5, 1.8))
+    dx = (int(g.integers(300, 1001)), int(g.integers(300, 1001)))
+    po, pc = both(d, resident=10, budget=budget, duplex=dx)
+    for _ in range(8):
+        cls = [int(c) for c in g.integers(0, 4, n)]
+        if cls[-1] == OS.RECOMPUTE:
+            cls[-1] = OS.SWAP
+        for sched in (OS.EAGER, OS.NAIVE, OS.SN):
+            _cmp_sim(po, pc, cls, sched)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_pooch_identical_to_oracle_shared_link(seed):
+    d, budget = _tight(seed + 100, 6 + seed % 5)
+    dx = (750 + 10 * seed, 760)
+    po, pc = both(d, resident=10, budget=budget, duplex=dx)
+    ref = OP.pooch(po, li_cap=16)
+    cls, rep = pc.plan("pooch", threads=4)
+    if not ref["feasible"]:
+        assert cls is None
+        return
+    assert cls == ref["cls"]
+    assert rep.makespan_ns == ref["makespan"]
+
+
 def _tight(seed, n):
     d = synthdata.random_profile(n, seed, dag=seed % 3 == 0)
     g = synthdata.rng(91 + seed)
