@@ -50,7 +50,7 @@ bool conv_shape_ok(const ConvGeom& g) {
 static CUtensorMap g_zero_map;  // placeholder parameter for the cp.async paths
 
 template <int MODE, int BN, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false, bool MNW = false,
-          bool E2 = false, bool SP = false, bool W2 = false>
+          bool E2 = false, bool SP = false, bool W2 = false, bool SPW = false>
 static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st, const CUtensorMap* ta = nullptr,
                                  const CUtensorMap* tb = nullptr, const CUtensorMap* tc = nullptr,
                                  const CUtensorMap* td = nullptr) {
@@ -72,7 +72,7 @@ static pooch_status launch_igemm(const GemmParams& p, dim3 grid, cudaStream_t st
   // TMA wgrad at BN = 64 (3xTF32): six blocks of 32x32 per stage -> six auxiliary warps, one
   // block each, instead of four warps doing one or two (the transposes bound these layers)
   constexpr int NAUX = (MODE == CONV_WGRAD && TMA && X3 && BN == 64 && !AT && !XF && !MNW) ? 6 : 4;
-  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX, MNW, E2, SP, W2>;
+  auto kern = igemm_kernel<MODE, BN, STAGES, X3, TMA, XF, AT, NSTG, NAUX, MNW, E2, SP, W2, SPW>;
   static bool configured = false;
   if (!configured) {
     POOCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -115,6 +115,14 @@ static bool a_in_tmem() {
 static bool w2() {
   static int on = getenv("POOCH_W2") ? atoi(getenv("POOCH_W2")) : 1;
   return on != 0;
+}
+// the same for the MN-major A-in-TMEM wgrad at BN = 64 (POOCH_WGRAD_W2: 0 off, 1 the stem patch
+// wgrad only -- the default: 0.88 -> 0.80 ms at batch 256 --, 2 every BN = 64 MN-major wgrad, which
+// measured 0-4 % slower for the stage-1 layers: W2's 128 accumulator columns leave TMEM for 4
+// A stages instead of 6)
+static int wgrad_w2() {
+  static int on = getenv("POOCH_WGRAD_W2") ? atoi(getenv("POOCH_WGRAD_W2")) : 1;
+  return on;
 }
 
 static int epi2() {
@@ -585,17 +593,18 @@ pooch_status launch_conv_dgrad(const ConvGeom& g, const float* dy, const float* 
 // layer does not pad the 128-row A tile (when that is x, A = im2col(x)^T and the reduction
 // transposes the workspace [split][RSC][Cout] into KRSC).
 struct WgradPlan {
-  bool tma, swap;
+  bool tma, swap, spw;
   int bn, mt, nt, kb, splits, kb_per_split;
   PixBox box;
 };
 
-static PixBox choose_kbox(int N3, int Ho, int Wo, int st, int st3) {
+static PixBox choose_kbox(int N3, int Ho, int Wo, int st, int st3, bool one_image = false) {
   PixBox best{};
   int64_t best_boxes = -1;
   for (int tw = 1; tw <= 32; tw *= 2)
     for (int th = 1; tw * th <= 32; th *= 2) {
       int tn = 32 / (tw * th);
+      if (one_image && tn != 1) continue;
       if (tw * st > 256 || th * st > 256 || tn * st3 > 256) continue;
       int64_t tx = (Wo + tw - 1) / tw, ty = (Ho + th - 1) / th, tz = (N3 + tn - 1) / tn;
       int64_t boxes = tx * ty * tz;
@@ -617,21 +626,37 @@ static bool wgrad_uses_tma(const ConvGeom& g) {
   return tma_enabled() && g.C % 32 == 0 && g.K % 32 == 0 && g.stride <= 2;
 }
 
+// The stem-patch wgrad (igemm.cuh SPW): a 4-channel 2D input, 3xTF32, at most 64 output
+// channels, one image per 32-pixel box, the patch under the box within the stage's 16 KB A region.
+// POOCH_STEM_PATCH_WGRAD=0 disables it (then the cp.async gathers).
+static bool wgrad_uses_stem_patch(const ConvGeom& g, const PixBox& b) {
+  static int on = getenv("POOCH_STEM_PATCH_WGRAD") ? atoi(getenv("POOCH_STEM_PATCH_WGRAD")) : 1;
+  if (!on || !tma_enabled() || g.C != 4 || g.is3d() || g.C1 > 0 || g.groups > 1 || !g.prec || g.K > 64 ||
+      g.K % 32 != 0 || g.stride > 2 || !mn_wgrad() || !mn_wgrad_at())
+    return false;
+  const int pw = (b.tw - 1) * g.stride + g.S, ph = (b.th - 1) * g.stride + g.R;
+  return b.tn == 1 && pw <= 256 && ph <= 256 && pw * ph * 16 <= BM * BK * 4;
+}
+
 static WgradPlan wgrad_plan(const ConvGeom& g) {
   WgradPlan w{};
   int rsc = g.T() * g.R * g.S * g.C;
   w.tma = wgrad_uses_tma(g);
+  if (!w.tma && g.C == 4 && !g.is3d()) {
+    const PixBox b = choose_kbox(g.N, g.Ho, g.Wo, g.stride, 1, true);
+    if (wgrad_uses_stem_patch(g, b)) w.tma = w.spw = true;
+  }
   int M = g.K, Ng = rsc;
   w.bn = 128;
   if (w.tma) {
-    w.box = choose_kbox(out3(g), g.Ho, g.Wo, g.stride, g.sd());
-    if (const char* e = getenv("POOCH_KBOX")) {  // profiling experiments only
+    w.box = choose_kbox(out3(g), g.Ho, g.Wo, g.stride, g.sd(), w.spw);
+    if (const char* e = w.spw ? nullptr : getenv("POOCH_KBOX")) {  // profiling experiments only
       int a = 0, b = 0, c = 0;
       if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && a * b * c == 32)
         w.box = PixBox{a, b, c, (g.Wo + a - 1) / a, (g.Ho + b - 1) / b, (out3(g) + c - 1) / c};
     }
     w.kb = w.box.tiles_w * w.box.tiles_h * w.box.tiles_n;
-    if (g.K <= 64 && rsc > 64) {
+    if ((g.K <= 64 && rsc > 64) || w.spw) {
       w.swap = true;
       M = rsc;
       Ng = g.K;
@@ -759,7 +784,7 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
     const bool mn = mn_wgrad() && !p.xf_scale;
     CUtensorMap tdy, tx, tx1;
     if (!map_act_chunks(&tdy, dy, out3(g), g.Ho, g.Wo, g.K, w.box.tw, w.box.th, w.box.tn, 1, 1, cb_dy, mn) ||
-        !map_act_chunks(&tx, x, in3(g), g.H, g.W, c0, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x, mn))
+        (!w.spw && !map_act_chunks(&tx, x, in3(g), g.H, g.W, c0, w.box.tw, w.box.th, w.box.tn, g.stride, st3, cb_x, mn)))
       return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv wgrad)");
     if (g.C1 > 0) {
       p.c_split = g.C1;
@@ -767,6 +792,25 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
                           mn))
         return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (conv wgrad, second source)");
     }
+    if (w.spw) {  // A: the input patch, box {4 channels, pw, ph, 1 image}, no swizzle (16 B per pixel)
+      const int pw = (w.box.tw - 1) * g.stride + g.S, ph = (w.box.th - 1) * g.stride + g.R;
+      p.patch_w = pw;
+      auto fn = encode_fn();
+      cuuint64_t dims[4] = {4, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+      cuuint64_t strides[3] = {16, (cuuint64_t)g.W * 16, (cuuint64_t)g.H * g.W * 16};
+      cuuint32_t box[4] = {4, (cuuint32_t)pw, (cuuint32_t)ph, 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      if (fn(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+        return fail(POOCH_ECUDA, "cuTensorMapEncodeTiled failed (patch wgrad)");
+      if (wgrad_w2() >= 1)
+        POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, true, true, false, false, true, true>(
+            p, grid, st, &tx, &tdy)));
+      else
+        POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, true, true, false, false, false, true>(
+            p, grid, st, &tx, &tdy)));
+    } else {
     const CUtensorMap* ta = w.swap ? &tx : &tdy;
     const CUtensorMap* tb = w.swap ? &tdy : &tx;
     const CUtensorMap* tc = g.C1 > 0 ? &tx1 : nullptr;
@@ -774,7 +818,9 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
       if (g.prec) {
         // A in TMEM (hi / lo gathered from the MN-major blocks) unless POOCH_WGRAD_AT=0
         if (mn_wgrad_at()) {
-          if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, true, true>(p, grid, st, ta, tb, tc)));
+          if (w.bn == 64 && wgrad_w2() >= 2)
+            POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
+          else if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, true, true>(p, grid, st, ta, tb, tc)));
           else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true, true, false, true, true>(p, grid, st, ta, tb, tc)));
         } else if (w.bn == 64) POOCH_CHECK((launch_igemm<CONV_WGRAD, 64, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
         else POOCH_CHECK((launch_igemm<CONV_WGRAD, 128, true, true, false, false, true>(p, grid, st, ta, tb, tc)));
@@ -786,6 +832,7 @@ pooch_status launch_conv_wgrad(const ConvGeom& g, const float* x, const float* d
     } else {
       POOCH_CHECK((launch_bn<CONV_WGRAD, true>(w.bn, p, grid, st, g.prec, ta, tb, tc)));
     }
+    }  // !spw
   } else if (g.is3d() || g.C1 > 0) {
     return fail(POOCH_EUSAGE, "3D / two-source conv needs the TMA path");
   } else if (g.prec) {

@@ -517,7 +517,8 @@ struct TileMap {
 };
 
 template <int MODE, int BN, int STAGES, bool X3 = false, bool TMA = false, bool XF = false, bool AT = false,
-          int NSTG = 1, int NAUX = 4, bool MNW = false, bool E2 = false, bool SP = false, bool W2 = false>
+          int NSTG = 1, int NAUX = 4, bool MNW = false, bool E2 = false, bool SP = false, bool W2 = false,
+          bool SPW = false>
 __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
     igemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d) {
@@ -542,7 +543,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
   // of three N = 64 ones (an N = 64 tcgen05.mma runs at ~2/3 of the per-flop rate of N = 128, and
   // each k-block's barrier wait in the issuing thread stalls the narrow ones longer:
   // tools/mmaprobe). The accumulator is [A*B | A*Bs] (2 * BN columns); the epilogue adds the halves.
-  static_assert(!W2 || (AT && BN == 64 && MODE != CONV_WGRAD && !MNW), "W2: AT fwd / dgrad at BN = 64");
+  // (MN-major wgrad, MNW: the B blocks and their residual blocks are 4 KB apart in one MN-major
+  // run, so [B; Bs] is one 128-row operand with the same LBO)
+  static_assert(!W2 || (AT && BN == 64 && (MODE != CONV_WGRAD || MNW)), "W2: AT fwd / dgrad / MN-major wgrad at BN = 64");
   constexpr uint32_t ACC_COLS = W2 ? 2u * BN : (uint32_t)BN;  // columns of one accumulator
   static_assert(!AT || 2 * ACC_COLS + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
   // E2: two epilogue warp groups drain each accumulator, one per half of its columns (the
@@ -557,6 +560,13 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
   // A row's 8 taps x 4 channels from the patch straight into TMEM (hi / lo) -- instead of 16
   // narrow TMA boxes per k-block (stem4 = 1) or 16-B cp.async gathers
   static_assert(!SP || (AT && MODE == CONV_FWD && !XF), "SP: AT fwd");
+  // SPW (stem patch wgrad, 4-channel input): the transposed MN-major wgrad (A = im2col(x)^T in
+  // TMEM, B = dy^T MN-major) whose A operand is gathered from one input patch per k-block -- the
+  // TMA box {4 channels, (tw - 1) * stride + S, (th - 1) * stride + R, 1 image} under the k-block's
+  // tw x th pixel box, 16 B per pixel, zero-filled padding -- instead of per-tap 32-channel boxes
+  // (a 4-channel input has no 32-channel chunks); lane = row (r, s, c) of A reads pixel k's tap at
+  // patch ((k / tw) * stride + r, (k % tw) * stride + s), channel c
+  static_assert(!SPW || (MODE == CONV_WGRAD && TMA && AT && MNW && X3), "SPW: 3xTF32 MN-major wgrad, A in TMEM");
   constexpr int PW = E2 ? 13 : 4;  // first producer warp
   constexpr uint32_t TMEM_COLS = AT ? 512u : 2u * BN;
   constexpr uint32_t A_TCOL = 2u * ACC_COLS;  // AT: stage s's hi tile at column A_TCOL + 64 s, lo at + 32
@@ -669,8 +679,12 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
             }
             ++nbox;
           };
-          for (int q = 0; q < BM / 32; q += p.wg_cba)
-            if (m0 + 32 * q < p.M) add_box(q * 4096, &tma_a, p.wg_a_is_x != 0, m0 + 32 * q, p.wg_cba);
+          if constexpr (SPW) {
+            bytes += (uint32_t)p.patch_w * ((p.th - 1) * p.stride + p.R) * 16u;
+          } else {
+            for (int q = 0; q < BM / 32; q += p.wg_cba)
+              if (m0 + 32 * q < p.M) add_box(q * 4096, &tma_a, p.wg_a_is_x != 0, m0 + 32 * q, p.wg_cba);
+          }
           for (int q = 0; q < BN / 32; q += p.wg_cbb)
             if (n0 + 32 * q < p.Ng) add_box(SM::A_BYTES + q * 4096, &tma_b, p.wg_a_is_x == 0, n0 + 32 * q, p.wg_cbb);
           int bw = kb0 % p.tiles_w, bh = (kb0 / p.tiles_w) % p.tiles_h, bn = kb0 / (p.tiles_w * p.tiles_h);
@@ -680,6 +694,8 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
             uint32_t st = sbase + s * SM::STAGE_BYTES;
             const int ow = bw * p.tw, oh = bh * p.th, on = bn * p.tn;
             ptx::mbar_arrive_expect_tx(&rawfull[s], bytes);
+            if constexpr (SPW)  // the input patch under the pixel box (A region of the stage)
+              ptx::tma_load_4d(st, &tma_a, &rawfull[s], 0, ow * p.stride - p.pad, oh * p.stride - p.pad, on);
             for (int i = 0; i < nbox; ++i) {
               if (bdx[i] == 0x40000000)
                 ptx::tma_load_5d(st + bdst[i], bmap[i], &rawfull[s], 0, ow, oh, on, bch[i]);
@@ -874,7 +890,7 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
       }
       ptx::cp_async_wait<0>();
     }
-  } else if (AUX && warp >= 9 && warp < 13) {
+  } else if (AUX && warp >= 9 && warp < 9 + NAUX) {  // (E2: warp 13 = 9 + NAUX is the producer)
     // ------------------------------------------------------------------ auxiliary warps
     // Per stage: wait for the raw operands, (wgrad) transpose every 4x4 block in place,
     // (3xTF32) write x - tf32(x) of every chunk, publish to the async proxy, arrive full[].
@@ -998,11 +1014,29 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
             const uint32_t blk = st + bi * 4096;
             if (bi < BM / 32) {
               float v[32], lo[32];
+              if constexpr (SPW) {
+                // row (r, s, c) of im2col(x)^T; pixel k = (k % tw, k / tw) of the box (tw a power of
+                // two, tw * th = 32); rows past R*S*4 are zero
+                const int row = m0 + 32 * bi + lane;
+                const bool ok = row < p.M;
+                const int rs = row >> 2, r = rs / p.S, sx = rs - r * p.S;
+                const uint32_t lb = st + (uint32_t)(((r * p.patch_w + sx) * 4 + (row & 3)) * 4);
+                const int ltw = __ffs(p.tw) - 1;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                  const uint32_t off = (uint32_t)((((k >> ltw) * p.patch_w + (k & (p.tw - 1))) * p.stride) * 16);
+                  if (ok)
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[k]) : "r"(lb + off));
+                  else
+                    v[k] = 0.f;
+                }
+              } else {
 #pragma unroll
               for (int k = 0; k < 32; ++k)
                 asm volatile("ld.shared.f32 %0, [%1];"
                              : "=f"(v[k])
                              : "r"(blk + k * 128 + ((((lane >> 3) ^ (k & 3))) << 5) + (lane & 7) * 4));
+              }
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 const float hi = __uint_as_float(__float_as_uint(v[i]) & 0xFFFFE000u);
@@ -1209,7 +1243,13 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
               const uint32_t ko = kk * 1024;
               const uint64_t ad = ptx::smem_desc(sa + ko, 4096, 512, 1);
               const uint64_t bd = ptx::smem_desc(sb + ko, 4096, 512, 1);
-              if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs MN-major
+              if constexpr (AT && W2) {  // [B; Bs] as one 128-row MN-major operand: lo first, then hi
+                constexpr uint32_t IDESC_TMN2 = ptx::idesc_tf32(BM, 2 * BN, false, true);
+                const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
+                ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_TMN2, (kb | kk) != 0 ? 1u : 0u);
+                ptx::mma_tf32_ts(acc, ta, bd, IDESC_TMN2, 1u);
+                (void)ad;
+              } else if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs MN-major
                 const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
                 const uint64_t bsd = ptx::smem_desc(sb + SM::BS_OFF + ko, 4096, 512, 1);
                 ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_TMN, (kb | kk) != 0 ? 1u : 0u);

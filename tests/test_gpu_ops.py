@@ -62,6 +62,7 @@ CONV_CASES = [
     # N, H, W, C, K, R, stride, pad   (ResNet-50 / tiny-CNN shapes, shrunk spatially)
     (2, 16, 16, 4, 64, 7, 2, 3),      # stem (Cin padded 3->4)
     (2, 50, 46, 4, 64, 7, 2, 3),      # stem, several ragged 16 x 8 output boxes (patch-gather kernel)
+    (2, 224, 224, 4, 64, 7, 2, 3),    # stem at full resolution (patch wgrad: 16 x 2 pixel boxes, split-K)
     (2, 8, 8, 64, 64, 1, 1, 0),       # 1x1
     (2, 8, 8, 64, 64, 3, 1, 1),       # 3x3
     (2, 9, 9, 128, 128, 3, 2, 1),     # strided 3x3, ragged
