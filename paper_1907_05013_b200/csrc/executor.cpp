@@ -412,7 +412,11 @@ double fwd_bytes(pooch_ctx* c, int t) {
   switch (T.kind) {
     case POOCH_L_CONV:
     case POOCH_L_CONV_RELU:
-    case POOCH_L_BNRELU_CONV: return 4.0 * (R.geom.N * din * R.geom.H * R.geom.W * R.geom.C + e +
+    case POOCH_L_BNRELU_CONV:
+      // depth-folded stem: its 2D conv reads X' (Do x H x W x 32, c->xs_bytes) -- the geometry's
+      // N is already the depth, so N * din would count X' din times over (as the wgrad mark does)
+      if (R.fold) return (double)c->xs_bytes + 4.0 * (e + (double)R.geom.K * R.geom.R * R.geom.S * R.geom.C);
+      return 4.0 * (R.geom.N * din * R.geom.H * R.geom.W * R.geom.C + e +
                                       (double)R.geom.K * R.geom.T() * R.geom.R * R.geom.S * R.geom.C /
                                           R.geom.groups);
     case POOCH_L_LRN: return 8.0 * e;
