@@ -1243,11 +1243,16 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
               const uint32_t ko = kk * 1024;
               const uint64_t ad = ptx::smem_desc(sa + ko, 4096, 512, 1);
               const uint64_t bd = ptx::smem_desc(sb + ko, 4096, 512, 1);
-              if constexpr (AT && W2) {  // [B; Bs] as one 128-row MN-major operand: lo first, then hi
+              if constexpr (AT && W2) {  // [B; Bs] as one 128-row MN-major operand (see the K-major W2 below)
                 constexpr uint32_t IDESC_TMN2 = ptx::idesc_tf32(BM, 2 * BN, false, true);
                 const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
+#ifdef POOCH_W2_FOUR
                 ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_TMN2, (kb | kk) != 0 ? 1u : 0u);
                 ptx::mma_tf32_ts(acc, ta, bd, IDESC_TMN2, 1u);
+#else
+                ptx::mma_tf32_ts(acc, ta, bd, IDESC_TMN2, (kb | kk) != 0 ? 1u : 0u);
+                ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_TMN, 1u);
+#endif
                 (void)ad;
               } else if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs MN-major
                 const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
@@ -1275,11 +1280,20 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
             const uint32_t la = sw ? 16 : A_LBO, lb = sw ? 16 : B_LBO, sbo = sw ? 1024 : 128, lay = sw ? 2 : 0;
             uint64_t ad = ptx::smem_desc(sa + ka, la, sbo, lay);
             uint64_t bd = ptx::smem_desc(sb + kbo, lb, sbo, lay);
-            if constexpr (W2) {  // [B; Bs] as one 128-row operand: lo first, then hi
+            if constexpr (W2) {
+              // [B; Bs] as one 128-row operand: hi * [B; Bs] (N = 128: A*B's hi part and hi * Bs into
+              // the two halves), then lo * B (N = 64, first half) -- the three 3xTF32 products at
+              // 64 + 47 instead of 3 x 47 cycles per k-step (tools/mmaprobe); POOCH_W2_FOUR builds
+              // the earlier lo * [B; Bs] + hi * [B; Bs] (a fourth, negligible product lo * Bs)
               constexpr uint32_t IDESC_W2 = ptx::idesc_tf32(BM, 2 * BN, false, false);
               const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
+#ifdef POOCH_W2_FOUR
               ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_W2, (kb | kk) != 0 ? 1u : 0u);
               ptx::mma_tf32_ts(acc, ta, bd, IDESC_W2, 1u);
+#else
+              ptx::mma_tf32_ts(acc, ta, bd, IDESC_W2, (kb | kk) != 0 ? 1u : 0u);
+              ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC, 1u);
+#endif
               (void)ad;
             } else if constexpr (AT) {  // A hi / lo from TMEM (this stage's columns), B / Bs from smem
               const uint32_t ta = tmem + A_TCOL + 64u * s + 8u * kk;
