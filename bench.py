@@ -879,6 +879,13 @@ def traffic_for(family, workload=""):
 
 def swap_stats(fam, prof):
     out = {"probe_d2h_gbs": prof["d2h_gbs"], "probe_h2d_gbs": prof["h2d_gbs"], "probe_duplex_gbs": prof["duplex_gbs"]}
+    # the planner's shared-link model (DESIGN.md Reading 51; executor make_problem): each direction's
+    # rate while both copy lanes are busy, per mille of its one-way rate
+    if prof["duplex_gbs"] > 0 and prof["d2h_gbs"] > 0 and prof["h2d_gbs"] > 0 and os.environ.get("POOCH_DUPLEX", "1") != "0":
+        out["link_model_permille"] = {"d2h": max(1, min(1000, int(1000 * prof["duplex_gbs"] / prof["d2h_gbs"]))),
+                                      "h2d": max(1, min(1000, int(1000 * prof["duplex_gbs"] / prof["h2d_gbs"])))}
+    else:
+        out["link_model_permille"] = None
     for k in ("swap_out", "swap_in"):
         v = fam[k]
         out[k + "_gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
