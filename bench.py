@@ -575,6 +575,7 @@ def our_arm(args):
         agreed = dp.agree_profile(prof, device="cuda")
         ctx.set_profile(agreed["fwd"], agreed["bwd"], agreed["rec"], agreed["d2h"], agreed["h2d"], agreed["tail"])
         ctx.set_link(agreed["d2h_gbs"], agreed["h2d_gbs"], agreed["duplex_gbs"])
+        prof.update(d2h_gbs=agreed["d2h_gbs"], h2d_gbs=agreed["h2d_gbs"], duplex_gbs=agreed["duplex_gbs"])
     prof_s = time.time() - t0
     paper = None
     if not args.no_paper and world == 1:
