@@ -616,10 +616,13 @@ static PixBox choose_kbox(int N3, int Ho, int Wo, int st, int st3, bool one_imag
   return best;
 }
 
-// k-blocks (32 pixels each) one wgrad split may accumulate (0: no cap); POOCH_WGRAD_KMAX overrides
+// k-blocks (32 pixels each) one wgrad split may accumulate: 1024 = 32,768 pixels, the longest
+// reduction whose 3xTF32 error was measured (2.3e-4 rel-L2, DESIGN.md Reading 43) -- binding only
+// at the benchmark batches (ResNet-50 at batch 2560: stage-1 splits of ~8,700 k-blocks otherwise);
+// POOCH_WGRAD_KMAX overrides (0: no cap)
 static int wgrad_kmax() {
-  const char* e = getenv("POOCH_WGRAD_KMAX");
-  return e ? atoi(e) : 0;
+  const char* e = getenv("POOCH_WGRAD_KMAX");  // read per call: tools/acc_probe.py switches it in-process
+  return e ? atoi(e) : 1024;
 }
 
 static bool wgrad_uses_tma(const ConvGeom& g) {
@@ -672,9 +675,13 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
   // persistent CTAs x (k-blocks per split + ~6 for pipeline fill and epilogue), plus the workspace
   // write + reduction read (8 B per dW element per split at ~6.5 TB/s ~ 4.5 MB per k-block time)
   const double ws_per_split = 8.0 * g.K * rsc / 4.5e6;
+  // accuracy cap on a split's length (wgrad_kmax): the search starts at the smallest split count
+  // that respects it, so the cost model still picks the wave-filling count above it
+  const int kmax = wgrad_kmax();
+  const int s_min = kmax > 0 ? std::max(1, (w.kb + kmax - 1) / kmax) : 1;
   double best = 1e300;
-  w.splits = 1;
-  for (int s = 1; s <= std::max(1, w.kb / 4); ++s) {
+  w.splits = s_min;
+  for (int s = s_min; s <= std::max(s_min, w.kb / 4); ++s) {
     const int64_t waves = (tiles * s + 147) / 148;
     const double cost = (double)waves * ((w.kb + s - 1) / s + 6) + (s > 1 ? s * ws_per_split : 0.0);
     if (cost < best - 1e-9) {
@@ -687,8 +694,7 @@ static WgradPlan wgrad_plan(const ConvGeom& g) {
   // linearly with the number of accumulated MMAs: 3xTF32 GEMM rel-L2 4.5e-6 at K = 576, 2.3e-4 at
   // K = 32768, measured), so no split accumulates more than wgrad_kmax() k-blocks in TMEM; the
   // split partials are summed in fixed order with round-to-nearest fp32 adds by the reduction
-  const int kmax = wgrad_kmax();
-  if (kmax > 0) w.splits = std::max(w.splits, (w.kb + kmax - 1) / kmax);
+  if (kmax > 0) w.splits = std::max(w.splits, s_min);
   w.kb_per_split = (w.kb + w.splits - 1) / w.splits;
   w.splits = (w.kb + w.kb_per_split - 1) / w.kb_per_split;
   return w;
