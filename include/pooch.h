@@ -232,7 +232,10 @@ typedef struct {
   const uint64_t* bytes;     /* feature-map bytes */
   int64_t tail_ns;           /* update (+ allreduce) after the last backward task */
   uint64_t resident_bytes;
-  double d2h_gbs, h2d_gbs, duplex_gbs; /* probed host-link bandwidth (GB/s) */
+  double d2h_gbs, h2d_gbs, duplex_gbs; /* probed host-link bandwidth (GB/s): one direction alone;
+                                        duplex = each direction while both run (median of three,
+                                        largest map that fits twice); the planner's shared-link
+                                        model uses duplex / d2h and duplex / h2d (Reading 51) */
   int32_t mode;              /* how the times were measured: POOCH_PROFILE_ISOLATED or _ALL_SWAP */
   const int64_t* d2h_issue_ns; /* ALL_SWAP only (else NULL): median issue time of each map's swap-out, */
   const int64_t* h2d_issue_ns; /*   swap-in, ns after the step starts (-1: never copied)       */
