@@ -15,15 +15,6 @@ constexpr int kSMs = 148;
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
-// the feature-map streams of the BN kernels (GBs per launch, no reuse through the 126 MB L2):
-// evict-first loads / stores (POOCH_NO_STREAMING builds plain ones, for A/B timing)
-#ifdef POOCH_NO_STREAMING
-__device__ __forceinline__ float4 ld4s(const float* p) { return ld4(p); }
-__device__ __forceinline__ void st4s(float* p, float4 v) { st4(p, v); }
-#else
-__device__ __forceinline__ float4 ld4s(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
-__device__ __forceinline__ void st4s(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
-#endif
 __device__ __forceinline__ float f4get(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
@@ -119,7 +110,7 @@ __global__ void bn_apply_kernel(const float* __restrict__ a, const float* __rest
     o.y = fmaxf(pre_act<MODE>(av.y, s1.y, t1.y, bv.y, s2.y, t2.y), 0.f);
     o.z = fmaxf(pre_act<MODE>(av.z, s1.z, t1.z, bv.z, s2.z, t2.z), 0.f);
     o.w = fmaxf(pre_act<MODE>(av.w, s1.w, t1.w, bv.w, s2.w, t2.w), 0.f);
-    st4s(y + 4 * k, o);
+    st4(y + 4 * k, o);
   };
   // two elements of the grid-stride loop per iteration, both loads issued before either store
   for (; i + stride < n4; i += 2 * stride) {
@@ -129,11 +120,11 @@ __global__ void bn_apply_kernel(const float* __restrict__ a, const float* __rest
     const int c1 = cg * 4;
     cg += cstep;
     if (cg >= C4) cg -= C4;
-    const float4 a0 = ld4s(a + 4 * i), a1 = ld4s(a + 4 * (i + stride));
+    const float4 a0 = ld4(a + 4 * i), a1 = ld4(a + 4 * (i + stride));
     float4 b0 = make_float4(0, 0, 0, 0), b1 = b0;
     if (MODE != 0) {
-      b0 = ld4s(b + 4 * i);
-      b1 = ld4s(b + 4 * (i + stride));
+      b0 = ld4(b + 4 * i);
+      b1 = ld4(b + 4 * (i + stride));
     }
     one(i, c0, a0, b0);
     one(i + stride, c1, a1, b1);
@@ -143,8 +134,8 @@ __global__ void bn_apply_kernel(const float* __restrict__ a, const float* __rest
     cg += cstep;
     if (cg >= C4) cg -= C4;
     float4 bv = make_float4(0, 0, 0, 0);
-    if (MODE != 0) bv = ld4s(b + 4 * i);
-    one(i, c, ld4s(a + 4 * i), bv);
+    if (MODE != 0) bv = ld4(b + 4 * i);
+    one(i, c, ld4(a + 4 * i), bv);
   }
 }
 
@@ -198,11 +189,11 @@ __global__ void __launch_bounds__(kBwdThreads) bn_bwd_reduce_kernel(BnBwdArgs p,
       // accumulation order as one row at a time
       for (; r + rpi < r1; r += 2 * rpi) {
         const size_t o0 = (size_t)r * C + c, o1 = o0 + (size_t)rpi * C;
-        const float4 a0 = ld4s(p.a + o0), g0 = ld4s(p.gy + o0), a1 = ld4s(p.a + o1), g1 = ld4s(p.gy + o1);
+        const float4 a0 = ld4(p.a + o0), g0 = ld4(p.gy + o0), a1 = ld4(p.a + o1), g1 = ld4(p.gy + o1);
         float4 b0 = make_float4(0, 0, 0, 0), b1 = b0;
         if (MODE != 0) {
-          b0 = ld4s(p.b + o0);
-          b1 = ld4s(p.b + o1);
+          b0 = ld4(p.b + o0);
+          b1 = ld4(p.b + o1);
         }
         row(a0, g0, b0);
         row(a1, g1, b1);
@@ -210,8 +201,8 @@ __global__ void __launch_bounds__(kBwdThreads) bn_bwd_reduce_kernel(BnBwdArgs p,
       for (; r < r1; r += rpi) {
         const size_t o0 = (size_t)r * C + c;
         float4 b0 = make_float4(0, 0, 0, 0);
-        if (MODE != 0) b0 = ld4s(p.b + o0);
-        row(ld4s(p.a + o0), ld4s(p.gy + o0), b0);
+        if (MODE != 0) b0 = ld4(p.b + o0);
+        row(ld4(p.a + o0), ld4(p.gy + o0), b0);
       }
     }
   }
@@ -288,11 +279,11 @@ __global__ void bn_bwd_apply_kernel(BnBwdArgs p, const float* __restrict__ coef,
     cg += cstep;
     if (cg >= C4) cg -= C4;
     size_t off = 4 * (size_t)i;
-    float4 av = ld4s(p.a + off), g = ld4s(p.gy + off);
+    float4 av = ld4(p.a + off), g = ld4(p.gy + off);
     float4 s1 = ld4(p.sa + c), t1 = ld4(p.ta + c), m1 = ld4(p.mean_a + c), i1 = ld4(p.invstd_a + c);
     float4 ka = ld4(coef + c), kb = ld4(coef + C + c), kc = ld4(coef + 2 * C + c);
     float4 bv = make_float4(0, 0, 0, 0), s2 = bv, t2 = bv, m2 = bv, i2 = bv, la = bv, lb = bv, lc = bv;
-    if (MODE != 0) bv = ld4s(p.b + off);
+    if (MODE != 0) bv = ld4(p.b + off);
     if (MODE == 1) {
       s2 = ld4(p.sb + c); t2 = ld4(p.tb + c); m2 = ld4(p.mean_b + c); i2 = ld4(p.invstd_b + c);
       la = ld4(coef + 3 * C + c); lb = ld4(coef + 4 * C + c); lc = ld4(coef + 5 * C + c);
@@ -311,15 +302,15 @@ __global__ void bn_bwd_apply_kernel(BnBwdArgs p, const float* __restrict__ coef,
         ob[e] = dz;
       }
     }
-    st4s(p.ga + off, make_float4(oa[0], oa[1], oa[2], oa[3]));
-    if (MODE == 1) st4s(p.gb + off, make_float4(ob[0], ob[1], ob[2], ob[3]));
+    st4(p.ga + off, make_float4(oa[0], oa[1], oa[2], oa[3]));
+    if (MODE == 1) st4(p.gb + off, make_float4(ob[0], ob[1], ob[2], ob[3]));
     if (MODE == 2) {
       float4 o = make_float4(ob[0], ob[1], ob[2], ob[3]);
       if (p.gb_accumulate) {
         float4 q = ld4(p.gb + off);
         o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
       }
-      st4s(p.gb + off, o);
+      st4(p.gb + off, o);
     }
   }
 }
