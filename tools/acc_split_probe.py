@@ -1,6 +1,6 @@
 """Accuracy of long wgrad splits (tensor-core accumulation bias, DESIGN.md Reading 43) at the lengths
 the benchmark batches would produce without the split cap: dW rel-L2 against fp64 for a forced split
-count (POOCH_WGRAD_SPLITS, cap off) and for the default cap (POOCH_WGRAD_KMAX = 1024 k-blocks).
+count (POOCH_WGRAD_SPLITS, cap off) and for the default cap (2048 k-blocks) and 1024.
 Each case runs in its own process (the switches are read by the library). GPU box:
     python tools/acc_split_probe.py > gpurun_out/acc_split_probe.log
 """
@@ -12,7 +12,7 @@ CASES = [  # name, B, H, Cin, K, R, stride, pad
     ("stem b32", 32, 224, 4, 64, 7, 2, 3),
     ("l1.c2 b32", 32, 56, 64, 64, 3, 1, 1),
 ]
-SETTINGS = [("cap 1024 (default)", {}), ("no cap, 8 splits", {"POOCH_WGRAD_KMAX": "0", "POOCH_WGRAD_SPLITS": "8"}),
+SETTINGS = [("default cap (2048)", {}), ("cap 1024", {"POOCH_WGRAD_KMAX": "1024"}), ("no cap, 8 splits", {"POOCH_WGRAD_KMAX": "0", "POOCH_WGRAD_SPLITS": "8"}),
             ("no cap, 2 splits", {"POOCH_WGRAD_KMAX": "0", "POOCH_WGRAD_SPLITS": "2"}),
             ("no cap, 1 split", {"POOCH_WGRAD_KMAX": "0", "POOCH_WGRAD_SPLITS": "1"})]
 
