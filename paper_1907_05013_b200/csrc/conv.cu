@@ -616,13 +616,13 @@ static PixBox choose_kbox(int N3, int Ho, int Wo, int st, int st3, bool one_imag
   return best;
 }
 
-// k-blocks (32 pixels each) one wgrad split may accumulate: 1024 = 32,768 pixels, the longest
-// reduction whose 3xTF32 error was measured (2.3e-4 rel-L2, DESIGN.md Reading 43) -- binding only
-// at the benchmark batches (ResNet-50 at batch 2560: stage-1 splits of ~8,700 k-blocks otherwise);
-// POOCH_WGRAD_KMAX overrides (0: no cap)
+// k-blocks (32 pixels each) one wgrad split may accumulate: 2048 = 65,536 pixels, where the
+// measured 3xTF32 wgrad error is ~4e-4 rel-L2 (2.3-3.5e-4 at 50 K pixels per split, 7e-4 at 100 K;
+// DESIGN.md Reading 43) -- binding only at the benchmark batches (ResNet-50 at batch 2560: stage-1
+// splits of ~8,700 k-blocks otherwise), not at batch 256; POOCH_WGRAD_KMAX overrides (0: no cap)
 static int wgrad_kmax() {
   const char* e = getenv("POOCH_WGRAD_KMAX");  // read per call: tools/acc_probe.py switches it in-process
-  return e ? atoi(e) : 1024;
+  return e ? atoi(e) : 2048;
 }
 
 static bool wgrad_uses_tma(const ConvGeom& g) {
