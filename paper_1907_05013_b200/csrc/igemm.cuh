@@ -547,6 +547,15 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
   // run, so [B; Bs] is one 128-row operand with the same LBO)
   static_assert(!W2 || (AT && BN == 64 && (MODE != CONV_WGRAD || MNW)), "W2: AT fwd / dgrad / MN-major wgrad at BN = 64");
   constexpr uint32_t ACC_COLS = W2 ? 2u * BN : (uint32_t)BN;  // columns of one accumulator
+  // W2 over a TMA-landed K-major A tile (not SP's gathered rows, not XF's transformed ones): the hi
+  // products read A straight from the stage -- the tensor core truncates fp32 operands to TF32
+  // (Reading 27), which is exactly hi -- so the auxiliary warps move only lo into TMEM (half the
+  // tcgen05.st traffic per k-block, the same operand values: bit-identical products)
+#ifdef POOCH_W2_HI_TMEM
+  constexpr bool W2_HI_SMEM = false;
+#else
+  constexpr bool W2_HI_SMEM = W2 && !SP && !XF && !MNW && MODE != CONV_WGRAD;
+#endif
   static_assert(!AT || 2 * ACC_COLS + 64 * STAGES <= 512, "AT: accumulators + A stages exceed TMEM");
   // E2: two epilogue warp groups drain each accumulator, one per half of its columns (the
   // 1x1 expand convs are epilogue-bound: TMEM -> smem staging -> BN partial sums -> TMA store);
@@ -1187,7 +1196,9 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
               v[i] = hi;
             }
             const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + A_TCOL + 64u * s;
-            if (!SP || p.epi_direct < 7) {  // 7 / 8: timing experiments (SP), no TMEM writes
+            if constexpr (W2_HI_SMEM) {  // hi is read by the tensor core from the stage itself
+              ptx::tmem_st32(ta + 32, lo);
+            } else if (!SP || p.epi_direct < 7) {  // 7 / 8: timing experiments (SP), no TMEM writes
               ptx::tmem_st32(ta, v);
               ptx::tmem_st32(ta + 32, lo);
             }
@@ -1291,7 +1302,10 @@ __global__ void __launch_bounds__(igemm_threads(MODE, X3, XF, NAUX, E2), 1)
               ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC_W2, (kb | kk) != 0 ? 1u : 0u);
               ptx::mma_tf32_ts(acc, ta, bd, IDESC_W2, 1u);
 #else
-              ptx::mma_tf32_ts(acc, ta, bd, IDESC_W2, (kb | kk) != 0 ? 1u : 0u);
+              if constexpr (W2_HI_SMEM)
+                ptx::mma_tf32(acc, ad, bd, IDESC_W2, (kb | kk) != 0 ? 1u : 0u);
+              else
+                ptx::mma_tf32_ts(acc, ta, bd, IDESC_W2, (kb | kk) != 0 ? 1u : 0u);
               ptx::mma_tf32_ts(acc, ta + 32, bd, IDESC, 1u);
 #endif
               (void)ad;
